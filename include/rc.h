@@ -1,0 +1,221 @@
+/*
+ * rc.h — C ABI of the B200 race checker (librc.so).
+ *
+ * What it computes: the concrete SIMD operational semantics of arXiv 1308.3203
+ * §4 for a kernel written in the §3 language
+ * (PAPER.md:85-107), run for one work-group of `work_group_size` work-items on
+ * each of `n_instances` independent input heaps, with the race rule read as in
+ * DESIGN.md §3 (delayed visibility inside a barrier interval, per-cell access
+ * conflicts between distinct tids, write-write conflicts classified benign /
+ * non-benign).
+ *
+ * Everything below is plain C: no C++ or torch types cross this boundary.
+ * Pointers marked "device" are CUDA device pointers on options->device;
+ * pointers marked "host" are ordinary host memory.  The library never aborts
+ * the process; every entry point returns an rc_status and sets a thread-local
+ * message readable with rc_last_error().
+ *
+ * Races and runtime errors in the USER kernel are reports, never call errors.
+ */
+#ifndef RC_H
+#define RC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RC_ABI_VERSION 1
+
+/* ---- status codes ------------------------------------------------------- */
+typedef enum {
+  RC_OK = 0,
+  RC_EINVAL = 1, /* malformed bytecode or arguments (message says which)    */
+  RC_ENOMEM = 2, /* device or host allocation failed                         */
+  RC_ECUDA = 3,  /* a CUDA runtime call failed (no device, launch error ...)  */
+  RC_ETRUNC = 4, /* more reports than `capacity`; the first `capacity` were
+                    written, *n_reports_total holds the full count (snprintf) */
+  RC_ELIMIT = 5  /* an implementation limit was hit: a work-item wrote more
+                    distinct cells in one interval than the own-write overlay
+                    holds (RC_OVERLAY_CAP), or cells per batch exceed 2^32     */
+} rc_status;
+
+/* ---- bytecode (RCB1) ----------------------------------------------------
+ * The §3 grammar lowered to three-address CFG bytecode
+ * (reading L10 in DESIGN.md).  Little-endian.
+ *   header (16 B): u32 magic = 'R''C''B''1' (0x31424352), u16 version = 1,
+ *                  u16 flags = 0, u16 n_regs (1..256), u16 n_arrays (0..256),
+ *                  u32 n_instr (1..65536)
+ *   then n_instr instructions of 8 B: {u8 op, u8 a, u8 b, u8 c, i32 imm}.
+ * `start` is pc 0.  Registers are the private variables
+ * `Locals`, zero-initialised (reading L18).  Arrays are the
+ * shared `GVar` arrays passed as `Args`; shared scalars
+ * are 1-element arrays (reading L12).  Values are int32, two's complement,
+ * wrapping (reading L7).  Booleans are 0/1; any non-zero value is true.     */
+#define RC_MAGIC 0x31424352u
+enum rc_opcode {
+  RC_OP_CONST = 1,  /* r[a] := imm                          v := c   */
+  RC_OP_MOV = 2,    /* r[a] := r[b]                         v := v'   */
+  RC_OP_TID = 3,    /* r[a] := tid  (0-based, reading L8)   tid   */
+  RC_OP_SIZE = 4,   /* r[a] := size(array b)                size(v)   */
+  RC_OP_ADD = 5,    /* r[a] := r[b] op r[c]                 op(e)   */
+  RC_OP_SUB = 6,
+  RC_OP_MUL = 7,
+  RC_OP_DIV = 8,    /* truncating; r[c]==0 -> DIV0 report, work-item halts */
+  RC_OP_MOD = 9,    /* C99 remainder; r[c]==0 -> DIV0; INT_MIN%-1 == 0      */
+  RC_OP_MIN = 10,
+  RC_OP_MAX = 11,
+  RC_OP_AND = 12,   /* bitwise */
+  RC_OP_OR = 13,
+  RC_OP_XOR = 14,
+  RC_OP_LT = 15,    /* r[a] := r[b] <  r[c] (signed)        e<e   */
+  RC_OP_EQ = 16,    /* r[a] := r[b] == r[c]                 e=e   */
+  RC_OP_LAND = 17,  /* r[a] := r[b]!=0 && r[c]!=0           b∧b   */
+  RC_OP_LNOT = 18,  /* r[a] := r[b]==0                      ¬b   */
+  RC_OP_LD = 19,    /* r[a] := array b [r[c]]               v:=a[v] */
+  RC_OP_ST = 20,    /* array a [r[b]] := r[c]               a[v]:=e */
+  RC_OP_BAR = 21,   /* barrier   */
+  RC_OP_ASSUME = 22,/* r[a]==0 -> work-item stops silently (⊤)   */
+  RC_OP_ASSERT = 23,/* r[a]==0 -> ASSERT report, work-item halts (⊥) */
+  RC_OP_BR = 24,    /* r[a]!=0 ? pc=imm : pc=b+256*c  (assume(b)/assume(¬b)
+                       successor pair of the CFG)          */
+  RC_OP_JMP = 25,   /* pc = imm                                              */
+  RC_OP_EXIT = 26,  /* the `exit` node; implicit final barrier */
+  RC_OP_ADDI = 27   /* r[a] := r[b] + imm   (op(v, c) with a constant)      */
+};
+
+/* ---- report kinds -------------------------------------------------------- */
+enum rc_kind {
+  RC_RW = 1,           /* a cell read by one tid and written by another     */
+  RC_WW_BENIGN = 2,    /* >= 2 writers, all final values equal  */
+  RC_WW_NONBENIGN = 3, /* >= 2 writers with different final values  */
+  RC_OOB = 4,          /* index outside [0,size): ⊥; array/index set */
+  RC_ASSERT = 5,       /* assert(false): ⊥; array=-1, index=pc      */
+  RC_DIV0 = 6,         /* division by zero: ⊥; array=-1, index=pc           */
+  RC_FUEL = 7,         /* per-interval fuel exhausted (tid1=tid, index=pc), or
+                          max_intervals reached (tid1=tid2=0xFFFFFFFF,
+                          index=-1, interval=max_intervals)                 */
+  RC_BARRIER_DIVERGENCE = 8 /* arrived work-items at different barrier nodes
+                          ("the same instruction barrier"); array=-1,
+                          index = pc of tid1's BAR or -1 for exit; tid1 = min
+                          arrived tid, tid2 = min arrived tid at another node */
+};
+
+/* 32-byte report.  Canonical order = ascending (instance, interval, array
+ * (signed), index (signed), kind, tid1, tid2); the array returned by rc_run is
+ * in that order.  For RW / WW_*: (tid1 < tid2) is the lexicographically
+ * smallest conflicting pair (reading L4); flags bit0 = tid1 read
+ * the cell, bit1 = tid1 wrote it, bit2 = tid2 read, bit3 = tid2 wrote (all in
+ * this interval).  For error kinds tid2 = 0xFFFFFFFF and flags = 0.         */
+typedef struct {
+  uint32_t instance; /* global instance id (includes options->instance_offset) */
+  uint32_t interval; /* barrier interval k (0-based)                          */
+  int32_t array;     /* array id, or -1                                       */
+  int32_t index;     /* cell index (may be out of bounds for OOB), or pc      */
+  uint32_t tid1, tid2;
+  uint16_t kind, flags;
+  uint32_t reserved; /* 0 */
+} rc_report;
+
+/* Exact counters; part of parity with the oracle. */
+typedef struct {
+  uint64_t checked_accesses; /* performed LD + ST (in-bounds) of all work-items */
+  uint64_t loads, stores;
+  uint64_t instructions;     /* executed bytecode instructions (the one refused
+                                by the fuel check is not counted)               */
+  uint64_t intervals_max;    /* max over instances of intervals executed        */
+  uint64_t lanes_final[8];   /* final work-item status histogram:
+                                [0] EXITED [1] PRUNED (assume false) [2] OOB
+                                [3] ASSERT [4] DIV0 [5] FUEL
+                                [6] still waiting when max_intervals stopped it
+                                [7] 0                                          */
+} rc_stats;
+
+/* Optional live profile (options->profile), filled when non-NULL: per kernel
+ * class, launches, summed CUDA-event time on the launch stream, and the
+ * ALGORITHMIC bytes those launches must move.               */
+enum rc_prof_class {
+  RC_PROF_INTERP = 0,   /* K1  interval interpretation + log append          */
+  RC_PROF_HIST = 1,     /* K2  onesweep upfront digit histograms             */
+  RC_PROF_SORT = 2,     /* K3  onesweep scatter passes                       */
+  RC_PROF_DETECT = 3,   /* K4+K5 segmented detect + commit                   */
+  RC_PROF_BOUNDARY = 4, /* A4  barrier bookkeeping, divergence               */
+  RC_PROF_FINALIZE = 5, /* K6  canonical report sort                         */
+  RC_PROF_COPY = 6,     /* heap init / final-heap copies                     */
+  RC_PROF_N = 8
+};
+typedef struct {
+  uint64_t launches[RC_PROF_N];
+  double ms[RC_PROF_N];
+  uint64_t alg_bytes[RC_PROF_N];
+  uint64_t items[RC_PROF_N]; /* records / lanes processed                    */
+  double total_ms;           /* whole rc_run on the stream                    */
+} rc_profile;
+
+/* One shared array of the kernel (an element of Args).
+ * `data` holds n_instances consecutive copies of the array:
+ * data[inst * size + i], int32.  Borrowed, read-only; the library copies it
+ * into its own working heap.  Device pointer unless RC_OPT_HOST_IO.         */
+typedef struct {
+  const int32_t* data;
+  uint32_t size; /* element count, < 2^31; size(v) of PAPER.md:87           */
+} rc_array;
+
+#define RC_OPT_HOST_IO 1u /* arrays[].data and final_heaps[] are HOST pointers;
+                             rc_run does the host<->device copies itself     */
+
+typedef struct {
+  uint32_t instance_offset;    /* added to report.instance (multi-GPU shards) */
+  uint32_t max_intervals;      /* default 65536 (reading L17)                  */
+  uint64_t fuel_per_interval;  /* per work-item per interval; default 2^20     */
+  int32_t device;              /* CUDA device ordinal; default 0               */
+  uint32_t flags;              /* RC_OPT_*                                     */
+  void* cuda_stream;           /* cudaStream_t; NULL = legacy default stream  */
+  uint32_t max_batch_instances;/* 0 = library chooses the instance batch      */
+  uint32_t reserved0;
+  rc_profile* profile;         /* nullable                                     */
+} rc_options;
+
+typedef struct rc_program rc_program; /* opaque, library-owned */
+
+/* Decode + validate bytecode (host only; no CUDA call, so it works without a
+ * GPU).  On success *out owns a copy of the program until rc_free_program.
+ * RC_EINVAL (+ message) for: bad magic/version/flags, size mismatch, n_regs
+ * or n_arrays or n_instr out of range, unknown opcode, register >= n_regs,
+ * array >= n_arrays, branch target >= n_instr, execution that can fall off
+ * the end, no EXIT reachable from pc 0.                                     */
+int rc_load_program(const void* bytecode, size_t nbytes, rc_program** out);
+void rc_free_program(rc_program* prog);
+/* n_regs, n_arrays, n_instr of a loaded program (any pointer may be NULL). */
+int rc_program_info(const rc_program* prog, uint32_t* n_regs, uint32_t* n_arrays,
+                    uint32_t* n_instr);
+
+/* Run `prog` with `work_group_size` work-items (tids 0..n-1) on each of
+ * `n_instances` instances.  `arrays` has exactly the program's n_arrays
+ * entries.  Reports go to the HOST buffer `out` (caller-owned, `capacity`
+ * entries, may be NULL when capacity == 0) in canonical order;
+ * *n_reports_total is always set (nullable).  `stats` (host, nullable).
+ * `final_heaps` (nullable): n_arrays pointers, each to n_instances*size int32
+ * (device, or host with RC_OPT_HOST_IO) receiving the final shared heap.
+ * Stream-ordered on options->cuda_stream; returns after the reports are on
+ * the host (synchronises that stream).  Not re-entrant on the same program
+ * object from two threads at once (the program caches device workspace).  */
+int rc_run(const rc_program* prog, uint32_t work_group_size, const rc_array* arrays,
+           uint32_t n_arrays, uint32_t n_instances, const rc_options* options,
+           rc_report* out, uint64_t capacity, uint64_t* n_reports_total,
+           rc_stats* stats, int32_t* const* final_heaps);
+
+/* Thread-local message describing the last non-OK status of this thread. */
+const char* rc_last_error(void);
+int rc_abi_version(void);
+/* Release all cached device workspace of `prog` (also done by rc_free_program). */
+int rc_release_workspace(rc_program* prog);
+
+#define RC_OVERLAY_CAP 32 /* distinct cells one work-item may write per interval */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RC_H */

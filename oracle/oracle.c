@@ -1,0 +1,649 @@
+/*
+ * oracle.c — TEST INFRASTRUCTURE ONLY.  Plain, slow, obviously-correct CPU
+ * definition of what the race-checking hot path computes.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may
+ * load this library.  It shares no code, header, table or constant with the
+ * CUDA path (paper_1308_3203_b200/): it has its own bytecode decoder, its own
+ * opcode numbers (re-typed from the RCB1 format description in DESIGN.md §2)
+ * and its own report layout.
+ *
+ * Two independent parts:
+ *
+ *  (1) oracle_run: the canonical algorithm of DESIGN.md §3 / SURVEY.md §8(c),
+ *      step by step: thread-local rules of PAPER.md:168-201 under delayed
+ *      visibility inside each barrier interval, the race rule of
+ *      PAPER.md:224-229 read as per-cell access conflicts (reading L1), the
+ *      benign test of PAPER.md:23, 229 on final per-thread values (L3), the
+ *      barrier release PAPER.md:220-222 as "max-tid writer wins" (I4), the
+ *      implicit final barrier PAPER.md:233.
+ *
+ *  (2) oracle_enumerate: the paper's own global semantics:
+ *      one thread steps at a time on a SHARED heap with immediate visibility,
+ *      every interleaving of one barrier interval is explored, and the set of
+ *      reachable end-of-interval states is returned.  Tests use it to check
+ *      invariants I1-I4 that tie (1) to the paper's race definition
+ *      (PAPER.md:230-232).
+ *
+ * Arithmetic is int32 two's complement with wrap (reading L7), done through
+ * uint32_t so C's signed-overflow UB is avoided.
+ */
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <pthread.h>
+
+/* ---- bytecode (RCB1) --------------------------------------- */
+enum {
+  O_CONST = 1, O_MOV, O_TID, O_SIZE, O_ADD, O_SUB, O_MUL, O_DIV, O_MOD, O_MIN,
+  O_MAX, O_AND, O_OR, O_XOR, O_LT, O_EQ, O_LAND, O_LNOT, O_LD, O_ST, O_BAR,
+  O_ASSUME, O_ASSERT, O_BR, O_JMP, O_EXIT, O_ADDI
+};
+
+typedef struct { uint8_t op, a, b, c; int32_t imm; } oins;
+typedef struct { uint32_t n_regs, n_arrays, n_instr; oins* code; } oprog;
+
+static uint32_t rd_u32(const uint8_t* p) { return (uint32_t)p[0] | (uint32_t)p[1] << 8 | (uint32_t)p[2] << 16 | (uint32_t)p[3] << 24; }
+static uint16_t rd_u16(const uint8_t* p) { return (uint16_t)(p[0] | p[1] << 8); }
+
+static int decode(const uint8_t* bc, size_t nbytes, oprog* P) {
+  if (nbytes < 16 || rd_u32(bc) != 0x31424352u) return -1;
+  P->n_regs = rd_u16(bc + 8);
+  P->n_arrays = rd_u16(bc + 10);
+  P->n_instr = rd_u32(bc + 12);
+  if (nbytes != 16 + 8 * (size_t)P->n_instr || P->n_regs == 0) return -1;
+  P->code = (oins*)malloc(sizeof(oins) * (P->n_instr ? P->n_instr : 1));
+  for (uint32_t i = 0; i < P->n_instr; i++) {
+    const uint8_t* q = bc + 16 + 8 * i;
+    P->code[i].op = q[0]; P->code[i].a = q[1]; P->code[i].b = q[2]; P->code[i].c = q[3];
+    P->code[i].imm = (int32_t)rd_u32(q + 4);
+  }
+  return 0;
+}
+
+/* ---- reports (own layout; 32 bytes, field order of DESIGN.md §2) --------- */
+typedef struct {
+  uint32_t instance, interval;
+  int32_t array, index;
+  uint32_t tid1, tid2;
+  uint16_t kind, flags;
+  uint32_t reserved;
+} orep;
+
+enum { K_RW = 1, K_WWB = 2, K_WWN = 3, K_OOB = 4, K_ASSERT = 5, K_DIV0 = 6, K_FUEL = 7, K_DIV = 8 };
+#define NOTID 0xFFFFFFFFu
+
+typedef struct { orep* v; size_t n, cap; } replist;
+static void rep_push(replist* L, orep r) {
+  if (L->n == L->cap) { L->cap = L->cap ? 2 * L->cap : 64; L->v = (orep*)realloc(L->v, L->cap * sizeof(orep)); }
+  L->v[L->n++] = r;
+}
+static orep mkrep(uint32_t inst, uint32_t k, int32_t arr, int32_t idx, uint32_t t1, uint32_t t2, int kind, int flags) {
+  orep r; memset(&r, 0, sizeof r);
+  r.instance = inst; r.interval = k; r.array = arr; r.index = idx; r.tid1 = t1; r.tid2 = t2;
+  r.kind = (uint16_t)kind; r.flags = (uint16_t)flags;
+  return r;
+}
+/* canonical order: (instance, interval, array, index, kind, tid1, tid2) */
+static int rep_cmp(const void* x, const void* y) {
+  const orep* a = (const orep*)x; const orep* b = (const orep*)y;
+#define C(f) if (a->f != b->f) return a->f < b->f ? -1 : 1;
+  C(instance) C(interval) C(array) C(index) C(kind) C(tid1) C(tid2)
+#undef C
+  return 0;
+}
+
+/* ---- lane (work-item) state ----------------------------------------------- */
+enum { S_RUNNING = 0, S_WAITING, S_EXITED, S_PRUNED, S_OOB, S_ASSERT, S_DIV0, S_FUEL };
+
+/* int32 semantics (reading L7) */
+static int32_t w_add(int32_t x, int32_t y) { return (int32_t)((uint32_t)x + (uint32_t)y); }
+static int32_t w_sub(int32_t x, int32_t y) { return (int32_t)((uint32_t)x - (uint32_t)y); }
+static int32_t w_mul(int32_t x, int32_t y) { return (int32_t)((uint32_t)x * (uint32_t)y); }
+static int32_t w_div(int32_t x, int32_t y) { /* y != 0; C99 truncation; INT_MIN/-1 = INT_MIN */
+  if (y == -1) return (int32_t)(0u - (uint32_t)x);
+  return x / y;
+}
+static int32_t w_mod(int32_t x, int32_t y) { if (y == -1) return 0; return x % y; }
+
+/* Outcome of one ALU/control instruction that does not touch shared memory.
+ * Returns 1 if handled (regs/pc updated), 0 if the instruction is a memory,
+ * barrier or termination instruction the caller must handle. */
+static int step_private(const oprog* P, const oins* I, int32_t* r, uint32_t tid,
+                        const uint32_t* sizes, uint32_t* pc, int* fault) {
+  *fault = 0;
+  switch (I->op) {
+    case O_CONST: r[I->a] = I->imm; break;
+    case O_MOV: r[I->a] = r[I->b]; break;
+    case O_TID: r[I->a] = (int32_t)tid; break;
+    case O_SIZE: r[I->a] = (int32_t)sizes[I->b]; break;
+    case O_ADD: r[I->a] = w_add(r[I->b], r[I->c]); break;
+    case O_SUB: r[I->a] = w_sub(r[I->b], r[I->c]); break;
+    case O_MUL: r[I->a] = w_mul(r[I->b], r[I->c]); break;
+    case O_DIV: if (r[I->c] == 0) { *fault = S_DIV0; return 1; } r[I->a] = w_div(r[I->b], r[I->c]); break;
+    case O_MOD: if (r[I->c] == 0) { *fault = S_DIV0; return 1; } r[I->a] = w_mod(r[I->b], r[I->c]); break;
+    case O_MIN: r[I->a] = r[I->b] < r[I->c] ? r[I->b] : r[I->c]; break;
+    case O_MAX: r[I->a] = r[I->b] > r[I->c] ? r[I->b] : r[I->c]; break;
+    case O_AND: r[I->a] = r[I->b] & r[I->c]; break;
+    case O_OR: r[I->a] = r[I->b] | r[I->c]; break;
+    case O_XOR: r[I->a] = r[I->b] ^ r[I->c]; break;
+    case O_LT: r[I->a] = r[I->b] < r[I->c]; break;
+    case O_EQ: r[I->a] = r[I->b] == r[I->c]; break;
+    case O_LAND: r[I->a] = (r[I->b] != 0) && (r[I->c] != 0); break;
+    case O_LNOT: r[I->a] = r[I->b] == 0; break;
+    case O_ADDI: r[I->a] = w_add(r[I->b], I->imm); break;
+    case O_BR: *pc = r[I->a] != 0 ? (uint32_t)I->imm : (uint32_t)I->b + 256u * I->c; return 1;
+    case O_JMP: *pc = (uint32_t)I->imm; return 1;
+    default: return 0;
+  }
+  (void)P;
+  *pc += 1;
+  return 1;
+}
+
+/* ---- (1) the canonical algorithm ---------------------------------------- */
+
+typedef struct { uint32_t cell_arr; int32_t idx; uint32_t tid; uint8_t w; int32_t val; } acc; /* one access record */
+typedef struct { acc* v; size_t n, cap; } acclist;
+static void acc_push(acclist* L, acc a) {
+  if (L->n == L->cap) { L->cap = L->cap ? 2 * L->cap : 1024; L->v = (acc*)realloc(L->v, L->cap * sizeof(acc)); }
+  L->v[L->n++] = a;
+}
+static int acc_cmp(const void* x, const void* y) {
+  const acc* a = (const acc*)x; const acc* b = (const acc*)y;
+  if (a->cell_arr != b->cell_arr) return a->cell_arr < b->cell_arr ? -1 : 1;
+  if (a->idx != b->idx) return a->idx < b->idx ? -1 : 1;
+  if (a->tid != b->tid) return a->tid < b->tid ? -1 : 1;
+  if (a->w != b->w) return a->w < b->w ? -1 : 1;
+  return 0;
+}
+
+typedef struct { uint32_t arr; int32_t idx; int32_t val; } ownw; /* own-write overlay entry */
+
+typedef struct {
+  uint64_t checked, loads, stores, instructions, intervals_max, lanes_final[8];
+} ostats;
+
+typedef struct {
+  const oprog* P; uint32_t n; const uint32_t* sizes;
+  const int32_t* const* inputs; uint32_t n_instances; uint32_t instance_offset;
+  uint64_t fuel; uint32_t max_intervals;
+  int32_t* const* final_heaps;
+  /* per-thread results */
+  int next_instance; pthread_mutex_t mu;
+} runctx;
+
+typedef struct { replist reps; ostats st; } thread_out;
+
+/* Run one instance exactly as DESIGN.md §3 describes.  If stop_at >= 0 the
+ * run stops at the START of interval stop_at and the lane state + heap are
+ * copied out (used to seed the enumerator); returns 1 if that interval is
+ * reached, 0 otherwise. */
+static int run_instance(const oprog* P, uint32_t n, const uint32_t* sizes, int32_t** heap,
+                        uint32_t inst_global, uint64_t fuel, uint32_t max_intervals,
+                        replist* reps, ostats* st, int stop_at,
+                        int32_t* out_regs, uint32_t* out_pc, uint8_t* out_status, uint64_t* out_intervals) {
+  uint32_t A = P->n_arrays, R = P->n_regs;
+  int32_t* regs = (int32_t*)calloc((size_t)n * R + 1, sizeof(int32_t)); /* registers start at 0 (L18) */
+  uint32_t* pc = (uint32_t*)calloc(n + 1, sizeof(uint32_t));              /* start = pc 0 */
+  uint8_t* status = (uint8_t*)calloc(n + 1, 1);                           /* RUNNING */
+  int32_t* node = (int32_t*)malloc((n + 1) * sizeof(int32_t));
+  uint8_t* arrived = (uint8_t*)malloc(n + 1);
+  int32_t** snap = (int32_t**)malloc((A + 1) * sizeof(int32_t*));
+  for (uint32_t a = 0; a < A; a++) snap[a] = (int32_t*)malloc(((size_t)sizes[a] + 1) * sizeof(int32_t));
+  acclist log = {0};
+  size_t own_cap = 16; ownw* own = (ownw*)malloc(own_cap * sizeof(ownw));
+  uint32_t k = 0;
+  int reached = 0;
+
+  for (;;) {
+    if (stop_at >= 0 && k == (uint32_t)stop_at) { reached = 1; break; }
+    /* interval k: snap <- heap (the shared state every read of this interval sees) */
+    for (uint32_t a = 0; a < A; a++) memcpy(snap[a], heap[a], (size_t)sizes[a] * sizeof(int32_t));
+    log.n = 0;
+    memset(arrived, 0, n);
+    for (uint32_t t = 0; t < n; t++) {
+      if (status[t] != S_RUNNING) continue;
+      int32_t* r = regs + (size_t)t * R;
+      size_t n_own = 0;
+      uint64_t steps = 0;
+      for (;;) {
+        if (steps == fuel) { /* fuel exhausted (reading L17) */
+          rep_push(reps, mkrep(inst_global, k, -1, (int32_t)pc[t], t, NOTID, K_FUEL, 0));
+          status[t] = S_FUEL; break;
+        }
+        steps++;
+        st->instructions++;
+        const oins* I = &P->code[pc[t]];
+        int fault;
+        if (step_private(P, I, r, t, sizes, &pc[t], &fault)) {
+          if (fault == S_DIV0) {
+            rep_push(reps, mkrep(inst_global, k, -1, (int32_t)pc[t], t, NOTID, K_DIV0, 0));
+            status[t] = S_DIV0; break;
+          }
+          continue;
+        }
+        if (I->op == O_LD) { /* v := a[w]   (reading L11) */
+          int32_t idx = r[I->c];
+          if (idx < 0 || (uint32_t)idx >= sizes[I->b]) { /* ⊥: not performed, not logged (L5) */
+            rep_push(reps, mkrep(inst_global, k, I->b, idx, t, NOTID, K_OOB, 0));
+            status[t] = S_OOB; break;
+          }
+          int32_t v = snap[I->b][idx];
+          for (size_t j = 0; j < n_own; j++)
+            if (own[j].arr == I->b && own[j].idx == idx) v = own[j].val; /* own earlier write */
+          acc a = {I->b, idx, t, 0, 0};
+          acc_push(&log, a);
+          st->checked++; st->loads++;
+          r[I->a] = v;
+          pc[t]++;
+        } else if (I->op == O_ST) { /* a[v] := e */
+          int32_t idx = r[I->b];
+          if (idx < 0 || (uint32_t)idx >= sizes[I->a]) {
+            rep_push(reps, mkrep(inst_global, k, I->a, idx, t, NOTID, K_OOB, 0));
+            status[t] = S_OOB; break;
+          }
+          size_t j;
+          for (j = 0; j < n_own; j++)
+            if (own[j].arr == I->a && own[j].idx == idx) break;
+          if (j == n_own) {
+            if (n_own == own_cap) { own_cap *= 2; own = (ownw*)realloc(own, own_cap * sizeof(ownw)); }
+            own[n_own].arr = I->a; own[n_own].idx = idx; n_own++;
+          }
+          own[j].val = r[I->c];
+          st->checked++; st->stores++;
+          pc[t]++;
+        } else if (I->op == O_BAR) { /* τ ⊡ σ */
+          status[t] = S_WAITING; node[t] = (int32_t)pc[t]; arrived[t] = 1; pc[t]++; break;
+        } else if (I->op == O_EXIT) { /* exit node = implicit final barrier */
+          status[t] = S_EXITED; node[t] = -1; arrived[t] = 1; break;
+        } else if (I->op == O_ASSUME) { /* false -> ⊤, reading L6 */
+          if (r[I->a] == 0) { status[t] = S_PRUNED; break; }
+          pc[t]++;
+        } else if (I->op == O_ASSERT) { /* false -> ⊥ */
+          if (r[I->a] == 0) {
+            rep_push(reps, mkrep(inst_global, k, -1, (int32_t)pc[t], t, NOTID, K_ASSERT, 0));
+            status[t] = S_ASSERT; break;
+          }
+          pc[t]++;
+        } else {
+          fprintf(stderr, "oracle: bad opcode %d\n", I->op); abort();
+        }
+      }
+      /* the work-item's writes of this interval, one per cell, final value (L3) */
+      for (size_t j = 0; j < n_own; j++) {
+        acc a = {own[j].arr, own[j].idx, t, 1, own[j].val};
+        acc_push(&log, a);
+      }
+    }
+
+    /* race rule per cell (PAPER.md:224-229 as reading L1), in (array,index) order */
+    qsort(log.v, log.n, sizeof(acc), acc_cmp);
+    size_t g = 0;
+    uint32_t* rt = NULL; uint32_t* wt = NULL; int32_t* wv = NULL; size_t cap = 0;
+    while (g < log.n) {
+      size_t e = g;
+      while (e < log.n && log.v[e].cell_arr == log.v[g].cell_arr && log.v[e].idx == log.v[g].idx) e++;
+      if (e - g > cap) { cap = e - g; rt = (uint32_t*)realloc(rt, cap * 4); wt = (uint32_t*)realloc(wt, cap * 4); wv = (int32_t*)realloc(wv, cap * 4); }
+      size_t nr = 0, nw = 0;  /* R(c): distinct readers ascending; W(c): writers ascending */
+      for (size_t i = g; i < e; i++) {
+        if (log.v[i].w) { wt[nw] = log.v[i].tid; wv[nw] = log.v[i].val; nw++; }
+        else if (nr == 0 || rt[nr - 1] != log.v[i].tid) rt[nr++] = log.v[i].tid;
+      }
+      uint32_t arr = log.v[g].cell_arr; int32_t idx = log.v[g].idx;
+      /* membership helpers (linear, plain) */
+#define IN_R(x) ({ int f_ = 0; for (size_t q_ = 0; q_ < nr; q_++) if (rt[q_] == (x)) f_ = 1; f_; })
+#define IN_W(x) ({ int f_ = 0; for (size_t q_ = 0; q_ < nw; q_++) if (wt[q_] == (x)) f_ = 1; f_; })
+#define FLAGS(a_, b_) ((IN_R(a_) ? 1 : 0) | (IN_W(a_) ? 2 : 0) | (IN_R(b_) ? 4 : 0) | (IN_W(b_) ? 8 : 0))
+      /* RW: lexicographically smallest (t1<t2), one reads and the other writes */
+      int have_rw = 0; uint32_t p1 = 0, p2 = 0;
+      if (nr > 0 && nw > 0) {
+        /* candidates in ascending order: the sorted union of R and W */
+        size_t nu = 0; uint32_t* u = (uint32_t*)malloc((nr + nw) * 4);
+        size_t i = 0, j = 0;
+        while (i < nr || j < nw) {
+          uint32_t x;
+          if (j >= nw || (i < nr && rt[i] < wt[j])) x = rt[i++];
+          else if (i >= nr || wt[j] < rt[i]) x = wt[j++];
+          else { x = rt[i]; i++; j++; }
+          u[nu++] = x;
+        }
+        for (size_t a1 = 0; a1 < nu && !have_rw; a1++)
+          for (size_t a2 = a1 + 1; a2 < nu; a2++)
+            if ((IN_R(u[a1]) && IN_W(u[a2])) || (IN_W(u[a1]) && IN_R(u[a2]))) {
+              have_rw = 1; p1 = u[a1]; p2 = u[a2]; break;
+            }
+        free(u);
+      }
+      if (have_rw) rep_push(reps, mkrep(inst_global, k, (int32_t)arr, idx, p1, p2, K_RW, FLAGS(p1, p2)));
+      /* WW: |W(c)| >= 2; non-benign iff two writers' final values differ */
+      if (nw >= 2) {
+        size_t d = 0;
+        for (size_t q = 1; q < nw; q++) if (wv[q] != wv[0]) { d = q; break; }
+        if (d) rep_push(reps, mkrep(inst_global, k, (int32_t)arr, idx, wt[0], wt[d], K_WWN, FLAGS(wt[0], wt[d])));
+        else rep_push(reps, mkrep(inst_global, k, (int32_t)arr, idx, wt[0], wt[1], K_WWB, FLAGS(wt[0], wt[1])));
+      }
+#undef IN_R
+#undef IN_W
+#undef FLAGS
+      /* barrier release: the max-tid writer's value is committed (I4) */
+      if (nw > 0) heap[arr][idx] = wv[nw - 1];
+      g = e;
+    }
+    free(rt); free(wt); free(wv);
+
+    /* barrier divergence among the work-items that arrived in this interval (L9) */
+    {
+      int64_t t1 = -1;
+      for (uint32_t t = 0; t < n; t++) if (arrived[t]) { t1 = t; break; }
+      if (t1 >= 0) {
+        for (uint32_t t = (uint32_t)t1 + 1; t < n; t++)
+          if (arrived[t] && node[t] != node[t1]) {
+            rep_push(reps, mkrep(inst_global, k, -1, node[t1], (uint32_t)t1, t, K_DIV, 0));
+            break;
+          }
+      }
+    }
+
+    int any_waiting = 0;
+    for (uint32_t t = 0; t < n; t++) if (status[t] == S_WAITING) { status[t] = S_RUNNING; any_waiting = 1; }
+    if (!any_waiting) break;
+    k++;
+    if (k >= max_intervals) {
+      rep_push(reps, mkrep(inst_global, k, -1, -1, NOTID, NOTID, K_FUEL, 0));
+      for (uint32_t t = 0; t < n; t++) if (status[t] == S_RUNNING) status[t] = S_WAITING;
+      k--; /* intervals executed = max_intervals */
+      break;
+    }
+  }
+  if (stop_at >= 0) { /* lane state at the start of interval stop_at (or at the end) */
+    memcpy(out_regs, regs, (size_t)n * R * sizeof(int32_t));
+    memcpy(out_pc, pc, n * sizeof(uint32_t));
+    memcpy(out_status, status, n);
+  }
+  if (!reached) {
+    for (uint32_t t = 0; t < n; t++) {
+      int s = status[t];
+      int slot = s == S_EXITED ? 0 : s == S_PRUNED ? 1 : s == S_OOB ? 2 : s == S_ASSERT ? 3 :
+                 s == S_DIV0 ? 4 : s == S_FUEL ? 5 : 6;
+      st->lanes_final[slot]++;
+    }
+    if ((uint64_t)k + 1 > st->intervals_max) st->intervals_max = (uint64_t)k + 1;
+    if (out_intervals) *out_intervals = (uint64_t)k + 1;
+  }
+  free(regs); free(pc); free(status); free(node); free(arrived);
+  for (uint32_t a = 0; a < A; a++) free(snap[a]);
+  free(snap); free(log.v); free(own);
+  return reached;
+}
+
+typedef struct { runctx* ctx; thread_out out; } worker_arg;
+
+static void* worker(void* p) {
+  worker_arg* W = (worker_arg*)p;
+  runctx* c = W->ctx;
+  const oprog* P = c->P;
+  int32_t** heap = (int32_t**)malloc((P->n_arrays + 1) * sizeof(int32_t*));
+  for (uint32_t a = 0; a < P->n_arrays; a++) heap[a] = (int32_t*)malloc(((size_t)c->sizes[a] + 1) * sizeof(int32_t));
+  for (;;) {
+    pthread_mutex_lock(&c->mu);
+    int i = c->next_instance++;
+    pthread_mutex_unlock(&c->mu);
+    if (i >= (int)c->n_instances) break;
+    for (uint32_t a = 0; a < P->n_arrays; a++)  /* heap <- copy(inputs[inst]) */
+      memcpy(heap[a], c->inputs[a] + (size_t)i * c->sizes[a], (size_t)c->sizes[a] * sizeof(int32_t));
+    run_instance(P, c->n, c->sizes, heap, c->instance_offset + (uint32_t)i, c->fuel, c->max_intervals,
+                 &W->out.reps, &W->out.st, -1, NULL, NULL, NULL, NULL);
+    if (c->final_heaps)
+      for (uint32_t a = 0; a < P->n_arrays; a++)
+        if (c->final_heaps[a])
+          memcpy(c->final_heaps[a] + (size_t)i * c->sizes[a], heap[a], (size_t)c->sizes[a] * sizeof(int32_t));
+  }
+  for (uint32_t a = 0; a < P->n_arrays; a++) free(heap[a]);
+  free(heap);
+  return NULL;
+}
+
+/* Public: run the canonical algorithm on n_instances instances.
+ * inputs[a] = n_instances * sizes[a] int32 (instance-major).  Reports are
+ * returned malloc'd in canonical order (free with oracle_free).  stats[13] =
+ * checked, loads, stores, instructions, intervals_max, lanes_final[8]. */
+int oracle_run(const uint8_t* bc, size_t nbytes, uint32_t n, const uint32_t* sizes,
+               const int32_t* const* inputs, uint32_t n_instances, uint32_t instance_offset,
+               uint64_t fuel, uint32_t max_intervals, int n_threads,
+               orep** reports, uint64_t* n_reports, int32_t* const* final_heaps, uint64_t* stats) {
+  oprog P;
+  if (decode(bc, nbytes, &P)) return -1;
+  runctx c;
+  memset(&c, 0, sizeof c);
+  c.P = &P; c.n = n; c.sizes = sizes; c.inputs = inputs; c.n_instances = n_instances;
+  c.instance_offset = instance_offset; c.fuel = fuel; c.max_intervals = max_intervals;
+  c.final_heaps = final_heaps;
+  pthread_mutex_init(&c.mu, NULL);
+  if (n_threads < 1) n_threads = 1;
+  worker_arg* W = (worker_arg*)calloc((size_t)n_threads, sizeof(worker_arg));
+  pthread_t* th = (pthread_t*)calloc((size_t)n_threads, sizeof(pthread_t));
+  for (int i = 0; i < n_threads; i++) { W[i].ctx = &c; pthread_create(&th[i], NULL, worker, &W[i]); }
+  for (int i = 0; i < n_threads; i++) pthread_join(th[i], NULL);
+  replist all = {0};
+  ostats S; memset(&S, 0, sizeof S);
+  for (int i = 0; i < n_threads; i++) {
+    for (size_t j = 0; j < W[i].out.reps.n; j++) rep_push(&all, W[i].out.reps.v[j]);
+    free(W[i].out.reps.v);
+    S.checked += W[i].out.st.checked; S.loads += W[i].out.st.loads; S.stores += W[i].out.st.stores;
+    S.instructions += W[i].out.st.instructions;
+    if (W[i].out.st.intervals_max > S.intervals_max) S.intervals_max = W[i].out.st.intervals_max;
+    for (int q = 0; q < 8; q++) S.lanes_final[q] += W[i].out.st.lanes_final[q];
+  }
+  if (all.n) qsort(all.v, all.n, sizeof(orep), rep_cmp);
+  *reports = all.v; *n_reports = all.n;
+  if (stats) {
+    stats[0] = S.checked; stats[1] = S.loads; stats[2] = S.stores; stats[3] = S.instructions;
+    stats[4] = S.intervals_max;
+    for (int q = 0; q < 8; q++) stats[5 + q] = S.lanes_final[q];
+  }
+  free(W); free(th); free(P.code);
+  pthread_mutex_destroy(&c.mu);
+  return 0;
+}
+
+void oracle_free(void* p) { free(p); }
+
+/* Public: canonical state at the START of interval k of ONE instance
+ * (heap per array concatenated into heap_out, lane regs/pc/status).
+ * Returns 1 if interval k is reached, 0 if the instance ended earlier, -1 on
+ * a decode error. */
+int oracle_state_at(const uint8_t* bc, size_t nbytes, uint32_t n, const uint32_t* sizes,
+                    const int32_t* const* inputs, uint64_t fuel, uint32_t k,
+                    int32_t* heap_out, int32_t* regs_out, uint32_t* pc_out, uint8_t* status_out) {
+  oprog P;
+  if (decode(bc, nbytes, &P)) return -1;
+  int32_t** heap = (int32_t**)malloc((P.n_arrays + 1) * sizeof(int32_t*));
+  for (uint32_t a = 0; a < P.n_arrays; a++) {
+    heap[a] = (int32_t*)malloc(((size_t)sizes[a] + 1) * sizeof(int32_t));
+    memcpy(heap[a], inputs[a], (size_t)sizes[a] * sizeof(int32_t));
+  }
+  replist reps = {0}; ostats st; memset(&st, 0, sizeof st);
+  int reached = run_instance(&P, n, sizes, heap, 0, fuel, 0xFFFFFFFFu, &reps, &st, (int)k,
+                             regs_out, pc_out, status_out, NULL);
+  size_t off = 0;
+  for (uint32_t a = 0; a < P.n_arrays; a++) {
+    memcpy(heap_out + off, heap[a], (size_t)sizes[a] * sizeof(int32_t));
+    off += sizes[a];
+    free(heap[a]);
+  }
+  free(heap); free(reps.v); free(P.code);
+  return reached;
+}
+
+/* ---- (2) the brute-force interleaving enumerator ------
+ * State = every thread's (pc, registers, status, steps) + ONE shared heap.
+ * A global step picks any RUNNING thread and applies one thread-local rule
+ * to the shared heap with immediate visibility
+ * (PAPER.md:212).  The interval ends when no thread is RUNNING (all
+ * suspended at a barrier, exited, or stopped by ⊥/⊤ as readings
+ * L5/L6).  Explores every interleaving; with memo != 0 identical states are
+ * merged (schedule counts are summed), without memo every schedule is walked
+ * (used for the C(a+b,a) count check). */
+
+typedef struct {
+  const oprog* P; uint32_t n; const uint32_t* sizes; uint32_t cells; uint64_t fuel;
+  size_t state_words;                  /* int32 words per state */
+  /* memo table: open addressing over state blobs */
+  int32_t* keys; uint64_t* counts; uint8_t* used; size_t tcap, tn;
+  /* terminal set */
+  int32_t* terms; uint8_t* tused; size_t ttcap, ttn;
+  uint64_t n_schedules; int memo; uint64_t budget; int over_budget;
+} enumctx;
+
+/* state layout (int32 words): heap[cells] | per thread: pc, status, steps_lo, steps_hi, regs[R] */
+static size_t lane_words(const oprog* P) { return 4 + P->n_regs; }
+
+static uint64_t hash_words(const int32_t* w, size_t n) {
+  uint64_t h = 1469598103934665603ull;
+  for (size_t i = 0; i < n; i++) { h ^= (uint32_t)w[i]; h *= 1099511628211ull; h ^= h >> 29; }
+  return h;
+}
+
+static int set_insert(int32_t** keys, uint8_t** used, size_t* cap, size_t* cnt, size_t words,
+                      const int32_t* s, size_t* slot_out, uint64_t** counts) {
+  if ((*cnt + 1) * 2 > *cap) { /* grow */
+    size_t ncap = *cap ? *cap * 2 : 1024;
+    int32_t* nk = (int32_t*)malloc(ncap * words * sizeof(int32_t));
+    uint8_t* nu = (uint8_t*)calloc(ncap, 1);
+    uint64_t* nc = counts ? (uint64_t*)calloc(ncap, sizeof(uint64_t)) : NULL;
+    for (size_t i = 0; i < *cap; i++) if ((*used)[i]) {
+      size_t h = hash_words(*keys + i * words, words) & (ncap - 1);
+      while (nu[h]) h = (h + 1) & (ncap - 1);
+      nu[h] = 1; memcpy(nk + h * words, *keys + i * words, words * sizeof(int32_t));
+      if (counts) nc[h] = (*counts)[i];
+    }
+    free(*keys); free(*used); *keys = nk; *used = nu; *cap = ncap;
+    if (counts) { free(*counts); *counts = nc; }
+  }
+  size_t h = hash_words(s, words) & (*cap - 1);
+  while ((*used)[h]) {
+    if (!memcmp(*keys + h * words, s, words * sizeof(int32_t))) { *slot_out = h; return 0; }
+    h = (h + 1) & (*cap - 1);
+  }
+  (*used)[h] = 1; memcpy(*keys + h * words, s, words * sizeof(int32_t)); (*cnt)++;
+  *slot_out = h;
+  return 1;
+}
+
+/* apply one step of thread t to state s (in place). */
+static void enum_step(enumctx* E, int32_t* s, uint32_t t) {
+  const oprog* P = E->P;
+  int32_t* heap = s;
+  int32_t* L = s + E->cells + (size_t)t * lane_words(P);
+  uint32_t* pc = (uint32_t*)&L[0];
+  int32_t* st = &L[1];
+  uint64_t steps = (uint32_t)L[2] | ((uint64_t)(uint32_t)L[3] << 32);
+  int32_t* r = L + 4;
+  if (steps == E->fuel) { *st = S_FUEL; return; }
+  steps++;
+  L[2] = (int32_t)(uint32_t)steps; L[3] = (int32_t)(uint32_t)(steps >> 32);
+  const oins* I = &P->code[*pc];
+  int fault;
+  if (step_private(P, I, r, t, E->sizes, pc, &fault)) { if (fault) *st = fault; return; }
+  size_t base = 0;
+  switch (I->op) {
+    case O_LD: {
+      for (uint32_t a = 0; a < I->b; a++) base += E->sizes[a];
+      int32_t idx = r[I->c];
+      if (idx < 0 || (uint32_t)idx >= E->sizes[I->b]) { *st = S_OOB; return; }
+      r[I->a] = heap[base + (uint32_t)idx]; (*pc)++; return;
+    }
+    case O_ST: {
+      for (uint32_t a = 0; a < I->a; a++) base += E->sizes[a];
+      int32_t idx = r[I->b];
+      if (idx < 0 || (uint32_t)idx >= E->sizes[I->a]) { *st = S_OOB; return; }
+      heap[base + (uint32_t)idx] = r[I->c]; (*pc)++; return;
+    }
+    case O_BAR: *st = S_WAITING; (*pc)++; return;
+    case O_EXIT: *st = S_EXITED; return;
+    case O_ASSUME: if (r[I->a] == 0) *st = S_PRUNED; else (*pc)++; return;
+    case O_ASSERT: if (r[I->a] == 0) *st = S_ASSERT; else (*pc)++; return;
+    default: abort();
+  }
+}
+
+static uint64_t enum_dfs(enumctx* E, int32_t* s) {
+  if (E->over_budget) return 0;
+  size_t W = E->state_words, LW = lane_words(E->P);
+  int any = 0;
+  for (uint32_t t = 0; t < E->n; t++) if (s[E->cells + (size_t)t * LW + 1] == S_RUNNING) { any = 1; break; }
+  if (!any) { /* end of interval: record the terminal state (steps zeroed: not observable) */
+    int32_t* c = (int32_t*)malloc(W * sizeof(int32_t));
+    memcpy(c, s, W * sizeof(int32_t));
+    for (uint32_t t = 0; t < E->n; t++) { c[E->cells + (size_t)t * LW + 2] = 0; c[E->cells + (size_t)t * LW + 3] = 0; }
+    size_t slot;
+    set_insert(&E->terms, &E->tused, &E->ttcap, &E->ttn, W, c, &slot, NULL);
+    free(c);
+    return 1;
+  }
+  size_t slot = 0;
+  if (E->memo) {
+    if (!set_insert(&E->keys, &E->used, &E->tcap, &E->tn, W, s, &slot, &E->counts))
+      return E->counts[slot];
+    if (E->tn > E->budget) { E->over_budget = 1; return 0; }
+  } else {
+    if (++E->tn > E->budget) { E->over_budget = 1; return 0; }
+  }
+  uint64_t total = 0;
+  int32_t* nxt = (int32_t*)malloc(W * sizeof(int32_t));
+  for (uint32_t t = 0; t < E->n; t++) {
+    if (s[E->cells + (size_t)t * LW + 1] != S_RUNNING) continue;
+    memcpy(nxt, s, W * sizeof(int32_t));
+    enum_step(E, nxt, t);
+    total += enum_dfs(E, nxt);
+  }
+  free(nxt);
+  if (E->memo) {
+    /* re-find the slot (the table may have grown) */
+    size_t h = hash_words(s, W) & (E->tcap - 1);
+    while (memcmp(E->keys + h * W, s, W * sizeof(int32_t))) h = (h + 1) & (E->tcap - 1);
+    E->counts[h] = total;
+  }
+  return total;
+}
+
+/* Public: explore all interleavings of one interval.
+ * heap0: all arrays concatenated (cells words); regs0 [n][n_regs]; pc0[n];
+ * status0[n] (0 = RUNNING, others are left as they are).
+ * Outputs: *n_schedules (saturating), terminal states malloc'd into *terms as
+ * *n_terms rows of (cells + n*(4+n_regs)) int32 words (heap, then per thread
+ * pc, status, 0, 0, regs).  Returns 0, or 1 if `budget` states/schedules were
+ * exceeded (results incomplete), -1 on decode error. */
+int oracle_enumerate(const uint8_t* bc, size_t nbytes, uint32_t n, const uint32_t* sizes,
+                     const int32_t* heap0, const int32_t* regs0, const uint32_t* pc0,
+                     const uint8_t* status0, uint64_t fuel, int memo, uint64_t budget,
+                     uint64_t* n_schedules, int32_t** terms, uint64_t* n_terms, uint64_t* row_words) {
+  oprog P;
+  if (decode(bc, nbytes, &P)) return -1;
+  enumctx E;
+  memset(&E, 0, sizeof E);
+  E.P = &P; E.n = n; E.sizes = sizes; E.fuel = fuel; E.memo = memo; E.budget = budget;
+  for (uint32_t a = 0; a < P.n_arrays; a++) E.cells += sizes[a];
+  size_t LW = lane_words(&P);
+  E.state_words = E.cells + (size_t)n * LW;
+  int32_t* s = (int32_t*)calloc(E.state_words, sizeof(int32_t));
+  memcpy(s, heap0, E.cells * sizeof(int32_t));
+  for (uint32_t t = 0; t < n; t++) {
+    int32_t* L = s + E.cells + (size_t)t * LW;
+    L[0] = (int32_t)pc0[t]; L[1] = status0[t]; L[2] = 0; L[3] = 0;
+    memcpy(L + 4, regs0 + (size_t)t * P.n_regs, P.n_regs * sizeof(int32_t));
+  }
+  uint64_t cnt = enum_dfs(&E, s);
+  *n_schedules = cnt;
+  *row_words = E.state_words;
+  *n_terms = E.ttn;
+  int32_t* out = (int32_t*)malloc((E.ttn ? E.ttn : 1) * E.state_words * sizeof(int32_t));
+  size_t o = 0;
+  for (size_t i = 0; i < E.ttcap; i++)
+    if (E.tused[i]) { memcpy(out + o * E.state_words, E.terms + i * E.state_words, E.state_words * sizeof(int32_t)); o++; }
+  *terms = out;
+  free(s); free(E.keys); free(E.counts); free(E.used); free(E.terms); free(E.tused); free(P.code);
+  return E.over_budget ? 1 : 0;
+}
