@@ -29,6 +29,12 @@ extern "C" {
 
 #define RC_ABI_VERSION 1
 
+#if defined(__GNUC__)
+#define RC_API __attribute__((visibility("default")))
+#else
+#define RC_API
+#endif
+
 /* ---- status codes ------------------------------------------------------- */
 typedef enum {
   RC_OK = 0,
@@ -186,10 +192,10 @@ typedef struct rc_program rc_program; /* opaque, library-owned */
  * or n_arrays or n_instr out of range, unknown opcode, register >= n_regs,
  * array >= n_arrays, branch target >= n_instr, execution that can fall off
  * the end, no EXIT reachable from pc 0.                                     */
-int rc_load_program(const void* bytecode, size_t nbytes, rc_program** out);
-void rc_free_program(rc_program* prog);
+RC_API int rc_load_program(const void* bytecode, size_t nbytes, rc_program** out);
+RC_API void rc_free_program(rc_program* prog);
 /* n_regs, n_arrays, n_instr of a loaded program (any pointer may be NULL). */
-int rc_program_info(const rc_program* prog, uint32_t* n_regs, uint32_t* n_arrays,
+RC_API int rc_program_info(const rc_program* prog, uint32_t* n_regs, uint32_t* n_arrays,
                     uint32_t* n_instr);
 
 /* Run `prog` with `work_group_size` work-items (tids 0..n-1) on each of
@@ -202,18 +208,18 @@ int rc_program_info(const rc_program* prog, uint32_t* n_regs, uint32_t* n_arrays
  * Stream-ordered on options->cuda_stream; returns after the reports are on
  * the host (synchronises that stream).  Not re-entrant on the same program
  * object from two threads at once (the program caches device workspace).  */
-int rc_run(const rc_program* prog, uint32_t work_group_size, const rc_array* arrays,
+RC_API int rc_run(const rc_program* prog, uint32_t work_group_size, const rc_array* arrays,
            uint32_t n_arrays, uint32_t n_instances, const rc_options* options,
            rc_report* out, uint64_t capacity, uint64_t* n_reports_total,
            rc_stats* stats, int32_t* const* final_heaps);
 
 /* Thread-local message describing the last non-OK status of this thread. */
-const char* rc_last_error(void);
-int rc_abi_version(void);
+RC_API const char* rc_last_error(void);
+RC_API int rc_abi_version(void);
 /* Release all cached device workspace of `prog` (also done by rc_free_program). */
-int rc_release_workspace(rc_program* prog);
+RC_API int rc_release_workspace(rc_program* prog);
 
-#define RC_OVERLAY_CAP 32 /* distinct cells one work-item may write per interval */
+#define RC_OVERLAY_CAP 16 /* distinct cells one work-item may write per interval */
 
 #ifdef __cplusplus
 }

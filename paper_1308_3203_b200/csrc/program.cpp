@@ -1,0 +1,145 @@
+// program.cpp — rc_load_program: RCB1 decode + CFG validation (host only).
+//
+// The bytecode encodes a kernel K(Args) = (tid, C, ->, Locals)
+// as a control-flow graph: instruction nodes, successors given by fall-through,
+// BR (the assume(b)/assume(¬b) successor pair) and JMP, a unique start (pc 0)
+// and the exit node (every EXIT instruction).  Validation guarantees the
+// interpreter never reads outside the program, registers or array table.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "rc_internal.h"
+
+namespace rc {
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+static uint32_t rd32(const uint8_t* p) { uint32_t v; memcpy(&v, p, 4); return v; }
+static uint16_t rd16(const uint8_t* p) { uint16_t v; memcpy(&v, p, 2); return v; }
+
+static const char* op_name(int op) {
+  static const char* names[] = {"?", "CONST", "MOV", "TID", "SIZE", "ADD", "SUB", "MUL", "DIV", "MOD", "MIN",
+                                "MAX", "AND", "OR", "XOR", "LT", "EQ", "LAND", "LNOT", "LD", "ST", "BAR",
+                                "ASSUME", "ASSERT", "BR", "JMP", "EXIT", "ADDI"};
+  return (op >= 1 && op <= RC_OP_ADDI) ? names[op] : "?";
+}
+
+// register / array operands of each opcode: 'r' register, 'a' array, '-' unused
+static const char* operand_kinds(int op) {
+  switch (op) {
+    case RC_OP_CONST: case RC_OP_TID: return "r--";
+    case RC_OP_MOV: case RC_OP_LNOT: case RC_OP_ADDI: return "rr-";
+    case RC_OP_SIZE: return "ra-";
+    case RC_OP_ADD: case RC_OP_SUB: case RC_OP_MUL: case RC_OP_DIV: case RC_OP_MOD: case RC_OP_MIN:
+    case RC_OP_MAX: case RC_OP_AND: case RC_OP_OR: case RC_OP_XOR: case RC_OP_LT: case RC_OP_EQ:
+    case RC_OP_LAND: return "rrr";
+    case RC_OP_LD: return "rar";
+    case RC_OP_ST: return "arr";
+    case RC_OP_ASSUME: case RC_OP_ASSERT: case RC_OP_BR: return "r--";
+    case RC_OP_BAR: case RC_OP_JMP: case RC_OP_EXIT: return "---";
+    default: return nullptr;
+  }
+}
+
+int validate(const uint8_t* bc, size_t nbytes, rc_program* P) {
+  if (!bc) return fail(RC_EINVAL, "bytecode pointer is NULL");
+  if (nbytes < 16) return fail(RC_EINVAL, "bytecode shorter than the 16-byte header (%zu bytes)", nbytes);
+  if (rd32(bc) != RC_MAGIC) return fail(RC_EINVAL, "bad magic 0x%08x (expected 'RCB1')", rd32(bc));
+  if (rd16(bc + 4) != 1) return fail(RC_EINVAL, "unsupported version %u", rd16(bc + 4));
+  if (rd16(bc + 6) != 0) return fail(RC_EINVAL, "header flags must be 0 (got %u)", rd16(bc + 6));
+  uint32_t n_regs = rd16(bc + 8), n_arrays = rd16(bc + 10), n_instr = rd32(bc + 12);
+  if (n_regs < 1 || n_regs > 256) return fail(RC_EINVAL, "n_regs %u outside 1..256", n_regs);
+  if (n_arrays > 256) return fail(RC_EINVAL, "n_arrays %u > 256", n_arrays);
+  if (n_instr < 1 || n_instr > 65536) return fail(RC_EINVAL, "n_instr %u outside 1..65536", n_instr);
+  if (nbytes != 16 + 8 * (size_t)n_instr)
+    return fail(RC_EINVAL, "size mismatch: %zu bytes for %u instructions (expected %zu)", nbytes, n_instr,
+                16 + 8 * (size_t)n_instr);
+  std::vector<Ins> code(n_instr);
+  memcpy(code.data(), bc + 16, 8 * (size_t)n_instr);
+  for (uint32_t pc = 0; pc < n_instr; pc++) {
+    const Ins& I = code[pc];
+    const char* k = operand_kinds(I.op);
+    if (!k) return fail(RC_EINVAL, "pc %u: unknown opcode %u", pc, I.op);
+    const uint8_t f[3] = {I.a, I.b, I.c};
+    for (int j = 0; j < 3; j++) {
+      if (k[j] == 'r' && f[j] >= n_regs)
+        return fail(RC_EINVAL, "pc %u (%s): register r%u >= n_regs %u", pc, op_name(I.op), f[j], n_regs);
+      if (k[j] == 'a' && f[j] >= n_arrays)
+        return fail(RC_EINVAL, "pc %u (%s): array %u >= n_arrays %u", pc, op_name(I.op), f[j], n_arrays);
+    }
+    if (I.op == RC_OP_BR) {
+      uint32_t t = (uint32_t)I.imm, e = (uint32_t)I.b + 256u * I.c;
+      if (I.imm < 0 || t >= n_instr) return fail(RC_EINVAL, "pc %u (BR): true target %d >= n_instr %u", pc, I.imm, n_instr);
+      if (e >= n_instr) return fail(RC_EINVAL, "pc %u (BR): false target %u >= n_instr %u", pc, e, n_instr);
+    }
+    if (I.op == RC_OP_JMP && (I.imm < 0 || (uint32_t)I.imm >= n_instr))
+      return fail(RC_EINVAL, "pc %u (JMP): target %d >= n_instr %u", pc, I.imm, n_instr);
+  }
+  // reachability from start (pc 0): no fall-through off the end, some EXIT reachable
+  std::vector<uint8_t> seen(n_instr, 0);
+  std::vector<uint32_t> stack{0};
+  bool exit_reachable = false;
+  seen[0] = 1;
+  while (!stack.empty()) {
+    uint32_t pc = stack.back();
+    stack.pop_back();
+    const Ins& I = code[pc];
+    uint32_t succ[2];
+    int ns = 0;
+    if (I.op == RC_OP_EXIT) { exit_reachable = true; continue; }
+    if (I.op == RC_OP_BR) { succ[ns++] = (uint32_t)I.imm; succ[ns++] = (uint32_t)I.b + 256u * I.c; }
+    else if (I.op == RC_OP_JMP) succ[ns++] = (uint32_t)I.imm;
+    else {
+      if (pc + 1 >= n_instr)
+        return fail(RC_EINVAL, "pc %u (%s): execution falls off the end of the program", pc, op_name(I.op));
+      succ[ns++] = pc + 1;
+    }
+    for (int j = 0; j < ns; j++)
+      if (!seen[succ[j]]) { seen[succ[j]] = 1; stack.push_back(succ[j]); }
+  }
+  if (!exit_reachable) return fail(RC_EINVAL, "no EXIT instruction is reachable from pc 0");
+  P->n_regs = n_regs;
+  P->n_arrays = n_arrays;
+  P->n_instr = n_instr;
+  P->code = std::move(code);
+  return RC_OK;
+}
+
+}  // namespace rc
+
+extern "C" {
+
+int rc_load_program(const void* bytecode, size_t nbytes, rc_program** out) {
+  if (!out) return rc::fail(RC_EINVAL, "out pointer is NULL");
+  *out = nullptr;
+  rc_program* P = new (std::nothrow) rc_program();
+  if (!P) return rc::fail(RC_ENOMEM, "host allocation failed");
+  int st = rc::validate(static_cast<const uint8_t*>(bytecode), nbytes, P);
+  if (st != RC_OK) { delete P; return st; }
+  *out = P;
+  return RC_OK;
+}
+
+int rc_program_info(const rc_program* P, uint32_t* n_regs, uint32_t* n_arrays, uint32_t* n_instr) {
+  if (!P) return rc::fail(RC_EINVAL, "program is NULL");
+  if (n_regs) *n_regs = P->n_regs;
+  if (n_arrays) *n_arrays = P->n_arrays;
+  if (n_instr) *n_instr = P->n_instr;
+  return RC_OK;
+}
+
+const char* rc_last_error(void) { return rc::g_last_error.c_str(); }
+int rc_abi_version(void) { return RC_ABI_VERSION; }
+
+}  // extern "C"

@@ -1,0 +1,169 @@
+// rc_internal.h — shared definitions of the CUDA path (librc.so).  Not part of
+// the ABI (include/rc.h is).  Nothing here is shared with oracle/.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "rc.h"
+
+namespace rc {
+
+struct Ins {  // 8-byte RCB1 instruction, include/rc.h
+  uint8_t op, a, b, c;
+  int32_t imm;
+};
+static_assert(sizeof(Ins) == 8, "instruction is 8 bytes");
+
+// work-item status (lane.status), DESIGN.md §5
+enum LaneStatus : uint8_t {
+  L_RUNNING = 0,
+  L_WAITING = 1,  // suspended at a barrier (τ ⊡ σ)
+  L_EXITED = 2,
+  L_PRUNED = 3,   // assume(false): ⊤
+  L_OOB = 4,      // ⊥ kinds
+  L_ASSERT = 5,
+  L_DIV0 = 6,
+  L_FUEL = 7,
+};
+constexpr int32_t NODE_NONE = -2;  // lane did not arrive in this interval
+constexpr int32_t NODE_EXIT = -1;  // arrived at the exit node
+constexpr uint32_t NOTID = 0xFFFFFFFFu;
+constexpr int OVL_CAP = 16;        // own-write overlay entries per work-item (smem)
+
+static_assert(RC_OVERLAY_CAP == OVL_CAP, "overlay capacity in rc.h and the interpreter agree");
+
+// Device counters of one run; zeroed per attempt where noted.
+struct DevCounters {
+  unsigned long long log_count;     // records appended this interval (per attempt)
+  unsigned long long report_count;  // reports appended (whole run, rolled back on retry)
+  unsigned long long iv_loads;      // per attempt
+  unsigned long long iv_stores;
+  unsigned long long iv_instr;
+  unsigned int log_overflow;        // per attempt
+  unsigned int ovl_overflow;        // per attempt
+  unsigned int any_waiting;         // per interval
+  unsigned int pad;
+  unsigned long long lanes_final[8];
+};
+
+// Parameters of the interval interpreter (K1), passed by value.
+struct InterpParams {
+  const Ins* code;
+  uint32_t n_instr, n_regs, n_arrays;
+  uint32_t n;                 // work-group size
+  uint32_t n_lanes;           // I_b * n
+  uint32_t cpi;               // cells per instance
+  uint64_t fuel;
+  uint32_t interval;
+  uint32_t inst_base;         // global instance id of batch instance 0
+  const uint32_t* arr_off;    // [n_arrays] cell offset of each array inside an instance
+  const uint32_t* arr_size;   // [n_arrays]
+  const int32_t* heap;        // interval-start shared heap [I_b][cpi]
+  // lane state in / out (SoA)
+  const int32_t* regs_in;     // [n_regs][n_lanes]
+  const uint32_t* pc_in;
+  const uint8_t* status_in;
+  int32_t* regs_out;
+  uint32_t* pc_out;
+  uint8_t* status_out;
+  int32_t* node_out;          // arrival node this interval
+  // log
+  uint32_t* log_keys;         // cell
+  uint64_t* log_vals;         // value << 32 | tid << 1 | is_write
+  unsigned long long log_cap;
+  rc_report* reports;
+  unsigned long long report_cap;
+  DevCounters* ctr;
+};
+
+struct DetectParams {
+  const uint32_t* keys;
+  const uint64_t* vals;
+  uint32_t n_records;
+  int32_t* heap;
+  uint32_t cpi, n_arrays;
+  const uint32_t* arr_off;
+  uint32_t interval, inst_base;
+  rc_report* reports;
+  unsigned long long report_cap;
+  DevCounters* ctr;
+};
+
+// ---- launchers (defined in the .cu files) --------------------------------
+size_t interp_smem_bytes(uint32_t n_regs, int threads);
+int interp_threads(uint32_t n_regs);
+cudaError_t launch_interp(const InterpParams& p, cudaStream_t s);
+
+struct SortWorkspace {
+  uint32_t* keys_alt = nullptr;
+  uint64_t* vals_alt = nullptr;
+  uint32_t* hist = nullptr;        // [4][256] digit histograms
+  uint32_t* bin_off = nullptr;     // [4][256] exclusive offsets
+  unsigned long long* status = nullptr;  // [tiles][256] decoupled look-back words
+  uint32_t* tile_ctr = nullptr;    // [4] dynamic tile counters
+  size_t status_tiles = 0;
+  uint32_t epoch = 0;              // look-back epoch (never reset memory)
+};
+constexpr int SORT_THREADS = 256;
+constexpr int SORT_ITEMS = 16;
+constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;
+size_t sort_tiles(size_t n);
+
+// Live profile: CUDA events recorded on the launch stream around each kernel
+// class; read back once at the end of rc_run (no per-kernel synchronisation).
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  struct Mark { int cls; size_t e0, e1; uint64_t bytes, items; };
+  std::vector<Mark> marks;
+  size_t used = 0;
+  size_t open_ev = 0;
+  cudaEvent_t ev(size_t i) { return pool[i]; }
+  size_t next();
+  void begin(cudaStream_t s);
+  void end(int cls, cudaStream_t s, uint64_t bytes, uint64_t items);
+  void reset() { marks.clear(); used = 0; }
+  void collect(rc_profile* out);
+  ~Profiler();
+};
+
+// Sort (keys, vals) by key bits [0, bits).  *in_alt tells whether the sorted
+// data ended in the alt buffers of `ws`.
+cudaError_t onesweep_sort(uint32_t* keys, uint64_t* vals, uint32_t n, int bits, SortWorkspace& ws,
+                          cudaStream_t s, bool* in_alt, Profiler* prof);
+
+cudaError_t launch_detect(const DetectParams& p, cudaStream_t s);
+
+struct BoundaryParams {
+  uint32_t n, n_lanes, n_inst, interval, inst_base;
+  const uint8_t* status;
+  const int32_t* node;
+  uint32_t* first_tid;   // [n_inst]
+  uint32_t* second_tid;  // [n_inst]
+  uint32_t* inst_waiting;// [n_inst]
+  rc_report* reports;
+  unsigned long long report_cap;
+  DevCounters* ctr;
+};
+cudaError_t launch_boundary(const BoundaryParams& p, cudaStream_t s);
+cudaError_t launch_max_intervals(const BoundaryParams& p, cudaStream_t s);
+cudaError_t launch_lane_hist(const uint8_t* status, uint32_t n_lanes, DevCounters* ctr, cudaStream_t s);
+cudaError_t launch_init_lanes(uint8_t* status, uint32_t* pc, int32_t* regs, uint32_t n_regs,
+                              uint32_t n_lanes, cudaStream_t s);
+cudaError_t finalize_reports(rc_report* reports, uint64_t n, rc_report* scratch, cudaStream_t s);
+
+}  // namespace rc
+
+// opaque program object (include/rc.h)
+struct rc_workspace;
+struct rc_program {
+  uint32_t n_regs = 0, n_arrays = 0, n_instr = 0;
+  std::vector<rc::Ins> code;
+  std::mutex mu;
+  rc_workspace* ws = nullptr;
+};

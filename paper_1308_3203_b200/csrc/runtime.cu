@@ -1,0 +1,554 @@
+// runtime.cu — rc_run: device workspace, instance batching and the barrier
+// interval loop.
+//
+// Per instance batch:
+//   A2  heap init: the caller's arrays are copied into one working heap laid
+//       out [instance][cells], array a at offset off[a] (cell id
+//       = inst_local * cpi + off[a] + index, a u32 key for the sort).
+//   per interval k:
+//     K1  interpret every live work-item until it suspends / exits / stops;
+//         log reads and final writes (interp.cu)
+//     K2/K3 onesweep sort of the log by cell (sort.cu)
+//     K4+K5 segmented detection + commit (detect.cu)
+//     A4  barrier bookkeeping / divergence (boundary.cu)
+//   until no work-item is suspended at a barrier.
+// After all batches: K6 canonical report order, copy to the host buffer.
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "rc_internal.h"
+
+namespace rc {
+int fail(int code, const char* fmt, ...);
+
+size_t Profiler::next() {
+  if (used == pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    pool.push_back(e);
+  }
+  return used++;
+}
+void Profiler::begin(cudaStream_t s) {
+  if (!on) return;
+  open_ev = next();
+  cudaEventRecord(pool[open_ev], s);
+}
+void Profiler::end(int cls, cudaStream_t s, uint64_t bytes, uint64_t items) {
+  if (!on) return;
+  size_t e1 = next();
+  cudaEventRecord(pool[e1], s);
+  marks.push_back({cls, open_ev, e1, bytes, items});
+}
+void Profiler::collect(rc_profile* out) {
+  for (const Mark& m : marks) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, pool[m.e0], pool[m.e1]);
+    out->launches[m.cls] += 1;
+    out->ms[m.cls] += ms;
+    out->alg_bytes[m.cls] += m.bytes;
+    out->items[m.cls] += m.items;
+  }
+}
+Profiler::~Profiler() {
+  for (cudaEvent_t e : pool) cudaEventDestroy(e);
+}
+
+}  // namespace rc
+
+using namespace rc;
+
+// grow-only device buffer
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t need, bool keep = false, cudaStream_t s = 0) {
+    if (need <= bytes) return cudaSuccess;
+    size_t nb = std::max(need, bytes + bytes / 2);
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, nb);
+    if (e != cudaSuccess) {
+      nb = need;  // retry without slack
+      cudaGetLastError();
+      e = cudaMalloc(&q, nb);
+      if (e != cudaSuccess) return e;
+    }
+    if (keep && p && bytes) {
+      cudaMemcpyAsync(q, p, bytes, cudaMemcpyDeviceToDevice, s);
+      cudaStreamSynchronize(s);
+    }
+    if (p) cudaFree(p);
+    p = q;
+    bytes = nb;
+    return cudaSuccess;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct rc_workspace {
+  int device = -1;
+  DevBuf code, arr_off, arr_size, heap;
+  DevBuf regs[2], pc[2], status[2], node;
+  DevBuf log_keys, log_vals, keys_alt, vals_alt, sort_status, sort_small;
+  DevBuf reports, reports_scratch;
+  DevBuf inst_tmp;  // first_tid | second_tid | inst_waiting
+  DevBuf ctr;
+  DevCounters* h_ctr = nullptr;  // pinned
+  SortWorkspace sort;
+  Profiler prof;
+  ~rc_workspace() {
+    for (DevBuf* b : {&code, &arr_off, &arr_size, &heap, &regs[0], &regs[1], &pc[0], &pc[1], &status[0],
+                      &status[1], &node, &log_keys, &log_vals, &keys_alt, &vals_alt, &sort_status,
+                      &sort_small, &reports, &reports_scratch, &inst_tmp, &ctr})
+      b->release();
+    if (h_ctr) cudaFreeHost(h_ctr);
+  }
+};
+
+namespace {
+
+#define CK(call)                                                                                     \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess)                                                                           \
+      return fail(e_ == cudaErrorMemoryAllocation ? RC_ENOMEM : RC_ECUDA, "%s failed: %s (%s:%d)",   \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                                \
+  } while (0)
+
+int bits_for(uint64_t x) {  // bits needed for values in [0, x)
+  if (x <= 1) return 0;
+  int b = 0;
+  uint64_t v = x - 1;
+  while (v) { b++; v >>= 1; }
+  return b;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Instance batch size: a batch's cells must fit the u32 key;
+// prefer the fewest 8-bit sort passes that still give >= ~4M lanes per batch,
+// then the largest batch with that pass count, within a memory budget.
+uint32_t plan_batch(uint32_t n_inst, uint32_t n, uint64_t cpi, uint32_t n_regs, uint32_t max_batch,
+                    size_t free_bytes) {
+  if (n_inst == 0) return 0;
+  const uint64_t cells_cap = cpi ? (uint64_t)0xFFFFFFFFull / cpi : (uint64_t)n_inst;
+  const uint64_t lane_cap = n ? ((uint64_t)1 << 31) / n : (uint64_t)n_inst;
+  // bytes per lane: 2x lane state + node + ~6 log records (keys+vals, double buffered)
+  const uint64_t per_lane = 2 * (4ull * n_regs + 5) + 4 + 6 * 24;
+  const uint64_t per_inst = (uint64_t)n * per_lane + cpi * 4 + 16;
+  const uint64_t mem_cap = std::max<uint64_t>(1, (uint64_t)(free_bytes * 0.5) / std::max<uint64_t>(per_inst, 1));
+  uint64_t hi = std::min<uint64_t>({(uint64_t)n_inst, cells_cap, lane_cap, mem_cap});
+  if (max_batch) hi = std::min<uint64_t>(hi, max_batch);
+  hi = std::max<uint64_t>(hi, 1);
+  const uint64_t target_lanes = 1ull << 22;
+  uint64_t need = n ? (target_lanes + n - 1) / n : hi;
+  need = std::min(std::max<uint64_t>(need, 1), hi);
+  const int passes = (bits_for(need * std::max<uint64_t>(cpi, 1)) + 7) / 8;
+  uint64_t best = need;
+  // largest batch <= hi with the same pass count
+  uint64_t lim = passes >= 4 ? hi : std::min<uint64_t>(hi, ((1ull << (8 * passes)) / std::max<uint64_t>(cpi, 1)));
+  best = std::max(best, lim);
+  best = std::min(best, hi);
+  return (uint32_t)std::max<uint64_t>(best, 1);
+}
+
+}  // namespace
+
+extern "C" {
+
+void rc_free_program(rc_program* P) {
+  if (!P) return;
+  if (P->ws) {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (P->ws->device >= 0) cudaSetDevice(P->ws->device);
+    delete P->ws;
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  delete P;
+}
+
+int rc_release_workspace(rc_program* P) {
+  if (!P) return fail(RC_EINVAL, "program is NULL");
+  std::lock_guard<std::mutex> lk(P->mu);
+  if (P->ws) {
+    DeviceGuard g(P->ws->device);
+    delete P->ws;
+    P->ws = nullptr;
+  }
+  return RC_OK;
+}
+
+int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t n_arrays, uint32_t n_inst,
+           const rc_options* options, rc_report* out, uint64_t capacity, uint64_t* n_reports_total,
+           rc_stats* stats, int32_t* const* final_heaps) {
+  if (n_reports_total) *n_reports_total = 0;
+  if (stats) memset(stats, 0, sizeof *stats);
+  if (!prog) return fail(RC_EINVAL, "program is NULL");
+  rc_program* P = const_cast<rc_program*>(prog);
+  if (n_arrays != P->n_arrays) return fail(RC_EINVAL, "n_arrays %u != program's %u", n_arrays, P->n_arrays);
+  if (n_arrays && !arrays) return fail(RC_EINVAL, "arrays is NULL");
+  if (n >= (1u << 31)) return fail(RC_EINVAL, "work_group_size %u >= 2^31", n);
+  if (capacity && !out) return fail(RC_EINVAL, "out is NULL with capacity %llu", (unsigned long long)capacity);
+  rc_options opt;
+  memset(&opt, 0, sizeof opt);
+  if (options) opt = *options;
+  if (!opt.max_intervals) opt.max_intervals = 65536;
+  if (!opt.fuel_per_interval) opt.fuel_per_interval = 1ull << 20;
+  const bool host_io = (opt.flags & RC_OPT_HOST_IO) != 0;
+  uint64_t cpi = 0;
+  std::vector<uint32_t> off(n_arrays + 1, 0), size(n_arrays + 1, 0);
+  for (uint32_t a = 0; a < n_arrays; a++) {
+    if (arrays[a].size >= (1u << 31)) return fail(RC_EINVAL, "array %u: size %u >= 2^31", a, arrays[a].size);
+    if (arrays[a].size && n_inst && !arrays[a].data) return fail(RC_EINVAL, "array %u: data is NULL", a);
+    off[a] = (uint32_t)cpi;
+    size[a] = arrays[a].size;
+    cpi += arrays[a].size;
+    if (cpi > 0xFFFFFFFFull) return fail(RC_ELIMIT, "cells per instance exceed 2^32");
+  }
+  if (final_heaps)
+    for (uint32_t a = 0; a < n_arrays; a++)
+      if (arrays[a].size && n_inst && !final_heaps[a]) return fail(RC_EINVAL, "final_heaps[%u] is NULL", a);
+
+  std::lock_guard<std::mutex> lk(P->mu);
+  DeviceGuard dg(opt.device);
+  cudaStream_t s = static_cast<cudaStream_t>(opt.cuda_stream);
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (opt.device < 0 || opt.device >= ndev) return fail(RC_EINVAL, "device %d not present", opt.device);
+  if (P->ws && P->ws->device != opt.device) {
+    delete P->ws;
+    P->ws = nullptr;
+  }
+  if (!P->ws) {
+    P->ws = new (std::nothrow) rc_workspace();
+    if (!P->ws) return fail(RC_ENOMEM, "host allocation failed");
+    P->ws->device = opt.device;
+    rc_workspace& W = *P->ws;
+    CK(W.code.ensure(P->code.size() * sizeof(Ins)));
+    CK(cudaMemcpy(W.code.p, P->code.data(), P->code.size() * sizeof(Ins), cudaMemcpyHostToDevice));
+    CK(W.ctr.ensure(sizeof(DevCounters)));
+    CK(cudaMallocHost(&W.h_ctr, sizeof(DevCounters)));
+    CK(W.sort_small.ensure(4096 * 4));
+    W.sort.hist = W.sort_small.as<uint32_t>();
+    W.sort.bin_off = W.sort.hist + 1024;
+    W.sort.tile_ctr = W.sort.bin_off + 1024;
+  }
+  rc_workspace& W = *P->ws;
+  W.prof.reset();
+  W.prof.on = opt.profile != nullptr;
+  if (opt.profile) memset(opt.profile, 0, sizeof(rc_profile));
+  cudaEvent_t t_begin = nullptr, t_end = nullptr;
+  if (W.prof.on) {
+    cudaEventCreate(&t_begin);
+    cudaEventCreate(&t_end);
+    cudaEventRecord(t_begin, s);
+  }
+
+  CK(W.arr_off.ensure((n_arrays + 1) * 4));
+  CK(W.arr_size.ensure((n_arrays + 1) * 4));
+  CK(cudaMemcpyAsync(W.arr_off.p, off.data(), (n_arrays + 1) * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(W.arr_size.p, size.data(), (n_arrays + 1) * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(W.ctr.p, 0, sizeof(DevCounters), s));
+
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  const uint32_t I_b = plan_batch(n_inst, n, cpi, P->n_regs, opt.max_batch_instances, free_b);
+  const uint64_t L_max = (uint64_t)I_b * n;
+  const int key_bits = bits_for((uint64_t)I_b * std::max<uint64_t>(cpi, 1));
+
+  // batch-sized buffers
+  if (I_b) {
+    CK(W.heap.ensure(std::max<uint64_t>(1, (uint64_t)I_b * cpi) * 4));
+    for (int b = 0; b < 2; b++) {
+      CK(W.regs[b].ensure(std::max<uint64_t>(1, L_max * P->n_regs) * 4));
+      CK(W.pc[b].ensure(std::max<uint64_t>(1, L_max) * 4));
+      CK(W.status[b].ensure(std::max<uint64_t>(1, L_max)));
+    }
+    CK(W.node.ensure(std::max<uint64_t>(1, L_max) * 4));
+    CK(W.inst_tmp.ensure((uint64_t)I_b * 12));
+  }
+  uint64_t log_cap = W.log_keys.bytes / 4;
+  {
+    const uint64_t want = std::max<uint64_t>(1u << 16, std::min<uint64_t>(L_max * 4, 0xFFFFFFFFull));
+    if (log_cap < want) {
+      CK(W.log_keys.ensure(want * 4));
+      CK(W.log_vals.ensure(want * 8));
+      CK(W.keys_alt.ensure(want * 4));
+      CK(W.vals_alt.ensure(want * 8));
+      log_cap = std::min(W.log_keys.bytes / 4, W.log_vals.bytes / 8);
+    }
+  }
+  auto ensure_sort_status = [&](uint64_t cap) -> cudaError_t {
+    const size_t tiles = sort_tiles(cap);
+    if (W.sort_status.bytes < tiles * 256 * 8) {
+      cudaError_t e = W.sort_status.ensure(tiles * 256 * 8);
+      if (e != cudaSuccess) return e;
+      e = cudaMemsetAsync(W.sort_status.p, 0, W.sort_status.bytes, s);
+      W.sort.epoch = 0;
+      if (e != cudaSuccess) return e;
+    }
+    W.sort.status = W.sort_status.as<unsigned long long>();
+    W.sort.status_tiles = W.sort_status.bytes / (256 * 8);
+    return cudaSuccess;
+  };
+  CK(ensure_sort_status(log_cap));
+  uint64_t rep_cap = W.reports.bytes / sizeof(rc_report);
+  if (rep_cap < (1u << 16)) {
+    CK(W.reports.ensure((1u << 16) * sizeof(rc_report)));
+    rep_cap = W.reports.bytes / sizeof(rc_report);
+  }
+
+  uint64_t tot_loads = 0, tot_stores = 0, tot_instr = 0, intervals_max = 0;
+  uint64_t rep_count = 0;  // host mirror of ctr.report_count
+  DevCounters* dctr = W.ctr.as<DevCounters>();
+
+  auto read_ctr = [&]() -> cudaError_t {
+    cudaError_t e = cudaMemcpyAsync(W.h_ctr, dctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return e;
+    return cudaStreamSynchronize(s);
+  };
+  auto set_report_count = [&](uint64_t v) -> cudaError_t {
+    W.h_ctr->report_count = v;
+    return cudaMemcpyAsync(&dctr->report_count, &W.h_ctr->report_count, 8, cudaMemcpyHostToDevice, s);
+  };
+  auto grow_reports = [&](uint64_t need) -> cudaError_t {
+    cudaError_t e = W.reports.ensure(need * sizeof(rc_report) * 5 / 4, true, s);
+    rep_cap = W.reports.bytes / sizeof(rc_report);
+    return e;
+  };
+
+  for (uint32_t b0 = 0; b0 < n_inst; b0 += I_b) {
+    const uint32_t nb = std::min(I_b, n_inst - b0);
+    const uint32_t L = nb * n;
+    const uint32_t inst_base = opt.instance_offset + b0;
+    // A2: heap init
+    W.prof.begin(s);
+    for (uint32_t a = 0; a < n_arrays; a++) {
+      if (!size[a]) continue;
+      CK(cudaMemcpy2DAsync(W.heap.as<int32_t>() + off[a], cpi * 4, arrays[a].data + (uint64_t)b0 * size[a],
+                           (size_t)size[a] * 4, (size_t)size[a] * 4, nb,
+                           host_io ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+    }
+    W.prof.end(RC_PROF_COPY, s, (uint64_t)nb * cpi * 8, (uint64_t)nb * cpi);
+    int cur = 0;
+    if (L) {
+      CK(cudaMemsetAsync(W.status[cur].p, 0, L, s));
+      CK(cudaMemsetAsync(W.pc[cur].p, 0, (size_t)L * 4, s));
+      CK(cudaMemsetAsync(W.regs[cur].p, 0, (size_t)L * P->n_regs * 4, s));  // registers start at 0 (L18)
+    }
+    uint32_t k = 0;
+    for (;;) {
+      // ---------------- K1
+      uint64_t rep_before = rep_count;
+      InterpParams ip;
+      for (;;) {
+        CK(cudaMemsetAsync(dctr, 0, offsetof(DevCounters, report_count), s));
+        CK(cudaMemsetAsync(&dctr->iv_loads, 0, offsetof(DevCounters, lanes_final) - offsetof(DevCounters, iv_loads), s));
+        ip.code = W.code.as<Ins>();
+        ip.n_instr = P->n_instr;
+        ip.n_regs = P->n_regs;
+        ip.n_arrays = n_arrays;
+        ip.n = n;
+        ip.n_lanes = L;
+        ip.cpi = (uint32_t)cpi;
+        ip.fuel = opt.fuel_per_interval;
+        ip.interval = k;
+        ip.inst_base = inst_base;
+        ip.arr_off = W.arr_off.as<uint32_t>();
+        ip.arr_size = W.arr_size.as<uint32_t>();
+        ip.heap = W.heap.as<int32_t>();
+        ip.regs_in = W.regs[cur].as<int32_t>();
+        ip.pc_in = W.pc[cur].as<uint32_t>();
+        ip.status_in = W.status[cur].as<uint8_t>();
+        ip.regs_out = W.regs[cur ^ 1].as<int32_t>();
+        ip.pc_out = W.pc[cur ^ 1].as<uint32_t>();
+        ip.status_out = W.status[cur ^ 1].as<uint8_t>();
+        ip.node_out = W.node.as<int32_t>();
+        ip.log_keys = W.log_keys.as<uint32_t>();
+        ip.log_vals = W.log_vals.as<uint64_t>();
+        ip.log_cap = log_cap;
+        ip.reports = W.reports.as<rc_report>();
+        ip.report_cap = rep_cap;
+        ip.ctr = dctr;
+        W.prof.begin(s);
+        CK(launch_interp(ip, s));
+        W.prof.end(RC_PROF_INTERP, s, 0, L);
+        CK(read_ctr());
+        if (W.h_ctr->ovl_overflow)
+          return fail(RC_ELIMIT,
+                      "a work-item wrote more than %d distinct cells in one barrier interval (instance batch at "
+                      "%u, interval %u)",
+                      OVL_CAP, inst_base, k);
+        const bool log_over = W.h_ctr->log_overflow || W.h_ctr->log_count > log_cap;
+        const bool rep_over = W.h_ctr->report_count > rep_cap;
+        if (!log_over && !rep_over) break;
+        if (log_over) {  // grow the log and re-run the interval from the saved lane state
+          const uint64_t want = std::min<uint64_t>(W.h_ctr->log_count + W.h_ctr->log_count / 4 + 1024, 0xFFFFFFFFull);
+          if (W.h_ctr->log_count > 0xFFFFFFFFull) return fail(RC_ELIMIT, "more than 2^32 access records in one interval");
+          CK(W.log_keys.ensure(want * 4));
+          CK(W.log_vals.ensure(want * 8));
+          CK(W.keys_alt.ensure(want * 4));
+          CK(W.vals_alt.ensure(want * 8));
+          log_cap = std::min(W.log_keys.bytes / 4, W.log_vals.bytes / 8);
+          CK(ensure_sort_status(log_cap));
+        }
+        if (rep_over) CK(grow_reports(W.h_ctr->report_count));
+        CK(set_report_count(rep_before));
+      }
+      const uint64_t N = W.h_ctr->log_count;
+      rep_count = W.h_ctr->report_count;
+      tot_loads += W.h_ctr->iv_loads;
+      tot_stores += W.h_ctr->iv_stores;
+      tot_instr += W.h_ctr->iv_instr;
+
+      // ---------------- K2/K3: sort the log by cell
+      bool in_alt = false;
+      W.sort.keys_alt = W.keys_alt.as<uint32_t>();
+      W.sort.vals_alt = W.vals_alt.as<uint64_t>();
+      CK(onesweep_sort(W.log_keys.as<uint32_t>(), W.log_vals.as<uint64_t>(), (uint32_t)N, key_bits, W.sort, s,
+                       &in_alt, W.prof.on ? &W.prof : nullptr));
+      const uint32_t* sk = in_alt ? W.keys_alt.as<uint32_t>() : W.log_keys.as<uint32_t>();
+      const uint64_t* sv = in_alt ? W.vals_alt.as<uint64_t>() : W.log_vals.as<uint64_t>();
+
+      // ---------------- K4+K5 and A4 (idempotent: re-run if the report buffer overflows)
+      const uint64_t rep_after_k1 = rep_count;
+      for (;;) {
+        DetectParams dp;
+        dp.keys = sk;
+        dp.vals = sv;
+        dp.n_records = (uint32_t)N;
+        dp.heap = W.heap.as<int32_t>();
+        dp.cpi = (uint32_t)std::max<uint64_t>(cpi, 1);
+        dp.n_arrays = n_arrays;
+        dp.arr_off = W.arr_off.as<uint32_t>();
+        dp.interval = k;
+        dp.inst_base = inst_base;
+        dp.reports = W.reports.as<rc_report>();
+        dp.report_cap = rep_cap;
+        dp.ctr = dctr;
+        W.prof.begin(s);
+        CK(launch_detect(dp, s));
+        W.prof.end(RC_PROF_DETECT, s, N * 12, N);
+        BoundaryParams bp;
+        bp.n = n;
+        bp.n_lanes = L;
+        bp.n_inst = nb;
+        bp.interval = k;
+        bp.inst_base = inst_base;
+        bp.status = W.status[cur ^ 1].as<uint8_t>();
+        bp.node = W.node.as<int32_t>();
+        bp.first_tid = W.inst_tmp.as<uint32_t>();
+        bp.second_tid = bp.first_tid + I_b;
+        bp.inst_waiting = bp.second_tid + I_b;
+        bp.reports = W.reports.as<rc_report>();
+        bp.report_cap = rep_cap;
+        bp.ctr = dctr;
+        CK(cudaMemsetAsync(&dctr->any_waiting, 0, 4, s));
+        W.prof.begin(s);
+        CK(launch_boundary(bp, s));
+        W.prof.end(RC_PROF_BOUNDARY, s, (uint64_t)L * 10, L);
+        CK(read_ctr());
+        if (W.h_ctr->report_count <= rep_cap) {
+          rep_count = W.h_ctr->report_count;
+          break;
+        }
+        CK(grow_reports(W.h_ctr->report_count));
+        CK(set_report_count(rep_after_k1));
+      }
+      cur ^= 1;  // the interval's lane state becomes current
+      const bool any_waiting = W.h_ctr->any_waiting != 0;
+      if (!any_waiting) break;
+      k++;
+      if (k >= opt.max_intervals) {  // instance-level FUEL (reading L17)
+        for (;;) {
+          BoundaryParams bp;
+          memset(&bp, 0, sizeof bp);
+          bp.n_inst = nb;
+          bp.interval = k;
+          bp.inst_base = inst_base;
+          bp.inst_waiting = W.inst_tmp.as<uint32_t>() + 2 * (size_t)I_b;
+          bp.reports = W.reports.as<rc_report>();
+          bp.report_cap = rep_cap;
+          bp.ctr = dctr;
+          CK(launch_max_intervals(bp, s));
+          CK(read_ctr());
+          if (W.h_ctr->report_count <= rep_cap) break;
+          CK(grow_reports(W.h_ctr->report_count));
+          CK(set_report_count(rep_count));
+        }
+        rep_count = W.h_ctr->report_count;
+        k--;  // intervals executed = max_intervals
+        break;
+      }
+    }
+    intervals_max = std::max<uint64_t>(intervals_max, (uint64_t)k + 1);
+    CK(launch_lane_hist(W.status[cur].as<uint8_t>(), L, dctr, s));
+    // final heaps out
+    if (final_heaps) {
+      W.prof.begin(s);
+      for (uint32_t a = 0; a < n_arrays; a++) {
+        if (!size[a]) continue;
+        CK(cudaMemcpy2DAsync(final_heaps[a] + (uint64_t)b0 * size[a], (size_t)size[a] * 4,
+                             W.heap.as<int32_t>() + off[a], cpi * 4, (size_t)size[a] * 4, nb,
+                             host_io ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+      }
+      W.prof.end(RC_PROF_COPY, s, (uint64_t)nb * cpi * 8, (uint64_t)nb * cpi);
+    }
+  }
+
+  // K6: canonical order, then the first min(capacity, total) to the host
+  if (rep_count > 1) {
+    CK(W.reports_scratch.ensure(std::max<uint64_t>(rep_count, 2048) * 2 * sizeof(rc_report)));
+    W.prof.begin(s);
+    CK(finalize_reports(W.reports.as<rc_report>(), rep_count, W.reports_scratch.as<rc_report>(), s));
+    W.prof.end(RC_PROF_FINALIZE, s, rep_count * 64, rep_count);
+  }
+  const uint64_t ncopy = std::min<uint64_t>(capacity, rep_count);
+  if (ncopy) CK(cudaMemcpyAsync(out, W.reports.p, ncopy * sizeof(rc_report), cudaMemcpyDeviceToHost, s));
+  CK(read_ctr());  // also waits for the report copy and lanes_final
+  if (W.prof.on) {
+    cudaEventRecord(t_end, s);
+    cudaEventSynchronize(t_end);
+    W.prof.collect(opt.profile);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t_begin, t_end);
+    opt.profile->total_ms = ms;
+    cudaEventDestroy(t_begin);
+    cudaEventDestroy(t_end);
+  }
+  if (stats) {
+    stats->loads = tot_loads;
+    stats->stores = tot_stores;
+    stats->checked_accesses = tot_loads + tot_stores;
+    stats->instructions = tot_instr;
+    stats->intervals_max = intervals_max;
+    for (int i = 0; i < 8; i++) stats->lanes_final[i] = W.h_ctr->lanes_final[i];
+  }
+  if (n_reports_total) *n_reports_total = rep_count;
+  if (rep_count > capacity)
+    return fail(RC_ETRUNC, "%llu reports, capacity %llu", (unsigned long long)rep_count,
+                (unsigned long long)capacity);
+  return RC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,311 @@
+// sort.cu — K2/K3: onesweep LSD radix sort of the access log by cell.
+//
+// Groups the interval's access records by cell so that
+// the race rule can be applied per cell.  Keys are the
+// batch-local linear cell id (u32); values are 8-byte payloads
+// (value << 32 | tid << 1 | is_write).  Only the cell bits are sorted; the
+// sort is stable, and the detector (detect.cu) only uses order-independent
+// reductions inside a cell, so within-cell order is irrelevant.
+//
+// Onesweep (Adinets & Merrill): one upfront pass computes the digit
+// histograms of every pass (K2), then each pass (K3) is a single kernel:
+//   * a block claims tile t from an atomic counter (in-order claiming gives
+//     forward progress to the look-back),
+//   * the tile (4096 records = 16 KB keys + 32 KB values) is staged into
+//     shared memory with two TMA bulk copies (cp.async.bulk + mbarrier),
+//   * stable in-tile ranking with __match_any_sync per warp,
+//   * per digit: publish the tile's count (AGGREGATE), look back over
+//     predecessors until an INCLUSIVE prefix is found, publish INCLUSIVE,
+//   * scatter to shared memory in digit order and write out coalesced runs.
+// Status words carry an epoch so the look-back array is never re-zeroed.
+#include "rc_internal.h"
+
+namespace rc {
+
+namespace {
+constexpr unsigned FULL = 0xFFFFFFFFu;
+constexpr int RADIX = 256;
+constexpr int WARPS = SORT_THREADS / 32;
+constexpr int WARP_ITEMS = SORT_ITEMS * 32;
+constexpr unsigned long long FLAG_AGG = 1ull << 62, FLAG_INC = 2ull << 62;
+constexpr unsigned long long VAL_MASK = (1ull << 40) - 1;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// exclusive scan of one value per thread over a 256-thread block
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* warp_tot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
+  __syncthreads();
+  uint32_t off = 0;
+  for (int i = 0; i < w; i++) off += warp_tot[i];
+  __syncthreads();
+  return off + x - v;
+}
+}  // namespace
+
+// ---- K2: all digit histograms in one read of the keys ----------------------
+__global__ void __launch_bounds__(256) hist_kernel(const uint32_t* __restrict__ keys, uint32_t n, int passes,
+                                                   uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[4][RADIX];
+  for (int i = threadIdx.x; i < 4 * RADIX; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  // each thread takes 16 consecutive keys and counts runs of equal digits
+  // (access logs are nearly sorted by cell, so runs are long)
+  const uint32_t chunk = 16;
+  for (uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * chunk; b < n;
+       b += (uint64_t)gridDim.x * blockDim.x * chunk) {
+    uint32_t k[16];
+    const uint32_t m = (uint32_t)umin64(chunk, n - b);
+    if (m == chunk && ((b & 3) == 0)) {
+      const uint4* q = reinterpret_cast<const uint4*>(keys + b);
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        uint4 v = __ldg(q + j);
+        k[4 * j] = v.x; k[4 * j + 1] = v.y; k[4 * j + 2] = v.z; k[4 * j + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; j++) k[j] = j < (int)m ? __ldg(keys + b + j) : 0;
+    }
+    for (int p = 0; p < passes; p++) {
+      const int sh = 8 * p;
+      uint32_t cur = (k[0] >> sh) & 0xFF, run = 1;
+#pragma unroll
+      for (int j = 1; j < 16; j++) {
+        if (j < (int)m) {
+          const uint32_t d = (k[j] >> sh) & 0xFF;
+          if (d == cur) run++;
+          else { atomicAdd(&h[p][cur], run); cur = d; run = 1; }
+        }
+      }
+      atomicAdd(&h[p][cur], run);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * RADIX; i += blockDim.x) {
+    const uint32_t v = (&h[0][0])[i];
+    if (v) atomicAdd(&hist[i], v);
+  }
+}
+
+// exclusive offsets of every digit, one block per pass
+__global__ void __launch_bounds__(256) bin_offsets_kernel(const uint32_t* __restrict__ hist,
+                                                          uint32_t* __restrict__ off) {
+  __shared__ uint32_t wt[WARPS];
+  const uint32_t v = hist[blockIdx.x * RADIX + threadIdx.x];
+  off[blockIdx.x * RADIX + threadIdx.x] = block_excl_scan(v, wt);
+}
+
+// ---- K3: one onesweep digit pass -------------------------------------------
+struct SortSmem {
+  uint64_t vals[SORT_TILE];
+  uint32_t keys[SORT_TILE];
+  uint32_t whist[WARPS][RADIX];
+  uint32_t tile_excl[RADIX];
+  uint32_t glob_base[RADIX];
+  uint32_t wt[WARPS];
+  uint32_t tile;
+  unsigned long long mbar;
+};
+
+__global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
+    const uint32_t* __restrict__ keys_in, const uint64_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
+    uint64_t* __restrict__ vals_out, uint32_t n, int shift, const uint32_t* __restrict__ bin_off,
+    unsigned long long* __restrict__ status, uint32_t* __restrict__ tile_ctr, uint32_t epoch) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+
+  for (int i = t; i < WARPS * RADIX; i += SORT_THREADS) (&S.whist[0][0])[i] = 0;
+  if (t == 0) {
+    S.tile = atomicAdd(tile_ctr, 1u);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t tile = S.tile;
+  const uint64_t base = (uint64_t)tile * SORT_TILE;
+  const uint32_t cnt = (uint32_t)umin64(SORT_TILE, n - base);
+
+  // ---- stage the tile into shared memory
+  if (cnt == SORT_TILE) {
+    if (t == 0) {
+      const uint32_t bar = smem_u32(&S.mbar);
+      const uint32_t bytes_k = SORT_TILE * 4, bytes_v = SORT_TILE * 8;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes_k + bytes_v)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(S.keys)),
+          "l"(keys_in + base), "r"(bytes_k), "r"(bar)
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(S.vals)),
+          "l"(vals_in + base), "r"(bytes_v), "r"(bar)
+          : "memory");
+    }
+    const uint32_t bar = smem_u32(&S.mbar);
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done)
+          : "r"(bar)
+          : "memory");
+    }
+  } else {
+    for (uint32_t i = t; i < cnt; i += SORT_THREADS) {
+      S.keys[i] = keys_in[base + i];
+      S.vals[i] = vals_in[base + i];
+    }
+    __syncthreads();
+  }
+
+  // ---- stable in-tile ranking (warp w owns items [w*512, w*512+512), striped)
+  uint32_t k[SORT_ITEMS];
+  uint64_t v[SORT_ITEMS];
+  uint32_t rk[SORT_ITEMS];  // digit << 16 | rank within the warp
+#pragma unroll
+  for (int j = 0; j < SORT_ITEMS; j++) {
+    const uint32_t idx = w * WARP_ITEMS + j * 32 + lane;
+    const bool valid = idx < cnt;
+    k[j] = valid ? S.keys[idx] : 0u;
+    v[j] = valid ? S.vals[idx] : 0ull;
+    const uint32_t d = valid ? (k[j] >> shift) & 0xFF : 0x100u;
+    const unsigned peers = __match_any_sync(FULL, d);
+    uint32_t prev = 0;
+    if (valid) prev = S.whist[w][d];
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) S.whist[w][d] = prev + __popc(peers);
+    __syncwarp();
+    rk[j] = (d << 16) | (prev + __popc(peers & lanemask_lt()));
+  }
+  __syncthreads();
+
+  // ---- per digit: warp-exclusive prefix, tile count, look-back
+  const int d = t;  // SORT_THREADS == RADIX
+  uint32_t tile_cnt = 0;
+#pragma unroll
+  for (int ww = 0; ww < WARPS; ww++) {
+    const uint32_t c = S.whist[ww][d];
+    S.whist[ww][d] = tile_cnt;
+    tile_cnt += c;
+  }
+  unsigned long long* my_status = status + (size_t)tile * RADIX + d;
+  const unsigned long long ep = (unsigned long long)(epoch & 0x3FFFFF) << 40;
+  if (tile == 0) st_relaxed(my_status, FLAG_INC | ep | tile_cnt);
+  else st_relaxed(my_status, FLAG_AGG | ep | tile_cnt);
+  const uint32_t excl_tile = block_excl_scan(tile_cnt, S.wt);
+  S.tile_excl[d] = excl_tile;
+  unsigned long long excl = 0;
+  if (tile > 0) {
+    int64_t tp = (int64_t)tile - 1;
+    for (;;) {
+      const unsigned long long s = ld_relaxed(status + (size_t)tp * RADIX + d);
+      if (((s >> 40) & 0x3FFFFF) != (epoch & 0x3FFFFF) || (s >> 62) == 0) continue;  // not ready yet
+      excl += s & VAL_MASK;
+      if ((s >> 62) == 2) break;
+      tp--;
+    }
+    st_relaxed(my_status, FLAG_INC | ep | (excl + tile_cnt));
+  }
+  S.glob_base[d] = (uint32_t)(bin_off[d] + excl) - excl_tile;
+  __syncthreads();
+
+  // ---- scatter into shared memory in digit order (stable)
+#pragma unroll
+  for (int j = 0; j < SORT_ITEMS; j++) {
+    const uint32_t dd = rk[j] >> 16;
+    if (dd < RADIX) {
+      const uint32_t pos = S.tile_excl[dd] + S.whist[w][dd] + (rk[j] & 0xFFFF);
+      S.keys[pos] = k[j];
+      S.vals[pos] = v[j];
+    }
+  }
+  __syncthreads();
+
+  // ---- coalesced write-out: sorted position i goes to glob_base[digit] + i
+  for (uint32_t i = t; i < cnt; i += SORT_THREADS) {
+    const uint32_t kk = S.keys[i];
+    const uint32_t o = S.glob_base[(kk >> shift) & 0xFF] + i;
+    keys_out[o] = kk;
+    vals_out[o] = S.vals[i];
+  }
+}
+
+size_t sort_tiles(size_t n) { return (n + SORT_TILE - 1) / SORT_TILE; }
+
+cudaError_t onesweep_sort(uint32_t* keys, uint64_t* vals, uint32_t n, int bits, SortWorkspace& ws,
+                          cudaStream_t s, bool* in_alt, Profiler* prof) {
+  *in_alt = false;
+  if (n == 0 || bits <= 0) return cudaSuccess;
+  const int passes = (bits + 7) / 8;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(SortSmem));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  cudaMemsetAsync(ws.hist, 0, 4 * RADIX * sizeof(uint32_t), s);
+  cudaMemsetAsync(ws.tile_ctr, 0, 4 * sizeof(uint32_t), s);
+  const uint32_t hist_grid = (uint32_t)umin64((uint64_t)nsm * 8, (n + 256 * 16 - 1) / (256 * 16));
+  if (prof) prof->begin(s);
+  hist_kernel<<<hist_grid, 256, 0, s>>>(keys, n, passes, ws.hist);
+  bin_offsets_kernel<<<passes, 256, 0, s>>>(ws.hist, ws.bin_off);
+  if (prof) prof->end(RC_PROF_HIST, s, (uint64_t)n * 4, n);
+  const uint32_t tiles = (uint32_t)sort_tiles(n);
+  uint32_t* kin = keys;
+  uint64_t* vin = vals;
+  uint32_t* kout = ws.keys_alt;
+  uint64_t* vout = ws.vals_alt;
+  for (int p = 0; p < passes; p++) {
+    if (++ws.epoch >= (1u << 22)) {  // epoch wrap: clear the look-back words once
+      cudaMemsetAsync(ws.status, 0, ws.status_tiles * RADIX * sizeof(unsigned long long), s);
+      ws.epoch = 1;
+    }
+    if (prof) prof->begin(s);
+    onesweep_kernel<<<tiles, SORT_THREADS, sizeof(SortSmem), s>>>(kin, vin, kout, vout, n, 8 * p,
+                                                                 ws.bin_off + p * RADIX, ws.status,
+                                                                 ws.tile_ctr + p, ws.epoch);
+    if (prof) prof->end(RC_PROF_SORT, s, (uint64_t)n * 24, n);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    std::swap(kin, kout);
+    std::swap(vin, vout);
+  }
+  *in_alt = (passes & 1) != 0;
+  return cudaGetLastError();
+}
+
+}  // namespace rc
