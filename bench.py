@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark of the race-checking hot path.
+
+One step = one rc_run over the whole workload (all §8(a) rows: heap init,
+every barrier interval's interpretation, onesweep sort, detect + commit,
+boundary bookkeeping, report finalize, report copy-out) plus, at N>1, the NCCL
+report gather.  Default workload = BASELINE config 5 (3-point stencil,
+2^20 work-items x 512 instances per GPU, 8 barrier intervals; weak scaling:
+every rank checks its own 512 instances).  Inputs (4.3 GB per GPU) are far
+larger than the 126 MB L2, so no explicit flush is needed.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0 (contract in the task statement / DESIGN.md §7).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from workloads import inputs as I  # noqa: E402
+from workloads import kernels as K  # noqa: E402
+
+WORKLOADS = {
+    "cfg5": dict(name="config5: 3-point stencil, 2^20 work-items x 512 instances per GPU, 8 barriers",
+                 n=1 << 20, per_gpu=512, src=lambda: K.program(K.STENCIL),
+                 gen=lambda lo, hi, n: I.cfg5_inputs(lo, hi, n)),
+    "cfg4": dict(name="config4: random straight-line stencil kernel (seed 0), 65536 work-items x 512 instances per GPU",
+                 n=65536, per_gpu=512, src=lambda: K.random_stencil_kernel(0),
+                 gen=lambda lo, hi, n: I.cfg4_inputs(lo, hi, n)),
+}
+METRIC = "checked memory accesses/s"
+UNIT = "Gaccess/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (recipe's clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[2:]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_cores():
+    return len(os.sched_getaffinity(0))
+
+
+def oracle_sample(wl, n_inst, threads):
+    """The oracle as it stands on a bounded sample: the first n_inst instances."""
+    import oracle
+    p = wl["src"]()
+    ins = wl["gen"](0, n_inst, wl["n"])
+    t0 = time.perf_counter()
+    r = oracle.run(p.bytecode, wl["n"], ins, threads=threads, want_final=False)
+    dt = time.perf_counter() - t0
+    return r.stats["checked_accesses"], dt
+
+
+def run_reference(args, wl):
+    """--impl reference: the CPU oracle timed on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = cpu_cores()
+    sample = min(wl["per_gpu"], cores)
+    for _ in range(args.warmup):
+        oracle_sample(wl, sample, cores)
+    acc = 0
+    tot = 0.0
+    for _ in range(args.steps):
+        a, dt = oracle_sample(wl, sample, cores)
+        acc += a
+        tot += dt
+    v = acc / tot / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic",
+            "config": {"workload": wl["name"], "work_items": wl["n"], "sample_instances_per_step": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"first {sample} instances of the workload per step (oracle/oracle.c, "
+                                       f"{cores} threads over instances)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg5", choices=list(WORKLOADS))
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--instances", type=int, default=0, help="override instances per GPU (debug)")
+    args = ap.parse_args()
+    wl = dict(WORKLOADS[args.workload])
+    if args.instances:
+        wl["per_gpu"] = args.instances
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1308_3203_b200 import rc_load_program, rc_run
+    from paper_1308_3203_b200.gather import gather_reports, shard
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    total_inst = wl["per_gpu"] * world if args.scaling == "weak" else wl["per_gpu"]
+    lo, hi = shard(total_inst, rank, world)
+    n = wl["n"]
+    p = wl["src"]()
+    prog = rc_load_program(p.bytecode)
+    host = wl["gen"](lo, hi, n)
+    arrays = [torch.from_numpy(x).to(dev) for x in host]
+    stream = torch.cuda.current_stream(dev)
+
+    def step(profile=False, arrs=arrays):
+        r = rc_run(prog, n, arrs, instance_offset=lo, want_final=False, profile=profile, device=local,
+                   stream=stream)
+        if world > 1:
+            reps, st = gather_reports(r.reports, r.stats, device=dev)
+        else:
+            reps, st = r.reports, r.stats
+        return r, reps, st
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    prof_sum = None
+    accesses = 0
+    n_reports = 0
+    with Clocks(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            r, reps, st = step(profile=not args.no_profile)
+            accesses += st["checked_accesses"]
+            n_reports = len(reps)
+            if r.profile:
+                if prof_sum is None:
+                    prof_sum = r.profile
+                else:
+                    for k, v in r.profile.items():
+                        if isinstance(v, dict):
+                            for kk in v:
+                                prof_sum[k][kk] += v[kk]
+                        else:
+                            prof_sum[k] += v
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    ms_step = ms / args.steps
+    # `accesses` already sums all ranks (gathered stats) at N>1
+    value = accesses / args.steps / (ms_step / 1000) / 1e9
+
+    # ---- end to end through the C ABI with HOST buffers (RC_OPT_HOST_IO)
+    e2e = None
+    if not args.no_e2e:
+        pinned = [torch.from_numpy(x).pin_memory() for x in host]
+        h2d = sum(x.numel() * 4 for x in pinned)
+        step(arrs=pinned)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        acc2 = 0
+        d2h = 0
+        a0.record(stream)
+        for _ in range(args.e2e_steps):
+            r, reps, st = step(arrs=pinned)
+            acc2 += st["checked_accesses"]
+            d2h = len(r.reports) * 32 + 13 * 8
+        a1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = a0.elapsed_time(a1)
+        if world > 1:
+            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": acc2 / args.e2e_steps / (ems / args.e2e_steps / 1000) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+               "ms_per_step": ems / args.e2e_steps}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    peak, peak_src = peaks()
+    roofline = None
+    kernels = None
+    gpu_launches = None
+    if prof_sum:
+        s = prof_sum["sort"]
+        achieved = s["alg_bytes"] / (s["ms"] / 1e3) / 1e9 if s["ms"] > 0 else None
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath) and s["launches"]:
+            with open(tpath) as f:
+                tr = json.load(f)
+            bpr = tr.get("onesweep_kernel", {}).get("dram_bytes_per_record")
+            if bpr:
+                traffic = bpr * s["items"] / s["launches"]
+        roofline = {"kernel": "onesweep_kernel (K3, one LSD digit pass)", "bound": "hbm",
+                    "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak if achieved else None,
+                    "traffic": traffic, "alg_bytes_per_launch": s["alg_bytes"] / max(1, s["launches"]),
+                    "alg_bytes_per_record": 24, "launches": s["launches"] // args.steps,
+                    "peak_source": peak_src}
+        kernels = {}
+        for c in ("interp", "hist", "sort", "detect", "boundary", "finalize", "copy"):
+            d = prof_sum[c]
+            kernels[c] = {"launches_per_step": d["launches"] / args.steps, "ms_per_step": d["ms"] / args.steps,
+                          "share": d["ms"] / prof_sum["total_ms"] if prof_sum["total_ms"] else None,
+                          "alg_GBps": d["alg_bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 and d["alg_bytes"] else None}
+        kernels["total_ms_per_step"] = prof_sum["total_ms"] / args.steps
+        gpu_launches = prof_sum["kernel_launches"]
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cores = cpu_cores()
+        sample = min(wl["per_gpu"], 2 * cores)
+        acc, dt = oracle_sample(wl, sample, cores)
+        cpu = {"value": acc / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"first {sample} instances of the workload ({n} work-items each), "
+                         f"{cores} threads over instances, {dt:.1f} s"}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": wl["name"], "work_items": n, "instances_per_gpu": hi - lo,
+                       "instances_total": total_inst, "parallelism": f"dp{world} (instance shards)",
+                       "l2": "inputs 4.3 GB/GPU >> 126 MB L2 (no flush needed)",
+                       "checked_accesses_per_step": accesses // args.steps, "reports_per_step": n_reports},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+            "clocks": clk.summary(), "kernels": kernels}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

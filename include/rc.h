@@ -158,6 +158,7 @@ typedef struct {
   uint64_t alg_bytes[RC_PROF_N];
   uint64_t items[RC_PROF_N]; /* records / lanes processed                    */
   double total_ms;           /* whole rc_run on the stream                    */
+  uint64_t kernel_launches;  /* librc kernels launched by this rc_run         */
 } rc_profile;
 
 /* One shared array of the kernel (an element of Args).

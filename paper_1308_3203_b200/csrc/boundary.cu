@@ -124,14 +124,17 @@ cudaError_t launch_boundary(const BoundaryParams& p, cudaStream_t s) {
     const uint32_t grid = (p.n_lanes + 255) / 256;
     boundary_min_kernel<<<grid, 256, 0, s>>>(p);
     boundary_second_kernel<<<grid, 256, 0, s>>>(p);
+    launched(2);
   }
   boundary_report_kernel<<<(p.n_inst + 255) / 256, 256, 0, s>>>(p);
+  launched();
   return cudaGetLastError();
 }
 
 cudaError_t launch_max_intervals(const BoundaryParams& p, cudaStream_t s) {
   if (p.n_inst == 0) return cudaSuccess;
   max_intervals_kernel<<<(p.n_inst + 255) / 256, 256, 0, s>>>(p);
+  launched();
   return cudaGetLastError();
 }
 
@@ -139,6 +142,7 @@ cudaError_t launch_lane_hist(const uint8_t* status, uint32_t n_lanes, DevCounter
   if (n_lanes == 0) return cudaSuccess;
   const uint32_t grid = (uint32_t)std::min<uint64_t>(1184, (n_lanes + 255) / 256);
   lane_hist_kernel<<<grid, 256, 0, s>>>(status, n_lanes, ctr);
+  launched();
   return cudaGetLastError();
 }
 
@@ -209,16 +213,21 @@ cudaError_t finalize_reports(rc_report* reports, uint64_t n, rc_report* scratch,
     attr = true;
   }
   cudaMemcpyAsync(scratch, reports, n * sizeof(rc_report), cudaMemcpyDeviceToDevice, s);
-  if (n2 > n) pad_kernel<<<(unsigned)((n2 - n + 255) / 256), 256, 0, s>>>(scratch, n, n2);
+  if (n2 > n) { pad_kernel<<<(unsigned)((n2 - n + 255) / 256), 256, 0, s>>>(scratch, n, n2); launched(); }
   const unsigned blocks_local = (unsigned)(n2 / (2 * BLK));
   const size_t smem = 2 * BLK * sizeof(rc_report);
   // all stages k <= 2*BLK inside blocks
   bitonic_local<<<blocks_local, BLK, smem, s>>>(scratch, 2, 2 * BLK, 1);
+  launched();
   for (uint64_t k = 4 * BLK; k <= n2; k <<= 1) {
     uint64_t j = k >> 1;
     for (; j >= 2 * BLK; j >>= 1)
+    {
       bitonic_global<<<(unsigned)((n2 + 255) / 256), 256, 0, s>>>(scratch, n2, k, j);
+      launched();
+    }
     bitonic_local<<<blocks_local, BLK, smem, s>>>(scratch, k, k, j);
+    launched();
   }
   cudaMemcpyAsync(reports, scratch, n * sizeof(rc_report), cudaMemcpyDeviceToDevice, s);
   return cudaGetLastError();

@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
 cudaError_t launch_detect(const DetectParams& p, cudaStream_t s) {
   if (p.n_records == 0) return cudaSuccess;
   detect_kernel<<<(p.n_records + 255) / 256, 256, 0, s>>>(p);
+  launched();
   return cudaGetLastError();
 }
 

@@ -375,6 +375,7 @@ cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
   }
   const uint32_t grid = (p.n_lanes + T - 1) / T;
   interp_kernel<<<grid, T, sm, s>>>(p);
+  launched();
   return cudaGetLastError();
 }
 

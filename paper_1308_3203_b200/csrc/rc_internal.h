@@ -2,6 +2,7 @@
 // the ABI (include/rc.h is).  Nothing here is shared with oracle/.
 #pragma once
 #include <cstddef>
+#include <atomic>
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -12,6 +13,10 @@
 #include "rc.h"
 
 namespace rc {
+
+// count of librc kernel launches (reported in rc_profile.kernel_launches)
+extern std::atomic<uint64_t> g_launches;
+inline void launched(uint64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
 struct Ins {  // 8-byte RCB1 instruction, include/rc.h
   uint8_t op, a, b, c;

@@ -23,6 +23,7 @@
 
 namespace rc {
 int fail(int code, const char* fmt, ...);
+std::atomic<uint64_t> g_launches{0};
 
 size_t Profiler::next() {
   if (used == pool.size()) {
@@ -257,6 +258,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   W.prof.reset();
   W.prof.on = opt.profile != nullptr;
   if (opt.profile) memset(opt.profile, 0, sizeof(rc_profile));
+  const uint64_t launches0 = g_launches.load();
   cudaEvent_t t_begin = nullptr, t_end = nullptr;
   if (W.prof.on) {
     cudaEventCreate(&t_begin);
@@ -533,6 +535,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     float ms = 0;
     cudaEventElapsedTime(&ms, t_begin, t_end);
     opt.profile->total_ms = ms;
+    opt.profile->kernel_launches = g_launches.load() - launches0;
     cudaEventDestroy(t_begin);
     cudaEventDestroy(t_end);
   }

@@ -283,6 +283,7 @@ cudaError_t onesweep_sort(uint32_t* keys, uint64_t* vals, uint32_t n, int bits, 
   if (prof) prof->begin(s);
   hist_kernel<<<hist_grid, 256, 0, s>>>(keys, n, passes, ws.hist);
   bin_offsets_kernel<<<passes, 256, 0, s>>>(ws.hist, ws.bin_off);
+  launched(2);
   if (prof) prof->end(RC_PROF_HIST, s, (uint64_t)n * 4, n);
   const uint32_t tiles = (uint32_t)sort_tiles(n);
   uint32_t* kin = keys;
@@ -298,6 +299,7 @@ cudaError_t onesweep_sort(uint32_t* keys, uint64_t* vals, uint32_t n, int bits, 
     onesweep_kernel<<<tiles, SORT_THREADS, sizeof(SortSmem), s>>>(kin, vin, kout, vout, n, 8 * p,
                                                                  ws.bin_off + p * RADIX, ws.status,
                                                                  ws.tile_ctr + p, ws.epoch);
+    launched();
     if (prof) prof->end(RC_PROF_SORT, s, (uint64_t)n * 24, n);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -41,7 +41,7 @@ class rc_stats(C.Structure):
 
 class rc_profile(C.Structure):
     _fields_ = [("launches", C.c_uint64 * 8), ("ms", C.c_double * 8), ("alg_bytes", C.c_uint64 * 8),
-                ("items", C.c_uint64 * 8), ("total_ms", C.c_double)]
+                ("items", C.c_uint64 * 8), ("total_ms", C.c_double), ("kernel_launches", C.c_uint64)]
 
 
 class rc_array(C.Structure):
@@ -144,7 +144,7 @@ def _stats_dict(s: rc_stats) -> dict:
 
 
 def _profile_dict(p: rc_profile) -> dict:
-    return {"total_ms": p.total_ms,
+    return {"total_ms": p.total_ms, "kernel_launches": int(p.kernel_launches),
             **{c: {"launches": int(p.launches[i]), "ms": float(p.ms[i]), "alg_bytes": int(p.alg_bytes[i]),
                    "items": int(p.items[i])} for i, c in enumerate(PROF_CLASSES)}}
 
