@@ -21,55 +21,61 @@ __device__ __forceinline__ void push_report(rc_report* reps, unsigned long long 
 }
 }  // namespace
 
-// first arrived tid per instance, waiting flags
-__global__ void boundary_min_kernel(const BoundaryParams p) {
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = g < p.n_lanes;
-  const uint32_t inst = valid ? g / p.n : 0xFFFFFFFFu;
-  const uint32_t tid = valid ? g - inst * p.n : 0;
-  const uint8_t st = valid ? p.status[g] : (uint8_t)L_EXITED;
-  const bool arrived = valid && p.node[g] != NODE_NONE;
-  const bool waiting = st == L_WAITING;
-  if (__any_sync(FULL, waiting)) {
-    if (waiting) p.inst_waiting[inst] = 1;
-    if ((threadIdx.x & 31) == __ffs(__ballot_sync(FULL, waiting)) - 1) p.ctr->any_waiting = 1;
-  }
-  // warp-uniform instance: one atomic per warp
-  const uint32_t inst0 = __shfl_sync(FULL, inst, 0);
-  const bool uniform = __all_sync(FULL, inst == inst0);
-  if (uniform) {
-    const uint32_t m = __reduce_min_sync(FULL, arrived ? tid : 0xFFFFFFFFu);
-    if ((threadIdx.x & 31) == 0 && m != 0xFFFFFFFFu) atomicMin(&p.first_tid[inst0], m);
-  } else if (arrived) {
-    atomicMin(&p.first_tid[inst], tid);
-  }
+__device__ __forceinline__ bool arrived_node(uint8_t st, uint32_t pc, int32_t* node) {
+  if (st == L_WAITING) { *node = (int32_t)pc - 1; return true; }
+  if (st == L_EXITED_NOW) { *node = NODE_EXIT; return true; }
+  return false;
 }
 
-// min arrived tid at a node different from the first arrived tid's node
-__global__ void boundary_second_kernel(const BoundaryParams p) {
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= p.n_lanes) return;
-  const int32_t nd = p.node[g];
-  if (nd == NODE_NONE) return;
-  const uint32_t inst = g / p.n;
-  const uint32_t tid = g - inst * p.n;
-  const uint32_t ft = p.first_tid[inst];
-  if (p.node[(size_t)inst * p.n + ft] != nd) atomicMin(&p.second_tid[inst], tid);
-}
-
-__global__ void boundary_report_kernel(const BoundaryParams p) {
+// per instance: did the arrivals of this interval reach more than one node?
+// (K1 reduced min / max arrival node per instance.)  Resets the range.
+__global__ void boundary_check_kernel(const BoundaryParams p) {
   const uint32_t inst = blockIdx.x * blockDim.x + threadIdx.x;
   if (inst >= p.n_inst) return;
-  const uint32_t t2 = p.second_tid[inst];
-  if (t2 == 0xFFFFFFFFu) return;
+  const int32_t lo = p.node_min[inst], hi = p.node_max[inst];
+  p.node_min[inst] = 0x7FFFFFFF;
+  p.node_max[inst] = (int32_t)0x80000000;
+  const bool div = lo < hi;
+  p.inst_flag[inst] = div;
+  if (div) p.ctr->diverged = 1;
+}
+
+// rare path 1: first arrived tid of each diverged instance
+__global__ void div_first_kernel(const BoundaryParams p) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= p.n_lanes) return;
+  const uint32_t inst = g / p.n;
+  int32_t nd;
+  if (!p.inst_flag[inst] || !arrived_node(p.status[g], p.pc[g], &nd)) return;
+  atomicMin(&p.first_tid[inst], g - inst * p.n);
+}
+
+// rare path 2: min arrived tid at a node different from the first arrival's
+__global__ void div_second_kernel(const BoundaryParams p) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= p.n_lanes) return;
+  const uint32_t inst = g / p.n;
+  int32_t nd, n1;
+  if (!p.inst_flag[inst] || !arrived_node(p.status[g], p.pc[g], &nd)) return;
+  const size_t f = (size_t)inst * p.n + p.first_tid[inst];
+  arrived_node(p.status[f], p.pc[f], &n1);
+  if (nd != n1) atomicMin(&p.second_tid[inst], g - inst * p.n);
+}
+
+__global__ void div_report_kernel(const BoundaryParams p) {
+  const uint32_t inst = blockIdx.x * blockDim.x + threadIdx.x;
+  if (inst >= p.n_inst || !p.inst_flag[inst]) return;
   const uint32_t t1 = p.first_tid[inst];
+  const size_t f = (size_t)inst * p.n + t1;
+  int32_t n1 = NODE_NONE;
+  arrived_node(p.status[f], p.pc[f], &n1);
   rc_report r;
   r.instance = p.inst_base + inst;
   r.interval = p.interval;
   r.array = -1;
-  r.index = p.node[(size_t)inst * p.n + t1];
+  r.index = n1;
   r.tid1 = t1;
-  r.tid2 = t2;
+  r.tid2 = p.second_tid[inst];
   r.kind = RC_BARRIER_DIVERGENCE;
   r.flags = 0;
   r.reserved = 0;
@@ -77,9 +83,15 @@ __global__ void boundary_report_kernel(const BoundaryParams p) {
 }
 
 // instance-level FUEL when max_intervals stops a batch with suspended work-items
+__global__ void waiting_scan_kernel(const BoundaryParams p) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= p.n_lanes) return;
+  if (p.status[g] == L_WAITING) p.inst_flag[g / p.n] = 1;
+}
+
 __global__ void max_intervals_kernel(const BoundaryParams p) {
   const uint32_t inst = blockIdx.x * blockDim.x + threadIdx.x;
-  if (inst >= p.n_inst || !p.inst_waiting[inst]) return;
+  if (inst >= p.n_inst || !p.inst_flag[inst]) return;
   rc_report r;
   r.instance = p.inst_base + inst;
   r.interval = p.interval;
@@ -101,7 +113,7 @@ __global__ void lane_hist_kernel(const uint8_t* __restrict__ status, uint32_t n_
     const uint8_t s = status[g];
     int slot;
     switch (s) {
-      case L_EXITED: slot = 0; break;
+      case L_EXITED: case L_EXITED_NOW: slot = 0; break;
       case L_PRUNED: slot = 1; break;
       case L_OOB: slot = 2; break;
       case L_ASSERT: slot = 3; break;
@@ -117,22 +129,30 @@ __global__ void lane_hist_kernel(const uint8_t* __restrict__ status, uint32_t n_
 
 cudaError_t launch_boundary(const BoundaryParams& p, cudaStream_t s) {
   if (p.n_inst == 0) return cudaSuccess;
+  boundary_check_kernel<<<(p.n_inst + 255) / 256, 256, 0, s>>>(p);
+  launched();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_divergence(const BoundaryParams& p, cudaStream_t s) {
+  if (p.n_inst == 0 || p.n_lanes == 0) return cudaSuccess;
   cudaMemsetAsync(p.first_tid, 0xFF, p.n_inst * sizeof(uint32_t), s);
   cudaMemsetAsync(p.second_tid, 0xFF, p.n_inst * sizeof(uint32_t), s);
-  cudaMemsetAsync(p.inst_waiting, 0, p.n_inst * sizeof(uint32_t), s);
-  if (p.n_lanes) {
-    const uint32_t grid = (p.n_lanes + 255) / 256;
-    boundary_min_kernel<<<grid, 256, 0, s>>>(p);
-    boundary_second_kernel<<<grid, 256, 0, s>>>(p);
-    launched(2);
-  }
-  boundary_report_kernel<<<(p.n_inst + 255) / 256, 256, 0, s>>>(p);
-  launched();
+  const uint32_t grid = (p.n_lanes + 255) / 256;
+  div_first_kernel<<<grid, 256, 0, s>>>(p);
+  div_second_kernel<<<grid, 256, 0, s>>>(p);
+  div_report_kernel<<<(p.n_inst + 255) / 256, 256, 0, s>>>(p);
+  launched(3);
   return cudaGetLastError();
 }
 
 cudaError_t launch_max_intervals(const BoundaryParams& p, cudaStream_t s) {
   if (p.n_inst == 0) return cudaSuccess;
+  cudaMemsetAsync(p.inst_flag, 0, p.n_inst * sizeof(uint32_t), s);
+  if (p.n_lanes) {
+    waiting_scan_kernel<<<(p.n_lanes + 255) / 256, 256, 0, s>>>(p);
+    launched();
+  }
   max_intervals_kernel<<<(p.n_inst + 255) / 256, 256, 0, s>>>(p);
   launched();
   return cudaGetLastError();

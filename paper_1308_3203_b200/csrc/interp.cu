@@ -1,16 +1,19 @@
 // interp.cu — K1: one barrier interval of the §4 thread-local semantics for
-// every live work-item of an instance batch.
+// every live work-item of an instance batch, fused with the interval-boundary
+// bookkeeping (A4).
 //
 // One CUDA thread = one simulated work-item (lane).  A warp is one instruction
 // stream: each step it executes the instruction at the minimum pc among its
-// running lanes (uniform fetch/decode), lanes at that pc execute it, the rest
-// wait — a lane's result never depends on the order because, inside an
-// interval, lanes only see the interval-start heap plus their own writes
-// (delayed visibility, reading L2).
+// running lanes (uniform fetch/decode from the program staged in shared
+// memory), lanes at that pc execute it, the rest wait — a lane's result never
+// depends on the order because, inside an interval, lanes only see the
+// interval-start heap plus their own writes (delayed visibility, reading L2).
 //
 // Per lane: registers (Locals) live in shared memory laid out
-// [reg][thread] (a warp touching one register hits 32 distinct banks); the
-// own-write overlay (cell, value) also lives in shared memory.
+// [reg][thread] (a warp touching one register hits 32 distinct banks); only
+// the registers live across a barrier (program.cpp analyze()) travel through
+// HBM between intervals.  The own-write overlay (cell, value), sized by the
+// static bound on stores per interval, also lives in shared memory.
 //
 // Rules implemented: assign (170), store (176/179) into the
 // overlay, load (182/185, reading L11) from the overlay else the interval-start
@@ -21,15 +24,18 @@
 // Log: a read record per performed LD, and at the end of the interval one
 // write record per distinct cell the lane wrote carrying its final value
 // (reading L3).  Records are staged per warp in shared memory and written out
-// by the block with ONE global atomic per block (per-warp atomics on a single
-// counter would serialise ~10^7 times per interval at config 5).
+// by the block with ONE global atomic per block.
+//
+// Fused A4 (reading L9): per instance the min / max arrival
+// node (BAR pc, or -1 for exit) of the lanes that arrived in this interval —
+// equal min and max means every arrival reached the same barrier — and a
+// global "some lane is suspended" flag.  One atomic per block and instance.
 #include "rc_internal.h"
 
 namespace rc {
 
 namespace {
 constexpr unsigned FULL = 0xFFFFFFFFu;
-constexpr int STAGE = 256;  // records staged per warp
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -37,58 +43,67 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
-__device__ __forceinline__ void emit_report(const InterpParams& p, uint32_t inst, int32_t arr, int32_t idx,
-                                            uint32_t t1, uint32_t t2, uint16_t kind) {
-  unsigned long long pos = atomicAdd(&p.ctr->report_count, 1ull);
-  if (pos < p.report_cap) {
+// (rare paths take explicit arguments so the kernel's parameter block is never
+// copied to local memory)
+__device__ __noinline__ void emit_report_(DevCounters* ctr, rc_report* reports, unsigned long long cap,
+                                          uint32_t instance, uint32_t interval, int32_t arr, int32_t idx,
+                                          uint32_t t1, uint32_t kind) {
+  unsigned long long pos = atomicAdd(&ctr->report_count, 1ull);
+  if (pos < cap) {
     rc_report r;
-    r.instance = p.inst_base + inst;
-    r.interval = p.interval;
+    r.instance = instance;
+    r.interval = interval;
     r.array = arr;
     r.index = idx;
     r.tid1 = t1;
-    r.tid2 = t2;
-    r.kind = kind;
+    r.tid2 = NOTID;
+    r.kind = (uint16_t)kind;
     r.flags = 0;
     r.reserved = 0;
-    p.reports[pos] = r;
+    reports[pos] = r;
   }
 }
+#define emit_report(p, inst, arr, idx, t1, kind) \
+  emit_report_((p).ctr, (p).reports, (p).report_cap, (p).inst_base + (inst), (p).interval, arr, idx, t1, kind)
 
 struct Stage {
   uint32_t* keys;  // this warp's staging area
   uint64_t* vals;
   uint32_t fill;   // warp-uniform
+  uint32_t cap;
 };
 
 // write this warp's staged records to the global log (mid-interval overflow path)
-__device__ __noinline__ void flush_warp(const InterpParams& p, Stage& S, int lane) {
+__device__ __noinline__ uint32_t flush_warp_(DevCounters* ctr, uint32_t* log_keys, uint64_t* log_vals,
+                                             unsigned long long log_cap, const uint32_t* skeys,
+                                             const uint64_t* svals, uint32_t fill, int lane) {
   __syncwarp();
   unsigned long long base = 0;
-  if (lane == 0) base = atomicAdd(&p.ctr->log_count, (unsigned long long)S.fill);
+  if (lane == 0) base = atomicAdd(&ctr->log_count, (unsigned long long)fill);
   base = __shfl_sync(FULL, base, 0);
   bool over = false;
-  for (uint32_t i = lane; i < S.fill; i += 32) {
+  for (uint32_t i = lane; i < fill; i += 32) {
     unsigned long long pos = base + i;
-    if (pos < p.log_cap) {
-      p.log_keys[pos] = S.keys[i];
-      p.log_vals[pos] = S.vals[i];
+    if (pos < log_cap) {
+      log_keys[pos] = skeys[i];
+      log_vals[pos] = svals[i];
     } else {
       over = true;
     }
   }
-  if (__any_sync(FULL, over) && lane == 0) p.ctr->log_overflow = 1;
+  if (__any_sync(FULL, over) && lane == 0) ctr->log_overflow = 1;
   __syncwarp();
-  S.fill = 0;
+  return 0;
 }
 
-// warp-aggregated append of one record per lane in `m` (must be called by the whole warp)
+// warp-aggregated append of one record per lane in `m` (called by the whole warp)
 __device__ __forceinline__ void stage_append(const InterpParams& p, Stage& S, int lane, unsigned m, bool mine,
                                              uint32_t key, uint64_t val) {
-  uint32_t cnt = __popc(m);
-  if (S.fill + cnt > STAGE) flush_warp(p, S, lane);
+  const uint32_t cnt = __popc(m);
+  if (S.fill + cnt > S.cap)
+    S.fill = flush_warp_(p.ctr, p.log_keys, p.log_vals, p.log_cap, S.keys, S.vals, S.fill, lane);
   if (mine) {
-    uint32_t pos = S.fill + __popc(m & lanemask_lt());
+    const uint32_t pos = S.fill + __popc(m & lanemask_lt());
     S.keys[pos] = key;
     S.vals[pos] = val;
   }
@@ -105,34 +120,44 @@ __device__ __forceinline__ int32_t wadd(int32_t x, int32_t y) { return (int32_t)
 
 }  // namespace
 
-__global__ void __launch_bounds__(256) interp_kernel(const InterpParams p) {
+template <bool CODE_SMEM>
+__global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int T = blockDim.x;
   const int W = T >> 5;
   const int t = threadIdx.x;
   const int warp = t >> 5, lane = t & 31;
-  const uint32_t R = p.n_regs;
+  const uint32_t R = p.n_regs, OV = p.ovl_cap;
 
-  uint64_t* st_vals = reinterpret_cast<uint64_t*>(smem);
-  uint32_t* st_keys = reinterpret_cast<uint32_t*>(st_vals + (size_t)W * STAGE);
-  int32_t* sregs = reinterpret_cast<int32_t*>(st_keys + (size_t)W * STAGE);
-  uint32_t* ocell = reinterpret_cast<uint32_t*>(sregs + (size_t)R * T);
-  int32_t* oval = reinterpret_cast<int32_t*>(ocell + (size_t)OVL_CAP * T);
-  uint32_t* s_off = reinterpret_cast<uint32_t*>(oval + (size_t)OVL_CAP * T);
-  uint32_t* s_size = s_off + p.n_arrays;
-  uint32_t* wcnt = s_size + p.n_arrays;       // [W]
-  unsigned long long* wbase = reinterpret_cast<unsigned long long*>(
-      (reinterpret_cast<uintptr_t>(wcnt + W) + 7) & ~uintptr_t(7));  // [W]
-  unsigned long long* wstat = wbase + W;      // [3][W]
+  // ---- shared memory carve-up (sizes mirrored in interp_smem_bytes)
+  unsigned char* q = smem;
+  uint64_t* st_vals = reinterpret_cast<uint64_t*>(q); q += (size_t)W * p.stage * 8;
+  uint2* s_code = reinterpret_cast<uint2*>(q); q += CODE_SMEM ? (size_t)p.n_instr * 8 : 0;
+  uint32_t* st_keys = reinterpret_cast<uint32_t*>(q); q += (size_t)W * p.stage * 4;
+  int32_t* sregs = reinterpret_cast<int32_t*>(q); q += (size_t)R * T * 4;
+  uint32_t* ocell = reinterpret_cast<uint32_t*>(q); q += (size_t)OV * T * 4;
+  int32_t* oval = reinterpret_cast<int32_t*>(q); q += (size_t)OV * T * 4;
+  uint32_t* s_off = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
+  uint32_t* s_size = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(q); q += (size_t)W * 4;
+  int32_t* wnode = reinterpret_cast<int32_t*>(q); q += (size_t)2 * W * 4;   // per-warp min / max node
+  q = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(q) + 7) & ~uintptr_t(7));
+  unsigned long long* wbase = reinterpret_cast<unsigned long long*>(q); q += (size_t)W * 8;
+  unsigned long long* wstat = reinterpret_cast<unsigned long long*>(q);    // [3][W]
 
   for (uint32_t a = t; a < p.n_arrays; a += T) {
     s_off[a] = p.arr_off[a];
     s_size[a] = p.arr_size[a];
   }
+  if (CODE_SMEM) {
+    const uint2* src = reinterpret_cast<const uint2*>(p.code);
+    for (uint32_t i = t; i < p.n_instr; i += T) s_code[i] = src[i];
+  }
 
   const uint32_t g = blockIdx.x * (uint32_t)T + t;
   const bool valid = g < p.n_lanes;
   uint8_t status = valid ? p.status_in[g] : (uint8_t)L_EXITED;
+  if (status == L_EXITED_NOW) status = L_EXITED;
   bool running = valid && (status == L_RUNNING || status == L_WAITING);
   const uint32_t inst = valid ? g / p.n : 0;
   const uint32_t tid = valid ? g - inst * p.n : 0;
@@ -140,25 +165,29 @@ __global__ void __launch_bounds__(256) interp_kernel(const InterpParams p) {
   uint32_t pc = running ? p.pc_in[g] : 0;
   int32_t* Rg = sregs + t;  // register r of this lane = Rg[r*T]
   if (running)
-    for (uint32_t r = 0; r < R; r++) Rg[r * T] = p.regs_in[(size_t)r * p.n_lanes + g];
+    for (uint32_t i = 0; i < p.n_live; i++) {
+      const uint32_t r = __ldg(p.live + i);
+      Rg[r * T] = p.regs_in[(size_t)r * p.n_lanes + g];
+    }
   __syncthreads();
 
   if (running) status = L_RUNNING;
   int n_own = 0;
-  int32_t node = NODE_NONE;
   unsigned long long steps = 0;
   uint32_t nloads = 0, nstores = 0;
   bool ovl_over = false;
-  Stage S{st_keys + (size_t)warp * STAGE, st_vals + (size_t)warp * STAGE, 0};
+  Stage S{st_keys + (size_t)warp * p.stage, st_vals + (size_t)warp * p.stage, 0, p.stage};
 
   for (;;) {
     if (__ballot_sync(FULL, running) == 0) break;
     const uint32_t minpc = __reduce_min_sync(FULL, running ? pc : 0xFFFFFFFFu);
     bool ex = running && pc == minpc;
-    const Ins I = p.code[minpc];
+    const uint2 raw = CODE_SMEM ? s_code[minpc] : __ldg(reinterpret_cast<const uint2*>(p.code) + minpc);
+    const uint32_t op = raw.x & 0xFF, ia = (raw.x >> 8) & 0xFF, ib = (raw.x >> 16) & 0xFF, ic = raw.x >> 24;
+    const int32_t imm = (int32_t)raw.y;
     if (ex) {  // fuel check before executing (reading L17)
       if (steps == p.fuel) {
-        emit_report(p, inst, -1, (int32_t)pc, tid, NOTID, RC_FUEL);
+        emit_report(p, inst, -1, (int32_t)pc, tid, RC_FUEL);
         running = false;
         status = L_FUEL;
         ex = false;
@@ -166,18 +195,18 @@ __global__ void __launch_bounds__(256) interp_kernel(const InterpParams p) {
         steps++;
       }
     }
-    switch (I.op) {  // warp-uniform
-      case RC_OP_CONST: if (ex) { Rg[I.a * T] = I.imm; pc++; } break;
-      case RC_OP_MOV: if (ex) { Rg[I.a * T] = Rg[I.b * T]; pc++; } break;
-      case RC_OP_TID: if (ex) { Rg[I.a * T] = (int32_t)tid; pc++; } break;
-      case RC_OP_SIZE: if (ex) { Rg[I.a * T] = (int32_t)s_size[I.b]; pc++; } break;
-      case RC_OP_ADDI: if (ex) { Rg[I.a * T] = wadd(Rg[I.b * T], I.imm); pc++; } break;
+    switch (op) {  // warp-uniform
+      case RC_OP_CONST: if (ex) { Rg[ia * T] = imm; pc++; } break;
+      case RC_OP_MOV: if (ex) { Rg[ia * T] = Rg[ib * T]; pc++; } break;
+      case RC_OP_TID: if (ex) { Rg[ia * T] = (int32_t)tid; pc++; } break;
+      case RC_OP_SIZE: if (ex) { Rg[ia * T] = (int32_t)s_size[ib]; pc++; } break;
+      case RC_OP_ADDI: if (ex) { Rg[ia * T] = wadd(Rg[ib * T], imm); pc++; } break;
       case RC_OP_ADD: case RC_OP_SUB: case RC_OP_MUL: case RC_OP_MIN: case RC_OP_MAX: case RC_OP_AND:
       case RC_OP_OR: case RC_OP_XOR: case RC_OP_LT: case RC_OP_EQ: case RC_OP_LAND:
         if (ex) {
-          const int32_t x = Rg[I.b * T], y = Rg[I.c * T];
+          const int32_t x = Rg[ib * T], y = Rg[ic * T];
           int32_t v;
-          switch (I.op) {
+          switch (op) {
             case RC_OP_ADD: v = wadd(x, y); break;
             case RC_OP_SUB: v = (int32_t)((uint32_t)x - (uint32_t)y); break;
             case RC_OP_MUL: v = (int32_t)((uint32_t)x * (uint32_t)y); break;
@@ -190,44 +219,44 @@ __global__ void __launch_bounds__(256) interp_kernel(const InterpParams p) {
             case RC_OP_EQ: v = x == y; break;
             default: v = (x != 0) && (y != 0); break;
           }
-          Rg[I.a * T] = v;
+          Rg[ia * T] = v;
           pc++;
         }
         break;
       case RC_OP_DIV: case RC_OP_MOD:
         if (ex) {
-          const int32_t x = Rg[I.b * T], y = Rg[I.c * T];
+          const int32_t x = Rg[ib * T], y = Rg[ic * T];
           if (y == 0) {
-            emit_report(p, inst, -1, (int32_t)pc, tid, NOTID, RC_DIV0);
+            emit_report(p, inst, -1, (int32_t)pc, tid, RC_DIV0);
             running = false;
             status = L_DIV0;
           } else {
             int32_t v;
-            if (I.op == RC_OP_DIV) v = (y == -1) ? (int32_t)(0u - (uint32_t)x) : x / y;
+            if (op == RC_OP_DIV) v = (y == -1) ? (int32_t)(0u - (uint32_t)x) : x / y;
             else v = (y == -1) ? 0 : x % y;
-            Rg[I.a * T] = v;
+            Rg[ia * T] = v;
             pc++;
           }
         }
         break;
-      case RC_OP_LNOT: if (ex) { Rg[I.a * T] = Rg[I.b * T] == 0; pc++; } break;
+      case RC_OP_LNOT: if (ex) { Rg[ia * T] = Rg[ib * T] == 0; pc++; } break;
       case RC_OP_LD: {
         bool ok = false;
         uint32_t cell = 0;
         if (ex) {
-          const int32_t idx = Rg[I.c * T];
-          if (idx < 0 || (uint32_t)idx >= s_size[I.b]) {
-            emit_report(p, inst, (int32_t)I.b, idx, tid, NOTID, RC_OOB);
+          const int32_t idx = Rg[ic * T];
+          if (idx < 0 || (uint32_t)idx >= s_size[ib]) {
+            emit_report(p, inst, (int32_t)ib, idx, tid, RC_OOB);
             running = false;
             status = L_OOB;
           } else {
-            cell = cell_base + s_off[I.b] + (uint32_t)idx;
+            cell = cell_base + s_off[ib] + (uint32_t)idx;
             int32_t v = 0;
             bool found = false;
             for (int j = 0; j < n_own; j++)
               if (ocell[j * T + t] == cell) { v = oval[j * T + t]; found = true; }
             if (!found) v = __ldg(p.heap + cell);
-            Rg[I.a * T] = v;
+            Rg[ia * T] = v;
             pc++;
             nloads++;
             ok = true;
@@ -239,37 +268,37 @@ __global__ void __launch_bounds__(256) interp_kernel(const InterpParams p) {
       }
       case RC_OP_ST:
         if (ex) {
-          const int32_t idx = Rg[I.b * T];
-          if (idx < 0 || (uint32_t)idx >= s_size[I.a]) {
-            emit_report(p, inst, (int32_t)I.a, idx, tid, NOTID, RC_OOB);
+          const int32_t idx = Rg[ib * T];
+          if (idx < 0 || (uint32_t)idx >= s_size[ia]) {
+            emit_report(p, inst, (int32_t)ia, idx, tid, RC_OOB);
             running = false;
             status = L_OOB;
           } else {
-            const uint32_t cell = cell_base + s_off[I.a] + (uint32_t)idx;
+            const uint32_t cell = cell_base + s_off[ia] + (uint32_t)idx;
             int j = 0;
             while (j < n_own && ocell[j * T + t] != cell) j++;
             if (j == n_own) {
-              if (n_own < OVL_CAP) { ocell[j * T + t] = cell; n_own++; }
+              if (n_own < (int)OV) { ocell[j * T + t] = cell; n_own++; }
               else { ovl_over = true; j = -1; }
             }
-            if (j >= 0) oval[j * T + t] = Rg[I.c * T];
+            if (j >= 0) oval[j * T + t] = Rg[ic * T];
             pc++;
             nstores++;
           }
         }
         break;
-      case RC_OP_BAR: if (ex) { node = (int32_t)pc; pc++; running = false; status = L_WAITING; } break;
-      case RC_OP_EXIT: if (ex) { node = NODE_EXIT; running = false; status = L_EXITED; } break;
+      case RC_OP_BAR: if (ex) { pc++; running = false; status = L_WAITING; } break;
+      case RC_OP_EXIT: if (ex) { running = false; status = L_EXITED_NOW; } break;
       case RC_OP_ASSUME:
         if (ex) {
-          if (Rg[I.a * T] == 0) { running = false; status = L_PRUNED; }
+          if (Rg[ia * T] == 0) { running = false; status = L_PRUNED; }
           else pc++;
         }
         break;
       case RC_OP_ASSERT:
         if (ex) {
-          if (Rg[I.a * T] == 0) {
-            emit_report(p, inst, -1, (int32_t)pc, tid, NOTID, RC_ASSERT);
+          if (Rg[ia * T] == 0) {
+            emit_report(p, inst, -1, (int32_t)pc, tid, RC_ASSERT);
             running = false;
             status = L_ASSERT;
           } else {
@@ -277,8 +306,8 @@ __global__ void __launch_bounds__(256) interp_kernel(const InterpParams p) {
           }
         }
         break;
-      case RC_OP_BR: if (ex) pc = Rg[I.a * T] != 0 ? (uint32_t)I.imm : (uint32_t)I.b + 256u * I.c; break;
-      case RC_OP_JMP: if (ex) pc = (uint32_t)I.imm; break;
+      case RC_OP_BR: if (ex) pc = Rg[ia * T] != 0 ? (uint32_t)imm : ib + 256u * ic; break;
+      case RC_OP_JMP: if (ex) pc = (uint32_t)imm; break;
       default: break;  // unreachable: the validator rejects unknown opcodes
     }
   }
@@ -297,17 +326,34 @@ __global__ void __launch_bounds__(256) interp_kernel(const InterpParams p) {
     stage_append(p, S, lane, m, has, c, v);
   }
 
-  // lane state out
+  // lane state out (only registers live across the barrier, only for suspended lanes)
   if (valid) {
     p.status_out[g] = status;
-    p.node_out[g] = node;
     if (status == L_WAITING) {
       p.pc_out[g] = pc;
-      for (uint32_t r = 0; r < R; r++) p.regs_out[(size_t)r * p.n_lanes + g] = Rg[r * T];
+      for (uint32_t i = 0; i < p.n_live; i++) {
+        const uint32_t r = __ldg(p.live + i);
+        p.regs_out[(size_t)r * p.n_lanes + g] = Rg[r * T];
+      }
     }
   }
 
-  // block-level log write-out: one atomic per block
+  // fused A4: arrival node range per instance, suspended flag
+  const bool arrived = valid && (status == L_WAITING || status == L_EXITED_NOW);
+  const int32_t node = status == L_WAITING ? (int32_t)pc - 1 : NODE_EXIT;
+  const bool any_wait = __any_sync(FULL, status == L_WAITING);
+  const uint32_t inst0 = __shfl_sync(FULL, inst, 0);
+  const bool warp_uniform = __all_sync(FULL, !valid || inst == inst0);
+  const unsigned am = __ballot_sync(FULL, arrived);
+  // nodes are >= -1; bias by 1 so unsigned reductions apply
+  const uint32_t nmin = __reduce_min_sync(FULL, arrived ? (uint32_t)(node + 1) : 0xFFFFFFFFu);
+  const uint32_t nmax = __reduce_max_sync(FULL, arrived ? (uint32_t)(node + 1) : 0u);
+  if (!warp_uniform && arrived) {  // small work-groups: per-lane atomics
+    atomicMin(p.node_min + inst, node);
+    atomicMax(p.node_max + inst, node);
+  }
+
+  // block-level log write-out (one atomic per block) and A4 reductions
   unsigned long long s0 = warp_sum64(steps), s1 = warp_sum64(nloads), s2 = warp_sum64(nstores);
   const bool any_ovl = __any_sync(FULL, ovl_over);
   if (lane == 0) {
@@ -316,13 +362,43 @@ __global__ void __launch_bounds__(256) interp_kernel(const InterpParams p) {
     wstat[W + warp] = s1;
     wstat[2 * W + warp] = s2;
     if (any_ovl) p.ctr->ovl_overflow = 1;
+    // per-warp node range; 0xFFFFFFFF marks "no warp-uniform arrival"
+    wnode[warp] = (warp_uniform && am) ? (int32_t)(nmin - 1) : 0x7FFFFFFF;
+    wnode[W + warp] = (warp_uniform && am) ? (int32_t)(nmax - 1) : (int32_t)0x80000000;
+    wcnt[warp] |= (any_wait ? 0x80000000u : 0u);
+    // instance of the warp (valid lanes only) kept in wbase temporarily
+    wbase[warp] = warp_uniform ? inst0 : 0xFFFFFFFFull;
   }
   __syncthreads();
   if (t == 0) {
     unsigned long long tot = 0, a0 = 0, a1 = 0, a2 = 0;
+    bool wait_any = false;
+    // node range: combine consecutive warps of the same instance
+    uint32_t cur_inst = 0xFFFFFFFFu;
+    int32_t cmin = 0x7FFFFFFF, cmax = (int32_t)0x80000000;
     for (int w = 0; w < W; w++) {
+      const uint32_t wi = (uint32_t)wbase[w];
+      if (wi != cur_inst) {
+        if (cur_inst != 0xFFFFFFFFu && cmin <= cmax) {
+          atomicMin(p.node_min + cur_inst, cmin);
+          atomicMax(p.node_max + cur_inst, cmax);
+        }
+        cur_inst = wi;
+        cmin = 0x7FFFFFFF;
+        cmax = (int32_t)0x80000000;
+      }
+      cmin = min(cmin, wnode[w]);
+      cmax = max(cmax, wnode[W + w]);
+    }
+    if (cur_inst != 0xFFFFFFFFu && cmin <= cmax) {
+      atomicMin(p.node_min + cur_inst, cmin);
+      atomicMax(p.node_max + cur_inst, cmax);
+    }
+    for (int w = 0; w < W; w++) {
+      wait_any |= (wcnt[w] & 0x80000000u) != 0;
+      const uint32_t c = wcnt[w] & 0x7FFFFFFFu;
       wbase[w] = tot;
-      tot += wcnt[w];
+      tot += c;
       a0 += wstat[w];
       a1 += wstat[W + w];
       a2 += wstat[2 * W + w];
@@ -333,6 +409,7 @@ __global__ void __launch_bounds__(256) interp_kernel(const InterpParams p) {
     if (a0) atomicAdd(&p.ctr->iv_instr, a0);
     if (a1) atomicAdd(&p.ctr->iv_loads, a1);
     if (a2) atomicAdd(&p.ctr->iv_stores, a2);
+    if (wait_any) p.ctr->any_waiting = 1;
   }
   __syncthreads();
   const unsigned long long base = wbase[warp];
@@ -345,36 +422,36 @@ __global__ void __launch_bounds__(256) interp_kernel(const InterpParams p) {
   }
 }
 
-int interp_threads(uint32_t n_regs) {
-  // keep the per-block shared memory within ~96 KB so >= 2 blocks fit per SM
-  for (int T = 256; T >= 32; T >>= 1)
-    if (interp_smem_bytes(n_regs, T) <= 96 * 1024) return T;
-  return 32;
-}
-
-size_t interp_smem_bytes(uint32_t n_regs, int T) {
+size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem) {
   const int W = T / 32;
-  size_t b = (size_t)W * STAGE * (8 + 4);         // staging
-  b += (size_t)n_regs * T * 4;                     // registers
-  b += (size_t)OVL_CAP * T * 8;                    // overlay
-  b += 2 * 256 * 4;                                // array offsets / sizes
-  b += (size_t)W * 4 + 8;                          // warp counts (+align)
+  size_t b = (size_t)W * p.stage * (8 + 4);        // staging
+  b += code_in_smem ? (size_t)p.n_instr * 8 : 0;   // program
+  b += (size_t)p.n_regs * T * 4;                   // registers
+  b += (size_t)p.ovl_cap * T * 8;                  // overlay
+  b += (size_t)p.n_arrays * 8;                     // array offsets / sizes
+  b += (size_t)W * 12 + 8;                         // warp counts, node range (+align)
   b += (size_t)W * 8 * 4;                          // warp bases + 3 stats
   return b;
 }
 
 cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
   if (p.n_lanes == 0) return cudaSuccess;
-  const int T = interp_threads(p.n_regs);
-  const size_t sm = interp_smem_bytes(p.n_regs, T);
-  static bool attr_set = false;  // per process; the attribute is per function
+  static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(interp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
+    for (auto f : {interp_kernel<true>, interp_kernel<false>}) {
+      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      if (e != cudaSuccess) return e;
+      cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
     attr_set = true;
   }
+  const bool code_smem = p.n_instr <= 2048;
+  int T = 256;
+  while (T > 32 && interp_smem_bytes(p, T, code_smem) > 96 * 1024) T >>= 1;
+  const size_t sm = interp_smem_bytes(p, T, code_smem);
   const uint32_t grid = (p.n_lanes + T - 1) / T;
-  interp_kernel<<<grid, T, sm, s>>>(p);
+  if (code_smem) interp_kernel<true><<<grid, T, sm, s>>>(p);
+  else interp_kernel<false><<<grid, T, sm, s>>>(p);
   launched();
   return cudaGetLastError();
 }

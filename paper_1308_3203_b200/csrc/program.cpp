@@ -25,6 +25,8 @@ int fail(int code, const char* fmt, ...) {
   return code;
 }
 
+void analyze(rc_program* P);
+
 static uint32_t rd32(const uint8_t* p) { uint32_t v; memcpy(&v, p, 4); return v; }
 static uint16_t rd16(const uint8_t* p) { uint16_t v; memcpy(&v, p, 2); return v; }
 
@@ -113,7 +115,165 @@ int validate(const uint8_t* bc, size_t nbytes, rc_program* P) {
   P->n_arrays = n_arrays;
   P->n_instr = n_instr;
   P->code = std::move(code);
+  analyze(P);
   return RC_OK;
+}
+
+// ---- static analysis used to size the interpreter (no semantic effect) ------
+//
+// (1) Registers live across a barrier: a work-item suspended at BAR b resumes
+//     at b+1 in the next interval (a new kernel launch), so only registers in
+//     live_in(b+1) — possibly read before redefined — must be saved / reloaded;
+//     interval 0 starts at pc 0 with all registers 0 (reading L18), so
+//     live_in(0) is loaded too (from the zeroed buffer).
+// (2) Bound on distinct cells one work-item writes in one interval: the max
+//     number of ST executions on a barrier-free path (unbounded if a
+//     barrier-free cycle contains a ST).  Sizes the own-write overlay.
+// (3) Bound on log records per work-item per interval (LD executions + (2)),
+//     sizing the per-warp staging buffer (overflow is handled either way).
+static void successors(const Ins& I, uint32_t pc, uint32_t n_instr, uint32_t* s, int* ns) {
+  *ns = 0;
+  if (I.op == RC_OP_EXIT) return;
+  if (I.op == RC_OP_BR) { s[(*ns)++] = (uint32_t)I.imm; s[(*ns)++] = (uint32_t)I.b + 256u * I.c; return; }
+  if (I.op == RC_OP_JMP) { s[(*ns)++] = (uint32_t)I.imm; return; }
+  if (pc + 1 < n_instr) s[(*ns)++] = pc + 1;
+}
+
+static void uses_defs(const Ins& I, int* use, int* nu, int* def) {
+  *nu = 0;
+  *def = -1;
+  const char* k = operand_kinds(I.op);
+  switch (I.op) {
+    case RC_OP_ST: use[(*nu)++] = I.b; use[(*nu)++] = I.c; return;
+    case RC_OP_LD: use[(*nu)++] = I.c; *def = I.a; return;
+    case RC_OP_ASSUME: case RC_OP_ASSERT: case RC_OP_BR: use[(*nu)++] = I.a; return;
+    case RC_OP_BAR: case RC_OP_JMP: case RC_OP_EXIT: return;
+    default: break;
+  }
+  *def = I.a;  // every remaining opcode writes register a
+  if (k[1] == 'r') use[(*nu)++] = I.b;
+  if (k[2] == 'r') use[(*nu)++] = I.c;
+}
+
+// Longest barrier-free path weight from any interval entry (pc 0 or BAR+1);
+// -1 = unbounded.  Tarjan SCCs of the barrier-free CFG (edges out of BAR and
+// EXIT removed): a cyclic SCC with positive weight is unbounded, otherwise DP
+// over the condensation (Tarjan emits SCCs in reverse topological order).
+static int64_t max_path_weight(const rc_program* P, const std::vector<int>& w) {
+  const uint32_t N = P->n_instr;
+  auto succ = [&](uint32_t pc, uint32_t* s, int* ns) {
+    successors(P->code[pc], pc, N, s, ns);
+    if (P->code[pc].op == RC_OP_BAR) *ns = 0;
+  };
+  std::vector<int64_t> index(N, -1), low(N, 0), comp(N, -1);
+  std::vector<uint8_t> on(N, 0);
+  std::vector<uint32_t> stk;
+  std::vector<int64_t> comp_best;
+  int64_t idx = 0;
+  bool unbounded = false;
+  for (uint32_t root = 0; root < N; root++) {
+    if (index[root] >= 0) continue;
+    std::vector<std::pair<uint32_t, int>> call{{root, 0}};
+    index[root] = low[root] = idx++;
+    stk.push_back(root);
+    on[root] = 1;
+    while (!call.empty()) {
+      uint32_t pc = call.back().first;
+      int& i = call.back().second;
+      uint32_t s[2];
+      int ns;
+      succ(pc, s, &ns);
+      if (i < ns) {
+        uint32_t q = s[i++];
+        if (index[q] < 0) {
+          index[q] = low[q] = idx++;
+          stk.push_back(q);
+          on[q] = 1;
+          call.push_back({q, 0});
+        } else if (on[q]) {
+          low[pc] = std::min(low[pc], index[q]);
+        }
+        continue;
+      }
+      if (low[pc] == index[pc]) {  // pc roots an SCC; successors' SCCs are complete
+        const int64_t c = (int64_t)comp_best.size();
+        std::vector<uint32_t> members;
+        uint32_t x;
+        do {
+          x = stk.back();
+          stk.pop_back();
+          on[x] = 0;
+          comp[x] = c;
+          members.push_back(x);
+        } while (x != pc);
+        int64_t weight = 0, out = 0;
+        bool cyclic = members.size() > 1;
+        for (uint32_t m : members) {
+          weight += w[m];
+          uint32_t s2[2];
+          int n2;
+          succ(m, s2, &n2);
+          for (int j = 0; j < n2; j++) {
+            if (s2[j] == m) cyclic = true;
+            if (comp[s2[j]] != c && comp[s2[j]] >= 0) out = std::max(out, comp_best[comp[s2[j]]]);
+          }
+        }
+        if (cyclic && weight > 0) unbounded = true;
+        comp_best.push_back(weight + out);
+      }
+      call.pop_back();
+      if (!call.empty()) low[call.back().first] = std::min(low[call.back().first], low[pc]);
+    }
+  }
+  if (unbounded) return -1;
+  int64_t m = comp_best[comp[0]];
+  for (uint32_t pc = 0; pc + 1 < N; pc++)
+    if (P->code[pc].op == RC_OP_BAR) m = std::max(m, comp_best[comp[pc + 1]]);
+  return m;
+}
+
+void analyze(rc_program* P) {
+  const uint32_t N = P->n_instr, R = P->n_regs;
+  // (1) liveness: live_in[pc] as bitsets over registers
+  const uint32_t words = (R + 63) / 64;
+  std::vector<uint64_t> live(N * (size_t)words, 0);
+  bool changed = true;
+  while (changed) {
+    changed = false;
+    for (int64_t pc = N - 1; pc >= 0; pc--) {
+      const Ins& I = P->code[pc];
+      uint32_t s[2];
+      int ns;
+      successors(I, (uint32_t)pc, N, s, &ns);
+      std::vector<uint64_t> v(words, 0);
+      for (int j = 0; j < ns; j++)
+        for (uint32_t k = 0; k < words; k++) v[k] |= live[s[j] * (size_t)words + k];
+      int use[3], nu, def;
+      uses_defs(I, use, &nu, &def);
+      if (def >= 0) v[def / 64] &= ~(1ull << (def % 64));
+      for (int j = 0; j < nu; j++) v[use[j] / 64] |= 1ull << (use[j] % 64);
+      for (uint32_t k = 0; k < words; k++)
+        if (v[k] != live[pc * (size_t)words + k]) { live[pc * (size_t)words + k] = v[k]; changed = true; }
+    }
+  }
+  std::vector<uint64_t> keep(words, 0);
+  for (uint32_t k = 0; k < words; k++) keep[k] = live[k];  // live_in(0)
+  for (uint32_t pc = 0; pc + 1 < N; pc++)
+    if (P->code[pc].op == RC_OP_BAR)
+      for (uint32_t k = 0; k < words; k++) keep[k] |= live[(pc + 1) * (size_t)words + k];
+  P->live_regs.clear();
+  for (uint32_t r = 0; r < R; r++)
+    if (keep[r / 64] >> (r % 64) & 1) P->live_regs.push_back((uint8_t)r);
+  // (2)/(3) per-interval bounds
+  std::vector<int> wst(N, 0), wrec(N, 0);
+  for (uint32_t pc = 0; pc < N; pc++) {
+    wst[pc] = P->code[pc].op == RC_OP_ST;
+    wrec[pc] = P->code[pc].op == RC_OP_ST || P->code[pc].op == RC_OP_LD;
+  }
+  const int64_t st = max_path_weight(P, wst);
+  const int64_t rec = max_path_weight(P, wrec);
+  P->ovl_cap = (st < 0 || st > OVL_CAP) ? OVL_CAP : (int)std::max<int64_t>(st, 1);
+  P->rec_bound = (rec < 0 || rec > 1024) ? -1 : (int)rec;
 }
 
 }  // namespace rc

@@ -34,9 +34,12 @@ enum LaneStatus : uint8_t {
   L_ASSERT = 5,
   L_DIV0 = 6,
   L_FUEL = 7,
+  L_EXITED_NOW = 8,  // reached EXIT in the interval just interpreted (arrived at the exit node)
 };
-constexpr int32_t NODE_NONE = -2;  // lane did not arrive in this interval
-constexpr int32_t NODE_EXIT = -1;  // arrived at the exit node
+// Arrival node of a work-item in the interval just run (reading L9): the pc of
+// its BAR (= pc_out - 1 for L_WAITING), NODE_EXIT for L_EXITED_NOW.
+constexpr int32_t NODE_NONE = -2;
+constexpr int32_t NODE_EXIT = -1;
 constexpr uint32_t NOTID = 0xFFFFFFFFu;
 constexpr int OVL_CAP = 16;        // own-write overlay entries per work-item (smem)
 
@@ -52,7 +55,7 @@ struct DevCounters {
   unsigned int log_overflow;        // per attempt
   unsigned int ovl_overflow;        // per attempt
   unsigned int any_waiting;         // per interval
-  unsigned int pad;
+  unsigned int diverged;            // per interval
   unsigned long long lanes_final[8];
 };
 
@@ -76,7 +79,12 @@ struct InterpParams {
   int32_t* regs_out;
   uint32_t* pc_out;
   uint8_t* status_out;
-  int32_t* node_out;          // arrival node this interval
+  const uint8_t* live;        // registers saved / restored across barriers
+  uint32_t n_live;
+  uint32_t ovl_cap;           // own-write overlay entries per work-item (static bound)
+  uint32_t stage;             // staged records per warp
+  int32_t* node_min;          // [I_b] min / max arrival node (fused A4)
+  int32_t* node_max;
   // log
   uint32_t* log_keys;         // cell
   uint64_t* log_vals;         // value << 32 | tid << 1 | is_write
@@ -100,8 +108,7 @@ struct DetectParams {
 };
 
 // ---- launchers (defined in the .cu files) --------------------------------
-size_t interp_smem_bytes(uint32_t n_regs, int threads);
-int interp_threads(uint32_t n_regs);
+size_t interp_smem_bytes(const InterpParams& p, int threads, bool code_in_smem);
 cudaError_t launch_interp(const InterpParams& p, cudaStream_t s);
 
 struct SortWorkspace {
@@ -146,16 +153,21 @@ cudaError_t launch_detect(const DetectParams& p, cudaStream_t s);
 
 struct BoundaryParams {
   uint32_t n, n_lanes, n_inst, interval, inst_base;
-  const uint8_t* status;
-  const int32_t* node;
-  uint32_t* first_tid;   // [n_inst]
-  uint32_t* second_tid;  // [n_inst]
-  uint32_t* inst_waiting;// [n_inst]
+  const uint8_t* status;   // status_out of the interval just run
+  const uint32_t* pc;      // pc_out of the interval just run
+  int32_t* node_min;       // [n_inst] from K1
+  int32_t* node_max;
+  uint32_t* first_tid;     // [n_inst]
+  uint32_t* second_tid;    // [n_inst]
+  uint32_t* inst_flag;     // [n_inst] diverged / waiting
   rc_report* reports;
   unsigned long long report_cap;
   DevCounters* ctr;
 };
+// per instance: divergence check on K1's node range, reset of the range
 cudaError_t launch_boundary(const BoundaryParams& p, cudaStream_t s);
+// rare path: lane scans for the divergence report of flagged instances
+cudaError_t launch_divergence(const BoundaryParams& p, cudaStream_t s);
 cudaError_t launch_max_intervals(const BoundaryParams& p, cudaStream_t s);
 cudaError_t launch_lane_hist(const uint8_t* status, uint32_t n_lanes, DevCounters* ctr, cudaStream_t s);
 cudaError_t launch_init_lanes(uint8_t* status, uint32_t* pc, int32_t* regs, uint32_t n_regs,
@@ -169,6 +181,10 @@ struct rc_workspace;
 struct rc_program {
   uint32_t n_regs = 0, n_arrays = 0, n_instr = 0;
   std::vector<rc::Ins> code;
+  // static analysis (program.cpp analyze()): sizing only, no semantic effect
+  std::vector<uint8_t> live_regs;  // registers live across a barrier (+ live at pc 0)
+  int ovl_cap = rc::OVL_CAP;       // max distinct cells written per work-item per interval
+  int rec_bound = -1;              // max log records per work-item per interval (-1 unbounded)
   std::mutex mu;
   rc_workspace* ws = nullptr;
 };

@@ -97,17 +97,17 @@ struct DevBuf {
 struct rc_workspace {
   int device = -1;
   DevBuf code, arr_off, arr_size, heap;
-  DevBuf regs[2], pc[2], status[2], node;
+  DevBuf regs[2], pc[2], status[2], live;
   DevBuf log_keys, log_vals, keys_alt, vals_alt, sort_status, sort_small;
   DevBuf reports, reports_scratch;
-  DevBuf inst_tmp;  // first_tid | second_tid | inst_waiting
+  DevBuf inst_tmp;  // node_min | node_max | first_tid | second_tid | inst_flag  ([I_b] each)
   DevBuf ctr;
   DevCounters* h_ctr = nullptr;  // pinned
   SortWorkspace sort;
   Profiler prof;
   ~rc_workspace() {
     for (DevBuf* b : {&code, &arr_off, &arr_size, &heap, &regs[0], &regs[1], &pc[0], &pc[1], &status[0],
-                      &status[1], &node, &log_keys, &log_vals, &keys_alt, &vals_alt, &sort_status,
+                      &status[1], &live, &log_keys, &log_vals, &keys_alt, &vals_alt, &sort_status,
                       &sort_small, &reports, &reports_scratch, &inst_tmp, &ctr})
       b->release();
     if (h_ctr) cudaFreeHost(h_ctr);
@@ -247,6 +247,9 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     rc_workspace& W = *P->ws;
     CK(W.code.ensure(P->code.size() * sizeof(Ins)));
     CK(cudaMemcpy(W.code.p, P->code.data(), P->code.size() * sizeof(Ins), cudaMemcpyHostToDevice));
+    CK(W.live.ensure(std::max<size_t>(1, P->live_regs.size())));
+    if (!P->live_regs.empty())
+      CK(cudaMemcpy(W.live.p, P->live_regs.data(), P->live_regs.size(), cudaMemcpyHostToDevice));
     CK(W.ctr.ensure(sizeof(DevCounters)));
     CK(cudaMallocHost(&W.h_ctr, sizeof(DevCounters)));
     CK(W.sort_small.ensure(4096 * 4));
@@ -286,8 +289,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       CK(W.pc[b].ensure(std::max<uint64_t>(1, L_max) * 4));
       CK(W.status[b].ensure(std::max<uint64_t>(1, L_max)));
     }
-    CK(W.node.ensure(std::max<uint64_t>(1, L_max) * 4));
-    CK(W.inst_tmp.ensure((uint64_t)I_b * 12));
+    CK(W.inst_tmp.ensure((uint64_t)I_b * 20));
   }
   uint64_t log_cap = W.log_keys.bytes / 4;
   {
@@ -352,6 +354,30 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
                            host_io ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
     }
     W.prof.end(RC_PROF_COPY, s, (uint64_t)nb * cpi * 8, (uint64_t)nb * cpi);
+    int32_t* node_min = W.inst_tmp.as<int32_t>();
+    int32_t* node_max = node_min + I_b;
+    uint32_t* first_tid = reinterpret_cast<uint32_t*>(node_max + I_b);
+    uint32_t* second_tid = first_tid + I_b;
+    uint32_t* inst_flag = second_tid + I_b;
+    CK(cudaMemsetAsync(node_min, 0x7F, (size_t)nb * 4, s));  // large positive: "no arrival"
+    CK(cudaMemsetAsync(node_max, 0x80, (size_t)nb * 4, s));  // large negative
+    auto bparams = [&](uint32_t interval) {
+      BoundaryParams bp;
+      bp.n = n;
+      bp.n_lanes = L;
+      bp.n_inst = nb;
+      bp.interval = interval;
+      bp.inst_base = inst_base;
+      bp.node_min = node_min;
+      bp.node_max = node_max;
+      bp.first_tid = first_tid;
+      bp.second_tid = second_tid;
+      bp.inst_flag = inst_flag;
+      bp.reports = W.reports.as<rc_report>();
+      bp.report_cap = rep_cap;
+      bp.ctr = dctr;
+      return bp;
+    };
     int cur = 0;
     if (L) {
       CK(cudaMemsetAsync(W.status[cur].p, 0, L, s));
@@ -385,7 +411,12 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         ip.regs_out = W.regs[cur ^ 1].as<int32_t>();
         ip.pc_out = W.pc[cur ^ 1].as<uint32_t>();
         ip.status_out = W.status[cur ^ 1].as<uint8_t>();
-        ip.node_out = W.node.as<int32_t>();
+        ip.live = W.live.as<uint8_t>();
+        ip.n_live = (uint32_t)P->live_regs.size();
+        ip.ovl_cap = (uint32_t)P->ovl_cap;
+        ip.stage = P->rec_bound > 0 ? (uint32_t)std::min(256, ((32 * P->rec_bound + 31) / 32) * 32) : 256u;
+        ip.node_min = node_min;
+        ip.node_max = node_max;
         ip.log_keys = W.log_keys.as<uint32_t>();
         ip.log_vals = W.log_vals.as<uint64_t>();
         ip.log_cap = log_cap;
@@ -400,7 +431,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
           return fail(RC_ELIMIT,
                       "a work-item wrote more than %d distinct cells in one barrier interval (instance batch at "
                       "%u, interval %u)",
-                      OVL_CAP, inst_base, k);
+                      P->ovl_cap, inst_base, k);
         const bool log_over = W.h_ctr->log_overflow || W.h_ctr->log_count > log_cap;
         const bool rep_over = W.h_ctr->report_count > rep_cap;
         if (!log_over && !rep_over) break;
@@ -434,6 +465,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
 
       // ---------------- K4+K5 and A4 (idempotent: re-run if the report buffer overflows)
       const uint64_t rep_after_k1 = rep_count;
+      bool checked = false, diverged = false;
       for (;;) {
         DetectParams dp;
         dp.keys = sk;
@@ -451,31 +483,28 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         W.prof.begin(s);
         CK(launch_detect(dp, s));
         W.prof.end(RC_PROF_DETECT, s, N * 12, N);
-        BoundaryParams bp;
-        bp.n = n;
-        bp.n_lanes = L;
-        bp.n_inst = nb;
-        bp.interval = k;
-        bp.inst_base = inst_base;
+        BoundaryParams bp = bparams(k);
         bp.status = W.status[cur ^ 1].as<uint8_t>();
-        bp.node = W.node.as<int32_t>();
-        bp.first_tid = W.inst_tmp.as<uint32_t>();
-        bp.second_tid = bp.first_tid + I_b;
-        bp.inst_waiting = bp.second_tid + I_b;
-        bp.reports = W.reports.as<rc_report>();
-        bp.report_cap = rep_cap;
-        bp.ctr = dctr;
-        CK(cudaMemsetAsync(&dctr->any_waiting, 0, 4, s));
-        W.prof.begin(s);
-        CK(launch_boundary(bp, s));
-        W.prof.end(RC_PROF_BOUNDARY, s, (uint64_t)L * 10, L);
-        CK(read_ctr());
+        bp.pc = W.pc[cur ^ 1].as<uint32_t>();
+        if (!checked) {  // consumes (and resets) K1's per-instance node ranges: once per interval
+          W.prof.begin(s);
+          CK(launch_boundary(bp, s));
+          W.prof.end(RC_PROF_BOUNDARY, s, (uint64_t)nb * 12, nb);
+          CK(read_ctr());
+          checked = true;
+          diverged = W.h_ctr->diverged != 0;
+        }
+        if (diverged) {  // rare path: lane scans for the divergence report (idempotent)
+          CK(launch_divergence(bp, s));
+        }
+        if (diverged || W.h_ctr->report_count > rep_cap) CK(read_ctr());
         if (W.h_ctr->report_count <= rep_cap) {
           rep_count = W.h_ctr->report_count;
           break;
         }
         CK(grow_reports(W.h_ctr->report_count));
         CK(set_report_count(rep_after_k1));
+        W.h_ctr->report_count = 0;  // force a fresh read after the re-run
       }
       cur ^= 1;  // the interval's lane state becomes current
       const bool any_waiting = W.h_ctr->any_waiting != 0;
@@ -483,15 +512,9 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       k++;
       if (k >= opt.max_intervals) {  // instance-level FUEL (reading L17)
         for (;;) {
-          BoundaryParams bp;
-          memset(&bp, 0, sizeof bp);
-          bp.n_inst = nb;
-          bp.interval = k;
-          bp.inst_base = inst_base;
-          bp.inst_waiting = W.inst_tmp.as<uint32_t>() + 2 * (size_t)I_b;
-          bp.reports = W.reports.as<rc_report>();
-          bp.report_cap = rep_cap;
-          bp.ctr = dctr;
+          BoundaryParams bp = bparams(k);
+          bp.status = W.status[cur].as<uint8_t>();
+          bp.pc = W.pc[cur].as<uint32_t>();
           CK(launch_max_intervals(bp, s));
           CK(read_ctr());
           if (W.h_ctr->report_count <= rep_cap) break;

@@ -131,7 +131,7 @@ struct SortSmem {
   unsigned long long mbar;
 };
 
-__global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
+__global__ void __launch_bounds__(SORT_THREADS, 3) onesweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint64_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint64_t* __restrict__ vals_out, uint32_t n, int shift, const uint32_t* __restrict__ bin_off,
     unsigned long long* __restrict__ status, uint32_t* __restrict__ tile_ctr, uint32_t epoch) {
@@ -190,11 +190,19 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
   uint64_t v[SORT_ITEMS];
   uint32_t rk[SORT_ITEMS];  // digit << 16 | rank within the warp
 #pragma unroll
+  for (int j = 0; j < SORT_ITEMS; j++) {  // batch the shared-memory loads (ILP)
+    const uint32_t idx = w * WARP_ITEMS + j * 32 + lane;
+    k[j] = idx < cnt ? S.keys[idx] : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < SORT_ITEMS; j++) {
+    const uint32_t idx = w * WARP_ITEMS + j * 32 + lane;
+    v[j] = idx < cnt ? S.vals[idx] : 0ull;
+  }
+#pragma unroll
   for (int j = 0; j < SORT_ITEMS; j++) {
     const uint32_t idx = w * WARP_ITEMS + j * 32 + lane;
     const bool valid = idx < cnt;
-    k[j] = valid ? S.keys[idx] : 0u;
-    v[j] = valid ? S.vals[idx] : 0ull;
     const uint32_t d = valid ? (k[j] >> shift) & 0xFF : 0x100u;
     const unsigned peers = __match_any_sync(FULL, d);
     uint32_t prev = 0;
@@ -249,11 +257,23 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
   __syncthreads();
 
   // ---- coalesced write-out: sorted position i goes to glob_base[digit] + i
-  for (uint32_t i = t; i < cnt; i += SORT_THREADS) {
-    const uint32_t kk = S.keys[i];
-    const uint32_t o = S.glob_base[(kk >> shift) & 0xFF] + i;
-    keys_out[o] = kk;
-    vals_out[o] = S.vals[i];
+  if (cnt == SORT_TILE) {
+    uint32_t o[SORT_ITEMS];
+#pragma unroll
+    for (int j = 0; j < SORT_ITEMS; j++) k[j] = S.keys[t + j * SORT_THREADS];
+#pragma unroll
+    for (int j = 0; j < SORT_ITEMS; j++) o[j] = S.glob_base[(k[j] >> shift) & 0xFF] + t + j * SORT_THREADS;
+#pragma unroll
+    for (int j = 0; j < SORT_ITEMS; j++) keys_out[o[j]] = k[j];
+#pragma unroll
+    for (int j = 0; j < SORT_ITEMS; j++) vals_out[o[j]] = S.vals[t + j * SORT_THREADS];
+  } else {
+    for (uint32_t i = t; i < cnt; i += SORT_THREADS) {
+      const uint32_t kk = S.keys[i];
+      const uint32_t o = S.glob_base[(kk >> shift) & 0xFF] + i;
+      keys_out[o] = kk;
+      vals_out[o] = S.vals[i];
+    }
   }
 }
 
@@ -269,6 +289,7 @@ cudaError_t onesweep_sort(uint32_t* keys, uint64_t* vals, uint32_t n, int bits, 
     cudaError_t e = cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sizeof(SortSmem));
     if (e != cudaSuccess) return e;
+    cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr_set = true;
   }
   static int nsm = 0;
