@@ -231,13 +231,23 @@ __global__ void __launch_bounds__(SORT_THREADS, 3) onesweep_kernel(
   S.tile_excl[d] = excl_tile;
   unsigned long long excl = 0;
   if (tile > 0) {
+    // look back LB predecessors per L2 round trip (the walk is latency-bound)
+    constexpr int LB = 8;
     int64_t tp = (int64_t)tile - 1;
-    for (;;) {
-      const unsigned long long s = ld_relaxed(status + (size_t)tp * RADIX + d);
-      if (((s >> 40) & 0x3FFFFF) != (epoch & 0x3FFFFF) || (s >> 62) == 0) continue;  // not ready yet
-      excl += s & VAL_MASK;
-      if ((s >> 62) == 2) break;
-      tp--;
+    bool done = false;
+    while (!done) {
+      unsigned long long s[LB];
+#pragma unroll
+      for (int j = 0; j < LB; j++) s[j] = tp - j >= 0 ? ld_relaxed(status + (size_t)(tp - j) * RADIX + d) : 0ull;
+#pragma unroll
+      for (int j = 0; j < LB; j++) {
+        if (done) break;
+        const bool ready = ((s[j] >> 40) & 0x3FFFFF) == (epoch & 0x3FFFFF) && (s[j] >> 62) != 0;
+        if (!ready) break;  // re-poll from this predecessor
+        excl += s[j] & VAL_MASK;
+        tp--;
+        if ((s[j] >> 62) == 2) done = true;
+      }
     }
     st_relaxed(my_status, FLAG_INC | ep | (excl + tile_cnt));
   }
