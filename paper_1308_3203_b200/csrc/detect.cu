@@ -129,68 +129,137 @@ __device__ __forceinline__ void serial_segment(const DetectParams& p, uint32_t i
 }
 }  // namespace
 
-constexpr uint32_t DET_ROUNDS = 8;  // 32-record rounds per warp
+constexpr uint32_t DET_ROUNDS = 16;  // 32-record rounds per warp
 constexpr uint32_t DET_CHUNK = 32 * DET_ROUNDS;
 
-// Warp-cooperative detection: a warp owns DET_CHUNK consecutive records and
-// reads them 32 at a time (coalesced).  __match_any_sync groups the lanes of
-// one cell; a cell whose whole segment lies in the round is reduced with
-// redux.sync / ballot / shfl over its group mask (groups run their collectives
-// concurrently, each with its own mask); a segment that starts in the round
-// but continues past it goes to serial_segment on its head lane; records of a
-// segment that started earlier belong to that segment's head.
+// Associative per-segment summary.  A cell is SIMPLE when it has at most one
+// writer and no reader other than that writer: it can produce no report and
+// only its commit is needed.  Everything else (>= 2 writers, or a reader that
+// is not the writer) is COMPLEX and goes to serial_segment (reports).
+struct Seg {
+  uint32_t rmin, rmax;  // reader tids (rmin = INF: no reader)
+  uint32_t w;           // a writer tid (the only one when nw == 1)
+  int32_t vw;           // its value
+  uint32_t nw;          // writers, saturating at 2
+};
+__device__ __forceinline__ Seg seg_merge(const Seg& a, const Seg& b) {
+  Seg r;
+  r.rmin = min(a.rmin, b.rmin);
+  r.rmax = max(a.rmax, b.rmax);
+  r.nw = min(2u, a.nw + b.nw);
+  r.w = a.nw ? a.w : b.w;
+  r.vw = a.nw ? a.vw : b.vw;
+  return r;
+}
+__device__ __forceinline__ bool seg_complex(const Seg& s) {
+  return s.nw >= 2 || (s.nw == 1 && s.rmin != INF && (s.rmin != s.w || s.rmax != s.w));
+}
+__device__ __forceinline__ Seg seg_shfl_down(const Seg& a, int off) {
+  const unsigned FULL = 0xFFFFFFFFu;
+  Seg r;
+  r.rmin = __shfl_down_sync(FULL, a.rmin, off);
+  r.rmax = __shfl_down_sync(FULL, a.rmax, off);
+  r.w = __shfl_down_sync(FULL, a.w, off);
+  r.vw = __shfl_down_sync(FULL, a.vw, off);
+  r.nw = __shfl_down_sync(FULL, a.nw, off);
+  return r;
+}
+__device__ __forceinline__ Seg seg_shfl(const Seg& a, int src) {
+  const unsigned FULL = 0xFFFFFFFFu;
+  Seg r;
+  r.rmin = __shfl_sync(FULL, a.rmin, src);
+  r.rmax = __shfl_sync(FULL, a.rmax, src);
+  r.w = __shfl_sync(FULL, a.w, src);
+  r.vw = __shfl_sync(FULL, a.vw, src);
+  r.nw = __shfl_sync(FULL, a.nw, src);
+  return r;
+}
+
+// Warp-cooperative detection.  A warp owns DET_CHUNK consecutive sorted
+// records and streams them 32 at a time (coalesced loads).  Segment heads /
+// tails come from comparing neighbouring keys (shuffles + one boundary load);
+// each lane's suffix summary over its segment is built by a segmented
+// shuffle reduction (log2(longest segment in the round) steps).  A segment
+// that crosses a round boundary is carried (warp-uniform state) into the next
+// round; one that crosses the chunk end, and every COMPLEX cell, is handled by
+// serial_segment from the segment's head.  Segments that start before the
+// chunk belong to the previous warp.
 __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
   const unsigned FULL = 0xFFFFFFFFu;
-  const uint32_t lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   const uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t c0 = wg * DET_CHUNK;
   if (c0 >= p.n_records) return;  // whole warp
   const uint64_t c1 = min((uint64_t)p.n_records, c0 + DET_CHUNK);
+  const Seg ident{INF, 0u, 0u, 0, 0u};
+  bool carry = false;       // an open segment started in an earlier round of this chunk
+  uint64_t carry_start = 0;
+  Seg cs = ident;
   for (uint64_t b = c0; b < c1; b += 32) {
     const uint64_t r = b + lane;
     const bool inb = r < c1;
-    const uint32_t key = inb ? __ldg(p.keys + r) : 0xFFFFFFFFu;  // cell ids are < 0xFFFFFFFF
+    const uint32_t key = inb ? __ldg(p.keys + r) : 0xFFFFFFFFu;
     const uint64_t v = inb ? __ldg(p.vals + r) : 0ull;
     uint32_t prev = __shfl_up_sync(FULL, key, 1);
     if (lane == 0) prev = b > 0 ? __ldg(p.keys + b - 1) : ~key;
     uint32_t next = __shfl_down_sync(FULL, key, 1);
     if (lane == 31) next = r + 1 < p.n_records ? __ldg(p.keys + r + 1) : ~key;
     const bool head = inb && prev != key;
-    const bool tail = inb && next != key;
-    const unsigned peers = __match_any_sync(FULL, key);
-    const int lo = __ffs(peers) - 1, hi = 31 - __clz(peers);
-    const bool lo_head = __shfl_sync(FULL, head, lo);
-    const bool hi_tail = __shfl_sync(FULL, tail, hi);
-    if (head && !hi_tail) serial_segment(p, (uint32_t)r);  // segment continues past this round
-    if (!(inb && lo_head && hi_tail)) continue;             // not a complete segment of this round
+    const bool tail = inb && next != key;  // last record of its segment (possibly beyond c1)
+    const unsigned heads = __ballot_sync(FULL, head);
+    const unsigned tails = __ballot_sync(FULL, tail);
+    const unsigned inbm = __ballot_sync(FULL, inb);
+    // hi = last lane of my segment inside this round
+    const unsigned t_at_or_after = tails & (~0u << lane);
+    const int last_inb = 31 - __clz(inbm);
+    const int hi = t_at_or_after ? __ffs(t_at_or_after) - 1 : last_inb;
+    const bool closes = (tails >> hi) & 1;  // segment ends inside this round
+    // per-record summary, then segmented suffix reduction over [lane, hi]
     const uint32_t tid = (uint32_t)v >> 1;
-    const bool isw = (v & 1) != 0;
-    const int32_t val = (int32_t)(v >> 32);
-    const uint32_t wmaxp1 = __reduce_max_sync(peers, isw ? tid + 1 : 0u);
-    if (wmaxp1 == 0) continue;  // only reads: no conflict, nothing to commit
-    const uint32_t r1 = __reduce_min_sync(peers, isw ? INF : tid);
-    const uint32_t r2 = __reduce_min_sync(peers, (!isw && tid != r1) ? tid : INF);
-    const uint32_t rmaxp1 = __reduce_max_sync(peers, isw ? 0u : tid + 1);
-    const uint32_t w1 = __reduce_min_sync(peers, isw ? tid : INF);
-    const uint32_t w2 = __reduce_min_sync(peers, (isw && tid != w1) ? tid : INF);
-    const uint32_t wmax = wmaxp1 - 1;
-    const unsigned wmask = __ballot_sync(peers, isw);
-    const int32_t vw1 = __shfl_sync(peers, val, __ffs(__ballot_sync(peers, isw && tid == w1)) - 1);
-    const int32_t vwmax = __shfl_sync(peers, val, __ffs(__ballot_sync(peers, isw && tid == wmax)) - 1);
-    uint32_t t1, t2;
-    rw_pair(rmaxp1 != 0, r1, r2, rmaxp1 - 1, w1, w2, wmax, &t1, &t2);
-    const uint32_t nb = __reduce_min_sync(peers, (isw && val != vw1) ? tid : INF);
-    const bool t1r = __ballot_sync(peers, !isw && tid == t1) != 0;
-    const bool t2r = __ballot_sync(peers, !isw && tid == t2) != 0;
-    const bool t2w = __ballot_sync(peers, isw && tid == t2) != 0;
-    const bool w1r = __ballot_sync(peers, !isw && tid == w1) != 0;
-    const bool w2r = __ballot_sync(peers, !isw && tid == w2) != 0;
-    const bool nbr = __ballot_sync(peers, !isw && tid == nb) != 0;
-    if ((int)lane == lo) {
-      p.heap[key] = vwmax;  // barrier release: max-tid writer wins
-      finish_cell(p, key, w1, w2, __popc(wmask), t1, t2, nb, t1r, t2r, t2w, w1r, w2r, nbr);
+    Seg S = ident;
+    if (inb) {
+      if (v & 1) { S.w = tid; S.vw = (int32_t)(v >> 32); S.nw = 1; }
+      else { S.rmin = tid; S.rmax = tid; }
+    }
+    const bool starter = head || lane == 0;  // lanes whose suffix summary is consumed
+    const uint32_t len = (starter && inb) ? (uint32_t)(hi - lane + 1) : 1u;
+    const uint32_t maxlen = __reduce_max_sync(FULL, len);
+    for (uint32_t off = 1; off < maxlen; off <<= 1) {
+      const Seg T = seg_shfl_down(S, (int)off);
+      if (lane + (int)off <= hi) S = seg_merge(S, T);
+    }
+    // lane 0's segment: continues the carried one, or belongs to the previous warp
+    const Seg S0 = seg_shfl(S, 0);
+    const bool l0_head = heads & 1u;
+    const bool l0_closes = __shfl_sync(FULL, closes, 0);
+    if (!l0_head && carry) {
+      const Seg M = seg_merge(cs, S0);
+      if (l0_closes) {
+        if (lane == 0) {
+          if (seg_complex(M)) serial_segment(p, (uint32_t)carry_start);
+          else if (M.nw == 1) p.heap[__ldg(p.keys + carry_start)] = M.vw;
+        }
+        carry = false;
+      } else {
+        cs = M;  // the whole round continues the carried segment
+      }
+    }
+    // segments starting in this round
+    if (head && closes) {
+      if (seg_complex(S)) serial_segment(p, (uint32_t)r);
+      else if (S.nw == 1) p.heap[key] = S.vw;
+    }
+    // the last segment of the round stays open: carry it
+    const bool opens = head && !closes;
+    const unsigned om = __ballot_sync(FULL, opens);
+    if (om) {
+      const int h = __ffs(om) - 1;
+      cs = seg_shfl(S, h);
+      carry_start = b + h;
+      carry = true;
     }
   }
+  if (carry && lane == 0) serial_segment(p, (uint32_t)carry_start);  // continues into the next chunk
 }
 
 cudaError_t launch_detect(const DetectParams& p, cudaStream_t s) {

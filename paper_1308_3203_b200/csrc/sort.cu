@@ -120,170 +120,202 @@ __global__ void __launch_bounds__(256) bin_offsets_kernel(const uint32_t* __rest
 }
 
 // ---- K3: one onesweep digit pass -------------------------------------------
-struct SortSmem {
+// Persistent: a resident grid of blocks claims tiles in order from an atomic
+// counter; each block keeps two tile buffers and prefetches (TMA) the next
+// claimed tile while it ranks / looks back / scatters the current one.
+struct TileBuf {
   uint64_t vals[SORT_TILE];
   uint32_t keys[SORT_TILE];
+};
+struct SortSmem {
+  TileBuf buf[2];
   uint32_t whist[WARPS][RADIX];
   uint32_t tile_excl[RADIX];
   uint32_t glob_base[RADIX];
   uint32_t wt[WARPS];
-  uint32_t tile;
-  unsigned long long mbar;
+  uint32_t tile[2];
+  unsigned long long mbar[2];
 };
 
-__global__ void __launch_bounds__(SORT_THREADS, 3) onesweep_kernel(
+__device__ __forceinline__ void tile_fetch(TileBuf& B, unsigned long long* mbar, const uint32_t* keys_in,
+                                           const uint64_t* vals_in, uint64_t base, uint32_t cnt) {
+  // one elected thread: bulk copies of the 16-byte-aligned part (cnt & ~3 records)
+  const uint32_t c4 = cnt & ~3u;
+  const uint32_t bar = smem_u32(mbar);
+  const uint32_t bk = c4 * 4, bv = c4 * 8;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bk + bv) : "memory");
+  if (c4) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(B.keys)),
+                 "l"(keys_in + base), "r"(bk), "r"(bar)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(B.vals)),
+                 "l"(vals_in + base), "r"(bv), "r"(bar)
+                 : "memory");
+  }
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* mbar, uint32_t phase) {
+  const uint32_t bar = smem_u32(mbar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(phase)
+        : "memory");
+  }
+}
+
+__global__ void __launch_bounds__(SORT_THREADS, 2) onesweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint64_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint64_t* __restrict__ vals_out, uint32_t n, int shift, const uint32_t* __restrict__ bin_off,
     unsigned long long* __restrict__ status, uint32_t* __restrict__ tile_ctr, uint32_t epoch) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const uint32_t n_tiles = (uint32_t)((n + SORT_TILE - 1) / SORT_TILE);
+  const unsigned long long ep = (unsigned long long)(epoch & 0x3FFFFF) << 40;
 
-  for (int i = t; i < WARPS * RADIX; i += SORT_THREADS) (&S.whist[0][0])[i] = 0;
   if (t == 0) {
-    S.tile = atomicAdd(tile_ctr, 1u);
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar)));
+    for (int b = 0; b < 2; b++)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar[b])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t t0 = atomicAdd(tile_ctr, 1u);
+    S.tile[0] = t0;
+    if (t0 < n_tiles)
+      tile_fetch(S.buf[0], &S.mbar[0], keys_in, vals_in, (uint64_t)t0 * SORT_TILE,
+                 (uint32_t)umin64(SORT_TILE, n - (uint64_t)t0 * SORT_TILE));
   }
   __syncthreads();
-  const uint32_t tile = S.tile;
-  const uint64_t base = (uint64_t)tile * SORT_TILE;
-  const uint32_t cnt = (uint32_t)umin64(SORT_TILE, n - base);
-
-  // ---- stage the tile into shared memory
-  if (cnt == SORT_TILE) {
+  uint32_t phase = 0;  // bit b = expected parity of buffer b's mbarrier
+  int cur = 0;
+  for (;;) {
+    const uint32_t tile = S.tile[cur];
+    if (tile >= n_tiles) break;  // block-uniform
+    // claim and prefetch the next tile into the other buffer (freed by the
+    // __syncthreads that ended the previous iteration)
     if (t == 0) {
-      const uint32_t bar = smem_u32(&S.mbar);
-      const uint32_t bytes_k = SORT_TILE * 4, bytes_v = SORT_TILE * 8;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes_k + bytes_v)
-                   : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_u32(S.keys)),
-          "l"(keys_in + base), "r"(bytes_k), "r"(bar)
-          : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_u32(S.vals)),
-          "l"(vals_in + base), "r"(bytes_v), "r"(bar)
-          : "memory");
+      const uint32_t tn = atomicAdd(tile_ctr, 1u);
+      S.tile[cur ^ 1] = tn;
+      if (tn < n_tiles)
+        tile_fetch(S.buf[cur ^ 1], &S.mbar[cur ^ 1], keys_in, vals_in, (uint64_t)tn * SORT_TILE,
+                   (uint32_t)umin64(SORT_TILE, n - (uint64_t)tn * SORT_TILE));
     }
-    const uint32_t bar = smem_u32(&S.mbar);
-    uint32_t done = 0;
-    while (!done) {
-      asm volatile(
-          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n"
-          : "=r"(done)
-          : "r"(bar)
-          : "memory");
-    }
-  } else {
-    for (uint32_t i = t; i < cnt; i += SORT_THREADS) {
-      S.keys[i] = keys_in[base + i];
-      S.vals[i] = vals_in[base + i];
+    for (int i = t; i < WARPS * RADIX; i += SORT_THREADS) (&S.whist[0][0])[i] = 0;
+    const uint64_t base = (uint64_t)tile * SORT_TILE;
+    const uint32_t cnt = (uint32_t)umin64(SORT_TILE, n - base);
+    TileBuf& B = S.buf[cur];
+    mbar_wait(&S.mbar[cur], (phase >> cur) & 1u);
+    phase ^= 1u << cur;
+    for (uint32_t i = (cnt & ~3u) + t; i < cnt; i += SORT_THREADS) {  // unaligned tail of the last tile
+      B.keys[i] = keys_in[base + i];
+      B.vals[i] = vals_in[base + i];
     }
     __syncthreads();
-  }
 
-  // ---- stable in-tile ranking (warp w owns items [w*512, w*512+512), striped)
-  uint32_t k[SORT_ITEMS];
-  uint64_t v[SORT_ITEMS];
-  uint32_t rk[SORT_ITEMS];  // digit << 16 | rank within the warp
+    // ---- stable in-tile ranking (warp w owns items [w*512, w*512+512), striped)
+    uint32_t k[SORT_ITEMS];
+    uint64_t v[SORT_ITEMS];
+    uint32_t rk[SORT_ITEMS];  // digit << 16 | rank within the warp
 #pragma unroll
-  for (int j = 0; j < SORT_ITEMS; j++) {  // batch the shared-memory loads (ILP)
-    const uint32_t idx = w * WARP_ITEMS + j * 32 + lane;
-    k[j] = idx < cnt ? S.keys[idx] : 0u;
-  }
+    for (int j = 0; j < SORT_ITEMS; j++) {
+      const uint32_t idx = w * WARP_ITEMS + j * 32 + lane;
+      k[j] = idx < cnt ? B.keys[idx] : 0u;
+    }
 #pragma unroll
-  for (int j = 0; j < SORT_ITEMS; j++) {
-    const uint32_t idx = w * WARP_ITEMS + j * 32 + lane;
-    v[j] = idx < cnt ? S.vals[idx] : 0ull;
-  }
+    for (int j = 0; j < SORT_ITEMS; j++) {
+      const uint32_t idx = w * WARP_ITEMS + j * 32 + lane;
+      v[j] = idx < cnt ? B.vals[idx] : 0ull;
+    }
 #pragma unroll
-  for (int j = 0; j < SORT_ITEMS; j++) {
-    const uint32_t idx = w * WARP_ITEMS + j * 32 + lane;
-    const bool valid = idx < cnt;
-    const uint32_t d = valid ? (k[j] >> shift) & 0xFF : 0x100u;
-    const unsigned peers = __match_any_sync(FULL, d);
-    uint32_t prev = 0;
-    if (valid) prev = S.whist[w][d];
-    __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) S.whist[w][d] = prev + __popc(peers);
-    __syncwarp();
-    rk[j] = (d << 16) | (prev + __popc(peers & lanemask_lt()));
-  }
-  __syncthreads();
+    for (int j = 0; j < SORT_ITEMS; j++) {
+      const uint32_t idx = w * WARP_ITEMS + j * 32 + lane;
+      const bool valid = idx < cnt;
+      const uint32_t d = valid ? (k[j] >> shift) & 0xFF : 0x100u;
+      const unsigned peers = __match_any_sync(FULL, d);
+      uint32_t prev = 0;
+      if (valid) prev = S.whist[w][d];
+      __syncwarp();
+      if (valid && lane == __ffs(peers) - 1) S.whist[w][d] = prev + __popc(peers);
+      __syncwarp();
+      rk[j] = (d << 16) | (prev + __popc(peers & lanemask_lt()));
+    }
+    __syncthreads();
 
-  // ---- per digit: warp-exclusive prefix, tile count, look-back
-  const int d = t;  // SORT_THREADS == RADIX
-  uint32_t tile_cnt = 0;
+    // ---- per digit: warp-exclusive prefix, tile count, publish, look-back
+    const int d = t;  // SORT_THREADS == RADIX
+    uint32_t tile_cnt = 0;
 #pragma unroll
-  for (int ww = 0; ww < WARPS; ww++) {
-    const uint32_t c = S.whist[ww][d];
-    S.whist[ww][d] = tile_cnt;
-    tile_cnt += c;
-  }
-  unsigned long long* my_status = status + (size_t)tile * RADIX + d;
-  const unsigned long long ep = (unsigned long long)(epoch & 0x3FFFFF) << 40;
-  if (tile == 0) st_relaxed(my_status, FLAG_INC | ep | tile_cnt);
-  else st_relaxed(my_status, FLAG_AGG | ep | tile_cnt);
-  const uint32_t excl_tile = block_excl_scan(tile_cnt, S.wt);
-  S.tile_excl[d] = excl_tile;
-  unsigned long long excl = 0;
-  if (tile > 0) {
-    // look back LB predecessors per L2 round trip (the walk is latency-bound)
-    constexpr int LB = 8;
-    int64_t tp = (int64_t)tile - 1;
-    bool done = false;
-    while (!done) {
-      unsigned long long s[LB];
+    for (int ww = 0; ww < WARPS; ww++) {
+      const uint32_t c = S.whist[ww][d];
+      S.whist[ww][d] = tile_cnt;
+      tile_cnt += c;
+    }
+    unsigned long long* my_status = status + (size_t)tile * RADIX + d;
+    if (tile == 0) st_relaxed(my_status, FLAG_INC | ep | tile_cnt);
+    else st_relaxed(my_status, FLAG_AGG | ep | tile_cnt);
+    const uint32_t excl_tile = block_excl_scan(tile_cnt, S.wt);
+    S.tile_excl[d] = excl_tile;
+    unsigned long long excl = 0;
+    if (tile > 0) {
+      // look back LB predecessors per L2 round trip (the walk is latency-bound)
+      constexpr int LB = 8;
+      int64_t tp = (int64_t)tile - 1;
+      bool done = false;
+      while (!done) {
+        unsigned long long sw[LB];
 #pragma unroll
-      for (int j = 0; j < LB; j++) s[j] = tp - j >= 0 ? ld_relaxed(status + (size_t)(tp - j) * RADIX + d) : 0ull;
+        for (int j = 0; j < LB; j++) sw[j] = tp - j >= 0 ? ld_relaxed(status + (size_t)(tp - j) * RADIX + d) : 0ull;
 #pragma unroll
-      for (int j = 0; j < LB; j++) {
-        if (done) break;
-        const bool ready = ((s[j] >> 40) & 0x3FFFFF) == (epoch & 0x3FFFFF) && (s[j] >> 62) != 0;
-        if (!ready) break;  // re-poll from this predecessor
-        excl += s[j] & VAL_MASK;
-        tp--;
-        if ((s[j] >> 62) == 2) done = true;
+        for (int j = 0; j < LB; j++) {
+          if (done) break;
+          const bool ready = ((sw[j] >> 40) & 0x3FFFFF) == (epoch & 0x3FFFFF) && (sw[j] >> 62) != 0;
+          if (!ready) break;  // re-poll from this predecessor
+          excl += sw[j] & VAL_MASK;
+          tp--;
+          if ((sw[j] >> 62) == 2) done = true;
+        }
+      }
+      st_relaxed(my_status, FLAG_INC | ep | (excl + tile_cnt));
+    }
+    S.glob_base[d] = (uint32_t)(bin_off[d] + excl) - excl_tile;
+    __syncthreads();
+
+    // ---- scatter into shared memory in digit order (stable), in place
+#pragma unroll
+    for (int j = 0; j < SORT_ITEMS; j++) {
+      const uint32_t dd = rk[j] >> 16;
+      if (dd < RADIX) {
+        const uint32_t pos = S.tile_excl[dd] + S.whist[w][dd] + (rk[j] & 0xFFFF);
+        B.keys[pos] = k[j];
+        B.vals[pos] = v[j];
       }
     }
-    st_relaxed(my_status, FLAG_INC | ep | (excl + tile_cnt));
-  }
-  S.glob_base[d] = (uint32_t)(bin_off[d] + excl) - excl_tile;
-  __syncthreads();
+    __syncthreads();
 
-  // ---- scatter into shared memory in digit order (stable)
+    // ---- coalesced write-out: sorted position i goes to glob_base[digit] + i
+    if (cnt == SORT_TILE) {
+      uint32_t o[SORT_ITEMS];
 #pragma unroll
-  for (int j = 0; j < SORT_ITEMS; j++) {
-    const uint32_t dd = rk[j] >> 16;
-    if (dd < RADIX) {
-      const uint32_t pos = S.tile_excl[dd] + S.whist[w][dd] + (rk[j] & 0xFFFF);
-      S.keys[pos] = k[j];
-      S.vals[pos] = v[j];
+      for (int j = 0; j < SORT_ITEMS; j++) k[j] = B.keys[t + j * SORT_THREADS];
+#pragma unroll
+      for (int j = 0; j < SORT_ITEMS; j++) o[j] = S.glob_base[(k[j] >> shift) & 0xFF] + t + j * SORT_THREADS;
+#pragma unroll
+      for (int j = 0; j < SORT_ITEMS; j++) keys_out[o[j]] = k[j];
+#pragma unroll
+      for (int j = 0; j < SORT_ITEMS; j++) vals_out[o[j]] = B.vals[t + j * SORT_THREADS];
+    } else {
+      for (uint32_t i = t; i < cnt; i += SORT_THREADS) {
+        const uint32_t kk = B.keys[i];
+        const uint32_t o = S.glob_base[(kk >> shift) & 0xFF] + i;
+        keys_out[o] = kk;
+        vals_out[o] = B.vals[i];
+      }
     }
-  }
-  __syncthreads();
-
-  // ---- coalesced write-out: sorted position i goes to glob_base[digit] + i
-  if (cnt == SORT_TILE) {
-    uint32_t o[SORT_ITEMS];
-#pragma unroll
-    for (int j = 0; j < SORT_ITEMS; j++) k[j] = S.keys[t + j * SORT_THREADS];
-#pragma unroll
-    for (int j = 0; j < SORT_ITEMS; j++) o[j] = S.glob_base[(k[j] >> shift) & 0xFF] + t + j * SORT_THREADS;
-#pragma unroll
-    for (int j = 0; j < SORT_ITEMS; j++) keys_out[o[j]] = k[j];
-#pragma unroll
-    for (int j = 0; j < SORT_ITEMS; j++) vals_out[o[j]] = S.vals[t + j * SORT_THREADS];
-  } else {
-    for (uint32_t i = t; i < cnt; i += SORT_THREADS) {
-      const uint32_t kk = S.keys[i];
-      const uint32_t o = S.glob_base[(kk >> shift) & 0xFF] + i;
-      keys_out[o] = kk;
-      vals_out[o] = S.vals[i];
-    }
+    __syncthreads();  // buffer `cur`, whist, glob_base free for reuse
+    cur ^= 1;
   }
 }
 
@@ -317,6 +349,13 @@ cudaError_t onesweep_sort(uint32_t* keys, uint64_t* vals, uint32_t n, int bits, 
   launched(2);
   if (prof) prof->end(RC_PROF_HIST, s, (uint64_t)n * 4, n);
   const uint32_t tiles = (uint32_t)sort_tiles(n);
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, onesweep_kernel, SORT_THREADS, sizeof(SortSmem));
+    if (per_sm < 1) per_sm = 1;
+  }
+  // persistent: never more blocks than can be resident (look-back progress)
+  const uint32_t grid = (uint32_t)umin64(tiles, (uint64_t)per_sm * nsm);
   uint32_t* kin = keys;
   uint64_t* vin = vals;
   uint32_t* kout = ws.keys_alt;
@@ -327,7 +366,7 @@ cudaError_t onesweep_sort(uint32_t* keys, uint64_t* vals, uint32_t n, int bits, 
       ws.epoch = 1;
     }
     if (prof) prof->begin(s);
-    onesweep_kernel<<<tiles, SORT_THREADS, sizeof(SortSmem), s>>>(kin, vin, kout, vout, n, 8 * p,
+    onesweep_kernel<<<grid, SORT_THREADS, sizeof(SortSmem), s>>>(kin, vin, kout, vout, n, 8 * p,
                                                                  ws.bin_off + p * RADIX, ws.status,
                                                                  ws.tile_ctr + p, ws.epoch);
     launched();
