@@ -23,6 +23,16 @@ namespace rc {
 namespace {
 constexpr uint32_t INF = 0xFFFFFFFFu;
 
+// record fields (rc_internal.h make_rec); a write's final value lives in the
+// side table wval[slot][lane], lane = (cell / cpi) * n + tid
+__device__ __forceinline__ uint32_t rec_cell(uint64_t r) { return (uint32_t)(r >> REC_CELL_SHIFT); }
+__device__ __forceinline__ uint32_t rec_tid(uint64_t r) { return ((uint32_t)r >> 5) & (MAX_WG - 1); }
+__device__ __forceinline__ bool rec_w(uint64_t r) { return (r & 1) != 0; }
+__device__ __forceinline__ int32_t rec_val(const DetectParams& p, uint64_t r) {
+  const uint32_t lane = (rec_cell(r) / p.cpi) * p.n + rec_tid(r);
+  return __ldg(p.wval + (size_t)(((uint32_t)r >> 1) & 0xF) * p.n_lanes + lane);
+}
+
 __device__ __forceinline__ void emit(const DetectParams& p, uint32_t cell, uint32_t t1, uint32_t t2, uint16_t kind,
                                   uint16_t flags) {
   const uint32_t inst = cell / p.cpi;
@@ -77,16 +87,16 @@ __device__ __forceinline__ void rw_pair(bool hasr, uint32_t r1, uint32_t r2, uin
 // thread walks it (pass 1: statistics; pass 2: first differing writer and
 // membership flags; pass 3 only for a non-benign pair with readers).
 __device__ __forceinline__ void serial_segment(const DetectParams& p, uint32_t i) {
-  const uint32_t key = __ldg(p.keys + i);
+  const uint32_t key = rec_cell(__ldg(p.recs + i));
   uint32_t r1 = INF, r2 = INF, rmax = 0, w1 = INF, w2 = INF, wmax = 0, nw = 0;
   bool hasr = false;
   int32_t vw1 = 0, vwmax = 0;
   uint32_t end = i;
   do {
-    const uint64_t v = __ldg(p.vals + end);
-    const uint32_t tid = (uint32_t)v >> 1;
-    if (v & 1) {
-      const int32_t val = (int32_t)(v >> 32);
+    const uint64_t v = __ldg(p.recs + end);
+    const uint32_t tid = rec_tid(v);
+    if (rec_w(v)) {
+      const int32_t val = rec_val(p, v);
       if (tid < w1) { w2 = w1; w1 = tid; vw1 = val; }
       else if (tid < w2) w2 = tid;
       if (nw == 0 || tid > wmax) { wmax = tid; vwmax = val; }
@@ -98,7 +108,7 @@ __device__ __forceinline__ void serial_segment(const DetectParams& p, uint32_t i
       hasr = true;
     }
     end++;
-  } while (end < p.n_records && __ldg(p.keys + end) == key);
+  } while (end < p.n_records && rec_cell(__ldg(p.recs + end)) == key);
   if (nw == 0) return;  // only reads: no conflict, nothing to commit
   p.heap[key] = vwmax;  // barrier release: max-tid writer wins
   uint32_t t1, t2;
@@ -107,10 +117,10 @@ __device__ __forceinline__ void serial_segment(const DetectParams& p, uint32_t i
   uint32_t nb = INF;
   bool t1r = false, t2r = false, t2w = false, w1r = false, w2r = false;
   for (uint32_t j = i; j < end; j++) {
-    const uint64_t v = __ldg(p.vals + j);
-    const uint32_t tid = (uint32_t)v >> 1;
-    if (v & 1) {
-      if ((int32_t)(v >> 32) != vw1 && tid < nb) nb = tid;
+    const uint64_t v = __ldg(p.recs + j);
+    const uint32_t tid = rec_tid(v);
+    if (rec_w(v)) {
+      if (rec_val(p, v) != vw1 && tid < nb) nb = tid;
       t2w |= tid == t2;
     } else {
       t1r |= tid == t1;
@@ -122,8 +132,8 @@ __device__ __forceinline__ void serial_segment(const DetectParams& p, uint32_t i
   bool nbr = false;
   if (nb != INF && hasr)
     for (uint32_t j = i; j < end; j++) {
-      const uint64_t v = __ldg(p.vals + j);
-      if (!(v & 1) && ((uint32_t)v >> 1) == nb) nbr = true;
+      const uint64_t v = __ldg(p.recs + j);
+      if (!rec_w(v) && rec_tid(v) == nb) nbr = true;
     }
   finish_cell(p, key, w1, w2, nw, t1, t2, nb, t1r, t2r, t2w, w1r, w2r, nbr);
 }
@@ -198,12 +208,12 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
   for (uint64_t b = c0; b < c1; b += 32) {
     const uint64_t r = b + lane;
     const bool inb = r < c1;
-    const uint32_t key = inb ? __ldg(p.keys + r) : 0xFFFFFFFFu;
-    const uint64_t v = inb ? __ldg(p.vals + r) : 0ull;
+    const uint64_t v = inb ? __ldg(p.recs + r) : ~0ull;
+    const uint32_t key = rec_cell(v);  // cell ids are < 0xFFFFFFFF
     uint32_t prev = __shfl_up_sync(FULL, key, 1);
-    if (lane == 0) prev = b > 0 ? __ldg(p.keys + b - 1) : ~key;
+    if (lane == 0) prev = b > 0 ? rec_cell(__ldg(p.recs + b - 1)) : ~key;
     uint32_t next = __shfl_down_sync(FULL, key, 1);
-    if (lane == 31) next = r + 1 < p.n_records ? __ldg(p.keys + r + 1) : ~key;
+    if (lane == 31) next = r + 1 < p.n_records ? rec_cell(__ldg(p.recs + r + 1)) : ~key;
     const bool head = inb && prev != key;
     const bool tail = inb && next != key;  // last record of its segment (possibly beyond c1)
     const unsigned heads = __ballot_sync(FULL, head);
@@ -215,10 +225,10 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
     const int hi = t_at_or_after ? __ffs(t_at_or_after) - 1 : last_inb;
     const bool closes = (tails >> hi) & 1;  // segment ends inside this round
     // per-record summary, then segmented suffix reduction over [lane, hi]
-    const uint32_t tid = (uint32_t)v >> 1;
+    const uint32_t tid = rec_tid(v);
     Seg S = ident;
     if (inb) {
-      if (v & 1) { S.w = tid; S.vw = (int32_t)(v >> 32); S.nw = 1; }
+      if (rec_w(v)) { S.w = tid; S.vw = rec_val(p, v); S.nw = 1; }
       else { S.rmin = tid; S.rmax = tid; }
     }
     const bool starter = head || lane == 0;  // lanes whose suffix summary is consumed
@@ -237,7 +247,7 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
       if (l0_closes) {
         if (lane == 0) {
           if (seg_complex(M)) serial_segment(p, (uint32_t)carry_start);
-          else if (M.nw == 1) p.heap[__ldg(p.keys + carry_start)] = M.vw;
+          else if (M.nw == 1) p.heap[rec_cell(__ldg(p.recs + carry_start))] = M.vw;
         }
         carry = false;
       } else {

@@ -67,29 +67,48 @@ __device__ __noinline__ void emit_report_(DevCounters* ctr, rc_report* reports, 
   emit_report_((p).ctr, (p).reports, (p).report_cap, (p).inst_base + (inst), (p).interval, arr, idx, t1, kind)
 
 struct Stage {
-  uint32_t* keys;  // this warp's staging area
-  uint64_t* vals;
+  uint64_t* recs;  // this warp's staging area
   uint32_t fill;   // warp-uniform
   uint32_t cap;
 };
 
+// Digit histograms of staged records (fused K2): each lane counts runs of
+// equal digits over a contiguous slice (staged records are nearly sorted by
+// cell, so runs are long) and adds each run once into the block histogram.
+__device__ __forceinline__ void hist_staged(const uint64_t* recs, uint32_t fill, int passes, uint32_t* bh,
+                                            int lane) {
+  const uint32_t per = (fill + 31) / 32;
+  const uint32_t lo = lane * per, hi = min(fill, lo + per);
+  for (int p = 0; p < passes; p++) {
+    const int sh = REC_CELL_SHIFT + 8 * p;
+    uint32_t cur = 0xFFFFFFFFu, run = 0;
+    for (uint32_t i = lo; i < hi; i++) {
+      const uint32_t d = (uint32_t)(recs[i] >> sh) & 0xFF;
+      if (d == cur) run++;
+      else {
+        if (run) atomicAdd(&bh[p * 256 + cur], run);
+        cur = d;
+        run = 1;
+      }
+    }
+    if (run) atomicAdd(&bh[p * 256 + cur], run);
+  }
+}
+
 // write this warp's staged records to the global log (mid-interval overflow path)
-__device__ __noinline__ uint32_t flush_warp_(DevCounters* ctr, uint32_t* log_keys, uint64_t* log_vals,
-                                             unsigned long long log_cap, const uint32_t* skeys,
-                                             const uint64_t* svals, uint32_t fill, int lane) {
+__device__ __noinline__ uint32_t flush_warp_(DevCounters* ctr, uint64_t* log, unsigned long long log_cap,
+                                             const uint64_t* srecs, uint32_t fill, int lane, int passes,
+                                             uint32_t* bh) {
   __syncwarp();
+  hist_staged(srecs, fill, passes, bh, lane);
   unsigned long long base = 0;
   if (lane == 0) base = atomicAdd(&ctr->log_count, (unsigned long long)fill);
   base = __shfl_sync(FULL, base, 0);
   bool over = false;
   for (uint32_t i = lane; i < fill; i += 32) {
     unsigned long long pos = base + i;
-    if (pos < log_cap) {
-      log_keys[pos] = skeys[i];
-      log_vals[pos] = svals[i];
-    } else {
-      over = true;
-    }
+    if (pos < log_cap) log[pos] = srecs[i];
+    else over = true;
   }
   if (__any_sync(FULL, over) && lane == 0) ctr->log_overflow = 1;
   __syncwarp();
@@ -98,15 +117,10 @@ __device__ __noinline__ uint32_t flush_warp_(DevCounters* ctr, uint32_t* log_key
 
 // warp-aggregated append of one record per lane in `m` (called by the whole warp)
 __device__ __forceinline__ void stage_append(const InterpParams& p, Stage& S, int lane, unsigned m, bool mine,
-                                             uint32_t key, uint64_t val) {
+                                             uint64_t rec, uint32_t* bh) {
   const uint32_t cnt = __popc(m);
-  if (S.fill + cnt > S.cap)
-    S.fill = flush_warp_(p.ctr, p.log_keys, p.log_vals, p.log_cap, S.keys, S.vals, S.fill, lane);
-  if (mine) {
-    const uint32_t pos = S.fill + __popc(m & lanemask_lt());
-    S.keys[pos] = key;
-    S.vals[pos] = val;
-  }
+  if (S.fill + cnt > S.cap) S.fill = flush_warp_(p.ctr, p.log, p.log_cap, S.recs, S.fill, lane, p.passes, bh);
+  if (mine) S.recs[S.fill + __popc(m & lanemask_lt())] = rec;
   S.fill += cnt;
 }
 
@@ -131,9 +145,9 @@ __global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
 
   // ---- shared memory carve-up (sizes mirrored in interp_smem_bytes)
   unsigned char* q = smem;
-  uint64_t* st_vals = reinterpret_cast<uint64_t*>(q); q += (size_t)W * p.stage * 8;
+  uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)W * p.stage * 8;
   uint2* s_code = reinterpret_cast<uint2*>(q); q += CODE_SMEM ? (size_t)p.n_instr * 8 : 0;
-  uint32_t* st_keys = reinterpret_cast<uint32_t*>(q); q += (size_t)W * p.stage * 4;
+  uint32_t* bhist = reinterpret_cast<uint32_t*>(q); q += (size_t)p.passes * 256 * 4;  // block digit histograms
   int32_t* sregs = reinterpret_cast<int32_t*>(q); q += (size_t)R * T * 4;
   uint32_t* ocell = reinterpret_cast<uint32_t*>(q); q += (size_t)OV * T * 4;
   int32_t* oval = reinterpret_cast<int32_t*>(q); q += (size_t)OV * T * 4;
@@ -153,6 +167,7 @@ __global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
     const uint2* src = reinterpret_cast<const uint2*>(p.code);
     for (uint32_t i = t; i < p.n_instr; i += T) s_code[i] = src[i];
   }
+  for (int i = t; i < p.passes * 256; i += T) bhist[i] = 0;
 
   const uint32_t g = blockIdx.x * (uint32_t)T + t;
   const bool valid = g < p.n_lanes;
@@ -176,7 +191,7 @@ __global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
   unsigned long long steps = 0;
   uint32_t nloads = 0, nstores = 0;
   bool ovl_over = false;
-  Stage S{st_keys + (size_t)warp * p.stage, st_vals + (size_t)warp * p.stage, 0, p.stage};
+  Stage S{st_recs + (size_t)warp * p.stage, 0, p.stage};
 
   for (;;) {
     if (__ballot_sync(FULL, running) == 0) break;
@@ -263,7 +278,7 @@ __global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
           }
         }
         const unsigned m = __ballot_sync(FULL, ok);
-        if (m) stage_append(p, S, lane, m, ok, cell, (uint64_t)(tid << 1));
+        if (m) stage_append(p, S, lane, m, ok, make_rec(cell, tid, 0, 0), bhist);
         break;
       }
       case RC_OP_ST:
@@ -312,18 +327,18 @@ __global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
     }
   }
 
-  // write records: one per distinct written cell, final value (reading L3)
+  // write records: one per distinct written cell; its final value (reading
+  // L3) goes to the side table wval[slot][lane] read by detect
   const int max_own = __reduce_max_sync(FULL, (unsigned)n_own);
   for (int j = 0; j < max_own; j++) {
     const bool has = j < n_own;
     const unsigned m = __ballot_sync(FULL, has);
-    uint64_t v = 0;
-    uint32_t c = 0;
+    uint64_t rec = 0;
     if (has) {
-      c = ocell[j * T + t];
-      v = ((uint64_t)(uint32_t)oval[j * T + t] << 32) | (uint64_t)(tid << 1) | 1ull;
+      rec = make_rec(ocell[j * T + t], tid, (uint32_t)j, 1);
+      p.wval[(size_t)j * p.n_lanes + g] = oval[j * T + t];
     }
-    stage_append(p, S, lane, m, has, c, v);
+    stage_append(p, S, lane, m, has, rec, bhist);
   }
 
   // lane state out (only registers live across the barrier, only for suspended lanes)
@@ -415,16 +430,18 @@ __global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
   const unsigned long long base = wbase[warp];
   for (uint32_t i = lane; i < S.fill; i += 32) {
     const unsigned long long pos = base + i;
-    if (pos < p.log_cap) {
-      p.log_keys[pos] = S.keys[i];
-      p.log_vals[pos] = S.vals[i];
-    }
+    if (pos < p.log_cap) p.log[pos] = S.recs[i];
   }
+  hist_staged(S.recs, S.fill, p.passes, bhist, lane);
+  __syncthreads();
+  for (int i = t; i < p.passes * 256; i += T)
+    if (bhist[i]) atomicAdd(&p.hist[i], bhist[i]);
 }
 
 size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem) {
   const int W = T / 32;
-  size_t b = (size_t)W * p.stage * (8 + 4);        // staging
+  size_t b = (size_t)W * p.stage * 8;              // staging
+  b += (size_t)p.passes * 256 * 4;                 // block digit histograms
   b += code_in_smem ? (size_t)p.n_instr * 8 : 0;   // program
   b += (size_t)p.n_regs * T * 4;                   // registers
   b += (size_t)p.ovl_cap * T * 8;                  // overlay

@@ -43,6 +43,17 @@ constexpr int32_t NODE_EXIT = -1;
 constexpr uint32_t NOTID = 0xFFFFFFFFu;
 constexpr int OVL_CAP = 16;        // own-write overlay entries per work-item (smem)
 
+// One access-log record is a single u64:
+//   bits 63..32  cell id (batch-local; the sort key — only these bits are sorted)
+//   bits 31..5   tid (< 2^27)
+//   bits  4..1   overlay slot of a write (its final value is wval[slot][lane])
+//   bit      0   1 = write, 0 = read
+constexpr int REC_CELL_SHIFT = 32;
+constexpr uint32_t MAX_WG = 1u << 27;
+__host__ __device__ inline uint64_t make_rec(uint32_t cell, uint32_t tid, uint32_t slot, uint32_t w) {
+  return ((uint64_t)cell << 32) | (tid << 5) | (slot << 1) | w;
+}
+
 static_assert(RC_OVERLAY_CAP == OVL_CAP, "overlay capacity in rc.h and the interpreter agree");
 
 // Device counters of one run; zeroed per attempt where noted.
@@ -86,17 +97,20 @@ struct InterpParams {
   int32_t* node_min;          // [I_b] min / max arrival node (fused A4)
   int32_t* node_max;
   // log
-  uint32_t* log_keys;         // cell
-  uint64_t* log_vals;         // value << 32 | tid << 1 | is_write
+  uint64_t* log;              // records (make_rec)
   unsigned long long log_cap;
+  int32_t* wval;              // [ovl_cap][n_lanes] final value of each written overlay slot
+  uint32_t* hist;             // [4][256] digit histograms of the cell bits (fused K2)
+  int passes;                 // 8-bit digit passes of the sort
   rc_report* reports;
   unsigned long long report_cap;
   DevCounters* ctr;
 };
 
 struct DetectParams {
-  const uint32_t* keys;
-  const uint64_t* vals;
+  const uint64_t* recs;       // sorted by cell
+  const int32_t* wval;        // [ovl_cap][n_lanes]
+  uint32_t n_lanes, n;        // lane = inst_local * n + tid
   uint32_t n_records;
   int32_t* heap;
   uint32_t cpi, n_arrays;
@@ -112,8 +126,7 @@ size_t interp_smem_bytes(const InterpParams& p, int threads, bool code_in_smem);
 cudaError_t launch_interp(const InterpParams& p, cudaStream_t s);
 
 struct SortWorkspace {
-  uint32_t* keys_alt = nullptr;
-  uint64_t* vals_alt = nullptr;
+  uint64_t* alt = nullptr;         // ping-pong buffer
   uint32_t* hist = nullptr;        // [4][256] digit histograms
   uint32_t* bin_off = nullptr;     // [4][256] exclusive offsets
   unsigned long long* status = nullptr;  // [tiles][256] decoupled look-back words
@@ -146,8 +159,10 @@ struct Profiler {
 
 // Sort (keys, vals) by key bits [0, bits).  *in_alt tells whether the sorted
 // data ended in the alt buffers of `ws`.
-cudaError_t onesweep_sort(uint32_t* keys, uint64_t* vals, uint32_t n, int bits, SortWorkspace& ws,
-                          cudaStream_t s, bool* in_alt, Profiler* prof);
+// hist_ready: ws.hist already holds the digit histograms (fused into K1);
+// otherwise an upfront histogram pass (K2) computes them.
+cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, int bits, SortWorkspace& ws, cudaStream_t s, bool* in_alt,
+                          Profiler* prof, bool hist_ready);
 
 cudaError_t launch_detect(const DetectParams& p, cudaStream_t s);
 

@@ -98,7 +98,7 @@ struct rc_workspace {
   int device = -1;
   DevBuf code, arr_off, arr_size, heap;
   DevBuf regs[2], pc[2], status[2], live;
-  DevBuf log_keys, log_vals, keys_alt, vals_alt, sort_status, sort_small;
+  DevBuf log, log_alt, wval, sort_status, sort_small;
   DevBuf reports, reports_scratch;
   DevBuf inst_tmp;  // node_min | node_max | first_tid | second_tid | inst_flag  ([I_b] each)
   DevBuf ctr;
@@ -107,7 +107,7 @@ struct rc_workspace {
   Profiler prof;
   ~rc_workspace() {
     for (DevBuf* b : {&code, &arr_off, &arr_size, &heap, &regs[0], &regs[1], &pc[0], &pc[1], &status[0],
-                      &status[1], &live, &log_keys, &log_vals, &keys_alt, &vals_alt, &sort_status,
+                      &status[1], &live, &log, &log_alt, &wval, &sort_status,
                       &sort_small, &reports, &reports_scratch, &inst_tmp, &ctr})
       b->release();
     if (h_ctr) cudaFreeHost(h_ctr);
@@ -208,7 +208,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   rc_program* P = const_cast<rc_program*>(prog);
   if (n_arrays != P->n_arrays) return fail(RC_EINVAL, "n_arrays %u != program's %u", n_arrays, P->n_arrays);
   if (n_arrays && !arrays) return fail(RC_EINVAL, "arrays is NULL");
-  if (n >= (1u << 31)) return fail(RC_EINVAL, "work_group_size %u >= 2^31", n);
+  if (n > MAX_WG) return fail(RC_EINVAL, "work_group_size %u > 2^27", n);
   if (capacity && !out) return fail(RC_EINVAL, "out is NULL with capacity %llu", (unsigned long long)capacity);
   rc_options opt;
   memset(&opt, 0, sizeof opt);
@@ -290,16 +290,16 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       CK(W.status[b].ensure(std::max<uint64_t>(1, L_max)));
     }
     CK(W.inst_tmp.ensure((uint64_t)I_b * 20));
+    CK(W.wval.ensure(std::max<uint64_t>(1, L_max * (uint64_t)P->ovl_cap) * 4));
   }
-  uint64_t log_cap = W.log_keys.bytes / 4;
+  const int passes = (key_bits + 7) / 8;
+  uint64_t log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
   {
     const uint64_t want = std::max<uint64_t>(1u << 16, std::min<uint64_t>(L_max * 4, 0xFFFFFFFFull));
     if (log_cap < want) {
-      CK(W.log_keys.ensure(want * 4));
-      CK(W.log_vals.ensure(want * 8));
-      CK(W.keys_alt.ensure(want * 4));
-      CK(W.vals_alt.ensure(want * 8));
-      log_cap = std::min(W.log_keys.bytes / 4, W.log_vals.bytes / 8);
+      CK(W.log.ensure(want * 8));
+      CK(W.log_alt.ensure(want * 8));
+      log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
     }
   }
   auto ensure_sort_status = [&](uint64_t cap) -> cudaError_t {
@@ -391,6 +391,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       InterpParams ip;
       for (;;) {
         CK(cudaMemsetAsync(dctr, 0, offsetof(DevCounters, report_count), s));
+        CK(cudaMemsetAsync(W.sort.hist, 0, 4 * 256 * sizeof(uint32_t), s));  // K1 fuses the digit histograms
         CK(cudaMemsetAsync(&dctr->iv_loads, 0, offsetof(DevCounters, lanes_final) - offsetof(DevCounters, iv_loads), s));
         ip.code = W.code.as<Ins>();
         ip.n_instr = P->n_instr;
@@ -417,9 +418,11 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         ip.stage = P->rec_bound > 0 ? (uint32_t)std::min(256, ((32 * P->rec_bound + 31) / 32) * 32) : 256u;
         ip.node_min = node_min;
         ip.node_max = node_max;
-        ip.log_keys = W.log_keys.as<uint32_t>();
-        ip.log_vals = W.log_vals.as<uint64_t>();
+        ip.log = W.log.as<uint64_t>();
         ip.log_cap = log_cap;
+        ip.wval = W.wval.as<int32_t>();
+        ip.hist = W.sort.hist;
+        ip.passes = passes;
         ip.reports = W.reports.as<rc_report>();
         ip.report_cap = rep_cap;
         ip.ctr = dctr;
@@ -438,11 +441,9 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         if (log_over) {  // grow the log and re-run the interval from the saved lane state
           const uint64_t want = std::min<uint64_t>(W.h_ctr->log_count + W.h_ctr->log_count / 4 + 1024, 0xFFFFFFFFull);
           if (W.h_ctr->log_count > 0xFFFFFFFFull) return fail(RC_ELIMIT, "more than 2^32 access records in one interval");
-          CK(W.log_keys.ensure(want * 4));
-          CK(W.log_vals.ensure(want * 8));
-          CK(W.keys_alt.ensure(want * 4));
-          CK(W.vals_alt.ensure(want * 8));
-          log_cap = std::min(W.log_keys.bytes / 4, W.log_vals.bytes / 8);
+          CK(W.log.ensure(want * 8));
+          CK(W.log_alt.ensure(want * 8));
+          log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
           CK(ensure_sort_status(log_cap));
         }
         if (rep_over) CK(grow_reports(W.h_ctr->report_count));
@@ -456,20 +457,20 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
 
       // ---------------- K2/K3: sort the log by cell
       bool in_alt = false;
-      W.sort.keys_alt = W.keys_alt.as<uint32_t>();
-      W.sort.vals_alt = W.vals_alt.as<uint64_t>();
-      CK(onesweep_sort(W.log_keys.as<uint32_t>(), W.log_vals.as<uint64_t>(), (uint32_t)N, key_bits, W.sort, s,
-                       &in_alt, W.prof.on ? &W.prof : nullptr));
-      const uint32_t* sk = in_alt ? W.keys_alt.as<uint32_t>() : W.log_keys.as<uint32_t>();
-      const uint64_t* sv = in_alt ? W.vals_alt.as<uint64_t>() : W.log_vals.as<uint64_t>();
+      W.sort.alt = W.log_alt.as<uint64_t>();
+      CK(onesweep_sort(W.log.as<uint64_t>(), (uint32_t)N, key_bits, W.sort, s, &in_alt,
+                       W.prof.on ? &W.prof : nullptr, /*hist_ready=*/true));
+      const uint64_t* sr = in_alt ? W.log_alt.as<uint64_t>() : W.log.as<uint64_t>();
 
       // ---------------- K4+K5 and A4 (idempotent: re-run if the report buffer overflows)
       const uint64_t rep_after_k1 = rep_count;
       bool checked = false, diverged = false;
       for (;;) {
         DetectParams dp;
-        dp.keys = sk;
-        dp.vals = sv;
+        dp.recs = sr;
+        dp.wval = W.wval.as<int32_t>();
+        dp.n_lanes = L;
+        dp.n = n;
         dp.n_records = (uint32_t)N;
         dp.heap = W.heap.as<int32_t>();
         dp.cpi = (uint32_t)std::max<uint64_t>(cpi, 1);
@@ -482,7 +483,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         dp.ctr = dctr;
         W.prof.begin(s);
         CK(launch_detect(dp, s));
-        W.prof.end(RC_PROF_DETECT, s, N * 12, N);
+        W.prof.end(RC_PROF_DETECT, s, N * 8, N);
         BoundaryParams bp = bparams(k);
         bp.status = W.status[cur ^ 1].as<uint8_t>();
         bp.pc = W.pc[cur ^ 1].as<uint32_t>();

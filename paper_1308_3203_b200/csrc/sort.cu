@@ -1,11 +1,10 @@
 // sort.cu — K2/K3: onesweep LSD radix sort of the access log by cell.
 //
 // Groups the interval's access records by cell so that
-// the race rule can be applied per cell.  Keys are the
-// batch-local linear cell id (u32); values are 8-byte payloads
-// (value << 32 | tid << 1 | is_write).  Only the cell bits are sorted; the
-// sort is stable, and the detector (detect.cu) only uses order-independent
-// reductions inside a cell, so within-cell order is irrelevant.
+// the race rule can be applied per cell.  A record is one
+// u64 (rc_internal.h make_rec) whose high 32 bits are the batch-local cell id;
+// only the live cell bits are sorted (8-bit digits).  The sort is stable, and
+// the detector only uses order-independent reductions inside a cell.
 //
 // Onesweep (Adinets & Merrill): one upfront pass computes the digit
 // histograms of every pass (K2), then each pass (K3) is a single kernel:
@@ -66,30 +65,41 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* warp_t
 }
 }  // namespace
 
-// ---- K2: all digit histograms in one read of the keys ----------------------
-__global__ void __launch_bounds__(256) hist_kernel(const uint32_t* __restrict__ keys, uint32_t n, int passes,
+#ifdef SORT_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[8];
+void sort_phase_io(unsigned long long* out, bool reset) {
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
+  } else {
+    cudaMemcpyFromSymbol(out, g_phase_cycles, 8 * sizeof(unsigned long long));
+  }
+}
+#define PHASE_T(i)                                       \
+  do {                                                   \
+    if (t == 0) {                                        \
+      const long long now_ = clock64();                  \
+      atomicAdd(&g_phase_cycles[i], now_ - tprev_);      \
+      tprev_ = now_;                                     \
+    }                                                    \
+  } while (0)
+#else
+#define PHASE_T(i) do {} while (0)
+#endif
+
+// ---- K2: all digit histograms in one read (fallback; K1 fuses it) ----------
+__global__ void __launch_bounds__(256) hist_kernel(const uint64_t* __restrict__ recs, uint32_t n, int passes,
                                                    uint32_t* __restrict__ hist) {
   __shared__ uint32_t h[4][RADIX];
   for (int i = threadIdx.x; i < 4 * RADIX; i += blockDim.x) (&h[0][0])[i] = 0;
   __syncthreads();
-  // each thread takes 16 consecutive keys and counts runs of equal digits
-  // (access logs are nearly sorted by cell, so runs are long)
-  const uint32_t chunk = 16;
+  const uint32_t chunk = 16;  // consecutive records per thread; count runs of equal digits
   for (uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * chunk; b < n;
        b += (uint64_t)gridDim.x * blockDim.x * chunk) {
     uint32_t k[16];
     const uint32_t m = (uint32_t)umin64(chunk, n - b);
-    if (m == chunk && ((b & 3) == 0)) {
-      const uint4* q = reinterpret_cast<const uint4*>(keys + b);
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        uint4 v = __ldg(q + j);
-        k[4 * j] = v.x; k[4 * j + 1] = v.y; k[4 * j + 2] = v.z; k[4 * j + 3] = v.w;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; j++) k[j] = j < (int)m ? __ldg(keys + b + j) : 0;
-    }
+    for (int j = 0; j < 16; j++) k[j] = j < (int)m ? (uint32_t)(__ldg(recs + b + j) >> REC_CELL_SHIFT) : 0u;
     for (int p = 0; p < passes; p++) {
       const int sh = 8 * p;
       uint32_t cur = (k[0] >> sh) & 0xFF, run = 1;
@@ -121,15 +131,13 @@ __global__ void __launch_bounds__(256) bin_offsets_kernel(const uint32_t* __rest
 
 // ---- K3: one onesweep digit pass -------------------------------------------
 // Persistent: a resident grid of blocks claims tiles in order from an atomic
-// counter; each block keeps two tile buffers and prefetches (TMA) the next
-// claimed tile while it ranks / looks back / scatters the current one.
-struct TileBuf {
-  uint64_t vals[SORT_TILE];
-  uint32_t keys[SORT_TILE];
-};
+// counter (claiming one tile ahead to hide the atomic); each block keeps two
+// tile buffers and prefetches (TMA) the next claimed tile while it processes
+// the current one.
 struct SortSmem {
-  TileBuf buf[2];
-  uint32_t whist[WARPS][RADIX];
+  uint64_t buf[2][SORT_TILE];
+  uint32_t whist[WARPS][RADIX];  // per-warp digit counters (ranking)
+  uint32_t thist[2][RADIX];      // early tile counts (two copies: fewer atomic conflicts)
   uint32_t tile_excl[RADIX];
   uint32_t glob_base[RADIX];
   uint32_t wt[WARPS];
@@ -137,23 +145,17 @@ struct SortSmem {
   unsigned long long mbar[2];
 };
 
-__device__ __forceinline__ void tile_fetch(TileBuf& B, unsigned long long* mbar, const uint32_t* keys_in,
-                                           const uint64_t* vals_in, uint64_t base, uint32_t cnt) {
-  // one elected thread: bulk copies of the 16-byte-aligned part (cnt & ~3 records)
-  const uint32_t c4 = cnt & ~3u;
+__device__ __forceinline__ void tile_fetch(uint64_t* dst, unsigned long long* mbar, const uint64_t* src,
+                                           uint32_t cnt) {
+  // one elected thread: bulk copy of the 16-byte-aligned part (cnt & ~1 records)
+  const uint32_t c2 = cnt & ~1u;
   const uint32_t bar = smem_u32(mbar);
-  const uint32_t bk = c4 * 4, bv = c4 * 8;
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bk + bv) : "memory");
-  if (c4) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(c2 * 8) : "memory");
+  if (c2)
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(B.keys)),
-                 "l"(keys_in + base), "r"(bk), "r"(bar)
+                     smem_u32(dst)),
+                 "l"(src), "r"(c2 * 8), "r"(bar)
                  : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(B.vals)),
-                 "l"(vals_in + base), "r"(bv), "r"(bar)
-                 : "memory");
-  }
 }
 
 __device__ __forceinline__ void mbar_wait(unsigned long long* mbar, uint32_t phase) {
@@ -168,15 +170,18 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* mbar, uint32_t pha
   }
 }
 
-__global__ void __launch_bounds__(SORT_THREADS, 2) onesweep_kernel(
-    const uint32_t* __restrict__ keys_in, const uint64_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
-    uint64_t* __restrict__ vals_out, uint32_t n, int shift, const uint32_t* __restrict__ bin_off,
-    unsigned long long* __restrict__ status, uint32_t* __restrict__ tile_ctr, uint32_t epoch) {
+__global__ void __launch_bounds__(SORT_THREADS, 3) onesweep_kernel(const uint64_t* __restrict__ in,
+                                                                   uint64_t* __restrict__ out, uint32_t n, int shift,
+                                                                   const uint32_t* __restrict__ bin_off,
+                                                                   unsigned long long* __restrict__ status,
+                                                                   uint32_t* __restrict__ tile_ctr, uint32_t epoch) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const uint32_t n_tiles = (uint32_t)((n + SORT_TILE - 1) / SORT_TILE);
   const unsigned long long ep = (unsigned long long)(epoch & 0x3FFFFF) << 40;
+  const int dsh = REC_CELL_SHIFT + shift;
+  uint32_t claimed = 0xFFFFFFFFu;  // thread 0: tile claimed ahead
 
   if (t == 0) {
     for (int b = 0; b < 2; b++)
@@ -184,78 +189,92 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) onesweep_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const uint32_t t0 = atomicAdd(tile_ctr, 1u);
     S.tile[0] = t0;
-    if (t0 < n_tiles)
-      tile_fetch(S.buf[0], &S.mbar[0], keys_in, vals_in, (uint64_t)t0 * SORT_TILE,
+    if (t0 < n_tiles) {
+      tile_fetch(S.buf[0], &S.mbar[0], in + (uint64_t)t0 * SORT_TILE,
                  (uint32_t)umin64(SORT_TILE, n - (uint64_t)t0 * SORT_TILE));
+      claimed = atomicAdd(tile_ctr, 1u);
+    }
   }
   __syncthreads();
   uint32_t phase = 0;  // bit b = expected parity of buffer b's mbarrier
   int cur = 0;
+#ifdef SORT_PHASE_TIMING
+  long long tprev_ = clock64();
+#endif
   for (;;) {
     const uint32_t tile = S.tile[cur];
     if (tile >= n_tiles) break;  // block-uniform
-    // claim and prefetch the next tile into the other buffer (freed by the
-    // __syncthreads that ended the previous iteration)
+    // fetch the tile claimed last iteration into the other buffer (freed by
+    // the __syncthreads that ended the previous iteration); claim the next
     if (t == 0) {
-      const uint32_t tn = atomicAdd(tile_ctr, 1u);
+      const uint32_t tn = claimed;
       S.tile[cur ^ 1] = tn;
-      if (tn < n_tiles)
-        tile_fetch(S.buf[cur ^ 1], &S.mbar[cur ^ 1], keys_in, vals_in, (uint64_t)tn * SORT_TILE,
+      claimed = 0xFFFFFFFFu;
+      if (tn < n_tiles) {
+        tile_fetch(S.buf[cur ^ 1], &S.mbar[cur ^ 1], in + (uint64_t)tn * SORT_TILE,
                    (uint32_t)umin64(SORT_TILE, n - (uint64_t)tn * SORT_TILE));
+        claimed = atomicAdd(tile_ctr, 1u);
+      }
     }
     for (int i = t; i < WARPS * RADIX; i += SORT_THREADS) (&S.whist[0][0])[i] = 0;
+    S.thist[0][t] = 0;
+    S.thist[1][t] = 0;
     const uint64_t base = (uint64_t)tile * SORT_TILE;
     const uint32_t cnt = (uint32_t)umin64(SORT_TILE, n - base);
-    TileBuf& B = S.buf[cur];
+    uint64_t* B = S.buf[cur];
+    PHASE_T(0);
     mbar_wait(&S.mbar[cur], (phase >> cur) & 1u);
     phase ^= 1u << cur;
-    for (uint32_t i = (cnt & ~3u) + t; i < cnt; i += SORT_THREADS) {  // unaligned tail of the last tile
-      B.keys[i] = keys_in[base + i];
-      B.vals[i] = vals_in[base + i];
-    }
+    if ((cnt & 1u) && t == 0) B[cnt - 1] = in[base + cnt - 1];  // odd tail of the last tile
     __syncthreads();
+    PHASE_T(1);
 
-    // ---- stable in-tile ranking (warp w owns items [w*512, w*512+512), striped)
-    uint32_t k[SORT_ITEMS];
-    uint64_t v[SORT_ITEMS];
-    uint32_t rk[SORT_ITEMS];  // digit << 16 | rank within the warp
+    // ---- records to registers, early tile counts, publish AGGREGATE
+    uint64_t k[SORT_ITEMS];
+    uint32_t dg[SORT_ITEMS];
 #pragma unroll
     for (int j = 0; j < SORT_ITEMS; j++) {
       const uint32_t idx = w * WARP_ITEMS + j * 32 + lane;
-      k[j] = idx < cnt ? B.keys[idx] : 0u;
+      k[j] = idx < cnt ? B[idx] : 0ull;
+      dg[j] = idx < cnt ? (uint32_t)(k[j] >> dsh) & 0xFF : 0x100u;
     }
 #pragma unroll
-    for (int j = 0; j < SORT_ITEMS; j++) {
-      const uint32_t idx = w * WARP_ITEMS + j * 32 + lane;
-      v[j] = idx < cnt ? B.vals[idx] : 0ull;
-    }
-#pragma unroll
-    for (int j = 0; j < SORT_ITEMS; j++) {
-      const uint32_t idx = w * WARP_ITEMS + j * 32 + lane;
-      const bool valid = idx < cnt;
-      const uint32_t d = valid ? (k[j] >> shift) & 0xFF : 0x100u;
-      const unsigned peers = __match_any_sync(FULL, d);
-      uint32_t prev = 0;
-      if (valid) prev = S.whist[w][d];
-      __syncwarp();
-      if (valid && lane == __ffs(peers) - 1) S.whist[w][d] = prev + __popc(peers);
-      __syncwarp();
-      rk[j] = (d << 16) | (prev + __popc(peers & lanemask_lt()));
-    }
+    for (int j = 0; j < SORT_ITEMS; j++)
+      if (dg[j] < RADIX) atomicAdd(&S.thist[w & 1][dg[j]], 1u);
     __syncthreads();
-
-    // ---- per digit: warp-exclusive prefix, tile count, publish, look-back
     const int d = t;  // SORT_THREADS == RADIX
-    uint32_t tile_cnt = 0;
-#pragma unroll
-    for (int ww = 0; ww < WARPS; ww++) {
-      const uint32_t c = S.whist[ww][d];
-      S.whist[ww][d] = tile_cnt;
-      tile_cnt += c;
-    }
+    const uint32_t tile_cnt = S.thist[0][d] + S.thist[1][d];
     unsigned long long* my_status = status + (size_t)tile * RADIX + d;
     if (tile == 0) st_relaxed(my_status, FLAG_INC | ep | tile_cnt);
     else st_relaxed(my_status, FLAG_AGG | ep | tile_cnt);
+    PHASE_T(2);
+
+    // ---- stable in-tile ranking (warp w owns items [w*512, w*512+512), striped)
+    uint32_t rk[SORT_ITEMS];  // rank within the warp
+#pragma unroll
+    for (int j = 0; j < SORT_ITEMS; j++) {
+      const bool valid = dg[j] < RADIX;
+      const unsigned peers = __match_any_sync(FULL, dg[j]);
+      uint32_t prev = 0;
+      if (valid) prev = S.whist[w][dg[j]];
+      __syncwarp();
+      if (valid && lane == __ffs(peers) - 1) S.whist[w][dg[j]] = prev + __popc(peers);
+      __syncwarp();
+      rk[j] = prev + __popc(peers & lanemask_lt());
+    }
+    __syncthreads();
+    PHASE_T(3);
+
+    // ---- per digit: warp-exclusive prefix, look-back, publish INCLUSIVE
+    {
+      uint32_t run = 0;
+#pragma unroll
+      for (int ww = 0; ww < WARPS; ww++) {
+        const uint32_t c = S.whist[ww][d];
+        S.whist[ww][d] = run;
+        run += c;
+      }
+    }
     const uint32_t excl_tile = block_excl_scan(tile_cnt, S.wt);
     S.tile_excl[d] = excl_tile;
     unsigned long long excl = 0;
@@ -282,99 +301,84 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) onesweep_kernel(
     }
     S.glob_base[d] = (uint32_t)(bin_off[d] + excl) - excl_tile;
     __syncthreads();
+    PHASE_T(4);
 
     // ---- scatter into shared memory in digit order (stable), in place
 #pragma unroll
     for (int j = 0; j < SORT_ITEMS; j++) {
-      const uint32_t dd = rk[j] >> 16;
-      if (dd < RADIX) {
-        const uint32_t pos = S.tile_excl[dd] + S.whist[w][dd] + (rk[j] & 0xFFFF);
-        B.keys[pos] = k[j];
-        B.vals[pos] = v[j];
-      }
+      const uint32_t dd = dg[j];
+      if (dd < RADIX) B[S.tile_excl[dd] + S.whist[w][dd] + rk[j]] = k[j];
     }
     __syncthreads();
+    PHASE_T(5);
 
     // ---- coalesced write-out: sorted position i goes to glob_base[digit] + i
     if (cnt == SORT_TILE) {
-      uint32_t o[SORT_ITEMS];
 #pragma unroll
-      for (int j = 0; j < SORT_ITEMS; j++) k[j] = B.keys[t + j * SORT_THREADS];
+      for (int j = 0; j < SORT_ITEMS; j++) k[j] = B[t + j * SORT_THREADS];
 #pragma unroll
-      for (int j = 0; j < SORT_ITEMS; j++) o[j] = S.glob_base[(k[j] >> shift) & 0xFF] + t + j * SORT_THREADS;
-#pragma unroll
-      for (int j = 0; j < SORT_ITEMS; j++) keys_out[o[j]] = k[j];
-#pragma unroll
-      for (int j = 0; j < SORT_ITEMS; j++) vals_out[o[j]] = B.vals[t + j * SORT_THREADS];
+      for (int j = 0; j < SORT_ITEMS; j++)
+        out[S.glob_base[(uint32_t)(k[j] >> dsh) & 0xFF] + t + j * SORT_THREADS] = k[j];
     } else {
       for (uint32_t i = t; i < cnt; i += SORT_THREADS) {
-        const uint32_t kk = B.keys[i];
-        const uint32_t o = S.glob_base[(kk >> shift) & 0xFF] + i;
-        keys_out[o] = kk;
-        vals_out[o] = B.vals[i];
+        const uint64_t kk = B[i];
+        out[S.glob_base[(uint32_t)(kk >> dsh) & 0xFF] + i] = kk;
       }
     }
     __syncthreads();  // buffer `cur`, whist, glob_base free for reuse
+    PHASE_T(6);
     cur ^= 1;
   }
 }
 
 size_t sort_tiles(size_t n) { return (n + SORT_TILE - 1) / SORT_TILE; }
 
-cudaError_t onesweep_sort(uint32_t* keys, uint64_t* vals, uint32_t n, int bits, SortWorkspace& ws,
-                          cudaStream_t s, bool* in_alt, Profiler* prof) {
+cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, int bits, SortWorkspace& ws, cudaStream_t s, bool* in_alt,
+                          Profiler* prof, bool hist_ready) {
   *in_alt = false;
   if (n == 0 || bits <= 0) return cudaSuccess;
   const int passes = (bits + 7) / 8;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(SortSmem));
-    if (e != cudaSuccess) return e;
-    cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    attr_set = true;
-  }
-  static int nsm = 0;
+  static int nsm = 0, per_sm = 0;
   if (!nsm) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
-  cudaMemsetAsync(ws.hist, 0, 4 * RADIX * sizeof(uint32_t), s);
-  cudaMemsetAsync(ws.tile_ctr, 0, 4 * sizeof(uint32_t), s);
-  const uint32_t hist_grid = (uint32_t)umin64((uint64_t)nsm * 8, (n + 256 * 16 - 1) / (256 * 16));
-  if (prof) prof->begin(s);
-  hist_kernel<<<hist_grid, 256, 0, s>>>(keys, n, passes, ws.hist);
-  bin_offsets_kernel<<<passes, 256, 0, s>>>(ws.hist, ws.bin_off);
-  launched(2);
-  if (prof) prof->end(RC_PROF_HIST, s, (uint64_t)n * 4, n);
-  const uint32_t tiles = (uint32_t)sort_tiles(n);
-  static int per_sm = 0;
-  if (!per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(SortSmem));
+    if (e != cudaSuccess) return e;
+    cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, onesweep_kernel, SORT_THREADS, sizeof(SortSmem));
     if (per_sm < 1) per_sm = 1;
   }
+  cudaMemsetAsync(ws.tile_ctr, 0, 4 * sizeof(uint32_t), s);
+  if (prof) prof->begin(s);
+  if (!hist_ready) {
+    cudaMemsetAsync(ws.hist, 0, 4 * RADIX * sizeof(uint32_t), s);
+    const uint32_t hist_grid = (uint32_t)umin64((uint64_t)nsm * 8, (n + 256 * 16 - 1) / (256 * 16));
+    hist_kernel<<<hist_grid, 256, 0, s>>>(recs, n, passes, ws.hist);
+    launched();
+  }
+  bin_offsets_kernel<<<passes, 256, 0, s>>>(ws.hist, ws.bin_off);
+  launched();
+  if (prof) prof->end(RC_PROF_HIST, s, hist_ready ? 0 : (uint64_t)n * 8, n);
+  const uint32_t tiles = (uint32_t)sort_tiles(n);
   // persistent: never more blocks than can be resident (look-back progress)
   const uint32_t grid = (uint32_t)umin64(tiles, (uint64_t)per_sm * nsm);
-  uint32_t* kin = keys;
-  uint64_t* vin = vals;
-  uint32_t* kout = ws.keys_alt;
-  uint64_t* vout = ws.vals_alt;
+  uint64_t* kin = recs;
+  uint64_t* kout = ws.alt;
   for (int p = 0; p < passes; p++) {
     if (++ws.epoch >= (1u << 22)) {  // epoch wrap: clear the look-back words once
       cudaMemsetAsync(ws.status, 0, ws.status_tiles * RADIX * sizeof(unsigned long long), s);
       ws.epoch = 1;
     }
     if (prof) prof->begin(s);
-    onesweep_kernel<<<grid, SORT_THREADS, sizeof(SortSmem), s>>>(kin, vin, kout, vout, n, 8 * p,
-                                                                 ws.bin_off + p * RADIX, ws.status,
-                                                                 ws.tile_ctr + p, ws.epoch);
+    onesweep_kernel<<<grid, SORT_THREADS, sizeof(SortSmem), s>>>(kin, kout, n, 8 * p, ws.bin_off + p * RADIX,
+                                                                ws.status, ws.tile_ctr + p, ws.epoch);
     launched();
-    if (prof) prof->end(RC_PROF_SORT, s, (uint64_t)n * 24, n);
+    if (prof) prof->end(RC_PROF_SORT, s, (uint64_t)n * 16, n);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     std::swap(kin, kout);
-    std::swap(vin, vout);
   }
   *in_alt = (passes & 1) != 0;
   return cudaGetLastError();
