@@ -289,7 +289,7 @@ def main():
                     "alg_bytes_per_record": 24, "launches": s["launches"] // args.steps,
                     "peak_source": peak_src}
         kernels = {}
-        for c in ("interp", "hist", "sort", "detect", "boundary", "finalize", "copy"):
+        for c in ("interp", "filter", "hist", "sort", "detect", "boundary", "finalize", "copy"):
             d = prof_sum[c]
             kernels[c] = {"launches_per_step": d["launches"] / args.steps, "ms_per_step": d["ms"] / args.steps,
                           "share": d["ms"] / prof_sum["total_ms"] if prof_sum["total_ms"] else None,

@@ -150,6 +150,7 @@ enum rc_prof_class {
   RC_PROF_BOUNDARY = 4, /* A4  barrier bookkeeping, divergence               */
   RC_PROF_FINALIZE = 5, /* K6  canonical report sort                         */
   RC_PROF_COPY = 6,     /* heap init / final-heap copies                     */
+  RC_PROF_FILTER = 7,   /* write-set filter of the read records  */
   RC_PROF_N = 8
 };
 typedef struct {

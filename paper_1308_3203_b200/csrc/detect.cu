@@ -86,7 +86,7 @@ __device__ __forceinline__ void rw_pair(bool hasr, uint32_t r1, uint32_t r2, uin
 // Serial path for a segment that does not fit one 32-record round: the head
 // thread walks it (pass 1: statistics; pass 2: first differing writer and
 // membership flags; pass 3 only for a non-benign pair with readers).
-__device__ __forceinline__ void serial_segment(const DetectParams& p, uint32_t i) {
+__device__ __forceinline__ void serial_segment(const DetectParams& p, uint32_t i, uint32_t n_records) {
   const uint32_t key = rec_cell(__ldg(p.recs + i));
   uint32_t r1 = INF, r2 = INF, rmax = 0, w1 = INF, w2 = INF, wmax = 0, nw = 0;
   bool hasr = false;
@@ -108,7 +108,7 @@ __device__ __forceinline__ void serial_segment(const DetectParams& p, uint32_t i
       hasr = true;
     }
     end++;
-  } while (end < p.n_records && rec_cell(__ldg(p.recs + end)) == key);
+  } while (end < n_records && rec_cell(__ldg(p.recs + end)) == key);
   if (nw == 0) return;  // only reads: no conflict, nothing to commit
   p.heap[key] = vwmax;  // barrier release: max-tid writer wins
   uint32_t t1, t2;
@@ -198,9 +198,10 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
   const unsigned FULL = 0xFFFFFFFFu;
   const int lane = threadIdx.x & 31;
   const uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t n_records = (uint32_t)(p.ctr->wlog_count + p.ctr->kept_count);
   const uint64_t c0 = wg * DET_CHUNK;
-  if (c0 >= p.n_records) return;  // whole warp
-  const uint64_t c1 = min((uint64_t)p.n_records, c0 + DET_CHUNK);
+  if (c0 >= n_records) return;  // whole warp
+  const uint64_t c1 = min((uint64_t)n_records, c0 + DET_CHUNK);
   const Seg ident{INF, 0u, 0u, 0, 0u};
   bool carry = false;       // an open segment started in an earlier round of this chunk
   uint64_t carry_start = 0;
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
     uint32_t prev = __shfl_up_sync(FULL, key, 1);
     if (lane == 0) prev = b > 0 ? rec_cell(__ldg(p.recs + b - 1)) : ~key;
     uint32_t next = __shfl_down_sync(FULL, key, 1);
-    if (lane == 31) next = r + 1 < p.n_records ? rec_cell(__ldg(p.recs + r + 1)) : ~key;
+    if (lane == 31) next = r + 1 < n_records ? rec_cell(__ldg(p.recs + r + 1)) : ~key;
     const bool head = inb && prev != key;
     const bool tail = inb && next != key;  // last record of its segment (possibly beyond c1)
     const unsigned heads = __ballot_sync(FULL, head);
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
       const Seg M = seg_merge(cs, S0);
       if (l0_closes) {
         if (lane == 0) {
-          if (seg_complex(M)) serial_segment(p, (uint32_t)carry_start);
+          if (seg_complex(M)) serial_segment(p, (uint32_t)carry_start, n_records);
           else if (M.nw == 1) p.heap[rec_cell(__ldg(p.recs + carry_start))] = M.vw;
         }
         carry = false;
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
     }
     // segments starting in this round
     if (head && closes) {
-      if (seg_complex(S)) serial_segment(p, (uint32_t)r);
+      if (seg_complex(S)) serial_segment(p, (uint32_t)r, n_records);
       else if (S.nw == 1) p.heap[key] = S.vw;
     }
     // the last segment of the round stays open: carry it
@@ -269,7 +270,7 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
       carry = true;
     }
   }
-  if (carry && lane == 0) serial_segment(p, (uint32_t)carry_start);  // continues into the next chunk
+  if (carry && lane == 0) serial_segment(p, (uint32_t)carry_start, n_records);  // continues into the next chunk
 }
 
 cudaError_t launch_detect(const DetectParams& p, cudaStream_t s) {

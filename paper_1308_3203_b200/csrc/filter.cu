@@ -1,0 +1,109 @@
+// filter.cu — write-set filter between K1 and the sort.
+//
+// A read record of a cell that no work-item wrote in this interval can take
+// part in no RW report (P:224-229 needs a writer), in no WW report and in no
+// commit, so it is dropped before the sort; the reads of written
+// cells are appended to the sort buffer after the write records.  K1 marked
+// every written cell in the byte map wmap (plain idempotent byte stores).
+// Exactness: the per-cell sets R(c) and W(c) of every cell with W(c) != {}
+// are unchanged, and cells with W(c) = {} produce no output.
+//
+// Also fuses the sort's digit histograms of the kept reads.
+#include "rc_internal.h"
+
+namespace rc {
+
+namespace {
+constexpr unsigned FULL = 0xFFFFFFFFu;
+constexpr int F_THREADS = 256, F_ITEMS = 4;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p) {
+  __shared__ uint32_t bh[4 * 256];
+  __shared__ uint32_t wcnt[F_THREADS / 32];
+  __shared__ unsigned long long sbase;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  for (int i = t; i < p.passes * 256; i += F_THREADS) bh[i] = 0;
+  const uint64_t nr = p.ctr->rlog_count;
+  const uint64_t nw = p.ctr->wlog_count;
+  const uint64_t step = (uint64_t)gridDim.x * F_THREADS * F_ITEMS;
+  __syncthreads();
+  for (uint64_t b0 = (uint64_t)blockIdx.x * F_THREADS * F_ITEMS; b0 < nr; b0 += step) {
+    uint64_t rec[F_ITEMS];
+    bool keep[F_ITEMS];
+#pragma unroll
+    for (int j = 0; j < F_ITEMS; j++) {
+      const uint64_t i = b0 + (uint64_t)j * F_THREADS + t;
+      rec[j] = i < nr ? __ldg(p.rlog + i) : 0ull;
+    }
+#pragma unroll
+    for (int j = 0; j < F_ITEMS; j++) {
+      const uint64_t i = b0 + (uint64_t)j * F_THREADS + t;
+      keep[j] = i < nr && __ldg(p.wmap + (rec[j] >> REC_CELL_SHIFT)) != 0;
+    }
+    uint32_t mine = 0;
+#pragma unroll
+    for (int j = 0; j < F_ITEMS; j++) mine += keep[j];
+    // block-exclusive offsets of this thread's kept records
+    uint32_t x = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wcnt[w] = x;
+    __syncthreads();
+    uint32_t woff = 0, tot = 0;
+    for (int i = 0; i < F_THREADS / 32; i++) {
+      if (i < w) woff += wcnt[i];
+      tot += wcnt[i];
+    }
+    if (t == 0) sbase = tot ? atomicAdd(&p.ctr->kept_count, (unsigned long long)tot) : 0ull;
+    __syncthreads();
+    uint64_t pos = nw + sbase + woff + x - mine;
+#pragma unroll
+    for (int j = 0; j < F_ITEMS; j++) {
+      if (keep[j]) p.out[pos++] = rec[j];
+      // digit histograms of kept reads (runs: one add when the warp agrees)
+      const unsigned mk = __ballot_sync(FULL, keep[j]);
+      if (mk) {
+        const int first = __ffs(mk) - 1;
+        for (int ps = 0; ps < p.passes; ps++) {
+          const uint32_t d = (uint32_t)(rec[j] >> (REC_CELL_SHIFT + 8 * ps)) & 0xFF;
+          const uint32_t d0 = __shfl_sync(FULL, d, first);
+          if (__all_sync(FULL, !keep[j] || d == d0)) {
+            if (lane == first) atomicAdd(&bh[ps * 256 + d0], (uint32_t)__popc(mk));
+          } else if (keep[j]) {
+            atomicAdd(&bh[ps * 256 + d], 1u);
+          }
+        }
+      }
+    }
+    __syncthreads();  // wcnt / sbase reuse
+  }
+  for (int i = t; i < p.passes * 256; i += F_THREADS)
+    if (bh[i]) atomicAdd(&p.hist[i], bh[i]);
+}
+
+cudaError_t launch_filter(const FilterParams& p, cudaStream_t s) {
+  if (p.n_reads_ub == 0) return cudaSuccess;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const uint64_t per_block = (uint64_t)F_THREADS * F_ITEMS;
+  const uint32_t grid = (uint32_t)std::min<uint64_t>((p.n_reads_ub + per_block - 1) / per_block, (uint64_t)nsm * 8);
+  filter_kernel<<<grid, F_THREADS, 0, s>>>(p);
+  launched();
+  return cudaGetLastError();
+}
+
+}  // namespace rc

@@ -1,6 +1,6 @@
 // interp.cu — K1: one barrier interval of the §4 thread-local semantics for
 // every live work-item of an instance batch, fused with the interval-boundary
-// bookkeeping (A4).
+// bookkeeping (A4), the write-set map and the sort's digit histograms.
 //
 // One CUDA thread = one simulated work-item (lane).  A warp is one instruction
 // stream: each step it executes the instruction at the minimum pc among its
@@ -8,6 +8,8 @@
 // memory), lanes at that pc execute it, the rest wait — a lane's result never
 // depends on the order because, inside an interval, lanes only see the
 // interval-start heap plus their own writes (delayed visibility, reading L2).
+// The grid is persistent: a block walks tiles of T lanes, so the program is
+// staged once and histograms / statistics are flushed once per block.
 //
 // Per lane: registers (Locals) live in shared memory laid out
 // [reg][thread] (a warp touching one register hits 32 distinct banks); only
@@ -22,14 +24,17 @@
 // costs one unit of fuel (reading L17).
 //
 // Log: a read record per performed LD, and at the end of the interval one
-// write record per distinct cell the lane wrote carrying its final value
-// (reading L3).  Records are staged per warp in shared memory and written out
-// by the block with ONE global atomic per block.
+// write record per distinct cell the lane wrote (its final value, reading L3,
+// goes to the side table wval[slot][lane]).  Records are staged per warp in
+// shared memory; the tile's write-out takes ONE atomic per record kind per
+// block: write records go straight into the sort buffer (and mark their cell
+// in the write-set byte map), read records into a staging buffer that the
+// write-set filter compacts (filter.cu).
 //
 // Fused A4 (reading L9): per instance the min / max arrival
 // node (BAR pc, or -1 for exit) of the lanes that arrived in this interval —
 // equal min and max means every arrival reached the same barrier — and a
-// global "some lane is suspended" flag.  One atomic per block and instance.
+// global "some lane is suspended" flag.
 #include "rc_internal.h"
 
 namespace rc {
@@ -72,56 +77,80 @@ struct Stage {
   uint32_t cap;
 };
 
-// Digit histograms of staged records (fused K2): each lane counts runs of
-// equal digits over a contiguous slice (staged records are nearly sorted by
-// cell, so runs are long) and adds each run once into the block histogram.
-__device__ __forceinline__ void hist_staged(const uint64_t* recs, uint32_t fill, int passes, uint32_t* bh,
+// digit histograms (fused K2) of the write records of one 32-record chunk:
+// when every write lane of the chunk has the same digit (long runs: records
+// are staged in lane order) one lane adds the whole count
+__device__ __forceinline__ void hist_writes(uint64_t rec, bool isw, unsigned mw, int passes, uint32_t* bh,
                                             int lane) {
-  const uint32_t per = (fill + 31) / 32;
-  const uint32_t lo = lane * per, hi = min(fill, lo + per);
+  if (!mw) return;
+  const int first = __ffs(mw) - 1;
   for (int p = 0; p < passes; p++) {
-    const int sh = REC_CELL_SHIFT + 8 * p;
-    uint32_t cur = 0xFFFFFFFFu, run = 0;
-    for (uint32_t i = lo; i < hi; i++) {
-      const uint32_t d = (uint32_t)(recs[i] >> sh) & 0xFF;
-      if (d == cur) run++;
-      else {
-        if (run) atomicAdd(&bh[p * 256 + cur], run);
-        cur = d;
-        run = 1;
-      }
+    const uint32_t d = (uint32_t)(rec >> (REC_CELL_SHIFT + 8 * p)) & 0xFF;
+    const uint32_t d0 = __shfl_sync(FULL, d, first);
+    if (__all_sync(FULL, !isw || d == d0)) {
+      if (lane == first) atomicAdd(&bh[p * 256 + d0], (uint32_t)__popc(mw));
+    } else if (isw) {
+      atomicAdd(&bh[p * 256 + d], 1u);
     }
-    if (run) atomicAdd(&bh[p * 256 + cur], run);
   }
 }
 
-// write this warp's staged records to the global log (mid-interval overflow path)
-__device__ __noinline__ uint32_t flush_warp_(DevCounters* ctr, uint64_t* log, unsigned long long log_cap,
-                                             const uint64_t* srecs, uint32_t fill, int lane, int passes,
-                                             uint32_t* bh) {
-  __syncwarp();
-  hist_staged(srecs, fill, passes, bh, lane);
-  unsigned long long base = 0;
-  if (lane == 0) base = atomicAdd(&ctr->log_count, (unsigned long long)fill);
-  base = __shfl_sync(FULL, base, 0);
-  bool over = false;
-  for (uint32_t i = lane; i < fill; i += 32) {
-    unsigned long long pos = base + i;
-    if (pos < log_cap) log[pos] = srecs[i];
-    else over = true;
+// Split-write `cnt` staged records of this warp: writes to wlog[bw + ...]
+// (marking wmap), reads to rlog[br + ...].  Whole warp.
+__device__ __forceinline__ void write_out(const InterpParams& p, const uint64_t* recs, uint32_t cnt,
+                                          unsigned long long bw, unsigned long long br, uint32_t* bh, int lane,
+                                          bool* over) {
+  uint32_t runw = 0, runr = 0;
+  for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const bool in = i < cnt;
+    const uint64_t rec = in ? recs[i] : 0ull;
+    const bool isw = in && (rec & 1);
+    const bool isr = in && !(rec & 1);
+    const unsigned mw = __ballot_sync(FULL, isw), mr = __ballot_sync(FULL, isr);
+    if (isw) {
+      const unsigned long long pos = bw + runw + __popc(mw & lanemask_lt());
+      if (pos < p.log_cap) p.wlog[pos] = rec;
+      else *over = true;
+      p.wmap[rec >> REC_CELL_SHIFT] = 1;
+    }
+    if (isr) {
+      const unsigned long long pos = br + runr + __popc(mr & lanemask_lt());
+      if (pos < p.log_cap) p.rlog[pos] = rec;
+      else *over = true;
+    }
+    hist_writes(rec, isw, mw, p.passes, bh, lane);
+    runw += __popc(mw);
+    runr += __popc(mr);
   }
-  if (__any_sync(FULL, over) && lane == 0) ctr->log_overflow = 1;
+}
+
+__device__ __forceinline__ uint32_t count_writes(const uint64_t* recs, uint32_t cnt, int lane) {
+  uint32_t c = 0;
+  for (uint32_t i = lane; i < cnt; i += 32) c += (uint32_t)(recs[i] & 1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+  return c;
+}
+
+// mid-interval overflow of a warp's staging buffer: flush it on its own
+__device__ __noinline__ uint32_t flush_warp_(const InterpParams* pp, const uint64_t* recs, uint32_t fill, int lane,
+                                             uint32_t* bh) {
+  const InterpParams& p = *pp;
+  __syncwarp();
+  const uint32_t nw = count_writes(recs, fill, lane);
+  unsigned long long bw = 0, br = 0;
+  if (lane == 0) {
+    bw = atomicAdd(&p.ctr->wlog_count, (unsigned long long)nw);
+    br = atomicAdd(&p.ctr->rlog_count, (unsigned long long)(fill - nw));
+  }
+  bw = __shfl_sync(FULL, bw, 0);
+  br = __shfl_sync(FULL, br, 0);
+  bool over = false;
+  write_out(p, recs, fill, bw, br, bh, lane, &over);
+  if (__any_sync(FULL, over) && lane == 0) p.ctr->log_overflow = 1;
   __syncwarp();
   return 0;
-}
-
-// warp-aggregated append of one record per lane in `m` (called by the whole warp)
-__device__ __forceinline__ void stage_append(const InterpParams& p, Stage& S, int lane, unsigned m, bool mine,
-                                             uint64_t rec, uint32_t* bh) {
-  const uint32_t cnt = __popc(m);
-  if (S.fill + cnt > S.cap) S.fill = flush_warp_(p.ctr, p.log, p.log_cap, S.recs, S.fill, lane, p.passes, bh);
-  if (mine) S.recs[S.fill + __popc(m & lanemask_lt())] = rec;
-  S.fill += cnt;
 }
 
 __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
@@ -153,11 +182,13 @@ __global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
   int32_t* oval = reinterpret_cast<int32_t*>(q); q += (size_t)OV * T * 4;
   uint32_t* s_off = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
   uint32_t* s_size = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
-  uint32_t* wcnt = reinterpret_cast<uint32_t*>(q); q += (size_t)W * 4;
-  int32_t* wnode = reinterpret_cast<int32_t*>(q); q += (size_t)2 * W * 4;   // per-warp min / max node
+  uint32_t* wcntw = reinterpret_cast<uint32_t*>(q); q += (size_t)W * 4;   // per-warp write records
+  uint32_t* wcntr = reinterpret_cast<uint32_t*>(q); q += (size_t)W * 4;   // per-warp read records (|wait flag)
+  int32_t* wnode = reinterpret_cast<int32_t*>(q); q += (size_t)2 * W * 4;  // per-warp min / max node
+  uint32_t* winst = reinterpret_cast<uint32_t*>(q); q += (size_t)W * 4;   // warp instance (or ~0)
   q = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(q) + 7) & ~uintptr_t(7));
-  unsigned long long* wbase = reinterpret_cast<unsigned long long*>(q); q += (size_t)W * 8;
-  unsigned long long* wstat = reinterpret_cast<unsigned long long*>(q);    // [3][W]
+  unsigned long long* wbase = reinterpret_cast<unsigned long long*>(q); q += (size_t)2 * W * 8;  // [W] w, [W] r
+  unsigned long long* wstat = reinterpret_cast<unsigned long long*>(q);  // [3][W]
 
   for (uint32_t a = t; a < p.n_arrays; a += T) {
     s_off[a] = p.arr_off[a];
@@ -169,304 +200,323 @@ __global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
   }
   for (int i = t; i < p.passes * 256; i += T) bhist[i] = 0;
 
-  const uint32_t g = blockIdx.x * (uint32_t)T + t;
-  const bool valid = g < p.n_lanes;
-  uint8_t status = valid ? p.status_in[g] : (uint8_t)L_EXITED;
-  if (status == L_EXITED_NOW) status = L_EXITED;
-  bool running = valid && (status == L_RUNNING || status == L_WAITING);
-  const uint32_t inst = valid ? g / p.n : 0;
-  const uint32_t tid = valid ? g - inst * p.n : 0;
-  const uint32_t cell_base = inst * p.cpi;
-  uint32_t pc = running ? p.pc_in[g] : 0;
-  int32_t* Rg = sregs + t;  // register r of this lane = Rg[r*T]
-  if (running)
-    for (uint32_t i = 0; i < p.n_live; i++) {
-      const uint32_t r = __ldg(p.live + i);
-      Rg[r * T] = p.regs_in[(size_t)r * p.n_lanes + g];
-    }
-  __syncthreads();
+  // block totals kept by thread 0 across tiles
+  unsigned long long b_instr = 0, b_loads = 0, b_stores = 0;
+  bool b_wait = false, b_over = false;
+  const uint32_t n_tiles = (p.n_lanes + T - 1) / T;
 
-  if (running) status = L_RUNNING;
-  int n_own = 0;
-  unsigned long long steps = 0;
-  uint32_t nloads = 0, nstores = 0;
-  bool ovl_over = false;
-  Stage S{st_recs + (size_t)warp * p.stage, 0, p.stage};
-
-  for (;;) {
-    if (__ballot_sync(FULL, running) == 0) break;
-    const uint32_t minpc = __reduce_min_sync(FULL, running ? pc : 0xFFFFFFFFu);
-    bool ex = running && pc == minpc;
-    const uint2 raw = CODE_SMEM ? s_code[minpc] : __ldg(reinterpret_cast<const uint2*>(p.code) + minpc);
-    const uint32_t op = raw.x & 0xFF, ia = (raw.x >> 8) & 0xFF, ib = (raw.x >> 16) & 0xFF, ic = raw.x >> 24;
-    const int32_t imm = (int32_t)raw.y;
-    if (ex) {  // fuel check before executing (reading L17)
-      if (steps == p.fuel) {
-        emit_report(p, inst, -1, (int32_t)pc, tid, RC_FUEL);
-        running = false;
-        status = L_FUEL;
-        ex = false;
-      } else {
-        steps++;
-      }
-    }
-    switch (op) {  // warp-uniform
-      case RC_OP_CONST: if (ex) { Rg[ia * T] = imm; pc++; } break;
-      case RC_OP_MOV: if (ex) { Rg[ia * T] = Rg[ib * T]; pc++; } break;
-      case RC_OP_TID: if (ex) { Rg[ia * T] = (int32_t)tid; pc++; } break;
-      case RC_OP_SIZE: if (ex) { Rg[ia * T] = (int32_t)s_size[ib]; pc++; } break;
-      case RC_OP_ADDI: if (ex) { Rg[ia * T] = wadd(Rg[ib * T], imm); pc++; } break;
-      case RC_OP_ADD: case RC_OP_SUB: case RC_OP_MUL: case RC_OP_MIN: case RC_OP_MAX: case RC_OP_AND:
-      case RC_OP_OR: case RC_OP_XOR: case RC_OP_LT: case RC_OP_EQ: case RC_OP_LAND:
-        if (ex) {
-          const int32_t x = Rg[ib * T], y = Rg[ic * T];
-          int32_t v;
-          switch (op) {
-            case RC_OP_ADD: v = wadd(x, y); break;
-            case RC_OP_SUB: v = (int32_t)((uint32_t)x - (uint32_t)y); break;
-            case RC_OP_MUL: v = (int32_t)((uint32_t)x * (uint32_t)y); break;
-            case RC_OP_MIN: v = min(x, y); break;
-            case RC_OP_MAX: v = max(x, y); break;
-            case RC_OP_AND: v = x & y; break;
-            case RC_OP_OR: v = x | y; break;
-            case RC_OP_XOR: v = x ^ y; break;
-            case RC_OP_LT: v = x < y; break;
-            case RC_OP_EQ: v = x == y; break;
-            default: v = (x != 0) && (y != 0); break;
-          }
-          Rg[ia * T] = v;
-          pc++;
-        }
-        break;
-      case RC_OP_DIV: case RC_OP_MOD:
-        if (ex) {
-          const int32_t x = Rg[ib * T], y = Rg[ic * T];
-          if (y == 0) {
-            emit_report(p, inst, -1, (int32_t)pc, tid, RC_DIV0);
-            running = false;
-            status = L_DIV0;
-          } else {
-            int32_t v;
-            if (op == RC_OP_DIV) v = (y == -1) ? (int32_t)(0u - (uint32_t)x) : x / y;
-            else v = (y == -1) ? 0 : x % y;
-            Rg[ia * T] = v;
-            pc++;
-          }
-        }
-        break;
-      case RC_OP_LNOT: if (ex) { Rg[ia * T] = Rg[ib * T] == 0; pc++; } break;
-      case RC_OP_LD: {
-        bool ok = false;
-        uint32_t cell = 0;
-        if (ex) {
-          const int32_t idx = Rg[ic * T];
-          if (idx < 0 || (uint32_t)idx >= s_size[ib]) {
-            emit_report(p, inst, (int32_t)ib, idx, tid, RC_OOB);
-            running = false;
-            status = L_OOB;
-          } else {
-            cell = cell_base + s_off[ib] + (uint32_t)idx;
-            int32_t v = 0;
-            bool found = false;
-            for (int j = 0; j < n_own; j++)
-              if (ocell[j * T + t] == cell) { v = oval[j * T + t]; found = true; }
-            if (!found) v = __ldg(p.heap + cell);
-            Rg[ia * T] = v;
-            pc++;
-            nloads++;
-            ok = true;
-          }
-        }
-        const unsigned m = __ballot_sync(FULL, ok);
-        if (m) stage_append(p, S, lane, m, ok, make_rec(cell, tid, 0, 0), bhist);
-        break;
-      }
-      case RC_OP_ST:
-        if (ex) {
-          const int32_t idx = Rg[ib * T];
-          if (idx < 0 || (uint32_t)idx >= s_size[ia]) {
-            emit_report(p, inst, (int32_t)ia, idx, tid, RC_OOB);
-            running = false;
-            status = L_OOB;
-          } else {
-            const uint32_t cell = cell_base + s_off[ia] + (uint32_t)idx;
-            int j = 0;
-            while (j < n_own && ocell[j * T + t] != cell) j++;
-            if (j == n_own) {
-              if (n_own < (int)OV) { ocell[j * T + t] = cell; n_own++; }
-              else { ovl_over = true; j = -1; }
-            }
-            if (j >= 0) oval[j * T + t] = Rg[ic * T];
-            pc++;
-            nstores++;
-          }
-        }
-        break;
-      case RC_OP_BAR: if (ex) { pc++; running = false; status = L_WAITING; } break;
-      case RC_OP_EXIT: if (ex) { running = false; status = L_EXITED_NOW; } break;
-      case RC_OP_ASSUME:
-        if (ex) {
-          if (Rg[ia * T] == 0) { running = false; status = L_PRUNED; }
-          else pc++;
-        }
-        break;
-      case RC_OP_ASSERT:
-        if (ex) {
-          if (Rg[ia * T] == 0) {
-            emit_report(p, inst, -1, (int32_t)pc, tid, RC_ASSERT);
-            running = false;
-            status = L_ASSERT;
-          } else {
-            pc++;
-          }
-        }
-        break;
-      case RC_OP_BR: if (ex) pc = Rg[ia * T] != 0 ? (uint32_t)imm : ib + 256u * ic; break;
-      case RC_OP_JMP: if (ex) pc = (uint32_t)imm; break;
-      default: break;  // unreachable: the validator rejects unknown opcodes
-    }
-  }
-
-  // write records: one per distinct written cell; its final value (reading
-  // L3) goes to the side table wval[slot][lane] read by detect
-  const int max_own = __reduce_max_sync(FULL, (unsigned)n_own);
-  for (int j = 0; j < max_own; j++) {
-    const bool has = j < n_own;
-    const unsigned m = __ballot_sync(FULL, has);
-    uint64_t rec = 0;
-    if (has) {
-      rec = make_rec(ocell[j * T + t], tid, (uint32_t)j, 1);
-      p.wval[(size_t)j * p.n_lanes + g] = oval[j * T + t];
-    }
-    stage_append(p, S, lane, m, has, rec, bhist);
-  }
-
-  // lane state out (only registers live across the barrier, only for suspended lanes)
-  if (valid) {
-    p.status_out[g] = status;
-    if (status == L_WAITING) {
-      p.pc_out[g] = pc;
+  for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const uint32_t g = tile * (uint32_t)T + t;
+    const bool valid = g < p.n_lanes;
+    uint8_t status = valid ? p.status_in[g] : (uint8_t)L_EXITED;
+    if (status == L_EXITED_NOW) status = L_EXITED;
+    bool running = valid && (status == L_RUNNING || status == L_WAITING);
+    const uint32_t inst = valid ? g / p.n : 0;
+    const uint32_t tid = valid ? g - inst * p.n : 0;
+    const uint32_t cell_base = inst * p.cpi;
+    uint32_t pc = running ? p.pc_in[g] : 0;
+    int32_t* Rg = sregs + t;  // register r of this lane = Rg[r*T]
+    if (running)
       for (uint32_t i = 0; i < p.n_live; i++) {
         const uint32_t r = __ldg(p.live + i);
-        p.regs_out[(size_t)r * p.n_lanes + g] = Rg[r * T];
+        Rg[r * T] = p.regs_in[(size_t)r * p.n_lanes + g];
       }
-    }
-  }
+    __syncthreads();
 
-  // fused A4: arrival node range per instance, suspended flag
-  const bool arrived = valid && (status == L_WAITING || status == L_EXITED_NOW);
-  const int32_t node = status == L_WAITING ? (int32_t)pc - 1 : NODE_EXIT;
-  const bool any_wait = __any_sync(FULL, status == L_WAITING);
-  const uint32_t inst0 = __shfl_sync(FULL, inst, 0);
-  const bool warp_uniform = __all_sync(FULL, !valid || inst == inst0);
-  const unsigned am = __ballot_sync(FULL, arrived);
-  // nodes are >= -1; bias by 1 so unsigned reductions apply
-  const uint32_t nmin = __reduce_min_sync(FULL, arrived ? (uint32_t)(node + 1) : 0xFFFFFFFFu);
-  const uint32_t nmax = __reduce_max_sync(FULL, arrived ? (uint32_t)(node + 1) : 0u);
-  if (!warp_uniform && arrived) {  // small work-groups: per-lane atomics
-    atomicMin(p.node_min + inst, node);
-    atomicMax(p.node_max + inst, node);
-  }
+    if (running) status = L_RUNNING;
+    int n_own = 0;
+    unsigned long long steps = 0;
+    uint32_t nloads = 0, nstores = 0;
+    bool ovl_over = false;
+    Stage S{st_recs + (size_t)warp * p.stage, 0, p.stage};
 
-  // block-level log write-out (one atomic per block) and A4 reductions
-  unsigned long long s0 = warp_sum64(steps), s1 = warp_sum64(nloads), s2 = warp_sum64(nstores);
-  const bool any_ovl = __any_sync(FULL, ovl_over);
-  if (lane == 0) {
-    wcnt[warp] = S.fill;
-    wstat[warp] = s0;
-    wstat[W + warp] = s1;
-    wstat[2 * W + warp] = s2;
-    if (any_ovl) p.ctr->ovl_overflow = 1;
-    // per-warp node range; 0xFFFFFFFF marks "no warp-uniform arrival"
-    wnode[warp] = (warp_uniform && am) ? (int32_t)(nmin - 1) : 0x7FFFFFFF;
-    wnode[W + warp] = (warp_uniform && am) ? (int32_t)(nmax - 1) : (int32_t)0x80000000;
-    wcnt[warp] |= (any_wait ? 0x80000000u : 0u);
-    // instance of the warp (valid lanes only) kept in wbase temporarily
-    wbase[warp] = warp_uniform ? inst0 : 0xFFFFFFFFull;
-  }
-  __syncthreads();
-  if (t == 0) {
-    unsigned long long tot = 0, a0 = 0, a1 = 0, a2 = 0;
-    bool wait_any = false;
-    // node range: combine consecutive warps of the same instance
-    uint32_t cur_inst = 0xFFFFFFFFu;
-    int32_t cmin = 0x7FFFFFFF, cmax = (int32_t)0x80000000;
-    for (int w = 0; w < W; w++) {
-      const uint32_t wi = (uint32_t)wbase[w];
-      if (wi != cur_inst) {
-        if (cur_inst != 0xFFFFFFFFu && cmin <= cmax) {
-          atomicMin(p.node_min + cur_inst, cmin);
-          atomicMax(p.node_max + cur_inst, cmax);
+    for (;;) {
+      if (__ballot_sync(FULL, running) == 0) break;
+      const uint32_t minpc = __reduce_min_sync(FULL, running ? pc : 0xFFFFFFFFu);
+      bool ex = running && pc == minpc;
+      const uint2 raw = CODE_SMEM ? s_code[minpc] : __ldg(reinterpret_cast<const uint2*>(p.code) + minpc);
+      const uint32_t op = raw.x & 0xFF, ia = (raw.x >> 8) & 0xFF, ib = (raw.x >> 16) & 0xFF, ic = raw.x >> 24;
+      const int32_t imm = (int32_t)raw.y;
+      if (ex) {  // fuel check before executing (reading L17)
+        if (steps == p.fuel) {
+          emit_report(p, inst, -1, (int32_t)pc, tid, RC_FUEL);
+          running = false;
+          status = L_FUEL;
+          ex = false;
+        } else {
+          steps++;
         }
-        cur_inst = wi;
-        cmin = 0x7FFFFFFF;
-        cmax = (int32_t)0x80000000;
       }
-      cmin = min(cmin, wnode[w]);
-      cmax = max(cmax, wnode[W + w]);
+      switch (op) {  // warp-uniform
+        case RC_OP_CONST: if (ex) { Rg[ia * T] = imm; pc++; } break;
+        case RC_OP_MOV: if (ex) { Rg[ia * T] = Rg[ib * T]; pc++; } break;
+        case RC_OP_TID: if (ex) { Rg[ia * T] = (int32_t)tid; pc++; } break;
+        case RC_OP_SIZE: if (ex) { Rg[ia * T] = (int32_t)s_size[ib]; pc++; } break;
+        case RC_OP_ADDI: if (ex) { Rg[ia * T] = wadd(Rg[ib * T], imm); pc++; } break;
+        case RC_OP_ADD: case RC_OP_SUB: case RC_OP_MUL: case RC_OP_MIN: case RC_OP_MAX: case RC_OP_AND:
+        case RC_OP_OR: case RC_OP_XOR: case RC_OP_LT: case RC_OP_EQ: case RC_OP_LAND:
+          if (ex) {
+            const int32_t x = Rg[ib * T], y = Rg[ic * T];
+            int32_t v;
+            switch (op) {
+              case RC_OP_ADD: v = wadd(x, y); break;
+              case RC_OP_SUB: v = (int32_t)((uint32_t)x - (uint32_t)y); break;
+              case RC_OP_MUL: v = (int32_t)((uint32_t)x * (uint32_t)y); break;
+              case RC_OP_MIN: v = min(x, y); break;
+              case RC_OP_MAX: v = max(x, y); break;
+              case RC_OP_AND: v = x & y; break;
+              case RC_OP_OR: v = x | y; break;
+              case RC_OP_XOR: v = x ^ y; break;
+              case RC_OP_LT: v = x < y; break;
+              case RC_OP_EQ: v = x == y; break;
+              default: v = (x != 0) && (y != 0); break;
+            }
+            Rg[ia * T] = v;
+            pc++;
+          }
+          break;
+        case RC_OP_DIV: case RC_OP_MOD:
+          if (ex) {
+            const int32_t x = Rg[ib * T], y = Rg[ic * T];
+            if (y == 0) {
+              emit_report(p, inst, -1, (int32_t)pc, tid, RC_DIV0);
+              running = false;
+              status = L_DIV0;
+            } else {
+              int32_t v;
+              if (op == RC_OP_DIV) v = (y == -1) ? (int32_t)(0u - (uint32_t)x) : x / y;
+              else v = (y == -1) ? 0 : x % y;
+              Rg[ia * T] = v;
+              pc++;
+            }
+          }
+          break;
+        case RC_OP_LNOT: if (ex) { Rg[ia * T] = Rg[ib * T] == 0; pc++; } break;
+        case RC_OP_LD: {
+          bool ok = false;
+          uint32_t cell = 0;
+          if (ex) {
+            const int32_t idx = Rg[ic * T];
+            if (idx < 0 || (uint32_t)idx >= s_size[ib]) {
+              emit_report(p, inst, (int32_t)ib, idx, tid, RC_OOB);
+              running = false;
+              status = L_OOB;
+            } else {
+              cell = cell_base + s_off[ib] + (uint32_t)idx;
+              int32_t v = 0;
+              bool found = false;
+              for (int j = 0; j < n_own; j++)
+                if (ocell[j * T + t] == cell) { v = oval[j * T + t]; found = true; }
+              if (!found) v = __ldg(p.heap + cell);
+              Rg[ia * T] = v;
+              pc++;
+              nloads++;
+              ok = true;
+            }
+          }
+          const unsigned m = __ballot_sync(FULL, ok);
+          if (m) {
+            if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(&p, S.recs, S.fill, lane, bhist);
+            if (ok) S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, tid, 0, 0);
+            S.fill += __popc(m);
+          }
+          break;
+        }
+        case RC_OP_ST:
+          if (ex) {
+            const int32_t idx = Rg[ib * T];
+            if (idx < 0 || (uint32_t)idx >= s_size[ia]) {
+              emit_report(p, inst, (int32_t)ia, idx, tid, RC_OOB);
+              running = false;
+              status = L_OOB;
+            } else {
+              const uint32_t cell = cell_base + s_off[ia] + (uint32_t)idx;
+              int j = 0;
+              while (j < n_own && ocell[j * T + t] != cell) j++;
+              if (j == n_own) {
+                if (n_own < (int)OV) { ocell[j * T + t] = cell; n_own++; }
+                else { ovl_over = true; j = -1; }
+              }
+              if (j >= 0) oval[j * T + t] = Rg[ic * T];
+              pc++;
+              nstores++;
+            }
+          }
+          break;
+        case RC_OP_BAR: if (ex) { pc++; running = false; status = L_WAITING; } break;
+        case RC_OP_EXIT: if (ex) { running = false; status = L_EXITED_NOW; } break;
+        case RC_OP_ASSUME:
+          if (ex) {
+            if (Rg[ia * T] == 0) { running = false; status = L_PRUNED; }
+            else pc++;
+          }
+          break;
+        case RC_OP_ASSERT:
+          if (ex) {
+            if (Rg[ia * T] == 0) {
+              emit_report(p, inst, -1, (int32_t)pc, tid, RC_ASSERT);
+              running = false;
+              status = L_ASSERT;
+            } else {
+              pc++;
+            }
+          }
+          break;
+        case RC_OP_BR: if (ex) pc = Rg[ia * T] != 0 ? (uint32_t)imm : ib + 256u * ic; break;
+        case RC_OP_JMP: if (ex) pc = (uint32_t)imm; break;
+        default: break;  // unreachable: the validator rejects unknown opcodes
+      }
     }
-    if (cur_inst != 0xFFFFFFFFu && cmin <= cmax) {
-      atomicMin(p.node_min + cur_inst, cmin);
-      atomicMax(p.node_max + cur_inst, cmax);
+
+    // write records: one per distinct written cell; its final value (reading
+    // L3) goes to the side table wval[slot][lane] read by detect
+    const int max_own = __reduce_max_sync(FULL, (unsigned)n_own);
+    for (int j = 0; j < max_own; j++) {
+      const bool has = j < n_own;
+      const unsigned m = __ballot_sync(FULL, has);
+      if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(&p, S.recs, S.fill, lane, bhist);
+      if (has) {
+        S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(ocell[j * T + t], tid, (uint32_t)j, 1);
+        p.wval[(size_t)j * p.n_lanes + g] = oval[j * T + t];
+      }
+      S.fill += __popc(m);
     }
-    for (int w = 0; w < W; w++) {
-      wait_any |= (wcnt[w] & 0x80000000u) != 0;
-      const uint32_t c = wcnt[w] & 0x7FFFFFFFu;
-      wbase[w] = tot;
-      tot += c;
-      a0 += wstat[w];
-      a1 += wstat[W + w];
-      a2 += wstat[2 * W + w];
+
+    // lane state out (only registers live across the barrier, only for suspended lanes)
+    if (valid) {
+      p.status_out[g] = status;
+      if (status == L_WAITING) {
+        p.pc_out[g] = pc;
+        for (uint32_t i = 0; i < p.n_live; i++) {
+          const uint32_t r = __ldg(p.live + i);
+          p.regs_out[(size_t)r * p.n_lanes + g] = Rg[r * T];
+        }
+      }
     }
-    const unsigned long long base = tot ? atomicAdd(&p.ctr->log_count, tot) : 0ull;
-    for (int w = 0; w < W; w++) wbase[w] += base;
-    if (base + tot > p.log_cap) p.ctr->log_overflow = 1;
-    if (a0) atomicAdd(&p.ctr->iv_instr, a0);
-    if (a1) atomicAdd(&p.ctr->iv_loads, a1);
-    if (a2) atomicAdd(&p.ctr->iv_stores, a2);
-    if (wait_any) p.ctr->any_waiting = 1;
+
+    // fused A4: arrival node range per instance, suspended flag
+    const bool arrived = valid && (status == L_WAITING || status == L_EXITED_NOW);
+    const int32_t node = status == L_WAITING ? (int32_t)pc - 1 : NODE_EXIT;
+    const bool any_wait = __any_sync(FULL, status == L_WAITING);
+    const uint32_t inst0 = __shfl_sync(FULL, inst, 0);
+    const bool warp_uniform = __all_sync(FULL, !valid || inst == inst0);
+    const unsigned am = __ballot_sync(FULL, arrived);
+    // nodes are >= -1; bias by 1 so unsigned reductions apply
+    const uint32_t nmin = __reduce_min_sync(FULL, arrived ? (uint32_t)(node + 1) : 0xFFFFFFFFu);
+    const uint32_t nmax = __reduce_max_sync(FULL, arrived ? (uint32_t)(node + 1) : 0u);
+    if (!warp_uniform && arrived) {  // small work-groups: per-lane atomics
+      atomicMin(p.node_min + inst, node);
+      atomicMax(p.node_max + inst, node);
+    }
+
+    // ---- tile write-out: one atomic per record kind per block
+    const unsigned long long s0 = warp_sum64(steps), s1 = warp_sum64(nloads), s2 = warp_sum64(nstores);
+    const bool any_ovl = __any_sync(FULL, ovl_over);
+    const uint32_t nw = count_writes(S.recs, S.fill, lane);
+    if (lane == 0) {
+      wcntw[warp] = nw;
+      wcntr[warp] = (S.fill - nw) | (any_wait ? 0x80000000u : 0u);
+      wstat[warp] = s0;
+      wstat[W + warp] = s1;
+      wstat[2 * W + warp] = s2;
+      if (any_ovl) p.ctr->ovl_overflow = 1;
+      wnode[warp] = (warp_uniform && am) ? (int32_t)(nmin - 1) : 0x7FFFFFFF;
+      wnode[W + warp] = (warp_uniform && am) ? (int32_t)(nmax - 1) : (int32_t)0x80000000;
+      winst[warp] = warp_uniform ? inst0 : 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    if (t == 0) {
+      // node range: combine consecutive warps of the same instance
+      uint32_t cur_inst = 0xFFFFFFFFu;
+      int32_t cmin = 0x7FFFFFFF, cmax = (int32_t)0x80000000;
+      for (int w = 0; w <= W; w++) {
+        const uint32_t wi = w < W ? winst[w] : 0xFFFFFFFFu;
+        if (w == W || wi != cur_inst) {
+          if (cur_inst != 0xFFFFFFFFu && cmin <= cmax) {
+            atomicMin(p.node_min + cur_inst, cmin);
+            atomicMax(p.node_max + cur_inst, cmax);
+          }
+          cur_inst = wi;
+          cmin = 0x7FFFFFFF;
+          cmax = (int32_t)0x80000000;
+        }
+        if (w < W) {
+          cmin = min(cmin, wnode[w]);
+          cmax = max(cmax, wnode[W + w]);
+        }
+      }
+      unsigned long long totw = 0, totr = 0;
+      for (int w = 0; w < W; w++) {
+        b_wait |= (wcntr[w] & 0x80000000u) != 0;
+        wbase[w] = totw;
+        wbase[W + w] = totr;
+        totw += wcntw[w];
+        totr += wcntr[w] & 0x7FFFFFFFu;
+        b_instr += wstat[w];
+        b_loads += wstat[W + w];
+        b_stores += wstat[2 * W + w];
+      }
+      const unsigned long long bw = totw ? atomicAdd(&p.ctr->wlog_count, totw) : 0ull;
+      const unsigned long long br = totr ? atomicAdd(&p.ctr->rlog_count, totr) : 0ull;
+      for (int w = 0; w < W; w++) {
+        wbase[w] += bw;
+        wbase[W + w] += br;
+      }
+    }
+    __syncthreads();
+    write_out(p, S.recs, S.fill, wbase[warp], wbase[W + warp], bhist, lane, &b_over);
+    __syncthreads();  // staging / overlay / registers reused by the next tile
   }
-  __syncthreads();
-  const unsigned long long base = wbase[warp];
-  for (uint32_t i = lane; i < S.fill; i += 32) {
-    const unsigned long long pos = base + i;
-    if (pos < p.log_cap) p.log[pos] = S.recs[i];
-  }
-  hist_staged(S.recs, S.fill, p.passes, bhist, lane);
-  __syncthreads();
+
+  // ---- block flush: histograms, statistics, flags
   for (int i = t; i < p.passes * 256; i += T)
     if (bhist[i]) atomicAdd(&p.hist[i], bhist[i]);
+  if (__any_sync(FULL, b_over) && lane == 0) p.ctr->log_overflow = 1;
+  if (t == 0) {
+    if (b_instr) atomicAdd(&p.ctr->iv_instr, b_instr);
+    if (b_loads) atomicAdd(&p.ctr->iv_loads, b_loads);
+    if (b_stores) atomicAdd(&p.ctr->iv_stores, b_stores);
+    if (b_wait) p.ctr->any_waiting = 1;
+  }
 }
 
 size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem) {
   const int W = T / 32;
   size_t b = (size_t)W * p.stage * 8;              // staging
-  b += (size_t)p.passes * 256 * 4;                 // block digit histograms
   b += code_in_smem ? (size_t)p.n_instr * 8 : 0;   // program
+  b += (size_t)p.passes * 256 * 4;                 // block digit histograms
   b += (size_t)p.n_regs * T * 4;                   // registers
   b += (size_t)p.ovl_cap * T * 8;                  // overlay
   b += (size_t)p.n_arrays * 8;                     // array offsets / sizes
-  b += (size_t)W * 12 + 8;                         // warp counts, node range (+align)
-  b += (size_t)W * 8 * 4;                          // warp bases + 3 stats
+  b += (size_t)W * 20 + 8;                         // warp counts, node range, instance (+align)
+  b += (size_t)W * 8 * 5;                          // warp bases (2) + 3 stats
   return b;
 }
 
 cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
   if (p.n_lanes == 0) return cudaSuccess;
   static bool attr_set = false;
+  static int nsm = 0;
   if (!attr_set) {
     for (auto f : {interp_kernel<true>, interp_kernel<false>}) {
       cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       if (e != cudaSuccess) return e;
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     attr_set = true;
   }
   const bool code_smem = p.n_instr <= 2048;
   int T = 256;
   while (T > 32 && interp_smem_bytes(p, T, code_smem) > 96 * 1024) T >>= 1;
   const size_t sm = interp_smem_bytes(p, T, code_smem);
-  const uint32_t grid = (p.n_lanes + T - 1) / T;
+  int per_sm = 1;
+  if (code_smem) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, interp_kernel<true>, T, sm);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, interp_kernel<false>, T, sm);
+  const uint32_t tiles = (p.n_lanes + T - 1) / T;
+  const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)std::max(1, per_sm) * nsm);
   if (code_smem) interp_kernel<true><<<grid, T, sm, s>>>(p);
   else interp_kernel<false><<<grid, T, sm, s>>>(p);
   launched();

@@ -58,7 +58,9 @@ static_assert(RC_OVERLAY_CAP == OVL_CAP, "overlay capacity in rc.h and the inter
 
 // Device counters of one run; zeroed per attempt where noted.
 struct DevCounters {
-  unsigned long long log_count;     // records appended this interval (per attempt)
+  unsigned long long wlog_count;    // write records this interval (per attempt)
+  unsigned long long rlog_count;    // read records this interval (per attempt)
+  unsigned long long kept_count;    // read records kept by the write-set filter
   unsigned long long report_count;  // reports appended (whole run, rolled back on retry)
   unsigned long long iv_loads;      // per attempt
   unsigned long long iv_stores;
@@ -96,9 +98,12 @@ struct InterpParams {
   uint32_t stage;             // staged records per warp
   int32_t* node_min;          // [I_b] min / max arrival node (fused A4)
   int32_t* node_max;
-  // log
-  uint64_t* log;              // records (make_rec)
-  unsigned long long log_cap;
+  // log: write records go straight to the sort buffer, read records to a
+  // staging buffer the write-set filter compacts
+  uint64_t* wlog;             // records (make_rec), [0, wlog_count)
+  uint64_t* rlog;             // [0, rlog_count)
+  unsigned long long log_cap; // capacity of each buffer (records); wlog+rlog must fit
+  uint8_t* wmap;              // [I_b * cpi] 1 = cell written in this interval
   int32_t* wval;              // [ovl_cap][n_lanes] final value of each written overlay slot
   uint32_t* hist;             // [4][256] digit histograms of the cell bits (fused K2)
   int passes;                 // 8-bit digit passes of the sort
@@ -108,10 +113,10 @@ struct InterpParams {
 };
 
 struct DetectParams {
-  const uint64_t* recs;       // sorted by cell
+  const uint64_t* recs;       // sorted by cell; count = ctr->wlog_count + ctr->kept_count
   const int32_t* wval;        // [ovl_cap][n_lanes]
   uint32_t n_lanes, n;        // lane = inst_local * n + tid
-  uint32_t n_records;
+  uint32_t n_records;         // host upper bound (grid size)
   int32_t* heap;
   uint32_t cpi, n_arrays;
   const uint32_t* arr_off;
@@ -124,6 +129,20 @@ struct DetectParams {
 // ---- launchers (defined in the .cu files) --------------------------------
 size_t interp_smem_bytes(const InterpParams& p, int threads, bool code_in_smem);
 cudaError_t launch_interp(const InterpParams& p, cudaStream_t s);
+
+// Write-set filter: keep the read records whose cell some work-item wrote in
+// this interval (others can produce no report and no commit); append them to
+// the sort buffer after the write records, with their digit histograms.
+struct FilterParams {
+  const uint64_t* rlog;
+  const uint8_t* wmap;
+  uint64_t* out;          // sort buffer; kept reads go to out[wlog_count + i]
+  uint32_t* hist;         // [4][256]
+  int passes;
+  DevCounters* ctr;
+  uint32_t n_reads_ub;    // host upper bound (= rlog_count)
+};
+cudaError_t launch_filter(const FilterParams& p, cudaStream_t s);
 
 struct SortWorkspace {
   uint64_t* alt = nullptr;         // ping-pong buffer
@@ -159,9 +178,12 @@ struct Profiler {
 
 // Sort (keys, vals) by key bits [0, bits).  *in_alt tells whether the sorted
 // data ended in the alt buffers of `ws`.
-// hist_ready: ws.hist already holds the digit histograms (fused into K1);
-// otherwise an upfront histogram pass (K2) computes them.
-cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, int bits, SortWorkspace& ws, cudaStream_t s, bool* in_alt,
+// hist_ready: ws.hist already holds the digit histograms (fused into K1 and
+// the filter); otherwise an upfront histogram pass (K2) computes them.
+// n_ub: host-side upper bound of the record count; the exact count is
+// *n_a + *n_b (device memory, may be NULL) read by the kernels.
+cudaError_t onesweep_sort(uint64_t* recs, uint32_t n_ub, const unsigned long long* n_a,
+                          const unsigned long long* n_b, int bits, SortWorkspace& ws, cudaStream_t s, bool* in_alt,
                           Profiler* prof, bool hist_ready);
 
 cudaError_t launch_detect(const DetectParams& p, cudaStream_t s);

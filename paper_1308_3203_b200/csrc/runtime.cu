@@ -98,7 +98,7 @@ struct rc_workspace {
   int device = -1;
   DevBuf code, arr_off, arr_size, heap;
   DevBuf regs[2], pc[2], status[2], live;
-  DevBuf log, log_alt, wval, sort_status, sort_small;
+  DevBuf log, log_alt, wval, wmap, sort_status, sort_small;
   DevBuf reports, reports_scratch;
   DevBuf inst_tmp;  // node_min | node_max | first_tid | second_tid | inst_flag  ([I_b] each)
   DevBuf ctr;
@@ -107,7 +107,7 @@ struct rc_workspace {
   Profiler prof;
   ~rc_workspace() {
     for (DevBuf* b : {&code, &arr_off, &arr_size, &heap, &regs[0], &regs[1], &pc[0], &pc[1], &status[0],
-                      &status[1], &live, &log, &log_alt, &wval, &sort_status,
+                      &status[1], &live, &log, &log_alt, &wval, &wmap, &sort_status,
                       &sort_small, &reports, &reports_scratch, &inst_tmp, &ctr})
       b->release();
     if (h_ctr) cudaFreeHost(h_ctr);
@@ -291,6 +291,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     }
     CK(W.inst_tmp.ensure((uint64_t)I_b * 20));
     CK(W.wval.ensure(std::max<uint64_t>(1, L_max * (uint64_t)P->ovl_cap) * 4));
+    CK(W.wmap.ensure(std::max<uint64_t>(1, (uint64_t)I_b * cpi)));
   }
   const int passes = (key_bits + 7) / 8;
   uint64_t log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
@@ -389,6 +390,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       // ---------------- K1
       uint64_t rep_before = rep_count;
       InterpParams ip;
+      if (cpi) CK(cudaMemsetAsync(W.wmap.p, 0, (size_t)nb * cpi, s));  // write-set map of this interval
       for (;;) {
         CK(cudaMemsetAsync(dctr, 0, offsetof(DevCounters, report_count), s));
         CK(cudaMemsetAsync(W.sort.hist, 0, 4 * 256 * sizeof(uint32_t), s));  // K1 fuses the digit histograms
@@ -418,8 +420,10 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         ip.stage = P->rec_bound > 0 ? (uint32_t)std::min(256, ((32 * P->rec_bound + 31) / 32) * 32) : 256u;
         ip.node_min = node_min;
         ip.node_max = node_max;
-        ip.log = W.log.as<uint64_t>();
+        ip.wlog = W.log.as<uint64_t>();
+        ip.rlog = W.log_alt.as<uint64_t>();
         ip.log_cap = log_cap;
+        ip.wmap = W.wmap.as<uint8_t>();
         ip.wval = W.wval.as<int32_t>();
         ip.hist = W.sort.hist;
         ip.passes = passes;
@@ -435,12 +439,13 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
                       "a work-item wrote more than %d distinct cells in one barrier interval (instance batch at "
                       "%u, interval %u)",
                       P->ovl_cap, inst_base, k);
-        const bool log_over = W.h_ctr->log_overflow || W.h_ctr->log_count > log_cap;
+        const uint64_t n_all = W.h_ctr->wlog_count + W.h_ctr->rlog_count;  // the sort buffer must hold both
+        const bool log_over = W.h_ctr->log_overflow || n_all > log_cap;
         const bool rep_over = W.h_ctr->report_count > rep_cap;
         if (!log_over && !rep_over) break;
         if (log_over) {  // grow the log and re-run the interval from the saved lane state
-          const uint64_t want = std::min<uint64_t>(W.h_ctr->log_count + W.h_ctr->log_count / 4 + 1024, 0xFFFFFFFFull);
-          if (W.h_ctr->log_count > 0xFFFFFFFFull) return fail(RC_ELIMIT, "more than 2^32 access records in one interval");
+          const uint64_t want = std::min<uint64_t>(n_all + n_all / 4 + 1024, 0xFFFFFFFFull);
+          if (n_all > 0xFFFFFFFFull) return fail(RC_ELIMIT, "more than 2^32 access records in one interval");
           CK(W.log.ensure(want * 8));
           CK(W.log_alt.ensure(want * 8));
           log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
@@ -449,17 +454,33 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         if (rep_over) CK(grow_reports(W.h_ctr->report_count));
         CK(set_report_count(rep_before));
       }
-      const uint64_t N = W.h_ctr->log_count;
+      const uint64_t Nw = W.h_ctr->wlog_count, Nr = W.h_ctr->rlog_count;
+      const uint64_t N = Nw + Nr;  // upper bound of the sorted records (exact count on the device)
       rep_count = W.h_ctr->report_count;
       tot_loads += W.h_ctr->iv_loads;
       tot_stores += W.h_ctr->iv_stores;
       tot_instr += W.h_ctr->iv_instr;
 
-      // ---------------- K2/K3: sort the log by cell
+      // ---------------- write-set filter: reads of written cells join the write records
+      const size_t mark0 = W.prof.marks.size();
+      {
+        FilterParams fp;
+        fp.rlog = W.log_alt.as<uint64_t>();
+        fp.wmap = W.wmap.as<uint8_t>();
+        fp.out = W.log.as<uint64_t>();
+        fp.hist = W.sort.hist;
+        fp.passes = passes;
+        fp.ctr = dctr;
+        fp.n_reads_ub = (uint32_t)Nr;
+        W.prof.begin(s);
+        CK(launch_filter(fp, s));
+        W.prof.end(RC_PROF_FILTER, s, Nr * 9, Nr);
+      }
+      // ---------------- K3: onesweep sort of the kept records by cell
       bool in_alt = false;
       W.sort.alt = W.log_alt.as<uint64_t>();
-      CK(onesweep_sort(W.log.as<uint64_t>(), (uint32_t)N, key_bits, W.sort, s, &in_alt,
-                       W.prof.on ? &W.prof : nullptr, /*hist_ready=*/true));
+      CK(onesweep_sort(W.log.as<uint64_t>(), (uint32_t)N, &dctr->wlog_count, &dctr->kept_count, key_bits, W.sort, s,
+                       &in_alt, W.prof.on ? &W.prof : nullptr, /*hist_ready=*/true));
       const uint64_t* sr = in_alt ? W.log_alt.as<uint64_t>() : W.log.as<uint64_t>();
 
       // ---------------- K4+K5 and A4 (idempotent: re-run if the report buffer overflows)
@@ -471,7 +492,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         dp.wval = W.wval.as<int32_t>();
         dp.n_lanes = L;
         dp.n = n;
-        dp.n_records = (uint32_t)N;
+        dp.n_records = (uint32_t)N;  // upper bound; the kernel reads the exact count
         dp.heap = W.heap.as<int32_t>();
         dp.cpi = (uint32_t)std::max<uint64_t>(cpi, 1);
         dp.n_arrays = n_arrays;
@@ -506,6 +527,15 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         CK(grow_reports(W.h_ctr->report_count));
         CK(set_report_count(rep_after_k1));
         W.h_ctr->report_count = 0;  // force a fresh read after the re-run
+      }
+      if (W.prof.on) {  // exact sorted-record count is known now: fix this interval's profile bytes
+        const uint64_t Ns = W.h_ctr->wlog_count + W.h_ctr->kept_count;
+        for (size_t i = mark0; i < W.prof.marks.size(); i++) {
+          Profiler::Mark& m = W.prof.marks[i];
+          if (m.cls == RC_PROF_SORT) { m.bytes = Ns * 16; m.items = Ns; }
+          if (m.cls == RC_PROF_DETECT) { m.bytes = Ns * 8; m.items = Ns; }
+          if (m.cls == RC_PROF_FILTER) { m.bytes = Nr * 9 + W.h_ctr->kept_count * 8; }
+        }
       }
       cur ^= 1;  // the interval's lane state becomes current
       const bool any_waiting = W.h_ctr->any_waiting != 0;

@@ -88,8 +88,16 @@ void sort_phase_io(unsigned long long* out, bool reset) {
 #endif
 
 // ---- K2: all digit histograms in one read (fallback; K1 fuses it) ----------
-__global__ void __launch_bounds__(256) hist_kernel(const uint64_t* __restrict__ recs, uint32_t n, int passes,
-                                                   uint32_t* __restrict__ hist) {
+__device__ __forceinline__ uint32_t dev_count(uint32_t n_host, const unsigned long long* n_a,
+                                              const unsigned long long* n_b) {
+  if (!n_a) return n_host;
+  return (uint32_t)(*n_a + (n_b ? *n_b : 0ull));
+}
+
+__global__ void __launch_bounds__(256) hist_kernel(const uint64_t* __restrict__ recs, uint32_t n_host,
+                                                   const unsigned long long* n_a, const unsigned long long* n_b,
+                                                   int passes, uint32_t* __restrict__ hist) {
+  const uint32_t n = dev_count(n_host, n_a, n_b);
   __shared__ uint32_t h[4][RADIX];
   for (int i = threadIdx.x; i < 4 * RADIX; i += blockDim.x) (&h[0][0])[i] = 0;
   __syncthreads();
@@ -134,9 +142,10 @@ __global__ void __launch_bounds__(256) bin_offsets_kernel(const uint32_t* __rest
 // counter (claiming one tile ahead to hide the atomic); each block keeps two
 // tile buffers and prefetches (TMA) the next claimed tile while it processes
 // the current one.
+template <int NBUF>
 struct SortSmem {
-  uint64_t buf[2][SORT_TILE];
-  uint32_t whist[WARPS][RADIX];  // per-warp digit counters (ranking)
+  uint64_t buf[NBUF][SORT_TILE];
+  uint16_t whist[WARPS][RADIX];  // per-warp digit counters (ranking; <= 512 per warp)
   uint32_t thist[2][RADIX];      // early tile counts (two copies: fewer atomic conflicts)
   uint32_t tile_excl[RADIX];
   uint32_t glob_base[RADIX];
@@ -170,14 +179,35 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* mbar, uint32_t pha
   }
 }
 
-__global__ void __launch_bounds__(SORT_THREADS, 3) onesweep_kernel(const uint64_t* __restrict__ in,
-                                                                   uint64_t* __restrict__ out, uint32_t n, int shift,
+// lanes of the warp holding the same 8-bit digit: one ballot per digit bit
+// (MATCH.ANY has far lower throughput on this part)
+__device__ __forceinline__ unsigned match_digit(uint32_t d, unsigned valid_mask) {
+  unsigned peers = valid_mask;
+#pragma unroll
+  for (int b = 0; b < 8; b++) {
+    const unsigned bb = __ballot_sync(FULL, (d >> b) & 1u);
+    peers &= ((d >> b) & 1u) ? bb : ~bb;
+  }
+  return peers;
+}
+
+// PERSISTENT: resident grid, two buffers, next tile prefetched (TMA) while
+// the current one is processed.  Otherwise: one tile per block (grid = tiles;
+// the hardware block scheduler staggers tiles, which keeps look-back walks
+// short) with a single buffer.
+template <bool PERSISTENT>
+__global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? 2 : 3) onesweep_kernel(const uint64_t* __restrict__ in,
+                                                                   uint64_t* __restrict__ out, uint32_t n_host,
+                                                                   const unsigned long long* n_a,
+                                                                   const unsigned long long* n_b, int shift,
                                                                    const uint32_t* __restrict__ bin_off,
                                                                    unsigned long long* __restrict__ status,
                                                                    uint32_t* __restrict__ tile_ctr, uint32_t epoch) {
+  constexpr int NB = PERSISTENT ? 2 : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
+  SortSmem<NB>& S = *reinterpret_cast<SortSmem<NB>*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const uint32_t n = dev_count(n_host, n_a, n_b);
   const uint32_t n_tiles = (uint32_t)((n + SORT_TILE - 1) / SORT_TILE);
   const unsigned long long ep = (unsigned long long)(epoch & 0x3FFFFF) << 40;
   const int dsh = REC_CELL_SHIFT + shift;
@@ -192,8 +222,9 @@ __global__ void __launch_bounds__(SORT_THREADS, 3) onesweep_kernel(const uint64_
     if (t0 < n_tiles) {
       tile_fetch(S.buf[0], &S.mbar[0], in + (uint64_t)t0 * SORT_TILE,
                  (uint32_t)umin64(SORT_TILE, n - (uint64_t)t0 * SORT_TILE));
-      claimed = atomicAdd(tile_ctr, 1u);
+      if (PERSISTENT) claimed = atomicAdd(tile_ctr, 1u);
     }
+    if (!PERSISTENT) S.tile[1] = 0xFFFFFFFFu;
   }
   __syncthreads();
   uint32_t phase = 0;  // bit b = expected parity of buffer b's mbarrier
@@ -206,12 +237,12 @@ __global__ void __launch_bounds__(SORT_THREADS, 3) onesweep_kernel(const uint64_
     if (tile >= n_tiles) break;  // block-uniform
     // fetch the tile claimed last iteration into the other buffer (freed by
     // the __syncthreads that ended the previous iteration); claim the next
-    if (t == 0) {
+    if (PERSISTENT && t == 0) {
       const uint32_t tn = claimed;
       S.tile[cur ^ 1] = tn;
       claimed = 0xFFFFFFFFu;
       if (tn < n_tiles) {
-        tile_fetch(S.buf[cur ^ 1], &S.mbar[cur ^ 1], in + (uint64_t)tn * SORT_TILE,
+        tile_fetch(S.buf[(cur ^ 1) % NB], &S.mbar[cur ^ 1], in + (uint64_t)tn * SORT_TILE,
                    (uint32_t)umin64(SORT_TILE, n - (uint64_t)tn * SORT_TILE));
         claimed = atomicAdd(tile_ctr, 1u);
       }
@@ -221,7 +252,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 3) onesweep_kernel(const uint64_
     S.thist[1][t] = 0;
     const uint64_t base = (uint64_t)tile * SORT_TILE;
     const uint32_t cnt = (uint32_t)umin64(SORT_TILE, n - base);
-    uint64_t* B = S.buf[cur];
+    uint64_t* B = S.buf[cur % NB];
     PHASE_T(0);
     mbar_wait(&S.mbar[cur], (phase >> cur) & 1u);
     phase ^= 1u << cur;
@@ -229,18 +260,30 @@ __global__ void __launch_bounds__(SORT_THREADS, 3) onesweep_kernel(const uint64_
     __syncthreads();
     PHASE_T(1);
 
-    // ---- records to registers, early tile counts, publish AGGREGATE
+    // ---- records to registers; digit groups of all items up front (the 16
+    //      MATCH.ANY are independent, so their latencies overlap)
     uint64_t k[SORT_ITEMS];
-    uint32_t dg[SORT_ITEMS];
+    uint32_t pm[SORT_ITEMS];  // peer mask, later the rank within the warp
 #pragma unroll
     for (int j = 0; j < SORT_ITEMS; j++) {
       const uint32_t idx = w * WARP_ITEMS + j * 32 + lane;
-      k[j] = idx < cnt ? B[idx] : 0ull;
-      dg[j] = idx < cnt ? (uint32_t)(k[j] >> dsh) & 0xFF : 0x100u;
+      k[j] = idx < cnt ? B[idx] : ~0ull;  // invalid items: digit 0x100 below
     }
+#define DIGIT(j) ((w * WARP_ITEMS + (j) * 32 + lane) < cnt ? (uint32_t)(k[j] >> dsh) & 0xFF : 0x100u)
+    {
+      const unsigned vm = cnt >= (uint32_t)(w * WARP_ITEMS + WARP_ITEMS) ? FULL : 0u;
 #pragma unroll
-    for (int j = 0; j < SORT_ITEMS; j++)
-      if (dg[j] < RADIX) atomicAdd(&S.thist[w & 1][dg[j]], 1u);
+      for (int j = 0; j < SORT_ITEMS; j++) {
+        const uint32_t dd = DIGIT(j);
+        pm[j] = match_digit(dd, vm ? vm : __ballot_sync(FULL, dd < RADIX));
+      }
+    }
+    // early tile counts: one shared atomic per digit group, then publish AGGREGATE
+#pragma unroll
+    for (int j = 0; j < SORT_ITEMS; j++) {
+      const uint32_t dd = DIGIT(j);
+      if (dd < RADIX && lane == __ffs(pm[j]) - 1) atomicAdd(&S.thist[w & 1][dd], (uint32_t)__popc(pm[j]));
+    }
     __syncthreads();
     const int d = t;  // SORT_THREADS == RADIX
     const uint32_t tile_cnt = S.thist[0][d] + S.thist[1][d];
@@ -250,37 +293,46 @@ __global__ void __launch_bounds__(SORT_THREADS, 3) onesweep_kernel(const uint64_
     PHASE_T(2);
 
     // ---- stable in-tile ranking (warp w owns items [w*512, w*512+512), striped)
-    uint32_t rk[SORT_ITEMS];  // rank within the warp
 #pragma unroll
     for (int j = 0; j < SORT_ITEMS; j++) {
-      const bool valid = dg[j] < RADIX;
-      const unsigned peers = __match_any_sync(FULL, dg[j]);
+      const uint32_t dd = DIGIT(j);
+      const bool valid = dd < RADIX;
       uint32_t prev = 0;
-      if (valid) prev = S.whist[w][dg[j]];
+      if (valid) prev = S.whist[w][dd];
       __syncwarp();
-      if (valid && lane == __ffs(peers) - 1) S.whist[w][dg[j]] = prev + __popc(peers);
+      if (valid && lane == __ffs(pm[j]) - 1) S.whist[w][dd] = (uint16_t)(prev + __popc(pm[j]));
       __syncwarp();
-      rk[j] = prev + __popc(peers & lanemask_lt());
+      pm[j] = prev + __popc(pm[j] & lanemask_lt());
     }
     __syncthreads();
-    PHASE_T(3);
-
-    // ---- per digit: warp-exclusive prefix, look-back, publish INCLUSIVE
-    {
+    {  // per digit: warp-exclusive prefix, tile-local digit offsets
       uint32_t run = 0;
 #pragma unroll
       for (int ww = 0; ww < WARPS; ww++) {
         const uint32_t c = S.whist[ww][d];
-        S.whist[ww][d] = run;
+        S.whist[ww][d] = (uint16_t)run;
         run += c;
       }
     }
     const uint32_t excl_tile = block_excl_scan(tile_cnt, S.wt);
     S.tile_excl[d] = excl_tile;
+    __syncthreads();
+    PHASE_T(3);
+
+    // ---- scatter into shared memory in digit order (stable), in place
+#pragma unroll
+    for (int j = 0; j < SORT_ITEMS; j++) {
+      const uint32_t dd = DIGIT(j);
+      if (dd < RADIX) B[S.tile_excl[dd] + S.whist[w][dd] + pm[j]] = k[j];
+    }
+#undef DIGIT
+    PHASE_T(4);
+
+    // ---- look-back (after the scatter: predecessors had time to publish
+    //      INCLUSIVE), then publish our INCLUSIVE prefix
     unsigned long long excl = 0;
     if (tile > 0) {
-      // look back LB predecessors per L2 round trip (the walk is latency-bound)
-      constexpr int LB = 8;
+      constexpr int LB = 16;  // predecessors per L2 round trip
       int64_t tp = (int64_t)tile - 1;
       bool done = false;
       while (!done) {
@@ -301,15 +353,6 @@ __global__ void __launch_bounds__(SORT_THREADS, 3) onesweep_kernel(const uint64_
     }
     S.glob_base[d] = (uint32_t)(bin_off[d] + excl) - excl_tile;
     __syncthreads();
-    PHASE_T(4);
-
-    // ---- scatter into shared memory in digit order (stable), in place
-#pragma unroll
-    for (int j = 0; j < SORT_ITEMS; j++) {
-      const uint32_t dd = dg[j];
-      if (dd < RADIX) B[S.tile_excl[dd] + S.whist[w][dd] + rk[j]] = k[j];
-    }
-    __syncthreads();
     PHASE_T(5);
 
     // ---- coalesced write-out: sorted position i goes to glob_base[digit] + i
@@ -327,15 +370,19 @@ __global__ void __launch_bounds__(SORT_THREADS, 3) onesweep_kernel(const uint64_
     }
     __syncthreads();  // buffer `cur`, whist, glob_base free for reuse
     PHASE_T(6);
+    if (!PERSISTENT) break;
     cur ^= 1;
   }
 }
 
+int g_sort_variant = 1;  // 1 = persistent double-buffered, 0 = one tile per block (sortbench knob)
+
 size_t sort_tiles(size_t n) { return (n + SORT_TILE - 1) / SORT_TILE; }
 
-cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, int bits, SortWorkspace& ws, cudaStream_t s, bool* in_alt,
-                          Profiler* prof, bool hist_ready) {
-  *in_alt = false;
+cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, const unsigned long long* n_a, const unsigned long long* n_b,
+                          int bits, SortWorkspace& ws, cudaStream_t s, bool* in_alt, Profiler* prof,
+                          bool hist_ready) {
+  *in_alt = false;  // n: upper bound of the record count (exact when n_a == NULL)
   if (n == 0 || bits <= 0) return cudaSuccess;
   const int passes = (bits + 7) / 8;
   static int nsm = 0, per_sm = 0;
@@ -343,11 +390,15 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, int bits, SortWorkspace& w
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(SortSmem));
+    cudaError_t e = cudaFuncSetAttribute(onesweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(SortSmem<2>));
     if (e != cudaSuccess) return e;
-    cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, onesweep_kernel, SORT_THREADS, sizeof(SortSmem));
+    e = cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(SortSmem<1>));
+    if (e != cudaSuccess) return e;
+    cudaFuncSetAttribute(onesweep_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, onesweep_kernel<true>, SORT_THREADS, sizeof(SortSmem<2>));
     if (per_sm < 1) per_sm = 1;
   }
   cudaMemsetAsync(ws.tile_ctr, 0, 4 * sizeof(uint32_t), s);
@@ -355,7 +406,7 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, int bits, SortWorkspace& w
   if (!hist_ready) {
     cudaMemsetAsync(ws.hist, 0, 4 * RADIX * sizeof(uint32_t), s);
     const uint32_t hist_grid = (uint32_t)umin64((uint64_t)nsm * 8, (n + 256 * 16 - 1) / (256 * 16));
-    hist_kernel<<<hist_grid, 256, 0, s>>>(recs, n, passes, ws.hist);
+    hist_kernel<<<hist_grid, 256, 0, s>>>(recs, n, n_a, n_b, passes, ws.hist);
     launched();
   }
   bin_offsets_kernel<<<passes, 256, 0, s>>>(ws.hist, ws.bin_off);
@@ -363,7 +414,8 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, int bits, SortWorkspace& w
   if (prof) prof->end(RC_PROF_HIST, s, hist_ready ? 0 : (uint64_t)n * 8, n);
   const uint32_t tiles = (uint32_t)sort_tiles(n);
   // persistent: never more blocks than can be resident (look-back progress)
-  const uint32_t grid = (uint32_t)umin64(tiles, (uint64_t)per_sm * nsm);
+  const bool pers = g_sort_variant == 1;
+  const uint32_t grid = pers ? (uint32_t)umin64(tiles, (uint64_t)per_sm * nsm) : tiles;
   uint64_t* kin = recs;
   uint64_t* kout = ws.alt;
   for (int p = 0; p < passes; p++) {
@@ -372,8 +424,12 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, int bits, SortWorkspace& w
       ws.epoch = 1;
     }
     if (prof) prof->begin(s);
-    onesweep_kernel<<<grid, SORT_THREADS, sizeof(SortSmem), s>>>(kin, kout, n, 8 * p, ws.bin_off + p * RADIX,
-                                                                ws.status, ws.tile_ctr + p, ws.epoch);
+    if (pers)
+      onesweep_kernel<true><<<grid, SORT_THREADS, sizeof(SortSmem<2>), s>>>(
+          kin, kout, n, n_a, n_b, 8 * p, ws.bin_off + p * RADIX, ws.status, ws.tile_ctr + p, ws.epoch);
+    else
+      onesweep_kernel<false><<<grid, SORT_THREADS, sizeof(SortSmem<1>), s>>>(
+          kin, kout, n, n_a, n_b, 8 * p, ws.bin_off + p * RADIX, ws.status, ws.tile_ctr + p, ws.epoch);
     launched();
     if (prof) prof->end(RC_PROF_SORT, s, (uint64_t)n * 16, n);
     cudaError_t e = cudaGetLastError();

@@ -21,7 +21,7 @@ STATUS_NAMES = {0: "RC_OK", 1: "RC_EINVAL", 2: "RC_ENOMEM", 3: "RC_ECUDA", 4: "R
 KINDS = {1: "RW", 2: "WW_BENIGN", 3: "WW_NONBENIGN", 4: "OOB", 5: "ASSERT", 6: "DIV0", 7: "FUEL",
          8: "BARRIER_DIVERGENCE"}
 RC_OPT_HOST_IO = 1
-PROF_CLASSES = ["interp", "hist", "sort", "detect", "boundary", "finalize", "copy", "reserved"]
+PROF_CLASSES = ["interp", "hist", "sort", "detect", "boundary", "finalize", "copy", "filter"]
 
 REPORT_DTYPE = np.dtype([("instance", "<u4"), ("interval", "<u4"), ("array", "<i4"), ("index", "<i4"),
                          ("tid1", "<u4"), ("tid2", "<u4"), ("kind", "<u2"), ("flags", "<u2"),

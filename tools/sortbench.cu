@@ -23,6 +23,7 @@ Profiler::~Profiler() {}
 #ifdef SORT_PHASE_TIMING
 void sort_phase_io(unsigned long long* out, bool reset);
 #endif
+extern int g_sort_variant;
 }  // namespace rc
 
 #define CK(x)                                                                      \
@@ -39,6 +40,8 @@ int main(int argc, char** argv) {
   const int bits = argc > 2 ? atoi(argv[2]) : 24;
   const std::string pat = argc > 3 ? argv[3] : "stencil";
   const int reps = argc > 4 ? atoi(argv[4]) : 10;
+  rc::g_sort_variant = argc > 5 ? atoi(argv[5]) : 1;
+  printf("variant %d\n", rc::g_sort_variant);
   std::vector<uint64_t> hk(n);
   // stencil-like log (config 5 even interval): per 32-lane warp: reads of
   // A[c-1], A[c], A[c+1] then the write of B[c]; instance-major
@@ -81,7 +84,7 @@ int main(int argc, char** argv) {
     rc::sort_phase_io(nullptr, true);
 #endif
     cudaEventRecord(e0);
-    CK(rc::onesweep_sort(dk, n, bits, ws, 0, &in_alt, nullptr, false));
+    CK(rc::onesweep_sort(dk, n, nullptr, nullptr, bits, ws, 0, &in_alt, nullptr, false));
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     float ms;
@@ -97,7 +100,7 @@ int main(int argc, char** argv) {
   unsigned long long ph[8];
   rc::sort_phase_io(ph, false);
   const double tiles = (double)rc::sort_tiles(n) * passes;
-  const char* names[] = {"claim+prefetch", "tma wait", "early count", "rank", "lookback", "scatter", "writeout", ""};
+  const char* names[] = {"claim+prefetch", "tma wait", "match+count", "rank", "scatter", "lookback", "writeout", ""};
   double tot = 0;
   for (int i = 0; i < 7; i++) tot += ph[i];
   for (int i = 0; i < 7; i++)
