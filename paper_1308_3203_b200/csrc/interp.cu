@@ -95,9 +95,20 @@ __device__ __forceinline__ void hist_writes(uint64_t rec, bool isw, unsigned mw,
   }
 }
 
+// the parts of InterpParams the log write-out needs (passed by value so the
+// kernel's parameter block is never copied to local memory)
+struct LogOut {
+  uint64_t* wlog;
+  uint64_t* rlog;
+  uint8_t* wmap;
+  DevCounters* ctr;
+  unsigned long long log_cap;
+  int passes;
+};
+
 // Split-write `cnt` staged records of this warp: writes to wlog[bw + ...]
 // (marking wmap), reads to rlog[br + ...].  Whole warp.
-__device__ __forceinline__ void write_out(const InterpParams& p, const uint64_t* recs, uint32_t cnt,
+__device__ __forceinline__ void write_out(const LogOut& p, const uint64_t* recs, uint32_t cnt,
                                           unsigned long long bw, unsigned long long br, uint32_t* bh, int lane,
                                           bool* over) {
   uint32_t runw = 0, runr = 0;
@@ -134,9 +145,8 @@ __device__ __forceinline__ uint32_t count_writes(const uint64_t* recs, uint32_t 
 }
 
 // mid-interval overflow of a warp's staging buffer: flush it on its own
-__device__ __noinline__ uint32_t flush_warp_(const InterpParams* pp, const uint64_t* recs, uint32_t fill, int lane,
+__device__ __noinline__ uint32_t flush_warp_(const LogOut p, const uint64_t* recs, uint32_t fill, int lane,
                                              uint32_t* bh) {
-  const InterpParams& p = *pp;
   __syncwarp();
   const uint32_t nw = count_writes(recs, fill, lane);
   unsigned long long bw = 0, br = 0;
@@ -164,13 +174,14 @@ __device__ __forceinline__ int32_t wadd(int32_t x, int32_t y) { return (int32_t)
 }  // namespace
 
 template <bool CODE_SMEM>
-__global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
+__global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int T = blockDim.x;
   const int W = T >> 5;
   const int t = threadIdx.x;
   const int warp = t >> 5, lane = t & 31;
   const uint32_t R = p.n_regs, OV = p.ovl_cap;
+  const LogOut lo{p.wlog, p.rlog, p.wmap, p.ctr, p.log_cap, p.passes};
 
   // ---- shared memory carve-up (sizes mirrored in interp_smem_bytes)
   unsigned char* q = smem;
@@ -182,10 +193,9 @@ __global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
   int32_t* oval = reinterpret_cast<int32_t*>(q); q += (size_t)OV * T * 4;
   uint32_t* s_off = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
   uint32_t* s_size = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
+  uint8_t* s_live = reinterpret_cast<uint8_t*>(q); q += (p.n_live + 3) & ~3u;
   uint32_t* wcntw = reinterpret_cast<uint32_t*>(q); q += (size_t)W * 4;   // per-warp write records
   uint32_t* wcntr = reinterpret_cast<uint32_t*>(q); q += (size_t)W * 4;   // per-warp read records (|wait flag)
-  int32_t* wnode = reinterpret_cast<int32_t*>(q); q += (size_t)2 * W * 4;  // per-warp min / max node
-  uint32_t* winst = reinterpret_cast<uint32_t*>(q); q += (size_t)W * 4;   // warp instance (or ~0)
   q = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(q) + 7) & ~uintptr_t(7));
   unsigned long long* wbase = reinterpret_cast<unsigned long long*>(q); q += (size_t)2 * W * 8;  // [W] w, [W] r
   unsigned long long* wstat = reinterpret_cast<unsigned long long*>(q);  // [3][W]
@@ -199,8 +209,10 @@ __global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
     for (uint32_t i = t; i < p.n_instr; i += T) s_code[i] = src[i];
   }
   for (int i = t; i < p.passes * 256; i += T) bhist[i] = 0;
+  for (uint32_t i = t; i < p.n_live; i += T) s_live[i] = p.live[i];
+  __syncthreads();
 
-  // block totals kept by thread 0 across tiles
+  // block totals: lane l of warp 0 accumulates the statistics of warp l
   unsigned long long b_instr = 0, b_loads = 0, b_stores = 0;
   bool b_wait = false, b_over = false;
   const uint32_t n_tiles = (p.n_lanes + T - 1) / T;
@@ -209,17 +221,22 @@ __global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
     const uint32_t g = tile * (uint32_t)T + t;
     const bool valid = g < p.n_lanes;
     uint8_t status = valid ? p.status_in[g] : (uint8_t)L_EXITED;
+    uint32_t pc = valid ? p.pc_in[g] : 0;  // independent of the status load
     if (status == L_EXITED_NOW) status = L_EXITED;
     bool running = valid && (status == L_RUNNING || status == L_WAITING);
     const uint32_t inst = valid ? g / p.n : 0;
     const uint32_t tid = valid ? g - inst * p.n : 0;
     const uint32_t cell_base = inst * p.cpi;
-    uint32_t pc = running ? p.pc_in[g] : 0;
     int32_t* Rg = sregs + t;  // register r of this lane = Rg[r*T]
-    if (running)
-      for (uint32_t i = 0; i < p.n_live; i++) {
-        const uint32_t r = __ldg(p.live + i);
-        Rg[r * T] = p.regs_in[(size_t)r * p.n_lanes + g];
+    if (running)  // live registers in batches of 4 independent loads
+      for (uint32_t i0 = 0; i0 < p.n_live; i0 += 4) {
+        int32_t v[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+          if (i0 + j < p.n_live) v[j] = p.regs_in[(size_t)s_live[i0 + j] * p.n_lanes + g];
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+          if (i0 + j < p.n_live) Rg[s_live[i0 + j] * T] = v[j];
       }
     __syncthreads();
 
@@ -316,7 +333,7 @@ __global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
           }
           const unsigned m = __ballot_sync(FULL, ok);
           if (m) {
-            if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(&p, S.recs, S.fill, lane, bhist);
+            if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane, bhist);
             if (ok) S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, tid, 0, 0);
             S.fill += __popc(m);
           }
@@ -374,7 +391,7 @@ __global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
     for (int j = 0; j < max_own; j++) {
       const bool has = j < n_own;
       const unsigned m = __ballot_sync(FULL, has);
-      if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(&p, S.recs, S.fill, lane, bhist);
+      if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane, bhist);
       if (has) {
         S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(ocell[j * T + t], tid, (uint32_t)j, 1);
         p.wval[(size_t)j * p.n_lanes + g] = oval[j * T + t];
@@ -382,29 +399,22 @@ __global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
       S.fill += __popc(m);
     }
 
-    // lane state out (only registers live across the barrier, only for suspended lanes)
-    if (valid) {
-      p.status_out[g] = status;
-      if (status == L_WAITING) {
-        p.pc_out[g] = pc;
-        for (uint32_t i = 0; i < p.n_live; i++) {
-          const uint32_t r = __ldg(p.live + i);
-          p.regs_out[(size_t)r * p.n_lanes + g] = Rg[r * T];
-        }
-      }
-    }
-
-    // fused A4: arrival node range per instance, suspended flag
+    // fused A4: arrival node range per instance (fire-and-forget atomics,
+    // one pair per warp when the warp lies in one instance), suspended flag
     const bool arrived = valid && (status == L_WAITING || status == L_EXITED_NOW);
     const int32_t node = status == L_WAITING ? (int32_t)pc - 1 : NODE_EXIT;
     const bool any_wait = __any_sync(FULL, status == L_WAITING);
     const uint32_t inst0 = __shfl_sync(FULL, inst, 0);
     const bool warp_uniform = __all_sync(FULL, !valid || inst == inst0);
-    const unsigned am = __ballot_sync(FULL, arrived);
-    // nodes are >= -1; bias by 1 so unsigned reductions apply
-    const uint32_t nmin = __reduce_min_sync(FULL, arrived ? (uint32_t)(node + 1) : 0xFFFFFFFFu);
-    const uint32_t nmax = __reduce_max_sync(FULL, arrived ? (uint32_t)(node + 1) : 0u);
-    if (!warp_uniform && arrived) {  // small work-groups: per-lane atomics
+    if (warp_uniform) {
+      // nodes are >= -1; bias by 1 so unsigned reductions apply
+      const uint32_t nmin = __reduce_min_sync(FULL, arrived ? (uint32_t)(node + 1) : 0xFFFFFFFFu);
+      const uint32_t nmax = __reduce_max_sync(FULL, arrived ? (uint32_t)(node + 1) : 0u);
+      if (lane == 0 && nmin != 0xFFFFFFFFu) {
+        atomicMin(p.node_min + inst0, (int32_t)(nmin - 1));
+        atomicMax(p.node_max + inst0, (int32_t)(nmax - 1));
+      }
+    } else if (arrived) {  // small work-groups: per-lane atomics
       atomicMin(p.node_min + inst, node);
       atomicMax(p.node_max + inst, node);
     }
@@ -415,56 +425,51 @@ __global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
     const uint32_t nw = count_writes(S.recs, S.fill, lane);
     if (lane == 0) {
       wcntw[warp] = nw;
-      wcntr[warp] = (S.fill - nw) | (any_wait ? 0x80000000u : 0u);
+      wcntr[warp] = S.fill - nw;
       wstat[warp] = s0;
       wstat[W + warp] = s1;
       wstat[2 * W + warp] = s2;
       if (any_ovl) p.ctr->ovl_overflow = 1;
-      wnode[warp] = (warp_uniform && am) ? (int32_t)(nmin - 1) : 0x7FFFFFFF;
-      wnode[W + warp] = (warp_uniform && am) ? (int32_t)(nmax - 1) : (int32_t)0x80000000;
-      winst[warp] = warp_uniform ? inst0 : 0xFFFFFFFFu;
     }
+    b_wait |= any_wait;
     __syncthreads();
-    if (t == 0) {
-      // node range: combine consecutive warps of the same instance
-      uint32_t cur_inst = 0xFFFFFFFFu;
-      int32_t cmin = 0x7FFFFFFF, cmax = (int32_t)0x80000000;
-      for (int w = 0; w <= W; w++) {
-        const uint32_t wi = w < W ? winst[w] : 0xFFFFFFFFu;
-        if (w == W || wi != cur_inst) {
-          if (cur_inst != 0xFFFFFFFFu && cmin <= cmax) {
-            atomicMin(p.node_min + cur_inst, cmin);
-            atomicMax(p.node_max + cur_inst, cmax);
-          }
-          cur_inst = wi;
-          cmin = 0x7FFFFFFF;
-          cmax = (int32_t)0x80000000;
-        }
-        if (w < W) {
-          cmin = min(cmin, wnode[w]);
-          cmax = max(cmax, wnode[W + w]);
-        }
+    if (warp == 0) {  // lanes < W: prefix over warps, both reservations in flight at once
+      const uint32_t cw = lane < W ? wcntw[lane] : 0u, cr = lane < W ? wcntr[lane] : 0u;
+      uint32_t xw = cw, xr = cr;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t yw = __shfl_up_sync(FULL, xw, o), yr = __shfl_up_sync(FULL, xr, o);
+        if (lane >= o) { xw += yw; xr += yr; }
       }
-      unsigned long long totw = 0, totr = 0;
-      for (int w = 0; w < W; w++) {
-        b_wait |= (wcntr[w] & 0x80000000u) != 0;
-        wbase[w] = totw;
-        wbase[W + w] = totr;
-        totw += wcntw[w];
-        totr += wcntr[w] & 0x7FFFFFFFu;
-        b_instr += wstat[w];
-        b_loads += wstat[W + w];
-        b_stores += wstat[2 * W + w];
+      const uint32_t totw = __shfl_sync(FULL, xw, 31), totr = __shfl_sync(FULL, xr, 31);
+      unsigned long long base = 0;
+      if (lane == 0 && totw) base = atomicAdd(&p.ctr->wlog_count, (unsigned long long)totw);
+      if (lane == 1 && totr) base = atomicAdd(&p.ctr->rlog_count, (unsigned long long)totr);
+      if (lane < W) {
+        b_instr += wstat[lane];
+        b_loads += wstat[W + lane];
+        b_stores += wstat[2 * W + lane];
       }
-      const unsigned long long bw = totw ? atomicAdd(&p.ctr->wlog_count, totw) : 0ull;
-      const unsigned long long br = totr ? atomicAdd(&p.ctr->rlog_count, totr) : 0ull;
-      for (int w = 0; w < W; w++) {
-        wbase[w] += bw;
-        wbase[W + w] += br;
+      const unsigned long long bw = __shfl_sync(FULL, base, 0), br = __shfl_sync(FULL, base, 1);
+      if (lane < W) {
+        wbase[lane] = bw + xw - cw;
+        wbase[W + lane] = br + xr - cr;
+      }
+    }
+    // lane state out (only registers live across the barrier, only for
+    // suspended lanes) while warp 0 waits for the reservations
+    if (valid) {
+      p.status_out[g] = status;
+      if (status == L_WAITING) {
+        p.pc_out[g] = pc;
+        for (uint32_t i = 0; i < p.n_live; i++) {
+          const uint32_t r = s_live[i];
+          p.regs_out[(size_t)r * p.n_lanes + g] = Rg[r * T];
+        }
       }
     }
     __syncthreads();
-    write_out(p, S.recs, S.fill, wbase[warp], wbase[W + warp], bhist, lane, &b_over);
+    write_out(lo, S.recs, S.fill, wbase[warp], wbase[W + warp], bhist, lane, &b_over);
     __syncthreads();  // staging / overlay / registers reused by the next tile
   }
 
@@ -472,12 +477,17 @@ __global__ void __launch_bounds__(256, 4) interp_kernel(const InterpParams p) {
   for (int i = t; i < p.passes * 256; i += T)
     if (bhist[i]) atomicAdd(&p.hist[i], bhist[i]);
   if (__any_sync(FULL, b_over) && lane == 0) p.ctr->log_overflow = 1;
-  if (t == 0) {
-    if (b_instr) atomicAdd(&p.ctr->iv_instr, b_instr);
-    if (b_loads) atomicAdd(&p.ctr->iv_loads, b_loads);
-    if (b_stores) atomicAdd(&p.ctr->iv_stores, b_stores);
-    if (b_wait) p.ctr->any_waiting = 1;
+  if (warp == 0) {
+    b_instr = warp_sum64(b_instr);
+    b_loads = warp_sum64(b_loads);
+    b_stores = warp_sum64(b_stores);
+    if (lane == 0) {
+      if (b_instr) atomicAdd(&p.ctr->iv_instr, b_instr);
+      if (b_loads) atomicAdd(&p.ctr->iv_loads, b_loads);
+      if (b_stores) atomicAdd(&p.ctr->iv_stores, b_stores);
+    }
   }
+  if (__any_sync(FULL, b_wait) && lane == 0) p.ctr->any_waiting = 1;
 }
 
 size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem) {
@@ -488,6 +498,7 @@ size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem) {
   b += (size_t)p.n_regs * T * 4;                   // registers
   b += (size_t)p.ovl_cap * T * 8;                  // overlay
   b += (size_t)p.n_arrays * 8;                     // array offsets / sizes
+  b += ((size_t)p.n_live + 3) & ~size_t(3);        // live register list
   b += (size_t)W * 20 + 8;                         // warp counts, node range, instance (+align)
   b += (size_t)W * 8 * 5;                          // warp bases (2) + 3 stats
   return b;
