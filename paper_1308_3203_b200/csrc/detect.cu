@@ -139,7 +139,7 @@ __device__ __forceinline__ void serial_segment(const DetectParams& p, uint32_t i
 }
 }  // namespace
 
-constexpr uint32_t DET_ROUNDS = 16;  // 32-record rounds per warp
+constexpr uint32_t DET_ROUNDS = 8;  // 32-record rounds per warp (all prefetched)
 constexpr uint32_t DET_CHUNK = 32 * DET_ROUNDS;
 
 // Associative per-segment summary.  A cell is SIMPLE when it has at most one
@@ -186,9 +186,10 @@ __device__ __forceinline__ Seg seg_shfl(const Seg& a, int src) {
 }
 
 // Warp-cooperative detection.  A warp owns DET_CHUNK consecutive sorted
-// records and streams them 32 at a time (coalesced loads).  Segment heads /
-// tails come from comparing neighbouring keys (shuffles + one boundary load);
-// each lane's suffix summary over its segment is built by a segmented
+// records; all of them (and the final values of its write records) are loaded
+// up front so the loads overlap, then processed 32 at a time.  Segment heads /
+// tails come from comparing neighbouring keys (shuffles + the two boundary
+// keys); each lane's suffix summary over its segment is built by a segmented
 // shuffle reduction (log2(longest segment in the round) steps).  A segment
 // that crosses a round boundary is carried (warp-uniform state) into the next
 // round; one that crosses the chunk end, and every COMPLEX cell, is handled by
@@ -202,19 +203,38 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
   const uint64_t c0 = wg * DET_CHUNK;
   if (c0 >= n_records) return;  // whole warp
   const uint64_t c1 = min((uint64_t)n_records, c0 + DET_CHUNK);
+  // ---- prefetch the chunk
+  uint64_t vr[DET_ROUNDS];
+  int32_t wv[DET_ROUNDS];
+#pragma unroll
+  for (int rd = 0; rd < (int)DET_ROUNDS; rd++) {
+    const uint64_t r = c0 + rd * 32 + lane;
+    vr[rd] = r < c1 ? __ldg(p.recs + r) : ~0ull;
+  }
+  const uint32_t key_before = c0 > 0 ? rec_cell(__ldg(p.recs + c0 - 1)) : 0xFFFFFFFFu;
+  const uint32_t key_after = c1 < n_records ? rec_cell(__ldg(p.recs + c1)) : 0xFFFFFFFFu;
+#pragma unroll
+  for (int rd = 0; rd < (int)DET_ROUNDS; rd++) wv[rd] = (vr[rd] != ~0ull && rec_w(vr[rd])) ? rec_val(p, vr[rd]) : 0;
+
   const Seg ident{INF, 0u, 0u, 0, 0u};
   bool carry = false;       // an open segment started in an earlier round of this chunk
   uint64_t carry_start = 0;
   Seg cs = ident;
-  for (uint64_t b = c0; b < c1; b += 32) {
+  uint32_t last_key = key_before;  // key of the record before this round
+#pragma unroll
+  for (int rd = 0; rd < (int)DET_ROUNDS; rd++) {
+    const uint64_t b = c0 + rd * 32;
+    if (b >= c1) break;  // warp-uniform
     const uint64_t r = b + lane;
     const bool inb = r < c1;
-    const uint64_t v = inb ? __ldg(p.recs + r) : ~0ull;
-    const uint32_t key = rec_cell(v);  // cell ids are < 0xFFFFFFFF
+    const uint64_t v = vr[rd];
+    const uint32_t key = rec_cell(v);  // invalid lanes: 0xFFFFFFFF (cell ids are smaller)
     uint32_t prev = __shfl_up_sync(FULL, key, 1);
-    if (lane == 0) prev = b > 0 ? rec_cell(__ldg(p.recs + b - 1)) : ~key;
+    if (lane == 0) prev = b > 0 ? last_key : ~key;
     uint32_t next = __shfl_down_sync(FULL, key, 1);
-    if (lane == 31) next = r + 1 < n_records ? rec_cell(__ldg(p.recs + r + 1)) : ~key;
+    const uint32_t next_round_first = rd + 1 < (int)DET_ROUNDS ? rec_cell(__shfl_sync(FULL, vr[rd + 1 < (int)DET_ROUNDS ? rd + 1 : rd], 0)) : 0u;
+    if (lane == 31) next = r + 1 < c1 ? next_round_first : (r + 1 < n_records ? key_after : ~key);
+    last_key = __shfl_sync(FULL, key, 31);
     const bool head = inb && prev != key;
     const bool tail = inb && next != key;  // last record of its segment (possibly beyond c1)
     const unsigned heads = __ballot_sync(FULL, head);
@@ -229,7 +249,7 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
     const uint32_t tid = rec_tid(v);
     Seg S = ident;
     if (inb) {
-      if (rec_w(v)) { S.w = tid; S.vw = rec_val(p, v); S.nw = 1; }
+      if (rec_w(v)) { S.w = tid; S.vw = wv[rd]; S.nw = 1; }
       else { S.rmin = tid; S.rmax = tid; }
     }
     const bool starter = head || lane == 0;  // lanes whose suffix summary is consumed
@@ -248,7 +268,7 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
       if (l0_closes) {
         if (lane == 0) {
           if (seg_complex(M)) serial_segment(p, (uint32_t)carry_start, n_records);
-          else if (M.nw == 1) p.heap[rec_cell(__ldg(p.recs + carry_start))] = M.vw;
+          else if (M.nw == 1) p.heap[key] = M.vw;
         }
         carry = false;
       } else {

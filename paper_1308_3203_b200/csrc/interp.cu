@@ -171,6 +171,27 @@ __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
 
 __device__ __forceinline__ int32_t wadd(int32_t x, int32_t y) { return (int32_t)((uint32_t)x + (uint32_t)y); }
 
+// Pre-decoded instruction (16 B, shared memory): register operands become word
+// offsets r*T into the [reg][thread] register file; LD/ST/SIZE fold in the
+// array's cell offset and size, BR its false target.
+//   x: op | aux(array id) << 8 | a*T << 16     y: b*T | c*T << 16
+//   z: imm, or the array's cell offset (LD/ST), or size (SIZE)
+//   w: BR false target, or the array's size (LD/ST)
+__device__ __forceinline__ uint4 predecode(uint2 raw, int T, const uint32_t* s_off, const uint32_t* s_size) {
+  const uint32_t op = raw.x & 0xFF, a = (raw.x >> 8) & 0xFF, b = (raw.x >> 16) & 0xFF, c = raw.x >> 24;
+  uint4 e;
+  uint32_t aux = 0, z = raw.y, w = 0;
+  if (op == RC_OP_LD) { aux = b; z = s_off[b]; w = s_size[b]; }
+  else if (op == RC_OP_ST) { aux = a; z = s_off[a]; w = s_size[a]; }
+  else if (op == RC_OP_SIZE) { z = s_size[b]; }
+  else if (op == RC_OP_BR) { w = b + 256u * c; }
+  e.x = op | (aux << 8) | ((a * (uint32_t)T) << 16);
+  e.y = (b * (uint32_t)T) | ((c * (uint32_t)T) << 16);
+  e.z = z;
+  e.w = w;
+  return e;
+}
+
 }  // namespace
 
 template <bool CODE_SMEM>
@@ -186,7 +207,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
   // ---- shared memory carve-up (sizes mirrored in interp_smem_bytes)
   unsigned char* q = smem;
   uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)W * p.stage * 8;
-  uint2* s_code = reinterpret_cast<uint2*>(q); q += CODE_SMEM ? (size_t)p.n_instr * 8 : 0;
+  uint4* s_code = reinterpret_cast<uint4*>(q); q += CODE_SMEM ? (size_t)p.n_instr * 16 : 0;
   uint32_t* bhist = reinterpret_cast<uint32_t*>(q); q += (size_t)p.passes * 256 * 4;  // block digit histograms
   int32_t* sregs = reinterpret_cast<int32_t*>(q); q += (size_t)R * T * 4;
   uint32_t* ocell = reinterpret_cast<uint32_t*>(q); q += (size_t)OV * T * 4;
@@ -204,10 +225,9 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
     s_off[a] = p.arr_off[a];
     s_size[a] = p.arr_size[a];
   }
-  if (CODE_SMEM) {
-    const uint2* src = reinterpret_cast<const uint2*>(p.code);
-    for (uint32_t i = t; i < p.n_instr; i += T) s_code[i] = src[i];
-  }
+  __syncthreads();  // s_off / s_size before the pre-decode
+  if (CODE_SMEM)
+    for (uint32_t i = t; i < p.n_instr; i += T) s_code[i] = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + i), T, s_off, s_size);
   for (int i = t; i < p.passes * 256; i += T) bhist[i] = 0;
   for (uint32_t i = t; i < p.n_live; i += T) s_live[i] = p.live[i];
   __syncthreads();
@@ -251,9 +271,13 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
       if (__ballot_sync(FULL, running) == 0) break;
       const uint32_t minpc = __reduce_min_sync(FULL, running ? pc : 0xFFFFFFFFu);
       bool ex = running && pc == minpc;
-      const uint2 raw = CODE_SMEM ? s_code[minpc] : __ldg(reinterpret_cast<const uint2*>(p.code) + minpc);
-      const uint32_t op = raw.x & 0xFF, ia = (raw.x >> 8) & 0xFF, ib = (raw.x >> 16) & 0xFF, ic = raw.x >> 24;
-      const int32_t imm = (int32_t)raw.y;
+      const uint4 e = CODE_SMEM ? s_code[minpc]
+                                : predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + minpc), T, s_off, s_size);
+      const uint32_t op = e.x & 0xFF, aux = (e.x >> 8) & 0xFF;
+      int32_t* const Ra = Rg + (e.x >> 16);  // register operands of this lane
+      int32_t* const Rb = Rg + (e.y & 0xFFFF);
+      int32_t* const Rc = Rg + (e.y >> 16);
+      const int32_t imm = (int32_t)e.z;
       if (ex) {  // fuel check before executing (reading L17)
         if (steps == p.fuel) {
           emit_report(p, inst, -1, (int32_t)pc, tid, RC_FUEL);
@@ -265,15 +289,15 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
         }
       }
       switch (op) {  // warp-uniform
-        case RC_OP_CONST: if (ex) { Rg[ia * T] = imm; pc++; } break;
-        case RC_OP_MOV: if (ex) { Rg[ia * T] = Rg[ib * T]; pc++; } break;
-        case RC_OP_TID: if (ex) { Rg[ia * T] = (int32_t)tid; pc++; } break;
-        case RC_OP_SIZE: if (ex) { Rg[ia * T] = (int32_t)s_size[ib]; pc++; } break;
-        case RC_OP_ADDI: if (ex) { Rg[ia * T] = wadd(Rg[ib * T], imm); pc++; } break;
+        case RC_OP_CONST: if (ex) { *Ra = imm; pc++; } break;
+        case RC_OP_MOV: if (ex) { *Ra = *Rb; pc++; } break;
+        case RC_OP_TID: if (ex) { *Ra = (int32_t)tid; pc++; } break;
+        case RC_OP_SIZE: if (ex) { *Ra = imm; pc++; } break;
+        case RC_OP_ADDI: if (ex) { *Ra = wadd(*Rb, imm); pc++; } break;
         case RC_OP_ADD: case RC_OP_SUB: case RC_OP_MUL: case RC_OP_MIN: case RC_OP_MAX: case RC_OP_AND:
         case RC_OP_OR: case RC_OP_XOR: case RC_OP_LT: case RC_OP_EQ: case RC_OP_LAND:
           if (ex) {
-            const int32_t x = Rg[ib * T], y = Rg[ic * T];
+            const int32_t x = *Rb, y = *Rc;
             int32_t v;
             switch (op) {
               case RC_OP_ADD: v = wadd(x, y); break;
@@ -288,13 +312,13 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
               case RC_OP_EQ: v = x == y; break;
               default: v = (x != 0) && (y != 0); break;
             }
-            Rg[ia * T] = v;
+            *Ra = v;
             pc++;
           }
           break;
         case RC_OP_DIV: case RC_OP_MOD:
           if (ex) {
-            const int32_t x = Rg[ib * T], y = Rg[ic * T];
+            const int32_t x = *Rb, y = *Rc;
             if (y == 0) {
               emit_report(p, inst, -1, (int32_t)pc, tid, RC_DIV0);
               running = false;
@@ -303,29 +327,29 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
               int32_t v;
               if (op == RC_OP_DIV) v = (y == -1) ? (int32_t)(0u - (uint32_t)x) : x / y;
               else v = (y == -1) ? 0 : x % y;
-              Rg[ia * T] = v;
+              *Ra = v;
               pc++;
             }
           }
           break;
-        case RC_OP_LNOT: if (ex) { Rg[ia * T] = Rg[ib * T] == 0; pc++; } break;
+        case RC_OP_LNOT: if (ex) { *Ra = *Rb == 0; pc++; } break;
         case RC_OP_LD: {
           bool ok = false;
           uint32_t cell = 0;
           if (ex) {
-            const int32_t idx = Rg[ic * T];
-            if (idx < 0 || (uint32_t)idx >= s_size[ib]) {
-              emit_report(p, inst, (int32_t)ib, idx, tid, RC_OOB);
+            const int32_t idx = *Rc;
+            if ((uint32_t)idx >= e.w) {  // also catches idx < 0
+              emit_report(p, inst, (int32_t)aux, idx, tid, RC_OOB);
               running = false;
               status = L_OOB;
             } else {
-              cell = cell_base + s_off[ib] + (uint32_t)idx;
+              cell = cell_base + e.z + (uint32_t)idx;
               int32_t v = 0;
               bool found = false;
               for (int j = 0; j < n_own; j++)
                 if (ocell[j * T + t] == cell) { v = oval[j * T + t]; found = true; }
               if (!found) v = __ldg(p.heap + cell);
-              Rg[ia * T] = v;
+              *Ra = v;
               pc++;
               nloads++;
               ok = true;
@@ -341,20 +365,20 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
         }
         case RC_OP_ST:
           if (ex) {
-            const int32_t idx = Rg[ib * T];
-            if (idx < 0 || (uint32_t)idx >= s_size[ia]) {
-              emit_report(p, inst, (int32_t)ia, idx, tid, RC_OOB);
+            const int32_t idx = *Rb;
+            if ((uint32_t)idx >= e.w) {  // also catches idx < 0
+              emit_report(p, inst, (int32_t)aux, idx, tid, RC_OOB);
               running = false;
               status = L_OOB;
             } else {
-              const uint32_t cell = cell_base + s_off[ia] + (uint32_t)idx;
+              const uint32_t cell = cell_base + e.z + (uint32_t)idx;
               int j = 0;
               while (j < n_own && ocell[j * T + t] != cell) j++;
               if (j == n_own) {
                 if (n_own < (int)OV) { ocell[j * T + t] = cell; n_own++; }
                 else { ovl_over = true; j = -1; }
               }
-              if (j >= 0) oval[j * T + t] = Rg[ic * T];
+              if (j >= 0) oval[j * T + t] = *Rc;
               pc++;
               nstores++;
             }
@@ -364,13 +388,13 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
         case RC_OP_EXIT: if (ex) { running = false; status = L_EXITED_NOW; } break;
         case RC_OP_ASSUME:
           if (ex) {
-            if (Rg[ia * T] == 0) { running = false; status = L_PRUNED; }
+            if (*Ra == 0) { running = false; status = L_PRUNED; }
             else pc++;
           }
           break;
         case RC_OP_ASSERT:
           if (ex) {
-            if (Rg[ia * T] == 0) {
+            if (*Ra == 0) {
               emit_report(p, inst, -1, (int32_t)pc, tid, RC_ASSERT);
               running = false;
               status = L_ASSERT;
@@ -379,7 +403,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
             }
           }
           break;
-        case RC_OP_BR: if (ex) pc = Rg[ia * T] != 0 ? (uint32_t)imm : ib + 256u * ic; break;
+        case RC_OP_BR: if (ex) pc = *Ra != 0 ? (uint32_t)imm : e.w; break;
         case RC_OP_JMP: if (ex) pc = (uint32_t)imm; break;
         default: break;  // unreachable: the validator rejects unknown opcodes
       }
@@ -493,7 +517,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
 size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem) {
   const int W = T / 32;
   size_t b = (size_t)W * p.stage * 8;              // staging
-  b += code_in_smem ? (size_t)p.n_instr * 8 : 0;   // program
+  b += code_in_smem ? (size_t)p.n_instr * 16 : 0;  // pre-decoded program
   b += (size_t)p.passes * 256 * 4;                 // block digit histograms
   b += (size_t)p.n_regs * T * 4;                   // registers
   b += (size_t)p.ovl_cap * T * 8;                  // overlay
