@@ -171,6 +171,45 @@ __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
 
 __device__ __forceinline__ int32_t wadd(int32_t x, int32_t y) { return (int32_t)((uint32_t)x + (uint32_t)y); }
 
+// ---- TMA bulk copies (cp.async.bulk) of lane-state rows ---------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(unsigned long long* mbar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(mbar)), "r"(parity)
+        : "memory");
+}
+
+// one thread: load the lane state (status, pc, live register rows) of `tile`
+// into shared-memory buffer b; rows are padded so every copy is 16-B aligned
+__device__ __forceinline__ void prefetch_lanes(const InterpParams& p, uint32_t tile, int T, uint8_t* st, uint32_t* pcs,
+                                               int32_t* regs, const uint8_t* live, unsigned long long* mbar) {
+  const uint32_t bytes = (uint32_t)T * (1 + 4 + 4 * p.n_live);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes) : "memory");
+  const size_t g0 = (size_t)tile * T;
+  bulk_g2s(st, p.status_in + g0, (uint32_t)T, mbar);
+  bulk_g2s(pcs, p.pc_in + g0, (uint32_t)T * 4, mbar);
+  for (uint32_t i = 0; i < p.n_live; i++) {
+    const uint32_t r = live[i];
+    bulk_g2s(regs + (size_t)r * T, p.regs_in + (size_t)r * p.reg_stride + g0, (uint32_t)T * 4, mbar);
+  }
+}
+
 // Pre-decoded instruction (16 B, shared memory): register operands become word
 // offsets r*T into the [reg][thread] register file; LD/ST/SIZE fold in the
 // array's cell offset and size, BR its false target.
@@ -206,10 +245,16 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
 
   // ---- shared memory carve-up (sizes mirrored in interp_smem_bytes)
   unsigned char* q = smem;
+  int32_t* sregs_b[2];   // register files [reg][thread], double-buffered (TMA)
+  uint8_t* sstat_b[2];
+  uint32_t* spc_b[2];
+  for (int b = 0; b < 2; b++) { sregs_b[b] = reinterpret_cast<int32_t*>(q); q += (size_t)R * T * 4; }
+  for (int b = 0; b < 2; b++) { spc_b[b] = reinterpret_cast<uint32_t*>(q); q += (size_t)T * 4; }
+  for (int b = 0; b < 2; b++) { sstat_b[b] = reinterpret_cast<uint8_t*>(q); q += (size_t)T; }
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(q); q += 16;
   uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)W * p.stage * 8;
   uint4* s_code = reinterpret_cast<uint4*>(q); q += CODE_SMEM ? (size_t)p.n_instr * 16 : 0;
   uint32_t* bhist = reinterpret_cast<uint32_t*>(q); q += (size_t)p.passes * 256 * 4;  // block digit histograms
-  int32_t* sregs = reinterpret_cast<int32_t*>(q); q += (size_t)R * T * 4;
   uint32_t* ocell = reinterpret_cast<uint32_t*>(q); q += (size_t)OV * T * 4;
   int32_t* oval = reinterpret_cast<int32_t*>(q); q += (size_t)OV * T * 4;
   uint32_t* s_off = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
@@ -230,37 +275,55 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
     for (uint32_t i = t; i < p.n_instr; i += T) s_code[i] = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + i), T, s_off, s_size);
   for (int i = t; i < p.passes * 256; i += T) bhist[i] = 0;
   for (uint32_t i = t; i < p.n_live; i += T) s_live[i] = p.live[i];
+  const uint32_t n_tiles0 = (p.n_lanes + T - 1) / T;
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
+  if (t == 0 && blockIdx.x < n_tiles0)
+    prefetch_lanes(p, blockIdx.x, T, sstat_b[0], spc_b[0], sregs_b[0], s_live, &mbar[0]);
 
   // block totals: lane l of warp 0 accumulates the statistics of warp l
   unsigned long long b_instr = 0, b_loads = 0, b_stores = 0;
   bool b_wait = false, b_over = false;
   const uint32_t n_tiles = (p.n_lanes + T - 1) / T;
 
-  for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  uint32_t parity = 0;  // bit b: expected phase of mbar[b]
+  int cur = 0;
+  for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, cur ^= 1) {
+    // prefetch the next tile's lane state into the other buffer once the bulk
+    // stores of its previous use have finished reading it
+    if (t == 0 && tile + gridDim.x < n_tiles) {
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      prefetch_lanes(p, tile + gridDim.x, T, sstat_b[cur ^ 1], spc_b[cur ^ 1], sregs_b[cur ^ 1], s_live,
+                     &mbar[cur ^ 1]);
+    }
+    mbar_wait_parity(&mbar[cur], (parity >> cur) & 1u);
+    parity ^= 1u << cur;
+    uint8_t* const sstat = sstat_b[cur];
+    uint32_t* const spc = spc_b[cur];
     const uint32_t g = tile * (uint32_t)T + t;
     const bool valid = g < p.n_lanes;
-    uint8_t status = valid ? p.status_in[g] : (uint8_t)L_EXITED;
-    uint32_t pc = valid ? p.pc_in[g] : 0;  // independent of the status load
+    uint8_t status = valid ? sstat[t] : (uint8_t)L_EXITED;
+    uint32_t pc = valid ? spc[t] : 0;
     if (status == L_EXITED_NOW) status = L_EXITED;
     bool running = valid && (status == L_RUNNING || status == L_WAITING);
     const uint32_t inst = valid ? g / p.n : 0;
     const uint32_t tid = valid ? g - inst * p.n : 0;
     const uint32_t cell_base = inst * p.cpi;
-    int32_t* Rg = sregs + t;  // register r of this lane = Rg[r*T]
-    if (running)  // live registers in batches of 4 independent loads
-      for (uint32_t i0 = 0; i0 < p.n_live; i0 += 4) {
-        int32_t v[4];
-#pragma unroll
-        for (int j = 0; j < 4; j++)
-          if (i0 + j < p.n_live) v[j] = p.regs_in[(size_t)s_live[i0 + j] * p.n_lanes + g];
-#pragma unroll
-        for (int j = 0; j < 4; j++)
-          if (i0 + j < p.n_live) Rg[s_live[i0 + j] * T] = v[j];
-      }
-    __syncthreads();
+    int32_t* Rg = sregs_b[cur] + t;  // register r of this lane = Rg[r*T] (live ones arrived by TMA)
 
     if (running) status = L_RUNNING;
+    // non-blocking loads: up to NP issued LDs whose destination register is
+    // written back only when an instruction touches it (software scoreboard)
+    constexpr int NP = 4;
+    int32_t pv[NP];
+    uint32_t pr[NP];  // destination word offset, or NOREG
+    constexpr uint32_t NOREG = 0xFFFFFFFFu;
+#pragma unroll
+    for (int j = 0; j < NP; j++) { pr[j] = NOREG; pv[j] = 0; }
     int n_own = 0;
     unsigned long long steps = 0;
     uint32_t nloads = 0, nstores = 0;
@@ -278,6 +341,16 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
       int32_t* const Rb = Rg + (e.y & 0xFFFF);
       int32_t* const Rc = Rg + (e.y >> 16);
       const int32_t imm = (int32_t)e.z;
+      if (__any_sync(FULL, ex && (pr[0] != NOREG || pr[1] != NOREG || pr[2] != NOREG || pr[3] != NOREG))) {
+        // an instruction touching a pending register materialises it first
+        const uint32_t oa = e.x >> 16, ob = e.y & 0xFFFF, oc = e.y >> 16;
+#pragma unroll
+        for (int j = 0; j < NP; j++)
+          if (ex && pr[j] != NOREG && (pr[j] == oa || pr[j] == ob || pr[j] == oc)) {
+            Rg[pr[j]] = pv[j];
+            pr[j] = NOREG;
+          }
+      }
       if (ex) {  // fuel check before executing (reading L17)
         if (steps == p.fuel) {
           emit_report(p, inst, -1, (int32_t)pc, tid, RC_FUEL);
@@ -348,8 +421,21 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
               bool found = false;
               for (int j = 0; j < n_own; j++)
                 if (ocell[j * T + t] == cell) { v = oval[j * T + t]; found = true; }
-              if (!found) v = __ldg(p.heap + cell);
-              *Ra = v;
+              if (found) {
+                *Ra = v;
+              } else {  // issue the load; write the register back later
+                if (pr[NP - 1] != NOREG) {  // all slots busy: retire them
+#pragma unroll
+                  for (int j = 0; j < NP; j++) { Rg[pr[j]] = pv[j]; pr[j] = NOREG; }
+                }
+                const int32_t lv = __ldg(p.heap + cell);
+                const uint32_t oa = e.x >> 16;
+                // first free slot (slots fill in order)
+                if (pr[0] == NOREG) { pv[0] = lv; pr[0] = oa; }
+                else if (pr[1] == NOREG) { pv[1] = lv; pr[1] = oa; }
+                else if (pr[2] == NOREG) { pv[2] = lv; pr[2] = oa; }
+                else { pv[3] = lv; pr[3] = oa; }
+              }
               pc++;
               nloads++;
               ok = true;
@@ -408,6 +494,11 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
         default: break;  // unreachable: the validator rejects unknown opcodes
       }
     }
+
+    // retire the pending loads (registers of suspended lanes are saved below)
+#pragma unroll
+    for (int j = 0; j < NP; j++)
+      if (pr[j] != NOREG) Rg[pr[j]] = pv[j];
 
     // write records: one per distinct written cell; its final value (reading
     // L3) goes to the side table wval[slot][lane] read by detect
@@ -480,23 +571,27 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
         wbase[W + lane] = br + xr - cr;
       }
     }
-    // lane state out (only registers live across the barrier, only for
-    // suspended lanes) while warp 0 waits for the reservations
-    if (valid) {
-      p.status_out[g] = status;
-      if (status == L_WAITING) {
-        p.pc_out[g] = pc;
-        for (uint32_t i = 0; i < p.n_live; i++) {
-          const uint32_t r = s_live[i];
-          p.regs_out[(size_t)r * p.n_lanes + g] = Rg[r * T];
-        }
-      }
-    }
+    // lane state out: status / pc into the shared rows (the live register
+    // rows already are), then bulk stores of every row
+    sstat[t] = valid ? status : (uint8_t)L_EXITED;
+    spc[t] = pc;
     __syncthreads();
+    if (t == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const size_t g0 = (size_t)tile * T;
+      bulk_s2g(p.status_out + g0, sstat, (uint32_t)T);
+      bulk_s2g(p.pc_out + g0, spc, (uint32_t)T * 4);
+      for (uint32_t i = 0; i < p.n_live; i++) {
+        const uint32_t r = s_live[i];
+        bulk_s2g(p.regs_out + (size_t)r * p.reg_stride + g0, sregs_b[cur] + (size_t)r * T, (uint32_t)T * 4);
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
     write_out(lo, S.recs, S.fill, wbase[warp], wbase[W + warp], bhist, lane, &b_over);
     __syncthreads();  // staging / overlay / registers reused by the next tile
   }
 
+  if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // lane-state stores complete
   // ---- block flush: histograms, statistics, flags
   for (int i = t; i < p.passes * 256; i += T)
     if (bhist[i]) atomicAdd(&p.hist[i], bhist[i]);
@@ -516,10 +611,11 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
 
 size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem) {
   const int W = T / 32;
-  size_t b = (size_t)W * p.stage * 8;              // staging
+  size_t b = (size_t)2 * p.n_regs * T * 4;         // register files (double-buffered)
+  b += (size_t)2 * T * 5 + 16;                     // status / pc rows, mbarriers
+  b += (size_t)W * p.stage * 8;                    // staging
   b += code_in_smem ? (size_t)p.n_instr * 16 : 0;  // pre-decoded program
   b += (size_t)p.passes * 256 * 4;                 // block digit histograms
-  b += (size_t)p.n_regs * T * 4;                   // registers
   b += (size_t)p.ovl_cap * T * 8;                  // overlay
   b += (size_t)p.n_arrays * 8;                     // array offsets / sizes
   b += ((size_t)p.n_live + 3) & ~size_t(3);        // live register list

@@ -49,6 +49,7 @@ constexpr int OVL_CAP = 16;        // own-write overlay entries per work-item (s
 //   bits  4..1   overlay slot of a write (its final value is wval[slot][lane])
 //   bit      0   1 = write, 0 = read
 constexpr int REC_CELL_SHIFT = 32;
+constexpr uint32_t LANE_PAD = 256;  // lane-state rows are padded to multiples of this (TMA tiles)
 constexpr uint32_t MAX_WG = 1u << 27;
 __host__ __device__ inline uint64_t make_rec(uint32_t cell, uint32_t tid, uint32_t slot, uint32_t w) {
   return ((uint64_t)cell << 32) | (tid << 5) | (slot << 1) | w;
@@ -86,7 +87,8 @@ struct InterpParams {
   const uint32_t* arr_size;   // [n_arrays]
   const int32_t* heap;        // interval-start shared heap [I_b][cpi]
   // lane state in / out (SoA)
-  const int32_t* regs_in;     // [n_regs][n_lanes]
+  uint32_t reg_stride;        // row stride of the register arrays (>= n_lanes, multiple of 256)
+  const int32_t* regs_in;     // [n_regs][reg_stride]; status / pc rows are padded to reg_stride too
   const uint32_t* pc_in;
   const uint8_t* status_in;
   int32_t* regs_out;

@@ -279,15 +279,16 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   CK(cudaMemGetInfo(&free_b, &total_b));
   const uint32_t I_b = plan_batch(n_inst, n, cpi, P->n_regs, opt.max_batch_instances, free_b);
   const uint64_t L_max = (uint64_t)I_b * n;
+  const uint64_t L_pad = (L_max + LANE_PAD - 1) / LANE_PAD * LANE_PAD + LANE_PAD;  // TMA rows, + a spare tile
   const int key_bits = bits_for((uint64_t)I_b * std::max<uint64_t>(cpi, 1));
 
   // batch-sized buffers
   if (I_b) {
     CK(W.heap.ensure(std::max<uint64_t>(1, (uint64_t)I_b * cpi) * 4));
     for (int b = 0; b < 2; b++) {
-      CK(W.regs[b].ensure(std::max<uint64_t>(1, L_max * P->n_regs) * 4));
-      CK(W.pc[b].ensure(std::max<uint64_t>(1, L_max) * 4));
-      CK(W.status[b].ensure(std::max<uint64_t>(1, L_max)));
+      CK(W.regs[b].ensure(L_pad * P->n_regs * 4));
+      CK(W.pc[b].ensure(L_pad * 4));
+      CK(W.status[b].ensure(L_pad));
     }
     CK(W.inst_tmp.ensure((uint64_t)I_b * 20));
     CK(W.wval.ensure(std::max<uint64_t>(1, L_max * (uint64_t)P->ovl_cap) * 4));
@@ -380,10 +381,11 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       return bp;
     };
     int cur = 0;
+    const uint32_t reg_stride = (uint32_t)((L + LANE_PAD - 1) / LANE_PAD * LANE_PAD);
     if (L) {
-      CK(cudaMemsetAsync(W.status[cur].p, 0, L, s));
-      CK(cudaMemsetAsync(W.pc[cur].p, 0, (size_t)L * 4, s));
-      CK(cudaMemsetAsync(W.regs[cur].p, 0, (size_t)L * P->n_regs * 4, s));  // registers start at 0 (L18)
+      CK(cudaMemsetAsync(W.status[cur].p, 0, reg_stride, s));
+      CK(cudaMemsetAsync(W.pc[cur].p, 0, (size_t)reg_stride * 4, s));
+      CK(cudaMemsetAsync(W.regs[cur].p, 0, (size_t)reg_stride * P->n_regs * 4, s));  // registers start at 0 (L18)
     }
     uint32_t k = 0;
     for (;;) {
@@ -408,6 +410,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         ip.arr_off = W.arr_off.as<uint32_t>();
         ip.arr_size = W.arr_size.as<uint32_t>();
         ip.heap = W.heap.as<int32_t>();
+        ip.reg_stride = reg_stride;
         ip.regs_in = W.regs[cur].as<int32_t>();
         ip.pc_in = W.pc[cur].as<uint32_t>();
         ip.status_in = W.status[cur].as<uint8_t>();
