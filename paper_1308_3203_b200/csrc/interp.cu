@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
               if (found) {
                 *Ra = v;
               } else {  // issue the load; write the register back later
-                if (pr[NP - 1] != NOREG) {  // all slots busy: retire them
+                if (pr[0] != NOREG && pr[1] != NOREG && pr[2] != NOREG && pr[3] != NOREG) {  // all busy: retire
 #pragma unroll
                   for (int j = 0; j < NP; j++) { Rg[pr[j]] = pv[j]; pr[j] = NOREG; }
                 }
