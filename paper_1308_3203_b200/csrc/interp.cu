@@ -233,6 +233,30 @@ __device__ __forceinline__ uint4 predecode(uint2 raw, int T, const uint32_t* s_o
 
 }  // namespace
 
+// dev-only per-phase cycle accounting (build with -DINTERP_PHASE_TIMING; the
+// runtime prints the totals to stderr when RC_PHASES is set)
+#ifdef INTERP_PHASE_TIMING
+__device__ unsigned long long g_iphase[8];
+void interp_phase_io(unsigned long long* out, bool reset) {
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_iphase, z, sizeof z);
+  } else {
+    cudaMemcpyFromSymbol(out, g_iphase, sizeof(unsigned long long) * 8);
+  }
+}
+#define IPHASE(i)                                 \
+  do {                                            \
+    if (t == 0) {                                 \
+      const long long now_ = clock64();           \
+      atomicAdd(&g_iphase[i], now_ - tprev_);     \
+      tprev_ = now_;                              \
+    }                                             \
+  } while (0)
+#else
+#define IPHASE(i) do {} while (0)
+#endif
+
 template <bool CODE_SMEM>
 __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -292,6 +316,9 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
 
   uint32_t parity = 0;  // bit b: expected phase of mbar[b]
   int cur = 0;
+#ifdef INTERP_PHASE_TIMING
+  long long tprev_ = clock64();
+#endif
   for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, cur ^= 1) {
     // prefetch the next tile's lane state into the other buffer once the bulk
     // stores of its previous use have finished reading it
@@ -300,8 +327,10 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
       prefetch_lanes(p, tile + gridDim.x, T, sstat_b[cur ^ 1], spc_b[cur ^ 1], sregs_b[cur ^ 1], s_live,
                      &mbar[cur ^ 1]);
     }
+    IPHASE(0);
     mbar_wait_parity(&mbar[cur], (parity >> cur) & 1u);
     parity ^= 1u << cur;
+    IPHASE(1);
     uint8_t* const sstat = sstat_b[cur];
     uint32_t* const spc = spc_b[cur];
     const uint32_t g = tile * (uint32_t)T + t;
@@ -495,6 +524,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
       }
     }
 
+    IPHASE(2);
     // retire the pending loads (registers of suspended lanes are saved below)
 #pragma unroll
     for (int j = 0; j < NP; j++)
@@ -514,6 +544,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
       S.fill += __popc(m);
     }
 
+    IPHASE(3);
     // fused A4: arrival node range per instance (fire-and-forget atomics,
     // one pair per warp when the warp lies in one instance), suspended flag
     const bool arrived = valid && (status == L_WAITING || status == L_EXITED_NOW);
@@ -548,6 +579,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
     }
     b_wait |= any_wait;
     __syncthreads();
+    IPHASE(4);
     if (warp == 0) {  // lanes < W: prefix over warps, both reservations in flight at once
       const uint32_t cw = lane < W ? wcntw[lane] : 0u, cr = lane < W ? wcntr[lane] : 0u;
       uint32_t xw = cw, xr = cr;
@@ -576,6 +608,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
     sstat[t] = valid ? status : (uint8_t)L_EXITED;
     spc[t] = pc;
     __syncthreads();
+    IPHASE(5);
     if (t == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       const size_t g0 = (size_t)tile * T;
@@ -588,7 +621,9 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
     write_out(lo, S.recs, S.fill, wbase[warp], wbase[W + warp], bhist, lane, &b_over);
+    IPHASE(6);
     __syncthreads();  // staging / overlay / registers reused by the next tile
+    IPHASE(7);
   }
 
   if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // lane-state stores complete

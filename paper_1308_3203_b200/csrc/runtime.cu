@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -23,6 +24,9 @@
 
 namespace rc {
 int fail(int code, const char* fmt, ...);
+#ifdef INTERP_PHASE_TIMING
+void interp_phase_io(unsigned long long* out, bool reset);
+#endif
 std::atomic<uint64_t> g_launches{0};
 
 size_t Profiler::next() {
@@ -575,6 +579,19 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     }
   }
 
+#ifdef INTERP_PHASE_TIMING
+  if (getenv("RC_PHASES")) {
+    unsigned long long ph[8];
+    cudaStreamSynchronize(s);
+    interp_phase_io(ph, false);
+    const char* nm[8] = {"prefetch-issue", "lane-state wait", "interpret", "pending+writes", "A4+counts+sync",
+                         "reserve+state", "write-out", "end sync"};
+    double tot = 0;
+    for (int i = 0; i < 8; i++) tot += (double)ph[i];
+    for (int i = 0; i < 8; i++) fprintf(stderr, "K1 phase %-16s %6.1f%%\n", nm[i], 100.0 * ph[i] / (tot > 0 ? tot : 1));
+    interp_phase_io(nullptr, true);
+  }
+#endif
   // K6: canonical order, then the first min(capacity, total) to the host
   if (rep_count > 1) {
     CK(W.reports_scratch.ensure(std::max<uint64_t>(rep_count, 2048) * 2 * sizeof(rc_report)));
