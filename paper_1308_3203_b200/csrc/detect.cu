@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
   const unsigned FULL = 0xFFFFFFFFu;
   const int lane = threadIdx.x & 31;
   const uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t n_records = (uint32_t)(p.ctr->wlog_count + p.ctr->kept_count);
+  const uint32_t n_records = (uint32_t)p.ctr->kept_count;
   const uint64_t c0 = wg * DET_CHUNK;
   if (c0 >= n_records) return;  // whole warp
   const uint64_t c1 = min((uint64_t)n_records, c0 + DET_CHUNK);

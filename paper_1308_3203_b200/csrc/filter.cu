@@ -1,14 +1,15 @@
-// filter.cu — write-set filter between K1 and the sort.
+// filter.cu — write-set filter / compaction between K1 and the sort.
 //
-// A read record of a cell that no work-item wrote in this interval can take
-// part in no RW report (P:224-229 needs a writer), in no WW report and in no
-// commit, so it is dropped before the sort; the reads of written
-// cells are appended to the sort buffer after the write records.  K1 marked
-// every written cell in the byte map wmap (plain idempotent byte stores).
-// Exactness: the per-cell sets R(c) and W(c) of every cell with W(c) != {}
-// are unchanged, and cells with W(c) = {} produce no output.
+// K1 staged the interval's access records in per-block chunks of one staging
+// buffer (unused chunk tails hold REC_SENTINEL) and marked every written cell
+// in the byte map wmap.  This pass keeps every write record and the read
+// records of written cells and writes them densely to the sort buffer.  A read
+// of a cell that no work-item wrote in this interval can take part in no RW
+// report (P:224-229 needs a writer), no WW report and no commit, so
+// dropping it is exact: R(c) and W(c) of every cell with W(c) != {} are
+// unchanged, and cells with W(c) = {} produce no output.
 //
-// Also fuses the sort's digit histograms of the kept reads.
+// Also computes the sort's digit histograms of the kept records (fused K2).
 #include "rc_internal.h"
 
 namespace rc {
@@ -30,8 +31,7 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
   __shared__ unsigned long long sbase;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   for (int i = t; i < p.passes * 256; i += F_THREADS) bh[i] = 0;
-  const uint64_t nr = p.ctr->rlog_count;
-  const uint64_t nw = p.ctr->wlog_count;
+  const uint64_t nr = p.ctr->stage_count;
   const uint64_t step = (uint64_t)gridDim.x * F_THREADS * F_ITEMS;
   __syncthreads();
   for (uint64_t b0 = (uint64_t)blockIdx.x * F_THREADS * F_ITEMS; b0 < nr; b0 += step) {
@@ -40,12 +40,12 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
 #pragma unroll
     for (int j = 0; j < F_ITEMS; j++) {
       const uint64_t i = b0 + (uint64_t)j * F_THREADS + t;
-      rec[j] = i < nr ? __ldg(p.rlog + i) : 0ull;
+      rec[j] = i < nr ? __ldg(p.stage + i) : REC_SENTINEL;
     }
 #pragma unroll
     for (int j = 0; j < F_ITEMS; j++) {
       const uint64_t i = b0 + (uint64_t)j * F_THREADS + t;
-      keep[j] = i < nr && __ldg(p.wmap + (rec[j] >> REC_CELL_SHIFT)) != 0;
+      keep[j] = rec[j] != REC_SENTINEL && ((rec[j] & 1) || __ldg(p.wmap + (rec[j] >> REC_CELL_SHIFT)) != 0);
     }
     uint32_t mine = 0;
 #pragma unroll
@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
     }
     if (t == 0) sbase = tot ? atomicAdd(&p.ctr->kept_count, (unsigned long long)tot) : 0ull;
     __syncthreads();
-    uint64_t pos = nw + sbase + woff + x - mine;
+    uint64_t pos = sbase + woff + x - mine;
 #pragma unroll
     for (int j = 0; j < F_ITEMS; j++) {
       if (keep[j]) p.out[pos++] = rec[j];
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
 }
 
 cudaError_t launch_filter(const FilterParams& p, cudaStream_t s) {
-  if (p.n_reads_ub == 0) return cudaSuccess;
+  if (p.n_slots == 0) return cudaSuccess;
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;
@@ -100,7 +100,7 @@ cudaError_t launch_filter(const FilterParams& p, cudaStream_t s) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   const uint64_t per_block = (uint64_t)F_THREADS * F_ITEMS;
-  const uint32_t grid = (uint32_t)std::min<uint64_t>((p.n_reads_ub + per_block - 1) / per_block, (uint64_t)nsm * 8);
+  const uint32_t grid = (uint32_t)std::min<uint64_t>((p.n_slots + per_block - 1) / per_block, (uint64_t)nsm * 8);
   filter_kernel<<<grid, F_THREADS, 0, s>>>(p);
   launched();
   return cudaGetLastError();

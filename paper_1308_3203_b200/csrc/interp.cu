@@ -77,91 +77,44 @@ struct Stage {
   uint32_t cap;
 };
 
-// digit histograms (fused K2) of the write records of one 32-record chunk:
-// when every write lane of the chunk has the same digit (long runs: records
-// are staged in lane order) one lane adds the whole count
-__device__ __forceinline__ void hist_writes(uint64_t rec, bool isw, unsigned mw, int passes, uint32_t* bh,
-                                            int lane) {
-  if (!mw) return;
-  const int first = __ffs(mw) - 1;
-  for (int p = 0; p < passes; p++) {
-    const uint32_t d = (uint32_t)(rec >> (REC_CELL_SHIFT + 8 * p)) & 0xFF;
-    const uint32_t d0 = __shfl_sync(FULL, d, first);
-    if (__all_sync(FULL, !isw || d == d0)) {
-      if (lane == first) atomicAdd(&bh[p * 256 + d0], (uint32_t)__popc(mw));
-    } else if (isw) {
-      atomicAdd(&bh[p * 256 + d], 1u);
-    }
-  }
-}
-
 // the parts of InterpParams the log write-out needs (passed by value so the
 // kernel's parameter block is never copied to local memory)
 struct LogOut {
-  uint64_t* wlog;
-  uint64_t* rlog;
+  uint64_t* stage;
   uint8_t* wmap;
   DevCounters* ctr;
-  unsigned long long log_cap;
-  int passes;
+  unsigned long long cap;
 };
 
-// Split-write `cnt` staged records of this warp: writes to wlog[bw + ...]
-// (marking wmap), reads to rlog[br + ...].  Whole warp.
+// Copy `cnt` staged records of this warp to stage[base, base + cnt) and mark
+// the cells of write records in the write-set map.  Whole warp.
 __device__ __forceinline__ void write_out(const LogOut& p, const uint64_t* recs, uint32_t cnt,
-                                          unsigned long long bw, unsigned long long br, uint32_t* bh, int lane,
-                                          bool* over) {
-  uint32_t runw = 0, runr = 0;
-  for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
-    const uint32_t i = i0 + lane;
-    const bool in = i < cnt;
-    const uint64_t rec = in ? recs[i] : 0ull;
-    const bool isw = in && (rec & 1);
-    const bool isr = in && !(rec & 1);
-    const unsigned mw = __ballot_sync(FULL, isw), mr = __ballot_sync(FULL, isr);
-    if (isw) {
-      const unsigned long long pos = bw + runw + __popc(mw & lanemask_lt());
-      if (pos < p.log_cap) p.wlog[pos] = rec;
-      else *over = true;
-      p.wmap[rec >> REC_CELL_SHIFT] = 1;
-    }
-    if (isr) {
-      const unsigned long long pos = br + runr + __popc(mr & lanemask_lt());
-      if (pos < p.log_cap) p.rlog[pos] = rec;
-      else *over = true;
-    }
-    hist_writes(rec, isw, mw, p.passes, bh, lane);
-    runw += __popc(mw);
-    runr += __popc(mr);
+                                          unsigned long long base, int lane, bool* over) {
+  for (uint32_t i = lane; i < cnt; i += 32) {
+    const uint64_t rec = recs[i];
+    if (base + i < p.cap) p.stage[base + i] = rec;
+    else *over = true;
+    if (rec & 1) p.wmap[rec >> REC_CELL_SHIFT] = 1;
   }
-}
-
-__device__ __forceinline__ uint32_t count_writes(const uint64_t* recs, uint32_t cnt, int lane) {
-  uint32_t c = 0;
-  for (uint32_t i = lane; i < cnt; i += 32) c += (uint32_t)(recs[i] & 1);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
-  return c;
 }
 
 // mid-interval overflow of a warp's staging buffer: flush it on its own
-__device__ __noinline__ uint32_t flush_warp_(const LogOut p, const uint64_t* recs, uint32_t fill, int lane,
-                                             uint32_t* bh) {
+__device__ __noinline__ uint32_t flush_warp_(const LogOut p, const uint64_t* recs, uint32_t fill, int lane) {
   __syncwarp();
-  const uint32_t nw = count_writes(recs, fill, lane);
-  unsigned long long bw = 0, br = 0;
+  unsigned long long base = 0;
   if (lane == 0) {
-    bw = atomicAdd(&p.ctr->wlog_count, (unsigned long long)nw);
-    br = atomicAdd(&p.ctr->rlog_count, (unsigned long long)(fill - nw));
+    base = atomicAdd(&p.ctr->stage_count, (unsigned long long)fill);
+    atomicAdd(&p.ctr->staged_recs, (unsigned long long)fill);
   }
-  bw = __shfl_sync(FULL, bw, 0);
-  br = __shfl_sync(FULL, br, 0);
+  base = __shfl_sync(FULL, base, 0);
   bool over = false;
-  write_out(p, recs, fill, bw, br, bh, lane, &over);
+  write_out(p, recs, fill, base, lane, &over);
   if (__any_sync(FULL, over) && lane == 0) p.ctr->log_overflow = 1;
   __syncwarp();
   return 0;
 }
+
+constexpr uint32_t STAGE_CHUNK = 8192;  // staging slots a block reserves at a time
 
 __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
 #pragma unroll
@@ -265,7 +218,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
   const int t = threadIdx.x;
   const int warp = t >> 5, lane = t & 31;
   const uint32_t R = p.n_regs, OV = p.ovl_cap;
-  const LogOut lo{p.wlog, p.rlog, p.wmap, p.ctr, p.log_cap, p.passes};
+  const LogOut lo{p.stage, p.wmap, p.ctr, p.stage_cap};
 
   // ---- shared memory carve-up (sizes mirrored in interp_smem_bytes)
   unsigned char* q = smem;
@@ -276,18 +229,16 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
   for (int b = 0; b < 2; b++) { spc_b[b] = reinterpret_cast<uint32_t*>(q); q += (size_t)T * 4; }
   for (int b = 0; b < 2; b++) { sstat_b[b] = reinterpret_cast<uint8_t*>(q); q += (size_t)T; }
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(q); q += 16;
-  uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)W * p.stage * 8;
+  uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)W * p.stage_warp * 8;
   uint4* s_code = reinterpret_cast<uint4*>(q); q += CODE_SMEM ? (size_t)p.n_instr * 16 : 0;
-  uint32_t* bhist = reinterpret_cast<uint32_t*>(q); q += (size_t)p.passes * 256 * 4;  // block digit histograms
   uint32_t* ocell = reinterpret_cast<uint32_t*>(q); q += (size_t)OV * T * 4;
   int32_t* oval = reinterpret_cast<int32_t*>(q); q += (size_t)OV * T * 4;
   uint32_t* s_off = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
   uint32_t* s_size = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
   uint8_t* s_live = reinterpret_cast<uint8_t*>(q); q += (p.n_live + 3) & ~3u;
-  uint32_t* wcntw = reinterpret_cast<uint32_t*>(q); q += (size_t)W * 4;   // per-warp write records
-  uint32_t* wcntr = reinterpret_cast<uint32_t*>(q); q += (size_t)W * 4;   // per-warp read records (|wait flag)
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(q); q += (size_t)W * 4 + 8;  // per-warp staged records, pad count
   q = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(q) + 7) & ~uintptr_t(7));
-  unsigned long long* wbase = reinterpret_cast<unsigned long long*>(q); q += (size_t)2 * W * 8;  // [W] w, [W] r
+  unsigned long long* wbase = reinterpret_cast<unsigned long long*>(q); q += (size_t)(W + 1) * 8;  // [W], pad start
   unsigned long long* wstat = reinterpret_cast<unsigned long long*>(q);  // [3][W]
 
   for (uint32_t a = t; a < p.n_arrays; a += T) {
@@ -297,7 +248,6 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
   __syncthreads();  // s_off / s_size before the pre-decode
   if (CODE_SMEM)
     for (uint32_t i = t; i < p.n_instr; i += T) s_code[i] = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + i), T, s_off, s_size);
-  for (int i = t; i < p.passes * 256; i += T) bhist[i] = 0;
   for (uint32_t i = t; i < p.n_live; i += T) s_live[i] = p.live[i];
   const uint32_t n_tiles0 = (p.n_lanes + T - 1) / T;
   if (t == 0) {
@@ -312,6 +262,9 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
   // block totals: lane l of warp 0 accumulates the statistics of warp l
   unsigned long long b_instr = 0, b_loads = 0, b_stores = 0;
   bool b_wait = false, b_over = false;
+  // the block's current staging chunk (thread 0)
+  unsigned long long c_base = 0;
+  uint32_t c_used = 0, c_cap = 0;
   const uint32_t n_tiles = (p.n_lanes + T - 1) / T;
 
   uint32_t parity = 0;  // bit b: expected phase of mbar[b]
@@ -357,7 +310,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
     unsigned long long steps = 0;
     uint32_t nloads = 0, nstores = 0;
     bool ovl_over = false;
-    Stage S{st_recs + (size_t)warp * p.stage, 0, p.stage};
+    Stage S{st_recs + (size_t)warp * p.stage_warp, 0, p.stage_warp};
 
     for (;;) {
       if (__ballot_sync(FULL, running) == 0) break;
@@ -472,7 +425,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
           }
           const unsigned m = __ballot_sync(FULL, ok);
           if (m) {
-            if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane, bhist);
+            if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane);
             if (ok) S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, tid, 0, 0);
             S.fill += __popc(m);
           }
@@ -536,7 +489,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
     for (int j = 0; j < max_own; j++) {
       const bool has = j < n_own;
       const unsigned m = __ballot_sync(FULL, has);
-      if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane, bhist);
+      if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane);
       if (has) {
         S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(ocell[j * T + t], tid, (uint32_t)j, 1);
         p.wval[(size_t)j * p.n_lanes + g] = oval[j * T + t];
@@ -565,13 +518,12 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
       atomicMax(p.node_max + inst, node);
     }
 
-    // ---- tile write-out: one atomic per record kind per block
+    // ---- tile write-out into the block's staging chunk (a new chunk — one
+    //      atomic — only when the current one is full; its tail is padded)
     const unsigned long long s0 = warp_sum64(steps), s1 = warp_sum64(nloads), s2 = warp_sum64(nstores);
     const bool any_ovl = __any_sync(FULL, ovl_over);
-    const uint32_t nw = count_writes(S.recs, S.fill, lane);
     if (lane == 0) {
-      wcntw[warp] = nw;
-      wcntr[warp] = S.fill - nw;
+      wcnt[warp] = S.fill;
       wstat[warp] = s0;
       wstat[W + warp] = s1;
       wstat[2 * W + warp] = s2;
@@ -580,27 +532,39 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
     b_wait |= any_wait;
     __syncthreads();
     IPHASE(4);
-    if (warp == 0) {  // lanes < W: prefix over warps, both reservations in flight at once
-      const uint32_t cw = lane < W ? wcntw[lane] : 0u, cr = lane < W ? wcntr[lane] : 0u;
-      uint32_t xw = cw, xr = cr;
+    if (warp == 0) {
+      const uint32_t c = lane < W ? wcnt[lane] : 0u;
+      uint32_t x = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t yw = __shfl_up_sync(FULL, xw, o), yr = __shfl_up_sync(FULL, xr, o);
-        if (lane >= o) { xw += yw; xr += yr; }
+        const uint32_t y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
       }
-      const uint32_t totw = __shfl_sync(FULL, xw, 31), totr = __shfl_sync(FULL, xr, 31);
-      unsigned long long base = 0;
-      if (lane == 0 && totw) base = atomicAdd(&p.ctr->wlog_count, (unsigned long long)totw);
-      if (lane == 1 && totr) base = atomicAdd(&p.ctr->rlog_count, (unsigned long long)totr);
+      const uint32_t tot = __shfl_sync(FULL, x, 31);
       if (lane < W) {
         b_instr += wstat[lane];
         b_loads += wstat[W + lane];
         b_stores += wstat[2 * W + lane];
       }
-      const unsigned long long bw = __shfl_sync(FULL, base, 0), br = __shfl_sync(FULL, base, 1);
-      if (lane < W) {
-        wbase[lane] = bw + xw - cw;
-        wbase[W + lane] = br + xr - cr;
+      unsigned long long pad_from = 0;
+      uint32_t pad_n = 0;
+      if (lane == 0 && tot) {
+        if (c_used + tot > c_cap) {  // pad the rest of the current chunk, take a new one
+          pad_from = c_base + c_used;
+          pad_n = c_cap - c_used;
+          const uint32_t sz = max(STAGE_CHUNK, tot);
+          c_base = atomicAdd(&p.ctr->stage_count, (unsigned long long)sz);
+          c_used = 0;
+          c_cap = sz;
+        }
+        atomicAdd(&p.ctr->staged_recs, (unsigned long long)tot);  // fire-and-forget
+      }
+      const unsigned long long cb = __shfl_sync(FULL, c_base + c_used, 0);
+      if (lane < W) wbase[lane] = cb + x - c;
+      if (lane == 0) {
+        c_used += tot;
+        wbase[W] = pad_from;
+        wcnt[W] = pad_n;
       }
     }
     // lane state out: status / pc into the shared rows (the live register
@@ -620,16 +584,23 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
       }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
-    write_out(lo, S.recs, S.fill, wbase[warp], wbase[W + warp], bhist, lane, &b_over);
+    write_out(lo, S.recs, S.fill, wbase[warp], lane, &b_over);
+    for (uint32_t i = t; i < wcnt[W]; i += T)  // sentinels in the abandoned chunk tail
+      if (wbase[W] + i < p.stage_cap) p.stage[wbase[W] + i] = REC_SENTINEL;
     IPHASE(6);
     __syncthreads();  // staging / overlay / registers reused by the next tile
     IPHASE(7);
   }
 
   if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // lane-state stores complete
-  // ---- block flush: histograms, statistics, flags
-  for (int i = t; i < p.passes * 256; i += T)
-    if (bhist[i]) atomicAdd(&p.hist[i], bhist[i]);
+  // ---- block flush: sentinels in the last chunk's tail, statistics, flags
+  if (t == 0) {
+    wbase[W] = c_base + c_used;
+    wcnt[W] = c_cap - c_used;
+  }
+  __syncthreads();
+  for (uint32_t i = t; i < wcnt[W]; i += T)
+    if (wbase[W] + i < p.stage_cap) p.stage[wbase[W] + i] = REC_SENTINEL;
   if (__any_sync(FULL, b_over) && lane == 0) p.ctr->log_overflow = 1;
   if (warp == 0) {
     b_instr = warp_sum64(b_instr);
@@ -648,9 +619,8 @@ size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem) {
   const int W = T / 32;
   size_t b = (size_t)2 * p.n_regs * T * 4;         // register files (double-buffered)
   b += (size_t)2 * T * 5 + 16;                     // status / pc rows, mbarriers
-  b += (size_t)W * p.stage * 8;                    // staging
+  b += (size_t)W * p.stage_warp * 8;                    // staging
   b += code_in_smem ? (size_t)p.n_instr * 16 : 0;  // pre-decoded program
-  b += (size_t)p.passes * 256 * 4;                 // block digit histograms
   b += (size_t)p.ovl_cap * T * 8;                  // overlay
   b += (size_t)p.n_arrays * 8;                     // array offsets / sizes
   b += ((size_t)p.n_live + 3) & ~size_t(3);        // live register list

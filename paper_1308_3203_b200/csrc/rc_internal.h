@@ -59,9 +59,9 @@ static_assert(RC_OVERLAY_CAP == OVL_CAP, "overlay capacity in rc.h and the inter
 
 // Device counters of one run; zeroed per attempt where noted.
 struct DevCounters {
-  unsigned long long wlog_count;    // write records this interval (per attempt)
-  unsigned long long rlog_count;    // read records this interval (per attempt)
-  unsigned long long kept_count;    // read records kept by the write-set filter
+  unsigned long long stage_count;   // staging slots reserved this interval (records + sentinels; per attempt)
+  unsigned long long staged_recs;   // access records staged this interval (per attempt)
+  unsigned long long kept_count;    // records the write-set filter passed to the sort
   unsigned long long report_count;  // reports appended (whole run, rolled back on retry)
   unsigned long long iv_loads;      // per attempt
   unsigned long long iv_stores;
@@ -97,25 +97,23 @@ struct InterpParams {
   const uint8_t* live;        // registers saved / restored across barriers
   uint32_t n_live;
   uint32_t ovl_cap;           // own-write overlay entries per work-item (static bound)
-  uint32_t stage;             // staged records per warp
+  uint32_t stage_warp;        // records staged per warp in shared memory
   int32_t* node_min;          // [I_b] min / max arrival node (fused A4)
   int32_t* node_max;
-  // log: write records go straight to the sort buffer, read records to a
-  // staging buffer the write-set filter compacts
-  uint64_t* wlog;             // records (make_rec), [0, wlog_count)
-  uint64_t* rlog;             // [0, rlog_count)
-  unsigned long long log_cap; // capacity of each buffer (records); wlog+rlog must fit
+  // log: records are staged in per-block chunks of one staging buffer
+  // (unused chunk tails hold the sentinel ~0); the write-set filter compacts
+  // it into the sort buffer
+  uint64_t* stage;            // [stage_cap] records (make_rec) and sentinels
+  unsigned long long stage_cap;
   uint8_t* wmap;              // [I_b * cpi] 1 = cell written in this interval
   int32_t* wval;              // [ovl_cap][n_lanes] final value of each written overlay slot
-  uint32_t* hist;             // [4][256] digit histograms of the cell bits (fused K2)
-  int passes;                 // 8-bit digit passes of the sort
   rc_report* reports;
   unsigned long long report_cap;
   DevCounters* ctr;
 };
 
 struct DetectParams {
-  const uint64_t* recs;       // sorted by cell; count = ctr->wlog_count + ctr->kept_count
+  const uint64_t* recs;       // sorted by cell; count = ctr->kept_count
   const int32_t* wval;        // [ovl_cap][n_lanes]
   uint32_t n_lanes, n;        // lane = inst_local * n + tid
   uint32_t n_records;         // host upper bound (grid size)
@@ -132,18 +130,20 @@ struct DetectParams {
 size_t interp_smem_bytes(const InterpParams& p, int threads, bool code_in_smem);
 cudaError_t launch_interp(const InterpParams& p, cudaStream_t s);
 
-// Write-set filter: keep the read records whose cell some work-item wrote in
-// this interval (others can produce no report and no commit); append them to
-// the sort buffer after the write records, with their digit histograms.
+// Write-set filter / compaction: from the staging buffer keep every write
+// record and the read records whose cell some work-item wrote in this
+// interval (the others can produce no report and no commit), drop sentinels;
+// write them densely to the sort buffer with their digit histograms (K2).
 struct FilterParams {
-  const uint64_t* rlog;
+  const uint64_t* stage;
   const uint8_t* wmap;
-  uint64_t* out;          // sort buffer; kept reads go to out[wlog_count + i]
+  uint64_t* out;          // sort buffer, [0, kept_count)
   uint32_t* hist;         // [4][256]
   int passes;
   DevCounters* ctr;
-  uint32_t n_reads_ub;    // host upper bound (= rlog_count)
+  uint32_t n_slots;       // staging slots (= stage_count)
 };
+constexpr uint64_t REC_SENTINEL = ~0ull;  // cell 0xFFFFFFFF is never a real cell
 cudaError_t launch_filter(const FilterParams& p, cudaStream_t s);
 
 struct SortWorkspace {

@@ -301,7 +301,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   const int passes = (key_bits + 7) / 8;
   uint64_t log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
   {
-    const uint64_t want = std::max<uint64_t>(1u << 16, std::min<uint64_t>(L_max * 4, 0xFFFFFFFFull));
+    // ~4 records per lane plus the tails of the per-block staging chunks (K1 grid <= 4 blocks per SM)
+    const uint64_t want = std::max<uint64_t>(1u << 16, std::min<uint64_t>(L_max * 4 + 148ull * 4 * 8192, 0xFFFFFFFFull));
     if (log_cap < want) {
       CK(W.log.ensure(want * 8));
       CK(W.log_alt.ensure(want * 8));
@@ -399,7 +400,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       if (cpi) CK(cudaMemsetAsync(W.wmap.p, 0, (size_t)nb * cpi, s));  // write-set map of this interval
       for (;;) {
         CK(cudaMemsetAsync(dctr, 0, offsetof(DevCounters, report_count), s));
-        CK(cudaMemsetAsync(W.sort.hist, 0, 4 * 256 * sizeof(uint32_t), s));  // K1 fuses the digit histograms
+        CK(cudaMemsetAsync(W.sort.hist, 0, 4 * 256 * sizeof(uint32_t), s));  // the filter fuses the histograms
         CK(cudaMemsetAsync(&dctr->iv_loads, 0, offsetof(DevCounters, lanes_final) - offsetof(DevCounters, iv_loads), s));
         ip.code = W.code.as<Ins>();
         ip.n_instr = P->n_instr;
@@ -424,16 +425,13 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         ip.live = W.live.as<uint8_t>();
         ip.n_live = (uint32_t)P->live_regs.size();
         ip.ovl_cap = (uint32_t)P->ovl_cap;
-        ip.stage = P->rec_bound > 0 ? (uint32_t)std::min(256, ((32 * P->rec_bound + 31) / 32) * 32) : 256u;
+        ip.stage_warp = P->rec_bound > 0 ? (uint32_t)std::min(256, ((32 * P->rec_bound + 31) / 32) * 32) : 256u;
         ip.node_min = node_min;
         ip.node_max = node_max;
-        ip.wlog = W.log.as<uint64_t>();
-        ip.rlog = W.log_alt.as<uint64_t>();
-        ip.log_cap = log_cap;
+        ip.stage = W.log_alt.as<uint64_t>();
+        ip.stage_cap = log_cap;
         ip.wmap = W.wmap.as<uint8_t>();
         ip.wval = W.wval.as<int32_t>();
-        ip.hist = W.sort.hist;
-        ip.passes = passes;
         ip.reports = W.reports.as<rc_report>();
         ip.report_cap = rep_cap;
         ip.ctr = dctr;
@@ -446,7 +444,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
                       "a work-item wrote more than %d distinct cells in one barrier interval (instance batch at "
                       "%u, interval %u)",
                       P->ovl_cap, inst_base, k);
-        const uint64_t n_all = W.h_ctr->wlog_count + W.h_ctr->rlog_count;  // the sort buffer must hold both
+        const uint64_t n_all = W.h_ctr->stage_count;  // staging slots; the sort buffer holds at most as many
         const bool log_over = W.h_ctr->log_overflow || n_all > log_cap;
         const bool rep_over = W.h_ctr->report_count > rep_cap;
         if (!log_over && !rep_over) break;
@@ -461,8 +459,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         if (rep_over) CK(grow_reports(W.h_ctr->report_count));
         CK(set_report_count(rep_before));
       }
-      const uint64_t Nw = W.h_ctr->wlog_count, Nr = W.h_ctr->rlog_count;
-      const uint64_t N = Nw + Nr;  // upper bound of the sorted records (exact count on the device)
+      const uint64_t Nr = W.h_ctr->stage_count;  // staging slots (records + sentinels)
+      const uint64_t N = Nr;  // upper bound of the sorted records (exact count on the device)
       rep_count = W.h_ctr->report_count;
       tot_loads += W.h_ctr->iv_loads;
       tot_stores += W.h_ctr->iv_stores;
@@ -472,13 +470,13 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       const size_t mark0 = W.prof.marks.size();
       {
         FilterParams fp;
-        fp.rlog = W.log_alt.as<uint64_t>();
+        fp.stage = W.log_alt.as<uint64_t>();
         fp.wmap = W.wmap.as<uint8_t>();
         fp.out = W.log.as<uint64_t>();
         fp.hist = W.sort.hist;
         fp.passes = passes;
         fp.ctr = dctr;
-        fp.n_reads_ub = (uint32_t)Nr;
+        fp.n_slots = (uint32_t)Nr;
         W.prof.begin(s);
         CK(launch_filter(fp, s));
         W.prof.end(RC_PROF_FILTER, s, Nr * 9, Nr);
@@ -486,7 +484,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       // ---------------- K3: onesweep sort of the kept records by cell
       bool in_alt = false;
       W.sort.alt = W.log_alt.as<uint64_t>();
-      CK(onesweep_sort(W.log.as<uint64_t>(), (uint32_t)N, &dctr->wlog_count, &dctr->kept_count, key_bits, W.sort, s,
+      CK(onesweep_sort(W.log.as<uint64_t>(), (uint32_t)N, &dctr->kept_count, nullptr, key_bits, W.sort, s,
                        &in_alt, W.prof.on ? &W.prof : nullptr, /*hist_ready=*/true));
       const uint64_t* sr = in_alt ? W.log_alt.as<uint64_t>() : W.log.as<uint64_t>();
 
@@ -536,7 +534,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         W.h_ctr->report_count = 0;  // force a fresh read after the re-run
       }
       if (W.prof.on) {  // exact sorted-record count is known now: fix this interval's profile bytes
-        const uint64_t Ns = W.h_ctr->wlog_count + W.h_ctr->kept_count;
+        const uint64_t Ns = W.h_ctr->kept_count;
         for (size_t i = mark0; i < W.prof.marks.size(); i++) {
           Profiler::Mark& m = W.prof.marks[i];
           if (m.cls == RC_PROF_SORT) { m.bytes = Ns * 16; m.items = Ns; }
