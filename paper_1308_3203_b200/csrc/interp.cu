@@ -222,12 +222,15 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
 
   // ---- shared memory carve-up (sizes mirrored in interp_smem_bytes)
   unsigned char* q = smem;
-  int32_t* sregs_b[2];   // register files [reg][thread], double-buffered (TMA)
-  uint8_t* sstat_b[2];
-  uint32_t* spc_b[2];
-  for (int b = 0; b < 2; b++) { sregs_b[b] = reinterpret_cast<int32_t*>(q); q += (size_t)R * T * 4; }
-  for (int b = 0; b < 2; b++) { spc_b[b] = reinterpret_cast<uint32_t*>(q); q += (size_t)T * 4; }
-  for (int b = 0; b < 2; b++) { sstat_b[b] = reinterpret_cast<uint8_t*>(q); q += (size_t)T; }
+  // register files [reg][thread], status and pc rows, double-buffered (TMA);
+  // buffer b is addressed arithmetically from these bases (a runtime-indexed
+  // array of pointers would lose the shared address space)
+  int32_t* const sregs0 = reinterpret_cast<int32_t*>(q); q += (size_t)2 * R * T * 4;
+  uint32_t* const spc0 = reinterpret_cast<uint32_t*>(q); q += (size_t)2 * T * 4;
+  uint8_t* const sstat0 = reinterpret_cast<uint8_t*>(q); q += (size_t)2 * T;
+#define SREGS(b) (sregs0 + (size_t)(b) * R * T)
+#define SPC(b) (spc0 + (size_t)(b) * T)
+#define SSTAT(b) (sstat0 + (size_t)(b) * T)
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(q); q += 16;
   uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)W * p.stage_warp * 8;
   uint4* s_code = reinterpret_cast<uint4*>(q); q += CODE_SMEM ? (size_t)p.n_instr * 16 : 0;
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
   }
   __syncthreads();
   if (t == 0 && blockIdx.x < n_tiles0)
-    prefetch_lanes(p, blockIdx.x, T, sstat_b[0], spc_b[0], sregs_b[0], s_live, &mbar[0]);
+    prefetch_lanes(p, blockIdx.x, T, SSTAT(0), SPC(0), SREGS(0), s_live, &mbar[0]);
 
   // block totals: lane l of warp 0 accumulates the statistics of warp l
   unsigned long long b_instr = 0, b_loads = 0, b_stores = 0;
@@ -277,15 +280,15 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
     // stores of its previous use have finished reading it
     if (t == 0 && tile + gridDim.x < n_tiles) {
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      prefetch_lanes(p, tile + gridDim.x, T, sstat_b[cur ^ 1], spc_b[cur ^ 1], sregs_b[cur ^ 1], s_live,
+      prefetch_lanes(p, tile + gridDim.x, T, SSTAT(cur ^ 1), SPC(cur ^ 1), SREGS(cur ^ 1), s_live,
                      &mbar[cur ^ 1]);
     }
     IPHASE(0);
     mbar_wait_parity(&mbar[cur], (parity >> cur) & 1u);
     parity ^= 1u << cur;
     IPHASE(1);
-    uint8_t* const sstat = sstat_b[cur];
-    uint32_t* const spc = spc_b[cur];
+    uint8_t* const sstat = SSTAT(cur);
+    uint32_t* const spc = SPC(cur);
     const uint32_t g = tile * (uint32_t)T + t;
     const bool valid = g < p.n_lanes;
     uint8_t status = valid ? sstat[t] : (uint8_t)L_EXITED;
@@ -295,7 +298,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
     const uint32_t inst = valid ? g / p.n : 0;
     const uint32_t tid = valid ? g - inst * p.n : 0;
     const uint32_t cell_base = inst * p.cpi;
-    int32_t* Rg = sregs_b[cur] + t;  // register r of this lane = Rg[r*T] (live ones arrived by TMA)
+    int32_t* Rg = SREGS(cur) + t;  // register r of this lane = Rg[r*T] (live ones arrived by TMA)
 
     if (running) status = L_RUNNING;
     // non-blocking loads: up to NP issued LDs whose destination register is
@@ -580,7 +583,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
       bulk_s2g(p.pc_out + g0, spc, (uint32_t)T * 4);
       for (uint32_t i = 0; i < p.n_live; i++) {
         const uint32_t r = s_live[i];
-        bulk_s2g(p.regs_out + (size_t)r * p.reg_stride + g0, sregs_b[cur] + (size_t)r * T, (uint32_t)T * 4);
+        bulk_s2g(p.regs_out + (size_t)r * p.reg_stride + g0, SREGS(cur) + (size_t)r * T, (uint32_t)T * 4);
       }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
