@@ -155,6 +155,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--instances", type=int, default=0, help="override instances per GPU (debug)")
+    ap.add_argument("--keep-all-reads", action="store_true",
+                    help="RC_OPT_KEEP_ALL_READS: sort every read record (no write-set pruning)")
     args = ap.parse_args()
     wl = dict(WORKLOADS[args.workload])
     if args.instances:
@@ -187,7 +189,7 @@ def main():
 
     def step(profile=False, arrs=arrays):
         r = rc_run(prog, n, arrs, instance_offset=lo, want_final=False, profile=profile, device=local,
-                   stream=stream)
+                   stream=stream, keep_all_reads=args.keep_all_reads)
         if world > 1:
             reps, st = gather_reports(r.reports, r.stats, device=dev)
         else:
@@ -286,7 +288,7 @@ def main():
                     "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak if achieved else None,
                     "traffic": traffic, "alg_bytes_per_launch": s["alg_bytes"] / max(1, s["launches"]),
-                    "alg_bytes_per_record": 24, "launches": s["launches"] // args.steps,
+                    "alg_bytes_per_record": 16, "launches": s["launches"] // args.steps,
                     "peak_source": peak_src}
         kernels = {}
         for c in ("interp", "filter", "hist", "sort", "detect", "boundary", "finalize", "copy"):
@@ -310,6 +312,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": wl["name"], "work_items": n, "instances_per_gpu": hi - lo,
+                       "write_set_filter": not args.keep_all_reads,
                        "instances_total": total_inst, "parallelism": f"dp{world} (instance shards)",
                        "l2": "inputs 4.3 GB/GPU >> 126 MB L2 (no flush needed)",
                        "checked_accesses_per_step": accesses // args.steps, "reports_per_step": n_reports},

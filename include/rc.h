@@ -173,6 +173,10 @@ typedef struct {
 
 #define RC_OPT_HOST_IO 1u /* arrays[].data and final_heaps[] are HOST pointers;
                              rc_run does the host<->device copies itself     */
+#define RC_OPT_KEEP_ALL_READS 2u /* sort every read record, also those of cells no
+                             work-item wrote in the interval (which can produce
+                             no report or commit; by default they are dropped
+                             before the sort) — same results     */
 
 typedef struct {
   uint32_t instance_offset;    /* added to report.instance (multi-GPU shards) */

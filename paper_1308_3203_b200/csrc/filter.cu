@@ -45,7 +45,8 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
 #pragma unroll
     for (int j = 0; j < F_ITEMS; j++) {
       const uint64_t i = b0 + (uint64_t)j * F_THREADS + t;
-      keep[j] = rec[j] != REC_SENTINEL && ((rec[j] & 1) || __ldg(p.wmap + (rec[j] >> REC_CELL_SHIFT)) != 0);
+      keep[j] = rec[j] != REC_SENTINEL &&
+                (p.keep_all || (rec[j] & 1) || __ldg(p.wmap + (rec[j] >> REC_CELL_SHIFT)) != 0);
     }
     uint32_t mine = 0;
 #pragma unroll

@@ -315,9 +315,10 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
     bool ovl_over = false;
     Stage S{st_recs + (size_t)warp * p.stage_warp, 0, p.stage_warp};
 
+    uint32_t npend = 0;  // occupied pending-load slots of this lane
     for (;;) {
-      if (__ballot_sync(FULL, running) == 0) break;
       const uint32_t minpc = __reduce_min_sync(FULL, running ? pc : 0xFFFFFFFFu);
+      if (minpc == 0xFFFFFFFFu) break;  // no lane of the warp is running (pcs are < 65536)
       bool ex = running && pc == minpc;
       const uint4 e = CODE_SMEM ? s_code[minpc]
                                 : predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + minpc), T, s_off, s_size);
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
       int32_t* const Rb = Rg + (e.y & 0xFFFF);
       int32_t* const Rc = Rg + (e.y >> 16);
       const int32_t imm = (int32_t)e.z;
-      if (__any_sync(FULL, ex && (pr[0] != NOREG || pr[1] != NOREG || pr[2] != NOREG || pr[3] != NOREG))) {
+      if (__any_sync(FULL, ex && npend)) {
         // an instruction touching a pending register materialises it first
         const uint32_t oa = e.x >> 16, ob = e.y & 0xFFFF, oc = e.y >> 16;
 #pragma unroll
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
           if (ex && pr[j] != NOREG && (pr[j] == oa || pr[j] == ob || pr[j] == oc)) {
             Rg[pr[j]] = pv[j];
             pr[j] = NOREG;
+            npend--;
           }
       }
       if (ex) {  // fuel check before executing (reading L17)
@@ -409,9 +411,10 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
               if (found) {
                 *Ra = v;
               } else {  // issue the load; write the register back later
-                if (pr[0] != NOREG && pr[1] != NOREG && pr[2] != NOREG && pr[3] != NOREG) {  // all busy: retire
+                if (npend == NP) {  // all busy: retire
 #pragma unroll
                   for (int j = 0; j < NP; j++) { Rg[pr[j]] = pv[j]; pr[j] = NOREG; }
+                  npend = 0;
                 }
                 const int32_t lv = __ldg(p.heap + cell);
                 const uint32_t oa = e.x >> 16;
@@ -420,6 +423,7 @@ __global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
                 else if (pr[1] == NOREG) { pv[1] = lv; pr[1] = oa; }
                 else if (pr[2] == NOREG) { pv[2] = lv; pr[2] = oa; }
                 else { pv[3] = lv; pr[3] = oa; }
+                npend++;
               }
               pc++;
               nloads++;

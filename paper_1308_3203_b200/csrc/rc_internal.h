@@ -142,6 +142,7 @@ struct FilterParams {
   int passes;
   DevCounters* ctr;
   uint32_t n_slots;       // staging slots (= stage_count)
+  bool keep_all;          // RC_OPT_KEEP_ALL_READS: only drop the sentinels
 };
 constexpr uint64_t REC_SENTINEL = ~0ull;  // cell 0xFFFFFFFF is never a real cell
 cudaError_t launch_filter(const FilterParams& p, cudaStream_t s);

@@ -477,6 +477,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         fp.passes = passes;
         fp.ctr = dctr;
         fp.n_slots = (uint32_t)Nr;
+        fp.keep_all = (opt.flags & RC_OPT_KEEP_ALL_READS) != 0;
         W.prof.begin(s);
         CK(launch_filter(fp, s));
         W.prof.end(RC_PROF_FILTER, s, Nr * 9, Nr);

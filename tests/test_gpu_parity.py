@@ -306,3 +306,27 @@ def test_deterministic_repeats(rc):
     assert a.reports.tobytes() == b.reports.tobytes()
     for x, y in zip(a.final, b.final):
         assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("src,n,gen", [
+    (K.FIG1, 8, lambda: I.cfg1_inputs()),
+    (K.TREE_OFF_BY_ONE, 256, lambda: I.cfg3_inputs(0, 16, 256)),
+    (K.BENIGN["K_inc"], 64, lambda: I.cfg2_inputs(0, 8, 64)),
+    (K.STENCIL, 500, lambda: I.cfg5_inputs(0, 3, 500)),
+])
+def test_keep_all_reads_same_results(rc, src, n, gen):
+    """RC_OPT_KEEP_ALL_READS (no write-set pruning before the sort) gives the
+    same reports, heaps and counters as the default path and the oracle."""
+    ins = gen()
+    p, g, o = run_both(rc, src, n, ins, keep_all_reads=True)
+    assert_parity(g, o, ins)
+
+
+def test_random_tiny_kernels_keep_all_reads(rc):
+    rng = np.random.default_rng(7)
+    for it in range(100):
+        n = int(rng.integers(1, 70))
+        pr = K.random_tiny_kernel(rng, n_arrays=2, n_regs=5, n_commands=int(rng.integers(3, 12)), size=5)
+        ins = [rng.integers(-3, 4, size=(2, 5)).astype(np.int32) for _ in range(2)]
+        p, g, o = run_both(rc, pr, n, ins, fuel=500, keep_all_reads=True)
+        assert_parity(g, o, ins)
