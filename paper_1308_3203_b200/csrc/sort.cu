@@ -19,6 +19,13 @@
 // Status words carry an epoch so the look-back array is never re-zeroed.
 #include "rc_internal.h"
 
+#ifndef SORT_LB
+#define SORT_LB 16
+#endif
+#ifndef SORT_EXP
+#define SORT_EXP 0
+#endif
+
 namespace rc {
 
 namespace {
@@ -275,14 +282,21 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? 2 : 3) onesweep_ker
 #pragma unroll
       for (int j = 0; j < SORT_ITEMS; j++) {
         const uint32_t dd = DIGIT(j);
+#if SORT_EXP == 2  // timing experiment only: no matching (wrong ranks)
+        pm[j] = 1u << lane;
+        (void)vm;
+#else
         pm[j] = match_digit(dd, vm ? vm : __ballot_sync(FULL, dd < RADIX));
+#endif
       }
     }
     // early tile counts: one shared atomic per digit group, then publish AGGREGATE
 #pragma unroll
     for (int j = 0; j < SORT_ITEMS; j++) {
       const uint32_t dd = DIGIT(j);
+#if SORT_EXP != 1  // timing experiment 1: no early counts
       if (dd < RADIX && lane == __ffs(pm[j]) - 1) atomicAdd(&S.thist[w & 1][dd], (uint32_t)__popc(pm[j]));
+#endif
     }
     __syncthreads();
     const int d = t;  // SORT_THREADS == RADIX
@@ -332,7 +346,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? 2 : 3) onesweep_ker
     //      INCLUSIVE), then publish our INCLUSIVE prefix
     unsigned long long excl = 0;
     if (tile > 0) {
-      constexpr int LB = 16;  // predecessors per L2 round trip
+      constexpr int LB = SORT_LB;  // predecessors per L2 round trip
       int64_t tp = (int64_t)tile - 1;
       bool done = false;
       while (!done) {
