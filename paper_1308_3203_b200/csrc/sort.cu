@@ -286,7 +286,18 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? 2 : 3) onesweep_ker
         pm[j] = 1u << lane;
         (void)vm;
 #else
-        pm[j] = match_digit(dd, vm ? vm : __ballot_sync(FULL, dd < RADIX));
+        // exact fast paths for the structured runs of access logs: a round
+        // whose 32 digits are all equal, or strictly increasing by lane
+        const unsigned valid = vm ? vm : __ballot_sync(FULL, dd < RADIX);
+        const uint32_t d0 = __shfl_sync(FULL, dd, 0);
+        const uint32_t dprev = __shfl_up_sync(FULL, dd, 1);
+        if (__all_sync(FULL, dd == d0)) {
+          pm[j] = dd < RADIX ? valid : 0u;
+        } else if (__all_sync(FULL, lane == 0 || dd > dprev)) {
+          pm[j] = 1u << lane;  // all distinct (invalid lanes carry 0x100, the largest)
+        } else {
+          pm[j] = match_digit(dd, valid);
+        }
 #endif
       }
     }
