@@ -73,13 +73,13 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* warp_t
 }  // namespace
 
 #ifdef SORT_PHASE_TIMING
-__device__ unsigned long long g_phase_cycles[8];
+__device__ unsigned long long g_phase_cycles[12];
 void sort_phase_io(unsigned long long* out, bool reset) {
   if (reset) {
-    unsigned long long z[8] = {0};
+    unsigned long long z[12] = {0};
     cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
   } else {
-    cudaMemcpyFromSymbol(out, g_phase_cycles, 8 * sizeof(unsigned long long));
+    cudaMemcpyFromSymbol(out, g_phase_cycles, 12 * sizeof(unsigned long long));
   }
 }
 #define PHASE_T(i)                                       \
@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? 2 : 3) onesweep_ker
       k[j] = idx < cnt ? B[idx] : ~0ull;  // invalid items: digit 0x100 below
     }
 #define DIGIT(j) ((w * WARP_ITEMS + (j) * 32 + lane) < cnt ? (uint32_t)(k[j] >> dsh) & 0xFF : 0x100u)
+    PHASE_T(2);
     {
       const unsigned vm = cnt >= (uint32_t)(w * WARP_ITEMS + WARP_ITEMS) ? FULL : 0u;
 #pragma unroll
@@ -301,6 +302,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? 2 : 3) onesweep_ker
 #endif
       }
     }
+    PHASE_T(3);
     // early tile counts: one shared atomic per digit group, then publish AGGREGATE
 #pragma unroll
     for (int j = 0; j < SORT_ITEMS; j++) {
@@ -315,7 +317,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? 2 : 3) onesweep_ker
     unsigned long long* my_status = status + (size_t)tile * RADIX + d;
     if (tile == 0) st_relaxed(my_status, FLAG_INC | ep | tile_cnt);
     else st_relaxed(my_status, FLAG_AGG | ep | tile_cnt);
-    PHASE_T(2);
+    PHASE_T(4);
 
     // ---- stable in-tile ranking (warp w owns items [w*512, w*512+512), striped)
 #pragma unroll
@@ -342,7 +344,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? 2 : 3) onesweep_ker
     const uint32_t excl_tile = block_excl_scan(tile_cnt, S.wt);
     S.tile_excl[d] = excl_tile;
     __syncthreads();
-    PHASE_T(3);
+    PHASE_T(5);
 
     // ---- scatter into shared memory in digit order (stable), in place
 #pragma unroll
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? 2 : 3) onesweep_ker
       if (dd < RADIX) B[S.tile_excl[dd] + S.whist[w][dd] + pm[j]] = k[j];
     }
 #undef DIGIT
-    PHASE_T(4);
+    PHASE_T(6);
 
     // ---- look-back (after the scatter: predecessors had time to publish
     //      INCLUSIVE), then publish our INCLUSIVE prefix
@@ -378,7 +380,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? 2 : 3) onesweep_ker
     }
     S.glob_base[d] = (uint32_t)(bin_off[d] + excl) - excl_tile;
     __syncthreads();
-    PHASE_T(5);
+    PHASE_T(7);
 
     // ---- coalesced write-out: sorted position i goes to glob_base[digit] + i
     if (cnt == SORT_TILE) {
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? 2 : 3) onesweep_ker
       }
     }
     __syncthreads();  // buffer `cur`, whist, glob_base free for reuse
-    PHASE_T(6);
+    PHASE_T(8);
     if (!PERSISTENT) break;
     cur ^= 1;
   }

@@ -97,13 +97,14 @@ int main(int argc, char** argv) {
   printf("n=%u bits=%d pattern=%s passes=%d: median %.3f ms  -> %.1f GB/s sort-alg (16 B/rec/pass + 8 B hist)\n",
          n, bits, pat.c_str(), passes, med, (double)n * (16.0 * passes + 8) / (med * 1e-3) / 1e9);
 #ifdef SORT_PHASE_TIMING
-  unsigned long long ph[8];
+  unsigned long long ph[12];
   rc::sort_phase_io(ph, false);
   const double tiles = (double)rc::sort_tiles(n) * passes;
-  const char* names[] = {"claim+prefetch", "tma wait", "match+count", "rank", "scatter", "lookback", "writeout", ""};
+  const char* names[] = {"claim+prefetch", "tma wait", "load keys", "match", "count+publish", "rank", "scatter",
+                         "lookback", "writeout", "", "", ""};
   double tot = 0;
-  for (int i = 0; i < 7; i++) tot += ph[i];
-  for (int i = 0; i < 7; i++)
+  for (int i = 0; i < 9; i++) tot += ph[i];
+  for (int i = 0; i < 9; i++)
     printf("  phase %-16s %9.0f cycles/tile (%.1f%%)\n", names[i], ph[i] / tiles, 100.0 * ph[i] / tot);
 #endif
   // verify: sorted by cell bits, a permutation, stable (low word = source index)
