@@ -37,6 +37,10 @@
 // global "some lane is suspended" flag.
 #include "rc_internal.h"
 
+#ifndef INTERP_MIN_BLOCKS
+#define INTERP_MIN_BLOCKS 3
+#endif
+
 namespace rc {
 
 namespace {
@@ -211,7 +215,7 @@ void interp_phase_io(unsigned long long* out, bool reset) {
 #endif
 
 template <bool CODE_SMEM>
-__global__ void __launch_bounds__(256, 3) interp_kernel(const InterpParams p) {
+__global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const InterpParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int T = blockDim.x;
   const int W = T >> 5;
