@@ -195,13 +195,10 @@ __device__ __forceinline__ Seg seg_shfl(const Seg& a, int src) {
 // round; one that crosses the chunk end, and every COMPLEX cell, is handled by
 // serial_segment from the segment's head.  Segments that start before the
 // chunk belong to the previous warp.
-__global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
+__device__ __forceinline__ void detect_chunk(const DetectParams& p, uint64_t wg, uint32_t n_records) {
   const unsigned FULL = 0xFFFFFFFFu;
   const int lane = threadIdx.x & 31;
-  const uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t n_records = (uint32_t)p.ctr->kept_count;
   const uint64_t c0 = wg * DET_CHUNK;
-  if (c0 >= n_records) return;  // whole warp
   const uint64_t c1 = min((uint64_t)n_records, c0 + DET_CHUNK);
   // ---- prefetch the chunk
   uint64_t vr[DET_ROUNDS];
@@ -293,10 +290,29 @@ __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
   if (carry && lane == 0) serial_segment(p, (uint32_t)carry_start, n_records);  // continues into the next chunk
 }
 
+// Persistent: warps stride over the chunks; the record count is read from
+// device memory (no host sync).  Skips everything (no commit) when this
+// interval's log overflowed or K1's reports overflowed: the host then re-runs
+// the interval from the saved lane state on an untouched heap.
+__global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
+  if (p.ctr->log_overflow || p.ctr->k1_reports > p.report_cap) return;
+  const uint32_t n_records = (uint32_t)p.ctr->kept_count;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wg * DET_CHUNK < n_records; wg += warps)
+    detect_chunk(p, wg, n_records);
+}
+
 cudaError_t launch_detect(const DetectParams& p, cudaStream_t s) {
   if (p.n_records == 0) return cudaSuccess;
-  const uint64_t warps = (p.n_records + DET_CHUNK - 1) / DET_CHUNK;
-  detect_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(p);
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const uint64_t warps = (p.n_records + DET_CHUNK - 1) / DET_CHUNK;  // upper bound
+  const unsigned grid = (unsigned)std::min<uint64_t>((warps + 7) / 8, (uint64_t)nsm * 8);
+  detect_kernel<<<grid, 256, 0, s>>>(p);
   launched();
   return cudaGetLastError();
 }

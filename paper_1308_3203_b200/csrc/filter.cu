@@ -31,6 +31,8 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
   __shared__ unsigned long long sbase;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   for (int i = t; i < p.passes * 256; i += F_THREADS) bh[i] = 0;
+  if (blockIdx.x == 0 && t == 0) p.ctr->k1_reports = p.ctr->report_count;  // K1 is complete here
+  if (p.ctr->log_overflow) return;  // the interval will be re-run
   const uint64_t nr = p.ctr->stage_count;
   const uint64_t step = (uint64_t)gridDim.x * F_THREADS * F_ITEMS;
   __syncthreads();

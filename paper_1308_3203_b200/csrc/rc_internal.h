@@ -70,6 +70,7 @@ struct DevCounters {
   unsigned int ovl_overflow;        // per attempt
   unsigned int any_waiting;         // per interval
   unsigned int diverged;            // per interval
+  unsigned long long k1_reports;    // report_count after K1 (snapshot taken by the filter)
   unsigned long long lanes_final[8];
 };
 

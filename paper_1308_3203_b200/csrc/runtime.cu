@@ -299,10 +299,14 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     CK(W.wmap.ensure(std::max<uint64_t>(1, (uint64_t)I_b * cpi)));
   }
   const int passes = (key_bits + 7) / 8;
+  // test hook: start from tiny log / report buffers so the grow-and-retry
+  // paths run (results must not change)
+  const bool small_buffers = getenv("RC_DEBUG_SMALL_BUFFERS") != nullptr;
   uint64_t log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
   {
     // ~4 records per lane plus the tails of the per-block staging chunks (K1 grid <= 4 blocks per SM)
-    const uint64_t want = std::max<uint64_t>(1u << 16, std::min<uint64_t>(L_max * 4 + 148ull * 4 * 8192, 0xFFFFFFFFull));
+    uint64_t want = std::max<uint64_t>(1u << 16, std::min<uint64_t>(L_max * 4 + 148ull * 4 * 8192, 0xFFFFFFFFull));
+    if (small_buffers) want = 1024;
     if (log_cap < want) {
       CK(W.log.ensure(want * 8));
       CK(W.log_alt.ensure(want * 8));
@@ -324,8 +328,11 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   };
   CK(ensure_sort_status(log_cap));
   uint64_t rep_cap = W.reports.bytes / sizeof(rc_report);
-  if (rep_cap < (1u << 16)) {
+  if (rep_cap < (1u << 16) && !small_buffers) {
     CK(W.reports.ensure((1u << 16) * sizeof(rc_report)));
+    rep_cap = W.reports.bytes / sizeof(rc_report);
+  } else if (small_buffers && rep_cap == 0) {
+    CK(W.reports.ensure(4 * sizeof(rc_report)));
     rep_cap = W.reports.bytes / sizeof(rc_report);
   }
 
@@ -394,10 +401,35 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     }
     uint32_t k = 0;
     for (;;) {
-      // ---------------- K1
-      uint64_t rep_before = rep_count;
+      // One host sync per interval: K1 → filter → sort → detect → A4 are
+      // queued back to back (every kernel after K1 reads its record count from
+      // device memory).  Overflows are detected at the sync: a log or K1-report
+      // overflow makes filter/detect skip their work (the heap stays
+      // untouched) and the interval is re-run from the saved lane state; a
+      // detect-report overflow re-runs detect only (its commits are idempotent).
+      const uint64_t rep_before = rep_count;
       InterpParams ip;
+      size_t mark0 = 0;
+      const uint64_t* sr = nullptr;
       if (cpi) CK(cudaMemsetAsync(W.wmap.p, 0, (size_t)nb * cpi, s));  // write-set map of this interval
+      auto detect_params = [&]() {
+        DetectParams dp;
+        dp.recs = sr;
+        dp.wval = W.wval.as<int32_t>();
+        dp.n_lanes = L;
+        dp.n = n;
+        dp.n_records = (uint32_t)log_cap;  // upper bound; the kernel reads the exact count
+        dp.heap = W.heap.as<int32_t>();
+        dp.cpi = (uint32_t)std::max<uint64_t>(cpi, 1);
+        dp.n_arrays = n_arrays;
+        dp.arr_off = W.arr_off.as<uint32_t>();
+        dp.interval = k;
+        dp.inst_base = inst_base;
+        dp.reports = W.reports.as<rc_report>();
+        dp.report_cap = rep_cap;
+        dp.ctr = dctr;
+        return dp;
+      };
       for (;;) {
         CK(cudaMemsetAsync(dctr, 0, offsetof(DevCounters, report_count), s));
         CK(cudaMemsetAsync(W.sort.hist, 0, 4 * 256 * sizeof(uint32_t), s));  // the filter fuses the histograms
@@ -435,40 +467,11 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         ip.reports = W.reports.as<rc_report>();
         ip.report_cap = rep_cap;
         ip.ctr = dctr;
+        mark0 = W.prof.marks.size();
         W.prof.begin(s);
         CK(launch_interp(ip, s));
         W.prof.end(RC_PROF_INTERP, s, 0, L);
-        CK(read_ctr());
-        if (W.h_ctr->ovl_overflow)
-          return fail(RC_ELIMIT,
-                      "a work-item wrote more than %d distinct cells in one barrier interval (instance batch at "
-                      "%u, interval %u)",
-                      P->ovl_cap, inst_base, k);
-        const uint64_t n_all = W.h_ctr->stage_count;  // staging slots; the sort buffer holds at most as many
-        const bool log_over = W.h_ctr->log_overflow || n_all > log_cap;
-        const bool rep_over = W.h_ctr->report_count > rep_cap;
-        if (!log_over && !rep_over) break;
-        if (log_over) {  // grow the log and re-run the interval from the saved lane state
-          const uint64_t want = std::min<uint64_t>(n_all + n_all / 4 + 1024, 0xFFFFFFFFull);
-          if (n_all > 0xFFFFFFFFull) return fail(RC_ELIMIT, "more than 2^32 access records in one interval");
-          CK(W.log.ensure(want * 8));
-          CK(W.log_alt.ensure(want * 8));
-          log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
-          CK(ensure_sort_status(log_cap));
-        }
-        if (rep_over) CK(grow_reports(W.h_ctr->report_count));
-        CK(set_report_count(rep_before));
-      }
-      const uint64_t Nr = W.h_ctr->stage_count;  // staging slots (records + sentinels)
-      const uint64_t N = Nr;  // upper bound of the sorted records (exact count on the device)
-      rep_count = W.h_ctr->report_count;
-      tot_loads += W.h_ctr->iv_loads;
-      tot_stores += W.h_ctr->iv_stores;
-      tot_instr += W.h_ctr->iv_instr;
-
-      // ---------------- write-set filter: reads of written cells join the write records
-      const size_t mark0 = W.prof.marks.size();
-      {
+        // ---- write-set filter: writes + reads of written cells, dense, with histograms
         FilterParams fp;
         fp.stage = W.log_alt.as<uint64_t>();
         fp.wmap = W.wmap.as<uint8_t>();
@@ -476,71 +479,86 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         fp.hist = W.sort.hist;
         fp.passes = passes;
         fp.ctr = dctr;
-        fp.n_slots = (uint32_t)Nr;
+        fp.n_slots = (uint32_t)log_cap;  // upper bound; the kernel reads stage_count
         fp.keep_all = (opt.flags & RC_OPT_KEEP_ALL_READS) != 0;
         W.prof.begin(s);
         CK(launch_filter(fp, s));
-        W.prof.end(RC_PROF_FILTER, s, Nr * 9, Nr);
-      }
-      // ---------------- K3: onesweep sort of the kept records by cell
-      bool in_alt = false;
-      W.sort.alt = W.log_alt.as<uint64_t>();
-      CK(onesweep_sort(W.log.as<uint64_t>(), (uint32_t)N, &dctr->kept_count, nullptr, key_bits, W.sort, s,
-                       &in_alt, W.prof.on ? &W.prof : nullptr, /*hist_ready=*/true));
-      const uint64_t* sr = in_alt ? W.log_alt.as<uint64_t>() : W.log.as<uint64_t>();
-
-      // ---------------- K4+K5 and A4 (idempotent: re-run if the report buffer overflows)
-      const uint64_t rep_after_k1 = rep_count;
-      bool checked = false, diverged = false;
-      for (;;) {
-        DetectParams dp;
-        dp.recs = sr;
-        dp.wval = W.wval.as<int32_t>();
-        dp.n_lanes = L;
-        dp.n = n;
-        dp.n_records = (uint32_t)N;  // upper bound; the kernel reads the exact count
-        dp.heap = W.heap.as<int32_t>();
-        dp.cpi = (uint32_t)std::max<uint64_t>(cpi, 1);
-        dp.n_arrays = n_arrays;
-        dp.arr_off = W.arr_off.as<uint32_t>();
-        dp.interval = k;
-        dp.inst_base = inst_base;
-        dp.reports = W.reports.as<rc_report>();
-        dp.report_cap = rep_cap;
-        dp.ctr = dctr;
+        W.prof.end(RC_PROF_FILTER, s, 0, 0);
+        // ---- K3: onesweep sort of the kept records by cell
+        bool in_alt = false;
+        W.sort.alt = W.log_alt.as<uint64_t>();
+        CK(onesweep_sort(W.log.as<uint64_t>(), (uint32_t)log_cap, &dctr->kept_count, nullptr, key_bits, W.sort, s,
+                         &in_alt, W.prof.on ? &W.prof : nullptr, /*hist_ready=*/true));
+        sr = in_alt ? W.log_alt.as<uint64_t>() : W.log.as<uint64_t>();
+        // ---- K4+K5 detect + commit, A4 check
+        DetectParams dp = detect_params();
         W.prof.begin(s);
         CK(launch_detect(dp, s));
-        W.prof.end(RC_PROF_DETECT, s, N * 8, N);
+        W.prof.end(RC_PROF_DETECT, s, 0, 0);
         BoundaryParams bp = bparams(k);
         bp.status = W.status[cur ^ 1].as<uint8_t>();
         bp.pc = W.pc[cur ^ 1].as<uint32_t>();
-        if (!checked) {  // consumes (and resets) K1's per-instance node ranges: once per interval
-          W.prof.begin(s);
-          CK(launch_boundary(bp, s));
-          W.prof.end(RC_PROF_BOUNDARY, s, (uint64_t)nb * 12, nb);
-          CK(read_ctr());
-          checked = true;
-          diverged = W.h_ctr->diverged != 0;
+        W.prof.begin(s);
+        CK(launch_boundary(bp, s));  // consumes (and resets) K1's per-instance node ranges
+        W.prof.end(RC_PROF_BOUNDARY, s, (uint64_t)nb * 12, nb);
+        CK(read_ctr());  // the interval's only sync
+        if (W.h_ctr->ovl_overflow)
+          return fail(RC_ELIMIT,
+                      "a work-item wrote more than %d distinct cells in one barrier interval (instance batch at "
+                      "%u, interval %u)",
+                      P->ovl_cap, inst_base, k);
+        const uint64_t n_all = W.h_ctr->stage_count;  // staging slots; the sort buffer holds at most as many
+        const bool log_over = W.h_ctr->log_overflow || n_all > log_cap;
+        const bool k1_rep_over = W.h_ctr->k1_reports > rep_cap;
+        if (log_over || k1_rep_over) {  // filter/detect skipped: grow and re-run the interval
+          if (log_over) {
+            const uint64_t want = std::min<uint64_t>(n_all + n_all / 4 + 1024, 0xFFFFFFFFull);
+            if (n_all > 0xFFFFFFFFull) return fail(RC_ELIMIT, "more than 2^32 access records in one interval");
+            CK(W.log.ensure(want * 8));
+            CK(W.log_alt.ensure(want * 8));
+            log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
+            CK(ensure_sort_status(log_cap));
+          }
+          if (k1_rep_over) CK(grow_reports(W.h_ctr->k1_reports));
+          CK(set_report_count(rep_before));
+          continue;
         }
-        if (diverged) {  // rare path: lane scans for the divergence report (idempotent)
-          CK(launch_divergence(bp, s));
-        }
-        if (diverged || W.h_ctr->report_count > rep_cap) CK(read_ctr());
-        if (W.h_ctr->report_count <= rep_cap) {
-          rep_count = W.h_ctr->report_count;
-          break;
-        }
+        break;
+      }
+      tot_loads += W.h_ctr->iv_loads;
+      tot_stores += W.h_ctr->iv_stores;
+      tot_instr += W.h_ctr->iv_instr;
+      const uint64_t Ns = W.h_ctr->kept_count, Nslots = W.h_ctr->stage_count;
+      const uint64_t rep_after_k1 = W.h_ctr->k1_reports;
+      const bool diverged = W.h_ctr->diverged != 0;
+      // detect reports overflowed: grow, re-run detect (idempotent commits)
+      while (W.h_ctr->report_count > rep_cap) {
         CK(grow_reports(W.h_ctr->report_count));
         CK(set_report_count(rep_after_k1));
-        W.h_ctr->report_count = 0;  // force a fresh read after the re-run
+        DetectParams dp = detect_params();
+        CK(launch_detect(dp, s));
+        CK(read_ctr());
       }
-      if (W.prof.on) {  // exact sorted-record count is known now: fix this interval's profile bytes
-        const uint64_t Ns = W.h_ctr->kept_count;
+      if (diverged) {  // rare path: lane scans for the divergence report (idempotent)
+        const uint64_t before = W.h_ctr->report_count;
+        for (;;) {
+          BoundaryParams bp = bparams(k);
+          bp.status = W.status[cur ^ 1].as<uint8_t>();
+          bp.pc = W.pc[cur ^ 1].as<uint32_t>();
+          CK(launch_divergence(bp, s));
+          CK(read_ctr());
+          if (W.h_ctr->report_count <= rep_cap) break;
+          CK(grow_reports(W.h_ctr->report_count));
+          CK(set_report_count(before));
+        }
+      }
+      rep_count = W.h_ctr->report_count;
+      if (W.prof.on) {  // exact record counts are known now: fix this interval's profile bytes
         for (size_t i = mark0; i < W.prof.marks.size(); i++) {
           Profiler::Mark& m = W.prof.marks[i];
           if (m.cls == RC_PROF_SORT) { m.bytes = Ns * 16; m.items = Ns; }
           if (m.cls == RC_PROF_DETECT) { m.bytes = Ns * 8; m.items = Ns; }
-          if (m.cls == RC_PROF_FILTER) { m.bytes = Nr * 9 + W.h_ctr->kept_count * 8; }
+          if (m.cls == RC_PROF_FILTER) { m.bytes = Nslots * 8 + (W.h_ctr->staged_recs) + Ns * 8; m.items = Nslots; }
         }
       }
       cur ^= 1;  // the interval's lane state becomes current

@@ -330,3 +330,20 @@ def test_random_tiny_kernels_keep_all_reads(rc):
         ins = [rng.integers(-3, 4, size=(2, 5)).astype(np.int32) for _ in range(2)]
         p, g, o = run_both(rc, pr, n, ins, fuel=500, keep_all_reads=True)
         assert_parity(g, o, ins)
+
+
+def test_grow_and_retry_paths(rc, monkeypatch):
+    """With RC_DEBUG_SMALL_BUFFERS the log and report buffers start tiny, so
+    every interval overflows first and is re-run after growing (K1 retry from
+    the saved lane state, detect re-run); results must be unchanged."""
+    monkeypatch.setenv("RC_DEBUG_SMALL_BUFFERS", "1")
+    cases = [(K.TREE_OFF_BY_ONE, 256, I.cfg3_inputs(0, 40, 256)),
+             (K.BENIGN["K_inc"], 128, I.cfg2_inputs(0, 16, 128)),
+             (K.FIG1, 8, I.cfg1_inputs())]
+    for src, n, ins in cases:
+        p, g, o = run_both(rc, src, n, ins)
+        assert_parity(g, o, ins)
+    ins = I.cfg4_inputs(0, 3, 300)
+    ins[3][:, 20:60] += 1
+    p, g, o = run_both(rc, K.random_stencil_kernel(2), 300, ins)
+    assert_parity(g, o, ins)
