@@ -33,7 +33,9 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
   for (int i = t; i < p.passes * 256; i += F_THREADS) bh[i] = 0;
   if (blockIdx.x == 0 && t == 0) p.ctr->k1_reports = p.ctr->report_count;  // K1 is complete here
   if (p.ctr->log_overflow) return;  // the interval will be re-run
-  const uint64_t nr = p.ctr->stage_count;
+  // slots reserved past the buffer end only ever held sentinel padding (a real
+  // record there sets log_overflow): clamp to the capacity
+  const uint64_t nr = min(p.ctr->stage_count, (unsigned long long)p.n_slots);
   const uint64_t step = (uint64_t)gridDim.x * F_THREADS * F_ITEMS;
   __syncthreads();
   for (uint64_t b0 = (uint64_t)blockIdx.x * F_THREADS * F_ITEMS; b0 < nr; b0 += step) {

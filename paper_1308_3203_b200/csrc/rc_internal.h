@@ -142,7 +142,7 @@ struct FilterParams {
   uint32_t* hist;         // [4][256]
   int passes;
   DevCounters* ctr;
-  uint32_t n_slots;       // staging slots (= stage_count)
+  uint32_t n_slots;       // staging buffer capacity (slots); the kernel reads stage_count
   bool keep_all;          // RC_OPT_KEEP_ALL_READS: only drop the sentinels
 };
 constexpr uint64_t REC_SENTINEL = ~0ull;  // cell 0xFFFFFFFF is never a real cell

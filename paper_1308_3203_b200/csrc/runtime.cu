@@ -507,8 +507,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
                       "a work-item wrote more than %d distinct cells in one barrier interval (instance batch at "
                       "%u, interval %u)",
                       P->ovl_cap, inst_base, k);
-        const uint64_t n_all = W.h_ctr->stage_count;  // staging slots; the sort buffer holds at most as many
-        const bool log_over = W.h_ctr->log_overflow || n_all > log_cap;
+        const uint64_t n_all = W.h_ctr->stage_count;  // staging slots reserved (records + padding)
+        const bool log_over = W.h_ctr->log_overflow != 0;  // a real record did not fit
         const bool k1_rep_over = W.h_ctr->k1_reports > rep_cap;
         if (log_over || k1_rep_over) {  // filter/detect skipped: grow and re-run the interval
           if (log_over) {
