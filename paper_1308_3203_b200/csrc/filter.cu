@@ -12,11 +12,14 @@
 // Also computes the sort's digit histograms of the kept records (fused K2).
 #include "rc_internal.h"
 
+#ifndef F_ITEMS_OPT
+#define F_ITEMS_OPT 16
+#endif
 namespace rc {
 
 namespace {
 constexpr unsigned FULL = 0xFFFFFFFFu;
-constexpr int F_THREADS = 256, F_ITEMS = 4;
+constexpr int F_THREADS = 256, F_ITEMS = F_ITEMS_OPT;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
