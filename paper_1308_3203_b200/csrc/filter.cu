@@ -13,7 +13,7 @@
 #include "rc_internal.h"
 
 #ifndef F_ITEMS_OPT
-#define F_ITEMS_OPT 16
+#define F_ITEMS_OPT 4
 #endif
 namespace rc {
 
@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
   __shared__ uint32_t bh[4 * 256];
   __shared__ uint32_t wcnt[F_THREADS / 32];
   __shared__ unsigned long long sbase;
+  __shared__ uint64_t sbuf[F_THREADS * F_ITEMS];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   for (int i = t; i < p.passes * 256; i += F_THREADS) bh[i] = 0;
   if (blockIdx.x == 0 && t == 0) p.ctr->k1_reports = p.ctr->report_count;  // K1 is complete here
@@ -73,23 +74,29 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
       tot += wcnt[i];
     }
     if (t == 0) sbase = tot ? atomicAdd(&p.ctr->kept_count, (unsigned long long)tot) : 0ull;
-    __syncthreads();
-    uint64_t pos = sbase + woff + x - mine;
+    // block-local compaction in shared memory, then coalesced stores
+    uint32_t pos = woff + x - mine;
 #pragma unroll
-    for (int j = 0; j < F_ITEMS; j++) {
-      if (keep[j]) p.out[pos++] = rec[j];
-      // digit histograms of kept reads (runs: one add when the warp agrees)
-      const unsigned mk = __ballot_sync(FULL, keep[j]);
-      if (mk) {
-        const int first = __ffs(mk) - 1;
-        for (int ps = 0; ps < p.passes; ps++) {
-          const uint32_t d = (uint32_t)(rec[j] >> (REC_CELL_SHIFT + 8 * ps)) & 0xFF;
-          const uint32_t d0 = __shfl_sync(FULL, d, first);
-          if (__all_sync(FULL, !keep[j] || d == d0)) {
-            if (lane == first) atomicAdd(&bh[ps * 256 + d0], (uint32_t)__popc(mk));
-          } else if (keep[j]) {
-            atomicAdd(&bh[ps * 256 + d], 1u);
-          }
+    for (int j = 0; j < F_ITEMS; j++)
+      if (keep[j]) sbuf[pos++] = rec[j];
+    __syncthreads();
+    const unsigned long long base = sbase;
+    for (uint32_t i0 = 0; i0 < tot; i0 += F_THREADS) {  // block-uniform trip count
+      const uint32_t i = i0 + t;
+      const bool v = i < tot;
+      const uint64_t r = v ? sbuf[i] : 0;
+      if (v) p.out[base + i] = r;
+      // digit histograms (runs: one add when the warp agrees)
+      const unsigned mk = __ballot_sync(FULL, v);
+      if (!mk) continue;
+      const int first = __ffs(mk) - 1;
+      for (int ps = 0; ps < p.passes; ps++) {
+        const uint32_t d = (uint32_t)(r >> (REC_CELL_SHIFT + 8 * ps)) & 0xFF;
+        const uint32_t d0 = __shfl_sync(FULL, d, first);
+        if (__all_sync(FULL, !v || d == d0)) {
+          if (lane == first) atomicAdd(&bh[ps * 256 + d0], (uint32_t)__popc(mk));
+        } else if (v) {
+          atomicAdd(&bh[ps * 256 + d], 1u);
         }
       }
     }

@@ -171,11 +171,16 @@ struct Profiler {
   std::vector<Mark> marks;
   size_t used = 0;
   size_t open_ev = 0;
+  // the last end event doubles as the next begin when nothing was launched
+  // in between (halves the event records per interval)
+  size_t last_end = (size_t)-1;
+  uint64_t launches_at_end = 0;
+  cudaStream_t end_stream = nullptr;
   cudaEvent_t ev(size_t i) { return pool[i]; }
   size_t next();
   void begin(cudaStream_t s);
   void end(int cls, cudaStream_t s, uint64_t bytes, uint64_t items);
-  void reset() { marks.clear(); used = 0; }
+  void reset() { marks.clear(); used = 0; last_end = (size_t)-1; }
   void collect(rc_profile* out);
   ~Profiler();
 };

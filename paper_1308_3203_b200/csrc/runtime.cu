@@ -39,6 +39,10 @@ size_t Profiler::next() {
 }
 void Profiler::begin(cudaStream_t s) {
   if (!on) return;
+  if (last_end != (size_t)-1 && end_stream == s && launches_at_end == g_launches.load()) {
+    open_ev = last_end;
+    return;
+  }
   open_ev = next();
   cudaEventRecord(pool[open_ev], s);
 }
@@ -47,6 +51,9 @@ void Profiler::end(int cls, cudaStream_t s, uint64_t bytes, uint64_t items) {
   size_t e1 = next();
   cudaEventRecord(pool[e1], s);
   marks.push_back({cls, open_ev, e1, bytes, items});
+  last_end = e1;
+  end_stream = s;
+  launches_at_end = g_launches.load();
 }
 void Profiler::collect(rc_profile* out) {
   for (const Mark& m : marks) {

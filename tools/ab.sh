@@ -6,5 +6,6 @@ for f in "$@"; do
   python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu-baseline ${BENCH_ARGS} 2>/dev/null | python -c "
 import json,sys
 d=json.loads(sys.stdin.read()); print(round(d['value'],3), 'Gaccess/s', round(d['ms_per_step'],1), 'ms')
-print('  ', {k:round(v['ms_per_step'],1) for k,v in d['kernels'].items() if isinstance(v,dict) and v['ms_per_step']>1})"
+k=d.get('kernels') or {}
+print('  ', {a:round(v['ms_per_step'],1) for a,v in k.items() if isinstance(v,dict) and v['ms_per_step']>1})"
 done
