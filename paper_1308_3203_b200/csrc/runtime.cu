@@ -311,8 +311,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   const bool small_buffers = getenv("RC_DEBUG_SMALL_BUFFERS") != nullptr;
   uint64_t log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
   {
-    // ~4 records per lane plus the tails of the per-block staging chunks (K1 grid <= 4 blocks per SM)
-    uint64_t want = std::max<uint64_t>(1u << 16, std::min<uint64_t>(L_max * 4 + 148ull * 4 * 8192, 0xFFFFFFFFull));
+    // ~4 records per lane plus the tails of the per-warp staging chunks (512 slots; <= 64 warps per SM)
+    uint64_t want = std::max<uint64_t>(1u << 16, std::min<uint64_t>(L_max * 4 + 148ull * 64 * 512, 0xFFFFFFFFull));
     if (small_buffers) want = 1024;
     if (log_cap < want) {
       CK(W.log.ensure(want * 8));

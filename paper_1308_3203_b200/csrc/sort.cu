@@ -25,6 +25,9 @@
 #ifndef SORT_EXP
 #define SORT_EXP 0
 #endif
+#ifndef SORT_MINB  // resident blocks per SM of the persistent pass (smem: ~72 KB each)
+#define SORT_MINB 2
+#endif
 
 namespace rc {
 
@@ -203,7 +206,7 @@ __device__ __forceinline__ unsigned match_digit(uint32_t d, unsigned valid_mask)
 // the hardware block scheduler staggers tiles, which keeps look-back walks
 // short) with a single buffer.
 template <bool PERSISTENT>
-__global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? 2 : 3) onesweep_kernel(const uint64_t* __restrict__ in,
+__global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) onesweep_kernel(const uint64_t* __restrict__ in,
                                                                    uint64_t* __restrict__ out, uint32_t n_host,
                                                                    const unsigned long long* n_a,
                                                                    const unsigned long long* n_b, int shift,
