@@ -29,13 +29,13 @@ __device__ __forceinline__ uint32_t rec_cell(uint64_t r) { return (uint32_t)(r >
 __device__ __forceinline__ uint32_t rec_tid(uint64_t r) { return ((uint32_t)r >> 5) & (MAX_WG - 1); }
 __device__ __forceinline__ bool rec_w(uint64_t r) { return (r & 1) != 0; }
 __device__ __forceinline__ int32_t rec_val(const DetectParams& p, uint64_t r) {
-  const uint32_t lane = (rec_cell(r) / p.cpi) * p.n + rec_tid(r);
+  const uint32_t lane = fast_div(rec_cell(r), p.cpi_magic) * p.n + rec_tid(r);
   return __ldg(p.wval + (size_t)(((uint32_t)r >> 1) & 0xF) * p.n_lanes + lane);
 }
 
 __device__ __forceinline__ void emit(const DetectParams& p, uint32_t cell, uint32_t t1, uint32_t t2, uint16_t kind,
                                   uint16_t flags) {
-  const uint32_t inst = cell / p.cpi;
+  const uint32_t inst = fast_div(cell, p.cpi_magic);
   const uint32_t rem = cell - inst * p.cpi;
   uint32_t a = 0;
   while (a + 1 < p.n_arrays && __ldg(p.arr_off + a + 1) <= rem) a++;

@@ -8,11 +8,8 @@
 // memory), lanes at that pc execute it, the rest wait — a lane's result never
 // depends on the order because, inside an interval, lanes only see the
 // interval-start heap plus their own writes (delayed visibility, reading L2).
-// The grid is persistent and every warp is an independent worker: it walks
-// tiles of 32 lanes with its own TMA-prefetched lane state (double-buffered),
-// its own staging chunk and bulk stores of the state it leaves — no block
-// barrier after the program is staged, so a warp waiting on its heap loads
-// never holds the others.
+// The grid is persistent: a block walks tiles of T lanes, so the program is
+// staged once and histograms / statistics are flushed once per block.
 //
 // Per lane: registers (Locals) live in shared memory laid out
 // [reg][thread] (a warp touching one register hits 32 distinct banks); only
@@ -29,10 +26,10 @@
 // Log: a read record per performed LD, and at the end of the interval one
 // write record per distinct cell the lane wrote (its final value, reading L3,
 // goes to the side table wval[slot][lane]).  Records are staged per warp in
-// shared memory and copied to the warp's chunk of the staging buffer (512
-// slots reserved with one atomic; an abandoned chunk tail holds sentinels);
-// write records also mark their cell in the write-set byte map.  The
-// write-set filter (filter.cu) compacts the staging buffer for the sort.
+// shared memory; the tile's write-out takes ONE atomic per record kind per
+// block: write records go straight into the sort buffer (and mark their cell
+// in the write-set byte map), read records into a staging buffer that the
+// write-set filter compacts (filter.cu).
 //
 // Fused A4 (reading L9): per instance the min / max arrival
 // node (BAR pc, or -1 for exit) of the lanes that arrived in this interval —
@@ -121,7 +118,7 @@ __device__ __noinline__ uint32_t flush_warp_(const LogOut p, const uint64_t* rec
   return 0;
 }
 
-constexpr uint32_t STAGE_CHUNK = 512;  // staging slots a warp reserves at a time
+constexpr uint32_t STAGE_CHUNK = 8192;  // staging slots a block reserves at a time
 
 __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
 #pragma unroll
@@ -217,36 +214,19 @@ void interp_phase_io(unsigned long long* out, bool reset) {
 #define IPHASE(i) do {} while (0)
 #endif
 
-__host__ __device__ inline size_t warp_smem_bytes(const InterpParams& p) {
-  constexpr size_t T = 32;
-  size_t b = 16 + (size_t)p.stage_warp * 8;  // mbarriers, staging
-  b += (size_t)2 * p.n_regs * T * 4;           // register files (double-buffered)
-  b += (size_t)2 * T * 5;                      // pc / status rows
-  b += (size_t)p.ovl_cap * T * 8;              // overlay
-  return (b + 15) & ~size_t(15);
-}
-
 template <bool CODE_SMEM>
 __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const InterpParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int T = 32;  // lanes per tile: a warp is an independent persistent worker
-  const int W = blockDim.x >> 5;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = blockDim.x;
+  const int W = T >> 5;
+  const int t = threadIdx.x;
+  const int warp = t >> 5, lane = t & 31;
   const uint32_t R = p.n_regs, OV = p.ovl_cap;
   const LogOut lo{p.stage, p.wmap, p.ctr, p.stage_cap};
 
-  // ---- shared memory carve-up (sizes mirrored in interp_smem_bytes): block
-  //      part (program, array table, live list), then one region per warp
+  // ---- shared memory carve-up (sizes mirrored in interp_smem_bytes)
   unsigned char* q = smem;
-  uint4* s_code = reinterpret_cast<uint4*>(q); q += CODE_SMEM ? (size_t)p.n_instr * 16 : 0;
-  uint32_t* s_off = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
-  uint32_t* s_size = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
-  uint8_t* s_live = reinterpret_cast<uint8_t*>(q); q += p.n_live;
-  q = smem + ((q - smem + 15) & ~size_t(15));
-  q += (size_t)warp * warp_smem_bytes(p);
-  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(q); q += 16;
-  uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)p.stage_warp * 8;
-  // register files [reg][lane], status and pc rows, double-buffered (TMA);
+  // register files [reg][thread], status and pc rows, double-buffered (TMA);
   // buffer b is addressed arithmetically from these bases (a runtime-indexed
   // array of pointers would lose the shared address space)
   int32_t* const sregs0 = reinterpret_cast<int32_t*>(q); q += (size_t)2 * R * T * 4;
@@ -255,50 +235,56 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
 #define SREGS(b) (sregs0 + (size_t)(b) * R * T)
 #define SPC(b) (spc0 + (size_t)(b) * T)
 #define SSTAT(b) (sstat0 + (size_t)(b) * T)
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(q); q += 16;
+  uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)W * p.stage_warp * 8;
+  uint4* s_code = reinterpret_cast<uint4*>(q); q += CODE_SMEM ? (size_t)p.n_instr * 16 : 0;
   uint32_t* ocell = reinterpret_cast<uint32_t*>(q); q += (size_t)OV * T * 4;
-  int32_t* oval = reinterpret_cast<int32_t*>(q);
+  int32_t* oval = reinterpret_cast<int32_t*>(q); q += (size_t)OV * T * 4;
+  uint32_t* s_off = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
+  uint32_t* s_size = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
+  uint8_t* s_live = reinterpret_cast<uint8_t*>(q); q += (p.n_live + 3) & ~3u;
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(q); q += (size_t)W * 4 + 8;  // per-warp staged records, pad count
+  q = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(q) + 7) & ~uintptr_t(7));
+  unsigned long long* wbase = reinterpret_cast<unsigned long long*>(q); q += (size_t)(W + 1) * 8;  // [W], pad start
 
-  for (uint32_t a = threadIdx.x; a < p.n_arrays; a += blockDim.x) {
+  for (uint32_t a = t; a < p.n_arrays; a += T) {
     s_off[a] = p.arr_off[a];
     s_size[a] = p.arr_size[a];
   }
   __syncthreads();  // s_off / s_size before the pre-decode
   if (CODE_SMEM)
-    for (uint32_t i = threadIdx.x; i < p.n_instr; i += blockDim.x)
-      s_code[i] = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + i), T, s_off, s_size);
-  for (uint32_t i = threadIdx.x; i < p.n_live; i += blockDim.x) s_live[i] = p.live[i];
-  if (lane == 0) {
+    for (uint32_t i = t; i < p.n_instr; i += T) s_code[i] = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + i), T, s_off, s_size);
+  for (uint32_t i = t; i < p.n_live; i += T) s_live[i] = p.live[i];
+  const uint32_t n_tiles0 = (p.n_lanes + T - 1) / T;
+  if (t == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[0])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();  // the only block barrier: program and tables staged
+  __syncthreads();
+  if (t == 0 && blockIdx.x < n_tiles0)
+    prefetch_lanes(p, blockIdx.x, T, SSTAT(0), SPC(0), SREGS(0), s_live, &mbar[0]);
 
-  const uint32_t n_tiles = (p.n_lanes + T - 1) / T;
-  const uint32_t gw = blockIdx.x * (uint32_t)W + warp, n_workers = gridDim.x * (uint32_t)W;
-  if (lane == 0 && gw < n_tiles) prefetch_lanes(p, gw, T, SSTAT(0), SPC(0), SREGS(0), s_live, &mbar[0]);
-
-  // per-lane totals, reduced once at the end
-  unsigned long long b_instr = 0;
-  uint32_t b_loads = 0, b_stores = 0;
+  // per-lane totals, reduced once at the end of the kernel
+  unsigned long long b_instr = 0, b_loads = 0, b_stores = 0;
   bool b_wait = false, b_over = false, b_ovl = false;
-  unsigned long long b_staged = 0;  // warp-uniform
-  // the warp's current staging chunk (warp-uniform)
+  // the block's current staging chunk (thread 0)
   unsigned long long c_base = 0;
   uint32_t c_used = 0, c_cap = 0;
+  const uint32_t n_tiles = (p.n_lanes + T - 1) / T;
 
   uint32_t parity = 0;  // bit b: expected phase of mbar[b]
   int cur = 0;
 #ifdef INTERP_PHASE_TIMING
-  const int t = lane;
   long long tprev_ = clock64();
 #endif
-  for (uint32_t tile = gw; tile < n_tiles; tile += n_workers, cur ^= 1) {
+  for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, cur ^= 1) {
     // prefetch the next tile's lane state into the other buffer once the bulk
     // stores of its previous use have finished reading it
-    if (lane == 0 && tile + n_workers < n_tiles) {
+    if (t == 0 && tile + gridDim.x < n_tiles) {
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      prefetch_lanes(p, tile + n_workers, T, SSTAT(cur ^ 1), SPC(cur ^ 1), SREGS(cur ^ 1), s_live, &mbar[cur ^ 1]);
+      prefetch_lanes(p, tile + gridDim.x, T, SSTAT(cur ^ 1), SPC(cur ^ 1), SREGS(cur ^ 1), s_live,
+                     &mbar[cur ^ 1]);
     }
     IPHASE(0);
     mbar_wait_parity(&mbar[cur], (parity >> cur) & 1u);
@@ -306,16 +292,16 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
     IPHASE(1);
     uint8_t* const sstat = SSTAT(cur);
     uint32_t* const spc = SPC(cur);
-    const uint32_t g = tile * (uint32_t)T + lane;
+    const uint32_t g = tile * (uint32_t)T + t;
     const bool valid = g < p.n_lanes;
-    uint8_t status = valid ? sstat[lane] : (uint8_t)L_EXITED;
-    uint32_t pc = valid ? spc[lane] : 0;
+    uint8_t status = valid ? sstat[t] : (uint8_t)L_EXITED;
+    uint32_t pc = valid ? spc[t] : 0;
     if (status == L_EXITED_NOW) status = L_EXITED;
     bool running = valid && (status == L_RUNNING || status == L_WAITING);
-    const uint32_t inst = valid ? g / p.n : 0;
+    const uint32_t inst = valid ? fast_div(g, p.n_magic) : 0;
     const uint32_t tid = valid ? g - inst * p.n : 0;
     const uint32_t cell_base = inst * p.cpi;
-    int32_t* Rg = SREGS(cur) + lane;  // register r of this lane = Rg[r*T] (live ones arrived by TMA)
+    int32_t* Rg = SREGS(cur) + t;  // register r of this lane = Rg[r*T] (live ones arrived by TMA)
 
     if (running) status = L_RUNNING;
     // non-blocking loads: up to NP issued LDs whose destination register is
@@ -328,8 +314,9 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
     for (int j = 0; j < NP; j++) { pr[j] = NOREG; pv[j] = 0; }
     int n_own = 0;
     unsigned long long steps = 0;
+    uint32_t nloads = 0, nstores = 0;
     bool ovl_over = false;
-    Stage S{st_recs, 0, p.stage_warp};
+    Stage S{st_recs + (size_t)warp * p.stage_warp, 0, p.stage_warp};
 
     uint32_t npend = 0;  // occupied pending-load slots of this lane
     for (;;) {
@@ -423,7 +410,7 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
               int32_t v = 0;
               bool found = false;
               for (int j = 0; j < n_own; j++)
-                if (ocell[j * T + lane] == cell) { v = oval[j * T + lane]; found = true; }
+                if (ocell[j * T + t] == cell) { v = oval[j * T + t]; found = true; }
               if (found) {
                 *Ra = v;
               } else {  // issue the load; write the register back later
@@ -442,7 +429,7 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
                 npend++;
               }
               pc++;
-              b_loads++;
+              nloads++;
               ok = true;
             }
           }
@@ -464,14 +451,14 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
             } else {
               const uint32_t cell = cell_base + e.z + (uint32_t)idx;
               int j = 0;
-              while (j < n_own && ocell[j * T + lane] != cell) j++;
+              while (j < n_own && ocell[j * T + t] != cell) j++;
               if (j == n_own) {
-                if (n_own < (int)OV) { ocell[j * T + lane] = cell; n_own++; }
+                if (n_own < (int)OV) { ocell[j * T + t] = cell; n_own++; }
                 else { ovl_over = true; j = -1; }
               }
-              if (j >= 0) oval[j * T + lane] = *Rc;
+              if (j >= 0) oval[j * T + t] = *Rc;
               pc++;
-              b_stores++;
+              nstores++;
             }
           }
           break;
@@ -514,8 +501,8 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
       const unsigned m = __ballot_sync(FULL, has);
       if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane);
       if (has) {
-        S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(ocell[j * T + lane], tid, (uint32_t)j, 1);
-        p.wval[(size_t)j * p.n_lanes + g] = oval[j * T + lane];
+        S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(ocell[j * T + t], tid, (uint32_t)j, 1);
+        p.wval[(size_t)j * p.n_lanes + g] = oval[j * T + t];
       }
       S.fill += __popc(m);
     }
@@ -539,36 +526,56 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
       atomicMin(p.node_min + inst, node);
       atomicMax(p.node_max + inst, node);
     }
-    b_instr += steps;
-    b_wait |= status == L_WAITING;
-    b_ovl |= ovl_over;
 
-    // ---- the tile's records into the warp's staging chunk (a new chunk —
-    //      one atomic — only when the current one is full; its tail is padded)
-    const uint32_t tot = S.fill;  // warp-uniform
-    if (tot) {
-      if (c_used + tot > c_cap) {
-        for (uint32_t i = lane; i < c_cap - c_used; i += 32)  // sentinels in the abandoned tail
-          if (c_base + c_used + i < p.stage_cap) p.stage[c_base + c_used + i] = REC_SENTINEL;
-        const uint32_t sz = max(STAGE_CHUNK, tot);
-        unsigned long long nb = 0;
-        if (lane == 0) nb = atomicAdd(&p.ctr->stage_count, (unsigned long long)sz);
-        c_base = __shfl_sync(FULL, nb, 0);
-        c_used = 0;
-        c_cap = sz;
-      }
-      write_out(lo, S.recs, tot, c_base + c_used, lane, &b_over);
-      c_used += tot;
-      b_staged += tot;
-    }
+    // ---- tile write-out into the block's staging chunk (a new chunk — one
+    //      atomic — only when the current one is full; its tail is padded)
+    // statistics stay per lane until the end of the kernel
+    b_instr += steps;
+    b_loads += nloads;
+    b_stores += nstores;
+    b_ovl |= ovl_over;
+    if (lane == 0) wcnt[warp] = S.fill;
+    b_wait |= status == L_WAITING;
+    __syncthreads();
     IPHASE(4);
+    if (warp == 0) {
+      const uint32_t c = lane < W ? wcnt[lane] : 0u;
+      uint32_t x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+      }
+      const uint32_t tot = __shfl_sync(FULL, x, 31);
+      unsigned long long pad_from = 0;
+      uint32_t pad_n = 0;
+      if (lane == 0 && tot) {
+        if (c_used + tot > c_cap) {  // pad the rest of the current chunk, take a new one
+          pad_from = c_base + c_used;
+          pad_n = c_cap - c_used;
+          const uint32_t sz = max(STAGE_CHUNK, tot);
+          c_base = atomicAdd(&p.ctr->stage_count, (unsigned long long)sz);
+          c_used = 0;
+          c_cap = sz;
+        }
+        atomicAdd(&p.ctr->staged_recs, (unsigned long long)tot);  // fire-and-forget
+      }
+      const unsigned long long cb = __shfl_sync(FULL, c_base + c_used, 0);
+      if (lane < W) wbase[lane] = cb + x - c;
+      if (lane == 0) {
+        c_used += tot;
+        wbase[W] = pad_from;
+        wcnt[W] = pad_n;
+      }
+    }
     // lane state out: status / pc into the shared rows (the live register
     // rows already are), then bulk stores of every row
-    sstat[lane] = valid ? status : (uint8_t)L_EXITED;
-    spc[lane] = pc;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
-    __syncwarp();
-    if (lane == 0) {
+    sstat[t] = valid ? status : (uint8_t)L_EXITED;
+    spc[t] = pc;
+    __syncthreads();
+    IPHASE(5);
+    if (t == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       const size_t g0 = (size_t)tile * T;
       bulk_s2g(p.status_out + g0, sstat, (uint32_t)T);
       bulk_s2g(p.pc_out + g0, spc, (uint32_t)T * 4);
@@ -578,37 +585,51 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
       }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
-    __syncwarp();  // staging / overlay reused by the next tile
-    IPHASE(5);
+    write_out(lo, S.recs, S.fill, wbase[warp], lane, &b_over);
+    for (uint32_t i = t; i < wcnt[W]; i += T)  // sentinels in the abandoned chunk tail
+      if (wbase[W] + i < p.stage_cap) p.stage[wbase[W] + i] = REC_SENTINEL;
+    IPHASE(6);
+    __syncthreads();  // staging / overlay / registers reused by the next tile
+    IPHASE(7);
   }
 
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // lane-state stores complete
-  // ---- warp flush: sentinels in the last chunk's tail, statistics, flags
-  for (uint32_t i = lane; i < c_cap - c_used; i += 32)
-    if (c_base + c_used + i < p.stage_cap) p.stage[c_base + c_used + i] = REC_SENTINEL;
-  b_instr = warp_sum64(b_instr);
-  const unsigned long long s_loads = warp_sum64(b_loads), s_stores = warp_sum64(b_stores);
-  const bool any_over = __any_sync(FULL, b_over), any_wait = __any_sync(FULL, b_wait),
-             any_ovl = __any_sync(FULL, b_ovl);
-  if (lane == 0) {
-    if (b_instr) atomicAdd(&p.ctr->iv_instr, b_instr);
-    if (s_loads) atomicAdd(&p.ctr->iv_loads, s_loads);
-    if (s_stores) atomicAdd(&p.ctr->iv_stores, s_stores);
-    if (b_staged) atomicAdd(&p.ctr->staged_recs, b_staged);
-    if (any_over) p.ctr->log_overflow = 1;
-    if (any_wait) p.ctr->any_waiting = 1;
-    if (any_ovl) p.ctr->ovl_overflow = 1;
+  if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // lane-state stores complete
+  // ---- block flush: sentinels in the last chunk's tail, statistics, flags
+  if (t == 0) {
+    wbase[W] = c_base + c_used;
+    wcnt[W] = c_cap - c_used;
   }
-#undef SREGS
-#undef SPC
-#undef SSTAT
+  __syncthreads();
+  for (uint32_t i = t; i < wcnt[W]; i += T)
+    if (wbase[W] + i < p.stage_cap) p.stage[wbase[W] + i] = REC_SENTINEL;
+  if (__any_sync(FULL, b_over) && lane == 0) p.ctr->log_overflow = 1;
+  {  // per-warp totals
+    b_instr = warp_sum64(b_instr);
+    b_loads = warp_sum64(b_loads);
+    b_stores = warp_sum64(b_stores);
+    const bool any_ovl = __any_sync(FULL, b_ovl);
+    if (lane == 0) {
+      if (b_instr) atomicAdd(&p.ctr->iv_instr, b_instr);
+      if (b_loads) atomicAdd(&p.ctr->iv_loads, b_loads);
+      if (b_stores) atomicAdd(&p.ctr->iv_stores, b_stores);
+      if (any_ovl) p.ctr->ovl_overflow = 1;
+    }
+  }
+  if (__any_sync(FULL, b_wait) && lane == 0) p.ctr->any_waiting = 1;
 }
 
-size_t interp_smem_bytes(const InterpParams& p, int threads, bool code_in_smem) {
-  size_t b = code_in_smem ? (size_t)p.n_instr * 16 : 0;  // pre-decoded program
-  b += (size_t)p.n_arrays * 8 + p.n_live;                // array offsets / sizes, live list
-  b = (b + 15) & ~size_t(15);
-  return b + (size_t)(threads / 32) * warp_smem_bytes(p);
+size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem) {
+  const int W = T / 32;
+  size_t b = (size_t)2 * p.n_regs * T * 4;         // register files (double-buffered)
+  b += (size_t)2 * T * 5 + 16;                     // status / pc rows, mbarriers
+  b += (size_t)W * p.stage_warp * 8;                    // staging
+  b += code_in_smem ? (size_t)p.n_instr * 16 : 0;  // pre-decoded program
+  b += (size_t)p.ovl_cap * T * 8;                  // overlay
+  b += (size_t)p.n_arrays * 8;                     // array offsets / sizes
+  b += ((size_t)p.n_live + 3) & ~size_t(3);        // live register list
+  b += (size_t)W * 20 + 8;                         // warp counts, node range, instance (+align)
+  b += (size_t)W * 8 * 5;                          // warp bases (2) + 3 stats
+  return b;
 }
 
 cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {

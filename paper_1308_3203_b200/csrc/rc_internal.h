@@ -51,6 +51,16 @@ constexpr int OVL_CAP = 16;        // own-write overlay entries per work-item (s
 constexpr int REC_CELL_SHIFT = 32;
 constexpr uint32_t LANE_PAD = 256;  // lane-state rows are padded to multiples of this (TMA tiles)
 constexpr uint32_t MAX_WG = 1u << 27;
+// Division by a run-constant divisor d (work-group size, cells per instance):
+// magic = ceil(2^64 / d) (0 for d == 1); x / d == umulhi64(x, magic) exactly
+// for every x < 2^32 (the rounding error is x * (magic - 2^64/d) / 2^64 <
+// 2^-32 <= 1/d).
+inline uint64_t div_magic(uint32_t d) { return d <= 1 ? 0ull : ~0ull / d + 1; }
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t fast_div(uint32_t x, uint64_t magic) {
+  return magic ? (uint32_t)__umul64hi((uint64_t)x, magic) : x;
+}
+#endif
 __host__ __device__ inline uint64_t make_rec(uint32_t cell, uint32_t tid, uint32_t slot, uint32_t w) {
   return ((uint64_t)cell << 32) | (tid << 5) | (slot << 1) | w;
 }
@@ -79,6 +89,7 @@ struct InterpParams {
   const Ins* code;
   uint32_t n_instr, n_regs, n_arrays;
   uint32_t n;                 // work-group size
+  uint64_t n_magic;           // div_magic(n)
   uint32_t n_lanes;           // I_b * n
   uint32_t cpi;               // cells per instance
   uint64_t fuel;
@@ -120,6 +131,7 @@ struct DetectParams {
   uint32_t n_records;         // host upper bound (grid size)
   int32_t* heap;
   uint32_t cpi, n_arrays;
+  uint64_t cpi_magic;         // div_magic(cpi)
   const uint32_t* arr_off;
   uint32_t interval, inst_base;
   rc_report* reports;
@@ -181,6 +193,7 @@ struct Profiler {
   void begin(cudaStream_t s);
   void end(int cls, cudaStream_t s, uint64_t bytes, uint64_t items);
   void reset() { marks.clear(); used = 0; last_end = (size_t)-1; }
+  void cut() { last_end = (size_t)-1; }  // host sync / memsets since the last end: fresh begin
   void collect(rc_profile* out);
   ~Profiler();
 };

@@ -311,8 +311,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   const bool small_buffers = getenv("RC_DEBUG_SMALL_BUFFERS") != nullptr;
   uint64_t log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
   {
-    // ~4 records per lane plus the tails of the per-warp staging chunks (512 slots; <= 64 warps per SM)
-    uint64_t want = std::max<uint64_t>(1u << 16, std::min<uint64_t>(L_max * 4 + 148ull * 64 * 512, 0xFFFFFFFFull));
+    // ~4 records per lane plus the tails of the per-block staging chunks (K1 grid <= 4 blocks per SM)
+    uint64_t want = std::max<uint64_t>(1u << 16, std::min<uint64_t>(L_max * 4 + 148ull * 4 * 8192, 0xFFFFFFFFull));
     if (small_buffers) want = 1024;
     if (log_cap < want) {
       CK(W.log.ensure(want * 8));
@@ -367,6 +367,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     const uint32_t L = nb * n;
     const uint32_t inst_base = opt.instance_offset + b0;
     // A2: heap init
+    W.prof.cut();
     W.prof.begin(s);
     for (uint32_t a = 0; a < n_arrays; a++) {
       if (!size[a]) continue;
@@ -428,6 +429,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         dp.n_records = (uint32_t)log_cap;  // upper bound; the kernel reads the exact count
         dp.heap = W.heap.as<int32_t>();
         dp.cpi = (uint32_t)std::max<uint64_t>(cpi, 1);
+        dp.cpi_magic = div_magic(dp.cpi);
         dp.n_arrays = n_arrays;
         dp.arr_off = W.arr_off.as<uint32_t>();
         dp.interval = k;
@@ -446,6 +448,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         ip.n_regs = P->n_regs;
         ip.n_arrays = n_arrays;
         ip.n = n;
+        ip.n_magic = div_magic(n);
         ip.n_lanes = L;
         ip.cpi = (uint32_t)cpi;
         ip.fuel = opt.fuel_per_interval;
@@ -475,6 +478,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         ip.report_cap = rep_cap;
         ip.ctr = dctr;
         mark0 = W.prof.marks.size();
+        W.prof.cut();
         W.prof.begin(s);
         CK(launch_interp(ip, s));
         W.prof.end(RC_PROF_INTERP, s, 0, L);
@@ -592,6 +596,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     CK(launch_lane_hist(W.status[cur].as<uint8_t>(), L, dctr, s));
     // final heaps out
     if (final_heaps) {
+      W.prof.cut();
       W.prof.begin(s);
       for (uint32_t a = 0; a < n_arrays; a++) {
         if (!size[a]) continue;
@@ -619,6 +624,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   // K6: canonical order, then the first min(capacity, total) to the host
   if (rep_count > 1) {
     CK(W.reports_scratch.ensure(std::max<uint64_t>(rep_count, 2048) * 2 * sizeof(rc_report)));
+    W.prof.cut();
     W.prof.begin(s);
     CK(finalize_reports(W.reports.as<rc_report>(), rep_count, W.reports_scratch.as<rc_report>(), s));
     W.prof.end(RC_PROF_FINALIZE, s, rep_count * 64, rep_count);
