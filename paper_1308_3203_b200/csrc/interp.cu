@@ -126,6 +126,20 @@ __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
   return v;
 }
 
+// heap load straight into pending slot K's register.  The four slots use
+// distinct (equivalent) L1 eviction hints so the compiler cannot merge the
+// slot branches into one load followed by moves — a move would wait for the
+// data and make the load blocking.
+template <int K>
+__device__ __forceinline__ int32_t ldg_slot(const int32_t* p) {
+  int32_t v;
+  if (K == 0) asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  else if (K == 1) asm volatile("ld.global.nc.L1::evict_normal.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  else if (K == 2) asm volatile("ld.global.nc.L1::evict_last.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  else asm volatile("ld.global.nc.L1::evict_unchanged.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ int32_t wadd(int32_t x, int32_t y) { return (int32_t)((uint32_t)x + (uint32_t)y); }
 
 // ---- TMA bulk copies (cp.async.bulk) of lane-state rows ---------------------
@@ -419,13 +433,14 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
                   for (int j = 0; j < NP; j++) { Rg[pr[j]] = pv[j]; pr[j] = NOREG; }
                   npend = 0;
                 }
-                const int32_t lv = __ldg(p.heap + cell);
+                const int32_t* const src = p.heap + cell;
                 const uint32_t oa = e.x >> 16;
-                // first free slot (slots fill in order)
-                if (pr[0] == NOREG) { pv[0] = lv; pr[0] = oa; }
-                else if (pr[1] == NOREG) { pv[1] = lv; pr[1] = oa; }
-                else if (pr[2] == NOREG) { pv[2] = lv; pr[2] = oa; }
-                else { pv[3] = lv; pr[3] = oa; }
+                // first free slot; each branch loads straight into its slot's
+                // register (a runtime-selected move would wait for the data)
+                if (pr[0] == NOREG) { pv[0] = ldg_slot<0>(src); pr[0] = oa; }
+                else if (pr[1] == NOREG) { pv[1] = ldg_slot<1>(src); pr[1] = oa; }
+                else if (pr[2] == NOREG) { pv[2] = ldg_slot<2>(src); pr[2] = oa; }
+                else { pv[3] = ldg_slot<3>(src); pr[3] = oa; }
                 npend++;
               }
               pc++;
