@@ -28,16 +28,33 @@ __device__ __forceinline__ bool arrived_node(uint8_t st, uint32_t pc, int32_t* n
 }
 
 // per instance: did the arrivals of this interval reach more than one node?
-// (K1 reduced min / max arrival node per instance.)  Resets the range.
+// (K1 reduced min / max arrival node per instance.)  Resets the range.  The
+// last block to finish takes the interval's verdict: `abort` when the host must
+// act before the next interval may run (DevCounters::abort).
 __global__ void boundary_check_kernel(const BoundaryParams p) {
+  DevCounters* c = p.ctr;
+  if (c->abort) return;  // speculative interval after one that needs the host
   const uint32_t inst = blockIdx.x * blockDim.x + threadIdx.x;
-  if (inst >= p.n_inst) return;
-  const int32_t lo = p.node_min[inst], hi = p.node_max[inst];
-  p.node_min[inst] = 0x7FFFFFFF;
-  p.node_max[inst] = (int32_t)0x80000000;
-  const bool div = lo < hi;
-  p.inst_flag[inst] = div;
-  if (div) p.ctr->diverged = 1;
+  if (inst < p.n_inst) {
+    const int32_t lo = p.node_min[inst], hi = p.node_max[inst];
+    p.node_min[inst] = 0x7FFFFFFF;
+    p.node_max[inst] = (int32_t)0x80000000;
+    const bool div = lo < hi;
+    p.inst_flag[inst] = div;
+    if (div) c->diverged = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&c->bdone, 1u) == gridDim.x - 1) {
+      __threadfence();
+      c->bdone = 0;
+      const volatile DevCounters* v = c;
+      const bool need_host = v->log_overflow || v->ovl_overflow || v->k1_reports > p.report_cap ||
+                             v->report_count > p.report_cap || v->diverged || !v->any_waiting;
+      if (need_host) c->abort = 1;
+    }
+  }
 }
 
 // rare path 1: first arrived tid of each diverged instance

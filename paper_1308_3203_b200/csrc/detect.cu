@@ -295,7 +295,7 @@ __device__ __forceinline__ void detect_chunk(const DetectParams& p, uint64_t wg,
 // interval's log overflowed or K1's reports overflowed: the host then re-runs
 // the interval from the saved lane state on an untouched heap.
 __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
-  if (p.ctr->log_overflow || p.ctr->k1_reports > p.report_cap) return;
+  if (p.ctr->abort || p.ctr->log_overflow || p.ctr->k1_reports > p.report_cap) return;
   const uint32_t n_records = (uint32_t)p.ctr->kept_count;
   const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wg * DET_CHUNK < n_records; wg += warps)

@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
   __shared__ uint32_t wcnt[F_THREADS / 32];
   __shared__ unsigned long long sbase;
   __shared__ uint64_t sbuf[F_THREADS * F_ITEMS];
+  if (p.ctr->abort) return;  // speculative interval (DevCounters::abort)
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   for (int i = t; i < p.passes * 256; i += F_THREADS) bh[i] = 0;
   if (blockIdx.x == 0 && t == 0) p.ctr->k1_reports = p.ctr->report_count;  // K1 is complete here

@@ -231,6 +231,7 @@ void interp_phase_io(unsigned long long* out, bool reset) {
 template <bool CODE_SMEM>
 __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const InterpParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
+  if (p.ctr->abort) return;  // speculative interval (DevCounters::abort)
   const int T = blockDim.x;
   const int W = T >> 5;
   const int t = threadIdx.x;

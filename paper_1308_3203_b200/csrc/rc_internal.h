@@ -82,6 +82,13 @@ struct DevCounters {
   unsigned int diverged;            // per interval
   unsigned long long k1_reports;    // report_count after K1 (snapshot taken by the filter)
   unsigned long long lanes_final[8];
+  // Speculation (runtime.cu): the host queues interval k+1 before it has seen
+  // interval k's counters.  A4's last block sets `abort` when interval k needs
+  // the host (overflow, divergence, nothing left waiting); every kernel of an
+  // interval returns at entry while it is set, so a speculative interval
+  // leaves no trace.  The host clears it.  Never zeroed per interval.
+  unsigned int abort;
+  unsigned int bdone;               // A4 blocks finished (last-block pattern; self-resetting)
 };
 
 // Parameters of the interval interpreter (K1), passed by value.

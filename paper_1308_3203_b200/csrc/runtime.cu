@@ -113,7 +113,8 @@ struct rc_workspace {
   DevBuf reports, reports_scratch;
   DevBuf inst_tmp;  // node_min | node_max | first_tid | second_tid | inst_flag  ([I_b] each)
   DevBuf ctr;
-  DevCounters* h_ctr = nullptr;  // pinned
+  DevCounters* h_ctr = nullptr;  // pinned [4]: interval slots 0/1, synchronous reads 2, copy source 3
+  cudaEvent_t iv_done[2] = {nullptr, nullptr};  // interval k's counters landed in h_ctr[k & 1]
   SortWorkspace sort;
   Profiler prof;
   ~rc_workspace() {
@@ -122,6 +123,8 @@ struct rc_workspace {
                       &sort_small, &reports, &reports_scratch, &inst_tmp, &ctr})
       b->release();
     if (h_ctr) cudaFreeHost(h_ctr);
+    for (cudaEvent_t e : iv_done)
+      if (e) cudaEventDestroy(e);
   }
 };
 
@@ -262,7 +265,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     if (!P->live_regs.empty())
       CK(cudaMemcpy(W.live.p, P->live_regs.data(), P->live_regs.size(), cudaMemcpyHostToDevice));
     CK(W.ctr.ensure(sizeof(DevCounters)));
-    CK(cudaMallocHost(&W.h_ctr, sizeof(DevCounters)));
+    CK(cudaMallocHost(&W.h_ctr, 4 * sizeof(DevCounters)));
+    for (cudaEvent_t& e : W.iv_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CK(W.sort_small.ensure(4096 * 4));
     W.sort.hist = W.sort_small.as<uint32_t>();
     W.sort.bin_off = W.sort.hist + 1024;
@@ -348,13 +352,13 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   DevCounters* dctr = W.ctr.as<DevCounters>();
 
   auto read_ctr = [&]() -> cudaError_t {
-    cudaError_t e = cudaMemcpyAsync(W.h_ctr, dctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s);
+    cudaError_t e = cudaMemcpyAsync(&W.h_ctr[2], dctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return e;
     return cudaStreamSynchronize(s);
   };
   auto set_report_count = [&](uint64_t v) -> cudaError_t {
-    W.h_ctr->report_count = v;
-    return cudaMemcpyAsync(&dctr->report_count, &W.h_ctr->report_count, 8, cudaMemcpyHostToDevice, s);
+    W.h_ctr[3].report_count = v;  // slot 3: only ever a copy source
+    return cudaMemcpyAsync(&dctr->report_count, &W.h_ctr[3].report_count, 8, cudaMemcpyHostToDevice, s);
   };
   auto grow_reports = [&](uint64_t need) -> cudaError_t {
     cudaError_t e = W.reports.ensure(need * sizeof(rc_report) * 5 / 4, true, s);
@@ -407,189 +411,223 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       CK(cudaMemsetAsync(W.pc[cur].p, 0, (size_t)reg_stride * 4, s));
       CK(cudaMemsetAsync(W.regs[cur].p, 0, (size_t)reg_stride * P->n_regs * 4, s));  // registers start at 0 (L18)
     }
-    uint32_t k = 0;
-    for (;;) {
-      // One host sync per interval: K1 → filter → sort → detect → A4 are
-      // queued back to back (every kernel after K1 reads its record count from
-      // device memory).  Overflows are detected at the sync: a log or K1-report
-      // overflow makes filter/detect skip their work (the heap stays
-      // untouched) and the interval is re-run from the saved lane state; a
-      // detect-report overflow re-runs detect only (its commits are idempotent).
-      const uint64_t rep_before = rep_count;
+    // ---- one interval = K1 → filter → sort → detect → A4 (+ verdict), then
+    //      the counters to a pinned slot and an event.  No kernel needs a host
+    //      count (each reads its record count from device memory).
+    const uint32_t stage_warp =
+        P->rec_bound > 0 ? (uint32_t)std::min(256, ((32 * P->rec_bound + 31) / 32) * 32) : 256u;
+    const uint64_t* sr = nullptr;  // sorted log of the last enqueued interval
+    auto detect_params = [&](uint32_t kk) {
+      DetectParams dp;
+      dp.recs = sr;
+      dp.wval = W.wval.as<int32_t>();
+      dp.n_lanes = L;
+      dp.n = n;
+      dp.n_records = (uint32_t)log_cap;  // upper bound; the kernel reads the exact count
+      dp.heap = W.heap.as<int32_t>();
+      dp.cpi = (uint32_t)std::max<uint64_t>(cpi, 1);
+      dp.cpi_magic = div_magic(dp.cpi);
+      dp.n_arrays = n_arrays;
+      dp.arr_off = W.arr_off.as<uint32_t>();
+      dp.interval = kk;
+      dp.inst_base = inst_base;
+      dp.reports = W.reports.as<rc_report>();
+      dp.report_cap = rep_cap;
+      dp.ctr = dctr;
+      return dp;
+    };
+    struct Marks { size_t m0 = 0, m1 = 0; };
+    auto enqueue_interval = [&](uint32_t kk, int cc, Marks* mk) -> cudaError_t {
+      cudaError_t e;
+#define EQ(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
+      if (cpi) EQ(cudaMemsetAsync(W.wmap.p, 0, (size_t)nb * cpi, s));  // write-set map of this interval
+      EQ(cudaMemsetAsync(dctr, 0, offsetof(DevCounters, report_count), s));
+      EQ(cudaMemsetAsync(W.sort.hist, 0, 4 * 256 * sizeof(uint32_t), s));  // the filter fuses the histograms
+      EQ(cudaMemsetAsync(&dctr->iv_loads, 0, offsetof(DevCounters, lanes_final) - offsetof(DevCounters, iv_loads), s));
       InterpParams ip;
-      size_t mark0 = 0;
-      const uint64_t* sr = nullptr;
-      if (cpi) CK(cudaMemsetAsync(W.wmap.p, 0, (size_t)nb * cpi, s));  // write-set map of this interval
-      auto detect_params = [&]() {
-        DetectParams dp;
-        dp.recs = sr;
-        dp.wval = W.wval.as<int32_t>();
-        dp.n_lanes = L;
-        dp.n = n;
-        dp.n_records = (uint32_t)log_cap;  // upper bound; the kernel reads the exact count
-        dp.heap = W.heap.as<int32_t>();
-        dp.cpi = (uint32_t)std::max<uint64_t>(cpi, 1);
-        dp.cpi_magic = div_magic(dp.cpi);
-        dp.n_arrays = n_arrays;
-        dp.arr_off = W.arr_off.as<uint32_t>();
-        dp.interval = k;
-        dp.inst_base = inst_base;
-        dp.reports = W.reports.as<rc_report>();
-        dp.report_cap = rep_cap;
-        dp.ctr = dctr;
-        return dp;
-      };
-      for (;;) {
-        CK(cudaMemsetAsync(dctr, 0, offsetof(DevCounters, report_count), s));
-        CK(cudaMemsetAsync(W.sort.hist, 0, 4 * 256 * sizeof(uint32_t), s));  // the filter fuses the histograms
-        CK(cudaMemsetAsync(&dctr->iv_loads, 0, offsetof(DevCounters, lanes_final) - offsetof(DevCounters, iv_loads), s));
-        ip.code = W.code.as<Ins>();
-        ip.n_instr = P->n_instr;
-        ip.n_regs = P->n_regs;
-        ip.n_arrays = n_arrays;
-        ip.n = n;
-        ip.n_magic = div_magic(n);
-        ip.n_lanes = L;
-        ip.cpi = (uint32_t)cpi;
-        ip.fuel = opt.fuel_per_interval;
-        ip.interval = k;
-        ip.inst_base = inst_base;
-        ip.arr_off = W.arr_off.as<uint32_t>();
-        ip.arr_size = W.arr_size.as<uint32_t>();
-        ip.heap = W.heap.as<int32_t>();
-        ip.reg_stride = reg_stride;
-        ip.regs_in = W.regs[cur].as<int32_t>();
-        ip.pc_in = W.pc[cur].as<uint32_t>();
-        ip.status_in = W.status[cur].as<uint8_t>();
-        ip.regs_out = W.regs[cur ^ 1].as<int32_t>();
-        ip.pc_out = W.pc[cur ^ 1].as<uint32_t>();
-        ip.status_out = W.status[cur ^ 1].as<uint8_t>();
-        ip.live = W.live.as<uint8_t>();
-        ip.n_live = (uint32_t)P->live_regs.size();
-        ip.ovl_cap = (uint32_t)P->ovl_cap;
-        ip.stage_warp = P->rec_bound > 0 ? (uint32_t)std::min(256, ((32 * P->rec_bound + 31) / 32) * 32) : 256u;
-        ip.node_min = node_min;
-        ip.node_max = node_max;
-        ip.stage = W.log_alt.as<uint64_t>();
-        ip.stage_cap = log_cap;
-        ip.wmap = W.wmap.as<uint8_t>();
-        ip.wval = W.wval.as<int32_t>();
-        ip.reports = W.reports.as<rc_report>();
-        ip.report_cap = rep_cap;
-        ip.ctr = dctr;
-        mark0 = W.prof.marks.size();
-        W.prof.cut();
-        W.prof.begin(s);
-        CK(launch_interp(ip, s));
-        W.prof.end(RC_PROF_INTERP, s, 0, L);
-        // ---- write-set filter: writes + reads of written cells, dense, with histograms
-        FilterParams fp;
-        fp.stage = W.log_alt.as<uint64_t>();
-        fp.wmap = W.wmap.as<uint8_t>();
-        fp.out = W.log.as<uint64_t>();
-        fp.hist = W.sort.hist;
-        fp.passes = passes;
-        fp.ctr = dctr;
-        fp.n_slots = (uint32_t)log_cap;  // upper bound; the kernel reads stage_count
-        fp.keep_all = (opt.flags & RC_OPT_KEEP_ALL_READS) != 0;
-        W.prof.begin(s);
-        CK(launch_filter(fp, s));
-        W.prof.end(RC_PROF_FILTER, s, 0, 0);
-        // ---- K3: onesweep sort of the kept records by cell
-        bool in_alt = false;
-        W.sort.alt = W.log_alt.as<uint64_t>();
-        CK(onesweep_sort(W.log.as<uint64_t>(), (uint32_t)log_cap, &dctr->kept_count, nullptr, key_bits, W.sort, s,
-                         &in_alt, W.prof.on ? &W.prof : nullptr, /*hist_ready=*/true));
-        sr = in_alt ? W.log_alt.as<uint64_t>() : W.log.as<uint64_t>();
-        // ---- K4+K5 detect + commit, A4 check
-        DetectParams dp = detect_params();
-        W.prof.begin(s);
-        CK(launch_detect(dp, s));
-        W.prof.end(RC_PROF_DETECT, s, 0, 0);
-        BoundaryParams bp = bparams(k);
-        bp.status = W.status[cur ^ 1].as<uint8_t>();
-        bp.pc = W.pc[cur ^ 1].as<uint32_t>();
-        W.prof.begin(s);
-        CK(launch_boundary(bp, s));  // consumes (and resets) K1's per-instance node ranges
-        W.prof.end(RC_PROF_BOUNDARY, s, (uint64_t)nb * 12, nb);
-        CK(read_ctr());  // the interval's only sync
-        if (W.h_ctr->ovl_overflow)
-          return fail(RC_ELIMIT,
-                      "a work-item wrote more than %d distinct cells in one barrier interval (instance batch at "
-                      "%u, interval %u)",
-                      P->ovl_cap, inst_base, k);
-        const uint64_t n_all = W.h_ctr->stage_count;  // staging slots reserved (records + padding)
-        const bool log_over = W.h_ctr->log_overflow != 0;  // a real record did not fit
-        const bool k1_rep_over = W.h_ctr->k1_reports > rep_cap;
-        if (log_over || k1_rep_over) {  // filter/detect skipped: grow and re-run the interval
-          if (log_over) {
-            const uint64_t want = std::min<uint64_t>(n_all + n_all / 4 + 1024, 0xFFFFFFFFull);
-            if (n_all > 0xFFFFFFFFull) return fail(RC_ELIMIT, "more than 2^32 access records in one interval");
-            CK(W.log.ensure(want * 8));
-            CK(W.log_alt.ensure(want * 8));
-            log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
-            CK(ensure_sort_status(log_cap));
-          }
-          if (k1_rep_over) CK(grow_reports(W.h_ctr->k1_reports));
-          CK(set_report_count(rep_before));
-          continue;
+      ip.code = W.code.as<Ins>();
+      ip.n_instr = P->n_instr;
+      ip.n_regs = P->n_regs;
+      ip.n_arrays = n_arrays;
+      ip.n = n;
+      ip.n_magic = div_magic(n);
+      ip.n_lanes = L;
+      ip.cpi = (uint32_t)cpi;
+      ip.fuel = opt.fuel_per_interval;
+      ip.interval = kk;
+      ip.inst_base = inst_base;
+      ip.arr_off = W.arr_off.as<uint32_t>();
+      ip.arr_size = W.arr_size.as<uint32_t>();
+      ip.heap = W.heap.as<int32_t>();
+      ip.reg_stride = reg_stride;
+      ip.regs_in = W.regs[cc].as<int32_t>();
+      ip.pc_in = W.pc[cc].as<uint32_t>();
+      ip.status_in = W.status[cc].as<uint8_t>();
+      ip.regs_out = W.regs[cc ^ 1].as<int32_t>();
+      ip.pc_out = W.pc[cc ^ 1].as<uint32_t>();
+      ip.status_out = W.status[cc ^ 1].as<uint8_t>();
+      ip.live = W.live.as<uint8_t>();
+      ip.n_live = (uint32_t)P->live_regs.size();
+      ip.ovl_cap = (uint32_t)P->ovl_cap;
+      ip.stage_warp = stage_warp;
+      ip.node_min = node_min;
+      ip.node_max = node_max;
+      ip.stage = W.log_alt.as<uint64_t>();
+      ip.stage_cap = log_cap;
+      ip.wmap = W.wmap.as<uint8_t>();
+      ip.wval = W.wval.as<int32_t>();
+      ip.reports = W.reports.as<rc_report>();
+      ip.report_cap = rep_cap;
+      ip.ctr = dctr;
+      mk->m0 = W.prof.marks.size();
+      W.prof.cut();
+      W.prof.begin(s);
+      EQ(launch_interp(ip, s));
+      W.prof.end(RC_PROF_INTERP, s, 0, L);
+      // ---- write-set filter: writes + reads of written cells, dense, with histograms
+      FilterParams fp;
+      fp.stage = W.log_alt.as<uint64_t>();
+      fp.wmap = W.wmap.as<uint8_t>();
+      fp.out = W.log.as<uint64_t>();
+      fp.hist = W.sort.hist;
+      fp.passes = passes;
+      fp.ctr = dctr;
+      fp.n_slots = (uint32_t)log_cap;  // upper bound; the kernel reads stage_count
+      fp.keep_all = (opt.flags & RC_OPT_KEEP_ALL_READS) != 0;
+      W.prof.begin(s);
+      EQ(launch_filter(fp, s));
+      W.prof.end(RC_PROF_FILTER, s, 0, 0);
+      // ---- K3: onesweep sort of the kept records by cell
+      bool in_alt = false;
+      W.sort.alt = W.log_alt.as<uint64_t>();
+      EQ(onesweep_sort(W.log.as<uint64_t>(), (uint32_t)log_cap, &dctr->kept_count, nullptr, key_bits, W.sort, s,
+                       &in_alt, W.prof.on ? &W.prof : nullptr, /*hist_ready=*/true));
+      sr = in_alt ? W.log_alt.as<uint64_t>() : W.log.as<uint64_t>();
+      // ---- K4+K5 detect + commit, A4 check + verdict
+      DetectParams dp = detect_params(kk);
+      W.prof.begin(s);
+      EQ(launch_detect(dp, s));
+      W.prof.end(RC_PROF_DETECT, s, 0, 0);
+      BoundaryParams bp = bparams(kk);
+      bp.status = W.status[cc ^ 1].as<uint8_t>();
+      bp.pc = W.pc[cc ^ 1].as<uint32_t>();
+      W.prof.begin(s);
+      EQ(launch_boundary(bp, s));  // consumes (and resets) K1's per-instance node ranges
+      W.prof.end(RC_PROF_BOUNDARY, s, (uint64_t)nb * 12, nb);
+      mk->m1 = W.prof.marks.size();
+      EQ(cudaMemcpyAsync(&W.h_ctr[kk & 1], dctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+      EQ(cudaEventRecord(W.iv_done[kk & 1], s));
+#undef EQ
+      return cudaSuccess;
+    };
+    auto clear_abort = [&]() { return cudaMemsetAsync(&dctr->abort, 0, sizeof(unsigned int), s); };
+
+    // Speculative pipeline: interval k+1 is queued before the host looks at
+    // interval k, so the GPU never waits for the host between intervals.  If
+    // k needs the host (overflow, divergence, or no lane left waiting), its
+    // verdict makes every kernel of k+1 return at entry; the host then acts
+    // and queues k+1 again.
+    uint32_t k = 0;
+    Marks mk_cur, mk_next;
+    CK(enqueue_interval(k, cur, &mk_cur));
+    for (;;) {
+      const uint64_t rep_before = rep_count;
+      const bool spec = (uint64_t)k + 1 < opt.max_intervals;
+      if (spec) CK(enqueue_interval(k + 1, cur ^ 1, &mk_next));
+      CK(cudaEventSynchronize(W.iv_done[k & 1]));
+      const DevCounters h = W.h_ctr[k & 1];  // interval k's counters
+      const bool next_aborted = h.abort != 0;
+      if (spec && next_aborted) W.prof.marks.resize(mk_next.m0);  // k+1 did nothing
+      if (h.ovl_overflow)
+        return fail(RC_ELIMIT,
+                    "a work-item wrote more than %d distinct cells in one barrier interval (instance batch at "
+                    "%u, interval %u)",
+                    P->ovl_cap, inst_base, k);
+      const uint64_t n_all = h.stage_count;  // staging slots reserved (records + padding)
+      const bool log_over = h.log_overflow != 0;  // a real record did not fit
+      const bool k1_rep_over = h.k1_reports > rep_cap;
+      if (log_over || k1_rep_over) {  // filter/detect skipped: grow and re-run the interval
+        if (log_over) {
+          const uint64_t want = std::min<uint64_t>(n_all + n_all / 4 + 1024, 0xFFFFFFFFull);
+          if (n_all > 0xFFFFFFFFull) return fail(RC_ELIMIT, "more than 2^32 access records in one interval");
+          CK(W.log.ensure(want * 8));
+          CK(W.log_alt.ensure(want * 8));
+          log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
+          CK(ensure_sort_status(log_cap));
         }
-        break;
+        if (k1_rep_over) CK(grow_reports(h.k1_reports));
+        CK(set_report_count(rep_before));
+        CK(clear_abort());
+        W.prof.marks.resize(mk_cur.m0);
+        CK(enqueue_interval(k, cur, &mk_cur));
+        continue;
       }
-      tot_loads += W.h_ctr->iv_loads;
-      tot_stores += W.h_ctr->iv_stores;
-      tot_instr += W.h_ctr->iv_instr;
-      const uint64_t Ns = W.h_ctr->kept_count, Nslots = W.h_ctr->stage_count;
-      const uint64_t rep_after_k1 = W.h_ctr->k1_reports;
-      const bool diverged = W.h_ctr->diverged != 0;
-      // detect reports overflowed: grow, re-run detect (idempotent commits)
-      while (W.h_ctr->report_count > rep_cap) {
-        CK(grow_reports(W.h_ctr->report_count));
-        CK(set_report_count(rep_after_k1));
-        DetectParams dp = detect_params();
-        CK(launch_detect(dp, s));
-        CK(read_ctr());
+      if (next_aborted) CK(clear_abort());  // k+1 (if queued) has drained as a no-op before this
+      tot_loads += h.iv_loads;
+      tot_stores += h.iv_stores;
+      tot_instr += h.iv_instr;
+      const uint64_t Ns = h.kept_count, Nslots = h.stage_count;
+      uint64_t rc = h.report_count;
+      // detect reports overflowed: grow, re-run detect (idempotent commits).  A
+      // speculative interval's counter reset may have run: restore the count.
+      if (rc > rep_cap) {
+        W.h_ctr[3].kept_count = Ns;
+        CK(cudaMemcpyAsync(&dctr->kept_count, &W.h_ctr[3].kept_count, 8, cudaMemcpyHostToDevice, s));
+        do {
+          CK(grow_reports(rc));
+          CK(set_report_count(h.k1_reports));
+          DetectParams dp = detect_params(k);
+          CK(launch_detect(dp, s));
+          CK(read_ctr());
+          rc = W.h_ctr[2].report_count;
+        } while (rc > rep_cap);
       }
-      if (diverged) {  // rare path: lane scans for the divergence report (idempotent)
-        const uint64_t before = W.h_ctr->report_count;
+      if (h.diverged) {  // rare path: lane scans for the divergence report (idempotent)
+        const uint64_t before = rc;
         for (;;) {
           BoundaryParams bp = bparams(k);
           bp.status = W.status[cur ^ 1].as<uint8_t>();
           bp.pc = W.pc[cur ^ 1].as<uint32_t>();
           CK(launch_divergence(bp, s));
           CK(read_ctr());
-          if (W.h_ctr->report_count <= rep_cap) break;
-          CK(grow_reports(W.h_ctr->report_count));
+          rc = W.h_ctr[2].report_count;
+          if (rc <= rep_cap) break;
+          CK(grow_reports(rc));
           CK(set_report_count(before));
         }
       }
-      rep_count = W.h_ctr->report_count;
+      rep_count = rc;
       if (W.prof.on) {  // exact record counts are known now: fix this interval's profile bytes
-        for (size_t i = mark0; i < W.prof.marks.size(); i++) {
+        for (size_t i = mk_cur.m0; i < mk_cur.m1; i++) {
           Profiler::Mark& m = W.prof.marks[i];
           if (m.cls == RC_PROF_SORT) { m.bytes = Ns * 16; m.items = Ns; }
           if (m.cls == RC_PROF_DETECT) { m.bytes = Ns * 8; m.items = Ns; }
-          if (m.cls == RC_PROF_FILTER) { m.bytes = Nslots * 8 + (W.h_ctr->staged_recs) + Ns * 8; m.items = Nslots; }
+          if (m.cls == RC_PROF_FILTER) { m.bytes = Nslots * 8 + h.staged_recs + Ns * 8; m.items = Nslots; }
         }
       }
       cur ^= 1;  // the interval's lane state becomes current
-      const bool any_waiting = W.h_ctr->any_waiting != 0;
-      if (!any_waiting) break;
+      if (!h.any_waiting) break;
       k++;
-      if (k >= opt.max_intervals) {  // instance-level FUEL (reading L17)
+      if (k >= opt.max_intervals) {  // instance-level FUEL (reading L17); nothing was speculated
         for (;;) {
           BoundaryParams bp = bparams(k);
           bp.status = W.status[cur].as<uint8_t>();
           bp.pc = W.pc[cur].as<uint32_t>();
           CK(launch_max_intervals(bp, s));
           CK(read_ctr());
-          if (W.h_ctr->report_count <= rep_cap) break;
-          CK(grow_reports(W.h_ctr->report_count));
+          if (W.h_ctr[2].report_count <= rep_cap) break;
+          CK(grow_reports(W.h_ctr[2].report_count));
           CK(set_report_count(rep_count));
         }
-        rep_count = W.h_ctr->report_count;
+        rep_count = W.h_ctr[2].report_count;
         k--;  // intervals executed = max_intervals
         break;
+      }
+      if (next_aborted) {
+        W.prof.marks.resize(std::min(W.prof.marks.size(), mk_next.m0));
+        CK(enqueue_interval(k, cur, &mk_cur));  // the speculative copy did nothing: queue it for real
+      } else {
+        mk_cur = mk_next;
       }
     }
     intervals_max = std::max<uint64_t>(intervals_max, (uint64_t)k + 1);
@@ -649,7 +687,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     stats->checked_accesses = tot_loads + tot_stores;
     stats->instructions = tot_instr;
     stats->intervals_max = intervals_max;
-    for (int i = 0; i < 8; i++) stats->lanes_final[i] = W.h_ctr->lanes_final[i];
+    for (int i = 0; i < 8; i++) stats->lanes_final[i] = W.h_ctr[2].lanes_final[i];
   }
   if (n_reports_total) *n_reports_total = rep_count;
   if (rep_count > capacity)

@@ -17,7 +17,7 @@ fname = ""
 line = None
 hdr = None
 for r in rows:
-    if len(r) >= 2 and r[0] == "File Name":
+    if len(r) >= 2 and r[0] in ("File Name", "File Path"):
         fname = r[1].split("/")[-1]
         continue
     if r and r[0] == "Line No":
