@@ -42,7 +42,7 @@ def launches(path):
         if len(r) <= mi:
             continue
         v = float(r[mi].replace(",", ""))
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(r[ui], 1.0)
+        v *= {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6}.get(r[ui], 1.0)
         a = agg[r[ki].split("(")[0]]
         a[0] += 1
         a[1] += v
