@@ -126,19 +126,17 @@ __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
   return v;
 }
 
-// heap load straight into pending slot K's register.  The four slots use
-// distinct (equivalent) L1 eviction hints so the compiler cannot merge the
-// slot branches into one load followed by moves — a move would wait for the
-// data and make the load blocking.
-template <int K>
-__device__ __forceinline__ int32_t ldg_slot(const int32_t* p) {
-  int32_t v;
-  if (K == 0) asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p));
-  else if (K == 1) asm volatile("ld.global.nc.L1::evict_normal.b32 %0, [%1];" : "=r"(v) : "l"(p));
-  else if (K == 2) asm volatile("ld.global.nc.L1::evict_last.b32 %0, [%1];" : "=r"(v) : "l"(p));
-  else asm volatile("ld.global.nc.L1::evict_unchanged.b32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
+// heap load as an asynchronous copy straight into the lane's destination
+// register in shared memory (LDGSTS): the lane keeps executing; it waits
+// (cp.async.wait_all) only before an instruction program.cpp flagged OP_WAIT
+// (one that may touch a register with an outstanding load) and at the end of
+// its interval.
+__device__ __forceinline__ void ld_async(int32_t* dst_smem, const int32_t* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst_smem))),
+               "l"(src)
+               : "memory");
 }
+__device__ __forceinline__ void ld_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __device__ __forceinline__ int32_t wadd(int32_t x, int32_t y) { return (int32_t)((uint32_t)x + (uint32_t)y); }
 
@@ -184,18 +182,18 @@ __device__ __forceinline__ void prefetch_lanes(const InterpParams& p, uint32_t t
 // Pre-decoded instruction (16 B, shared memory): register operands become word
 // offsets r*T into the [reg][thread] register file; LD/ST/SIZE fold in the
 // array's cell offset and size, BR its false target.
-//   x: op | aux(array id) << 8 | a*T << 16     y: b*T | c*T << 16
+//   x: op (bit 7 = OP_WAIT) | aux(array id) << 8 | a*T << 16     y: b*T | c*T << 16
 //   z: imm, or the array's cell offset (LD/ST), or size (SIZE)
 //   w: BR false target, or the array's size (LD/ST)
 __device__ __forceinline__ uint4 predecode(uint2 raw, int T, const uint32_t* s_off, const uint32_t* s_size) {
-  const uint32_t op = raw.x & 0xFF, a = (raw.x >> 8) & 0xFF, b = (raw.x >> 16) & 0xFF, c = raw.x >> 24;
+  const uint32_t op = raw.x & 0x7F, a = (raw.x >> 8) & 0xFF, b = (raw.x >> 16) & 0xFF, c = raw.x >> 24;
   uint4 e;
   uint32_t aux = 0, z = raw.y, w = 0;
   if (op == RC_OP_LD) { aux = b; z = s_off[b]; w = s_size[b]; }
   else if (op == RC_OP_ST) { aux = a; z = s_off[a]; w = s_size[a]; }
   else if (op == RC_OP_SIZE) { z = s_size[b]; }
   else if (op == RC_OP_BR) { w = b + 256u * c; }
-  e.x = op | (aux << 8) | ((a * (uint32_t)T) << 16);
+  e.x = (raw.x & 0xFF) | (aux << 8) | ((a * (uint32_t)T) << 16);  // op with its OP_WAIT bit
   e.y = (b * (uint32_t)T) | ((c * (uint32_t)T) << 16);
   e.z = z;
   e.w = w;
@@ -252,7 +250,7 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
 #define SSTAT(b) (sstat0 + (size_t)(b) * T)
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(q); q += 16;
   uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)W * p.stage_warp * 8;
-  uint4* s_code = reinterpret_cast<uint4*>(q); q += CODE_SMEM ? (size_t)p.n_instr * 16 : 0;
+  uint4* s_code = reinterpret_cast<uint4*>(q); q += CODE_SMEM ? (size_t)(p.n_instr + 1) * 16 : 0;  // + pad entry
   uint32_t* ocell = reinterpret_cast<uint32_t*>(q); q += (size_t)OV * T * 4;
   int32_t* oval = reinterpret_cast<int32_t*>(q); q += (size_t)OV * T * 4;
   uint32_t* s_off = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
@@ -267,8 +265,10 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
     s_size[a] = p.arr_size[a];
   }
   __syncthreads();  // s_off / s_size before the pre-decode
-  if (CODE_SMEM)
+  if (CODE_SMEM) {
     for (uint32_t i = t; i < p.n_instr; i += T) s_code[i] = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + i), T, s_off, s_size);
+    if (t == 0) s_code[p.n_instr] = make_uint4(0, 0, 0, 0);  // fetched ahead of the last pc, never executed
+  }
   for (uint32_t i = t; i < p.n_live; i += T) s_live[i] = p.live[i];
   const uint32_t n_tiles0 = (p.n_lanes + T - 1) / T;
   if (t == 0) {
@@ -319,43 +319,38 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
     int32_t* Rg = SREGS(cur) + t;  // register r of this lane = Rg[r*T] (live ones arrived by TMA)
 
     if (running) status = L_RUNNING;
-    // non-blocking loads: up to NP issued LDs whose destination register is
-    // written back only when an instruction touches it (software scoreboard)
-    constexpr int NP = 4;
-    int32_t pv[NP];
-    uint32_t pr[NP];  // destination word offset, or NOREG
-    constexpr uint32_t NOREG = 0xFFFFFFFFu;
-#pragma unroll
-    for (int j = 0; j < NP; j++) { pr[j] = NOREG; pv[j] = 0; }
     int n_own = 0;
     unsigned long long steps = 0;
     uint32_t nloads = 0, nstores = 0;
     bool ovl_over = false;
     Stage S{st_recs + (size_t)warp * p.stage_warp, 0, p.stage_warp};
 
-    uint32_t npend = 0;  // occupied pending-load slots of this lane
+    // the instruction after the last executed one is fetched one step ahead
+    // (straight-line code: the next minimum pc is pc + 1), off the critical path
+    uint32_t pnext = 0xFFFFFFFFu;
+    uint4 enext = make_uint4(0, 0, 0, 0);
     for (;;) {
       const uint32_t minpc = __reduce_min_sync(FULL, running ? pc : 0xFFFFFFFFu);
       if (minpc == 0xFFFFFFFFu) break;  // no lane of the warp is running (pcs are < 65536)
       bool ex = running && pc == minpc;
-      const uint4 e = CODE_SMEM ? s_code[minpc]
-                                : predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + minpc), T, s_off, s_size);
-      const uint32_t op = e.x & 0xFF, aux = (e.x >> 8) & 0xFF;
+      uint4 e;
+      if (CODE_SMEM) {
+        e = enext;
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.u32 p, %4, %5;\n @p ld.shared.v4.u32 {%0, %1, %2, %3}, [%6];\n}\n"
+            : "+r"(e.x), "+r"(e.y), "+r"(e.z), "+r"(e.w)
+            : "r"(minpc), "r"(pnext), "r"(smem_u32(s_code + minpc)));
+        enext = s_code[minpc + 1];
+        pnext = minpc + 1;
+      } else {
+        e = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + minpc), T, s_off, s_size);
+      }
+      const uint32_t op = e.x & 0x7F, aux = (e.x >> 8) & 0xFF;
       int32_t* const Ra = Rg + (e.x >> 16);  // register operands of this lane
       int32_t* const Rb = Rg + (e.y & 0xFFFF);
       int32_t* const Rc = Rg + (e.y >> 16);
       const int32_t imm = (int32_t)e.z;
-      if (__any_sync(FULL, ex && npend)) {
-        // an instruction touching a pending register materialises it first
-        const uint32_t oa = e.x >> 16, ob = e.y & 0xFFFF, oc = e.y >> 16;
-#pragma unroll
-        for (int j = 0; j < NP; j++)
-          if (ex && pr[j] != NOREG && (pr[j] == oa || pr[j] == ob || pr[j] == oc)) {
-            Rg[pr[j]] = pv[j];
-            pr[j] = NOREG;
-            npend--;
-          }
-      }
+      if (e.x & OP_WAIT) ld_async_wait();  // warp-uniform
       if (ex) {  // fuel check before executing (reading L17)
         if (steps == p.fuel) {
           emit_report(p, inst, -1, (int32_t)pc, tid, RC_FUEL);
@@ -426,24 +421,8 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
               bool found = false;
               for (int j = 0; j < n_own; j++)
                 if (ocell[j * T + t] == cell) { v = oval[j * T + t]; found = true; }
-              if (found) {
-                *Ra = v;
-              } else {  // issue the load; write the register back later
-                if (npend == NP) {  // all busy: retire
-#pragma unroll
-                  for (int j = 0; j < NP; j++) { Rg[pr[j]] = pv[j]; pr[j] = NOREG; }
-                  npend = 0;
-                }
-                const int32_t* const src = p.heap + cell;
-                const uint32_t oa = e.x >> 16;
-                // first free slot; each branch loads straight into its slot's
-                // register (a runtime-selected move would wait for the data)
-                if (pr[0] == NOREG) { pv[0] = ldg_slot<0>(src); pr[0] = oa; }
-                else if (pr[1] == NOREG) { pv[1] = ldg_slot<1>(src); pr[1] = oa; }
-                else if (pr[2] == NOREG) { pv[2] = ldg_slot<2>(src); pr[2] = oa; }
-                else { pv[3] = ldg_slot<3>(src); pr[3] = oa; }
-                npend++;
-              }
+              if (found) *Ra = v;
+              else ld_async(Ra, p.heap + cell);
               pc++;
               nloads++;
               ok = true;
@@ -504,10 +483,7 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
     }
 
     IPHASE(2);
-    // retire the pending loads (registers of suspended lanes are saved below)
-#pragma unroll
-    for (int j = 0; j < NP; j++)
-      if (pr[j] != NOREG) Rg[pr[j]] = pv[j];
+    ld_async_wait();  // registers of suspended lanes are saved below
 
     // write records: one per distinct written cell; its final value (reading
     // L3) goes to the side table wval[slot][lane] read by detect
@@ -639,7 +615,7 @@ size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem) {
   size_t b = (size_t)2 * p.n_regs * T * 4;         // register files (double-buffered)
   b += (size_t)2 * T * 5 + 16;                     // status / pc rows, mbarriers
   b += (size_t)W * p.stage_warp * 8;                    // staging
-  b += code_in_smem ? (size_t)p.n_instr * 16 : 0;  // pre-decoded program
+  b += code_in_smem ? (size_t)(p.n_instr + 1) * 16 : 0;  // pre-decoded program + pad entry
   b += (size_t)p.ovl_cap * T * 8;                  // overlay
   b += (size_t)p.n_arrays * 8;                     // array offsets / sizes
   b += ((size_t)p.n_live + 3) & ~size_t(3);        // live register list

@@ -131,6 +131,13 @@ int validate(const uint8_t* bc, size_t nbytes, rc_program* P) {
 //     barrier-free cycle contains a ST).  Sizes the own-write overlay.
 // (3) Bound on log records per work-item per interval (LD executions + (2)),
 //     sizing the per-warp staging buffer (overflow is handled either way).
+// (4) K1 issues every heap LD as an asynchronous copy (cp.async) straight into
+//     the destination register and waits for its outstanding copies only
+//     before an instruction that may read or write a register some pending
+//     load targets: a forward may-analysis of pending load targets; an
+//     instruction flagged OP_WAIT empties the set, BAR / EXIT end the interval
+//     (the lane waits for everything there).  The flag travels in the device
+//     copy of the program (dev_code).
 static void successors(const Ins& I, uint32_t pc, uint32_t n_instr, uint32_t* s, int* ns) {
   *ns = 0;
   if (I.op == RC_OP_EXIT) return;
@@ -274,6 +281,49 @@ void analyze(rc_program* P) {
   const int64_t rec = max_path_weight(P, wrec);
   P->ovl_cap = (st < 0 || st > OVL_CAP) ? OVL_CAP : (int)std::max<int64_t>(st, 1);
   P->rec_bound = (rec < 0 || rec > 1024) ? -1 : (int)rec;
+  // (4) asynchronous loads: pend[pc] = registers that may still be the target
+  //     of an LD issued (and not yet waited on) when pc is reached.
+  //     Outer loop: pend is the least fixpoint for the current wait flags; a
+  //     flag is added wherever the instruction touches a pending register,
+  //     until no flag changes (flags only grow, so this terminates).
+  std::vector<uint64_t> pend(N * (size_t)words, 0);
+  std::vector<uint8_t> wait(N, 0);
+  auto touches_pending = [&](uint32_t pc) {
+    int use[3], nu, def;
+    uses_defs(P->code[pc], use, &nu, &def);
+    const uint64_t* in = &pend[pc * (size_t)words];
+    bool w = def >= 0 && (in[def / 64] >> (def % 64) & 1);
+    for (int j = 0; j < nu; j++) w = w || (in[use[j] / 64] >> (use[j] % 64) & 1);
+    return w;
+  };
+  for (bool grew = true; grew;) {
+    std::fill(pend.begin(), pend.end(), 0ull);
+    for (changed = true; changed;) {
+      changed = false;
+      for (uint32_t pc = 0; pc < N; pc++) {
+        const Ins& I = P->code[pc];
+        if (I.op == RC_OP_BAR || I.op == RC_OP_EXIT) continue;  // the lane waits at the end of its interval
+        std::vector<uint64_t> out(words, 0);
+        if (!wait[pc])
+          for (uint32_t k = 0; k < words; k++) out[k] = pend[pc * (size_t)words + k];
+        if (I.op == RC_OP_LD) out[I.a / 64] |= 1ull << (I.a % 64);
+        uint32_t s[2];
+        int ns;
+        successors(I, pc, N, s, &ns);
+        for (int j = 0; j < ns; j++)
+          for (uint32_t k = 0; k < words; k++) {
+            uint64_t& d = pend[s[j] * (size_t)words + k];
+            if ((d | out[k]) != d) { d |= out[k]; changed = true; }
+          }
+      }
+    }
+    grew = false;
+    for (uint32_t pc = 0; pc < N; pc++)
+      if (!wait[pc] && touches_pending(pc)) { wait[pc] = 1; grew = true; }
+  }
+  P->dev_code = P->code;
+  for (uint32_t pc = 0; pc < N; pc++)
+    if (wait[pc]) P->dev_code[pc].op |= OP_WAIT;
 }
 
 }  // namespace rc

@@ -23,6 +23,9 @@ struct Ins {  // 8-byte RCB1 instruction, include/rc.h
   int32_t imm;
 };
 static_assert(sizeof(Ins) == 8, "instruction is 8 bytes");
+// device copy of the program only: the instruction may touch a register with an
+// outstanding asynchronous load (program.cpp analyze() (4)); opcodes are < 0x80
+constexpr uint8_t OP_WAIT = 0x80;
 
 // work-item status (lane.status), DESIGN.md §5
 enum LaneStatus : uint8_t {
@@ -248,6 +251,7 @@ struct rc_program {
   uint32_t n_regs = 0, n_arrays = 0, n_instr = 0;
   std::vector<rc::Ins> code;
   // static analysis (program.cpp analyze()): sizing only, no semantic effect
+  std::vector<rc::Ins> dev_code;    // code with OP_WAIT flags (uploaded for K1)
   std::vector<uint8_t> live_regs;  // registers live across a barrier (+ live at pc 0)
   int ovl_cap = rc::OVL_CAP;       // max distinct cells written per work-item per interval
   int rec_bound = -1;              // max log records per work-item per interval (-1 unbounded)

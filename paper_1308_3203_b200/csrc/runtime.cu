@@ -260,7 +260,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     P->ws->device = opt.device;
     rc_workspace& W = *P->ws;
     CK(W.code.ensure(P->code.size() * sizeof(Ins)));
-    CK(cudaMemcpy(W.code.p, P->code.data(), P->code.size() * sizeof(Ins), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(W.code.p, P->dev_code.data(), P->dev_code.size() * sizeof(Ins), cudaMemcpyHostToDevice));
     CK(W.live.ensure(std::max<size_t>(1, P->live_regs.size())));
     if (!P->live_regs.empty())
       CK(cudaMemcpy(W.live.p, P->live_regs.data(), P->live_regs.size(), cudaMemcpyHostToDevice));
