@@ -20,10 +20,25 @@
 #include "rc_internal.h"
 
 #ifndef SORT_LB
-#define SORT_LB 16
+#define SORT_LB 4
 #endif
 #ifndef SORT_EXP
 #define SORT_EXP 0
+#endif
+#ifndef SORT_MATCH  // in-tile digit matching: 0 fast paths + ballots, 1 ballots only (branch-free)
+#define SORT_MATCH 3
+#endif
+#ifndef SORT_RANK  // ranking: 0 per-round LDS/STS with __syncwarp, 1 leader atomicAdd + shuffle
+#define SORT_RANK 0
+#endif
+#ifndef SORT_BACKOFF  // ns to sleep before re-polling a look-back predecessor (0 = spin)
+#define SORT_BACKOFF 0
+#endif
+#ifndef SORT_EARLY_LB  // predecessors read right after publishing AGGREGATE (0 = none)
+#define SORT_EARLY_LB 0
+#endif
+#ifndef SORT_CLAIM_LATE  // 1: claim the next tile after the look-back, 0: one tile ahead
+#define SORT_CLAIM_LATE 1
 #endif
 #ifndef SORT_MINB  // resident blocks per SM of the persistent pass (smem: ~72 KB each)
 #define SORT_MINB 2
@@ -155,9 +170,11 @@ __global__ void __launch_bounds__(256) bin_offsets_kernel(const uint32_t* __rest
 template <int NBUF>
 struct SortSmem {
   uint64_t buf[NBUF][SORT_TILE];
-  uint16_t whist[WARPS][RADIX];  // per-warp digit counters (ranking; <= 512 per warp)
+  uint32_t whist[WARPS][RADIX];  // per-warp digit counters (ranking; <= 512 per warp)
+#if SORT_MATCH == 3
+  uint32_t wmask[3][WARPS][RADIX];  // per-warp digit lane masks (zero between uses)
+#endif
   uint32_t thist[2][RADIX];      // early tile counts (two copies: fewer atomic conflicts)
-  uint32_t tile_excl[RADIX];
   uint32_t glob_base[RADIX];
   uint32_t wt[WARPS];
   uint32_t tile[2];
@@ -223,6 +240,9 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
   const int dsh = REC_CELL_SHIFT + shift;
   uint32_t claimed = 0xFFFFFFFFu;  // thread 0: tile claimed ahead
 
+#if SORT_MATCH == 3
+  for (int i = t; i < 3 * WARPS * RADIX; i += SORT_THREADS) (&S.wmask[0][0][0])[i] = 0u;
+#endif
   if (t == 0) {
     for (int b = 0; b < 2; b++)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar[b])));
@@ -232,7 +252,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
     if (t0 < n_tiles) {
       tile_fetch(S.buf[0], &S.mbar[0], in + (uint64_t)t0 * SORT_TILE,
                  (uint32_t)umin64(SORT_TILE, n - (uint64_t)t0 * SORT_TILE));
-      if (PERSISTENT) claimed = atomicAdd(tile_ctr, 1u);
+      if (PERSISTENT && !SORT_CLAIM_LATE) claimed = atomicAdd(tile_ctr, 1u);
     }
     if (!PERSISTENT) S.tile[1] = 0xFFFFFFFFu;
   }
@@ -247,7 +267,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
     if (tile >= n_tiles) break;  // block-uniform
     // fetch the tile claimed last iteration into the other buffer (freed by
     // the __syncthreads that ended the previous iteration); claim the next
-    if (PERSISTENT && t == 0) {
+    if (PERSISTENT && !SORT_CLAIM_LATE && t == 0) {
       const uint32_t tn = claimed;
       S.tile[cur ^ 1] = tn;
       claimed = 0xFFFFFFFFu;
@@ -289,6 +309,26 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
 #if SORT_EXP == 2  // timing experiment only: no matching (wrong ranks)
         pm[j] = 1u << lane;
         (void)vm;
+#elif SORT_MATCH == 1
+        const unsigned valid = vm ? vm : __ballot_sync(FULL, dd < RADIX);
+        pm[j] = dd < RADIX ? match_digit(dd, valid) : 0u;
+#elif SORT_MATCH == 2
+        (void)vm;
+        pm[j] = __match_any_sync(FULL, dd);
+        if (dd >= RADIX) pm[j] = 0u;
+#elif SORT_MATCH == 3
+        // peers through shared-memory lane masks: three mask sets rotate so
+        // one __syncwarp per round suffices (set j%3 is cleared in round j+1,
+        // after that round's __syncwarp, and reused in round j+3)
+        (void)vm;
+        if (dd < RADIX) atomicOr(&S.wmask[j % 3][w][dd], 1u << lane);
+        __syncwarp();
+        const unsigned m = dd < RADIX ? S.wmask[j % 3][w][dd] : 0u;
+        if (j > 0) {
+          const uint32_t dp = DIGIT(j - 1);
+          if (dp < RADIX && lane == __ffs(pm[j - 1]) - 1) S.wmask[(j - 1) % 3][w][dp] = 0u;
+        }
+        pm[j] = m;
 #else
         // exact fast paths for the structured runs of access logs: a round
         // whose 32 digits are all equal, or strictly increasing by lane
@@ -305,6 +345,13 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
 #endif
       }
     }
+#if SORT_MATCH == 3
+    __syncwarp();
+    {
+      const uint32_t dp = DIGIT(SORT_ITEMS - 1);
+      if (dp < RADIX && lane == __ffs(pm[SORT_ITEMS - 1]) - 1) S.wmask[(SORT_ITEMS - 1) % 3][w][dp] = 0u;
+    }
+#endif
     PHASE_T(3);
     // early tile counts: one shared atomic per digit group, then publish AGGREGATE
 #pragma unroll
@@ -320,9 +367,31 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
     unsigned long long* my_status = status + (size_t)tile * RADIX + d;
     if (tile == 0) st_relaxed(my_status, FLAG_INC | ep | tile_cnt);
     else st_relaxed(my_status, FLAG_AGG | ep | tile_cnt);
+    const uint32_t excl_tile = block_excl_scan(tile_cnt, S.wt);  // tile-local start of digit d
+#if SORT_EARLY_LB
+    // first look-back round issued now; its latency hides behind rank + scatter
+    unsigned long long esw[SORT_EARLY_LB];
+#pragma unroll
+    for (int j = 0; j < SORT_EARLY_LB; j++)
+      esw[j] = (int64_t)tile - 1 - j >= 0 ? ld_relaxed(status + (size_t)(tile - 1 - j) * RADIX + d) : 0ull;
+#endif
     PHASE_T(4);
 
     // ---- stable in-tile ranking (warp w owns items [w*512, w*512+512), striped)
+#if SORT_RANK == 1
+    // the round's leader adds the group size to the warp's digit counter and
+    // hands the previous count to its peers (the warp's shared-memory atomics
+    // execute in issue order, so rounds rank in order)
+#pragma unroll
+    for (int j = 0; j < SORT_ITEMS; j++) {
+      const uint32_t dd = DIGIT(j);
+      const int leader = __ffs(pm[j]) - 1;
+      uint32_t prev = 0;
+      if (dd < RADIX && lane == leader) prev = atomicAdd(&S.whist[w][dd], (uint32_t)__popc(pm[j]));
+      prev = __shfl_sync(FULL, prev, leader < 0 ? lane : leader);
+      pm[j] = prev + __popc(pm[j] & lanemask_lt());
+    }
+#else
 #pragma unroll
     for (int j = 0; j < SORT_ITEMS; j++) {
       const uint32_t dd = DIGIT(j);
@@ -330,22 +399,21 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
       uint32_t prev = 0;
       if (valid) prev = S.whist[w][dd];
       __syncwarp();
-      if (valid && lane == __ffs(pm[j]) - 1) S.whist[w][dd] = (uint16_t)(prev + __popc(pm[j]));
+      if (valid && lane == __ffs(pm[j]) - 1) S.whist[w][dd] = (prev + __popc(pm[j]));
       __syncwarp();
       pm[j] = prev + __popc(pm[j] & lanemask_lt());
     }
+#endif
     __syncthreads();
-    {  // per digit: warp-exclusive prefix, tile-local digit offsets
-      uint32_t run = 0;
+    {  // per digit: tile-local start of each warp's items of digit d
+      uint32_t run = excl_tile;
 #pragma unroll
       for (int ww = 0; ww < WARPS; ww++) {
         const uint32_t c = S.whist[ww][d];
-        S.whist[ww][d] = (uint16_t)run;
+        S.whist[ww][d] = run;
         run += c;
       }
     }
-    const uint32_t excl_tile = block_excl_scan(tile_cnt, S.wt);
-    S.tile_excl[d] = excl_tile;
     __syncthreads();
     PHASE_T(5);
 
@@ -353,7 +421,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
 #pragma unroll
     for (int j = 0; j < SORT_ITEMS; j++) {
       const uint32_t dd = DIGIT(j);
-      if (dd < RADIX) B[S.tile_excl[dd] + S.whist[w][dd] + pm[j]] = k[j];
+      if (dd < RADIX) B[S.whist[w][dd] + pm[j]] = k[j];
     }
 #undef DIGIT
     PHASE_T(6);
@@ -365,6 +433,17 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
       constexpr int LB = SORT_LB;  // predecessors per L2 round trip
       int64_t tp = (int64_t)tile - 1;
       bool done = false;
+#if SORT_EARLY_LB
+#pragma unroll
+      for (int j = 0; j < SORT_EARLY_LB; j++) {
+        if (done) break;
+        const bool ready = ((esw[j] >> 40) & 0x3FFFFF) == (epoch & 0x3FFFFF) && (esw[j] >> 62) != 0;
+        if (!ready) break;
+        excl += esw[j] & VAL_MASK;
+        tp--;
+        if ((esw[j] >> 62) == 2) done = true;
+      }
+#endif
       while (!done) {
         unsigned long long sw[LB];
 #pragma unroll
@@ -373,7 +452,12 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
         for (int j = 0; j < LB; j++) {
           if (done) break;
           const bool ready = ((sw[j] >> 40) & 0x3FFFFF) == (epoch & 0x3FFFFF) && (sw[j] >> 62) != 0;
-          if (!ready) break;  // re-poll from this predecessor
+          if (!ready) {  // re-poll from this predecessor
+#if SORT_BACKOFF
+            __nanosleep(SORT_BACKOFF);
+#endif
+            break;
+          }
           excl += sw[j] & VAL_MASK;
           tp--;
           if ((sw[j] >> 62) == 2) done = true;
@@ -382,6 +466,18 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
       st_relaxed(my_status, FLAG_INC | ep | (excl + tile_cnt));
     }
     S.glob_base[d] = (uint32_t)(bin_off[d] + excl) - excl_tile;
+#if SORT_CLAIM_LATE
+    // claim the next tile only now (its AGGREGATE follows within a few
+    // thousand cycles, so successors' look-backs never wait on a tile claimed
+    // long before it is processed); its TMA load overlaps the write-out
+    if (PERSISTENT && t == 0) {
+      const uint32_t tn = atomicAdd(tile_ctr, 1u);
+      S.tile[cur ^ 1] = tn;
+      if (tn < n_tiles)
+        tile_fetch(S.buf[(cur ^ 1) % NB], &S.mbar[cur ^ 1], in + (uint64_t)tn * SORT_TILE,
+                   (uint32_t)umin64(SORT_TILE, n - (uint64_t)tn * SORT_TILE));
+    }
+#endif
     __syncthreads();
     PHASE_T(7);
 
