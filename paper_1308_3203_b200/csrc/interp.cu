@@ -37,6 +37,9 @@
 // global "some lane is suspended" flag.
 #include "rc_internal.h"
 
+#ifndef LS_NB  // lane-state buffers (TMA prefetch pipeline depth + 1)
+#define LS_NB 2
+#endif
 #ifndef INTERP_MIN_BLOCKS
 #define INTERP_MIN_BLOCKS 3
 #endif
@@ -239,16 +242,18 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
 
   // ---- shared memory carve-up (sizes mirrored in interp_smem_bytes)
   unsigned char* q = smem;
-  // register files [reg][thread], status and pc rows, double-buffered (TMA);
+  // register files [reg][thread], status and pc rows, NB-buffered (TMA: the
+  // next tile's state lands while this one runs; a buffer is refilled only
+  // after the bulk stores of its tile two steps back have read it);
   // buffer b is addressed arithmetically from these bases (a runtime-indexed
   // array of pointers would lose the shared address space)
-  int32_t* const sregs0 = reinterpret_cast<int32_t*>(q); q += (size_t)2 * R * T * 4;
-  uint32_t* const spc0 = reinterpret_cast<uint32_t*>(q); q += (size_t)2 * T * 4;
-  uint8_t* const sstat0 = reinterpret_cast<uint8_t*>(q); q += (size_t)2 * T;
+  int32_t* const sregs0 = reinterpret_cast<int32_t*>(q); q += (size_t)LS_NB * R * T * 4;
+  uint32_t* const spc0 = reinterpret_cast<uint32_t*>(q); q += (size_t)LS_NB * T * 4;
+  uint8_t* const sstat0 = reinterpret_cast<uint8_t*>(q); q += (size_t)LS_NB * T;
 #define SREGS(b) (sregs0 + (size_t)(b) * R * T)
 #define SPC(b) (spc0 + (size_t)(b) * T)
 #define SSTAT(b) (sstat0 + (size_t)(b) * T)
-  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(q); q += 16;
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(q); q += (8 * LS_NB + 15) & ~15;
   uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)W * p.stage_warp * 8;
   uint4* s_code = reinterpret_cast<uint4*>(q); q += CODE_SMEM ? (size_t)(p.n_instr + 1) * 16 : 0;  // + pad entry
   uint32_t* ocell = reinterpret_cast<uint32_t*>(q); q += (size_t)OV * T * 4;
@@ -272,8 +277,7 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
   for (uint32_t i = t; i < p.n_live; i += T) s_live[i] = p.live[i];
   const uint32_t n_tiles0 = (p.n_lanes + T - 1) / T;
   if (t == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[0])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[1])));
+    for (int b = 0; b < LS_NB; b++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[b])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -288,18 +292,22 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
   uint32_t c_used = 0, c_cap = 0;
   const uint32_t n_tiles = (p.n_lanes + T - 1) / T;
 
+  uint32_t a4_inst = 0xFFFFFFFFu;  // arrival-node range this warp pushed (warp-uniform)
+  int32_t a4_lo = 0, a4_hi = 0;
+  unsigned long long b_staged = 0;  // thread 0: records staged by the block
   uint32_t parity = 0;  // bit b: expected phase of mbar[b]
   int cur = 0;
 #ifdef INTERP_PHASE_TIMING
   long long tprev_ = clock64();
 #endif
-  for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, cur ^= 1) {
-    // prefetch the next tile's lane state into the other buffer once the bulk
-    // stores of its previous use have finished reading it
+  for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, cur = cur + 1 == LS_NB ? 0 : cur + 1) {
+    // prefetch the next tile's lane state into the next buffer once the bulk
+    // stores of its previous use (LS_NB - 1 tiles back) have read it
     if (t == 0 && tile + gridDim.x < n_tiles) {
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      prefetch_lanes(p, tile + gridDim.x, T, SSTAT(cur ^ 1), SPC(cur ^ 1), SREGS(cur ^ 1), s_live,
-                     &mbar[cur ^ 1]);
+      const int nx = cur + 1 == LS_NB ? 0 : cur + 1;
+      if (LS_NB == 2) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      prefetch_lanes(p, tile + gridDim.x, T, SSTAT(nx), SPC(nx), SREGS(nx), s_live, &mbar[nx]);
     }
     IPHASE(0);
     mbar_wait_parity(&mbar[cur], (parity >> cur) & 1u);
@@ -510,9 +518,17 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
       // nodes are >= -1; bias by 1 so unsigned reductions apply
       const uint32_t nmin = __reduce_min_sync(FULL, arrived ? (uint32_t)(node + 1) : 0xFFFFFFFFu);
       const uint32_t nmax = __reduce_max_sync(FULL, arrived ? (uint32_t)(node + 1) : 0u);
-      if (lane == 0 && nmin != 0xFFFFFFFFu) {
-        atomicMin(p.node_min + inst0, (int32_t)(nmin - 1));
-        atomicMax(p.node_max + inst0, (int32_t)(nmax - 1));
+      // push only what widens the range this warp already pushed for the
+      // instance (min/max atomics are idempotent): ~one pair per warp and
+      // instance instead of one per tile
+      const int32_t lo_ = (int32_t)(nmin - 1), hi_ = (int32_t)(nmax - 1);
+      if (nmin != 0xFFFFFFFFu && !(inst0 == a4_inst && lo_ >= a4_lo && hi_ <= a4_hi)) {
+        if (inst0 != a4_inst) { a4_inst = inst0; a4_lo = lo_; a4_hi = hi_; }
+        else { a4_lo = min(a4_lo, lo_); a4_hi = max(a4_hi, hi_); }
+        if (lane == 0) {
+          atomicMin(p.node_min + inst0, lo_);
+          atomicMax(p.node_max + inst0, hi_);
+        }
       }
     } else if (arrived) {  // small work-groups: per-lane atomics
       atomicMin(p.node_min + inst, node);
@@ -550,7 +566,7 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
           c_used = 0;
           c_cap = sz;
         }
-        atomicAdd(&p.ctr->staged_recs, (unsigned long long)tot);  // fire-and-forget
+        b_staged += tot;
       }
       const unsigned long long cb = __shfl_sync(FULL, c_base + c_used, 0);
       if (lane < W) wbase[lane] = cb + x - c;
@@ -585,7 +601,10 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
     IPHASE(7);
   }
 
-  if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // lane-state stores complete
+  if (t == 0) {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // lane-state stores complete
+    if (b_staged) atomicAdd(&p.ctr->staged_recs, b_staged);
+  }
   // ---- block flush: sentinels in the last chunk's tail, statistics, flags
   if (t == 0) {
     wbase[W] = c_base + c_used;
@@ -612,8 +631,8 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
 
 size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem) {
   const int W = T / 32;
-  size_t b = (size_t)2 * p.n_regs * T * 4;         // register files (double-buffered)
-  b += (size_t)2 * T * 5 + 16;                     // status / pc rows, mbarriers
+  size_t b = (size_t)LS_NB * p.n_regs * T * 4;     // register files (LS_NB buffers)
+  b += (size_t)LS_NB * T * 5 + ((8 * LS_NB + 15) & ~15);  // status / pc rows, mbarriers
   b += (size_t)W * p.stage_warp * 8;                    // staging
   b += code_in_smem ? (size_t)(p.n_instr + 1) * 16 : 0;  // pre-decoded program + pad entry
   b += (size_t)p.ovl_cap * T * 8;                  // overlay
