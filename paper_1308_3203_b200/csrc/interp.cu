@@ -35,6 +35,8 @@
 // node (BAR pc, or -1 for exit) of the lanes that arrived in this interval —
 // equal min and max means every arrival reached the same barrier — and a
 // global "some lane is suspended" flag.
+#include <type_traits>
+
 #include "rc_internal.h"
 
 #ifndef LS_NB  // lane-state buffers (TMA prefetch pipeline depth + 1)
@@ -229,7 +231,10 @@ void interp_phase_io(unsigned long long* out, bool reset) {
 #define IPHASE(i) do {} while (0)
 #endif
 
-template <bool CODE_SMEM>
+// FUEL: per-instruction fuel check (reading L17).  Off when the program's
+// longest barrier-free path (program.cpp analyze()) fits in the fuel, so no
+// work-item can run out in any interval.
+template <bool CODE_SMEM, bool FUEL>
 __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const InterpParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (p.ctr->abort) return;  // speculative interval (DevCounters::abort)
@@ -328,7 +333,8 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
 
     if (running) status = L_RUNNING;
     int n_own = 0;
-    unsigned long long steps = 0;
+    // instructions this lane executed in the interval (< 2^31 when !FUEL)
+    typename std::conditional<FUEL, unsigned long long, uint32_t>::type steps = 0;
     uint32_t nloads = 0, nstores = 0;
     bool ovl_over = false;
     Stage S{st_recs + (size_t)warp * p.stage_warp, 0, p.stage_warp};
@@ -359,7 +365,7 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
       int32_t* const Rc = Rg + (e.y >> 16);
       const int32_t imm = (int32_t)e.z;
       if (e.x & OP_WAIT) ld_async_wait();  // warp-uniform
-      if (ex) {  // fuel check before executing (reading L17)
+      if (FUEL && ex) {  // fuel check before executing (reading L17)
         if (steps == p.fuel) {
           emit_report(p, inst, -1, (int32_t)pc, tid, RC_FUEL);
           running = false;
@@ -369,6 +375,7 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
           steps++;
         }
       }
+      if (!FUEL) steps += ex;
       switch (op) {  // warp-uniform
         case RC_OP_CONST: if (ex) { *Ra = imm; pc++; } break;
         case RC_OP_MOV: if (ex) { *Ra = *Rb; pc++; } break;
@@ -648,7 +655,8 @@ cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
   static bool attr_set = false;
   static int nsm = 0;
   if (!attr_set) {
-    for (auto f : {interp_kernel<true>, interp_kernel<false>}) {
+    for (auto f : {interp_kernel<true, true>, interp_kernel<false, true>, interp_kernel<true, false>,
+                   interp_kernel<false, false>}) {
       cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       if (e != cudaSuccess) return e;
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -662,13 +670,13 @@ cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
   int T = 256;
   while (T > 32 && interp_smem_bytes(p, T, code_smem) > 96 * 1024) T >>= 1;
   const size_t sm = interp_smem_bytes(p, T, code_smem);
+  auto kern = code_smem ? (p.fuel_check ? interp_kernel<true, true> : interp_kernel<true, false>)
+                        : (p.fuel_check ? interp_kernel<false, true> : interp_kernel<false, false>);
   int per_sm = 1;
-  if (code_smem) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, interp_kernel<true>, T, sm);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, interp_kernel<false>, T, sm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, sm);
   const uint32_t tiles = (p.n_lanes + T - 1) / T;
   const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)std::max(1, per_sm) * nsm);
-  if (code_smem) interp_kernel<true><<<grid, T, sm, s>>>(p);
-  else interp_kernel<false><<<grid, T, sm, s>>>(p);
+  kern<<<grid, T, sm, s>>>(p);
   launched();
   return cudaGetLastError();
 }

@@ -130,7 +130,11 @@ int validate(const uint8_t* bc, size_t nbytes, rc_program* P) {
 //     number of ST executions on a barrier-free path (unbounded if a
 //     barrier-free cycle contains a ST).  Sizes the own-write overlay.
 // (3) Bound on log records per work-item per interval (LD executions + (2)),
-//     sizing the per-warp staging buffer (overflow is handled either way).
+//     sizing the per-warp staging buffer (overflow is handled either way),
+//     and on executed instructions per work-item per interval (every node of a
+//     barrier-free path, its final BAR / EXIT included): when it is <= the
+//     fuel no work-item can exhaust its fuel, so K1 skips the per-instruction
+//     check (the FUEL report cannot occur).
 // (4) K1 issues every heap LD as an asynchronous copy (cp.async) straight into
 //     the destination register and waits for its outstanding copies only
 //     before an instruction that may read or write a register some pending
@@ -281,6 +285,8 @@ void analyze(rc_program* P) {
   const int64_t rec = max_path_weight(P, wrec);
   P->ovl_cap = (st < 0 || st > OVL_CAP) ? OVL_CAP : (int)std::max<int64_t>(st, 1);
   P->rec_bound = (rec < 0 || rec > 1024) ? -1 : (int)rec;
+  const int64_t ins = max_path_weight(P, std::vector<int>(N, 1));
+  P->instr_bound = (ins < 0 || ins >= (1ll << 31)) ? -1 : ins;
   // (4) asynchronous loads: pend[pc] = registers that may still be the target
   //     of an LD issued (and not yet waited on) when pc is reached.
   //     Outer loop: pend is the least fixpoint for the current wait flags; a

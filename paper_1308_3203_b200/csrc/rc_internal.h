@@ -103,6 +103,7 @@ struct InterpParams {
   uint32_t n_lanes;           // I_b * n
   uint32_t cpi;               // cells per instance
   uint64_t fuel;
+  bool fuel_check;            // false: no work-item can exhaust its fuel (static bound <= fuel)
   uint32_t interval;
   uint32_t inst_base;         // global instance id of batch instance 0
   const uint32_t* arr_off;    // [n_arrays] cell offset of each array inside an instance
@@ -255,6 +256,7 @@ struct rc_program {
   std::vector<uint8_t> live_regs;  // registers live across a barrier (+ live at pc 0)
   int ovl_cap = rc::OVL_CAP;       // max distinct cells written per work-item per interval
   int rec_bound = -1;              // max log records per work-item per interval (-1 unbounded)
+  int64_t instr_bound = -1;        // max instructions per work-item per interval (-1 unbounded)
   std::mutex mu;
   rc_workspace* ws = nullptr;
 };

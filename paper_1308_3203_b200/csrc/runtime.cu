@@ -454,6 +454,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       ip.n_lanes = L;
       ip.cpi = (uint32_t)cpi;
       ip.fuel = opt.fuel_per_interval;
+      ip.fuel_check = P->instr_bound < 0 || (uint64_t)P->instr_bound > opt.fuel_per_interval;
       ip.interval = kk;
       ip.inst_base = inst_base;
       ip.arr_off = W.arr_off.as<uint32_t>();

@@ -191,6 +191,19 @@ b2:
     assert {5, 6, 7, 8} <= kinds
 
 
+@pytest.mark.parametrize("fuel", [1, 5, 8, 9, 10, 40])
+def test_fuel_around_static_bound(rc, fuel):
+    """Straight-line intervals (FIG1: the longest barrier-free path is
+    9 instructions, BAR / EXIT included): K1 drops the per-instruction fuel check
+    when that bound fits in the fuel (reading L17); FUEL reports must appear
+    exactly as the oracle's on both sides of the bound."""
+    ins = I.cfg1_inputs()
+    p, g, o = run_both(rc, K.FIG1, 8, ins, fuel=fuel)
+    assert_parity(g, o, ins)
+    has_fuel = any(t[4] == 7 for t in o.report_tuples())
+    assert has_fuel == (fuel < 9)
+
+
 def test_max_intervals(rc):
     src = (".arrays A\n tid r0\n addi r2, r0, 1\nloop:\n bar\n ld r1, A, r0\n addi r1, r1, 1\n st A, r0, r1\n"
            " br r2, loop, end\nend:\n exit")
