@@ -57,16 +57,15 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
-// (rare paths take explicit arguments so the kernel's parameter block is never
-// copied to local memory)
-__device__ __noinline__ void emit_report_(DevCounters* ctr, rc_report* reports, unsigned long long cap,
-                                          uint32_t instance, uint32_t interval, int32_t arr, int32_t idx,
+// rare path: reads what it needs from the kernel's parameter block through a
+// pointer (__grid_constant__), so the interpreter loop keeps none of it live
+__device__ __noinline__ void emit_report_(const InterpParams* pp, uint32_t inst, int32_t arr, int32_t idx,
                                           uint32_t t1, uint32_t kind) {
-  unsigned long long pos = atomicAdd(&ctr->report_count, 1ull);
-  if (pos < cap) {
+  unsigned long long pos = atomicAdd(&pp->ctr->report_count, 1ull);
+  if (pos < pp->report_cap) {
     rc_report r;
-    r.instance = instance;
-    r.interval = interval;
+    r.instance = pp->inst_base + inst;
+    r.interval = pp->interval;
     r.array = arr;
     r.index = idx;
     r.tid1 = t1;
@@ -74,11 +73,17 @@ __device__ __noinline__ void emit_report_(DevCounters* ctr, rc_report* reports, 
     r.kind = (uint16_t)kind;
     r.flags = 0;
     r.reserved = 0;
-    reports[pos] = r;
+    pp->reports[pos] = r;
   }
 }
-#define emit_report(p, inst, arr, idx, t1, kind) \
-  emit_report_((p).ctr, (p).reports, (p).report_cap, (p).inst_base + (inst), (p).interval, arr, idx, t1, kind)
+#define emit_report(p, inst, arr, idx, t1, kind) emit_report_(&(p), inst, arr, idx, t1, kind)
+
+// a value the compiler must keep in a register (loop invariants it would
+// otherwise re-derive from the parameter block every interpreter step)
+__device__ __forceinline__ uint32_t pin(uint32_t v) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(v));
+  return v;
+}
 
 struct Stage {
   uint64_t* recs;  // this warp's staging area
@@ -136,10 +141,8 @@ __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
 // (cp.async.wait_all) only before an instruction program.cpp flagged OP_WAIT
 // (one that may touch a register with an outstanding load) and at the end of
 // its interval.
-__device__ __forceinline__ void ld_async(int32_t* dst_smem, const int32_t* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst_smem))),
-               "l"(src)
-               : "memory");
+__device__ __forceinline__ void ld_async(uint32_t dst_smem, const int32_t* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst_smem), "l"(src) : "memory");
 }
 __device__ __forceinline__ void ld_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -184,25 +187,41 @@ __device__ __forceinline__ void prefetch_lanes(const InterpParams& p, uint32_t t
   }
 }
 
-// Pre-decoded instruction (16 B, shared memory): register operands become word
-// offsets r*T into the [reg][thread] register file; LD/ST/SIZE fold in the
-// array's cell offset and size, BR its false target.
-//   x: op (bit 7 = OP_WAIT) | aux(array id) << 8 | a*T << 16     y: b*T | c*T << 16
-//   z: imm, or the array's cell offset (LD/ST), or size (SIZE)
-//   w: BR false target, or the array's size (LD/ST)
-__device__ __forceinline__ uint4 predecode(uint2 raw, int T, const uint32_t* s_off, const uint32_t* s_size) {
+// shared-memory accesses through 32-bit shared-window addresses (the
+// register file, overlay and program are addressed once per tile, not
+// re-derived from generic pointers every step)
+__device__ __forceinline__ int32_t lds32(uint32_t a) {
+  int32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, int32_t v) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// Pre-decoded instruction (24 B, shared memory: a 16-B head and an 8-B tail
+// in two arrays).  Register operands become byte offsets r*T*4 into the
+// [reg][thread] register file; LD/ST/SIZE fold in the array's cell offset and
+// size, BR its false target.
+//   head.x: op (bit 7 = OP_WAIT) | aux(array id) << 8    head.y/z/w: a/b/c byte offsets
+//   tail.x: imm, or the array's cell offset (LD/ST), or size (SIZE)
+//   tail.y: BR false target, or the array's size (LD/ST)
+struct Dec {
+  uint4 h;
+  uint2 t;
+};
+__device__ __forceinline__ Dec predecode(uint2 raw, int T, const uint32_t* s_off, const uint32_t* s_size) {
   const uint32_t op = raw.x & 0x7F, a = (raw.x >> 8) & 0xFF, b = (raw.x >> 16) & 0xFF, c = raw.x >> 24;
-  uint4 e;
   uint32_t aux = 0, z = raw.y, w = 0;
   if (op == RC_OP_LD) { aux = b; z = s_off[b]; w = s_size[b]; }
   else if (op == RC_OP_ST) { aux = a; z = s_off[a]; w = s_size[a]; }
   else if (op == RC_OP_SIZE) { z = s_size[b]; }
   else if (op == RC_OP_BR) { w = b + 256u * c; }
-  e.x = (raw.x & 0xFF) | (aux << 8) | ((a * (uint32_t)T) << 16);  // op with its OP_WAIT bit
-  e.y = (b * (uint32_t)T) | ((c * (uint32_t)T) << 16);
-  e.z = z;
-  e.w = w;
-  return e;
+  const uint32_t rb = 4u * (uint32_t)T;  // bytes per register row
+  Dec d;
+  d.h = make_uint4((raw.x & 0xFF) | (aux << 8), a * rb, b * rb, c * rb);  // op keeps its OP_WAIT bit
+  d.t = make_uint2(z, w);
+  return d;
 }
 
 }  // namespace
@@ -235,7 +254,7 @@ void interp_phase_io(unsigned long long* out, bool reset) {
 // longest barrier-free path (program.cpp analyze()) fits in the fuel, so no
 // work-item can run out in any interval.
 template <bool CODE_SMEM, bool FUEL>
-__global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const InterpParams p) {
+__global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __grid_constant__ InterpParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (p.ctr->abort) return;  // speculative interval (DevCounters::abort)
   const int T = blockDim.x;
@@ -260,7 +279,8 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
 #define SSTAT(b) (sstat0 + (size_t)(b) * T)
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(q); q += (8 * LS_NB + 15) & ~15;
   uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)W * p.stage_warp * 8;
-  uint4* s_code = reinterpret_cast<uint4*>(q); q += CODE_SMEM ? (size_t)(p.n_instr + 1) * 16 : 0;  // + pad entry
+  uint4* s_code = reinterpret_cast<uint4*>(q); q += CODE_SMEM ? (size_t)(p.n_instr + 1) * 16 : 0;  // heads + pad entry
+  uint2* s_tail = reinterpret_cast<uint2*>(q); q += CODE_SMEM ? (size_t)(p.n_instr + 1) * 8 : 0;   // tails + pad
   uint32_t* ocell = reinterpret_cast<uint32_t*>(q); q += (size_t)OV * T * 4;
   int32_t* oval = reinterpret_cast<int32_t*>(q); q += (size_t)OV * T * 4;
   uint32_t* s_off = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
@@ -276,9 +296,17 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
   }
   __syncthreads();  // s_off / s_size before the pre-decode
   if (CODE_SMEM) {
-    for (uint32_t i = t; i < p.n_instr; i += T) s_code[i] = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + i), T, s_off, s_size);
-    if (t == 0) s_code[p.n_instr] = make_uint4(0, 0, 0, 0);  // fetched ahead of the last pc, never executed
+    for (uint32_t i = t; i < p.n_instr; i += T) {
+      const Dec d = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + i), T, s_off, s_size);
+      s_code[i] = d.h;
+      s_tail[i] = d.t;
+    }
+    if (t == 0) {  // fetched ahead of the last pc, never executed
+      s_code[p.n_instr] = make_uint4(0, 0, 0, 0);
+      s_tail[p.n_instr] = make_uint2(0, 0);
+    }
   }
+  const uint32_t code_h = pin(smem_u32(s_code)), code_t = pin(smem_u32(s_tail));
   for (uint32_t i = t; i < p.n_live; i += T) s_live[i] = p.live[i];
   const uint32_t n_tiles0 = (p.n_lanes + T - 1) / T;
   if (t == 0) {
@@ -329,7 +357,11 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
     const uint32_t inst = valid ? fast_div(g, p.n_magic) : 0;
     const uint32_t tid = valid ? g - inst * p.n : 0;
     const uint32_t cell_base = inst * p.cpi;
-    int32_t* Rg = SREGS(cur) + t;  // register r of this lane = Rg[r*T] (live ones arrived by TMA)
+    // byte address of this lane's register 0; register r is at rg + r*T*4
+    // (the live ones arrived by TMA)
+    const uint32_t rg = pin(smem_u32(SREGS(cur)) + 4u * (uint32_t)t);
+    const uint32_t oc = pin(smem_u32(ocell) + 4u * (uint32_t)t), ov = pin(smem_u32(oval) + 4u * (uint32_t)t);
+    const uint32_t orow = 4u * (uint32_t)T;  // overlay row stride (bytes)
 
     if (running) status = L_RUNNING;
     int n_own = 0;
@@ -342,29 +374,38 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
     // the instruction after the last executed one is fetched one step ahead
     // (straight-line code: the next minimum pc is pc + 1), off the critical path
     uint32_t pnext = 0xFFFFFFFFu;
-    uint4 enext = make_uint4(0, 0, 0, 0);
+    uint4 nh = make_uint4(0, 0, 0, 0);
+    uint2 nt = make_uint2(0, 0);
     for (;;) {
       const uint32_t minpc = __reduce_min_sync(FULL, running ? pc : 0xFFFFFFFFu);
       if (minpc == 0xFFFFFFFFu) break;  // no lane of the warp is running (pcs are < 65536)
       bool ex = running && pc == minpc;
-      uint4 e;
+      uint4 eh;
+      uint2 et;
       if (CODE_SMEM) {
-        e = enext;
+        eh = nh;
+        et = nt;
         asm volatile(
-            "{\n .reg .pred p;\n setp.ne.u32 p, %4, %5;\n @p ld.shared.v4.u32 {%0, %1, %2, %3}, [%6];\n}\n"
-            : "+r"(e.x), "+r"(e.y), "+r"(e.z), "+r"(e.w)
-            : "r"(minpc), "r"(pnext), "r"(smem_u32(s_code + minpc)));
-        enext = s_code[minpc + 1];
+            "{\n .reg .pred p;\n setp.ne.u32 p, %6, %7;\n"
+            " @p ld.shared.v4.u32 {%0, %1, %2, %3}, [%8];\n @p ld.shared.v2.u32 {%4, %5}, [%9];\n}\n"
+            : "+r"(eh.x), "+r"(eh.y), "+r"(eh.z), "+r"(eh.w), "+r"(et.x), "+r"(et.y)
+            : "r"(minpc), "r"(pnext), "r"(code_h + 16u * minpc), "r"(code_t + 8u * minpc)
+            : "memory");
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(nh.x), "=r"(nh.y), "=r"(nh.z), "=r"(nh.w)
+                     : "r"(code_h + 16u * minpc + 16u)
+                     : "memory");
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nt.x), "=r"(nt.y) : "r"(code_t + 8u * minpc + 8u) : "memory");
         pnext = minpc + 1;
       } else {
-        e = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + minpc), T, s_off, s_size);
+        const Dec d = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + minpc), T, s_off, s_size);
+        eh = d.h;
+        et = d.t;
       }
-      const uint32_t op = e.x & 0x7F, aux = (e.x >> 8) & 0xFF;
-      int32_t* const Ra = Rg + (e.x >> 16);  // register operands of this lane
-      int32_t* const Rb = Rg + (e.y & 0xFFFF);
-      int32_t* const Rc = Rg + (e.y >> 16);
-      const int32_t imm = (int32_t)e.z;
-      if (e.x & OP_WAIT) ld_async_wait();  // warp-uniform
+      const uint32_t op = eh.x & 0x7F;
+      const uint32_t ra = rg + eh.y, rb = rg + eh.z, rc = rg + eh.w;  // this lane's operand registers
+      const int32_t imm = (int32_t)et.x;
+      if (eh.x & OP_WAIT) ld_async_wait();  // warp-uniform
       if (FUEL && ex) {  // fuel check before executing (reading L17)
         if (steps == p.fuel) {
           emit_report(p, inst, -1, (int32_t)pc, tid, RC_FUEL);
@@ -376,16 +417,17 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
         }
       }
       if (!FUEL) steps += ex;
-      switch (op) {  // warp-uniform
-        case RC_OP_CONST: if (ex) { *Ra = imm; pc++; } break;
-        case RC_OP_MOV: if (ex) { *Ra = *Rb; pc++; } break;
-        case RC_OP_TID: if (ex) { *Ra = (int32_t)tid; pc++; } break;
-        case RC_OP_SIZE: if (ex) { *Ra = imm; pc++; } break;
-        case RC_OP_ADDI: if (ex) { *Ra = wadd(*Rb, imm); pc++; } break;
+      switch (op & 31) {  // warp-uniform; every value has a case: a bare jump table
+        case 0: case 28: case 29: case 30: case 31: break;  // unused (the validator rejects them)
+        case RC_OP_CONST: if (ex) { sts32(ra, imm); pc++; } break;
+        case RC_OP_MOV: if (ex) { sts32(ra, lds32(rb)); pc++; } break;
+        case RC_OP_TID: if (ex) { sts32(ra, (int32_t)tid); pc++; } break;
+        case RC_OP_SIZE: if (ex) { sts32(ra, imm); pc++; } break;
+        case RC_OP_ADDI: if (ex) { sts32(ra, wadd(lds32(rb), imm)); pc++; } break;
         case RC_OP_ADD: case RC_OP_SUB: case RC_OP_MUL: case RC_OP_MIN: case RC_OP_MAX: case RC_OP_AND:
         case RC_OP_OR: case RC_OP_XOR: case RC_OP_LT: case RC_OP_EQ: case RC_OP_LAND:
           if (ex) {
-            const int32_t x = *Rb, y = *Rc;
+            const int32_t x = lds32(rb), y = lds32(rc);
             int32_t v;
             switch (op) {
               case RC_OP_ADD: v = wadd(x, y); break;
@@ -400,13 +442,13 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
               case RC_OP_EQ: v = x == y; break;
               default: v = (x != 0) && (y != 0); break;
             }
-            *Ra = v;
+            sts32(ra, v);
             pc++;
           }
           break;
         case RC_OP_DIV: case RC_OP_MOD:
           if (ex) {
-            const int32_t x = *Rb, y = *Rc;
+            const int32_t x = lds32(rb), y = lds32(rc);
             if (y == 0) {
               emit_report(p, inst, -1, (int32_t)pc, tid, RC_DIV0);
               running = false;
@@ -415,29 +457,29 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
               int32_t v;
               if (op == RC_OP_DIV) v = (y == -1) ? (int32_t)(0u - (uint32_t)x) : x / y;
               else v = (y == -1) ? 0 : x % y;
-              *Ra = v;
+              sts32(ra, v);
               pc++;
             }
           }
           break;
-        case RC_OP_LNOT: if (ex) { *Ra = *Rb == 0; pc++; } break;
+        case RC_OP_LNOT: if (ex) { sts32(ra, lds32(rb) == 0); pc++; } break;
         case RC_OP_LD: {
           bool ok = false;
           uint32_t cell = 0;
           if (ex) {
-            const int32_t idx = *Rc;
-            if ((uint32_t)idx >= e.w) {  // also catches idx < 0
-              emit_report(p, inst, (int32_t)aux, idx, tid, RC_OOB);
+            const int32_t idx = lds32(rc);
+            if ((uint32_t)idx >= et.y) {  // also catches idx < 0
+              emit_report(p, inst, (int32_t)((eh.x >> 8) & 0xFF), idx, tid, RC_OOB);
               running = false;
               status = L_OOB;
             } else {
-              cell = cell_base + e.z + (uint32_t)idx;
+              cell = cell_base + et.x + (uint32_t)idx;
               int32_t v = 0;
               bool found = false;
               for (int j = 0; j < n_own; j++)
-                if (ocell[j * T + t] == cell) { v = oval[j * T + t]; found = true; }
-              if (found) *Ra = v;
-              else ld_async(Ra, p.heap + cell);
+                if ((uint32_t)lds32(oc + j * orow) == cell) { v = lds32(ov + j * orow); found = true; }
+              if (found) sts32(ra, v);
+              else ld_async(ra, p.heap + cell);
               pc++;
               nloads++;
               ok = true;
@@ -453,20 +495,20 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
         }
         case RC_OP_ST:
           if (ex) {
-            const int32_t idx = *Rb;
-            if ((uint32_t)idx >= e.w) {  // also catches idx < 0
-              emit_report(p, inst, (int32_t)aux, idx, tid, RC_OOB);
+            const int32_t idx = lds32(rb);
+            if ((uint32_t)idx >= et.y) {  // also catches idx < 0
+              emit_report(p, inst, (int32_t)((eh.x >> 8) & 0xFF), idx, tid, RC_OOB);
               running = false;
               status = L_OOB;
             } else {
-              const uint32_t cell = cell_base + e.z + (uint32_t)idx;
+              const uint32_t cell = cell_base + et.x + (uint32_t)idx;
               int j = 0;
-              while (j < n_own && ocell[j * T + t] != cell) j++;
+              while (j < n_own && (uint32_t)lds32(oc + j * orow) != cell) j++;
               if (j == n_own) {
-                if (n_own < (int)OV) { ocell[j * T + t] = cell; n_own++; }
+                if (n_own < (int)OV) { sts32(oc + j * orow, (int32_t)cell); n_own++; }
                 else { ovl_over = true; j = -1; }
               }
-              if (j >= 0) oval[j * T + t] = *Rc;
+              if (j >= 0) sts32(ov + j * orow, lds32(rc));
               pc++;
               nstores++;
             }
@@ -476,13 +518,13 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
         case RC_OP_EXIT: if (ex) { running = false; status = L_EXITED_NOW; } break;
         case RC_OP_ASSUME:
           if (ex) {
-            if (*Ra == 0) { running = false; status = L_PRUNED; }
+            if (lds32(ra) == 0) { running = false; status = L_PRUNED; }
             else pc++;
           }
           break;
         case RC_OP_ASSERT:
           if (ex) {
-            if (*Ra == 0) {
+            if (lds32(ra) == 0) {
               emit_report(p, inst, -1, (int32_t)pc, tid, RC_ASSERT);
               running = false;
               status = L_ASSERT;
@@ -491,9 +533,8 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const In
             }
           }
           break;
-        case RC_OP_BR: if (ex) pc = *Ra != 0 ? (uint32_t)imm : e.w; break;
+        case RC_OP_BR: if (ex) pc = lds32(ra) != 0 ? (uint32_t)imm : et.y; break;
         case RC_OP_JMP: if (ex) pc = (uint32_t)imm; break;
-        default: break;  // unreachable: the validator rejects unknown opcodes
       }
     }
 
@@ -641,7 +682,7 @@ size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem) {
   size_t b = (size_t)LS_NB * p.n_regs * T * 4;     // register files (LS_NB buffers)
   b += (size_t)LS_NB * T * 5 + ((8 * LS_NB + 15) & ~15);  // status / pc rows, mbarriers
   b += (size_t)W * p.stage_warp * 8;                    // staging
-  b += code_in_smem ? (size_t)(p.n_instr + 1) * 16 : 0;  // pre-decoded program + pad entry
+  b += code_in_smem ? (size_t)(p.n_instr + 1) * 24 : 0;  // pre-decoded program + pad entry
   b += (size_t)p.ovl_cap * T * 8;                  // overlay
   b += (size_t)p.n_arrays * 8;                     // array offsets / sizes
   b += ((size_t)p.n_live + 3) & ~size_t(3);        // live register list

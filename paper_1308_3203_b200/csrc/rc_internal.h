@@ -180,7 +180,10 @@ struct SortWorkspace {
   size_t status_tiles = 0;
   uint32_t epoch = 0;              // look-back epoch (never reset memory)
 };
-constexpr int SORT_THREADS = 256;
+#ifndef SORT_THREADS_OPT
+#define SORT_THREADS_OPT 256
+#endif
+constexpr int SORT_THREADS = SORT_THREADS_OPT;  // >= 256 (one thread per digit for the per-digit steps)
 constexpr int SORT_ITEMS = 16;
 constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;
 size_t sort_tiles(size_t n);

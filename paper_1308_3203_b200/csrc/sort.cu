@@ -223,7 +223,7 @@ __device__ __forceinline__ unsigned match_digit(uint32_t d, unsigned valid_mask)
 // the hardware block scheduler staggers tiles, which keeps look-back walks
 // short) with a single buffer.
 template <bool PERSISTENT>
-__global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) onesweep_kernel(const uint64_t* __restrict__ in,
+__global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256 / SORT_THREADS) onesweep_kernel(const uint64_t* __restrict__ in,
                                                                    uint64_t* __restrict__ out, uint32_t n_host,
                                                                    const unsigned long long* n_a,
                                                                    const unsigned long long* n_b, int shift,
@@ -278,8 +278,10 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
       }
     }
     for (int i = t; i < WARPS * RADIX; i += SORT_THREADS) (&S.whist[0][0])[i] = 0;
-    S.thist[0][t] = 0;
-    S.thist[1][t] = 0;
+    if (t < RADIX) {
+      S.thist[0][t] = 0;
+      S.thist[1][t] = 0;
+    }
     const uint64_t base = (uint64_t)tile * SORT_TILE;
     const uint32_t cnt = (uint32_t)umin64(SORT_TILE, n - base);
     uint64_t* B = S.buf[cur % NB];
@@ -362,18 +364,22 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
 #endif
     }
     __syncthreads();
-    const int d = t;  // SORT_THREADS == RADIX
-    const uint32_t tile_cnt = S.thist[0][d] + S.thist[1][d];
+    // per-digit steps: thread d < RADIX owns digit d
+    const int d = t < RADIX ? t : RADIX - 1;
+    const bool dig = t < RADIX;
+    const uint32_t tile_cnt = dig ? S.thist[0][d] + S.thist[1][d] : 0u;
     unsigned long long* my_status = status + (size_t)tile * RADIX + d;
-    if (tile == 0) st_relaxed(my_status, FLAG_INC | ep | tile_cnt);
-    else st_relaxed(my_status, FLAG_AGG | ep | tile_cnt);
+    if (dig) {
+      if (tile == 0) st_relaxed(my_status, FLAG_INC | ep | tile_cnt);
+      else st_relaxed(my_status, FLAG_AGG | ep | tile_cnt);
+    }
     const uint32_t excl_tile = block_excl_scan(tile_cnt, S.wt);  // tile-local start of digit d
 #if SORT_EARLY_LB
     // first look-back round issued now; its latency hides behind rank + scatter
     unsigned long long esw[SORT_EARLY_LB];
 #pragma unroll
     for (int j = 0; j < SORT_EARLY_LB; j++)
-      esw[j] = (int64_t)tile - 1 - j >= 0 ? ld_relaxed(status + (size_t)(tile - 1 - j) * RADIX + d) : 0ull;
+      esw[j] = dig && (int64_t)tile - 1 - j >= 0 ? ld_relaxed(status + (size_t)(tile - 1 - j) * RADIX + d) : 0ull;
 #endif
     PHASE_T(4);
 
@@ -405,7 +411,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
     }
 #endif
     __syncthreads();
-    {  // per digit: tile-local start of each warp's items of digit d
+    if (dig) {  // per digit: tile-local start of each warp's items of digit d
       uint32_t run = excl_tile;
 #pragma unroll
       for (int ww = 0; ww < WARPS; ww++) {
@@ -429,7 +435,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
     // ---- look-back (after the scatter: predecessors had time to publish
     //      INCLUSIVE), then publish our INCLUSIVE prefix
     unsigned long long excl = 0;
-    if (tile > 0) {
+    if (tile > 0 && dig) {
       constexpr int LB = SORT_LB;  // predecessors per L2 round trip
       int64_t tp = (int64_t)tile - 1;
       bool done = false;
@@ -444,7 +450,13 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
         if ((esw[j] >> 62) == 2) done = true;
       }
 #endif
+#ifdef SORT_PHASE_TIMING
+      uint32_t st_rounds = 0, st_notready = 0, st_walk = 0;
+#endif
       while (!done) {
+#ifdef SORT_PHASE_TIMING
+        st_rounds++;
+#endif
         unsigned long long sw[LB];
 #pragma unroll
         for (int j = 0; j < LB; j++) sw[j] = tp - j >= 0 ? ld_relaxed(status + (size_t)(tp - j) * RADIX + d) : 0ull;
@@ -453,6 +465,9 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
           if (done) break;
           const bool ready = ((sw[j] >> 40) & 0x3FFFFF) == (epoch & 0x3FFFFF) && (sw[j] >> 62) != 0;
           if (!ready) {  // re-poll from this predecessor
+#ifdef SORT_PHASE_TIMING
+            st_notready++;
+#endif
 #if SORT_BACKOFF
             __nanosleep(SORT_BACKOFF);
 #endif
@@ -464,8 +479,18 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3) ones
         }
       }
       st_relaxed(my_status, FLAG_INC | ep | (excl + tile_cnt));
+#ifdef SORT_PHASE_TIMING
+      st_walk = (uint32_t)((int64_t)tile - 1 - tp);
+      {
+        uint32_t a = st_rounds, b = st_notready, c = st_walk;
+        for (int o = 16; o; o >>= 1) {
+          a += __shfl_xor_sync(FULL, a, o); b += __shfl_xor_sync(FULL, b, o); c += __shfl_xor_sync(FULL, c, o);
+        }
+        if (lane == 0) { atomicAdd(&g_phase_cycles[9], a); atomicAdd(&g_phase_cycles[10], b); atomicAdd(&g_phase_cycles[11], c); }
+      }
+#endif
     }
-    S.glob_base[d] = (uint32_t)(bin_off[d] + excl) - excl_tile;
+    if (dig) S.glob_base[d] = (uint32_t)(bin_off[d] + excl) - excl_tile;
 #if SORT_CLAIM_LATE
     // claim the next tile only now (its AGGREGATE follows within a few
     // thousand cycles, so successors' look-backs never wait on a tile claimed

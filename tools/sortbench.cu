@@ -106,6 +106,8 @@ int main(int argc, char** argv) {
   for (int i = 0; i < 9; i++) tot += ph[i];
   for (int i = 0; i < 9; i++)
     printf("  phase %-16s %9.0f cycles/tile (%.1f%%)\n", names[i], ph[i] / tiles, 100.0 * ph[i] / tot);
+  printf("  look-back per digit-tile: %.2f rounds, %.2f not-ready polls, %.2f predecessors walked\n",
+         ph[9] / (tiles * 256), ph[10] / (tiles * 256), ph[11] / (tiles * 256));
 #endif
   // verify: sorted by cell bits, a permutation, stable (low word = source index)
   std::vector<uint64_t> ok(n);
