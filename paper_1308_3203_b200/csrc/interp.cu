@@ -100,15 +100,14 @@ struct LogOut {
   unsigned long long cap;
 };
 
-// Copy `cnt` staged records of this warp to stage[base, base + cnt) and mark
-// the cells of write records in the write-set map.  Whole warp.
+// Copy `cnt` staged records of this warp to stage[base, base + cnt).  Whole
+// warp (rare path; the tile write-out is a bulk copy).
 __device__ __forceinline__ void write_out(const LogOut& p, const uint64_t* recs, uint32_t cnt,
                                           unsigned long long base, int lane, bool* over) {
   for (uint32_t i = lane; i < cnt; i += 32) {
     const uint64_t rec = recs[i];
     if (base + i < p.cap) p.stage[base + i] = rec;
     else *over = true;
-    if (rec & 1) p.wmap[rec >> REC_CELL_SHIFT] = 1;
   }
 }
 
@@ -116,13 +115,15 @@ __device__ __forceinline__ void write_out(const LogOut& p, const uint64_t* recs,
 __device__ __noinline__ uint32_t flush_warp_(const LogOut p, const uint64_t* recs, uint32_t fill, int lane) {
   __syncwarp();
   unsigned long long base = 0;
+  const uint32_t even = (fill + 1) & ~1u;  // slot counts stay even (16-byte bulk copies)
   if (lane == 0) {
-    base = atomicAdd(&p.ctr->stage_count, (unsigned long long)fill);
+    base = atomicAdd(&p.ctr->stage_count, (unsigned long long)even);
     atomicAdd(&p.ctr->staged_recs, (unsigned long long)fill);
   }
   base = __shfl_sync(FULL, base, 0);
   bool over = false;
   write_out(p, recs, fill, base, lane, &over);
+  if (even != fill && lane == 0 && base + fill < p.cap) p.stage[base + fill] = REC_SENTINEL;
   if (__any_sync(FULL, over) && lane == 0) p.ctr->log_overflow = 1;
   __syncwarp();
   return 0;
@@ -364,6 +365,9 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __
     const uint32_t orow = 4u * (uint32_t)T;  // overlay row stride (bytes)
 
     if (running) status = L_RUNNING;
+    // the previous tile's bulk store of this warp's staged records has read them
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncwarp();
     int n_own = 0;
     // instructions this lane executed in the interval (< 2^31 when !FUEL)
     typename std::conditional<FUEL, unsigned long long, uint32_t>::type steps = 0;
@@ -549,8 +553,10 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __
       const unsigned m = __ballot_sync(FULL, has);
       if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane);
       if (has) {
-        S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(ocell[j * T + t], tid, (uint32_t)j, 1);
+        const uint32_t cell = ocell[j * T + t];
+        S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, tid, (uint32_t)j, 1);
         p.wval[(size_t)j * p.n_lanes + g] = oval[j * T + t];
+        p.wmap[cell] = 1;  // write-set map (filter.cu)
       }
       S.fill += __popc(m);
     }
@@ -590,6 +596,10 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __
     b_loads += nloads;
     b_stores += nstores;
     b_ovl |= ovl_over;
+    if (S.fill & 1) {  // even record counts: every warp's slice is a 16-byte bulk copy
+      if (lane == 0) S.recs[S.fill] = REC_SENTINEL;
+      S.fill++;
+    }
     if (lane == 0) wcnt[warp] = S.fill;
     b_wait |= status == L_WAITING;
     __syncthreads();
@@ -641,16 +651,31 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __
       }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
-    write_out(lo, S.recs, S.fill, wbase[warp], lane, &b_over);
+    // this warp's records: one bulk copy (its lane 0 waits for the read before
+    // the next tile stages records again)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0 && S.fill) {
+      const unsigned long long b = wbase[warp];
+      if (b + S.fill <= p.stage_cap) {
+        bulk_s2g(p.stage + b, S.recs, S.fill * 8u);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      } else {
+        b_over = true;
+      }
+    }
     for (uint32_t i = t; i < wcnt[W]; i += T)  // sentinels in the abandoned chunk tail
       if (wbase[W] + i < p.stage_cap) p.stage[wbase[W] + i] = REC_SENTINEL;
     IPHASE(6);
-    __syncthreads();  // staging / overlay / registers reused by the next tile
+    // no block barrier here: the next tile's first __syncthreads orders every
+    // shared word a warp could overwrite early (wcnt / wbase are rewritten only
+    // after it; lane-state buffers are refilled only after their bulk stores
+    // have read them)
     IPHASE(7);
   }
 
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // record / lane-state stores complete
   if (t == 0) {
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // lane-state stores complete
     if (b_staged) atomicAdd(&p.ctr->staged_recs, b_staged);
   }
   // ---- block flush: sentinels in the last chunk's tail, statistics, flags
