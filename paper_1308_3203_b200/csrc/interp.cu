@@ -39,6 +39,9 @@
 
 #include "rc_internal.h"
 
+#ifndef INTERP_PREFETCH  // 1: fetch the next instruction one step ahead
+#define INTERP_PREFETCH 0
+#endif
 #ifndef LS_NB  // lane-state buffers (TMA prefetch pipeline depth + 1)
 #define LS_NB 2
 #endif
@@ -386,7 +389,14 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __
       bool ex = running && pc == minpc;
       uint4 eh;
       uint2 et;
-      if (CODE_SMEM) {
+      if (CODE_SMEM && !INTERP_PREFETCH) {
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(eh.x), "=r"(eh.y), "=r"(eh.z), "=r"(eh.w)
+                     : "r"(code_h + 16u * minpc)
+                     : "memory");
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(et.x), "=r"(et.y) : "r"(code_t + 8u * minpc) : "memory");
+        (void)nh; (void)nt; (void)pnext;
+      } else if (CODE_SMEM) {
         eh = nh;
         et = nt;
         asm volatile(
@@ -421,35 +431,84 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __
         }
       }
       if (!FUEL) steps += ex;
-      switch (op & 31) {  // warp-uniform; every value has a case: a bare jump table
+      // dispatch (warp-uniform): the heap accesses first, the rest through a switch
+      if (op == RC_OP_LD) {
+        bool ok = false;
+        uint32_t cell = 0;
+        if (ex) {
+          const int32_t idx = lds32(rc);
+          if ((uint32_t)idx >= et.y) {  // also catches idx < 0
+            emit_report(p, inst, (int32_t)((eh.x >> 8) & 0xFF), idx, tid, RC_OOB);
+            running = false;
+            status = L_OOB;
+          } else {
+            cell = cell_base + et.x + (uint32_t)idx;
+            int32_t v = 0;
+            bool found = false;
+            for (int j = 0; j < n_own; j++)
+              if ((uint32_t)lds32(oc + j * orow) == cell) { v = lds32(ov + j * orow); found = true; }
+            if (found) sts32(ra, v);
+            else ld_async(ra, p.heap + cell);
+            pc++;
+            nloads++;
+            ok = true;
+          }
+        }
+        const unsigned m = __ballot_sync(FULL, ok);
+        if (m) {
+          if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane);
+          if (ok) S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, tid, 0, 0);
+          S.fill += __popc(m);
+        }
+      } else if (op == RC_OP_ST) {
+        if (ex) {
+          const int32_t idx = lds32(rb);
+          if ((uint32_t)idx >= et.y) {  // also catches idx < 0
+            emit_report(p, inst, (int32_t)((eh.x >> 8) & 0xFF), idx, tid, RC_OOB);
+            running = false;
+            status = L_OOB;
+          } else {
+            const uint32_t cell = cell_base + et.x + (uint32_t)idx;
+            int j = 0;
+            while (j < n_own && (uint32_t)lds32(oc + j * orow) != cell) j++;
+            if (j == n_own) {
+              if (n_own < (int)OV) { sts32(oc + j * orow, (int32_t)cell); n_own++; }
+              else { ovl_over = true; j = -1; }
+            }
+            if (j >= 0) sts32(ov + j * orow, lds32(rc));
+            pc++;
+            nstores++;
+          }
+        }
+      } else switch (op & 31) {
+        case RC_OP_LD: case RC_OP_ST: break;  // handled above
         case 0: case 28: case 29: case 30: case 31: break;  // unused (the validator rejects them)
         case RC_OP_CONST: if (ex) { sts32(ra, imm); pc++; } break;
         case RC_OP_MOV: if (ex) { sts32(ra, lds32(rb)); pc++; } break;
         case RC_OP_TID: if (ex) { sts32(ra, (int32_t)tid); pc++; } break;
         case RC_OP_SIZE: if (ex) { sts32(ra, imm); pc++; } break;
         case RC_OP_ADDI: if (ex) { sts32(ra, wadd(lds32(rb), imm)); pc++; } break;
-        case RC_OP_ADD: case RC_OP_SUB: case RC_OP_MUL: case RC_OP_MIN: case RC_OP_MAX: case RC_OP_AND:
-        case RC_OP_OR: case RC_OP_XOR: case RC_OP_LT: case RC_OP_EQ: case RC_OP_LAND:
-          if (ex) {
-            const int32_t x = lds32(rb), y = lds32(rc);
-            int32_t v;
-            switch (op) {
-              case RC_OP_ADD: v = wadd(x, y); break;
-              case RC_OP_SUB: v = (int32_t)((uint32_t)x - (uint32_t)y); break;
-              case RC_OP_MUL: v = (int32_t)((uint32_t)x * (uint32_t)y); break;
-              case RC_OP_MIN: v = min(x, y); break;
-              case RC_OP_MAX: v = max(x, y); break;
-              case RC_OP_AND: v = x & y; break;
-              case RC_OP_OR: v = x | y; break;
-              case RC_OP_XOR: v = x ^ y; break;
-              case RC_OP_LT: v = x < y; break;
-              case RC_OP_EQ: v = x == y; break;
-              default: v = (x != 0) && (y != 0); break;
-            }
-            sts32(ra, v);
-            pc++;
-          }
-          break;
+        // binary ALU ops, one case each (a flat jump table; int32 wrap, reading L7)
+#define ALU2(OPC, EXPR)                         \
+  case OPC:                                     \
+    if (ex) {                                   \
+      const int32_t x = lds32(rb), y = lds32(rc); \
+      sts32(ra, (EXPR));                        \
+      pc++;                                     \
+    }                                           \
+    break;
+        ALU2(RC_OP_ADD, wadd(x, y))
+        ALU2(RC_OP_SUB, (int32_t)((uint32_t)x - (uint32_t)y))
+        ALU2(RC_OP_MUL, (int32_t)((uint32_t)x * (uint32_t)y))
+        ALU2(RC_OP_MIN, min(x, y))
+        ALU2(RC_OP_MAX, max(x, y))
+        ALU2(RC_OP_AND, x & y)
+        ALU2(RC_OP_OR, x | y)
+        ALU2(RC_OP_XOR, x ^ y)
+        ALU2(RC_OP_LT, (int32_t)(x < y))
+        ALU2(RC_OP_EQ, (int32_t)(x == y))
+        ALU2(RC_OP_LAND, (int32_t)((x != 0) && (y != 0)))
+#undef ALU2
         case RC_OP_DIV: case RC_OP_MOD:
           if (ex) {
             const int32_t x = lds32(rb), y = lds32(rc);
@@ -467,57 +526,6 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __
           }
           break;
         case RC_OP_LNOT: if (ex) { sts32(ra, lds32(rb) == 0); pc++; } break;
-        case RC_OP_LD: {
-          bool ok = false;
-          uint32_t cell = 0;
-          if (ex) {
-            const int32_t idx = lds32(rc);
-            if ((uint32_t)idx >= et.y) {  // also catches idx < 0
-              emit_report(p, inst, (int32_t)((eh.x >> 8) & 0xFF), idx, tid, RC_OOB);
-              running = false;
-              status = L_OOB;
-            } else {
-              cell = cell_base + et.x + (uint32_t)idx;
-              int32_t v = 0;
-              bool found = false;
-              for (int j = 0; j < n_own; j++)
-                if ((uint32_t)lds32(oc + j * orow) == cell) { v = lds32(ov + j * orow); found = true; }
-              if (found) sts32(ra, v);
-              else ld_async(ra, p.heap + cell);
-              pc++;
-              nloads++;
-              ok = true;
-            }
-          }
-          const unsigned m = __ballot_sync(FULL, ok);
-          if (m) {
-            if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane);
-            if (ok) S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, tid, 0, 0);
-            S.fill += __popc(m);
-          }
-          break;
-        }
-        case RC_OP_ST:
-          if (ex) {
-            const int32_t idx = lds32(rb);
-            if ((uint32_t)idx >= et.y) {  // also catches idx < 0
-              emit_report(p, inst, (int32_t)((eh.x >> 8) & 0xFF), idx, tid, RC_OOB);
-              running = false;
-              status = L_OOB;
-            } else {
-              const uint32_t cell = cell_base + et.x + (uint32_t)idx;
-              int j = 0;
-              while (j < n_own && (uint32_t)lds32(oc + j * orow) != cell) j++;
-              if (j == n_own) {
-                if (n_own < (int)OV) { sts32(oc + j * orow, (int32_t)cell); n_own++; }
-                else { ovl_over = true; j = -1; }
-              }
-              if (j >= 0) sts32(ov + j * orow, lds32(rc));
-              pc++;
-              nstores++;
-            }
-          }
-          break;
         case RC_OP_BAR: if (ex) { pc++; running = false; status = L_WAITING; } break;
         case RC_OP_EXIT: if (ex) { running = false; status = L_EXITED_NOW; } break;
         case RC_OP_ASSUME:
