@@ -86,7 +86,8 @@ __device__ __forceinline__ void rw_pair(bool hasr, uint32_t r1, uint32_t r2, uin
 // Serial path for a segment that does not fit one 32-record round: the head
 // thread walks it (pass 1: statistics; pass 2: first differing writer and
 // membership flags; pass 3 only for a non-benign pair with readers).
-__device__ __forceinline__ void serial_segment(const DetectParams& p, uint32_t i, uint32_t n_records) {
+// (out of line: the rare path stays out of the streaming loop's instruction footprint)
+__device__ __noinline__ void serial_segment(const DetectParams& p, uint32_t i, uint32_t n_records) {
   const uint32_t key = rec_cell(__ldg(p.recs + i));
   uint32_t r1 = INF, r2 = INF, rmax = 0, w1 = INF, w2 = INF, wmax = 0, nw = 0;
   bool hasr = false;
@@ -139,7 +140,10 @@ __device__ __forceinline__ void serial_segment(const DetectParams& p, uint32_t i
 }
 }  // namespace
 
-constexpr uint32_t DET_ROUNDS = 8;  // 32-record rounds per warp (all prefetched)
+#ifndef DET_ROUNDS_OPT
+#define DET_ROUNDS_OPT 8
+#endif
+constexpr uint32_t DET_ROUNDS = DET_ROUNDS_OPT;  // 32-record rounds per warp (all prefetched)
 constexpr uint32_t DET_CHUNK = 32 * DET_ROUNDS;
 
 // Associative per-segment summary.  A cell is SIMPLE when it has at most one
@@ -290,28 +294,71 @@ __device__ __forceinline__ void detect_chunk(const DetectParams& p, uint64_t wg,
   if (carry && lane == 0) serial_segment(p, (uint32_t)carry_start, n_records);  // continues into the next chunk
 }
 
+// A4 fused as the tail of K4 (readings L9, L17): the
+// last block to finish checks, per instance, whether the work-items that
+// arrived in this interval reached more than one barrier node (K1 reduced the
+// min / max arrival node), resets the ranges, and takes the interval's
+// verdict: `abort` when the host must act before the next interval may run
+// (DevCounters::abort).
+__device__ __noinline__ void boundary_tail(const DetectParams& p) {
+  __shared__ bool last;
+  DevCounters* c = p.ctr;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&c->bdone, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (uint32_t inst = threadIdx.x; inst < p.n_inst; inst += blockDim.x) {
+    const int32_t lo = p.node_min[inst], hi = p.node_max[inst];
+    p.node_min[inst] = 0x7FFFFFFF;
+    p.node_max[inst] = (int32_t)0x80000000;
+    const bool div = lo < hi;
+    p.inst_flag[inst] = div;
+    if (div) c->diverged = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    c->bdone = 0;
+    const volatile DevCounters* v = c;
+    const bool need_host = v->log_overflow || v->ovl_overflow || v->k1_reports > p.report_cap ||
+                           v->report_count > p.report_cap || v->diverged || !v->any_waiting;
+    if (need_host) c->abort = 1;
+  }
+}
+
 // Persistent: warps stride over the chunks; the record count is read from
-// device memory (no host sync).  Skips everything (no commit) when this
+// device memory (no host sync).  Skips the detection (no commit) when this
 // interval's log overflowed or K1's reports overflowed: the host then re-runs
 // the interval from the saved lane state on an untouched heap.
 __global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
-  if (p.ctr->abort || p.ctr->log_overflow || p.ctr->k1_reports > p.report_cap) return;
-  const uint32_t n_records = (uint32_t)p.ctr->kept_count;
-  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wg * DET_CHUNK < n_records; wg += warps)
-    detect_chunk(p, wg, n_records);
+  if (p.ctr->abort) return;  // speculative interval after one that needs the host (uniform)
+  if (!(p.ctr->log_overflow || p.ctr->k1_reports > p.report_cap)) {
+    const uint32_t n_records = (uint32_t)p.ctr->kept_count;
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wg * DET_CHUNK < n_records;
+         wg += warps)
+      detect_chunk(p, wg, n_records);
+  }
+  if (p.with_boundary) boundary_tail(p);
 }
 
 cudaError_t launch_detect(const DetectParams& p, cudaStream_t s) {
-  if (p.n_records == 0) return cudaSuccess;
-  static int nsm = 0;
+  if (p.n_records == 0 && !p.with_boundary) return cudaSuccess;
+  static int nsm = 0, per_sm = 1;
   if (!nsm) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, detect_kernel, 256, 0);
+    per_sm = std::max(per_sm, 1);
   }
+  // one resident wave (persistent warps stride over the chunks)
   const uint64_t warps = (p.n_records + DET_CHUNK - 1) / DET_CHUNK;  // upper bound
-  const unsigned grid = (unsigned)std::min<uint64_t>((warps + 7) / 8, (uint64_t)nsm * 8);
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((warps + 7) / 8, (uint64_t)nsm * per_sm));
   detect_kernel<<<grid, 256, 0, s>>>(p);
   launched();
   return cudaGetLastError();

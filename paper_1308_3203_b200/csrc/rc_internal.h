@@ -148,6 +148,12 @@ struct DetectParams {
   rc_report* reports;
   unsigned long long report_cap;
   DevCounters* ctr;
+  // fused A4 tail (detect.cu boundary_tail); off for a detect-only re-run
+  bool with_boundary;
+  uint32_t n_inst;
+  int32_t* node_min;          // [n_inst] from K1, reset by the tail
+  int32_t* node_max;
+  uint32_t* inst_flag;        // [n_inst] diverged
 };
 
 // ---- launchers (defined in the .cu files) --------------------------------

@@ -434,6 +434,11 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       dp.reports = W.reports.as<rc_report>();
       dp.report_cap = rep_cap;
       dp.ctr = dctr;
+      dp.with_boundary = false;
+      dp.n_inst = nb;
+      dp.node_min = node_min;
+      dp.node_max = node_max;
+      dp.inst_flag = inst_flag;
       return dp;
     };
     struct Marks { size_t m0 = 0, m1 = 0; };
@@ -506,15 +511,10 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       sr = in_alt ? W.log_alt.as<uint64_t>() : W.log.as<uint64_t>();
       // ---- K4+K5 detect + commit, A4 check + verdict
       DetectParams dp = detect_params(kk);
+      dp.with_boundary = true;  // A4 as detect's tail: consumes (and resets) K1's per-instance node ranges
       W.prof.begin(s);
       EQ(launch_detect(dp, s));
       W.prof.end(RC_PROF_DETECT, s, 0, 0);
-      BoundaryParams bp = bparams(kk);
-      bp.status = W.status[cc ^ 1].as<uint8_t>();
-      bp.pc = W.pc[cc ^ 1].as<uint32_t>();
-      W.prof.begin(s);
-      EQ(launch_boundary(bp, s));  // consumes (and resets) K1's per-instance node ranges
-      W.prof.end(RC_PROF_BOUNDARY, s, (uint64_t)nb * 12, nb);
       mk->m1 = W.prof.marks.size();
       EQ(cudaMemcpyAsync(&W.h_ctr[kk & 1], dctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
       EQ(cudaEventRecord(W.iv_done[kk & 1], s));

@@ -154,13 +154,6 @@ __global__ void __launch_bounds__(256) hist_kernel(const uint64_t* __restrict__ 
   }
 }
 
-// exclusive offsets of every digit, one block per pass
-__global__ void __launch_bounds__(256) bin_offsets_kernel(const uint32_t* __restrict__ hist,
-                                                          uint32_t* __restrict__ off) {
-  __shared__ uint32_t wt[WARPS];
-  const uint32_t v = hist[blockIdx.x * RADIX + threadIdx.x];
-  off[blockIdx.x * RADIX + threadIdx.x] = block_excl_scan(v, wt);
-}
 
 // ---- K3: one onesweep digit pass -------------------------------------------
 // Persistent: a resident grid of blocks claims tiles in order from an atomic
@@ -176,6 +169,7 @@ struct SortSmem {
 #endif
   uint32_t thist[2][RADIX];      // early tile counts (two copies: fewer atomic conflicts)
   uint32_t glob_base[RADIX];
+  uint32_t bin_base[RADIX];      // global exclusive start of each digit (this pass)
   uint32_t wt[WARPS];
   uint32_t tile[2];
   unsigned long long mbar[2];
@@ -227,7 +221,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
                                                                    uint64_t* __restrict__ out, uint32_t n_host,
                                                                    const unsigned long long* n_a,
                                                                    const unsigned long long* n_b, int shift,
-                                                                   const uint32_t* __restrict__ bin_off,
+                                                                   const uint32_t* __restrict__ hist,
                                                                    unsigned long long* __restrict__ status,
                                                                    uint32_t* __restrict__ tile_ctr, uint32_t epoch) {
   constexpr int NB = PERSISTENT ? 2 : 1;
@@ -255,6 +249,10 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
       if (PERSISTENT && !SORT_CLAIM_LATE) claimed = atomicAdd(tile_ctr, 1u);
     }
     if (!PERSISTENT) S.tile[1] = 0xFFFFFFFFu;
+  }
+  {  // global start of every digit of this pass: exclusive scan of its counts
+    const uint32_t e = block_excl_scan(t < RADIX ? hist[t] : 0u, S.wt);  // (synchronises the block)
+    if (t < RADIX) S.bin_base[t] = e;
   }
   __syncthreads();
   uint32_t phase = 0;  // bit b = expected parity of buffer b's mbarrier
@@ -490,7 +488,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
       }
 #endif
     }
-    if (dig) S.glob_base[d] = (uint32_t)(bin_off[d] + excl) - excl_tile;
+    if (dig) S.glob_base[d] = (uint32_t)(S.bin_base[d] + excl) - excl_tile;
 #if SORT_CLAIM_LATE
     // claim the next tile only now (its AGGREGATE follows within a few
     // thousand cycles, so successors' look-backs never wait on a tile claimed
@@ -553,16 +551,14 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, const unsigned long long* 
     if (per_sm < 1) per_sm = 1;
   }
   cudaMemsetAsync(ws.tile_ctr, 0, 4 * sizeof(uint32_t), s);
-  if (prof) prof->begin(s);
-  if (!hist_ready) {
+  if (!hist_ready) {  // (each pass scans its digit counts itself)
+    if (prof) prof->begin(s);
     cudaMemsetAsync(ws.hist, 0, 4 * RADIX * sizeof(uint32_t), s);
     const uint32_t hist_grid = (uint32_t)umin64((uint64_t)nsm * 8, (n + 256 * 16 - 1) / (256 * 16));
     hist_kernel<<<hist_grid, 256, 0, s>>>(recs, n, n_a, n_b, passes, ws.hist);
     launched();
+    if (prof) prof->end(RC_PROF_HIST, s, (uint64_t)n * 8, n);
   }
-  bin_offsets_kernel<<<passes, 256, 0, s>>>(ws.hist, ws.bin_off);
-  launched();
-  if (prof) prof->end(RC_PROF_HIST, s, hist_ready ? 0 : (uint64_t)n * 8, n);
   const uint32_t tiles = (uint32_t)sort_tiles(n);
   // persistent: never more blocks than can be resident (look-back progress)
   const bool pers = g_sort_variant == 1;
@@ -577,10 +573,10 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, const unsigned long long* 
     if (prof) prof->begin(s);
     if (pers)
       onesweep_kernel<true><<<grid, SORT_THREADS, sizeof(SortSmem<2>), s>>>(
-          kin, kout, n, n_a, n_b, 8 * p, ws.bin_off + p * RADIX, ws.status, ws.tile_ctr + p, ws.epoch);
+          kin, kout, n, n_a, n_b, 8 * p, ws.hist + p * RADIX, ws.status, ws.tile_ctr + p, ws.epoch);
     else
       onesweep_kernel<false><<<grid, SORT_THREADS, sizeof(SortSmem<1>), s>>>(
-          kin, kout, n, n_a, n_b, 8 * p, ws.bin_off + p * RADIX, ws.status, ws.tile_ctr + p, ws.epoch);
+          kin, kout, n, n_a, n_b, 8 * p, ws.hist + p * RADIX, ws.status, ws.tile_ctr + p, ws.epoch);
     launched();
     if (prof) prof->end(RC_PROF_SORT, s, (uint64_t)n * 16, n);
     cudaError_t e = cudaGetLastError();
