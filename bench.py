@@ -220,7 +220,7 @@ def main():
                         if isinstance(v, dict):
                             for kk in v:
                                 prof_sum[k][kk] += v[kk]
-                        else:
+                        elif k != "sample_every":
                             prof_sum[k] += v
         e1.record(stream)
         torch.cuda.synchronize(dev)
@@ -269,11 +269,13 @@ def main():
             dist.destroy_process_group()
         return 0
 
+    PER_INTERVAL = ("interp", "filter", "hist", "sort", "detect", "boundary")
     peak, peak_src = peaks()
     roofline = None
     kernels = None
     gpu_launches = None
     if prof_sum:
+        every = max(1, int(prof_sum.get("sample_every", 1)))
         s = prof_sum["sort"]
         achieved = s["alg_bytes"] / (s["ms"] / 1e3) / 1e9 if s["ms"] > 0 else None
         traffic = None
@@ -288,13 +290,15 @@ def main():
                     "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak if achieved else None,
                     "traffic": traffic, "alg_bytes_per_launch": s["alg_bytes"] / max(1, s["launches"]),
-                    "alg_bytes_per_record": 16, "launches": s["launches"] // args.steps,
+                    "alg_bytes_per_record": 16, "launches_sampled": s["launches"],
+                    "sampling": f"CUDA events around every {every}th interval's kernels of the timed steps",
                     "peak_source": peak_src}
-        kernels = {}
+        kernels = {"sample_every": every}
         for c in ("interp", "filter", "hist", "sort", "detect", "boundary", "finalize", "copy"):
             d = prof_sum[c]
-            kernels[c] = {"launches_per_step": d["launches"] / args.steps, "ms_per_step": d["ms"] / args.steps,
-                          "share": d["ms"] / prof_sum["total_ms"] if prof_sum["total_ms"] else None,
+            k = every if c in PER_INTERVAL else 1  # sampled classes: per-step totals are estimates
+            kernels[c] = {"launches_per_step": k * d["launches"] / args.steps, "ms_per_step": k * d["ms"] / args.steps,
+                          "share": k * d["ms"] / prof_sum["total_ms"] if prof_sum["total_ms"] else None,
                           "alg_GBps": d["alg_bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 and d["alg_bytes"] else None}
         kernels["total_ms_per_step"] = prof_sum["total_ms"] / args.steps
         gpu_launches = prof_sum["kernel_launches"]

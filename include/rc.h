@@ -160,6 +160,14 @@ typedef struct {
   uint64_t items[RC_PROF_N]; /* records / lanes processed                    */
   double total_ms;           /* whole rc_run on the stream                    */
   uint64_t kernel_launches;  /* librc kernels launched by this rc_run         */
+  /* in: record the per-interval kernels of every k-th interval only (0 = the
+   * default, 7: coprime with the 2-interval period of alternating kernels);
+   * out: the k used.  launches/ms/alg_bytes/items of the
+   * per-interval classes cover the sampled intervals only (per-launch
+   * averages are unbiased; totals scale by k).  Event bookkeeping for every
+   * interval would cost the host more than the GPU work of small intervals. */
+  uint32_t sample_every;
+  uint32_t reserved;
 } rc_profile;
 
 /* One shared array of the kernel (an element of Args).

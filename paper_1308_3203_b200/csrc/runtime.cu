@@ -20,6 +20,8 @@
 #include <cstring>
 #include <new>
 
+#include <array>
+
 #include "rc_internal.h"
 
 namespace rc {
@@ -275,6 +277,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   rc_workspace& W = *P->ws;
   W.prof.reset();
   W.prof.on = opt.profile != nullptr;
+  const uint32_t prof_every = opt.profile ? (opt.profile->sample_every ? opt.profile->sample_every : 7u) : 1u;
+  uint64_t prof_intervals = 0;  // interval enqueues so far (sampling clock)
   if (opt.profile) memset(opt.profile, 0, sizeof(rc_profile));
   const uint64_t launches0 = g_launches.load();
   cudaEvent_t t_begin = nullptr, t_end = nullptr;
@@ -366,6 +370,11 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     return e;
   };
 
+  // dev instrumentation (RC_GAPS=1): GPU time inside interval enqueues vs the whole run
+  const bool gaps = getenv("RC_GAPS") != nullptr;
+  std::vector<std::array<cudaEvent_t, 2>> gap_ev;
+  cudaEvent_t g0 = nullptr, g1 = nullptr;
+  if (gaps) { cudaEventCreate(&g0); cudaEventCreate(&g1); cudaEventRecord(g0, s); }
   for (uint32_t b0 = 0; b0 < n_inst; b0 += I_b) {
     const uint32_t nb = std::min(I_b, n_inst - b0);
     const uint32_t L = nb * n;
@@ -445,6 +454,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     auto enqueue_interval = [&](uint32_t kk, int cc, Marks* mk) -> cudaError_t {
       cudaError_t e;
 #define EQ(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
+      if (gaps) { gap_ev.push_back({}); cudaEventCreate(&gap_ev.back()[0]); cudaEventCreate(&gap_ev.back()[1]); cudaEventRecord(gap_ev.back()[0], s); }
+      if (opt.profile) W.prof.on = (prof_intervals++ % prof_every) == 0;  // sampled interval profile
       if (cpi) EQ(cudaMemsetAsync(W.wmap.p, 0, (size_t)nb * cpi, s));  // write-set map of this interval
       EQ(cudaMemsetAsync(dctr, 0, offsetof(DevCounters, report_count), s));
       EQ(cudaMemsetAsync(W.sort.hist, 0, 4 * 256 * sizeof(uint32_t), s));  // the filter fuses the histograms
@@ -518,6 +529,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       mk->m1 = W.prof.marks.size();
       EQ(cudaMemcpyAsync(&W.h_ctr[kk & 1], dctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
       EQ(cudaEventRecord(W.iv_done[kk & 1], s));
+      if (gaps) cudaEventRecord(gap_ev.back()[1], s);
+      if (opt.profile) W.prof.on = true;  // batch-level marks (copies, finalize) are always recorded
 #undef EQ
       return cudaSuccess;
     };
@@ -647,6 +660,21 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     }
   }
 
+  if (gaps) {
+    cudaEventRecord(g1, s);
+    cudaEventSynchronize(g1);
+    float tot = 0, iv = 0, gapsum = 0;
+    cudaEventElapsedTime(&tot, g0, g1);
+    for (size_t i = 0; i < gap_ev.size(); i++) {
+      float x = 0;
+      cudaEventElapsedTime(&x, gap_ev[i][0], gap_ev[i][1]);
+      iv += x;
+      if (i + 1 < gap_ev.size()) { float y = 0; cudaEventElapsedTime(&y, gap_ev[i][1], gap_ev[i + 1][0]); gapsum += y; }
+      cudaEventDestroy(gap_ev[i][0]);
+      cudaEventDestroy(gap_ev[i][1]);
+    }
+    fprintf(stderr, "RC_GAPS run %.2f ms, %zu interval enqueues %.2f ms, between them %.2f ms\n", tot, gap_ev.size(), iv, gapsum);
+  }
 #ifdef INTERP_PHASE_TIMING
   if (getenv("RC_PHASES")) {
     unsigned long long ph[8];
@@ -679,6 +707,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     cudaEventElapsedTime(&ms, t_begin, t_end);
     opt.profile->total_ms = ms;
     opt.profile->kernel_launches = g_launches.load() - launches0;
+    opt.profile->sample_every = prof_every;
     cudaEventDestroy(t_begin);
     cudaEventDestroy(t_end);
   }

@@ -42,7 +42,8 @@ class rc_stats(C.Structure):
 
 class rc_profile(C.Structure):
     _fields_ = [("launches", C.c_uint64 * 8), ("ms", C.c_double * 8), ("alg_bytes", C.c_uint64 * 8),
-                ("items", C.c_uint64 * 8), ("total_ms", C.c_double), ("kernel_launches", C.c_uint64)]
+                ("items", C.c_uint64 * 8), ("total_ms", C.c_double), ("kernel_launches", C.c_uint64),
+                ("sample_every", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 class rc_array(C.Structure):
@@ -145,7 +146,7 @@ def _stats_dict(s: rc_stats) -> dict:
 
 
 def _profile_dict(p: rc_profile) -> dict:
-    return {"total_ms": p.total_ms, "kernel_launches": int(p.kernel_launches),
+    return {"total_ms": p.total_ms, "kernel_launches": int(p.kernel_launches), "sample_every": int(p.sample_every),
             **{c: {"launches": int(p.launches[i]), "ms": float(p.ms[i]), "alg_bytes": int(p.alg_bytes[i]),
                    "items": int(p.items[i])} for i, c in enumerate(PROF_CLASSES)}}
 
@@ -219,14 +220,15 @@ def rc_run(prog: Program, work_group_size: int, arrays: list, *, n_instances: in
             finals = [torch.empty_like(a) for a in keep]
         fin_ptrs = (C.c_void_p * len(arrays))(*[(f.ctypes.data if isinstance(f, np.ndarray) else f.data_ptr())
                                                  for f in finals])
-    out = (rc_report * max(1, capacity))()
+    # report buffer: uninitialised (the library writes the first min(capacity,
+    # total) records; zero-filling a large ctypes array costs milliseconds)
+    out = np.empty(max(1, capacity), dtype=REPORT_DTYPE)
     total = C.c_uint64()
     st = rc_stats()
-    code = lib().rc_run(prog._h, work_group_size, arr, len(arrays), n_instances, C.byref(opt), out, capacity,
-                        C.byref(total), C.byref(st), fin_ptrs)
+    code = lib().rc_run(prog._h, work_group_size, arr, len(arrays), n_instances, C.byref(opt),
+                        out.ctypes.data_as(C.POINTER(rc_report)), capacity, C.byref(total), C.byref(st), fin_ptrs)
     if code not in (RC_OK, RC_ETRUNC) or (code == RC_ETRUNC and not allow_truncate):
         raise RCError(code, rc_last_error())
     n = min(total.value, capacity)
-    reps = np.frombuffer(bytes(C.string_at(C.addressof(out), n * 32)), dtype=REPORT_DTYPE).copy() if n else \
-        np.zeros(0, dtype=REPORT_DTYPE)
+    reps = out[:n].copy()
     return RunResult(reps, int(total.value), _stats_dict(st), finals, _profile_dict(prof) if profile else None)
