@@ -280,12 +280,10 @@ def main():
         achieved = s["alg_bytes"] / (s["ms"] / 1e3) / 1e9 if s["ms"] > 0 else None
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tpath) and s["launches"]:
+        if os.path.exists(tpath):
             with open(tpath) as f:
                 tr = json.load(f)
-            bpr = tr.get("onesweep_kernel", {}).get("dram_bytes_per_record")
-            if bpr:
-                traffic = bpr * s["items"] / s["launches"]
+            traffic = tr.get("onesweep_kernel", {}).get("dram_bytes_per_launch")
         roofline = {"kernel": "onesweep_kernel (K3, one LSD digit pass)", "bound": "hbm",
                     "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak if achieved else None,

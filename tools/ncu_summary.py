@@ -7,7 +7,7 @@
   command) -> per-kernel count / total / share / average.
 * *.ncu-rep (`--set full` captures) -> key metrics, stall reasons, hottest
   SASS lines; the onesweep capture also refreshes profiles/ncu_traffic.json
-  (DRAM bytes per record, read by bench.py for roofline.traffic).
+  (DRAM bytes of that launch, read by bench.py for roofline.traffic).
 """
 from __future__ import annotations
 
@@ -108,16 +108,14 @@ def main():
         s, d = summarize_rep(rep)
         open(os.path.join(PROF, f"{a.round}{tag}_ncu_{base}.txt"), "w").write(s + "\n")
         print(s)
-        if "onesweep" in base:
-            grid = float(d["launch__grid_size"].replace(",", ""))
-            recs = grid * 4096
+        if base == "prof_onesweep":
             mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             byts = sum(float(d[k].replace(",", "")) * mult[d["_units"][k]]
                        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-            bpr = byts / recs
-            json.dump({"onesweep_kernel": {"dram_bytes_per_record": bpr, "alg_bytes_per_record": 24,
-                                           "source": f"profiles/{a.round}{tag}_ncu_{base}.txt (ncu --set full, "
-                                                     f"one launch, {int(recs)} records, tiles x 4096)"}},
+            json.dump({"onesweep_kernel": {"dram_bytes_per_launch": byts,
+                                           "source": f"profiles/{a.round}{tag}_ncu_{base}.txt (ncu --set full "
+                                                     "--cache-control all, one launch of the bench workload: "
+                                                     "dram__bytes_read.sum + dram__bytes_write.sum)"}},
                       open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
 
 
