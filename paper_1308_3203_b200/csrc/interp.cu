@@ -35,12 +35,16 @@
 // node (BAR pc, or -1 for exit) of the lanes that arrived in this interval —
 // equal min and max means every arrival reached the same barrier — and a
 // global "some lane is suspended" flag.
+#include <cstdlib>
 #include <type_traits>
 
 #include "rc_internal.h"
 
-#ifndef INTERP_PREFETCH  // 1: fetch the next instruction one step ahead
-#define INTERP_PREFETCH 0
+#ifndef INTERP_H  // work-items per thread for large batches (1 or 2)
+#define INTERP_H 2
+#endif
+#ifndef INTERP_MIN_BLOCKS_H  // resident blocks per SM of the 2-work-items-per-thread kernel
+#define INTERP_MIN_BLOCKS_H 3
 #endif
 #ifndef LS_NB  // lane-state buffers (TMA prefetch pipeline depth + 1)
 #define LS_NB 2
@@ -257,36 +261,43 @@ void interp_phase_io(unsigned long long* out, bool reset) {
 // FUEL: per-instruction fuel check (reading L17).  Off when the program's
 // longest barrier-free path (program.cpp analyze()) fits in the fuel, so no
 // work-item can run out in any interval.
-template <bool CODE_SMEM, bool FUEL>
-__global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __grid_constant__ InterpParams p) {
+// H: work-items per thread.  Thread t runs lanes t, t + T, ... of a tile of
+// H*T lanes side by side: one instruction fetch, decode, dispatch and warp
+// vote serve H lanes, and each lane's heap loads add to the memory-level
+// parallelism of the warp.
+template <bool CODE_SMEM, bool FUEL, int H>
+__global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_BLOCKS_H)
+    interp_kernel(const __grid_constant__ InterpParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (p.ctr->abort) return;  // speculative interval (DevCounters::abort)
   const int T = blockDim.x;
+  const int TL = H * T;  // lanes per tile
   const int W = T >> 5;
   const int t = threadIdx.x;
   const int warp = t >> 5, lane = t & 31;
   const uint32_t R = p.n_regs, OV = p.ovl_cap;
+  const uint32_t SW = H * p.stage_warp;  // staged records per warp
   const LogOut lo{p.stage, p.wmap, p.ctr, p.stage_cap};
 
   // ---- shared memory carve-up (sizes mirrored in interp_smem_bytes)
   unsigned char* q = smem;
-  // register files [reg][thread], status and pc rows, NB-buffered (TMA: the
+  // register files [reg][lane], status and pc rows, LS_NB-buffered (TMA: the
   // next tile's state lands while this one runs; a buffer is refilled only
-  // after the bulk stores of its tile two steps back have read it);
-  // buffer b is addressed arithmetically from these bases (a runtime-indexed
-  // array of pointers would lose the shared address space)
-  int32_t* const sregs0 = reinterpret_cast<int32_t*>(q); q += (size_t)LS_NB * R * T * 4;
-  uint32_t* const spc0 = reinterpret_cast<uint32_t*>(q); q += (size_t)LS_NB * T * 4;
-  uint8_t* const sstat0 = reinterpret_cast<uint8_t*>(q); q += (size_t)LS_NB * T;
-#define SREGS(b) (sregs0 + (size_t)(b) * R * T)
-#define SPC(b) (spc0 + (size_t)(b) * T)
-#define SSTAT(b) (sstat0 + (size_t)(b) * T)
+  // after the bulk stores of its previous tile have read it); buffer b is
+  // addressed arithmetically from these bases (a runtime-indexed array of
+  // pointers would lose the shared address space)
+  int32_t* const sregs0 = reinterpret_cast<int32_t*>(q); q += (size_t)LS_NB * R * TL * 4;
+  uint32_t* const spc0 = reinterpret_cast<uint32_t*>(q); q += (size_t)LS_NB * TL * 4;
+  uint8_t* const sstat0 = reinterpret_cast<uint8_t*>(q); q += (size_t)LS_NB * TL;
+#define SREGS(b) (sregs0 + (size_t)(b) * R * TL)
+#define SPC(b) (spc0 + (size_t)(b) * TL)
+#define SSTAT(b) (sstat0 + (size_t)(b) * TL)
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(q); q += (8 * LS_NB + 15) & ~15;
-  uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)W * p.stage_warp * 8;
+  uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)W * SW * 8;
   uint4* s_code = reinterpret_cast<uint4*>(q); q += CODE_SMEM ? (size_t)(p.n_instr + 1) * 16 : 0;  // heads + pad entry
   uint2* s_tail = reinterpret_cast<uint2*>(q); q += CODE_SMEM ? (size_t)(p.n_instr + 1) * 8 : 0;   // tails + pad
-  uint32_t* ocell = reinterpret_cast<uint32_t*>(q); q += (size_t)OV * T * 4;
-  int32_t* oval = reinterpret_cast<int32_t*>(q); q += (size_t)OV * T * 4;
+  uint32_t* ocell = reinterpret_cast<uint32_t*>(q); q += (size_t)OV * TL * 4;
+  int32_t* oval = reinterpret_cast<int32_t*>(q); q += (size_t)OV * TL * 4;
   uint32_t* s_off = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
   uint32_t* s_size = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
   uint8_t* s_live = reinterpret_cast<uint8_t*>(q); q += (p.n_live + 3) & ~3u;
@@ -301,25 +312,25 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __
   __syncthreads();  // s_off / s_size before the pre-decode
   if (CODE_SMEM) {
     for (uint32_t i = t; i < p.n_instr; i += T) {
-      const Dec d = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + i), T, s_off, s_size);
+      const Dec d = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + i), TL, s_off, s_size);
       s_code[i] = d.h;
       s_tail[i] = d.t;
     }
-    if (t == 0) {  // fetched ahead of the last pc, never executed
+    if (t == 0) {  // pad entry (never executed)
       s_code[p.n_instr] = make_uint4(0, 0, 0, 0);
       s_tail[p.n_instr] = make_uint2(0, 0);
     }
   }
   const uint32_t code_h = pin(smem_u32(s_code)), code_t = pin(smem_u32(s_tail));
   for (uint32_t i = t; i < p.n_live; i += T) s_live[i] = p.live[i];
-  const uint32_t n_tiles0 = (p.n_lanes + T - 1) / T;
+  const uint32_t n_tiles = (p.n_lanes + TL - 1) / TL;
   if (t == 0) {
     for (int b = 0; b < LS_NB; b++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[b])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (t == 0 && blockIdx.x < n_tiles0)
-    prefetch_lanes(p, blockIdx.x, T, SSTAT(0), SPC(0), SREGS(0), s_live, &mbar[0]);
+  if (t == 0 && blockIdx.x < n_tiles)
+    prefetch_lanes(p, blockIdx.x, TL, SSTAT(0), SPC(0), SREGS(0), s_live, &mbar[0]);
 
   // per-lane totals, reduced once at the end of the kernel
   unsigned long long b_instr = 0, b_loads = 0, b_stores = 0;
@@ -327,7 +338,6 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __
   // the block's current staging chunk (thread 0)
   unsigned long long c_base = 0;
   uint32_t c_used = 0, c_cap = 0;
-  const uint32_t n_tiles = (p.n_lanes + T - 1) / T;
 
   uint32_t a4_inst = 0xFFFFFFFFu;  // arrival-node range this warp pushed (warp-uniform)
   int32_t a4_lo = 0, a4_hi = 0;
@@ -344,7 +354,7 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __
       const int nx = cur + 1 == LS_NB ? 0 : cur + 1;
       if (LS_NB == 2) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-      prefetch_lanes(p, tile + gridDim.x, T, SSTAT(nx), SPC(nx), SREGS(nx), s_live, &mbar[nx]);
+      prefetch_lanes(p, tile + gridDim.x, TL, SSTAT(nx), SPC(nx), SREGS(nx), s_live, &mbar[nx]);
     }
     IPHASE(0);
     mbar_wait_parity(&mbar[cur], (parity >> cur) & 1u);
@@ -352,150 +362,159 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __
     IPHASE(1);
     uint8_t* const sstat = SSTAT(cur);
     uint32_t* const spc = SPC(cur);
-    const uint32_t g = tile * (uint32_t)T + t;
-    const bool valid = g < p.n_lanes;
-    uint8_t status = valid ? sstat[t] : (uint8_t)L_EXITED;
-    uint32_t pc = valid ? spc[t] : 0;
-    if (status == L_EXITED_NOW) status = L_EXITED;
-    bool running = valid && (status == L_RUNNING || status == L_WAITING);
-    const uint32_t inst = valid ? fast_div(g, p.n_magic) : 0;
-    const uint32_t tid = valid ? g - inst * p.n : 0;
-    const uint32_t cell_base = inst * p.cpi;
-    // byte address of this lane's register 0; register r is at rg + r*T*4
-    // (the live ones arrived by TMA)
-    const uint32_t rg = pin(smem_u32(SREGS(cur)) + 4u * (uint32_t)t);
-    const uint32_t oc = pin(smem_u32(ocell) + 4u * (uint32_t)t), ov = pin(smem_u32(oval) + 4u * (uint32_t)t);
-    const uint32_t orow = 4u * (uint32_t)T;  // overlay row stride (bytes)
-
-    if (running) status = L_RUNNING;
+    // per-lane state, lane h*T + t of the tile
+    uint32_t g[H], pc[H], inst[H], tid[H], cell_base[H], rg[H], oc[H], ov[H];
+    uint8_t status[H];
+    bool valid[H], running[H];
+    int n_own[H];
+    // instructions each lane executed in the interval (< 2^31 when !FUEL)
+    typename std::conditional<FUEL, unsigned long long, uint32_t>::type steps[H];
+    uint32_t nloads[H], nstores[H];
+    bool ovl_over[H];
+#pragma unroll
+    for (int h = 0; h < H; h++) {
+      const int l = h * T + t;
+      g[h] = tile * (uint32_t)TL + l;
+      valid[h] = g[h] < p.n_lanes;
+      status[h] = valid[h] ? sstat[l] : (uint8_t)L_EXITED;
+      pc[h] = valid[h] ? spc[l] : 0;
+      if (status[h] == L_EXITED_NOW) status[h] = L_EXITED;
+      running[h] = valid[h] && (status[h] == L_RUNNING || status[h] == L_WAITING);
+      if (running[h]) status[h] = L_RUNNING;
+      inst[h] = valid[h] ? fast_div(g[h], p.n_magic) : 0;
+      tid[h] = valid[h] ? g[h] - inst[h] * p.n : 0;
+      cell_base[h] = inst[h] * p.cpi;
+      // byte address of this lane's register 0; register r is at rg + r*TL*4
+      // (the live ones arrived by TMA)
+      rg[h] = pin(smem_u32(SREGS(cur)) + 4u * (uint32_t)l);
+      oc[h] = pin(smem_u32(ocell) + 4u * (uint32_t)l);
+      ov[h] = pin(smem_u32(oval) + 4u * (uint32_t)l);
+      n_own[h] = 0;
+      steps[h] = 0;
+      nloads[h] = 0;
+      nstores[h] = 0;
+      ovl_over[h] = false;
+    }
+    const uint32_t orow = 4u * (uint32_t)TL;  // overlay row stride (bytes)
     // the previous tile's bulk store of this warp's staged records has read them
     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     __syncwarp();
-    int n_own = 0;
-    // instructions this lane executed in the interval (< 2^31 when !FUEL)
-    typename std::conditional<FUEL, unsigned long long, uint32_t>::type steps = 0;
-    uint32_t nloads = 0, nstores = 0;
-    bool ovl_over = false;
-    Stage S{st_recs + (size_t)warp * p.stage_warp, 0, p.stage_warp};
+    Stage S{st_recs + (size_t)warp * SW, 0, SW};
 
-    // the instruction after the last executed one is fetched one step ahead
-    // (straight-line code: the next minimum pc is pc + 1), off the critical path
-    uint32_t pnext = 0xFFFFFFFFu;
-    uint4 nh = make_uint4(0, 0, 0, 0);
-    uint2 nt = make_uint2(0, 0);
     for (;;) {
-      const uint32_t minpc = __reduce_min_sync(FULL, running ? pc : 0xFFFFFFFFu);
+      uint32_t mine = 0xFFFFFFFFu;
+#pragma unroll
+      for (int h = 0; h < H; h++)
+        if (running[h]) mine = min(mine, pc[h]);
+      const uint32_t minpc = __reduce_min_sync(FULL, mine);
       if (minpc == 0xFFFFFFFFu) break;  // no lane of the warp is running (pcs are < 65536)
-      bool ex = running && pc == minpc;
+      bool ex[H];
+#pragma unroll
+      for (int h = 0; h < H; h++) ex[h] = running[h] && pc[h] == minpc;
       uint4 eh;
       uint2 et;
-      if (CODE_SMEM && !INTERP_PREFETCH) {
+      if (CODE_SMEM) {
         asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                      : "=r"(eh.x), "=r"(eh.y), "=r"(eh.z), "=r"(eh.w)
                      : "r"(code_h + 16u * minpc)
                      : "memory");
         asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(et.x), "=r"(et.y) : "r"(code_t + 8u * minpc) : "memory");
-        (void)nh; (void)nt; (void)pnext;
-      } else if (CODE_SMEM) {
-        eh = nh;
-        et = nt;
-        asm volatile(
-            "{\n .reg .pred p;\n setp.ne.u32 p, %6, %7;\n"
-            " @p ld.shared.v4.u32 {%0, %1, %2, %3}, [%8];\n @p ld.shared.v2.u32 {%4, %5}, [%9];\n}\n"
-            : "+r"(eh.x), "+r"(eh.y), "+r"(eh.z), "+r"(eh.w), "+r"(et.x), "+r"(et.y)
-            : "r"(minpc), "r"(pnext), "r"(code_h + 16u * minpc), "r"(code_t + 8u * minpc)
-            : "memory");
-        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(nh.x), "=r"(nh.y), "=r"(nh.z), "=r"(nh.w)
-                     : "r"(code_h + 16u * minpc + 16u)
-                     : "memory");
-        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nt.x), "=r"(nt.y) : "r"(code_t + 8u * minpc + 8u) : "memory");
-        pnext = minpc + 1;
       } else {
-        const Dec d = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + minpc), T, s_off, s_size);
+        const Dec d = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + minpc), TL, s_off, s_size);
         eh = d.h;
         et = d.t;
       }
       const uint32_t op = eh.x & 0x7F;
-      const uint32_t ra = rg + eh.y, rb = rg + eh.z, rc = rg + eh.w;  // this lane's operand registers
       const int32_t imm = (int32_t)et.x;
       if (eh.x & OP_WAIT) ld_async_wait();  // warp-uniform
-      if (FUEL && ex) {  // fuel check before executing (reading L17)
-        if (steps == p.fuel) {
-          emit_report(p, inst, -1, (int32_t)pc, tid, RC_FUEL);
-          running = false;
-          status = L_FUEL;
-          ex = false;
-        } else {
-          steps++;
+#pragma unroll
+      for (int h = 0; h < H; h++) {
+        if (FUEL && ex[h]) {  // fuel check before executing (reading L17)
+          if (steps[h] == p.fuel) {
+            emit_report(p, inst[h], -1, (int32_t)pc[h], tid[h], RC_FUEL);
+            running[h] = false;
+            status[h] = L_FUEL;
+            ex[h] = false;
+          } else {
+            steps[h]++;
+          }
         }
+        if (!FUEL) steps[h] += ex[h];
       }
-      if (!FUEL) steps += ex;
+      // this lane's operand registers
+#define RA(h) (rg[h] + eh.y)
+#define RB(h) (rg[h] + eh.z)
+#define RC(h) (rg[h] + eh.w)
+#define EACH(...) \
+  _Pragma("unroll") for (int h = 0; h < H; h++) if (ex[h]) { __VA_ARGS__; }
       // dispatch (warp-uniform): the heap accesses first, the rest through a switch
       if (op == RC_OP_LD) {
-        bool ok = false;
-        uint32_t cell = 0;
-        if (ex) {
-          const int32_t idx = lds32(rc);
-          if ((uint32_t)idx >= et.y) {  // also catches idx < 0
-            emit_report(p, inst, (int32_t)((eh.x >> 8) & 0xFF), idx, tid, RC_OOB);
-            running = false;
-            status = L_OOB;
-          } else {
-            cell = cell_base + et.x + (uint32_t)idx;
-            int32_t v = 0;
-            bool found = false;
-            for (int j = 0; j < n_own; j++)
-              if ((uint32_t)lds32(oc + j * orow) == cell) { v = lds32(ov + j * orow); found = true; }
-            if (found) sts32(ra, v);
-            else ld_async(ra, p.heap + cell);
-            pc++;
-            nloads++;
-            ok = true;
+#pragma unroll
+        for (int h = 0; h < H; h++) {
+          bool ok = false;
+          uint32_t cell = 0;
+          if (ex[h]) {
+            const int32_t idx = lds32(RC(h));
+            if ((uint32_t)idx >= et.y) {  // also catches idx < 0
+              emit_report(p, inst[h], (int32_t)((eh.x >> 8) & 0xFF), idx, tid[h], RC_OOB);
+              running[h] = false;
+              status[h] = L_OOB;
+            } else {
+              cell = cell_base[h] + et.x + (uint32_t)idx;
+              int32_t v = 0;
+              bool found = false;
+              for (int j = 0; j < n_own[h]; j++)
+                if ((uint32_t)lds32(oc[h] + j * orow) == cell) { v = lds32(ov[h] + j * orow); found = true; }
+              if (found) sts32(RA(h), v);
+              else ld_async(RA(h), p.heap + cell);
+              pc[h]++;
+              nloads[h]++;
+              ok = true;
+            }
           }
-        }
-        const unsigned m = __ballot_sync(FULL, ok);
-        if (m) {
-          if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane);
-          if (ok) S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, tid, 0, 0);
-          S.fill += __popc(m);
+          const unsigned m = __ballot_sync(FULL, ok);
+          if (m) {
+            if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane);
+            if (ok) S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, tid[h], 0, 0);
+            S.fill += __popc(m);
+          }
         }
       } else if (op == RC_OP_ST) {
-        if (ex) {
-          const int32_t idx = lds32(rb);
+        EACH({
+          const int32_t idx = lds32(RB(h));
           if ((uint32_t)idx >= et.y) {  // also catches idx < 0
-            emit_report(p, inst, (int32_t)((eh.x >> 8) & 0xFF), idx, tid, RC_OOB);
-            running = false;
-            status = L_OOB;
+            emit_report(p, inst[h], (int32_t)((eh.x >> 8) & 0xFF), idx, tid[h], RC_OOB);
+            running[h] = false;
+            status[h] = L_OOB;
           } else {
-            const uint32_t cell = cell_base + et.x + (uint32_t)idx;
+            const uint32_t cell = cell_base[h] + et.x + (uint32_t)idx;
             int j = 0;
-            while (j < n_own && (uint32_t)lds32(oc + j * orow) != cell) j++;
-            if (j == n_own) {
-              if (n_own < (int)OV) { sts32(oc + j * orow, (int32_t)cell); n_own++; }
-              else { ovl_over = true; j = -1; }
+            while (j < n_own[h] && (uint32_t)lds32(oc[h] + j * orow) != cell) j++;
+            if (j == n_own[h]) {
+              if (n_own[h] < (int)OV) { sts32(oc[h] + j * orow, (int32_t)cell); n_own[h]++; }
+              else { ovl_over[h] = true; j = -1; }
             }
-            if (j >= 0) sts32(ov + j * orow, lds32(rc));
-            pc++;
-            nstores++;
+            if (j >= 0) sts32(ov[h] + j * orow, lds32(RC(h)));
+            pc[h]++;
+            nstores[h]++;
           }
-        }
+        })
       } else switch (op & 31) {
         case RC_OP_LD: case RC_OP_ST: break;  // handled above
         case 0: case 28: case 29: case 30: case 31: break;  // unused (the validator rejects them)
-        case RC_OP_CONST: if (ex) { sts32(ra, imm); pc++; } break;
-        case RC_OP_MOV: if (ex) { sts32(ra, lds32(rb)); pc++; } break;
-        case RC_OP_TID: if (ex) { sts32(ra, (int32_t)tid); pc++; } break;
-        case RC_OP_SIZE: if (ex) { sts32(ra, imm); pc++; } break;
-        case RC_OP_ADDI: if (ex) { sts32(ra, wadd(lds32(rb), imm)); pc++; } break;
+        case RC_OP_CONST: EACH({ sts32(RA(h), imm); pc[h]++; }) break;
+        case RC_OP_MOV: EACH({ sts32(RA(h), lds32(RB(h))); pc[h]++; }) break;
+        case RC_OP_TID: EACH({ sts32(RA(h), (int32_t)tid[h]); pc[h]++; }) break;
+        case RC_OP_SIZE: EACH({ sts32(RA(h), imm); pc[h]++; }) break;
+        case RC_OP_ADDI: EACH({ sts32(RA(h), wadd(lds32(RB(h)), imm)); pc[h]++; }) break;
         // binary ALU ops, one case each (a flat jump table; int32 wrap, reading L7)
-#define ALU2(OPC, EXPR)                         \
-  case OPC:                                     \
-    if (ex) {                                   \
-      const int32_t x = lds32(rb), y = lds32(rc); \
-      sts32(ra, (EXPR));                        \
-      pc++;                                     \
-    }                                           \
+#define ALU2(OPC, EXPR)                                \
+  case OPC:                                            \
+    EACH({                                             \
+      const int32_t x = lds32(RB(h)), y = lds32(RC(h)); \
+      sts32(RA(h), (EXPR));                            \
+      pc[h]++;                                         \
+    })                                                 \
     break;
         ALU2(RC_OP_ADD, wadd(x, y))
         ALU2(RC_OP_SUB, (int32_t)((uint32_t)x - (uint32_t)y))
@@ -510,44 +529,48 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __
         ALU2(RC_OP_LAND, (int32_t)((x != 0) && (y != 0)))
 #undef ALU2
         case RC_OP_DIV: case RC_OP_MOD:
-          if (ex) {
-            const int32_t x = lds32(rb), y = lds32(rc);
+          EACH({
+            const int32_t x = lds32(RB(h)), y = lds32(RC(h));
             if (y == 0) {
-              emit_report(p, inst, -1, (int32_t)pc, tid, RC_DIV0);
-              running = false;
-              status = L_DIV0;
+              emit_report(p, inst[h], -1, (int32_t)pc[h], tid[h], RC_DIV0);
+              running[h] = false;
+              status[h] = L_DIV0;
             } else {
               int32_t v;
               if (op == RC_OP_DIV) v = (y == -1) ? (int32_t)(0u - (uint32_t)x) : x / y;
               else v = (y == -1) ? 0 : x % y;
-              sts32(ra, v);
-              pc++;
+              sts32(RA(h), v);
+              pc[h]++;
             }
-          }
+          })
           break;
-        case RC_OP_LNOT: if (ex) { sts32(ra, lds32(rb) == 0); pc++; } break;
-        case RC_OP_BAR: if (ex) { pc++; running = false; status = L_WAITING; } break;
-        case RC_OP_EXIT: if (ex) { running = false; status = L_EXITED_NOW; } break;
+        case RC_OP_LNOT: EACH({ sts32(RA(h), lds32(RB(h)) == 0); pc[h]++; }) break;
+        case RC_OP_BAR: EACH({ pc[h]++; running[h] = false; status[h] = L_WAITING; }) break;
+        case RC_OP_EXIT: EACH({ running[h] = false; status[h] = L_EXITED_NOW; }) break;
         case RC_OP_ASSUME:
-          if (ex) {
-            if (lds32(ra) == 0) { running = false; status = L_PRUNED; }
-            else pc++;
-          }
+          EACH({
+            if (lds32(RA(h)) == 0) { running[h] = false; status[h] = L_PRUNED; }
+            else pc[h]++;
+          })
           break;
         case RC_OP_ASSERT:
-          if (ex) {
-            if (lds32(ra) == 0) {
-              emit_report(p, inst, -1, (int32_t)pc, tid, RC_ASSERT);
-              running = false;
-              status = L_ASSERT;
+          EACH({
+            if (lds32(RA(h)) == 0) {
+              emit_report(p, inst[h], -1, (int32_t)pc[h], tid[h], RC_ASSERT);
+              running[h] = false;
+              status[h] = L_ASSERT;
             } else {
-              pc++;
+              pc[h]++;
             }
-          }
+          })
           break;
-        case RC_OP_BR: if (ex) pc = lds32(ra) != 0 ? (uint32_t)imm : et.y; break;
-        case RC_OP_JMP: if (ex) pc = (uint32_t)imm; break;
+        case RC_OP_BR: EACH({ pc[h] = lds32(RA(h)) != 0 ? (uint32_t)imm : et.y; }) break;
+        case RC_OP_JMP: EACH({ pc[h] = (uint32_t)imm; }) break;
       }
+#undef EACH
+#undef RA
+#undef RB
+#undef RC
     }
 
     IPHASE(2);
@@ -555,61 +578,66 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __
 
     // write records: one per distinct written cell; its final value (reading
     // L3) goes to the side table wval[slot][lane] read by detect
-    const int max_own = __reduce_max_sync(FULL, (unsigned)n_own);
-    for (int j = 0; j < max_own; j++) {
-      const bool has = j < n_own;
-      const unsigned m = __ballot_sync(FULL, has);
-      if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane);
-      if (has) {
-        const uint32_t cell = ocell[j * T + t];
-        S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, tid, (uint32_t)j, 1);
-        p.wval[(size_t)j * p.n_lanes + g] = oval[j * T + t];
-        p.wmap[cell] = 1;  // write-set map (filter.cu)
+#pragma unroll
+    for (int h = 0; h < H; h++) {
+      const int l = h * T + t;
+      const int max_own = __reduce_max_sync(FULL, (unsigned)n_own[h]);
+      for (int j = 0; j < max_own; j++) {
+        const bool has = j < n_own[h];
+        const unsigned m = __ballot_sync(FULL, has);
+        if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane);
+        if (has) {
+          const uint32_t cell = ocell[j * TL + l];
+          S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, tid[h], (uint32_t)j, 1);
+          p.wval[(size_t)j * p.n_lanes + g[h]] = oval[j * TL + l];
+          p.wmap[cell] = 1;  // write-set map (filter.cu)
+        }
+        S.fill += __popc(m);
       }
-      S.fill += __popc(m);
     }
 
     IPHASE(3);
     // fused A4: arrival node range per instance (fire-and-forget atomics,
-    // one pair per warp when the warp lies in one instance), suspended flag
-    const bool arrived = valid && (status == L_WAITING || status == L_EXITED_NOW);
-    const int32_t node = status == L_WAITING ? (int32_t)pc - 1 : NODE_EXIT;
-    const uint32_t inst0 = __shfl_sync(FULL, inst, 0);
-    const bool warp_uniform = __all_sync(FULL, !valid || inst == inst0);
-    if (warp_uniform) {
-      // nodes are >= -1; bias by 1 so unsigned reductions apply
-      const uint32_t nmin = __reduce_min_sync(FULL, arrived ? (uint32_t)(node + 1) : 0xFFFFFFFFu);
-      const uint32_t nmax = __reduce_max_sync(FULL, arrived ? (uint32_t)(node + 1) : 0u);
-      // push only what widens the range this warp already pushed for the
-      // instance (min/max atomics are idempotent): ~one pair per warp and
-      // instance instead of one per tile
-      const int32_t lo_ = (int32_t)(nmin - 1), hi_ = (int32_t)(nmax - 1);
-      if (nmin != 0xFFFFFFFFu && !(inst0 == a4_inst && lo_ >= a4_lo && hi_ <= a4_hi)) {
-        if (inst0 != a4_inst) { a4_inst = inst0; a4_lo = lo_; a4_hi = hi_; }
-        else { a4_lo = min(a4_lo, lo_); a4_hi = max(a4_hi, hi_); }
-        if (lane == 0) {
-          atomicMin(p.node_min + inst0, lo_);
-          atomicMax(p.node_max + inst0, hi_);
+    // pushed only when they widen what this warp already pushed), suspended flag
+#pragma unroll
+    for (int h = 0; h < H; h++) {
+      const bool arrived = valid[h] && (status[h] == L_WAITING || status[h] == L_EXITED_NOW);
+      const int32_t node = status[h] == L_WAITING ? (int32_t)pc[h] - 1 : NODE_EXIT;
+      const uint32_t inst0 = __shfl_sync(FULL, inst[h], 0);
+      const bool warp_uniform = __all_sync(FULL, !valid[h] || inst[h] == inst0);
+      if (warp_uniform) {
+        // nodes are >= -1; bias by 1 so unsigned reductions apply
+        const uint32_t nmin = __reduce_min_sync(FULL, arrived ? (uint32_t)(node + 1) : 0xFFFFFFFFu);
+        const uint32_t nmax = __reduce_max_sync(FULL, arrived ? (uint32_t)(node + 1) : 0u);
+        // min/max atomics are idempotent: ~one pair per warp and instance
+        const int32_t lo_ = (int32_t)(nmin - 1), hi_ = (int32_t)(nmax - 1);
+        if (nmin != 0xFFFFFFFFu && !(inst0 == a4_inst && lo_ >= a4_lo && hi_ <= a4_hi)) {
+          if (inst0 != a4_inst) { a4_inst = inst0; a4_lo = lo_; a4_hi = hi_; }
+          else { a4_lo = min(a4_lo, lo_); a4_hi = max(a4_hi, hi_); }
+          if (lane == 0) {
+            atomicMin(p.node_min + inst0, lo_);
+            atomicMax(p.node_max + inst0, hi_);
+          }
         }
+      } else if (arrived) {  // small work-groups: per-lane atomics
+        atomicMin(p.node_min + inst[h], node);
+        atomicMax(p.node_max + inst[h], node);
       }
-    } else if (arrived) {  // small work-groups: per-lane atomics
-      atomicMin(p.node_min + inst, node);
-      atomicMax(p.node_max + inst, node);
+      // statistics stay per lane until the end of the kernel
+      b_instr += steps[h];
+      b_loads += nloads[h];
+      b_stores += nstores[h];
+      b_ovl |= ovl_over[h];
+      b_wait |= status[h] == L_WAITING;
     }
 
     // ---- tile write-out into the block's staging chunk (a new chunk — one
     //      atomic — only when the current one is full; its tail is padded)
-    // statistics stay per lane until the end of the kernel
-    b_instr += steps;
-    b_loads += nloads;
-    b_stores += nstores;
-    b_ovl |= ovl_over;
     if (S.fill & 1) {  // even record counts: every warp's slice is a 16-byte bulk copy
       if (lane == 0) S.recs[S.fill] = REC_SENTINEL;
       S.fill++;
     }
     if (lane == 0) wcnt[warp] = S.fill;
-    b_wait |= status == L_WAITING;
     __syncthreads();
     IPHASE(4);
     if (warp == 0) {
@@ -644,18 +672,21 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __
     }
     // lane state out: status / pc into the shared rows (the live register
     // rows already are), then bulk stores of every row
-    sstat[t] = valid ? status : (uint8_t)L_EXITED;
-    spc[t] = pc;
+#pragma unroll
+    for (int h = 0; h < H; h++) {
+      sstat[h * T + t] = valid[h] ? status[h] : (uint8_t)L_EXITED;
+      spc[h * T + t] = pc[h];
+    }
     __syncthreads();
     IPHASE(5);
     if (t == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const size_t g0 = (size_t)tile * T;
-      bulk_s2g(p.status_out + g0, sstat, (uint32_t)T);
-      bulk_s2g(p.pc_out + g0, spc, (uint32_t)T * 4);
+      const size_t g0 = (size_t)tile * TL;
+      bulk_s2g(p.status_out + g0, sstat, (uint32_t)TL);
+      bulk_s2g(p.pc_out + g0, spc, (uint32_t)TL * 4);
       for (uint32_t i = 0; i < p.n_live; i++) {
         const uint32_t r = s_live[i];
-        bulk_s2g(p.regs_out + (size_t)r * p.reg_stride + g0, SREGS(cur) + (size_t)r * T, (uint32_t)T * 4);
+        bulk_s2g(p.regs_out + (size_t)r * p.reg_stride + g0, SREGS(cur) + (size_t)r * TL, (uint32_t)TL * 4);
       }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
@@ -708,29 +739,52 @@ __global__ void __launch_bounds__(256, INTERP_MIN_BLOCKS) interp_kernel(const __
     }
   }
   if (__any_sync(FULL, b_wait) && lane == 0) p.ctr->any_waiting = 1;
+#undef SREGS
+#undef SPC
+#undef SSTAT
 }
 
-size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem) {
-  const int W = T / 32;
-  size_t b = (size_t)LS_NB * p.n_regs * T * 4;     // register files (LS_NB buffers)
-  b += (size_t)LS_NB * T * 5 + ((8 * LS_NB + 15) & ~15);  // status / pc rows, mbarriers
-  b += (size_t)W * p.stage_warp * 8;                    // staging
-  b += code_in_smem ? (size_t)(p.n_instr + 1) * 24 : 0;  // pre-decoded program + pad entry
-  b += (size_t)p.ovl_cap * T * 8;                  // overlay
-  b += (size_t)p.n_arrays * 8;                     // array offsets / sizes
-  b += ((size_t)p.n_live + 3) & ~size_t(3);        // live register list
-  b += (size_t)W * 20 + 8;                         // warp counts, node range, instance (+align)
-  b += (size_t)W * 8 * 5;                          // warp bases (2) + 3 stats
+size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem, int H) {
+  const int W = T / 32, TL = H * T;
+  size_t b = (size_t)LS_NB * p.n_regs * TL * 4;                // register files (LS_NB buffers)
+  b += (size_t)LS_NB * TL * 5 + ((8 * LS_NB + 15) & ~15);      // status / pc rows, mbarriers
+  b += (size_t)W * H * p.stage_warp * 8;                        // staging
+  b += code_in_smem ? (size_t)(p.n_instr + 1) * 24 : 0;        // pre-decoded program + pad entry
+  b += (size_t)p.ovl_cap * TL * 8;                             // overlay
+  b += (size_t)p.n_arrays * 8;                                 // array offsets / sizes
+  b += ((size_t)p.n_live + 3) & ~size_t(3);                    // live register list
+  b += (size_t)W * 4 + 8 + 8;                                  // warp counts, pad count (+align)
+  b += (size_t)(W + 1) * 8;                                    // warp bases, pad start
   return b;
 }
+
+namespace {
+template <int H>
+cudaError_t launch_interp_h(const InterpParams& p, cudaStream_t s, int nsm) {
+  const bool code_smem = p.n_instr <= 2048;
+  int T = 256;
+  while (T > 32 && interp_smem_bytes(p, T, code_smem, H) > 96 * 1024) T >>= 1;
+  const size_t sm = interp_smem_bytes(p, T, code_smem, H);
+  auto kern = code_smem ? (p.fuel_check ? interp_kernel<true, true, H> : interp_kernel<true, false, H>)
+                        : (p.fuel_check ? interp_kernel<false, true, H> : interp_kernel<false, false, H>);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, sm);
+  const uint32_t tiles = (p.n_lanes + H * T - 1) / (H * T);
+  const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)std::max(1, per_sm) * nsm);
+  kern<<<grid, T, sm, s>>>(p);
+  launched();
+  return cudaGetLastError();
+}
+}  // namespace
 
 cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
   if (p.n_lanes == 0) return cudaSuccess;
   static bool attr_set = false;
   static int nsm = 0;
   if (!attr_set) {
-    for (auto f : {interp_kernel<true, true>, interp_kernel<false, true>, interp_kernel<true, false>,
-                   interp_kernel<false, false>}) {
+    for (auto f : {interp_kernel<true, true, 1>, interp_kernel<false, true, 1>, interp_kernel<true, false, 1>,
+                   interp_kernel<false, false, 1>, interp_kernel<true, true, 2>, interp_kernel<false, true, 2>,
+                   interp_kernel<true, false, 2>, interp_kernel<false, false, 2>}) {
       cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       if (e != cudaSuccess) return e;
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -740,19 +794,12 @@ cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     attr_set = true;
   }
-  const bool code_smem = p.n_instr <= 2048;
-  int T = 256;
-  while (T > 32 && interp_smem_bytes(p, T, code_smem) > 96 * 1024) T >>= 1;
-  const size_t sm = interp_smem_bytes(p, T, code_smem);
-  auto kern = code_smem ? (p.fuel_check ? interp_kernel<true, true> : interp_kernel<true, false>)
-                        : (p.fuel_check ? interp_kernel<false, true> : interp_kernel<false, false>);
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, sm);
-  const uint32_t tiles = (p.n_lanes + T - 1) / T;
-  const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)std::max(1, per_sm) * nsm);
-  kern<<<grid, T, sm, s>>>(p);
-  launched();
-  return cudaGetLastError();
+  // two work-items per thread when the batch has enough lanes to fill the GPU
+  // (test hook RC_DEBUG_INTERP_H=1|2 forces one variant; results never differ)
+  const char* force = getenv("RC_DEBUG_INTERP_H");
+  const int h = force ? (force[0] == '2' ? 2 : 1)
+                      : (INTERP_H == 2 && p.n_lanes >= 2u * 256u * (uint32_t)nsm ? 2 : 1);
+  return h == 2 ? launch_interp_h<2>(p, s, nsm) : launch_interp_h<1>(p, s, nsm);
 }
 
 }  // namespace rc

@@ -52,7 +52,7 @@ constexpr int OVL_CAP = 16;        // own-write overlay entries per work-item (s
 //   bits  4..1   overlay slot of a write (its final value is wval[slot][lane])
 //   bit      0   1 = write, 0 = read
 constexpr int REC_CELL_SHIFT = 32;
-constexpr uint32_t LANE_PAD = 256;  // lane-state rows are padded to multiples of this (TMA tiles)
+constexpr uint32_t LANE_PAD = 512;  // lane-state rows are padded to multiples of this (K1 tiles of <= 512 lanes)
 constexpr uint32_t MAX_WG = 1u << 27;
 // Division by a run-constant divisor d (work-group size, cells per instance):
 // magic = ceil(2^64 / d) (0 for d == 1); x / d == umulhi64(x, magic) exactly
@@ -157,7 +157,7 @@ struct DetectParams {
 };
 
 // ---- launchers (defined in the .cu files) --------------------------------
-size_t interp_smem_bytes(const InterpParams& p, int threads, bool code_in_smem);
+size_t interp_smem_bytes(const InterpParams& p, int threads, bool code_in_smem, int lanes_per_thread);
 cudaError_t launch_interp(const InterpParams& p, cudaStream_t s);
 
 // Write-set filter / compaction: from the staging buffer keep every write

@@ -307,6 +307,32 @@ def test_random_tiny_kernels(rc):
         assert_parity(g, o, ins)
 
 
+@pytest.mark.parametrize("h", ["1", "2"])
+def test_interp_lanes_per_thread(rc, monkeypatch, h):
+    """K1 runs one or two work-items per thread (two only for large batches
+    by default); RC_DEBUG_INTERP_H forces either so both are checked on small
+    cases: ragged tiles, every report kind, divergence, overlay hits, loops."""
+    monkeypatch.setenv("RC_DEBUG_INTERP_H", h)
+    rng = np.random.default_rng(7 + int(h))
+    for it in range(120):
+        n = int(rng.integers(1, 600))
+        pr = K.random_tiny_kernel(rng, n_arrays=2, n_regs=5, n_commands=int(rng.integers(3, 12)), size=5)
+        ins = [rng.integers(-3, 4, size=(int(rng.integers(1, 4)), 5)).astype(np.int32)]
+        ins.append(rng.integers(-3, 4, size=(ins[0].shape[0], 5)).astype(np.int32))
+        p, g, o = run_both(rc, pr, n, ins, fuel=500)
+        assert_parity(g, o, ins)
+    for src, n, ins in [(K.TREE_OFF_BY_ONE, 1024, I.cfg3_inputs(0, 5, 1024)),
+                        (K.BENIGN["K_last"], 256, I.cfg2_inputs(0, 9, 256)),
+                        (K.STENCIL, 1000, I.cfg5_inputs(0, 3, 1000)),
+                        (K.FIG1, 8, I.cfg1_inputs())]:
+        p, g, o = run_both(rc, src, n, ins)
+        assert_parity(g, o, ins)
+    ins = I.cfg4_inputs(0, 2, 700)
+    ins[3][:, 100:140] += 1
+    p, g, o = run_both(rc, K.random_stencil_kernel(5), 700, ins)
+    assert_parity(g, o, ins)
+
+
 def test_deterministic_repeats(rc):
     """repeated runs are byte-identical."""
     ins = I.cfg4_inputs(0, 4, 300)
