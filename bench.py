@@ -205,12 +205,14 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
     prof_sum = None
     accesses = 0
+    instrs = 0
     n_reports = 0
     with Clocks(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
             r, reps, st = step(profile=not args.no_profile)
             accesses += st["checked_accesses"]
+            instrs += st["instructions"]
             n_reports = len(reps)
             if r.profile:
                 if prof_sum is None:
@@ -319,6 +321,9 @@ def main():
                        "l2": "inputs 4.3 GB/GPU >> 126 MB L2 (no flush needed)",
                        "checked_accesses_per_step": accesses // args.steps, "reports_per_step": n_reports},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+            "interpreter": {"bytecode_instr_per_s": instrs / args.steps / (ms_step / 1000),
+                            "bytecode_instr_per_step": instrs / args.steps,
+                            "bound": "issue (ALU/LSU pipes; ncu sm__inst_executed.avg.per_cycle_active in profiles/)"},
             "clocks": clk.summary(), "kernels": kernels}
     print(json.dumps(line), flush=True)
     if world > 1:
