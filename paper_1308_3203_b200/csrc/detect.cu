@@ -140,6 +140,9 @@ __device__ __noinline__ void serial_segment(const DetectParams& p, uint32_t i, u
 }
 }  // namespace
 
+#ifndef DET_MINB  // resident blocks per SM (register cap)
+#define DET_MINB 2
+#endif
 #ifndef DET_ROUNDS_OPT
 #define DET_ROUNDS_OPT 8
 #endif
@@ -241,6 +244,12 @@ __device__ __forceinline__ void detect_chunk(const DetectParams& p, uint64_t wg,
     const unsigned heads = __ballot_sync(FULL, head);
     const unsigned tails = __ballot_sync(FULL, tail);
     const unsigned inbm = __ballot_sync(FULL, inb);
+    if (!carry && (heads & tails) == inbm) {
+      // fast path: every record of the round is alone in its cell — a lone
+      // writer only commits (no report is possible), a lone read does nothing
+      if (inb && rec_w(v)) p.heap[key] = wv[rd];
+      continue;
+    }
     // hi = last lane of my segment inside this round
     const unsigned t_at_or_after = tails & (~0u << lane);
     const int last_inb = 31 - __clz(inbm);
@@ -334,7 +343,7 @@ __device__ __noinline__ void boundary_tail(const DetectParams& p) {
 // device memory (no host sync).  Skips the detection (no commit) when this
 // interval's log overflowed or K1's reports overflowed: the host then re-runs
 // the interval from the saved lane state on an untouched heap.
-__global__ void __launch_bounds__(256) detect_kernel(const DetectParams p) {
+__global__ void __launch_bounds__(256, DET_MINB) detect_kernel(const DetectParams p) {
   if (p.ctr->abort) return;  // speculative interval after one that needs the host (uniform)
   if (!(p.ctr->log_overflow || p.ctr->k1_reports > p.report_cap)) {
     const uint32_t n_records = (uint32_t)p.ctr->kept_count;
