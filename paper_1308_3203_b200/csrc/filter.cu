@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
     for (int j = 0; j < F_ITEMS; j++) {
       const uint64_t i = b0 + (uint64_t)j * F_THREADS + t;
       keep[j] = rec[j] != REC_SENTINEL &&
-                (p.keep_all || (rec[j] & 1) || __ldg(p.wmap + (rec[j] >> REC_CELL_SHIFT)) != 0);
+                (p.keep_all || (rec[j] & 1) || __ldg(p.wmap + (rec[j] >> REC_CELL_SHIFT)) == p.wtag);
     }
     uint32_t mine = 0;
 #pragma unroll

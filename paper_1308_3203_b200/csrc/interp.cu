@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
           const uint32_t cell = ocell[j * TL + l];
           S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, tid[h], (uint32_t)j, 1);
           p.wval[(size_t)j * p.n_lanes + g[h]] = oval[j * TL + l];
-          p.wmap[cell] = 1;  // write-set map (filter.cu)
+          p.wmap[cell] = p.wtag;  // write-set map (filter.cu)
         }
         S.fill += __popc(m);
       }

@@ -269,6 +269,9 @@ void analyze(rc_program* P) {
   }
   std::vector<uint64_t> keep(words, 0);
   for (uint32_t k = 0; k < words; k++) keep[k] = live[k];  // live_in(0)
+  P->live_at_entry.clear();
+  for (uint32_t r = 0; r < R; r++)
+    if (live[r / 64] >> (r % 64) & 1) P->live_at_entry.push_back((uint8_t)r);
   for (uint32_t pc = 0; pc + 1 < N; pc++)
     if (P->code[pc].op == RC_OP_BAR)
       for (uint32_t k = 0; k < words; k++) keep[k] |= live[(pc + 1) * (size_t)words + k];

@@ -75,7 +75,6 @@ struct DevCounters {
   unsigned long long stage_count;   // staging slots reserved this interval (records + sentinels; per attempt)
   unsigned long long staged_recs;   // access records staged this interval (per attempt)
   unsigned long long kept_count;    // records the write-set filter passed to the sort
-  unsigned long long report_count;  // reports appended (whole run, rolled back on retry)
   unsigned long long iv_loads;      // per attempt
   unsigned long long iv_stores;
   unsigned long long iv_instr;
@@ -84,6 +83,8 @@ struct DevCounters {
   unsigned int any_waiting;         // per interval
   unsigned int diverged;            // per interval
   unsigned long long k1_reports;    // report_count after K1 (snapshot taken by the filter)
+  // ---- fields above: zeroed per interval attempt (one memset, runtime.cu)
+  unsigned long long report_count;  // reports appended (whole run, rolled back on retry)
   unsigned long long lanes_final[8];
   // Speculation (runtime.cu): the host queues interval k+1 before it has seen
   // interval k's counters.  A4's last block sets `abort` when interval k needs
@@ -128,7 +129,8 @@ struct InterpParams {
   // it into the sort buffer
   uint64_t* stage;            // [stage_cap] records (make_rec) and sentinels
   unsigned long long stage_cap;
-  uint8_t* wmap;              // [I_b * cpi] 1 = cell written in this interval
+  uint8_t* wmap;              // [I_b * cpi] == wtag: cell written in this interval
+  uint8_t wtag;               // this interval's tag (1..255; the map is zeroed when tags wrap)
   int32_t* wval;              // [ovl_cap][n_lanes] final value of each written overlay slot
   rc_report* reports;
   unsigned long long report_cap;
@@ -167,6 +169,7 @@ cudaError_t launch_interp(const InterpParams& p, cudaStream_t s);
 struct FilterParams {
   const uint64_t* stage;
   const uint8_t* wmap;
+  uint8_t wtag;           // wmap[c] == wtag: c written in this interval
   uint64_t* out;          // sort buffer, [0, kept_count)
   uint32_t* hist;         // [4][256]
   int passes;
@@ -185,6 +188,7 @@ struct SortWorkspace {
   uint32_t* tile_ctr = nullptr;    // [4] dynamic tile counters
   size_t status_tiles = 0;
   uint32_t epoch = 0;              // look-back epoch (never reset memory)
+  bool reset_tile_ctr = true;      // false: the caller zeroes tile_ctr (per-interval memset)
 };
 #ifndef SORT_THREADS_OPT
 #define SORT_THREADS_OPT 256
@@ -263,6 +267,7 @@ struct rc_program {
   // static analysis (program.cpp analyze()): sizing only, no semantic effect
   std::vector<rc::Ins> dev_code;    // code with OP_WAIT flags (uploaded for K1)
   std::vector<uint8_t> live_regs;  // registers live across a barrier (+ live at pc 0)
+  std::vector<uint8_t> live_at_entry;  // live_in(pc 0): the rows zeroed at a batch start (reading L18)
   int ovl_cap = rc::OVL_CAP;       // max distinct cells written per work-item per interval
   int rec_bound = -1;              // max log records per work-item per interval (-1 unbounded)
   int64_t instr_bound = -1;        // max instructions per work-item per interval (-1 unbounded)

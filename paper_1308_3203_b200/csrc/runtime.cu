@@ -107,11 +107,16 @@ struct DevBuf {
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
+// interval scratch layout (one memset per interval attempt): digit histograms
+// [4][256] u32, sort tile counters, then DevCounters
+constexpr size_t CTR_OFF = 4096 + 64;
+
 struct rc_workspace {
   int device = -1;
   DevBuf code, arr_off, arr_size, heap;
   DevBuf regs[2], pc[2], status[2], live;
-  DevBuf log, log_alt, wval, wmap, sort_status, sort_small;
+  DevBuf log, log_alt, wval, wmap, sort_status, ctr_block;
+  uint8_t wtag = 0;  // write-set map tag of the last interval attempt
   DevBuf reports, reports_scratch;
   DevBuf inst_tmp;  // node_min | node_max | first_tid | second_tid | inst_flag  ([I_b] each)
   DevBuf ctr;
@@ -122,7 +127,7 @@ struct rc_workspace {
   ~rc_workspace() {
     for (DevBuf* b : {&code, &arr_off, &arr_size, &heap, &regs[0], &regs[1], &pc[0], &pc[1], &status[0],
                       &status[1], &live, &log, &log_alt, &wval, &wmap, &sort_status,
-                      &sort_small, &reports, &reports_scratch, &inst_tmp, &ctr})
+                      &ctr_block, &reports, &reports_scratch, &inst_tmp})  // (ctr is a view into ctr_block)
       b->release();
     if (h_ctr) cudaFreeHost(h_ctr);
     for (cudaEvent_t e : iv_done)
@@ -266,13 +271,17 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     CK(W.live.ensure(std::max<size_t>(1, P->live_regs.size())));
     if (!P->live_regs.empty())
       CK(cudaMemcpy(W.live.p, P->live_regs.data(), P->live_regs.size(), cudaMemcpyHostToDevice));
-    CK(W.ctr.ensure(sizeof(DevCounters)));
+    // interval scratch in one allocation, zeroed by one memset per interval:
+    // [digit histograms 4 KB][sort tile counters, 64 B][DevCounters]
+    CK(W.ctr_block.ensure(CTR_OFF + sizeof(DevCounters)));
+    W.ctr.p = static_cast<char*>(W.ctr_block.p) + CTR_OFF;
+    W.ctr.bytes = sizeof(DevCounters);
     CK(cudaMallocHost(&W.h_ctr, 4 * sizeof(DevCounters)));
     for (cudaEvent_t& e : W.iv_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    CK(W.sort_small.ensure(4096 * 4));
-    W.sort.hist = W.sort_small.as<uint32_t>();
-    W.sort.bin_off = W.sort.hist + 1024;
-    W.sort.tile_ctr = W.sort.bin_off + 1024;
+    W.sort.hist = W.ctr_block.as<uint32_t>();
+    W.sort.bin_off = nullptr;  // each pass scans its counts itself
+    W.sort.tile_ctr = W.sort.hist + 1024;
+    W.sort.reset_tile_ctr = false;
   }
   rc_workspace& W = *P->ws;
   W.prof.reset();
@@ -311,7 +320,9 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     }
     CK(W.inst_tmp.ensure((uint64_t)I_b * 20));
     CK(W.wval.ensure(std::max<uint64_t>(1, L_max * (uint64_t)P->ovl_cap) * 4));
+    const void* wmap_before = W.wmap.p;
     CK(W.wmap.ensure(std::max<uint64_t>(1, (uint64_t)I_b * cpi)));
+    if (W.wmap.p != wmap_before) W.wtag = 0;  // new memory: zero it before the next tag is used
   }
   const int passes = (key_bits + 7) / 8;
   // test hook: start from tiny log / report buffers so the grow-and-retry
@@ -418,7 +429,11 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     if (L) {
       CK(cudaMemsetAsync(W.status[cur].p, 0, reg_stride, s));
       CK(cudaMemsetAsync(W.pc[cur].p, 0, (size_t)reg_stride * 4, s));
-      CK(cudaMemsetAsync(W.regs[cur].p, 0, (size_t)reg_stride * P->n_regs * 4, s));  // registers start at 0 (L18)
+      // registers start at 0 (reading L18): only a register read before it is
+      // written in interval 0 (live_in(pc 0)) can observe it; the other rows K1
+      // loads are overwritten before any read
+      for (uint8_t r : P->live_at_entry)
+        CK(cudaMemsetAsync(W.regs[cur].as<int32_t>() + (size_t)r * reg_stride, 0, (size_t)reg_stride * 4, s));
     }
     // ---- one interval = K1 → filter → sort → detect → A4 (+ verdict), then
     //      the counters to a pinned slot and an event.  No kernel needs a host
@@ -456,10 +471,13 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
 #define EQ(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
       if (gaps) { gap_ev.push_back({}); cudaEventCreate(&gap_ev.back()[0]); cudaEventCreate(&gap_ev.back()[1]); cudaEventRecord(gap_ev.back()[0], s); }
       if (opt.profile) W.prof.on = (prof_intervals++ % prof_every) == 0;  // sampled interval profile
-      if (cpi) EQ(cudaMemsetAsync(W.wmap.p, 0, (size_t)nb * cpi, s));  // write-set map of this interval
-      EQ(cudaMemsetAsync(dctr, 0, offsetof(DevCounters, report_count), s));
-      EQ(cudaMemsetAsync(W.sort.hist, 0, 4 * 256 * sizeof(uint32_t), s));  // the filter fuses the histograms
-      EQ(cudaMemsetAsync(&dctr->iv_loads, 0, offsetof(DevCounters, lanes_final) - offsetof(DevCounters, iv_loads), s));
+      // write-set map: a fresh tag per interval attempt; zeroed only when the tags wrap
+      if (++W.wtag == 0 || W.wtag == 1) {
+        W.wtag = 1;
+        if (cpi) EQ(cudaMemsetAsync(W.wmap.p, 0, W.wmap.bytes, s));
+      }
+      // histograms, sort tile counters and the per-attempt counters
+      EQ(cudaMemsetAsync(W.ctr_block.p, 0, CTR_OFF + offsetof(DevCounters, report_count), s));
       InterpParams ip;
       ip.code = W.code.as<Ins>();
       ip.n_instr = P->n_instr;
@@ -492,6 +510,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       ip.stage = W.log_alt.as<uint64_t>();
       ip.stage_cap = log_cap;
       ip.wmap = W.wmap.as<uint8_t>();
+      ip.wtag = W.wtag;
       ip.wval = W.wval.as<int32_t>();
       ip.reports = W.reports.as<rc_report>();
       ip.report_cap = rep_cap;
@@ -505,6 +524,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       FilterParams fp;
       fp.stage = W.log_alt.as<uint64_t>();
       fp.wmap = W.wmap.as<uint8_t>();
+      fp.wtag = W.wtag;
       fp.out = W.log.as<uint64_t>();
       fp.hist = W.sort.hist;
       fp.passes = passes;

@@ -550,7 +550,7 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, const unsigned long long* 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, onesweep_kernel<true>, SORT_THREADS, sizeof(SortSmem<2>));
     if (per_sm < 1) per_sm = 1;
   }
-  cudaMemsetAsync(ws.tile_ctr, 0, 4 * sizeof(uint32_t), s);
+  if (ws.reset_tile_ctr) cudaMemsetAsync(ws.tile_ctr, 0, 4 * sizeof(uint32_t), s);
   if (!hist_ready) {  // (each pass scans its digit counts itself)
     if (prof) prof->begin(s);
     cudaMemsetAsync(ws.hist, 0, 4 * RADIX * sizeof(uint32_t), s);
