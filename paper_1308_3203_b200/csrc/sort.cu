@@ -116,7 +116,10 @@ void sort_phase_io(unsigned long long* out, bool reset) {
 __device__ __forceinline__ uint32_t dev_count(uint32_t n_host, const unsigned long long* n_a,
                                               const unsigned long long* n_b) {
   if (!n_a) return n_host;
-  return (uint32_t)(*n_a + (n_b ? *n_b : 0ull));
+  // the device count may exceed the buffer when the interval overflowed (K1
+  // reserves sort-buffer room with atomics; the interval is then re-run and
+  // this sort's output unused): never walk past the buffer / look-back words
+  return (uint32_t)umin64(*n_a + (n_b ? *n_b : 0ull), n_host);
 }
 
 __global__ void __launch_bounds__(256) hist_kernel(const uint64_t* __restrict__ recs, uint32_t n_host,
