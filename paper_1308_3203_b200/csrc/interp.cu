@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
     uint8_t* const sstat = SSTAT(cur);
     uint32_t* const spc = SPC(cur);
     // per-lane state, lane h*T + t of the tile
-    uint32_t g[H], pc[H], inst[H], tid[H], cell_base[H], rg[H], oc[H], ov[H];
+    uint32_t g[H], pc[H], inst[H], tid[H], cell_base[H];
     uint8_t status[H];
     bool valid[H], running[H];
     int n_own[H];
@@ -384,11 +384,6 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
       inst[h] = valid[h] ? fast_div(g[h], p.n_magic) : 0;
       tid[h] = valid[h] ? g[h] - inst[h] * p.n : 0;
       cell_base[h] = inst[h] * p.cpi;
-      // byte address of this lane's register 0; register r is at rg + r*TL*4
-      // (the live ones arrived by TMA)
-      rg[h] = pin(smem_u32(SREGS(cur)) + 4u * (uint32_t)l);
-      oc[h] = pin(smem_u32(ocell) + 4u * (uint32_t)l);
-      ov[h] = pin(smem_u32(oval) + 4u * (uint32_t)l);
       n_own[h] = 0;
       steps[h] = 0;
       nloads[h] = 0;
@@ -396,6 +391,15 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
       ovl_over[h] = false;
     }
     const uint32_t orow = 4u * (uint32_t)TL;  // overlay row stride (bytes)
+    // byte address of lane t's register 0 (lane h*T + t: + 4*T*h); register r
+    // is at + r*TL*4 (the live ones arrived by TMA); the overlay cells and
+    // values likewise (oval follows ocell)
+    const uint32_t rg0 = pin(smem_u32(SREGS(cur)) + 4u * (uint32_t)t);
+    const uint32_t oc0 = pin(smem_u32(ocell) + 4u * (uint32_t)t);
+    const uint32_t ovd = OV * orow;  // ocell -> oval
+#define RG(h) (rg0 + (uint32_t)(h) * 4u * (uint32_t)T)
+#define OC(h) (oc0 + (uint32_t)(h) * 4u * (uint32_t)T)
+#define OVL(h) (OC(h) + ovd)
     // the previous tile's bulk store of this warp's staged records has read them
     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     __syncwarp();
@@ -442,9 +446,9 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
         if (!FUEL) steps[h] += ex[h];
       }
       // this lane's operand registers
-#define RA(h) (rg[h] + eh.y)
-#define RB(h) (rg[h] + eh.z)
-#define RC(h) (rg[h] + eh.w)
+#define RA(h) (RG(h) + eh.y)
+#define RB(h) (RG(h) + eh.z)
+#define RC(h) (RG(h) + eh.w)
 #define EACH(...) \
   _Pragma("unroll") for (int h = 0; h < H; h++) if (ex[h]) { __VA_ARGS__; }
       // dispatch (warp-uniform): the heap accesses first, the rest through a switch
@@ -464,7 +468,7 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
               int32_t v = 0;
               bool found = false;
               for (int j = 0; j < n_own[h]; j++)
-                if ((uint32_t)lds32(oc[h] + j * orow) == cell) { v = lds32(ov[h] + j * orow); found = true; }
+                if ((uint32_t)lds32(OC(h) + j * orow) == cell) { v = lds32(OVL(h) + j * orow); found = true; }
               if (found) sts32(RA(h), v);
               else ld_async(RA(h), p.heap + cell);
               pc[h]++;
@@ -489,12 +493,12 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
           } else {
             const uint32_t cell = cell_base[h] + et.x + (uint32_t)idx;
             int j = 0;
-            while (j < n_own[h] && (uint32_t)lds32(oc[h] + j * orow) != cell) j++;
+            while (j < n_own[h] && (uint32_t)lds32(OC(h) + j * orow) != cell) j++;
             if (j == n_own[h]) {
-              if (n_own[h] < (int)OV) { sts32(oc[h] + j * orow, (int32_t)cell); n_own[h]++; }
+              if (n_own[h] < (int)OV) { sts32(OC(h) + j * orow, (int32_t)cell); n_own[h]++; }
               else { ovl_over[h] = true; j = -1; }
             }
-            if (j >= 0) sts32(ov[h] + j * orow, lds32(RC(h)));
+            if (j >= 0) sts32(OVL(h) + j * orow, lds32(RC(h)));
             pc[h]++;
             nstores[h]++;
           }
@@ -571,6 +575,9 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
 #undef RA
 #undef RB
 #undef RC
+#undef RG
+#undef OC
+#undef OVL
     }
 
     IPHASE(2);
