@@ -187,7 +187,8 @@ struct SortWorkspace {
   unsigned long long* status = nullptr;  // [tiles][256] decoupled look-back words
   uint32_t* tile_ctr = nullptr;    // [4] dynamic tile counters
   size_t status_tiles = 0;
-  uint32_t epoch = 0;              // look-back epoch (never reset memory)
+  uint32_t epoch = 0;              // look-back epoch (memory cleared only when it wraps)
+  int status_fmt = -1;             // word format of the last pass (0: 64-bit, 1: 32-bit)
   bool reset_tile_ctr = true;      // false: the caller zeroes tile_ctr (per-interval memset)
 };
 #ifndef SORT_THREADS_OPT

@@ -346,6 +346,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       if (e != cudaSuccess) return e;
       e = cudaMemsetAsync(W.sort_status.p, 0, W.sort_status.bytes, s);
       W.sort.epoch = 0;
+      W.sort.status_fmt = -1;
       if (e != cudaSuccess) return e;
     }
     W.sort.status = W.sort_status.as<unsigned long long>();

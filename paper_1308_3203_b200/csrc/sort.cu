@@ -16,7 +16,10 @@
 //   * per digit: publish the tile's count (AGGREGATE), look back over
 //     predecessors until an INCLUSIVE prefix is found, publish INCLUSIVE,
 //   * scatter to shared memory in digit order and write out coalesced runs.
-// Status words carry an epoch so the look-back array is never re-zeroed.
+// Status words carry an epoch so the look-back array is re-zeroed only when
+// the epoch wraps (32-bit words for sorts of < 2^26 records, else 64-bit).
+#include <cstdlib>
+
 #include "rc_internal.h"
 
 #ifndef SORT_LB
@@ -40,6 +43,9 @@
 #ifndef SORT_CLAIM_LATE  // 1: claim the next tile after the look-back, 0: one tile ahead
 #define SORT_CLAIM_LATE 1
 #endif
+#ifndef SORT_W32  // 1: 32-bit look-back status words for sorts of < 2^26 records
+#define SORT_W32 1
+#endif
 #ifndef SORT_MINB  // resident blocks per SM of the persistent pass (smem: ~72 KB each)
 #define SORT_MINB 2
 #endif
@@ -51,8 +57,7 @@ constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr int RADIX = 256;
 constexpr int WARPS = SORT_THREADS / 32;
 constexpr int WARP_ITEMS = SORT_ITEMS * 32;
-constexpr unsigned long long FLAG_AGG = 1ull << 62, FLAG_INC = 2ull << 62;
-constexpr unsigned long long VAL_MASK = (1ull << 40) - 1;
+constexpr uint32_t FLAG_AGG = 1, FLAG_INC = 2;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -67,7 +72,43 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void st_relaxed(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// Decoupled look-back status word: flag (AGGREGATE / INCLUSIVE), epoch (so
+// the array is never re-zeroed between passes), value.
+//   64-bit: flag 2 | epoch 22 | value 40
+//   32-bit: flag 2 | epoch 4  | value 26   (sorts of < 2^26 records: half the
+//           look-back bytes per predecessor)
+template <typename W>
+struct LB;
+template <>
+struct LB<unsigned long long> {
+  __device__ static unsigned long long make(uint32_t flag, uint32_t ep, unsigned long long v) {
+    return ((unsigned long long)flag << 62) | ((unsigned long long)(ep & 0x3FFFFF) << 40) | v;
+  }
+  __device__ static bool ready(unsigned long long w, uint32_t ep) {
+    return ((w >> 40) & 0x3FFFFF) == (ep & 0x3FFFFF) && (w >> 62) != 0;
+  }
+  __device__ static bool inclusive(unsigned long long w) { return (w >> 62) == 2; }
+  __device__ static unsigned long long value(unsigned long long w) { return w & ((1ull << 40) - 1); }
+};
+template <>
+struct LB<unsigned> {
+  __device__ static unsigned make(uint32_t flag, uint32_t ep, unsigned long long v) {
+    return (flag << 30) | ((ep & 0xF) << 26) | (unsigned)v;
+  }
+  __device__ static bool ready(unsigned w, uint32_t ep) { return ((w >> 26) & 0xF) == (ep & 0xF) && (w >> 30) != 0; }
+  __device__ static bool inclusive(unsigned w) { return (w >> 30) == 2; }
+  __device__ static unsigned long long value(unsigned w) { return w & ((1u << 26) - 1); }
+};
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -219,21 +260,21 @@ __device__ __forceinline__ unsigned match_digit(uint32_t d, unsigned valid_mask)
 // the current one is processed.  Otherwise: one tile per block (grid = tiles;
 // the hardware block scheduler staggers tiles, which keeps look-back walks
 // short) with a single buffer.
-template <bool PERSISTENT>
+template <bool PERSISTENT, typename SWORD>
 __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256 / SORT_THREADS) onesweep_kernel(const uint64_t* __restrict__ in,
                                                                    uint64_t* __restrict__ out, uint32_t n_host,
                                                                    const unsigned long long* n_a,
                                                                    const unsigned long long* n_b, int shift,
                                                                    const uint32_t* __restrict__ hist,
-                                                                   unsigned long long* __restrict__ status,
+                                                                   SWORD* __restrict__ status,
                                                                    uint32_t* __restrict__ tile_ctr, uint32_t epoch) {
+  using L = LB<SWORD>;
   constexpr int NB = PERSISTENT ? 2 : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SortSmem<NB>& S = *reinterpret_cast<SortSmem<NB>*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const uint32_t n = dev_count(n_host, n_a, n_b);
   const uint32_t n_tiles = (uint32_t)((n + SORT_TILE - 1) / SORT_TILE);
-  const unsigned long long ep = (unsigned long long)(epoch & 0x3FFFFF) << 40;
   const int dsh = REC_CELL_SHIFT + shift;
   uint32_t claimed = 0xFFFFFFFFu;  // thread 0: tile claimed ahead
 
@@ -369,18 +410,15 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
     const int d = t < RADIX ? t : RADIX - 1;
     const bool dig = t < RADIX;
     const uint32_t tile_cnt = dig ? S.thist[0][d] + S.thist[1][d] : 0u;
-    unsigned long long* my_status = status + (size_t)tile * RADIX + d;
-    if (dig) {
-      if (tile == 0) st_relaxed(my_status, FLAG_INC | ep | tile_cnt);
-      else st_relaxed(my_status, FLAG_AGG | ep | tile_cnt);
-    }
+    SWORD* my_status = status + (size_t)tile * RADIX + d;
+    if (dig) st_relaxed(my_status, L::make(tile == 0 ? FLAG_INC : FLAG_AGG, epoch, tile_cnt));
     const uint32_t excl_tile = block_excl_scan(tile_cnt, S.wt);  // tile-local start of digit d
 #if SORT_EARLY_LB
     // first look-back round issued now; its latency hides behind rank + scatter
-    unsigned long long esw[SORT_EARLY_LB];
+    SWORD esw[SORT_EARLY_LB];
 #pragma unroll
     for (int j = 0; j < SORT_EARLY_LB; j++)
-      esw[j] = dig && (int64_t)tile - 1 - j >= 0 ? ld_relaxed(status + (size_t)(tile - 1 - j) * RADIX + d) : 0ull;
+      esw[j] = dig && (int64_t)tile - 1 - j >= 0 ? ld_relaxed(status + (size_t)(tile - 1 - j) * RADIX + d) : (SWORD)0;
 #endif
     PHASE_T(4);
 
@@ -437,18 +475,17 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
     //      INCLUSIVE), then publish our INCLUSIVE prefix
     unsigned long long excl = 0;
     if (tile > 0 && dig) {
-      constexpr int LB = SORT_LB;  // predecessors per L2 round trip
+      constexpr int LBN = SORT_LB;  // predecessors per L2 round trip
       int64_t tp = (int64_t)tile - 1;
       bool done = false;
 #if SORT_EARLY_LB
 #pragma unroll
       for (int j = 0; j < SORT_EARLY_LB; j++) {
         if (done) break;
-        const bool ready = ((esw[j] >> 40) & 0x3FFFFF) == (epoch & 0x3FFFFF) && (esw[j] >> 62) != 0;
-        if (!ready) break;
-        excl += esw[j] & VAL_MASK;
+        if (!L::ready(esw[j], epoch)) break;
+        excl += L::value(esw[j]);
         tp--;
-        if ((esw[j] >> 62) == 2) done = true;
+        if (L::inclusive(esw[j])) done = true;
       }
 #endif
 #ifdef SORT_PHASE_TIMING
@@ -458,13 +495,13 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
 #ifdef SORT_PHASE_TIMING
         st_rounds++;
 #endif
-        unsigned long long sw[LB];
+        SWORD sw[LBN];
 #pragma unroll
-        for (int j = 0; j < LB; j++) sw[j] = tp - j >= 0 ? ld_relaxed(status + (size_t)(tp - j) * RADIX + d) : 0ull;
+        for (int j = 0; j < LBN; j++) sw[j] = tp - j >= 0 ? ld_relaxed(status + (size_t)(tp - j) * RADIX + d) : (SWORD)0;
 #pragma unroll
-        for (int j = 0; j < LB; j++) {
+        for (int j = 0; j < LBN; j++) {
           if (done) break;
-          const bool ready = ((sw[j] >> 40) & 0x3FFFFF) == (epoch & 0x3FFFFF) && (sw[j] >> 62) != 0;
+          const bool ready = L::ready(sw[j], epoch);
           if (!ready) {  // re-poll from this predecessor
 #ifdef SORT_PHASE_TIMING
             st_notready++;
@@ -474,12 +511,12 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
 #endif
             break;
           }
-          excl += sw[j] & VAL_MASK;
+          excl += L::value(sw[j]);
           tp--;
-          if ((sw[j] >> 62) == 2) done = true;
+          if (L::inclusive(sw[j])) done = true;
         }
       }
-      st_relaxed(my_status, FLAG_INC | ep | (excl + tile_cnt));
+      st_relaxed(my_status, L::make(FLAG_INC, epoch, excl + tile_cnt));
 #ifdef SORT_PHASE_TIMING
       st_walk = (uint32_t)((int64_t)tile - 1 - tp);
       {
@@ -542,15 +579,18 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, const unsigned long long* 
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(onesweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(SortSmem<2>));
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(SortSmem<1>));
-    if (e != cudaSuccess) return e;
-    cudaFuncSetAttribute(onesweep_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(onesweep_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, onesweep_kernel<true>, SORT_THREADS, sizeof(SortSmem<2>));
+    const void* ks[4] = {(const void*)onesweep_kernel<true, unsigned long long>,
+                         (const void*)onesweep_kernel<true, unsigned>,
+                         (const void*)onesweep_kernel<false, unsigned long long>,
+                         (const void*)onesweep_kernel<false, unsigned>};
+    for (int i = 0; i < 4; i++) {
+      cudaError_t e = cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           i < 2 ? (int)sizeof(SortSmem<2>) : (int)sizeof(SortSmem<1>));
+      if (e != cudaSuccess) return e;
+      cudaFuncSetAttribute(ks[i], cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, onesweep_kernel<true, unsigned long long>, SORT_THREADS,
+                                                  sizeof(SortSmem<2>));
     if (per_sm < 1) per_sm = 1;
   }
   if (ws.reset_tile_ctr) cudaMemsetAsync(ws.tile_ctr, 0, 4 * sizeof(uint32_t), s);
@@ -568,18 +608,29 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, const unsigned long long* 
   const uint32_t grid = pers ? (uint32_t)umin64(tiles, (uint64_t)per_sm * nsm) : tiles;
   uint64_t* kin = recs;
   uint64_t* kout = ws.alt;
+  // 32-bit look-back words when every prefix fits 26 bits
+  // (test hook RC_DEBUG_SORT_W64 forces the 64-bit words; results never differ)
+  const int fmt = (SORT_W32 && n < (1u << 26) && !getenv("RC_DEBUG_SORT_W64")) ? 1 : 0;
+  const uint32_t epochs = fmt ? 16u : (1u << 22);
   for (int p = 0; p < passes; p++) {
-    if (++ws.epoch >= (1u << 22)) {  // epoch wrap: clear the look-back words once
+    if (fmt != ws.status_fmt || ++ws.epoch >= epochs) {  // format switch or epoch wrap: clear the words once
       cudaMemsetAsync(ws.status, 0, ws.status_tiles * RADIX * sizeof(unsigned long long), s);
       ws.epoch = 1;
+      ws.status_fmt = fmt;
     }
     if (prof) prof->begin(s);
-    if (pers)
-      onesweep_kernel<true><<<grid, SORT_THREADS, sizeof(SortSmem<2>), s>>>(
-          kin, kout, n, n_a, n_b, 8 * p, ws.hist + p * RADIX, ws.status, ws.tile_ctr + p, ws.epoch);
+    const dim3 g(grid), b(SORT_THREADS);
+    const uint32_t* h = ws.hist + p * RADIX;
+    uint32_t* tc = ws.tile_ctr + p;
+    unsigned* st32 = reinterpret_cast<unsigned*>(ws.status);
+    if (pers && fmt)
+      onesweep_kernel<true, unsigned><<<g, b, sizeof(SortSmem<2>), s>>>(kin, kout, n, n_a, n_b, 8 * p, h, st32, tc, ws.epoch);
+    else if (pers)
+      onesweep_kernel<true, unsigned long long><<<g, b, sizeof(SortSmem<2>), s>>>(kin, kout, n, n_a, n_b, 8 * p, h, ws.status, tc, ws.epoch);
+    else if (fmt)
+      onesweep_kernel<false, unsigned><<<g, b, sizeof(SortSmem<1>), s>>>(kin, kout, n, n_a, n_b, 8 * p, h, st32, tc, ws.epoch);
     else
-      onesweep_kernel<false><<<grid, SORT_THREADS, sizeof(SortSmem<1>), s>>>(
-          kin, kout, n, n_a, n_b, 8 * p, ws.hist + p * RADIX, ws.status, ws.tile_ctr + p, ws.epoch);
+      onesweep_kernel<false, unsigned long long><<<g, b, sizeof(SortSmem<1>), s>>>(kin, kout, n, n_a, n_b, 8 * p, h, ws.status, tc, ws.epoch);
     launched();
     if (prof) prof->end(RC_PROF_SORT, s, (uint64_t)n * 16, n);
     cudaError_t e = cudaGetLastError();

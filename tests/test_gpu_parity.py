@@ -307,6 +307,20 @@ def test_random_tiny_kernels(rc):
         assert_parity(g, o, ins)
 
 
+def test_sort_64bit_lookback_words(rc, monkeypatch):
+    """The onesweep look-back uses 32-bit status words for sorts of < 2^26
+    records and 64-bit words otherwise; RC_DEBUG_SORT_W64 forces the 64-bit
+    format on small sorts (the format switch clears the words)."""
+    monkeypatch.setenv("RC_DEBUG_SORT_W64", "1")
+    for src, n, ins in [(K.TREE_OFF_BY_ONE, 1024, I.cfg3_inputs(0, 6, 1024)),
+                        (K.BENIGN["K_Btid"], 256, I.cfg2_inputs(0, 9, 256)),
+                        (K.STENCIL, 3000, I.cfg5_inputs(0, 3, 3000))]:
+        p, g, o = run_both(rc, src, n, ins)
+        assert_parity(g, o, ins)
+        p, g, o = run_both(rc, src, n, ins, keep_all_reads=True)
+        assert_parity(g, o, ins)
+
+
 @pytest.mark.parametrize("h", ["1", "2"])
 def test_interp_lanes_per_thread(rc, monkeypatch, h):
     """K1 runs one or two work-items per thread (two only for large batches
