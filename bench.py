@@ -43,6 +43,26 @@ METRIC = "checked memory accesses/s"
 UNIT = "Gaccess/s"
 
 
+def cub_baseline():
+    """CUB's device radix sort on the same keys (7.3 M records, 24 cell bits,
+    as in one config-5 interval), from the committed tools/cubbench.cu run."""
+    path = os.path.join(ROOT, "profiles", "r01_sort_vs_cub.txt")
+    if not os.path.exists(path):
+        return None
+    ours = cub = None
+    for line in open(path):
+        if "n=7340032" in line and "pattern=stencil" in line:
+            gbs = float(line.split("->")[1].split("GB/s")[0])
+            if line.startswith("CUB"):
+                cub = gbs
+            else:
+                ours = gbs
+    if cub is None:
+        return None
+    return {"kernel": "cub::DeviceRadixSort::SortKeys (CUB 2.8.2), same u64 records and 24 cell bits",
+            "GBps": cub, "this_sort_GBps": ours, "records": 7340032, "source": "profiles/r01_sort_vs_cub.txt"}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -292,7 +312,7 @@ def main():
                     "traffic": traffic, "alg_bytes_per_launch": s["alg_bytes"] / max(1, s["launches"]),
                     "alg_bytes_per_record": 16, "launches_sampled": s["launches"],
                     "sampling": f"CUDA events around every {every}th interval's kernels of the timed steps",
-                    "peak_source": peak_src}
+                    "peak_source": peak_src, "library_baseline": cub_baseline()}
         kernels = {"sample_every": every}
         for c in ("interp", "filter", "hist", "sort", "detect", "boundary", "finalize", "copy"):
             d = prof_sum[c]
