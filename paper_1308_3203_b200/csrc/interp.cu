@@ -40,6 +40,9 @@
 
 #include "rc_internal.h"
 
+#ifndef INTERP_T  // threads per block (<= 256)
+#define INTERP_T 256
+#endif
 #ifndef INTERP_H  // work-items per thread for large batches (1 or 2)
 #define INTERP_H 2
 #endif
@@ -769,7 +772,7 @@ namespace {
 template <int H>
 cudaError_t launch_interp_h(const InterpParams& p, cudaStream_t s, int nsm) {
   const bool code_smem = p.n_instr <= 2048;
-  int T = 256;
+  int T = INTERP_T;
   while (T > 32 && interp_smem_bytes(p, T, code_smem, H) > 96 * 1024) T >>= 1;
   const size_t sm = interp_smem_bytes(p, T, code_smem, H);
   auto kern = code_smem ? (p.fuel_check ? interp_kernel<true, true, H> : interp_kernel<true, false, H>)
