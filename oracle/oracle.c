@@ -170,20 +170,107 @@ typedef struct {
   const int32_t* const* inputs; uint32_t n_instances; uint32_t instance_offset;
   uint64_t fuel; uint32_t max_intervals;
   int32_t* const* final_heaps;
+  int classify;
   /* per-thread results */
   int next_instance; pthread_mutex_t mu;
 } runctx;
 
 typedef struct { replist reps; ostats st; } thread_out;
 
+/* One work-item's part of interval k (PAPER.md:168-201 under delayed
+ * visibility, reading L2): it runs from pc[t] until it suspends, exits or
+ * halts, logging one read record per performed LD and, at the end, one write
+ * record per distinct cell with its final value (reading L3).  A read of cell
+ * c sees the work-item's own earlier write, else snap[c] — or alt[c] when
+ * altmask[c] is set (the second visibility of the RW value classification,
+ * DESIGN.md §3; NULL in the canonical run). */
+static void exec_thread(const oprog* P, uint32_t t, const uint32_t* sizes, int32_t* r, uint32_t* pc,
+                        uint8_t* status, int32_t* node, uint8_t* arrived, int32_t* const* snap,
+                        int32_t* const* alt, uint8_t* const* altmask, uint64_t fuel, uint32_t inst_global,
+                        uint32_t k, replist* reps, ostats* st, acclist* log, ownw** ownp, size_t* own_cap) {
+  ownw* own = *ownp;
+  size_t n_own = 0;
+  uint64_t steps = 0;
+  for (;;) {
+    if (steps == fuel) { /* fuel exhausted (reading L17) */
+      rep_push(reps, mkrep(inst_global, k, -1, (int32_t)pc[t], t, NOTID, K_FUEL, 0));
+      status[t] = S_FUEL; break;
+    }
+    steps++;
+    st->instructions++;
+    const oins* I = &P->code[pc[t]];
+    int fault;
+    if (step_private(P, I, r, t, sizes, &pc[t], &fault)) {
+      if (fault == S_DIV0) {
+        rep_push(reps, mkrep(inst_global, k, -1, (int32_t)pc[t], t, NOTID, K_DIV0, 0));
+        status[t] = S_DIV0; break;
+      }
+      continue;
+    }
+    if (I->op == O_LD) { /* v := a[w]   (reading L11) */
+      int32_t idx = r[I->c];
+      if (idx < 0 || (uint32_t)idx >= sizes[I->b]) { /* ⊥: not performed, not logged (L5) */
+        rep_push(reps, mkrep(inst_global, k, I->b, idx, t, NOTID, K_OOB, 0));
+        status[t] = S_OOB; break;
+      }
+      int32_t v = (altmask && altmask[I->b][idx]) ? alt[I->b][idx] : snap[I->b][idx];
+      for (size_t j = 0; j < n_own; j++)
+        if (own[j].arr == I->b && own[j].idx == idx) v = own[j].val; /* own earlier write */
+      acc a = {I->b, idx, t, 0, 0};
+      acc_push(log, a);
+      st->checked++; st->loads++;
+      r[I->a] = v;
+      pc[t]++;
+    } else if (I->op == O_ST) { /* a[v] := e */
+      int32_t idx = r[I->b];
+      if (idx < 0 || (uint32_t)idx >= sizes[I->a]) {
+        rep_push(reps, mkrep(inst_global, k, I->a, idx, t, NOTID, K_OOB, 0));
+        status[t] = S_OOB; break;
+      }
+      size_t j;
+      for (j = 0; j < n_own; j++)
+        if (own[j].arr == I->a && own[j].idx == idx) break;
+      if (j == n_own) {
+        if (n_own == *own_cap) { *own_cap *= 2; own = (ownw*)realloc(own, *own_cap * sizeof(ownw)); *ownp = own; }
+        own[n_own].arr = I->a; own[n_own].idx = idx; n_own++;
+      }
+      own[j].val = r[I->c];
+      st->checked++; st->stores++;
+      pc[t]++;
+    } else if (I->op == O_BAR) { /* τ ⊡ σ */
+      status[t] = S_WAITING; node[t] = (int32_t)pc[t]; arrived[t] = 1; pc[t]++; break;
+    } else if (I->op == O_EXIT) { /* exit node = implicit final barrier */
+      status[t] = S_EXITED; node[t] = -1; arrived[t] = 1; break;
+    } else if (I->op == O_ASSUME) { /* false -> ⊤, reading L6 */
+      if (r[I->a] == 0) { status[t] = S_PRUNED; break; }
+      pc[t]++;
+    } else if (I->op == O_ASSERT) { /* false -> ⊥ */
+      if (r[I->a] == 0) {
+        rep_push(reps, mkrep(inst_global, k, -1, (int32_t)pc[t], t, NOTID, K_ASSERT, 0));
+        status[t] = S_ASSERT; break;
+      }
+      pc[t]++;
+    } else {
+      fprintf(stderr, "oracle: bad opcode %d\n", I->op); abort();
+    }
+  }
+  /* the work-item's writes of this interval, one per cell, final value (L3) */
+  for (size_t j = 0; j < n_own; j++) {
+    acc a = {own[j].arr, own[j].idx, t, 1, own[j].val};
+    acc_push(log, a);
+  }
+}
+
 /* Run one instance exactly as DESIGN.md §3 describes.  If stop_at >= 0 the
  * run stops at the START of interval stop_at and the lane state + heap are
  * copied out (used to seed the enumerator); returns 1 if that interval is
- * reached, 0 otherwise. */
+ * reached, 0 otherwise.  classify: RW value classification of every interval
+ * with an RW report. */
 static int run_instance(const oprog* P, uint32_t n, const uint32_t* sizes, int32_t** heap,
                         uint32_t inst_global, uint64_t fuel, uint32_t max_intervals,
                         replist* reps, ostats* st, int stop_at,
-                        int32_t* out_regs, uint32_t* out_pc, uint8_t* out_status, uint64_t* out_intervals) {
+                        int32_t* out_regs, uint32_t* out_pc, uint8_t* out_status, uint64_t* out_intervals,
+                        int classify) {
   uint32_t A = P->n_arrays, R = P->n_regs;
   int32_t* regs = (int32_t*)calloc((size_t)n * R + 1, sizeof(int32_t)); /* registers start at 0 (L18) */
   uint32_t* pc = (uint32_t*)calloc(n + 1, sizeof(uint32_t));              /* start = pc 0 */
@@ -192,6 +279,16 @@ static int run_instance(const oprog* P, uint32_t n, const uint32_t* sizes, int32
   uint8_t* arrived = (uint8_t*)malloc(n + 1);
   int32_t** snap = (int32_t**)malloc((A + 1) * sizeof(int32_t*));
   for (uint32_t a = 0; a < A; a++) snap[a] = (int32_t*)malloc(((size_t)sizes[a] + 1) * sizeof(int32_t));
+  /* classification: the lane state at the interval start, a second heap, the flagged-cell masks */
+  int32_t* regs0 = classify ? (int32_t*)malloc(((size_t)n * R + 1) * sizeof(int32_t)) : NULL;
+  uint32_t* pc0 = classify ? (uint32_t*)malloc((n + 1) * sizeof(uint32_t)) : NULL;
+  uint8_t* status0 = classify ? (uint8_t*)malloc(n + 1) : NULL;
+  int32_t** heapB = classify ? (int32_t**)malloc((A + 1) * sizeof(int32_t*)) : NULL;
+  uint8_t** mask = classify ? (uint8_t**)malloc((A + 1) * sizeof(uint8_t*)) : NULL;
+  for (uint32_t a = 0; classify && a < A; a++) {
+    heapB[a] = (int32_t*)malloc(((size_t)sizes[a] + 1) * sizeof(int32_t));
+    mask[a] = (uint8_t*)malloc((size_t)sizes[a] + 1);
+  }
   acclist log = {0};
   size_t own_cap = 16; ownw* own = (ownw*)malloc(own_cap * sizeof(ownw));
   uint32_t k = 0;
@@ -201,83 +298,20 @@ static int run_instance(const oprog* P, uint32_t n, const uint32_t* sizes, int32
     if (stop_at >= 0 && k == (uint32_t)stop_at) { reached = 1; break; }
     /* interval k: snap <- heap (the shared state every read of this interval sees) */
     for (uint32_t a = 0; a < A; a++) memcpy(snap[a], heap[a], (size_t)sizes[a] * sizeof(int32_t));
+    if (classify) {
+      memcpy(regs0, regs, (size_t)n * R * sizeof(int32_t));
+      memcpy(pc0, pc, n * sizeof(uint32_t));
+      memcpy(status0, status, n);
+    }
     log.n = 0;
     memset(arrived, 0, n);
     for (uint32_t t = 0; t < n; t++) {
       if (status[t] != S_RUNNING) continue;
-      int32_t* r = regs + (size_t)t * R;
-      size_t n_own = 0;
-      uint64_t steps = 0;
-      for (;;) {
-        if (steps == fuel) { /* fuel exhausted (reading L17) */
-          rep_push(reps, mkrep(inst_global, k, -1, (int32_t)pc[t], t, NOTID, K_FUEL, 0));
-          status[t] = S_FUEL; break;
-        }
-        steps++;
-        st->instructions++;
-        const oins* I = &P->code[pc[t]];
-        int fault;
-        if (step_private(P, I, r, t, sizes, &pc[t], &fault)) {
-          if (fault == S_DIV0) {
-            rep_push(reps, mkrep(inst_global, k, -1, (int32_t)pc[t], t, NOTID, K_DIV0, 0));
-            status[t] = S_DIV0; break;
-          }
-          continue;
-        }
-        if (I->op == O_LD) { /* v := a[w]   (reading L11) */
-          int32_t idx = r[I->c];
-          if (idx < 0 || (uint32_t)idx >= sizes[I->b]) { /* ⊥: not performed, not logged (L5) */
-            rep_push(reps, mkrep(inst_global, k, I->b, idx, t, NOTID, K_OOB, 0));
-            status[t] = S_OOB; break;
-          }
-          int32_t v = snap[I->b][idx];
-          for (size_t j = 0; j < n_own; j++)
-            if (own[j].arr == I->b && own[j].idx == idx) v = own[j].val; /* own earlier write */
-          acc a = {I->b, idx, t, 0, 0};
-          acc_push(&log, a);
-          st->checked++; st->loads++;
-          r[I->a] = v;
-          pc[t]++;
-        } else if (I->op == O_ST) { /* a[v] := e */
-          int32_t idx = r[I->b];
-          if (idx < 0 || (uint32_t)idx >= sizes[I->a]) {
-            rep_push(reps, mkrep(inst_global, k, I->a, idx, t, NOTID, K_OOB, 0));
-            status[t] = S_OOB; break;
-          }
-          size_t j;
-          for (j = 0; j < n_own; j++)
-            if (own[j].arr == I->a && own[j].idx == idx) break;
-          if (j == n_own) {
-            if (n_own == own_cap) { own_cap *= 2; own = (ownw*)realloc(own, own_cap * sizeof(ownw)); }
-            own[n_own].arr = I->a; own[n_own].idx = idx; n_own++;
-          }
-          own[j].val = r[I->c];
-          st->checked++; st->stores++;
-          pc[t]++;
-        } else if (I->op == O_BAR) { /* τ ⊡ σ */
-          status[t] = S_WAITING; node[t] = (int32_t)pc[t]; arrived[t] = 1; pc[t]++; break;
-        } else if (I->op == O_EXIT) { /* exit node = implicit final barrier */
-          status[t] = S_EXITED; node[t] = -1; arrived[t] = 1; break;
-        } else if (I->op == O_ASSUME) { /* false -> ⊤, reading L6 */
-          if (r[I->a] == 0) { status[t] = S_PRUNED; break; }
-          pc[t]++;
-        } else if (I->op == O_ASSERT) { /* false -> ⊥ */
-          if (r[I->a] == 0) {
-            rep_push(reps, mkrep(inst_global, k, -1, (int32_t)pc[t], t, NOTID, K_ASSERT, 0));
-            status[t] = S_ASSERT; break;
-          }
-          pc[t]++;
-        } else {
-          fprintf(stderr, "oracle: bad opcode %d\n", I->op); abort();
-        }
-      }
-      /* the work-item's writes of this interval, one per cell, final value (L3) */
-      for (size_t j = 0; j < n_own; j++) {
-        acc a = {own[j].arr, own[j].idx, t, 1, own[j].val};
-        acc_push(&log, a);
-      }
+      exec_thread(P, t, sizes, regs + (size_t)t * R, pc, status, node, arrived, snap, NULL, NULL, fuel,
+                  inst_global, k, reps, st, &log, &own, &own_cap);
     }
 
+    const size_t rep_mark = reps->n;  /* reports of this interval start here */
     /* race rule per cell (PAPER.md:224-229 as reading L1), in (array,index) order */
     qsort(log.v, log.n, sizeof(acc), acc_cmp);
     size_t g = 0;
@@ -333,6 +367,49 @@ static int run_instance(const oprog* P, uint32_t n, const uint32_t* sizes, int32
     }
     free(rt); free(wt); free(wv);
 
+    /* RW value classification (reading L19): re-run interval k
+     * from its start state with reads of the RW-flagged cells seeing the value
+     * the canonical run committed (writers first); commit the second run's
+     * writes (max-tid writer) onto the interval-start heap and compare the two
+     * committed heaps.  Every RW report of the interval gets flag bit 4 (equal:
+     * the RW races of this interval do not change the state, for this input)
+     * or bit 5 (the committed state depends on the read values). */
+    if (classify && reps->n > rep_mark) {
+      int any_rw = 0;
+      for (uint32_t a = 0; a < A; a++) memset(mask[a], 0, sizes[a]);
+      for (size_t i = rep_mark; i < reps->n; i++)
+        if (reps->v[i].kind == K_RW) { mask[reps->v[i].array][reps->v[i].index] = 1; any_rw = 1; }
+      if (any_rw) {
+        int32_t* rB = (int32_t*)malloc(((size_t)n * R + 1) * sizeof(int32_t));
+        uint32_t* pB = (uint32_t*)malloc((n + 1) * sizeof(uint32_t));
+        uint8_t* sB = (uint8_t*)malloc(n + 1);
+        int32_t* nodeB = (int32_t*)malloc((n + 1) * sizeof(int32_t));
+        uint8_t* arrB = (uint8_t*)calloc(n + 1, 1);
+        memcpy(rB, regs0, (size_t)n * R * sizeof(int32_t));
+        memcpy(pB, pc0, n * sizeof(uint32_t));
+        memcpy(sB, status0, n);
+        replist junk = {0};
+        ostats junk_st; memset(&junk_st, 0, sizeof junk_st);
+        acclist logB = {0};
+        for (uint32_t t = 0; t < n; t++) {
+          if (sB[t] != S_RUNNING) continue;
+          exec_thread(P, t, sizes, rB + (size_t)t * R, pB, sB, nodeB, arrB, snap, heap, mask, fuel,
+                      inst_global, k, &junk, &junk_st, &logB, &own, &own_cap);
+        }
+        for (uint32_t a = 0; a < A; a++) memcpy(heapB[a], snap[a], (size_t)sizes[a] * sizeof(int32_t));
+        /* barrier release of the second run: write records are in ascending tid
+         * order, so the last assignment to a cell is its max-tid writer's (I4) */
+        for (size_t i = 0; i < logB.n; i++)
+          if (logB.v[i].w) heapB[logB.v[i].cell_arr][logB.v[i].idx] = logB.v[i].val;
+        int diff = 0;
+        for (uint32_t a = 0; a < A && !diff; a++)
+          if (memcmp(heapB[a], heap[a], (size_t)sizes[a] * sizeof(int32_t))) diff = 1;
+        for (size_t i = rep_mark; i < reps->n; i++)
+          if (reps->v[i].kind == K_RW) reps->v[i].flags |= diff ? 0x20 : 0x10;
+        free(rB); free(pB); free(sB); free(nodeB); free(arrB); free(junk.v); free(logB.v);
+      }
+    }
+
     /* barrier divergence among the work-items that arrived in this interval (L9) */
     {
       int64_t t1 = -1;
@@ -375,6 +452,10 @@ static int run_instance(const oprog* P, uint32_t n, const uint32_t* sizes, int32
   free(regs); free(pc); free(status); free(node); free(arrived);
   for (uint32_t a = 0; a < A; a++) free(snap[a]);
   free(snap); free(log.v); free(own);
+  if (classify) {
+    for (uint32_t a = 0; a < A; a++) { free(heapB[a]); free(mask[a]); }
+    free(heapB); free(mask); free(regs0); free(pc0); free(status0);
+  }
   return reached;
 }
 
@@ -394,7 +475,7 @@ static void* worker(void* p) {
     for (uint32_t a = 0; a < P->n_arrays; a++)  /* heap <- copy(inputs[inst]) */
       memcpy(heap[a], c->inputs[a] + (size_t)i * c->sizes[a], (size_t)c->sizes[a] * sizeof(int32_t));
     run_instance(P, c->n, c->sizes, heap, c->instance_offset + (uint32_t)i, c->fuel, c->max_intervals,
-                 &W->out.reps, &W->out.st, -1, NULL, NULL, NULL, NULL);
+                 &W->out.reps, &W->out.st, -1, NULL, NULL, NULL, NULL, c->classify);
     if (c->final_heaps)
       for (uint32_t a = 0; a < P->n_arrays; a++)
         if (c->final_heaps[a])
@@ -408,11 +489,12 @@ static void* worker(void* p) {
 /* Public: run the canonical algorithm on n_instances instances.
  * inputs[a] = n_instances * sizes[a] int32 (instance-major).  Reports are
  * returned malloc'd in canonical order (free with oracle_free).  stats[13] =
- * checked, loads, stores, instructions, intervals_max, lanes_final[8]. */
+ * checked, loads, stores, instructions, intervals_max, lanes_final[8].
+ * classify != 0: RW value classification flags on the RW reports. */
 int oracle_run(const uint8_t* bc, size_t nbytes, uint32_t n, const uint32_t* sizes,
                const int32_t* const* inputs, uint32_t n_instances, uint32_t instance_offset,
                uint64_t fuel, uint32_t max_intervals, int n_threads,
-               orep** reports, uint64_t* n_reports, int32_t* const* final_heaps, uint64_t* stats) {
+               orep** reports, uint64_t* n_reports, int32_t* const* final_heaps, uint64_t* stats, int classify) {
   oprog P;
   if (decode(bc, nbytes, &P)) return -1;
   runctx c;
@@ -420,6 +502,7 @@ int oracle_run(const uint8_t* bc, size_t nbytes, uint32_t n, const uint32_t* siz
   c.P = &P; c.n = n; c.sizes = sizes; c.inputs = inputs; c.n_instances = n_instances;
   c.instance_offset = instance_offset; c.fuel = fuel; c.max_intervals = max_intervals;
   c.final_heaps = final_heaps;
+  c.classify = classify;
   pthread_mutex_init(&c.mu, NULL);
   if (n_threads < 1) n_threads = 1;
   worker_arg* W = (worker_arg*)calloc((size_t)n_threads, sizeof(worker_arg));
@@ -466,7 +549,7 @@ int oracle_state_at(const uint8_t* bc, size_t nbytes, uint32_t n, const uint32_t
   }
   replist reps = {0}; ostats st; memset(&st, 0, sizeof st);
   int reached = run_instance(&P, n, sizes, heap, 0, fuel, 0xFFFFFFFFu, &reps, &st, (int)k,
-                             regs_out, pc_out, status_out, NULL);
+                             regs_out, pc_out, status_out, NULL, 0);
   size_t off = 0;
   for (uint32_t a = 0; a < P.n_arrays; a++) {
     memcpy(heap_out + off, heap[a], (size_t)sizes[a] * sizeof(int32_t));
