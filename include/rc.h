@@ -114,7 +114,11 @@ enum rc_kind {
  * in that order.  For RW / WW_*: (tid1 < tid2) is the lexicographically
  * smallest conflicting pair (reading L4); flags bit0 = tid1 read
  * the cell, bit1 = tid1 wrote it, bit2 = tid2 read, bit3 = tid2 wrote (all in
- * this interval).  For error kinds tid2 = 0xFFFFFFFF and flags = 0.         */
+ * this interval).  With RC_OPT_CLASSIFY_RW an RW report also carries bit4
+ * (0x10: re-running its interval with writers-first visibility of the RW
+ * cells commits the same heap — the read values do not matter for this
+ * input) or bit5 (0x20: the committed heap differs), DESIGN.md §3 reading
+ * L19.  For error kinds tid2 = 0xFFFFFFFF and flags = 0.                    */
 typedef struct {
   uint32_t instance; /* global instance id (includes options->instance_offset) */
   uint32_t interval; /* barrier interval k (0-based)                          */
@@ -185,6 +189,11 @@ typedef struct {
                              work-item wrote in the interval (which can produce
                              no report or commit; by default they are dropped
                              before the sort) — same results     */
+#define RC_OPT_CLASSIFY_RW 4u /* RW value classification:
+                             every interval with an RW report is re-run under a
+                             second visibility and the RW reports get flag bit 4
+                             or 5 (see rc_report); costs a heap snapshot per
+                             interval and one extra pass per racy interval     */
 
 typedef struct {
   uint32_t instance_offset;    /* added to report.instance (multi-GPU shards) */

@@ -35,6 +35,8 @@ __device__ __forceinline__ int32_t rec_val(const DetectParams& p, uint64_t r) {
 
 __device__ __forceinline__ void emit(const DetectParams& p, uint32_t cell, uint32_t t1, uint32_t t2, uint16_t kind,
                                   uint16_t flags) {
+  if (p.quiet) return;  // classification re-run: commit only
+  if (kind == RC_RW) atomicAdd(&p.ctr->rw_reports, 1ull);
   const uint32_t inst = fast_div(cell, p.cpi_magic);
   const uint32_t rem = cell - inst * p.cpi;
   uint32_t a = 0;
@@ -334,7 +336,8 @@ __device__ __noinline__ void boundary_tail(const DetectParams& p) {
     c->bdone = 0;
     const volatile DevCounters* v = c;
     const bool need_host = v->log_overflow || v->ovl_overflow || v->k1_reports > p.report_cap ||
-                           v->report_count > p.report_cap || v->diverged || !v->any_waiting;
+                           v->report_count > p.report_cap || v->diverged || !v->any_waiting ||
+                           (p.classify && v->rw_reports > 0);
     if (need_host) c->abort = 1;
   }
 }
@@ -353,6 +356,52 @@ __global__ void __launch_bounds__(256, DET_MINB) detect_kernel(const DetectParam
       detect_chunk(p, wg, n_records);
   }
   if (p.with_boundary) boundary_tail(p);
+}
+
+// ---- RW value classification helpers (DESIGN.md §3 reading L19) -----------
+__global__ void rw_mark_kernel(const rc_report* __restrict__ reports, uint64_t r0, uint64_t r1, uint32_t inst_base,
+                               uint32_t cpi, const uint32_t* __restrict__ arr_off, uint8_t* __restrict__ mask) {
+  const uint64_t i = r0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= r1) return;
+  const rc_report r = reports[i];
+  if (r.kind != RC_RW) return;
+  mask[(uint64_t)(r.instance - inst_base) * cpi + arr_off[r.array] + (uint32_t)r.index] = 1;
+}
+
+// per instance (instances are independent runs): do the two heaps differ?
+__global__ void heap_compare_kernel(const int32_t* __restrict__ a, const int32_t* __restrict__ b, uint64_t n,
+                                    uint32_t cpi, uint32_t* __restrict__ diff) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    if (a[i] != b[i]) diff[i / cpi] = 1;
+}
+
+__global__ void rw_flag_kernel(rc_report* __restrict__ reports, uint64_t r0, uint64_t r1, uint32_t inst_base,
+                               const uint32_t* __restrict__ diff) {
+  const uint64_t i = r0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= r1 || reports[i].kind != RC_RW) return;
+  reports[i].flags |= diff[reports[i].instance - inst_base] ? 0x20 : 0x10;
+}
+
+cudaError_t launch_rw_mark(const rc_report* reports, uint64_t r0, uint64_t r1, uint32_t inst_base, uint32_t cpi,
+                           const uint32_t* arr_off, uint8_t* mask, cudaStream_t s) {
+  if (r1 <= r0) return cudaSuccess;
+  rw_mark_kernel<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(reports, r0, r1, inst_base, cpi, arr_off, mask);
+  launched();
+  return cudaGetLastError();
+}
+cudaError_t launch_heap_compare(const int32_t* a, const int32_t* b, uint64_t n, uint32_t cpi, uint32_t* diff,
+                                cudaStream_t s) {
+  if (!n) return cudaSuccess;
+  heap_compare_kernel<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 8), 256, 0, s>>>(a, b, n, cpi, diff);
+  launched();
+  return cudaGetLastError();
+}
+cudaError_t launch_rw_flag(rc_report* reports, uint64_t r0, uint64_t r1, uint32_t inst_base, const uint32_t* diff,
+                           cudaStream_t s) {
+  if (r1 <= r0) return cudaSuccess;
+  rw_flag_kernel<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, s>>>(reports, r0, r1, inst_base, diff);
+  launched();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_detect(const DetectParams& p, cudaStream_t s) {

@@ -268,7 +268,8 @@ void interp_phase_io(unsigned long long* out, bool reset) {
 // H*T lanes side by side: one instruction fetch, decode, dispatch and warp
 // vote serve H lanes, and each lane's heap loads add to the memory-level
 // parallelism of the warp.
-template <bool CODE_SMEM, bool FUEL, int H>
+// ALT: the RW-classification re-run (reads of alt_mask cells see alt_heap).
+template <bool CODE_SMEM, bool FUEL, int H, bool ALT>
 __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_BLOCKS_H)
     interp_kernel(const __grid_constant__ InterpParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -472,8 +473,13 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
               bool found = false;
               for (int j = 0; j < n_own[h]; j++)
                 if ((uint32_t)lds32(OC(h) + j * orow) == cell) { v = lds32(OVL(h) + j * orow); found = true; }
-              if (found) sts32(RA(h), v);
-              else ld_async(RA(h), p.heap + cell);
+              if (found) {
+                sts32(RA(h), v);
+              } else {
+                const int32_t* src = p.heap + cell;
+                if (ALT && p.alt_mask[cell]) src = p.alt_heap + cell;  // writers-first visibility
+                ld_async(RA(h), src);
+              }
               pc[h]++;
               nloads[h]++;
               ok = true;
@@ -769,14 +775,14 @@ size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem, int H)
 }
 
 namespace {
-template <int H>
+template <int H, bool ALT>
 cudaError_t launch_interp_h(const InterpParams& p, cudaStream_t s, int nsm) {
   const bool code_smem = p.n_instr <= 2048;
   int T = INTERP_T;
   while (T > 32 && interp_smem_bytes(p, T, code_smem, H) > 96 * 1024) T >>= 1;
   const size_t sm = interp_smem_bytes(p, T, code_smem, H);
-  auto kern = code_smem ? (p.fuel_check ? interp_kernel<true, true, H> : interp_kernel<true, false, H>)
-                        : (p.fuel_check ? interp_kernel<false, true, H> : interp_kernel<false, false, H>);
+  auto kern = code_smem ? (p.fuel_check ? interp_kernel<true, true, H, ALT> : interp_kernel<true, false, H, ALT>)
+                        : (p.fuel_check ? interp_kernel<false, true, H, ALT> : interp_kernel<false, false, H, ALT>);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, sm);
   const uint32_t tiles = (p.n_lanes + H * T - 1) / (H * T);
@@ -792,9 +798,12 @@ cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
   static bool attr_set = false;
   static int nsm = 0;
   if (!attr_set) {
-    for (auto f : {interp_kernel<true, true, 1>, interp_kernel<false, true, 1>, interp_kernel<true, false, 1>,
-                   interp_kernel<false, false, 1>, interp_kernel<true, true, 2>, interp_kernel<false, true, 2>,
-                   interp_kernel<true, false, 2>, interp_kernel<false, false, 2>}) {
+    for (auto f : {interp_kernel<true, true, 1, false>, interp_kernel<false, true, 1, false>,
+                   interp_kernel<true, false, 1, false>, interp_kernel<false, false, 1, false>,
+                   interp_kernel<true, true, 2, false>, interp_kernel<false, true, 2, false>,
+                   interp_kernel<true, false, 2, false>, interp_kernel<false, false, 2, false>,
+                   interp_kernel<true, true, 1, true>, interp_kernel<false, true, 1, true>,
+                   interp_kernel<true, false, 1, true>, interp_kernel<false, false, 1, true>}) {
       cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       if (e != cudaSuccess) return e;
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -809,7 +818,8 @@ cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
   const char* force = getenv("RC_DEBUG_INTERP_H");
   const int h = force ? (force[0] == '2' ? 2 : 1)
                       : (INTERP_H == 2 && p.n_lanes >= 2u * 256u * (uint32_t)nsm ? 2 : 1);
-  return h == 2 ? launch_interp_h<2>(p, s, nsm) : launch_interp_h<1>(p, s, nsm);
+  if (p.alt_mask) return launch_interp_h<1, true>(p, s, nsm);  // classification re-run (rare)
+  return h == 2 ? launch_interp_h<2, false>(p, s, nsm) : launch_interp_h<1, false>(p, s, nsm);
 }
 
 }  // namespace rc

@@ -83,6 +83,7 @@ struct DevCounters {
   unsigned int any_waiting;         // per interval
   unsigned int diverged;            // per interval
   unsigned long long k1_reports;    // report_count after K1 (snapshot taken by the filter)
+  unsigned long long rw_reports;    // RW reports emitted by detect (RC_OPT_CLASSIFY_RW)
   // ---- fields above: zeroed per interval attempt (one memset, runtime.cu)
   unsigned long long report_count;  // reports appended (whole run, rolled back on retry)
   unsigned long long lanes_final[8];
@@ -129,6 +130,10 @@ struct InterpParams {
   // it into the sort buffer
   uint64_t* stage;            // [stage_cap] records (make_rec) and sentinels
   unsigned long long stage_cap;
+  // RW classification re-run (null in a canonical run): a read of cell c with
+  // alt_mask[c] set (and no own earlier write) returns alt_heap[c]
+  const int32_t* alt_heap;
+  const uint8_t* alt_mask;
   uint8_t* wmap;              // [I_b * cpi] == wtag: cell written in this interval
   uint8_t wtag;               // this interval's tag (1..255; the map is zeroed when tags wrap)
   int32_t* wval;              // [ovl_cap][n_lanes] final value of each written overlay slot
@@ -152,6 +157,8 @@ struct DetectParams {
   DevCounters* ctr;
   // fused A4 tail (detect.cu boundary_tail); off for a detect-only re-run
   bool with_boundary;
+  bool classify;              // the verdict also asks the host for RW classification
+  bool quiet;                 // commit only (classification re-run): no reports
   uint32_t n_inst;
   int32_t* node_min;          // [n_inst] from K1, reset by the tail
   int32_t* node_max;
@@ -234,6 +241,15 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n_ub, const unsigned long lon
                           Profiler* prof, bool hist_ready);
 
 cudaError_t launch_detect(const DetectParams& p, cudaStream_t s);
+// RW classification helpers (detect.cu): mark the cells of the RW reports in
+// reports[r0, r1) (instance ids relative to inst_base), compare two heaps per
+// instance (diff[inst] = 1), set flag bit 4 / 5 on the RW reports of [r0, r1)
+cudaError_t launch_rw_mark(const rc_report* reports, uint64_t r0, uint64_t r1, uint32_t inst_base, uint32_t cpi,
+                           const uint32_t* arr_off, uint8_t* mask, cudaStream_t s);
+cudaError_t launch_heap_compare(const int32_t* a, const int32_t* b, uint64_t n, uint32_t cpi, uint32_t* diff,
+                                cudaStream_t s);
+cudaError_t launch_rw_flag(rc_report* reports, uint64_t r0, uint64_t r1, uint32_t inst_base, const uint32_t* diff,
+                           cudaStream_t s);
 
 struct BoundaryParams {
   uint32_t n, n_lanes, n_inst, interval, inst_base;

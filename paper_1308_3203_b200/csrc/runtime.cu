@@ -119,6 +119,9 @@ struct rc_workspace {
   uint8_t wtag = 0;  // write-set map tag of the last interval attempt
   DevBuf reports, reports_scratch;
   DevBuf inst_tmp;  // node_min | node_max | first_tid | second_tid | inst_flag  ([I_b] each)
+  // RW classification: interval-start heaps (two slots), the re-run's heap,
+  // the RW-cell mask, the re-run's (discarded) lane state
+  DevBuf heap_snap[2], heapB, amap, regs_b, pc_b, status_b, cmp_inst;
   DevBuf ctr;
   DevCounters* h_ctr = nullptr;  // pinned [4]: interval slots 0/1, synchronous reads 2, copy source 3
   cudaEvent_t iv_done[2] = {nullptr, nullptr};  // interval k's counters landed in h_ctr[k & 1]
@@ -127,7 +130,8 @@ struct rc_workspace {
   ~rc_workspace() {
     for (DevBuf* b : {&code, &arr_off, &arr_size, &heap, &regs[0], &regs[1], &pc[0], &pc[1], &status[0],
                       &status[1], &live, &log, &log_alt, &wval, &wmap, &sort_status,
-                      &ctr_block, &reports, &reports_scratch, &inst_tmp})  // (ctr is a view into ctr_block)
+                      &ctr_block, &reports, &reports_scratch, &inst_tmp, &heap_snap[0], &heap_snap[1], &heapB, &amap,
+                      &regs_b, &pc_b, &status_b, &cmp_inst})  // (ctr is a view into ctr_block)
       b->release();
     if (h_ctr) cudaFreeHost(h_ctr);
     for (cudaEvent_t e : iv_done)
@@ -237,6 +241,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   if (!opt.max_intervals) opt.max_intervals = 65536;
   if (!opt.fuel_per_interval) opt.fuel_per_interval = 1ull << 20;
   const bool host_io = (opt.flags & RC_OPT_HOST_IO) != 0;
+  const bool classify = (opt.flags & RC_OPT_CLASSIFY_RW) != 0;  // RW value classification (reading L19)
   uint64_t cpi = 0;
   std::vector<uint32_t> off(n_arrays + 1, 0), size(n_arrays + 1, 0);
   for (uint32_t a = 0; a < n_arrays; a++) {
@@ -319,6 +324,17 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       CK(W.status[b].ensure(L_pad));
     }
     CK(W.inst_tmp.ensure((uint64_t)I_b * 20));
+    if (classify) {
+      const uint64_t hb = std::max<uint64_t>(1, (uint64_t)I_b * cpi) * 4;
+      CK(W.heap_snap[0].ensure(hb));
+      CK(W.heap_snap[1].ensure(hb));
+      CK(W.heapB.ensure(hb));
+      CK(W.amap.ensure(hb / 4));
+      CK(W.regs_b.ensure(L_pad * P->n_regs * 4));
+      CK(W.pc_b.ensure(L_pad * 4));
+      CK(W.status_b.ensure(L_pad));
+      CK(W.cmp_inst.ensure((uint64_t)I_b * 4));
+    }
     CK(W.wval.ensure(std::max<uint64_t>(1, L_max * (uint64_t)P->ovl_cap) * 4));
     const void* wmap_before = W.wmap.p;
     CK(W.wmap.ensure(std::max<uint64_t>(1, (uint64_t)I_b * cpi)));
@@ -460,6 +476,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       dp.report_cap = rep_cap;
       dp.ctr = dctr;
       dp.with_boundary = false;
+      dp.classify = classify;
+      dp.quiet = false;
       dp.n_inst = nb;
       dp.node_min = node_min;
       dp.node_max = node_max;
@@ -467,18 +485,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       return dp;
     };
     struct Marks { size_t m0 = 0, m1 = 0; };
-    auto enqueue_interval = [&](uint32_t kk, int cc, Marks* mk) -> cudaError_t {
-      cudaError_t e;
-#define EQ(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
-      if (gaps) { gap_ev.push_back({}); cudaEventCreate(&gap_ev.back()[0]); cudaEventCreate(&gap_ev.back()[1]); cudaEventRecord(gap_ev.back()[0], s); }
-      if (opt.profile) W.prof.on = (prof_intervals++ % prof_every) == 0;  // sampled interval profile
-      // write-set map: a fresh tag per interval attempt; zeroed only when the tags wrap
-      if (++W.wtag == 0 || W.wtag == 1) {
-        W.wtag = 1;
-        if (cpi) EQ(cudaMemsetAsync(W.wmap.p, 0, W.wmap.bytes, s));
-      }
-      // histograms, sort tile counters and the per-attempt counters
-      EQ(cudaMemsetAsync(W.ctr_block.p, 0, CTR_OFF + offsetof(DevCounters, report_count), s));
+    auto make_ip = [&](uint32_t kk, int cc) {
       InterpParams ip;
       ip.code = W.code.as<Ins>();
       ip.n_instr = P->n_instr;
@@ -516,6 +523,28 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       ip.reports = W.reports.as<rc_report>();
       ip.report_cap = rep_cap;
       ip.ctr = dctr;
+      ip.alt_heap = nullptr;
+      ip.alt_mask = nullptr;
+      return ip;
+    };
+    auto enqueue_interval = [&](uint32_t kk, int cc, Marks* mk) -> cudaError_t {
+      cudaError_t e;
+#define EQ(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
+      if (gaps) { gap_ev.push_back({}); cudaEventCreate(&gap_ev.back()[0]); cudaEventCreate(&gap_ev.back()[1]); cudaEventRecord(gap_ev.back()[0], s); }
+      if (opt.profile) W.prof.on = (prof_intervals++ % prof_every) == 0;  // sampled interval profile
+      // write-set map: a fresh tag per interval attempt; zeroed only when the tags wrap
+      if (++W.wtag == 0 || W.wtag == 1) {
+        W.wtag = 1;
+        if (cpi) EQ(cudaMemsetAsync(W.wmap.p, 0, W.wmap.bytes, s));
+      }
+      // histograms, sort tile counters and the per-attempt counters
+      EQ(cudaMemsetAsync(W.ctr_block.p, 0, CTR_OFF + offsetof(DevCounters, report_count), s));
+      // RW classification: the interval-start heap, kept until the host has
+      // seen this interval (two slots: the speculative next interval's copy
+      // must not overwrite it)
+      if (classify && cpi)
+        EQ(cudaMemcpyAsync(W.heap_snap[kk & 1].p, W.heap.p, (size_t)nb * cpi * 4, cudaMemcpyDeviceToDevice, s));
+      InterpParams ip = make_ip(kk, cc);
       mk->m0 = W.prof.marks.size();
       W.prof.cut();
       W.prof.begin(s);
@@ -556,6 +585,80 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       return cudaSuccess;
     };
     auto clear_abort = [&]() { return cudaMemsetAsync(&dctr->abort, 0, sizeof(unsigned int), s); };
+
+    // RW value classification of interval kk (DESIGN.md §3 reading L19): the
+    // interval is re-run from its start state (lane state `cur`, heap snapshot)
+    // with reads of its RW cells seeing the committed heap; the re-run commits
+    // onto a copy of the snapshot, the two heaps are compared and the RW
+    // reports in [r0, r1) get flag bit 4 or 5.  Nothing of the re-run survives
+    // but the flags (its lane state goes to scratch rows, its reports are not
+    // written, the report count and K1's node ranges are restored).  The host
+    // reaches this with the speculative next interval aborted (the verdict
+    // asks for it), so the interval's input lane state is intact.
+    auto classify_interval = [&](uint32_t kk, uint64_t r0, uint64_t r1) -> cudaError_t {
+      cudaError_t e;
+#define EQ(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
+      const size_t cells = (size_t)nb * cpi;
+      EQ(cudaMemsetAsync(W.amap.p, 0, cells, s));
+      EQ(launch_rw_mark(W.reports.as<rc_report>(), r0, r1, inst_base, (uint32_t)cpi, W.arr_off.as<uint32_t>(),
+                        W.amap.as<uint8_t>(), s));
+      for (int attempt = 0;; attempt++) {
+        EQ(cudaMemcpyAsync(W.heapB.p, W.heap_snap[kk & 1].p, cells * 4, cudaMemcpyDeviceToDevice, s));
+        if (++W.wtag == 0 || W.wtag == 1) {
+          W.wtag = 1;
+          EQ(cudaMemsetAsync(W.wmap.p, 0, W.wmap.bytes, s));
+        }
+        EQ(cudaMemsetAsync(W.ctr_block.p, 0, CTR_OFF + offsetof(DevCounters, report_count), s));
+        InterpParams ip = make_ip(kk, cur);
+        ip.heap = W.heap_snap[kk & 1].as<int32_t>();  // interval-start heap
+        ip.alt_heap = W.heap.as<int32_t>();           // committed heap (writers first)
+        ip.alt_mask = W.amap.as<uint8_t>();
+        ip.regs_out = W.regs_b.as<int32_t>();
+        ip.pc_out = W.pc_b.as<uint32_t>();
+        ip.status_out = W.status_b.as<uint8_t>();
+        ip.report_cap = 0;  // error reports of the re-run are not written (the count is restored below)
+        EQ(launch_interp(ip, s));
+        FilterParams fp;
+        fp.stage = W.log_alt.as<uint64_t>();
+        fp.wmap = W.wmap.as<uint8_t>();
+        fp.wtag = W.wtag;
+        fp.out = W.log.as<uint64_t>();
+        fp.hist = W.sort.hist;
+        fp.passes = passes;
+        fp.ctr = dctr;
+        fp.n_slots = (uint32_t)log_cap;
+        fp.keep_all = false;
+        EQ(launch_filter(fp, s));
+        bool in_alt = false;
+        W.sort.alt = W.log_alt.as<uint64_t>();
+        EQ(onesweep_sort(W.log.as<uint64_t>(), (uint32_t)log_cap, &dctr->kept_count, nullptr, key_bits, W.sort, s,
+                         &in_alt, nullptr, /*hist_ready=*/true));
+        DetectParams dp = detect_params(kk);
+        dp.recs = in_alt ? W.log_alt.as<uint64_t>() : W.log.as<uint64_t>();
+        dp.heap = W.heapB.as<int32_t>();
+        dp.quiet = true;
+        dp.report_cap = ~0ull;  // (quiet: nothing is written; K1's uncounted reports never skip the commit)
+        EQ(launch_detect(dp, s));
+        EQ(read_ctr());
+        if (!W.h_ctr[2].log_overflow || attempt >= 8) break;
+        const uint64_t n_all = W.h_ctr[2].stage_count;  // grow the log and re-run (as for an interval)
+        const uint64_t want = std::min<uint64_t>(n_all + n_all / 4 + 1024, 0xFFFFFFFFull);
+        EQ(W.log.ensure(want * 8));
+        EQ(W.log_alt.ensure(want * 8));
+        log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
+        EQ(ensure_sort_status(log_cap));
+      }
+      if (W.h_ctr[2].log_overflow) return cudaErrorMemoryAllocation;
+      EQ(cudaMemsetAsync(W.cmp_inst.p, 0, (size_t)nb * 4, s));
+      EQ(launch_heap_compare(W.heapB.as<int32_t>(), W.heap.as<int32_t>(), cells, (uint32_t)cpi,
+                             W.cmp_inst.as<uint32_t>(), s));
+      EQ(launch_rw_flag(W.reports.as<rc_report>(), r0, r1, inst_base, W.cmp_inst.as<uint32_t>(), s));
+      EQ(set_report_count(r1));
+      EQ(cudaMemsetAsync(node_min, 0x7F, (size_t)nb * 4, s));
+      EQ(cudaMemsetAsync(node_max, 0x80, (size_t)nb * 4, s));
+#undef EQ
+      return cudaSuccess;
+    };
 
     // Speculative pipeline: interval k+1 is queued before the host looks at
     // interval k, so the GPU never waits for the host between intervals.  If
@@ -632,6 +735,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         }
       }
       rep_count = rc;
+      if (classify && h.rw_reports > 0 && cpi) CK(classify_interval(k, rep_before, rc));
       if (W.prof.on) {  // exact record counts are known now: fix this interval's profile bytes
         for (size_t i = mk_cur.m0; i < mk_cur.m1; i++) {
           Profiler::Mark& m = W.prof.marks[i];

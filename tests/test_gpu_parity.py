@@ -37,7 +37,7 @@ def run_both(rc, src_or_prog, n, ins, *, fuel=0, max_intervals=0, host=False, **
     g = rc.rc_run(prog, n, arrays, fuel_per_interval=fuel, max_intervals=max_intervals, **kw)
     o = oracle.run(p.bytecode, n, ins, fuel=fuel or oracle.oracle.DEFAULT_FUEL,
                    max_intervals=max_intervals or oracle.oracle.DEFAULT_MAX_INTERVALS,
-                   instance_offset=kw.get("instance_offset", 0))
+                   instance_offset=kw.get("instance_offset", 0), classify_rw=kw.get("classify_rw", False))
     return p, g, o
 
 
@@ -305,6 +305,36 @@ def test_random_tiny_kernels(rc):
         ins.append(rng.integers(-3, 4, size=(ins[0].shape[0], 5)).astype(np.int32))
         p, g, o = run_both(rc, pr, n, ins, fuel=500)
         assert_parity(g, o, ins)
+
+
+def test_rw_classification(rc):
+    """SURVEY §8(f) row 1 (reading L19): with RC_OPT_CLASSIFY_RW every RW
+    report carries bit 4 or 5 exactly as the oracle's re-run decides; all
+    other results are unchanged."""
+    cases = [(K.BENIGN["K_inc"], 64, I.cfg2_inputs(0, 6, 64)),
+             (".arrays A\n const r0, 0\n ld r1, A, r0\n const r2, 5\n st A, r0, r2\n exit\n", 40,
+              [np.array([[9], [5], [1]], np.int32)]),
+             (".arrays A B\n tid r0\n addi r1, r0, 1\n ld r2, A, r1\n st A, r0, r0\n st B, r0, r2\n exit\n", 50,
+              [np.arange(3 * 51, dtype=np.int32).reshape(3, 51), np.zeros((3, 50), np.int32)]),
+             (K.FIG1, 8, I.cfg1_inputs()),
+             (K.TREE_OFF_BY_ONE, 256, I.cfg3_inputs(0, 5, 256)),
+             (K.STENCIL, 100, I.cfg5_inputs(0, 2, 100))]
+    for src, n, ins in cases:
+        p, g, o = run_both(rc, src, n, ins, classify_rw=True)
+        assert_parity(g, o, ins)
+        assert all(t[7] & 0x30 in (0x10, 0x20) for t in g.report_tuples() if t[4] == 1)
+    rng = np.random.default_rng(17)
+    for it in range(150):
+        n = int(rng.integers(1, 40))
+        pr = K.random_tiny_kernel(rng, n_arrays=2, n_regs=5, n_commands=int(rng.integers(3, 12)), size=5)
+        ins = [rng.integers(-3, 4, size=(int(rng.integers(1, 4)), 5)).astype(np.int32)]
+        ins.append(rng.integers(-3, 4, size=(ins[0].shape[0], 5)).astype(np.int32))
+        p, g, o = run_both(rc, pr, n, ins, fuel=500, classify_rw=True)
+        assert_parity(g, o, ins)
+    ins = I.cfg4_inputs(0, 2, 400)
+    ins[3][:, 50:90] += 1
+    p, g, o = run_both(rc, K.random_stencil_kernel(3), 400, ins, classify_rw=True)
+    assert_parity(g, o, ins)
 
 
 def test_sort_64bit_lookback_words(rc, monkeypatch):
