@@ -38,6 +38,12 @@ WORKLOADS = {
     "cfg4": dict(name="config4: random straight-line stencil kernel (seed 0), 65536 work-items x 512 instances per GPU",
                  n=65536, per_gpu=512, src=lambda: K.random_stencil_kernel(0),
                  gen=lambda lo, hi, n: I.cfg4_inputs(lo, hi, n)),
+    "cfg3": dict(name="config3: race-free tree reduction, 1024 work-items x 16384 instances per GPU, 11 intervals",
+                 n=1024, per_gpu=16384, src=lambda: K.program(K.TREE),
+                 gen=lambda lo, hi, n: I.cfg3_inputs(lo, hi, n)),
+    "cfg3off": dict(name="config3: off-by-one tree reduction (1 OOB + 9 RW per instance), 1024 work-items x 16384 "
+                         "instances per GPU", n=1024, per_gpu=16384, src=lambda: K.program(K.TREE_OFF_BY_ONE),
+                    gen=lambda lo, hi, n: I.cfg3_inputs(lo, hi, n)),
 }
 METRIC = "checked memory accesses/s"
 UNIT = "Gaccess/s"
@@ -175,6 +181,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--instances", type=int, default=0, help="override instances per GPU (debug)")
+    ap.add_argument("--classify-rw", action="store_true",
+                    help="RW value classification (RC_OPT_CLASSIFY_RW, SURVEY §8(f) row 1)")
     ap.add_argument("--keep-all-reads", action="store_true",
                     help="RC_OPT_KEEP_ALL_READS: sort every read record (no write-set pruning)")
     args = ap.parse_args()
@@ -209,7 +217,7 @@ def main():
 
     def step(profile=False, arrs=arrays):
         r = rc_run(prog, n, arrs, instance_offset=lo, want_final=False, profile=profile, device=local,
-                   stream=stream, keep_all_reads=args.keep_all_reads)
+                   stream=stream, keep_all_reads=args.keep_all_reads, classify_rw=args.classify_rw)
         if world > 1:
             reps, st = gather_reports(r.reports, r.stats, device=dev)
         else:
@@ -336,7 +344,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": wl["name"], "work_items": n, "instances_per_gpu": hi - lo,
-                       "write_set_filter": not args.keep_all_reads,
+                       "write_set_filter": not args.keep_all_reads, "classify_rw": args.classify_rw,
                        "instances_total": total_inst, "parallelism": f"dp{world} (instance shards)",
                        "l2": "inputs 4.3 GB/GPU >> 126 MB L2 (no flush needed)",
                        "checked_accesses_per_step": accesses // args.steps, "reports_per_step": n_reports},
