@@ -113,7 +113,9 @@ constexpr size_t CTR_OFF = 4096 + 64;
 
 struct rc_workspace {
   int device = -1;
-  DevBuf code, arr_off, arr_size, heap;
+  DevBuf code, arr_off, arr_size, heap, heap2;  // working heaps of alternate batches (A2 double-buffered)
+  cudaStream_t copy_stream = nullptr;            // A2: the next batch's inputs copy in while this one runs
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_start = nullptr;
   DevBuf regs[2], pc[2], status[2], live;
   DevBuf log, log_alt, wval, wmap, sort_status, ctr_block;
   uint8_t wtag = 0;  // write-set map tag of the last interval attempt
@@ -128,7 +130,10 @@ struct rc_workspace {
   SortWorkspace sort;
   Profiler prof;
   ~rc_workspace() {
-    for (DevBuf* b : {&code, &arr_off, &arr_size, &heap, &regs[0], &regs[1], &pc[0], &pc[1], &status[0],
+    for (cudaEvent_t e : {ev_in[0], ev_in[1], ev_free[0], ev_free[1], ev_start})
+      if (e) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    for (DevBuf* b : {&code, &arr_off, &arr_size, &heap, &heap2, &regs[0], &regs[1], &pc[0], &pc[1], &status[0],
                       &status[1], &live, &log, &log_alt, &wval, &wmap, &sort_status,
                       &ctr_block, &reports, &reports_scratch, &inst_tmp, &heap_snap[0], &heap_snap[1], &heapB, &amap,
                       &regs_b, &pc_b, &status_b, &cmp_inst})  // (ctr is a view into ctr_block)
@@ -283,6 +288,9 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     W.ctr.bytes = sizeof(DevCounters);
     CK(cudaMallocHost(&W.h_ctr, 4 * sizeof(DevCounters)));
     for (cudaEvent_t& e : W.iv_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&W.copy_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&W.ev_in[0], &W.ev_in[1], &W.ev_free[0], &W.ev_free[1], &W.ev_start})
+      CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     W.sort.hist = W.ctr_block.as<uint32_t>();
     W.sort.bin_off = nullptr;  // each pass scans its counts itself
     W.sort.tile_ctr = W.sort.hist + 1024;
@@ -318,6 +326,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   // batch-sized buffers
   if (I_b) {
     CK(W.heap.ensure(std::max<uint64_t>(1, (uint64_t)I_b * cpi) * 4));
+    if (n_inst > I_b) CK(W.heap2.ensure(std::max<uint64_t>(1, (uint64_t)I_b * cpi) * 4));
     for (int b = 0; b < 2; b++) {
       CK(W.regs[b].ensure(L_pad * P->n_regs * 4));
       CK(W.pc[b].ensure(L_pad * 4));
@@ -403,20 +412,37 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   std::vector<std::array<cudaEvent_t, 2>> gap_ev;
   cudaEvent_t g0 = nullptr, g1 = nullptr;
   if (gaps) { cudaEventCreate(&g0); cudaEventCreate(&g1); cudaEventRecord(g0, s); }
-  for (uint32_t b0 = 0; b0 < n_inst; b0 += I_b) {
+  // A2, double-buffered: batch i's inputs are copied (2-D copies into the
+  // instance-major working heap) on a copy stream into heap[i & 1] while batch
+  // i - 1 runs; batch i waits for its copy, the copy of batch i + 2 waits for
+  // batch i to release the buffer (after its final-heap copy).
+  auto heap_buf = [&](uint64_t bi) -> int32_t* { return ((bi & 1) ? W.heap2 : W.heap).as<int32_t>(); };
+  bool free_recorded[2] = {false, false};
+  auto enqueue_inputs = [&](uint64_t bi, uint32_t b0) -> cudaError_t {
+    const uint32_t nb = std::min(I_b, n_inst - b0);
+    cudaError_t e = cudaSuccess;
+    if (free_recorded[bi & 1]) e = cudaStreamWaitEvent(W.copy_stream, W.ev_free[bi & 1], 0);
+    for (uint32_t a = 0; a < n_arrays && e == cudaSuccess; a++) {
+      if (!size[a]) continue;
+      e = cudaMemcpy2DAsync(heap_buf(bi) + off[a], cpi * 4, arrays[a].data + (uint64_t)b0 * size[a],
+                            (size_t)size[a] * 4, (size_t)size[a] * 4, nb,
+                            host_io ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, W.copy_stream);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(W.ev_in[bi & 1], W.copy_stream);
+    return e;
+  };
+  if (n_inst && I_b) {
+    CK(cudaEventRecord(W.ev_start, s));  // inputs the caller produced on its stream
+    CK(cudaStreamWaitEvent(W.copy_stream, W.ev_start, 0));
+    CK(enqueue_inputs(0, 0));
+  }
+  for (uint32_t b0 = 0, bi = 0; b0 < n_inst; b0 += I_b, bi++) {
     const uint32_t nb = std::min(I_b, n_inst - b0);
     const uint32_t L = nb * n;
     const uint32_t inst_base = opt.instance_offset + b0;
-    // A2: heap init
-    W.prof.cut();
-    W.prof.begin(s);
-    for (uint32_t a = 0; a < n_arrays; a++) {
-      if (!size[a]) continue;
-      CK(cudaMemcpy2DAsync(W.heap.as<int32_t>() + off[a], cpi * 4, arrays[a].data + (uint64_t)b0 * size[a],
-                           (size_t)size[a] * 4, (size_t)size[a] * 4, nb,
-                           host_io ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
-    }
-    W.prof.end(RC_PROF_COPY, s, (uint64_t)nb * cpi * 8, (uint64_t)nb * cpi);
+    int32_t* const heap_cur = heap_buf(bi);  // this batch's working heap
+    CK(cudaStreamWaitEvent(s, W.ev_in[bi & 1], 0));
+    if (b0 + I_b < n_inst) CK(enqueue_inputs(bi + 1, b0 + I_b));  // overlaps this batch
     int32_t* node_min = W.inst_tmp.as<int32_t>();
     int32_t* node_max = node_min + I_b;
     uint32_t* first_tid = reinterpret_cast<uint32_t*>(node_max + I_b);
@@ -465,7 +491,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       dp.n_lanes = L;
       dp.n = n;
       dp.n_records = (uint32_t)log_cap;  // upper bound; the kernel reads the exact count
-      dp.heap = W.heap.as<int32_t>();
+      dp.heap = heap_cur;
       dp.cpi = (uint32_t)std::max<uint64_t>(cpi, 1);
       dp.cpi_magic = div_magic(dp.cpi);
       dp.n_arrays = n_arrays;
@@ -501,7 +527,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       ip.inst_base = inst_base;
       ip.arr_off = W.arr_off.as<uint32_t>();
       ip.arr_size = W.arr_size.as<uint32_t>();
-      ip.heap = W.heap.as<int32_t>();
+      ip.heap = heap_cur;
       ip.reg_stride = reg_stride;
       ip.regs_in = W.regs[cc].as<int32_t>();
       ip.pc_in = W.pc[cc].as<uint32_t>();
@@ -543,7 +569,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       // seen this interval (two slots: the speculative next interval's copy
       // must not overwrite it)
       if (classify && cpi)
-        EQ(cudaMemcpyAsync(W.heap_snap[kk & 1].p, W.heap.p, (size_t)nb * cpi * 4, cudaMemcpyDeviceToDevice, s));
+        EQ(cudaMemcpyAsync(W.heap_snap[kk & 1].p, heap_cur, (size_t)nb * cpi * 4, cudaMemcpyDeviceToDevice, s));
       InterpParams ip = make_ip(kk, cc);
       mk->m0 = W.prof.marks.size();
       W.prof.cut();
@@ -611,7 +637,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         EQ(cudaMemsetAsync(W.ctr_block.p, 0, CTR_OFF + offsetof(DevCounters, report_count), s));
         InterpParams ip = make_ip(kk, cur);
         ip.heap = W.heap_snap[kk & 1].as<int32_t>();  // interval-start heap
-        ip.alt_heap = W.heap.as<int32_t>();           // committed heap (writers first)
+        ip.alt_heap = heap_cur;                       // committed heap (writers first)
         ip.alt_mask = W.amap.as<uint8_t>();
         ip.regs_out = W.regs_b.as<int32_t>();
         ip.pc_out = W.pc_b.as<uint32_t>();
@@ -650,7 +676,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       }
       if (W.h_ctr[2].log_overflow) return cudaErrorMemoryAllocation;
       EQ(cudaMemsetAsync(W.cmp_inst.p, 0, (size_t)nb * 4, s));
-      EQ(launch_heap_compare(W.heapB.as<int32_t>(), W.heap.as<int32_t>(), cells, (uint32_t)cpi,
+      EQ(launch_heap_compare(W.heapB.as<int32_t>(), heap_cur, cells, (uint32_t)cpi,
                              W.cmp_inst.as<uint32_t>(), s));
       EQ(launch_rw_flag(W.reports.as<rc_report>(), r0, r1, inst_base, W.cmp_inst.as<uint32_t>(), s));
       EQ(set_report_count(r1));
@@ -778,11 +804,13 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       for (uint32_t a = 0; a < n_arrays; a++) {
         if (!size[a]) continue;
         CK(cudaMemcpy2DAsync(final_heaps[a] + (uint64_t)b0 * size[a], (size_t)size[a] * 4,
-                             W.heap.as<int32_t>() + off[a], cpi * 4, (size_t)size[a] * 4, nb,
+                             heap_cur + off[a], cpi * 4, (size_t)size[a] * 4, nb,
                              host_io ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
       }
-      W.prof.end(RC_PROF_COPY, s, (uint64_t)nb * cpi * 8, (uint64_t)nb * cpi);
+      W.prof.end(RC_PROF_COPY, s, (uint64_t)nb * cpi * 4, (uint64_t)nb * cpi);
     }
+    CK(cudaEventRecord(W.ev_free[bi & 1], s));  // this batch's working heap may be refilled
+    free_recorded[bi & 1] = true;
   }
 
   if (gaps) {
