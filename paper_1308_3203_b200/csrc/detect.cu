@@ -322,10 +322,16 @@ __device__ __noinline__ void boundary_tail(const DetectParams& p) {
   __syncthreads();
   if (!last) return;
   __threadfence();
+  // an interval that will be re-run (its log or K1's reports overflowed)
+  // leaves the divergence flags of the previous interval in place: the re-run
+  // of K1 reads them (static write-set elision, InterpParams::inst_div)
+  const volatile DevCounters* cv = c;
+  const bool rerun = cv->log_overflow || cv->k1_reports > p.report_cap;
   for (uint32_t inst = threadIdx.x; inst < p.n_inst; inst += blockDim.x) {
     const int32_t lo = p.node_min[inst], hi = p.node_max[inst];
     p.node_min[inst] = 0x7FFFFFFF;
     p.node_max[inst] = (int32_t)0x80000000;
+    if (rerun) continue;
     const bool div = lo < hi;
     p.inst_flag[inst] = div;
     if (div) c->diverged = 1;

@@ -375,6 +375,7 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
     typename std::conditional<FUEL, unsigned long long, uint32_t>::type steps[H];
     uint32_t nloads[H], nstores[H];
     bool ovl_over[H];
+    uint32_t ro[H];  // arrays whose reads this lane need not log (static write-set elision)
 #pragma unroll
     for (int h = 0; h < H; h++) {
       const int l = h * T + t;
@@ -388,6 +389,11 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
       inst[h] = valid[h] ? fast_div(g[h], p.n_magic) : 0;
       tid[h] = valid[h] ? g[h] - inst[h] * p.n : 0;
       cell_base[h] = inst[h] * p.cpi;
+      // every running lane of the instance starts this interval at the same
+      // entry (interval 0, or no barrier divergence in the previous one): no
+      // lane writes an array its region never stores to (program.cpp (5))
+      ro[h] = (!ALT && p.ro_skip && running[h] && (p.interval == 0 || !p.inst_div[inst[h]]))
+                  ? __ldg(p.entry_ro + pc[h]) : 0u;
       n_own[h] = 0;
       steps[h] = 0;
       nloads[h] = 0;
@@ -482,7 +488,8 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
               }
               pc[h]++;
               nloads[h]++;
-              ok = true;
+              const uint32_t arr = (eh.x >> 8) & 0xFF;
+              ok = arr >= 32 || !((ro[h] >> arr) & 1u);  // a read of a written-in-no-way array is not logged
             }
           }
           const unsigned m = __ballot_sync(FULL, ok);

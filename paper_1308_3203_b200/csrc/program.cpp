@@ -142,6 +142,8 @@ int validate(const uint8_t* bc, size_t nbytes, rc_program* P) {
 //     instruction flagged OP_WAIT empties the set, BAR / EXIT end the interval
 //     (the lane waits for everything there).  The flag travels in the device
 //     copy of the program (dev_code).
+// (5) Per interval entry, the arrays no instruction of its barrier-free region
+//     stores to (entry_ro; see the comment at the computation).
 static void successors(const Ins& I, uint32_t pc, uint32_t n_instr, uint32_t* s, int* ns) {
   *ns = 0;
   if (I.op == RC_OP_EXIT) return;
@@ -333,6 +335,42 @@ void analyze(rc_program* P) {
   P->dev_code = P->code;
   for (uint32_t pc = 0; pc < N; pc++)
     if (wait[pc]) P->dev_code[pc].op |= OP_WAIT;
+  // (5) arrays no instruction of an interval region stores to: for every
+  //     interval entry e (pc 0, BAR + 1), the instructions reachable from e
+  //     without crossing a BAR; entry_ro[e] bit a (a < 32) = no ST to array a
+  //     there.  When every running work-item of an instance starts interval k
+  //     at the same entry e (interval 0, or interval k - 1 had no barrier
+  //     divergence), no work-item writes array a in interval k, so a read of a
+  //     can take part in no RW / WW report and no commit and
+  //     K1 need not log it — the static half of the write-set filter.
+  P->entry_ro.assign(N, 0u);
+  if ((uint64_t)N * 64 <= (1ull << 26)) {  // (bounded work: skip for huge programs)
+    std::vector<uint32_t> mark(N, 0xFFFFFFFFu), stack;
+    for (uint32_t e = 0; e < N; e++) {
+      if (!(e == 0 || P->code[e - 1].op == RC_OP_BAR)) continue;
+      uint32_t stored = 0;
+      bool big = false;  // a store to an array >= 32 (not in the mask) is fine; track nothing for it
+      stack.assign(1, e);
+      mark[e] = e;
+      while (!stack.empty()) {
+        const uint32_t pc = stack.back();
+        stack.pop_back();
+        const Ins& I = P->code[pc];
+        if (I.op == RC_OP_ST) {
+          if (I.a < 32) stored |= 1u << I.a;
+          else big = true;
+        }
+        if (I.op == RC_OP_BAR) continue;  // the region ends at the barrier
+        uint32_t sc[2];
+        int ns;
+        successors(I, pc, N, sc, &ns);
+        for (int j = 0; j < ns; j++)
+          if (mark[sc[j]] != e) { mark[sc[j]] = e; stack.push_back(sc[j]); }
+      }
+      (void)big;
+      P->entry_ro[e] = ~stored & (P->n_arrays >= 32 ? 0xFFFFFFFFu : ((1u << P->n_arrays) - 1));
+    }
+  }
 }
 
 }  // namespace rc

@@ -130,6 +130,12 @@ struct InterpParams {
   // it into the sort buffer
   uint64_t* stage;            // [stage_cap] records (make_rec) and sentinels
   unsigned long long stage_cap;
+  // static write-set elision (program.cpp analyze() (5)): a lane of an
+  // instance whose running lanes all start the interval at one entry does not
+  // log reads of the arrays entry_ro[entry] marks
+  const uint32_t* entry_ro;   // [n_instr]
+  const uint32_t* inst_div;   // [I_b] the instance's previous interval diverged (A4)
+  bool ro_skip;               // off with RC_OPT_KEEP_ALL_READS
   // RW classification re-run (null in a canonical run): a read of cell c with
   // alt_mask[c] set (and no own earlier write) returns alt_heap[c]
   const int32_t* alt_heap;
@@ -285,6 +291,7 @@ struct rc_program {
   std::vector<rc::Ins> dev_code;    // code with OP_WAIT flags (uploaded for K1)
   std::vector<uint8_t> live_regs;  // registers live across a barrier (+ live at pc 0)
   std::vector<uint8_t> live_at_entry;  // live_in(pc 0): the rows zeroed at a batch start (reading L18)
+  std::vector<uint32_t> entry_ro;  // [n_instr] at interval entries: arrays (< 32) the region never stores to
   int ovl_cap = rc::OVL_CAP;       // max distinct cells written per work-item per interval
   int rec_bound = -1;              // max log records per work-item per interval (-1 unbounded)
   int64_t instr_bound = -1;        // max instructions per work-item per interval (-1 unbounded)

@@ -116,7 +116,7 @@ struct rc_workspace {
   DevBuf code, arr_off, arr_size, heap, heap2;  // working heaps of alternate batches (A2 double-buffered)
   cudaStream_t copy_stream = nullptr;            // A2: the next batch's inputs copy in while this one runs
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_start = nullptr;
-  DevBuf regs[2], pc[2], status[2], live;
+  DevBuf regs[2], pc[2], status[2], live, entry_ro;
   DevBuf log, log_alt, wval, wmap, sort_status, ctr_block;
   uint8_t wtag = 0;  // write-set map tag of the last interval attempt
   DevBuf reports, reports_scratch;
@@ -134,7 +134,7 @@ struct rc_workspace {
       if (e) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     for (DevBuf* b : {&code, &arr_off, &arr_size, &heap, &heap2, &regs[0], &regs[1], &pc[0], &pc[1], &status[0],
-                      &status[1], &live, &log, &log_alt, &wval, &wmap, &sort_status,
+                      &status[1], &live, &entry_ro, &log, &log_alt, &wval, &wmap, &sort_status,
                       &ctr_block, &reports, &reports_scratch, &inst_tmp, &heap_snap[0], &heap_snap[1], &heapB, &amap,
                       &regs_b, &pc_b, &status_b, &cmp_inst})  // (ctr is a view into ctr_block)
       b->release();
@@ -278,6 +278,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     rc_workspace& W = *P->ws;
     CK(W.code.ensure(P->code.size() * sizeof(Ins)));
     CK(cudaMemcpy(W.code.p, P->dev_code.data(), P->dev_code.size() * sizeof(Ins), cudaMemcpyHostToDevice));
+    CK(W.entry_ro.ensure(P->entry_ro.size() * 4));
+    CK(cudaMemcpy(W.entry_ro.p, P->entry_ro.data(), P->entry_ro.size() * 4, cudaMemcpyHostToDevice));
     CK(W.live.ensure(std::max<size_t>(1, P->live_regs.size())));
     if (!P->live_regs.empty())
       CK(cudaMemcpy(W.live.p, P->live_regs.data(), P->live_regs.size(), cudaMemcpyHostToDevice));
@@ -551,6 +553,9 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       ip.ctr = dctr;
       ip.alt_heap = nullptr;
       ip.alt_mask = nullptr;
+      ip.entry_ro = W.entry_ro.as<uint32_t>();
+      ip.inst_div = inst_flag;
+      ip.ro_skip = (opt.flags & RC_OPT_KEEP_ALL_READS) == 0;
       return ip;
     };
     auto enqueue_interval = [&](uint32_t kk, int cc, Marks* mk) -> cudaError_t {

@@ -307,6 +307,38 @@ def test_random_tiny_kernels(rc):
         assert_parity(g, o, ins)
 
 
+def test_static_write_set_elision_after_divergence(rc):
+    """K1 skips the read records of arrays an interval region never stores to
+    (program.cpp analyze() (5)) only when every running work-item of the
+    instance starts the interval at the same entry.  Here the work-items split
+    over two barriers; in the next interval the ones after b1 read X[0] (their
+    region stores no X) while the ones after b2 write it: the RW race must be
+    reported, and the instance without the split (n = 2) must stay clean."""
+    src = """
+.arrays X Y
+    tid r0
+    const r1, 2
+    lt r2, r0, r1
+    br r2, left, right
+left:
+    bar
+    const r5, 0
+    ld r3, X, r5
+    exit
+right:
+    bar
+    const r5, 0
+    st X, r5, r0
+    exit
+"""
+    for n in (2, 5, 300):
+        ins = [np.arange(4, dtype=np.int32).reshape(2, 2), np.zeros((2, 3), np.int32)]
+        p, g, o = run_both(rc, src, n, ins)
+        assert_parity(g, o, ins)
+        kinds = {t[4] for t in o.report_tuples()}
+        assert (1 in kinds) == (n > 2) and (8 in kinds) == (n > 2)
+
+
 def test_rw_classification(rc):
     """SURVEY §8(f) row 1 (reading L19): with RC_OPT_CLASSIFY_RW every RW
     report carries bit 4 or 5 exactly as the oracle's re-run decides; all
