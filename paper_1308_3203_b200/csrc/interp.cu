@@ -139,7 +139,10 @@ __device__ __noinline__ uint32_t flush_warp_(const LogOut p, const uint64_t* rec
   return 0;
 }
 
-constexpr uint32_t STAGE_CHUNK = 8192;  // staging slots a block reserves at a time
+#ifndef STAGE_CHUNK_OPT
+#define STAGE_CHUNK_OPT 8192
+#endif
+constexpr uint32_t STAGE_CHUNK = STAGE_CHUNK_OPT;  // staging slots a block reserves at a time
 
 __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
 #pragma unroll
@@ -810,7 +813,12 @@ cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
                    interp_kernel<true, true, 2, false>, interp_kernel<false, true, 2, false>,
                    interp_kernel<true, false, 2, false>, interp_kernel<false, false, 2, false>,
                    interp_kernel<true, true, 1, true>, interp_kernel<false, true, 1, true>,
-                   interp_kernel<true, false, 1, true>, interp_kernel<false, false, 1, true>}) {
+                   interp_kernel<true, false, 1, true>, interp_kernel<false, false, 1, true>
+#if INTERP_H == 4
+                   , interp_kernel<true, true, 4, false>, interp_kernel<false, true, 4, false>,
+                   interp_kernel<true, false, 4, false>, interp_kernel<false, false, 4, false>
+#endif
+                   }) {
       cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       if (e != cudaSuccess) return e;
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -824,8 +832,11 @@ cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
   // (test hook RC_DEBUG_INTERP_H=1|2 forces one variant; results never differ)
   const char* force = getenv("RC_DEBUG_INTERP_H");
   const int h = force ? (force[0] == '2' ? 2 : 1)
-                      : (INTERP_H == 2 && p.n_lanes >= 2u * 256u * (uint32_t)nsm ? 2 : 1);
+                      : (INTERP_H >= 2 && p.n_lanes >= (uint32_t)INTERP_H * 256u * (uint32_t)nsm ? INTERP_H : 1);
   if (p.alt_mask) return launch_interp_h<1, true>(p, s, nsm);  // classification re-run (rare)
+#if INTERP_H == 4
+  if (h == 4) return launch_interp_h<4, false>(p, s, nsm);
+#endif
   return h == 2 ? launch_interp_h<2, false>(p, s, nsm) : launch_interp_h<1, false>(p, s, nsm);
 }
 

@@ -52,7 +52,7 @@ constexpr int OVL_CAP = 16;        // own-write overlay entries per work-item (s
 //   bits  4..1   overlay slot of a write (its final value is wval[slot][lane])
 //   bit      0   1 = write, 0 = read
 constexpr int REC_CELL_SHIFT = 32;
-constexpr uint32_t LANE_PAD = 512;  // lane-state rows are padded to multiples of this (K1 tiles of <= 512 lanes)
+constexpr uint32_t LANE_PAD = 1024;  // lane-state rows are padded to multiples of this (K1 tiles of <= 1024 lanes)
 constexpr uint32_t MAX_WG = 1u << 27;
 // Division by a run-constant divisor d (work-group size, cells per instance):
 // magic = ceil(2^64 / d) (0 for d == 1); x / d == umulhi64(x, magic) exactly
