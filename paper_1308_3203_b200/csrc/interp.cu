@@ -139,6 +139,13 @@ __device__ __noinline__ uint32_t flush_warp_(const LogOut p, const uint64_t* rec
   return 0;
 }
 
+#ifndef INTERP_INDEP  // 1: no block barrier in the tile loop (per-warp chunks and stores); measured 30% slower
+#define INTERP_INDEP 0
+#endif
+#ifndef STAGE_CHUNK_W_OPT
+#define STAGE_CHUNK_W_OPT 1024
+#endif
+constexpr uint32_t STAGE_CHUNK_W = STAGE_CHUNK_W_OPT;  // staging slots a warp reserves at a time (INTERP_INDEP)
 #ifndef STAGE_CHUNK_OPT
 #define STAGE_CHUNK_OPT 8192
 #endif
@@ -299,7 +306,9 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
 #define SREGS(b) (sregs0 + (size_t)(b) * R * TL)
 #define SPC(b) (spc0 + (size_t)(b) * TL)
 #define SSTAT(b) (sstat0 + (size_t)(b) * TL)
-  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(q); q += (8 * LS_NB + 15) & ~15;
+  // mbar[0, LS_NB): lane state of a buffer landed (TMA); mbar[LS_NB + b]
+  // (INTERP_INDEP): every warp's bulk stores have read buffer b
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(q); q += (16 * LS_NB + 15) & ~15;
   uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)W * SW * 8;
   uint4* s_code = reinterpret_cast<uint4*>(q); q += CODE_SMEM ? (size_t)(p.n_instr + 1) * 16 : 0;  // heads + pad entry
   uint2* s_tail = reinterpret_cast<uint2*>(q); q += CODE_SMEM ? (size_t)(p.n_instr + 1) * 8 : 0;   // tails + pad
@@ -311,6 +320,8 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
   uint32_t* wcnt = reinterpret_cast<uint32_t*>(q); q += (size_t)W * 4 + 8;  // per-warp staged records, pad count
   q = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(q) + 7) & ~uintptr_t(7));
   unsigned long long* wbase = reinterpret_cast<unsigned long long*>(q); q += (size_t)(W + 1) * 8;  // [W], pad start
+  (void)wcnt;
+  (void)wbase;
 
   for (uint32_t a = t; a < p.n_arrays; a += T) {
     s_off[a] = p.arr_off[a];
@@ -333,6 +344,8 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
   const uint32_t n_tiles = (p.n_lanes + TL - 1) / TL;
   if (t == 0) {
     for (int b = 0; b < LS_NB; b++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[b])));
+    for (int b = 0; b < LS_NB; b++)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar[LS_NB + b])), "r"(W));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -351,18 +364,46 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
   unsigned long long b_staged = 0;  // thread 0: records staged by the block
   uint32_t parity = 0;  // bit b: expected phase of mbar[b]
   int cur = 0;
+#if INTERP_INDEP
+  // every warp is independent inside the tile loop: its own staging chunk and
+  // its own lane-state bulk stores; buffer b is refilled only after all warps
+  // arrived on mbar[LS_NB + b] (their stores read it)
+  unsigned long long w_base = 0;  // this warp's staging chunk (warp-uniform)
+  uint32_t w_used = 0, w_cap = 0;
+  uint32_t eparity = 0;           // thread 0: expected phase of each empty barrier
+  uint32_t eused = 0;             // thread 0: buffers that held a tile before
+  int prev = -1;                  // buffer of this warp's previous tile
+#endif
 #ifdef INTERP_PHASE_TIMING
   long long tprev_ = clock64();
 #endif
   for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, cur = cur + 1 == LS_NB ? 0 : cur + 1) {
     // prefetch the next tile's lane state into the next buffer once the bulk
     // stores of its previous use (LS_NB - 1 tiles back) have read it
+#if INTERP_INDEP
+    // this warp's stores of its previous tile have read their buffer: say so
+    if (lane == 0 && prev >= 0) {
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&mbar[LS_NB + prev])) : "memory");
+    }
+    if (t == 0 && tile + gridDim.x < n_tiles) {
+      const int nx = cur + 1 == LS_NB ? 0 : cur + 1;
+      if ((eused >> nx) & 1u) {  // its previous tile's stores must be done
+        mbar_wait_parity(&mbar[LS_NB + nx], (eparity >> nx) & 1u);
+        eparity ^= 1u << nx;
+      }
+      eused |= 1u << nx;
+      prefetch_lanes(p, tile + gridDim.x, TL, SSTAT(nx), SPC(nx), SREGS(nx), s_live, &mbar[nx]);
+    }
+    if (t == 0) eused |= 1u << cur;
+#else
     if (t == 0 && tile + gridDim.x < n_tiles) {
       const int nx = cur + 1 == LS_NB ? 0 : cur + 1;
       if (LS_NB == 2) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       prefetch_lanes(p, tile + gridDim.x, TL, SSTAT(nx), SPC(nx), SREGS(nx), s_live, &mbar[nx]);
     }
+#endif
     IPHASE(0);
     mbar_wait_parity(&mbar[cur], (parity >> cur) & 1u);
     parity ^= 1u << cur;
@@ -663,6 +704,57 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
       if (lane == 0) S.recs[S.fill] = REC_SENTINEL;
       S.fill++;
     }
+#if INTERP_INDEP
+    {
+      // this warp's staging room: its own chunk (a new one — one atomic — when
+      // full; the abandoned tail is padded with sentinels)
+      unsigned long long pad_from = 0;
+      uint32_t pad_n = 0;
+      if (S.fill && w_used + S.fill > w_cap) {
+        pad_from = w_base + w_used;
+        pad_n = w_cap - w_used;
+        const uint32_t sz = max(STAGE_CHUNK_W, S.fill);
+        unsigned long long nb = 0;
+        if (lane == 0) nb = atomicAdd(&p.ctr->stage_count, (unsigned long long)sz);
+        w_base = __shfl_sync(FULL, nb, 0);
+        w_used = 0;
+        w_cap = sz;
+      }
+      const unsigned long long base = w_base + w_used;
+      w_used += S.fill;
+      if (lane == 0) b_staged += S.fill;
+      for (uint32_t i = lane; i < pad_n; i += 32)
+        if (pad_from + i < p.stage_cap) p.stage[pad_from + i] = REC_SENTINEL;
+      // lane state out: this warp's slices of the status / pc / live register
+      // rows, and its records: bulk stores issued by lane 0
+#pragma unroll
+      for (int h = 0; h < H; h++) {
+        sstat[h * T + t] = valid[h] ? status[h] : (uint8_t)L_EXITED;
+        spc[h * T + t] = pc[h];
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int h = 0; h < H; h++) {
+          const uint32_t l0 = h * T + warp * 32;
+          const size_t g0 = (size_t)tile * TL + l0;
+          bulk_s2g(p.status_out + g0, sstat + l0, 32u);
+          bulk_s2g(p.pc_out + g0, spc + l0, 128u);
+          for (uint32_t i = 0; i < p.n_live; i++) {
+            const uint32_t r = s_live[i];
+            bulk_s2g(p.regs_out + (size_t)r * p.reg_stride + g0, SREGS(cur) + (size_t)r * TL + l0, 128u);
+          }
+        }
+        if (S.fill) {
+          if (base + S.fill <= p.stage_cap) bulk_s2g(p.stage + base, S.recs, S.fill * 8u);
+          else b_over = true;
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      prev = cur;
+    }
+#else
     if (lane == 0) wcnt[warp] = S.fill;
     __syncthreads();
     IPHASE(4);
@@ -731,6 +823,7 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
     }
     for (uint32_t i = t; i < wcnt[W]; i += T)  // sentinels in the abandoned chunk tail
       if (wbase[W] + i < p.stage_cap) p.stage[wbase[W] + i] = REC_SENTINEL;
+#endif
     IPHASE(6);
     // no block barrier here: the next tile's first __syncthreads orders every
     // shared word a warp could overwrite early (wcnt / wbase are rewritten only
@@ -740,6 +833,11 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
   }
 
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // record / lane-state stores complete
+#if INTERP_INDEP
+  if (lane == 0 && b_staged) atomicAdd(&p.ctr->staged_recs, b_staged);
+  for (uint32_t i = lane; i < w_cap - w_used; i += 32)  // sentinels in this warp's last chunk tail
+    if (w_base + w_used + i < p.stage_cap) p.stage[w_base + w_used + i] = REC_SENTINEL;
+#else
   if (t == 0) {
     if (b_staged) atomicAdd(&p.ctr->staged_recs, b_staged);
   }
@@ -751,6 +849,7 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
   __syncthreads();
   for (uint32_t i = t; i < wcnt[W]; i += T)
     if (wbase[W] + i < p.stage_cap) p.stage[wbase[W] + i] = REC_SENTINEL;
+#endif
   if (__any_sync(FULL, b_over) && lane == 0) p.ctr->log_overflow = 1;
   {  // per-warp totals
     b_instr = warp_sum64(b_instr);
@@ -773,7 +872,7 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
 size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem, int H) {
   const int W = T / 32, TL = H * T;
   size_t b = (size_t)LS_NB * p.n_regs * TL * 4;                // register files (LS_NB buffers)
-  b += (size_t)LS_NB * TL * 5 + ((8 * LS_NB + 15) & ~15);      // status / pc rows, mbarriers
+  b += (size_t)LS_NB * TL * 5 + ((16 * LS_NB + 15) & ~15);     // status / pc rows, mbarriers
   b += (size_t)W * H * p.stage_warp * 8;                        // staging
   b += code_in_smem ? (size_t)(p.n_instr + 1) * 24 : 0;        // pre-decoded program + pad entry
   b += (size_t)p.ovl_cap * TL * 8;                             // overlay
