@@ -300,8 +300,11 @@ def main():
         return 0
 
     PER_INTERVAL = ("interp", "filter", "hist", "sort", "detect", "boundary")
+    clocks = clk.summary()
+    clk_mhz = clocks.get("sm_mhz")  # median SM clock during the timed steps
+    n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
     peak, peak_src = peaks()
-    roofline = None
+    roofline = roofline_interp = roofline_detect = None
     kernels = None
     gpu_launches = None
     if prof_sum:
@@ -310,6 +313,7 @@ def main():
         achieved = s["alg_bytes"] / (s["ms"] / 1e3) / 1e9 if s["ms"] > 0 else None
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        tr = {}
         if os.path.exists(tpath):
             with open(tpath) as f:
                 tr = json.load(f)
@@ -321,6 +325,32 @@ def main():
                     "alg_bytes_per_record": 16, "launches_sampled": s["launches"],
                     "sampling": f"CUDA events around every {every}th interval's kernels of the timed steps",
                     "peak_source": peak_src, "library_baseline": cub_baseline()}
+        # the detect kernel (K4+K5): every sorted record read, one value
+        # gathered and one cell committed per write record
+        dd = prof_sum["detect"]
+        dach = dd["alg_bytes"] / (dd["ms"] / 1e3) / 1e9 if dd["ms"] > 0 else None
+        roofline_detect = {"kernel": "detect_kernel (K4+K5, segmented detect + commit, A4 tail)", "bound": "hbm",
+                           "achieved": dach, "peak": peak, "unit": "GB/s",
+                           "frac": dach / peak if dach else None,
+                           "traffic": tr.get("detect_kernel", {}).get("dram_bytes_per_launch"),
+                           "alg_bytes_per_launch": dd["alg_bytes"] / max(1, dd["launches"]),
+                           "alg_bytes": "8 per sorted record + 8 per write record"}
+        # the interpreter (K1), the largest share of the step: issue-bound
+        # (ALU/LSU pipes, no contraction).  Achieved = ncu's warp instructions
+        # of one launch / (live average launch duration x SM clock x SMs);
+        # peak = 4 warp instructions per cycle per SM (4 SMSPs, 1 issue each).
+        di = prof_sum["interp"]
+        ti = tr.get("interp_kernel", {})
+        ipc = None
+        if di["ms"] > 0 and di["launches"] and ti.get("warp_instructions_per_launch") and clk_mhz:
+            avg_s = di["ms"] / di["launches"] / 1e3
+            ipc = ti["warp_instructions_per_launch"] / (avg_s * clk_mhz * 1e6 * n_sms)
+        roofline_interp = {"kernel": "interp_kernel (K1, bytecode interpreter)", "bound": "alu",
+                           "achieved": ipc, "peak": 4.0, "unit": "warp-instr/cycle/SM",
+                           "frac": ipc / 4.0 if ipc else None,
+                           "ncu_ipc_per_sm": ti.get("ipc_per_sm"),
+                           "peak_source": "B200: 4 SMSPs per SM, one warp instruction issued per SMSP per cycle",
+                           "traffic": ti.get("dram_bytes_per_launch")}
         kernels = {"sample_every": every}
         for c in ("interp", "filter", "hist", "sort", "detect", "boundary", "finalize", "copy"):
             d = prof_sum[c]
@@ -348,11 +378,12 @@ def main():
                        "instances_total": total_inst, "parallelism": f"dp{world} (instance shards)",
                        "l2": "inputs 4.3 GB/GPU >> 126 MB L2 (no flush needed)",
                        "checked_accesses_per_step": accesses // args.steps, "reports_per_step": n_reports},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+            "roofline": roofline, "roofline_interp": roofline_interp, "roofline_detect": roofline_detect,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
             "interpreter": {"bytecode_instr_per_s": instrs / args.steps / (ms_step / 1000),
                             "bytecode_instr_per_step": instrs / args.steps,
                             "bound": "issue (ALU/LSU pipes; ncu sm__inst_executed.avg.per_cycle_active in profiles/)"},
-            "clocks": clk.summary(), "kernels": kernels}
+            "clocks": clocks, "kernels": kernels}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
   // record there sets log_overflow): clamp to the capacity
   const uint64_t nr = min(p.ctr->stage_count, (unsigned long long)p.n_slots);
   const uint64_t step = (uint64_t)gridDim.x * F_THREADS * F_ITEMS;
+  uint32_t kept_w = 0;  // kept write records (profile: detect's value gathers and commits)
   __syncthreads();
   for (uint64_t b0 = (uint64_t)blockIdx.x * F_THREADS * F_ITEMS; b0 < nr; b0 += step) {
     uint64_t rec[F_ITEMS];
@@ -59,7 +60,10 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
     }
     uint32_t mine = 0;
 #pragma unroll
-    for (int j = 0; j < F_ITEMS; j++) mine += keep[j];
+    for (int j = 0; j < F_ITEMS; j++) {
+      mine += keep[j];
+      kept_w += keep[j] && (rec[j] & 1);
+    }
     // block-exclusive offsets of this thread's kept records
     uint32_t x = mine;
 #pragma unroll
@@ -105,6 +109,8 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
   }
   for (int i = t; i < p.passes * 256; i += F_THREADS)
     if (bh[i]) atomicAdd(&p.hist[i], bh[i]);
+  for (int o = 16; o > 0; o >>= 1) kept_w += __shfl_xor_sync(FULL, kept_w, o);
+  if (lane == 0 && kept_w) atomicAdd(&p.ctr->kept_writes, (unsigned long long)kept_w);
 }
 
 cudaError_t launch_filter(const FilterParams& p, cudaStream_t s) {

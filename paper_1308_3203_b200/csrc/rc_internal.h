@@ -84,6 +84,7 @@ struct DevCounters {
   unsigned int diverged;            // per interval
   unsigned long long k1_reports;    // report_count after K1 (snapshot taken by the filter)
   unsigned long long rw_reports;    // RW reports emitted by detect (RC_OPT_CLASSIFY_RW)
+  unsigned long long kept_writes;   // write records among the kept ones (profile bytes of detect)
   // ---- fields above: zeroed per interval attempt (one memset, runtime.cu)
   unsigned long long report_count;  // reports appended (whole run, rolled back on retry)
   unsigned long long lanes_final[8];

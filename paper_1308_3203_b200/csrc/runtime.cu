@@ -771,7 +771,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         for (size_t i = mk_cur.m0; i < mk_cur.m1; i++) {
           Profiler::Mark& m = W.prof.marks[i];
           if (m.cls == RC_PROF_SORT) { m.bytes = Ns * 16; m.items = Ns; }
-          if (m.cls == RC_PROF_DETECT) { m.bytes = Ns * 8; m.items = Ns; }
+          // detect: every record read, a value gathered and a cell committed per write record
+          if (m.cls == RC_PROF_DETECT) { m.bytes = Ns * 8 + h.kept_writes * 8; m.items = Ns; }
           if (m.cls == RC_PROF_FILTER) { m.bytes = Nslots * 8 + h.staged_recs + Ns * 8; m.items = Nslots; }
         }
       }

@@ -108,15 +108,20 @@ def main():
         s, d = summarize_rep(rep)
         open(os.path.join(PROF, f"{a.round}{tag}_ncu_{base}.txt"), "w").write(s + "\n")
         print(s)
-        if base == "prof_onesweep":
+        if base in ("prof_onesweep", "prof_detect", "prof_interp"):
             mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             byts = sum(float(d[k].replace(",", "")) * mult[d["_units"][k]]
                        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-            json.dump({"onesweep_kernel": {"dram_bytes_per_launch": byts,
-                                           "source": f"profiles/{a.round}{tag}_ncu_{base}.txt (ncu --set full "
-                                                     "--cache-control all, one launch of the bench workload: "
-                                                     "dram__bytes_read.sum + dram__bytes_write.sum)"}},
-                      open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
+            path = os.path.join(PROF, "ncu_traffic.json")
+            tr = json.load(open(path)) if os.path.exists(path) else {}
+            name = {"prof_onesweep": "onesweep_kernel", "prof_detect": "detect_kernel",
+                    "prof_interp": "interp_kernel"}[base]
+            tr[name] = {"dram_bytes_per_launch": byts,
+                        "warp_instructions_per_launch": float(d["smsp__inst_executed.sum"].replace(",", "")),
+                        "ipc_per_sm": float(d["sm__inst_executed.avg.per_cycle_active"].replace(",", "")),
+                        "source": f"profiles/{a.round}{tag}_ncu_{base}.txt (ncu --set full --cache-control all, "
+                                  "one launch of the bench workload)"}
+            json.dump(tr, open(path, "w"), indent=1)
 
 
 if __name__ == "__main__":
