@@ -145,7 +145,7 @@ __device__ __noinline__ uint32_t flush_warp_(const LogOut p, const uint64_t* rec
 #ifndef STAGE_CHUNK_W_OPT
 #define STAGE_CHUNK_W_OPT 1024
 #endif
-constexpr uint32_t STAGE_CHUNK_W = STAGE_CHUNK_W_OPT;  // staging slots a warp reserves at a time (INTERP_INDEP)
+[[maybe_unused]] constexpr uint32_t STAGE_CHUNK_W = STAGE_CHUNK_W_OPT;  // staging slots a warp reserves at a time (INTERP_INDEP)
 #ifndef STAGE_CHUNK_OPT
 #define STAGE_CHUNK_OPT 8192
 #endif
