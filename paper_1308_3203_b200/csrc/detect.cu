@@ -26,11 +26,13 @@ constexpr uint32_t INF = 0xFFFFFFFFu;
 // record fields (rc_internal.h make_rec); a write's final value lives in the
 // side table wval[slot][lane], lane = (cell / cpi) * n + tid
 __device__ __forceinline__ uint32_t rec_cell(uint64_t r) { return (uint32_t)(r >> REC_CELL_SHIFT); }
+// the batch lane of the access (inst_local * n + tid): inside one cell (one
+// instance) lanes order exactly like tids, so every statistic below is kept on
+// lanes and emit() turns them into tids
 __device__ __forceinline__ uint32_t rec_tid(uint64_t r) { return ((uint32_t)r >> 5) & (MAX_WG - 1); }
 __device__ __forceinline__ bool rec_w(uint64_t r) { return (r & 1) != 0; }
 __device__ __forceinline__ int32_t rec_val(const DetectParams& p, uint64_t r) {
-  const uint32_t lane = fast_div(rec_cell(r), p.cpi_magic) * p.n + rec_tid(r);
-  return __ldg(p.wval + (size_t)(((uint32_t)r >> 1) & 0xF) * p.n_lanes + lane);
+  return __ldg(p.wval + (size_t)(((uint32_t)r >> 1) & 0xF) * p.n_lanes + rec_tid(r));
 }
 
 __device__ __forceinline__ void emit(const DetectParams& p, uint32_t cell, uint32_t t1, uint32_t t2, uint16_t kind,
@@ -39,6 +41,8 @@ __device__ __forceinline__ void emit(const DetectParams& p, uint32_t cell, uint3
   if (kind == RC_RW) atomicAdd(&p.ctr->rw_reports, 1ull);
   const uint32_t inst = fast_div(cell, p.cpi_magic);
   const uint32_t rem = cell - inst * p.cpi;
+  t1 -= inst * p.n;  // batch lanes -> tids
+  if (t2 != INF) t2 -= inst * p.n;
   uint32_t a = 0;
   while (a + 1 < p.n_arrays && __ldg(p.arr_off + a + 1) <= rem) a++;
   unsigned long long pos = atomicAdd(&p.ctr->report_count, 1ull);

@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
           const unsigned m = __ballot_sync(FULL, ok);
           if (m) {
             if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane);
-            if (ok) S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, tid[h], 0, 0);
+            if (ok) S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, g[h], 0, 0);
             S.fill += __popc(m);
           }
         }
@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
         if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane);
         if (has) {
           const uint32_t cell = ocell[j * TL + l];
-          S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, tid[h], (uint32_t)j, 1);
+          S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, g[h], (uint32_t)j, 1);
           p.wval[(size_t)j * p.n_lanes + g[h]] = oval[j * TL + l];
           p.wmap[cell] = p.wtag;  // write-set map (filter.cu)
         }

@@ -48,7 +48,9 @@ constexpr int OVL_CAP = 16;        // own-write overlay entries per work-item (s
 
 // One access-log record is a single u64:
 //   bits 63..32  cell id (batch-local; the sort key — only these bits are sorted)
-//   bits 31..5   tid (< 2^27)
+//   bits 31..5   batch lane = inst_local * n + tid (< 2^27; within one cell —
+//                one instance — lanes order like tids, and the lane indexes
+//                the write-value side table without a division)
 //   bits  4..1   overlay slot of a write (its final value is wval[slot][lane])
 //   bit      0   1 = write, 0 = read
 constexpr int REC_CELL_SHIFT = 32;
@@ -64,8 +66,8 @@ __device__ __forceinline__ uint32_t fast_div(uint32_t x, uint64_t magic) {
   return magic ? (uint32_t)__umul64hi((uint64_t)x, magic) : x;
 }
 #endif
-__host__ __device__ inline uint64_t make_rec(uint32_t cell, uint32_t tid, uint32_t slot, uint32_t w) {
-  return ((uint64_t)cell << 32) | (tid << 5) | (slot << 1) | w;
+__host__ __device__ inline uint64_t make_rec(uint32_t cell, uint32_t lane, uint32_t slot, uint32_t w) {
+  return ((uint64_t)cell << 32) | (lane << 5) | (slot << 1) | w;
 }
 
 static_assert(RC_OVERLAY_CAP == OVL_CAP, "overlay capacity in rc.h and the interpreter agree");

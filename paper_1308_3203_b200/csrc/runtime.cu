@@ -182,7 +182,7 @@ uint32_t plan_batch(uint32_t n_inst, uint32_t n, uint64_t cpi, uint32_t n_regs, 
                     size_t free_bytes) {
   if (n_inst == 0) return 0;
   const uint64_t cells_cap = cpi ? (uint64_t)0xFFFFFFFFull / cpi : (uint64_t)n_inst;
-  const uint64_t lane_cap = n ? ((uint64_t)1 << 31) / n : (uint64_t)n_inst;
+  const uint64_t lane_cap = n ? ((uint64_t)1 << 27) / n : (uint64_t)n_inst;  // batch lanes fit the record's 27 bits
   // bytes per lane: 2x lane state + node + ~6 log records (keys+vals, double buffered)
   const uint64_t per_lane = 2 * (4ull * n_regs + 5) + 4 + 6 * 24;
   const uint64_t per_inst = (uint64_t)n * per_lane + cpi * 4 + 16;
