@@ -202,10 +202,18 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    # (RC_BENCH_BACKEND=gloo: test hook that runs the N>1 path on one GPU —
+    # ranks share device 0 — when no multi-GPU box is at hand)
+    backend = os.environ.get("RC_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cdev = dev if backend == "nccl" else torch.device("cpu")  # where collectives' tensors live
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     total_inst = wl["per_gpu"] * world if args.scaling == "weak" else wl["per_gpu"]
     lo, hi = shard(total_inst, rank, world)
     n = wl["n"]
@@ -219,7 +227,7 @@ def main():
         r = rc_run(prog, n, arrs, instance_offset=lo, want_final=False, profile=profile, device=local,
                    stream=stream, keep_all_reads=args.keep_all_reads, classify_rw=args.classify_rw)
         if world > 1:
-            reps, st = gather_reports(r.reports, r.stats, device=dev)
+            reps, st = gather_reports(r.reports, r.stats, device=cdev)
         else:
             reps, st = r.reports, r.stats
         return r, reps, st
@@ -256,7 +264,7 @@ def main():
         torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms], device=cdev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
@@ -286,7 +294,7 @@ def main():
         torch.cuda.synchronize(dev)
         ems = a0.elapsed_time(a1)
         if world > 1:
-            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            t = torch.tensor([ems], device=cdev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         e2e = {"value": acc2 / args.e2e_steps / (ems / args.e2e_steps / 1000) / 1e9, "unit": UNIT,
