@@ -312,6 +312,7 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
   uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)W * SW * 8;
   uint4* s_code = reinterpret_cast<uint4*>(q); q += CODE_SMEM ? (size_t)(p.n_instr + 1) * 16 : 0;  // heads + pad entry
   uint2* s_tail = reinterpret_cast<uint2*>(q); q += CODE_SMEM ? (size_t)(p.n_instr + 1) * 8 : 0;   // tails + pad
+  uint32_t* s_ro = reinterpret_cast<uint32_t*>(q); q += CODE_SMEM ? (size_t)(p.n_instr + 1) * 4 : 0; // entry_ro
   uint32_t* ocell = reinterpret_cast<uint32_t*>(q); q += (size_t)OV * TL * 4;
   int32_t* oval = reinterpret_cast<int32_t*>(q); q += (size_t)OV * TL * 4;
   uint32_t* s_off = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
@@ -333,6 +334,7 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
       const Dec d = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + i), TL, s_off, s_size);
       s_code[i] = d.h;
       s_tail[i] = d.t;
+      s_ro[i] = __ldg(p.entry_ro + i);
     }
     if (t == 0) {  // pad entry (never executed)
       s_code[p.n_instr] = make_uint4(0, 0, 0, 0);
@@ -405,13 +407,20 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
     }
 #endif
     IPHASE(0);
+    // per-lane state, lane h*T + t of the tile
+    uint32_t g[H], pc[H], inst[H], tid[H], cell_base[H];
+    uint32_t div[H];  // the instance's previous interval diverged (loaded before the lane state lands)
+#pragma unroll
+    for (int h = 0; h < H; h++) {
+      g[h] = tile * (uint32_t)TL + h * T + t;
+      inst[h] = g[h] < p.n_lanes ? fast_div(g[h], p.n_magic) : 0;
+      div[h] = (!ALT && p.ro_skip && p.interval > 0 && g[h] < p.n_lanes) ? __ldg(p.inst_div + inst[h]) : 0u;
+    }
     mbar_wait_parity(&mbar[cur], (parity >> cur) & 1u);
     parity ^= 1u << cur;
     IPHASE(1);
     uint8_t* const sstat = SSTAT(cur);
     uint32_t* const spc = SPC(cur);
-    // per-lane state, lane h*T + t of the tile
-    uint32_t g[H], pc[H], inst[H], tid[H], cell_base[H];
     uint8_t status[H];
     bool valid[H], running[H];
     int n_own[H];
@@ -423,21 +432,19 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
 #pragma unroll
     for (int h = 0; h < H; h++) {
       const int l = h * T + t;
-      g[h] = tile * (uint32_t)TL + l;
       valid[h] = g[h] < p.n_lanes;
       status[h] = valid[h] ? sstat[l] : (uint8_t)L_EXITED;
       pc[h] = valid[h] ? spc[l] : 0;
       if (status[h] == L_EXITED_NOW) status[h] = L_EXITED;
       running[h] = valid[h] && (status[h] == L_RUNNING || status[h] == L_WAITING);
       if (running[h]) status[h] = L_RUNNING;
-      inst[h] = valid[h] ? fast_div(g[h], p.n_magic) : 0;
       tid[h] = valid[h] ? g[h] - inst[h] * p.n : 0;
       cell_base[h] = inst[h] * p.cpi;
       // every running lane of the instance starts this interval at the same
       // entry (interval 0, or no barrier divergence in the previous one): no
       // lane writes an array its region never stores to (program.cpp (5))
-      ro[h] = (!ALT && p.ro_skip && running[h] && (p.interval == 0 || !p.inst_div[inst[h]]))
-                  ? __ldg(p.entry_ro + pc[h]) : 0u;
+      ro[h] = (!ALT && p.ro_skip && running[h] && !div[h])
+                  ? (CODE_SMEM ? s_ro[pc[h]] : __ldg(p.entry_ro + pc[h])) : 0u;
       n_own[h] = 0;
       steps[h] = 0;
       nloads[h] = 0;
@@ -874,7 +881,7 @@ size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem, int H)
   size_t b = (size_t)LS_NB * p.n_regs * TL * 4;                // register files (LS_NB buffers)
   b += (size_t)LS_NB * TL * 5 + ((16 * LS_NB + 15) & ~15);     // status / pc rows, mbarriers
   b += (size_t)W * H * p.stage_warp * 8;                        // staging
-  b += code_in_smem ? (size_t)(p.n_instr + 1) * 24 : 0;        // pre-decoded program + pad entry
+  b += code_in_smem ? (size_t)(p.n_instr + 1) * 28 : 0;        // pre-decoded program + pad entry, entry_ro
   b += (size_t)p.ovl_cap * TL * 8;                             // overlay
   b += (size_t)p.n_arrays * 8;                                 // array offsets / sizes
   b += ((size_t)p.n_live + 3) & ~size_t(3);                    // live register list
