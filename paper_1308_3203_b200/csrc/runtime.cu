@@ -119,6 +119,9 @@ struct rc_workspace {
   DevBuf regs[2], pc[2], status[2], live, entry_ro;
   DevBuf log, log_alt, wval, wmap, sort_status, ctr_block;
   uint8_t wtag = 0;  // write-set map tag of the last interval attempt
+  bool plan_valid = false;      // cached batch plan (rc_run)
+  uint64_t plan_key[4] = {0, 0, 0, 0};
+  uint32_t plan_ib = 0;
   DevBuf reports, reports_scratch;
   DevBuf inst_tmp;  // node_min | node_max | first_tid | second_tid | inst_flag  ([I_b] each)
   // RW classification: interval-start heaps (two slots), the re-run's heap,
@@ -318,9 +321,17 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   CK(cudaMemcpyAsync(W.arr_size.p, size.data(), (n_arrays + 1) * 4, cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(W.ctr.p, 0, sizeof(DevCounters), s));
 
-  size_t free_b = 0, total_b = 0;
-  CK(cudaMemGetInfo(&free_b, &total_b));
-  const uint32_t I_b = plan_batch(n_inst, n, cpi, P->n_regs, opt.max_batch_instances, free_b);
+  // batch plan, cached per shape: cudaMemGetInfo can take milliseconds (it
+  // was the largest host stall between back-to-back runs)
+  const uint64_t plan_key[4] = {n_inst, n, cpi, opt.max_batch_instances};
+  if (!W.plan_valid || memcmp(plan_key, W.plan_key, sizeof plan_key) != 0) {
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    W.plan_ib = plan_batch(n_inst, n, cpi, P->n_regs, opt.max_batch_instances, free_b);
+    memcpy(W.plan_key, plan_key, sizeof plan_key);
+    W.plan_valid = true;
+  }
+  const uint32_t I_b = W.plan_ib;
   const uint64_t L_max = (uint64_t)I_b * n;
   const uint64_t L_pad = (L_max + LANE_PAD - 1) / LANE_PAD * LANE_PAD + LANE_PAD;  // TMA rows, + a spare tile
   const int key_bits = bits_for((uint64_t)I_b * std::max<uint64_t>(cpi, 1));
