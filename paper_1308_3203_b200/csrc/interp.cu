@@ -1,40 +1,49 @@
 // interp.cu — K1: one barrier interval of the §4 thread-local semantics for
 // every live work-item of an instance batch, fused with the interval-boundary
-// bookkeeping (A4), the write-set map and the sort's digit histograms.
+// bookkeeping (A4) and the write-set map.
 //
-// One CUDA thread = one simulated work-item (lane).  A warp is one instruction
-// stream: each step it executes the instruction at the minimum pc among its
-// running lanes (uniform fetch/decode from the program staged in shared
-// memory), lanes at that pc execute it, the rest wait — a lane's result never
-// depends on the order because, inside an interval, lanes only see the
-// interval-start heap plus their own writes (delayed visibility, reading L2).
-// The grid is persistent: a block walks tiles of T lanes, so the program is
-// staged once and histograms / statistics are flushed once per block.
+// One simulated work-item = one lane; a CUDA thread runs H lanes (H = 2 for
+// large batches: lanes t and t + T of a tile of H·T lanes).  A warp is one
+// instruction stream: each step it executes the instruction at the minimum pc
+// among its running lanes (one redux.sync, a uniform fetch of the pre-decoded
+// instruction from shared memory, a flat jump table), lanes at that pc
+// execute it, the rest wait — a lane's result never depends on the order
+// because, inside an interval, lanes only see the interval-start heap plus
+// their own writes (delayed visibility, reading L2).  The grid is persistent:
+// a block walks tiles, so the program is staged once and statistics are
+// flushed once per block.
 //
 // Per lane: registers (Locals) live in shared memory laid out
-// [reg][thread] (a warp touching one register hits 32 distinct banks); only
-// the registers live across a barrier (program.cpp analyze()) travel through
-// HBM between intervals.  The own-write overlay (cell, value), sized by the
-// static bound on stores per interval, also lives in shared memory.
+// [reg][lane] (a warp touching one register hits 32 distinct banks),
+// addressed through 32-bit shared-window addresses; only the registers live
+// across a barrier (program.cpp analyze()) travel between intervals, as TMA
+// bulk copies (the next tile's rows land while this tile runs).  The
+// own-write overlay (cell, value), sized by the static bound on stores per
+// interval, also lives in shared memory.  A heap LD is a cp.async straight
+// into the destination register; the lane waits only before an instruction
+// the static pending-load analysis flagged (OP_WAIT).
 //
 // Rules implemented: assign (170), store (176/179) into the
 // overlay, load (182/185, reading L11) from the overlay else the interval-start
 // heap, assert (188) -> ⊥ report, assume (194) -> ⊤, barrier (200) -> suspend.
 // ⊥ halts only the faulting lane (reading L5).  Every executed instruction
-// costs one unit of fuel (reading L17).
+// costs one unit of fuel (reading L17); the check is compiled out when the
+// static longest barrier-free path fits in the fuel.
 //
-// Log: a read record per performed LD, and at the end of the interval one
-// write record per distinct cell the lane wrote (its final value, reading L3,
-// goes to the side table wval[slot][lane]).  Records are staged per warp in
-// shared memory; the tile's write-out takes ONE atomic per record kind per
-// block: write records go straight into the sort buffer (and mark their cell
-// in the write-set byte map), read records into a staging buffer that the
-// write-set filter compacts (filter.cu).
+// Log: a read record per performed LD (unless static write-set elision
+// proves the array unwritten in this interval), and at the end of the
+// interval one write record per distinct cell the lane wrote (its final
+// value, reading L3, goes to the side table wval[slot][lane]; the cell is
+// marked in the tagged write-set map).  Records are staged per warp in shared
+// memory, and each warp's slice leaves as one TMA bulk store into the block's
+// chunk of the staging buffer (one atomic per 8192 slots); the write-set
+// filter (filter.cu) compacts it for the sort.
 //
 // Fused A4 (reading L9): per instance the min / max arrival
 // node (BAR pc, or -1 for exit) of the lanes that arrived in this interval —
-// equal min and max means every arrival reached the same barrier — and a
-// global "some lane is suspended" flag.
+// equal min and max means every arrival reached the same barrier — pushed
+// only when it widens what the warp pushed before, and a global "some lane is
+// suspended" flag.
 #include <cstdlib>
 #include <type_traits>
 

@@ -6,15 +6,20 @@
 // only the live cell bits are sorted (8-bit digits).  The sort is stable, and
 // the detector only uses order-independent reductions inside a cell.
 //
-// Onesweep (Adinets & Merrill): one upfront pass computes the digit
-// histograms of every pass (K2), then each pass (K3) is a single kernel:
+// Onesweep (Adinets & Merrill): the digit histograms of every pass come
+// first (fused into the write-set filter; hist_kernel otherwise), then each
+// pass (K3) is a single persistent kernel, 2 blocks per SM:
+//   * each block scans the pass's digit counts (global digit starts),
 //   * a block claims tile t from an atomic counter (in-order claiming gives
-//     forward progress to the look-back),
-//   * the tile (4096 records = 16 KB keys + 32 KB values) is staged into
-//     shared memory with two TMA bulk copies (cp.async.bulk + mbarrier),
-//   * stable in-tile ranking with __match_any_sync per warp,
+//     forward progress to the look-back) only after its previous tile's
+//     look-back; the tile (4096 records, 32 KB) arrives by a TMA bulk copy
+//     (cp.async.bulk + mbarrier) while the previous tile is written out,
+//   * digit peers per warp round through shared-memory lane masks (atomicOr,
+//     three rotating mask sets), stable in-tile ranking from per-warp digit
+//     counters,
 //   * per digit: publish the tile's count (AGGREGATE), look back over
-//     predecessors until an INCLUSIVE prefix is found, publish INCLUSIVE,
+//     predecessors (4 per L2 round trip) until an INCLUSIVE prefix is found,
+//     publish INCLUSIVE,
 //   * scatter to shared memory in digit order and write out coalesced runs.
 // Status words carry an epoch so the look-back array is re-zeroed only when
 // the epoch wraps (32-bit words for sorts of < 2^26 records, else 64-bit).
