@@ -2,7 +2,8 @@
 //
 // K1 staged the interval's access records in per-block chunks of one staging
 // buffer (unused chunk tails hold REC_SENTINEL) and marked every written cell
-// in the byte map wmap.  This pass keeps every write record and the read
+// in the byte map wmap with this interval's tag.  This pass keeps every write
+// record and the read
 // records of written cells and writes them densely to the sort buffer.  A read
 // of a cell that no work-item wrote in this interval can take part in no RW
 // report (P:224-229 needs a writer), no WW report and no commit, so

@@ -5,12 +5,15 @@
 //   A2  heap init: the caller's arrays are copied into one working heap laid
 //       out [instance][cells], array a at offset off[a] (cell id
 //       = inst_local * cpi + off[a] + index, a u32 key for the sort).
-//   per interval k:
+//       (double-buffered: the next batch's inputs copy in on a second stream)
+//   per interval k, queued one interval ahead of the host:
 //     K1  interpret every live work-item until it suspends / exits / stops;
 //         log reads and final writes (interp.cu)
-//     K2/K3 onesweep sort of the log by cell (sort.cu)
-//     K4+K5 segmented detection + commit (detect.cu)
-//     A4  barrier bookkeeping / divergence (boundary.cu)
+//     F   write-set filter + the sort's digit histograms (filter.cu)
+//     K3  onesweep sort of the log by cell (sort.cu)
+//     K4+K5 segmented detection + commit, A4 tail: divergence check and the
+//         interval's verdict (detect.cu); rare paths (overflow re-runs,
+//         divergence lane scans, RW classification) on the host's word
 //   until no work-item is suspended at a barrier.
 // After all batches: K6 canonical report order, copy to the host buffer.
 #include <algorithm>
