@@ -148,6 +148,9 @@ __device__ __noinline__ uint32_t flush_warp_(const LogOut p, const uint64_t* rec
   return 0;
 }
 
+#ifndef INTERP_CONV  // 1: converged-warp steps skip the minimum pc (parity-green, measured 15% slower)
+#define INTERP_CONV 0
+#endif
 #ifndef INTERP_INDEP  // 1: no block barrier in the tile loop (per-warp chunks and stores); measured 30% slower
 #define INTERP_INDEP 0
 #endif
@@ -475,16 +478,36 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
     __syncwarp();
     Stage S{st_recs + (size_t)warp * SW, 0, SW};
 
+    // Converged mode (warp-uniform `conv`): every running lane of the warp is
+    // at pc `upc`, so the step needs no minimum and no pc comparison.  It is
+    // entered after a step whose running lanes all sat at the minimum (one
+    // vote), kept across every instruction that only advances or stops lanes,
+    // and left at BR / JMP (the next step takes the minimum again — that is
+    // also where a warp whose lanes all stopped notices it).
+    bool conv = false;
+    uint32_t upc = 0;
     for (;;) {
-      uint32_t mine = 0xFFFFFFFFu;
-#pragma unroll
-      for (int h = 0; h < H; h++)
-        if (running[h]) mine = min(mine, pc[h]);
-      const uint32_t minpc = __reduce_min_sync(FULL, mine);
-      if (minpc == 0xFFFFFFFFu) break;  // no lane of the warp is running (pcs are < 65536)
+      uint32_t minpc;
       bool ex[H];
+      if (INTERP_CONV && conv) {
+        minpc = upc;
 #pragma unroll
-      for (int h = 0; h < H; h++) ex[h] = running[h] && pc[h] == minpc;
+        for (int h = 0; h < H; h++) ex[h] = running[h];
+      } else {
+        uint32_t mine = 0xFFFFFFFFu;
+#pragma unroll
+        for (int h = 0; h < H; h++)
+          if (running[h]) mine = min(mine, pc[h]);
+        minpc = __reduce_min_sync(FULL, mine);
+        if (minpc == 0xFFFFFFFFu) break;  // no lane of the warp is running (pcs are < 65536)
+        bool all = true;
+#pragma unroll
+        for (int h = 0; h < H; h++) {
+          ex[h] = running[h] && pc[h] == minpc;
+          all = all && (ex[h] || !running[h]);
+        }
+        if (INTERP_CONV) conv = __all_sync(FULL, all);
+      }
       uint4 eh;
       uint2 et;
       if (CODE_SMEM) {
@@ -646,6 +669,13 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
           break;
         case RC_OP_BR: EACH({ pc[h] = lds32(RA(h)) != 0 ? (uint32_t)imm : et.y; }) break;
         case RC_OP_JMP: EACH({ pc[h] = (uint32_t)imm; }) break;
+      }
+      if (INTERP_CONV) {
+        // every executing lane advanced to minpc + 1 or stopped (BAR / EXIT
+        // stop all of them in converged mode: nothing is left to run)
+        if (op == RC_OP_BR || op == RC_OP_JMP) conv = false;
+        else if (conv && (op == RC_OP_BAR || op == RC_OP_EXIT)) break;
+        upc = minpc + 1;
       }
 #undef EACH
 #undef RA
