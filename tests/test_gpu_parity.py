@@ -271,6 +271,28 @@ def test_instance_offset_and_batches(rc):
         assert_parity(g, o, ins)
 
 
+def test_batches_host_io_shapes_and_workspace(rc):
+    """Several batches through host buffers (A2 double-buffered copy stream,
+    final heaps copied back per batch), with and without RW classification;
+    the same program re-run with other shapes (batch plan cache) and after
+    its device workspace was released."""
+    p = K.program(K.TREE_OFF_BY_ONE)
+    prog = rc.rc_load_program(p.bytecode)
+    for n, n_inst, mb in ((128, 37, 5), (256, 9, 2), (64, 50, 0), (128, 37, 4)):
+        ins = I.cfg3_inputs(0, n_inst, n)
+        for classify in (False, True):
+            g = rc.rc_run(prog, n, ins, max_batch_instances=mb, classify_rw=classify)
+            o = oracle.run(p.bytecode, n, ins, classify_rw=classify)
+            assert_parity(g, o, ins)
+        prog.release_workspace()
+    ins = I.cfg5_inputs(0, 5, 300)
+    p5 = K.program(K.STENCIL)
+    prog5 = rc.rc_load_program(p5.bytecode)
+    for mb in (1, 2, 0):
+        g = rc.rc_run(prog5, 300, ins, max_batch_instances=mb)
+        assert_parity(g, oracle.run(p5.bytecode, 300, ins), ins)
+
+
 def test_truncation(rc):
     ins = I.cfg3_inputs(0, 50, 64)
     p = K.program(K.TREE_OFF_BY_ONE)
