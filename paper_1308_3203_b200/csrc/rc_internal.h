@@ -211,7 +211,10 @@ struct SortWorkspace {
 #define SORT_THREADS_OPT 256
 #endif
 constexpr int SORT_THREADS = SORT_THREADS_OPT;  // >= 256 (one thread per digit for the per-digit steps)
-constexpr int SORT_ITEMS = 16;
+#ifndef SORT_ITEMS_OPT
+#define SORT_ITEMS_OPT 16
+#endif
+constexpr int SORT_ITEMS = SORT_ITEMS_OPT;
 constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;
 size_t sort_tiles(size_t n);
 
