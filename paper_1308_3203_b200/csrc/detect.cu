@@ -32,7 +32,8 @@ __device__ __forceinline__ uint32_t rec_cell(uint64_t r) { return (uint32_t)(r >
 __device__ __forceinline__ uint32_t rec_tid(uint64_t r) { return ((uint32_t)r >> 5) & (MAX_WG - 1); }
 __device__ __forceinline__ bool rec_w(uint64_t r) { return (r & 1) != 0; }
 __device__ __forceinline__ int32_t rec_val(const DetectParams& p, uint64_t r) {
-  return __ldg(p.wval + (size_t)(((uint32_t)r >> 1) & 0xF) * p.n_lanes + rec_tid(r));
+  // slot * n_lanes + lane < 16 * 2^27: 32-bit index arithmetic
+  return __ldg(p.wval + ((((uint32_t)r >> 1) & 0xF) * p.n_lanes + rec_tid(r)));
 }
 
 __device__ __forceinline__ void emit(const DetectParams& p, uint32_t cell, uint32_t t1, uint32_t t2, uint16_t kind,
@@ -211,14 +212,15 @@ __device__ __forceinline__ Seg seg_shfl(const Seg& a, int src) {
 __device__ __forceinline__ void detect_chunk(const DetectParams& p, uint64_t wg, uint32_t n_records) {
   const unsigned FULL = 0xFFFFFFFFu;
   const int lane = threadIdx.x & 31;
-  const uint64_t c0 = wg * DET_CHUNK;
-  const uint64_t c1 = min((uint64_t)n_records, c0 + DET_CHUNK);
+  // record indices are < 2^32 (n_records is): 32-bit index arithmetic
+  const uint32_t c0 = (uint32_t)wg * DET_CHUNK;
+  const uint32_t c1 = min(n_records, c0 + DET_CHUNK);
   // ---- prefetch the chunk
   uint64_t vr[DET_ROUNDS];
   int32_t wv[DET_ROUNDS];
 #pragma unroll
   for (int rd = 0; rd < (int)DET_ROUNDS; rd++) {
-    const uint64_t r = c0 + rd * 32 + lane;
+    const uint32_t r = c0 + rd * 32 + lane;
     vr[rd] = r < c1 ? __ldg(p.recs + r) : ~0ull;
   }
   const uint32_t key_before = c0 > 0 ? rec_cell(__ldg(p.recs + c0 - 1)) : 0xFFFFFFFFu;
@@ -228,14 +230,14 @@ __device__ __forceinline__ void detect_chunk(const DetectParams& p, uint64_t wg,
 
   const Seg ident{INF, 0u, 0u, 0, 0u};
   bool carry = false;       // an open segment started in an earlier round of this chunk
-  uint64_t carry_start = 0;
+  uint32_t carry_start = 0;
   Seg cs = ident;
   uint32_t last_key = key_before;  // key of the record before this round
 #pragma unroll
   for (int rd = 0; rd < (int)DET_ROUNDS; rd++) {
-    const uint64_t b = c0 + rd * 32;
+    const uint32_t b = c0 + rd * 32;
     if (b >= c1) break;  // warp-uniform
-    const uint64_t r = b + lane;
+    const uint32_t r = b + lane;
     const bool inb = r < c1;
     const uint64_t v = vr[rd];
     const uint32_t key = rec_cell(v);  // invalid lanes: 0xFFFFFFFF (cell ids are smaller)
