@@ -22,11 +22,6 @@ namespace {
 constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr int F_THREADS = 256, F_ITEMS = F_ITEMS_OPT;
 
-__device__ __forceinline__ unsigned lanemask_lt() {
-  unsigned m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
 }  // namespace
 
 __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p) {
@@ -41,21 +36,21 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
   if (p.ctr->log_overflow) return;  // the interval will be re-run
   // slots reserved past the buffer end only ever held sentinel padding (a real
   // record there sets log_overflow): clamp to the capacity
-  const uint64_t nr = min(p.ctr->stage_count, (unsigned long long)p.n_slots);
-  const uint64_t step = (uint64_t)gridDim.x * F_THREADS * F_ITEMS;
+  // (slot indices < n_slots < 2^32: 32-bit index arithmetic)
+  const uint32_t nr = (uint32_t)min(p.ctr->stage_count, (unsigned long long)p.n_slots);
+  const uint32_t step = gridDim.x * F_THREADS * F_ITEMS;
   uint32_t kept_w = 0;  // kept write records (profile: detect's value gathers and commits)
   __syncthreads();
-  for (uint64_t b0 = (uint64_t)blockIdx.x * F_THREADS * F_ITEMS; b0 < nr; b0 += step) {
+  for (uint32_t b0 = blockIdx.x * F_THREADS * F_ITEMS; b0 < nr; b0 = nr - b0 > step ? b0 + step : nr) {
     uint64_t rec[F_ITEMS];
     bool keep[F_ITEMS];
 #pragma unroll
     for (int j = 0; j < F_ITEMS; j++) {
-      const uint64_t i = b0 + (uint64_t)j * F_THREADS + t;
+      const uint32_t i = b0 + j * F_THREADS + t;
       rec[j] = i < nr ? __ldg(p.stage + i) : REC_SENTINEL;
     }
 #pragma unroll
     for (int j = 0; j < F_ITEMS; j++) {
-      const uint64_t i = b0 + (uint64_t)j * F_THREADS + t;
       keep[j] = rec[j] != REC_SENTINEL &&
                 (p.keep_all || (rec[j] & 1) || __ldg(p.wmap + (rec[j] >> REC_CELL_SHIFT)) == p.wtag);
     }
