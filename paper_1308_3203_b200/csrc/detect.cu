@@ -312,38 +312,41 @@ __device__ __forceinline__ void detect_chunk(const DetectParams& p, uint64_t wg,
 }
 
 // A4 fused as the tail of K4 (readings L9, L17): the
-// last block to finish checks, per instance, whether the work-items that
-// arrived in this interval reached more than one barrier node (K1 reduced the
-// min / max arrival node), resets the ranges, and takes the interval's
-// verdict: `abort` when the host must act before the next interval may run
-// (DevCounters::abort).
-__device__ __noinline__ void boundary_tail(const DetectParams& p) {
-  __shared__ bool last;
+// last WARP to finish (a grid-wide warp counter, no block barrier: warps of a
+// block finish independently) checks, per instance, whether the work-items
+// that arrived in this interval reached more than one barrier node (K1
+// reduced the min / max arrival node), resets the ranges, and takes the
+// interval's verdict: `abort` when the host must act before the next interval
+// may run (DevCounters::abort).  Called by converged full warps.
+__device__ __forceinline__ void boundary_tail(const DetectParams& p) {
   DevCounters* c = p.ctr;
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t done = 0;
+  if (lane == 0) {
     __threadfence();
-    last = atomicAdd(&c->bdone, 1u) == gridDim.x - 1;
+    done = atomicAdd(&c->bdone, 1u);
   }
-  __syncthreads();
-  if (!last) return;
+  done = __shfl_sync(0xFFFFFFFFu, done, 0);
+  if (done != ((gridDim.x * blockDim.x) >> 5) - 1) return;
   __threadfence();
   // an interval that will be re-run (its log or K1's reports overflowed)
   // leaves the divergence flags of the previous interval in place: the re-run
   // of K1 reads them (static write-set elision, InterpParams::inst_div)
   const volatile DevCounters* cv = c;
   const bool rerun = cv->log_overflow || cv->k1_reports > p.report_cap;
-  for (uint32_t inst = threadIdx.x; inst < p.n_inst; inst += blockDim.x) {
+  bool any_div = false;
+  for (uint32_t inst = lane; inst < p.n_inst; inst += 32) {
     const int32_t lo = p.node_min[inst], hi = p.node_max[inst];
     p.node_min[inst] = 0x7FFFFFFF;
     p.node_max[inst] = (int32_t)0x80000000;
     if (rerun) continue;
     const bool div = lo < hi;
     p.inst_flag[inst] = div;
-    if (div) c->diverged = 1;
+    any_div |= div;
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if (__any_sync(0xFFFFFFFFu, any_div) && lane == 0) c->diverged = 1;
+  __syncwarp();
+  if (lane == 0) {
     __threadfence();
     c->bdone = 0;
     const volatile DevCounters* v = c;
@@ -359,7 +362,7 @@ __device__ __noinline__ void boundary_tail(const DetectParams& p) {
 // interval's log overflowed or K1's reports overflowed: the host then re-runs
 // the interval from the saved lane state on an untouched heap.
 __global__ void __launch_bounds__(256, DET_MINB) detect_kernel(const DetectParams p) {
-  if (p.ctr->abort) return;  // speculative interval after one that needs the host (uniform)
+  if (p.ctr->abort) return;  // speculative interval after one that needs the host (grid-uniform)
   if (!(p.ctr->log_overflow || p.ctr->k1_reports > p.report_cap)) {
     const uint32_t n_records = (uint32_t)p.ctr->kept_count;
     const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -367,6 +370,7 @@ __global__ void __launch_bounds__(256, DET_MINB) detect_kernel(const DetectParam
          wg += warps)
       detect_chunk(p, wg, n_records);
   }
+  __syncwarp();
   if (p.with_boundary) boundary_tail(p);
 }
 

@@ -91,12 +91,12 @@ struct DevCounters {
   unsigned long long report_count;  // reports appended (whole run, rolled back on retry)
   unsigned long long lanes_final[8];
   // Speculation (runtime.cu): the host queues interval k+1 before it has seen
-  // interval k's counters.  A4's last block sets `abort` when interval k needs
+  // interval k's counters.  A4's last warp sets `abort` when interval k needs
   // the host (overflow, divergence, nothing left waiting); every kernel of an
   // interval returns at entry while it is set, so a speculative interval
   // leaves no trace.  The host clears it.  Never zeroed per interval.
   unsigned int abort;
-  unsigned int bdone;               // A4 blocks finished (last-block pattern; self-resetting)
+  unsigned int bdone;               // A4 blocks (K4 tail: warps) finished (last-one pattern; self-resetting)
 };
 
 // Parameters of the interval interpreter (K1), passed by value.
