@@ -244,6 +244,58 @@ RC_API int rc_release_workspace(rc_program* prog);
 
 #define RC_OVERLAY_CAP 16 /* distinct cells one work-item may write per interval */
 
+/* ---- interleaving explorer -------------------------
+ * Every interleaving of ONE barrier interval under the paper's global
+ * semantics: one work-item steps at a time on the shared
+ * heap with immediate visibility; the interval ends when no work-item is
+ * RUNNING (all suspended at a barrier P:218, exited, or stopped by ⊥ / ⊤ as
+ * readings L5 / L6).  The paper's race definition is
+ * non-determinism of the end states: n_differ > 0.  The explorer is a witness
+ * generator: `witness` is a schedule whose end heap differs from schedule 0's
+ * (always run the lowest runnable tid), as a choice sequence of tids.
+ *
+ * Schedules are numbered: index i decodes in mixed radix over the runnable
+ * work-items of each state (d = i mod r, i /= r, step the d-th runnable);
+ * an index is a schedule of its own when the quotient left at the end is 0,
+ * otherwise it repeats a lower one and is not counted.  `complete` = every
+ * schedule has an index in [0, index_end) (proved from max_product <=
+ * index_end, explore.cu); else call again with a larger index_end.
+ * RC_EXPLORE_REDUCED steps only the shared accesses (LD/ST) and runs the
+ * private instructions between them eagerly: the same terminal states (they
+ * commute with every other work-item's steps) and far fewer schedules.      */
+#define RC_EXPLORE_REDUCED 1u
+
+typedef struct {
+  uint64_t n_schedules; /* schedules (own indices) among [index_begin, index_end) */
+  uint64_t n_differ;    /* of them, end heap != schedule 0's end heap         */
+  uint64_t witness;     /* smallest such index, UINT64_MAX if none            */
+  uint64_t max_product; /* max radix product over the examined indices        */
+  uint64_t n_terminal;  /* rows written to `terminals` (<= cap)               */
+  uint32_t witness_len; /* choices in the witness schedule (may exceed max_len) */
+  uint32_t complete;    /* 1: index_begin == 0 and every schedule was examined */
+} rc_explore_result;
+
+/* Explore the interval of `prog` that starts in the given state, n work-items
+ * (1..32).  sizes: HOST, n_arrays element counts.  heap (all arrays
+ * concatenated, sum(sizes) int32), regs [n][n_regs] int32, pc [n] u32, status
+ * [n] u8 (0 RUNNING 1 WAITING 2 EXITED 3 PRUNED 4 OOB 5 ASSERT 6 DIV0 7 FUEL;
+ * only RUNNING work-items step): device or host pointers, borrowed, read
+ * once.  fuel: per work-item instruction budget for the interval (0 = 2^20;
+ * reading L17: the work-item whose budget is spent stops with status FUEL).
+ * terminals (DEVICE, nullable when cap == 0): receives up to `cap` end states,
+ * one row of sum(sizes) + n*(4+n_regs) int32 per counted schedule, in no
+ * particular order: the heap, then per work-item pc, status, 0, 0, registers.
+ * witness_sched (DEVICE, nullable when max_len == 0): the witness's first
+ * max_len choices (tids).  out (HOST) is always written.  Synchronises
+ * `cuda_stream` (cudaStream_t, NULL = legacy default) on the current device.
+ * RC_EINVAL for bad arguments, RC_ELIMIT when the state row exceeds 4096
+ * words, RC_ENOMEM / RC_ECUDA for device failures.                         */
+RC_API int rc_explore(const rc_program* prog, uint32_t n, const uint32_t* sizes, const int32_t* heap,
+               const int32_t* regs, const uint32_t* pc, const uint8_t* status, uint64_t fuel,
+               uint64_t index_begin, uint64_t index_end, uint32_t flags, int32_t* terminals,
+               uint64_t cap, uint32_t* witness_sched, uint32_t max_len, void* cuda_stream,
+               rc_explore_result* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,11 +1,11 @@
 """B200-native concrete SIMD race checker for the §3 kernel language of
 arXiv 1308.3203 (the data-parallel hot path of SURVEY.md §8).
 
-    from paper_1308_3203_b200 import rc_load_program, rc_run
+    from paper_1308_3203_b200 import rc_load_program, rc_run, rc_explore
 
 The compute path is librc.so (hand-written sm_100a CUDA behind the C ABI in
 include/rc.h); this package is its thin ctypes binding plus the multi-GPU
 report gather (gather.py).
 """
-from .rc import (KINDS, REPORT_DTYPE, Program, RCError, RunResult, lib, rc_last_error, rc_load_program,  # noqa: F401
-                 rc_run)
+from .rc import (KINDS, REPORT_DTYPE, ExploreResult, Program, RCError, RunResult, lib, rc_explore,  # noqa: F401
+                 rc_last_error, rc_load_program, rc_run)

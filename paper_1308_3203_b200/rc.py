@@ -60,6 +60,13 @@ class rc_options(C.Structure):
 
 assert C.sizeof(rc_report) == 32
 
+class rc_explore_result(C.Structure):
+    _fields_ = [("n_schedules", C.c_uint64), ("n_differ", C.c_uint64), ("witness", C.c_uint64),
+                ("max_product", C.c_uint64), ("n_terminal", C.c_uint64), ("witness_len", C.c_uint32),
+                ("complete", C.c_uint32)]
+
+
+RC_EXPLORE_REDUCED = 1
 _lib = None
 
 
@@ -91,6 +98,10 @@ def lib():
         L.rc_abi_version.restype = C.c_int
         L.rc_release_workspace.argtypes = [C.c_void_p]
         L.rc_release_workspace.restype = C.c_int
+        L.rc_explore.argtypes = [C.c_void_p, C.c_uint32, P(C.c_uint32), C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_void_p,
+                                 C.c_uint64, C.c_void_p, C.c_uint32, C.c_void_p, P(rc_explore_result)]
+        L.rc_explore.restype = C.c_int
         _lib = L
     return _lib
 
@@ -234,3 +245,55 @@ def rc_run(prog: Program, work_group_size: int, arrays: list, *, n_instances: in
     n = min(total.value, capacity)
     reps = out[:n].copy()
     return RunResult(reps, int(total.value), _stats_dict(st), finals, _profile_dict(prof) if profile else None)
+
+
+@dataclass
+class ExploreResult:
+    n_schedules: int
+    n_differ: int
+    witness: int | None          # schedule index whose end heap differs from schedule 0's
+    witness_sched: list          # its choices (tids), up to max_len
+    max_product: int
+    complete: bool
+    terminals: object            # CUDA int32 tensor [n_terminal, row_words] or None
+
+
+def rc_explore(prog: Program, work_group_size: int, heap, *, regs=None, pc=None, status=None, sizes=None,
+               fuel: int = 0, index_end: int = 1 << 20, index_begin: int = 0, reduced: bool = True,
+               cap: int = 0, max_len: int = 256, stream=None) -> ExploreResult:
+    """Every interleaving of one barrier interval (include/rc.h rc_explore).
+
+    heap: CUDA int32 tensor of all arrays concatenated; `sizes` their element
+    counts (default: one array holding the whole heap when the program has
+    one).  regs [n, n_regs] / pc [n] / status [n] CUDA tensors (default:
+    zeros = the kernel's start state, reading L18).
+    """
+    import torch  # plumbing only: device memory and streams
+
+    n = work_group_size
+    dev = heap.device
+    if sizes is None:
+        if prog.n_arrays != 1:
+            raise ValueError("sizes is required for programs with more than one array")
+        sizes = [heap.numel()]
+    sz = (C.c_uint32 * max(1, len(sizes)))(*sizes)
+    heap = heap.to(torch.int32).contiguous()
+    regs = torch.zeros((n, prog.n_regs), dtype=torch.int32, device=dev) if regs is None else regs.to(torch.int32).contiguous()
+    pc = torch.zeros(n, dtype=torch.int32, device=dev) if pc is None else pc.to(torch.int32).contiguous()
+    status = torch.zeros(n, dtype=torch.uint8, device=dev) if status is None else status.to(torch.uint8).contiguous()
+    row_words = int(sum(sizes)) + n * (4 + prog.n_regs)
+    terms = torch.empty((max(1, cap), row_words), dtype=torch.int32, device=dev)
+    wsched = torch.empty(max(1, max_len), dtype=torch.int32, device=dev)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    out = rc_explore_result()
+    code = lib().rc_explore(prog._h, n, sz, heap.data_ptr(), regs.data_ptr(), pc.data_ptr(), status.data_ptr(), fuel,
+                            index_begin, index_end, RC_EXPLORE_REDUCED if reduced else 0, terms.data_ptr(), cap,
+                            wsched.data_ptr(), max_len, C.c_void_p(stream.cuda_stream), C.byref(out))
+    if code != RC_OK:
+        raise RCError(code, rc_last_error())
+    wl = min(out.witness_len, max_len)
+    return ExploreResult(int(out.n_schedules), int(out.n_differ),
+                         None if out.witness == (1 << 64) - 1 else int(out.witness),
+                         wsched[:wl].cpu().tolist() if out.witness != (1 << 64) - 1 else [],
+                         int(out.max_product), bool(out.complete), terms[:out.n_terminal] if cap else None)
