@@ -21,6 +21,7 @@ namespace rc {
 namespace {
 constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr int F_THREADS = 256, F_ITEMS = F_ITEMS_OPT;
+static_assert(F_ITEMS % 2 == 0, "two records per 16-byte load");
 
 }  // namespace
 
@@ -28,7 +29,7 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
   __shared__ uint32_t bh[4 * 256];
   __shared__ uint32_t wcnt[F_THREADS / 32];
   __shared__ unsigned long long sbase;
-  __shared__ uint64_t sbuf[F_THREADS * F_ITEMS];
+  __shared__ uint64_t sbuf[F_THREADS * F_ITEMS + 8 * F_ITEMS];
   if (p.ctr->abort) return;  // speculative interval (DevCounters::abort)
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   for (int i = t; i < p.passes * 256; i += F_THREADS) bh[i] = 0;
@@ -42,12 +43,22 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
   uint32_t kept_w = 0;  // kept write records (profile: detect's value gathers and commits)
   __syncthreads();
   for (uint32_t b0 = blockIdx.x * F_THREADS * F_ITEMS; b0 < nr; b0 = nr - b0 > step ? b0 + step : nr) {
+    // F_ITEMS consecutive slots per thread (the block's slots in order), so
+    // the kept records keep the staging order and a thread's records are
+    // mostly consecutive cells: its digit counts go in runs
     uint64_t rec[F_ITEMS];
     bool keep[F_ITEMS];
+    const uint32_t i0 = b0 + (uint32_t)t * F_ITEMS;
+    if (i0 + F_ITEMS <= nr) {
 #pragma unroll
-    for (int j = 0; j < F_ITEMS; j++) {
-      const uint32_t i = b0 + j * F_THREADS + t;
-      rec[j] = i < nr ? __ldg(p.stage + i) : REC_SENTINEL;
+      for (int j = 0; j < F_ITEMS; j += 2) {
+        const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p.stage + i0 + j));
+        rec[j] = v.x;
+        rec[j + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < F_ITEMS; j++) rec[j] = i0 + j < nr ? __ldg(p.stage + i0 + j) : REC_SENTINEL;
     }
 #pragma unroll
     for (int j = 0; j < F_ITEMS; j++) {
@@ -60,6 +71,26 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
       mine += keep[j];
       kept_w += keep[j] && (rec[j] & 1);
     }
+    // digit histograms of the kept records: one shared add per run of equal digits
+    if (mine) {
+      for (int ps = 0; ps < p.passes; ps++) {
+        const int sh = REC_CELL_SHIFT + 8 * ps;
+        uint32_t cur = 0xFFFFFFFFu, run = 0;
+#pragma unroll
+        for (int j = 0; j < F_ITEMS; j++) {
+          if (!keep[j]) continue;
+          const uint32_t d = (uint32_t)(rec[j] >> sh) & 0xFF;
+          if (d == cur) {
+            run++;
+          } else {
+            if (run) atomicAdd(&bh[ps * 256 + cur], run);
+            cur = d;
+            run = 1;
+          }
+        }
+        atomicAdd(&bh[ps * 256 + cur], run);
+      }
+    }
     // block-exclusive offsets of this thread's kept records
     uint32_t x = mine;
 #pragma unroll
@@ -70,38 +101,37 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
     if (lane == 31) wcnt[w] = x;
     __syncthreads();
     uint32_t woff = 0, tot = 0;
+#pragma unroll
     for (int i = 0; i < F_THREADS / 32; i++) {
-      if (i < w) woff += wcnt[i];
-      tot += wcnt[i];
+      const uint32_t c = wcnt[i];
+      woff += i < w ? c : 0u;
+      tot += c;
     }
     if (t == 0) sbase = tot ? atomicAdd(&p.ctr->kept_count, (unsigned long long)tot) : 0ull;
-    // block-local compaction in shared memory, then coalesced stores
+    // block-local compaction in shared memory, then coalesced stores, F_ITEMS-
+    // way interleaved: output F_ITEMS*m + r <- kept record r*Q + m (Q = tot /
+    // F_ITEMS), so records F_THREADS slots apart — in lane-ordered staging,
+    // cells a multiple of 256 apart: the same low digit — sit next to each
+    // other, which the onesweep ranking's warp matching merges.  Any order is
+    // correct (a stable sort by cell; detect reduces each cell's segment
+    // order-independently).  Group r lives at r*(Q+8) in sbuf: the 8-word skew
+    // keeps a warp's interleaved reads at two wavefronts.
+    const uint32_t Q = tot / F_ITEMS, QF = Q * F_ITEMS;
     uint32_t pos = woff + x - mine;
 #pragma unroll
     for (int j = 0; j < F_ITEMS; j++)
-      if (keep[j]) sbuf[pos++] = rec[j];
+      if (keep[j]) {
+        uint32_t r = 0;
+#pragma unroll
+        for (int g = 1; g <= F_ITEMS; g++) r += pos >= (uint32_t)g * Q;
+        sbuf[pos + 8 * r] = rec[j];
+        pos++;
+      }
     __syncthreads();
     const unsigned long long base = sbase;
-    for (uint32_t i0 = 0; i0 < tot; i0 += F_THREADS) {  // block-uniform trip count
-      const uint32_t i = i0 + t;
-      const bool v = i < tot;
-      const uint64_t r = v ? sbuf[i] : 0;
-      if (v) p.out[base + i] = r;
-      // digit histograms (runs: one add when the warp agrees)
-      const unsigned mk = __ballot_sync(FULL, v);
-      if (!mk) continue;
-      const int first = __ffs(mk) - 1;
-      for (int ps = 0; ps < p.passes; ps++) {
-        const uint32_t d = (uint32_t)(r >> (REC_CELL_SHIFT + 8 * ps)) & 0xFF;
-        const uint32_t d0 = __shfl_sync(FULL, d, first);
-        if (__all_sync(FULL, !v || d == d0)) {
-          if (lane == first) atomicAdd(&bh[ps * 256 + d0], (uint32_t)__popc(mk));
-        } else if (v) {
-          atomicAdd(&bh[ps * 256 + d], 1u);
-        }
-      }
-    }
-    __syncthreads();  // wcnt / sbase reuse
+    for (uint32_t i = t; i < tot; i += F_THREADS)
+      p.out[base + i] = sbuf[i < QF ? (i % F_ITEMS) * (Q + 8) + i / F_ITEMS : i + 8 * F_ITEMS];
+    __syncthreads();  // wcnt / sbase / sbuf reuse
   }
   for (int i = t; i < p.passes * 256; i += F_THREADS)
     if (bh[i]) atomicAdd(&p.hist[i], bh[i]);
