@@ -104,3 +104,41 @@ def test_run_without_gpu_fails_loudly(rc):
     with pytest.raises(rc.RCError) as ei:
         rc.rc_run(prog, 4, [np.zeros((1, 4), np.int32)])
     assert ei.value.code in (3, 1)  # RC_ECUDA (no device)
+
+
+def test_explore_result_layout(rc):
+    from paper_1308_3203_b200 import rc as b
+    assert ctypes.sizeof(b.rc_explore_result) == 6 * 8
+    src = open(os.path.join(ROOT, "include", "rc.h")).read()
+    assert re.search(r"#define RC_EXPLORE_REDUCED 1u", src) and b.RC_EXPLORE_REDUCED == 1
+
+
+def test_explore_argument_errors_without_gpu(rc):
+    """rc_explore validates its arguments before any CUDA call: each bad
+    argument gives RC_EINVAL / RC_ELIMIT with a message (include/rc.h)."""
+    from paper_1308_3203_b200 import rc as b
+    L = rc.lib()
+    p = rc.rc_load_program(assemble(K.BENIGN["K_inc"]).bytecode)  # 2 arrays
+    sizes = (ctypes.c_uint32 * 2)(1, 4)
+    buf = (ctypes.c_int32 * 4096)()
+    ptr = ctypes.cast(buf, ctypes.c_void_p)
+    out = b.rc_explore_result()
+
+    def call(prog=p._h, n=4, sz=sizes, heap=ptr, regs=ptr, pc=ptr, st=ptr, begin=0, end=16, flags=1,
+             term=None, cap=0, ws=None, max_len=0):
+        return L.rc_explore(prog, n, sz, heap, regs, pc, st, 0, begin, end, flags, term, cap, ws, max_len, None,
+                            ctypes.byref(out))
+
+    EINVAL, ELIMIT = 1, 5
+    assert call(prog=None) == EINVAL
+    assert call(n=0) == EINVAL and "work_group_size" in rc.rc_last_error()
+    assert call(n=33) == EINVAL
+    assert call(sz=None) == EINVAL and "sizes" in rc.rc_last_error()
+    assert call(pc=None) == EINVAL and "lane state" in rc.rc_last_error()
+    assert call(begin=5, end=4) == EINVAL
+    assert call(flags=2) == EINVAL and "flags" in rc.rc_last_error()
+    assert call(cap=8) == EINVAL and "terminals" in rc.rc_last_error()
+    assert call(max_len=8) == EINVAL and "witness_sched" in rc.rc_last_error()
+    big = (ctypes.c_uint32 * 2)(4000, 100)
+    assert call(sz=big) == ELIMIT and "state row" in rc.rc_last_error()
+    assert out.n_schedules == 0 and out.complete == 0  # `out` is cleared on every call
