@@ -288,6 +288,8 @@ typedef struct {
  * witness_sched (DEVICE, nullable when max_len == 0): the witness's first
  * max_len choices (tids).  out (HOST) is always written.  Synchronises
  * `cuda_stream` (cudaStream_t, NULL = legacy default) on the current device.
+ * Device buffers are cached on `prog` (freed by rc_release_workspace /
+ * rc_free_program); like rc_run, not re-entrant on one program object.
  * RC_EINVAL for bad arguments, RC_ELIMIT when the state row exceeds 4096
  * words, RC_ENOMEM / RC_ECUDA for device failures.                         */
 RC_API int rc_explore(const rc_program* prog, uint32_t n, const uint32_t* sizes, const int32_t* heap,

@@ -25,13 +25,14 @@
 // n_schedules equals the number of interleavings of the paper's semantics.
 //
 // Per-thread state (heap + lanes, the oracle enumerator's row layout: heap
-// cells, then per work-item pc, status, 0, 0, registers) lives in a global
-// scratch slice, word-interleaved across threads ([word][thread]) so the
-// lock-step words (pc, status, registers) coalesce; it stays in L1/L2 for the
-// small problems this is for.
+// cells, then per work-item pc, status, 0, 0, registers) is word-interleaved
+// across threads ([word][thread]: conflict-free / coalesced) in shared memory
+// when a block's rows fit in 96 KB, else in a global scratch slice.
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "rc_internal.h"
@@ -56,7 +57,8 @@ struct ExploreParams {
   uint64_t fuel, index_begin, index_end;
   bool reduced;
   int32_t* scratch;          // [row_words][G]
-  uint64_t G;                // threads in the grid (scratch stride)
+  uint64_t G;                // threads in the grid (index stride)
+  uint64_t scr_stride;       // word stride of the global scratch rows (G, or 1 when the grid uses shared memory)
   unsigned long long* ctr;   // [0] n_schedules [1] n_differ [2] witness [3] max_product [4] n_terminal
   int32_t* terminals;        // [cap][row_words] or null
   uint64_t cap;
@@ -124,14 +126,14 @@ __device__ void step(const ExploreParams& p, int32_t* H, const Lane& L, uint32_t
       const int32_t idx = L.r(I.c);
       const uint32_t size = p.arr_off[I.b + 1] - p.arr_off[I.b];
       if (idx < 0 || (uint32_t)idx >= size) { L.st() = X_OOB; return; }
-      L.r(I.a) = H[(uint64_t)(p.arr_off[I.b] + (uint32_t)idx) * p.G];
+      L.r(I.a) = H[(uint64_t)(p.arr_off[I.b] + (uint32_t)idx) * L.G];
       break;
     }
     case RC_OP_ST: {
       const int32_t idx = L.r(I.b);
       const uint32_t size = p.arr_off[I.a + 1] - p.arr_off[I.a];
       if (idx < 0 || (uint32_t)idx >= size) { L.st() = X_OOB; return; }
-      H[(uint64_t)(p.arr_off[I.a] + (uint32_t)idx) * p.G] = L.r(I.c);
+      H[(uint64_t)(p.arr_off[I.a] + (uint32_t)idx) * L.G] = L.r(I.c);
       break;
     }
     case RC_OP_BAR: L.st() = X_WAITING; break;            // suspended τ⊡σ, pc past the BAR
@@ -160,13 +162,13 @@ __device__ __forceinline__ unsigned long long sat_mul(unsigned long long a, unsi
 // Replay schedule `idx` in the thread's scratch slice.  Returns the quotient
 // left over (0 = idx is this schedule's own index) and the radix product.
 // `choices` (nullable) receives the chosen tids.
-__device__ unsigned long long replay(const ExploreParams& p, int32_t* S, unsigned long long idx,
+__device__ unsigned long long replay(const ExploreParams& p, int32_t* S, uint64_t sst, unsigned long long idx,
                                      unsigned long long& prod, uint32_t* choices, uint32_t max_len,
                                      uint32_t& len) {
-  for (uint32_t wd = 0; wd < p.row_words; wd++) S[(uint64_t)wd * p.G] = p.start[wd];
+  for (uint32_t wd = 0; wd < p.row_words; wd++) S[(uint64_t)wd * sst] = p.start[wd];
   uint64_t steps[X_MAX_N];
   const uint32_t LW = 4 + p.n_regs;
-  auto lane = [&](uint32_t t) { return Lane{S + (uint64_t)(p.cells + t * LW) * p.G, p.G}; };
+  auto lane = [&](uint32_t t) { return Lane{S + (uint64_t)(p.cells + t * LW) * sst, sst}; };
   for (uint32_t t = 0; t < p.n; t++) steps[t] = 0;
   if (p.reduced)
     for (uint32_t t = 0; t < p.n; t++) run_private(p, S, lane(t), t, steps[t]);
@@ -196,23 +198,28 @@ __device__ unsigned long long replay(const ExploreParams& p, int32_t* S, unsigne
 __global__ void explore_ref_kernel(ExploreParams p, int32_t* ref) {
   unsigned long long prod;
   uint32_t len;
-  replay(p, p.scratch, 0, prod, nullptr, 0, len);
-  for (uint32_t c = 0; c < p.cells; c++) ref[c] = p.scratch[(uint64_t)c * p.G];
+  replay(p, p.scratch, p.scr_stride, 0, prod, nullptr, 0, len);
+  for (uint32_t c = 0; c < p.cells; c++) ref[c] = p.scratch[(uint64_t)c * p.scr_stride];
 }
 
+// SMEM: the state rows live in shared memory ([word][thread] per block),
+// else in the global scratch ([word][grid thread]).
+template <bool SMEM>
 __global__ void __launch_bounds__(128) explore_kernel(ExploreParams p) {
+  extern __shared__ int32_t s_rows[];
   const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int32_t* S = p.scratch + g;
+  int32_t* S = SMEM ? s_rows + threadIdx.x : p.scratch + g;
+  const uint64_t sst = SMEM ? blockDim.x : p.G;
   unsigned long long n_sched = 0, n_diff = 0, wit = ~0ull, maxp = 0;
   for (uint64_t i = p.index_begin + g; i < p.index_end; i += p.G) {
     unsigned long long prod;
     uint32_t len;
-    const unsigned long long rem = replay(p, S, i, prod, nullptr, 0, len);
+    const unsigned long long rem = replay(p, S, sst, i, prod, nullptr, 0, len);
     maxp = prod > maxp ? prod : maxp;
     if (rem) continue;  // a duplicate of schedule i mod P(s)
     n_sched++;
     bool differ = false;
-    for (uint32_t c = 0; c < p.cells; c++) differ |= S[(uint64_t)c * p.G] != p.ref_heap[c];
+    for (uint32_t c = 0; c < p.cells; c++) differ |= S[(uint64_t)c * sst] != p.ref_heap[c];
     if (differ) {
       n_diff++;
       wit = i < wit ? i : wit;
@@ -221,7 +228,7 @@ __global__ void __launch_bounds__(128) explore_kernel(ExploreParams p) {
       const unsigned long long slot = atomicAdd(&p.ctr[4], 1ull);
       if (slot < p.cap) {
         int32_t* row = p.terminals + slot * p.row_words;
-        for (uint32_t wd = 0; wd < p.row_words; wd++) row[wd] = S[(uint64_t)wd * p.G];
+        for (uint32_t wd = 0; wd < p.row_words; wd++) row[wd] = S[(uint64_t)wd * sst];
         for (uint32_t t = 0; t < p.n; t++) {  // steps are not observable (enumerator rows zero them)
           row[p.cells + t * (4 + p.n_regs) + 2] = 0;
           row[p.cells + t * (4 + p.n_regs) + 3] = 0;
@@ -252,19 +259,20 @@ __global__ void explore_witness_kernel(ExploreParams p) {
   if (w == ~0ull) { *p.wlen = 0; return; }
   unsigned long long prod;
   uint32_t len;
-  replay(p, p.scratch, w, prod, p.wsched, p.max_len, len);
+  replay(p, p.scratch, p.scr_stride, w, prod, p.wsched, p.max_len, len);
   *p.wlen = len;
 }
 
-struct Dev {  // per-call device allocations, freed on every exit path
-  void* ptr[4] = {nullptr, nullptr, nullptr, nullptr};
-  ~Dev() {
-    for (void* q : ptr)
-      if (q) cudaFree(q);
-  }
-};
-
 }  // namespace
+
+void ExploreCache::release() {
+  for (int i = 0; i < 3; i++) {
+    if (p[i]) cudaFree(p[i]);
+    p[i] = nullptr;
+    cap[i] = 0;
+  }
+  device = -1;
+}
 }  // namespace rc
 
 using namespace rc;
@@ -325,16 +333,46 @@ extern "C" int rc_explore(const rc_program* prog, uint32_t n, const uint32_t* si
   while (blocks > 1 && blocks * 128 / 2 >= todo) blocks /= 2;
   const uint64_t G = blocks * 128;
 
-  Dev d;
+  // device buffers cached on the program (grow-only; rc_release_workspace /
+  // rc_free_program free them); the program is not re-entrant (include/rc.h)
+  rc_program* P = const_cast<rc_program*>(prog);
+  std::lock_guard<std::mutex> lk(P->mu);
+  if (P->xc.device != dev) {
+    if (P->xc.device >= 0) {
+      int cur = dev;
+      cudaSetDevice(P->xc.device);
+      P->xc.release();
+      cudaSetDevice(cur);
+    }
+    P->xc.device = dev;
+  }
+  auto buf = [&](int i, size_t bytes) -> void* {
+    if (P->xc.cap[i] < bytes) {
+      if (P->xc.p[i]) cudaFree(P->xc.p[i]);
+      P->xc.p[i] = nullptr;
+      P->xc.cap[i] = 0;
+      if (cudaMalloc(&P->xc.p[i], bytes) != cudaSuccess) return nullptr;
+      P->xc.cap[i] = bytes;
+    }
+    return P->xc.p[i];
+  };
   const size_t row_b = row_words * 4;
-  if (cudaMalloc(&d.ptr[0], row_b + cells * 4 + (prog->n_arrays + 2) * 4 + prog->n_instr * sizeof(Ins)) != cudaSuccess ||
-      cudaMalloc(&d.ptr[1], row_words * G * 4) != cudaSuccess || cudaMalloc(&d.ptr[2], 64) != cudaSuccess)
-    return fail(RC_ENOMEM, "rc_explore: device allocation failed");
-  int32_t* start = static_cast<int32_t*>(d.ptr[0]);
+  // state rows in shared memory when a block's rows fit (small problems: all
+  // the explorer is for), else in the L1/L2-cached global scratch
+  const size_t smem = row_b * 128;
+  const bool use_smem = smem <= 96 * 1024 && !getenv("RC_DEBUG_EXPLORE_GLOBAL") &&  // (test hook)
+                        cudaFuncSetAttribute(explore_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem) == cudaSuccess;
+  const uint64_t scr_stride = use_smem ? 1 : G;
+  void* b0 = buf(0, row_b + cells * 4 + (prog->n_arrays + 2) * 4 + prog->n_instr * sizeof(Ins));
+  void* b1 = buf(1, row_words * scr_stride * 4);
+  void* b2 = buf(2, 64);
+  if (!b0 || !b1 || !b2) return fail(RC_ENOMEM, "rc_explore: device allocation failed");
+  int32_t* start = static_cast<int32_t*>(b0);
   int32_t* ref = start + row_words;
   uint32_t* d_off = reinterpret_cast<uint32_t*>(ref + cells);
   Ins* d_code = reinterpret_cast<Ins*>(d_off + prog->n_arrays + 2);
-  unsigned long long* ctr = static_cast<unsigned long long*>(d.ptr[2]);
+  unsigned long long* ctr = static_cast<unsigned long long*>(b2);
   uint32_t* d_wlen = reinterpret_cast<uint32_t*>(ctr + 5);
   const unsigned long long init[6] = {0, 0, ~0ull, 0, 0, 0};
   ok &= cudaMemcpyAsync(start, row.data(), row_b, cudaMemcpyHostToDevice, s) == cudaSuccess;
@@ -357,8 +395,9 @@ extern "C" int rc_explore(const rc_program* prog, uint32_t n, const uint32_t* si
   p.index_begin = index_begin;
   p.index_end = index_end;
   p.reduced = (flags & RC_EXPLORE_REDUCED) != 0;
-  p.scratch = static_cast<int32_t*>(d.ptr[1]);
+  p.scratch = static_cast<int32_t*>(b1);
   p.G = G;
+  p.scr_stride = scr_stride;
   p.ctr = ctr;
   p.terminals = cap ? terminals : nullptr;
   p.cap = cap;
@@ -366,7 +405,8 @@ extern "C" int rc_explore(const rc_program* prog, uint32_t n, const uint32_t* si
   p.max_len = max_len;
   p.wlen = d_wlen;
   explore_ref_kernel<<<1, 1, 0, s>>>(p, ref);
-  if (todo) explore_kernel<<<(unsigned)blocks, 128, 0, s>>>(p);
+  if (todo && use_smem) explore_kernel<true><<<(unsigned)blocks, 128, smem, s>>>(p);
+  else if (todo) explore_kernel<false><<<(unsigned)blocks, 128, 0, s>>>(p);
   explore_witness_kernel<<<1, 1, 0, s>>>(p);
   g_launches += todo ? 3 : 2;
   unsigned long long h[6];

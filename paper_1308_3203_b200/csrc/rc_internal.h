@@ -290,6 +290,15 @@ cudaError_t finalize_reports(rc_report* reports, uint64_t n, rc_report* scratch,
 
 // opaque program object (include/rc.h)
 struct rc_workspace;
+namespace rc {
+struct ExploreCache {  // rc_explore's device buffers: grown on demand, freed with the program
+  int device = -1;
+  void* p[3] = {nullptr, nullptr, nullptr};
+  size_t cap[3] = {0, 0, 0};
+  void release();  // explore.cu (on the current device)
+};
+}  // namespace rc
+
 struct rc_program {
   uint32_t n_regs = 0, n_arrays = 0, n_instr = 0;
   std::vector<rc::Ins> code;
@@ -303,4 +312,5 @@ struct rc_program {
   int64_t instr_bound = -1;        // max instructions per work-item per interval (-1 unbounded)
   std::mutex mu;
   rc_workspace* ws = nullptr;
+  rc::ExploreCache xc;
 };

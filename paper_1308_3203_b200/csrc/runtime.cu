@@ -214,11 +214,17 @@ extern "C" {
 
 void rc_free_program(rc_program* P) {
   if (!P) return;
-  if (P->ws) {
+  if (P->ws || P->xc.device >= 0) {
     int prev = -1;
     cudaGetDevice(&prev);
-    if (P->ws->device >= 0) cudaSetDevice(P->ws->device);
-    delete P->ws;
+    if (P->ws) {
+      if (P->ws->device >= 0) cudaSetDevice(P->ws->device);
+      delete P->ws;
+    }
+    if (P->xc.device >= 0) {
+      cudaSetDevice(P->xc.device);
+      P->xc.release();
+    }
     if (prev >= 0) cudaSetDevice(prev);
   }
   delete P;
@@ -231,6 +237,10 @@ int rc_release_workspace(rc_program* P) {
     DeviceGuard g(P->ws->device);
     delete P->ws;
     P->ws = nullptr;
+  }
+  if (P->xc.device >= 0) {
+    DeviceGuard g(P->xc.device);
+    P->xc.release();
   }
   return RC_OK;
 }

@@ -171,3 +171,16 @@ def test_explore_random_tiny_kernels(oracle_lib):
         e = check_interval(oracle_lib, p, n, [3, 3], heap, regs, pc, st, full=(n == 2), fuel=64)
         racy += len(e.heaps) > 1
     assert racy > 10  # the family does produce non-deterministic intervals
+
+
+def test_explore_global_scratch_path(oracle_lib, monkeypatch):
+    """State rows in the global scratch instead of shared memory (the path of
+    large rows; forced by a test hook): the same end states and counts."""
+    monkeypatch.setenv("RC_DEBUG_EXPLORE_GLOBAL", "1")
+    p = K.program(K.FIG2)
+    ins = [np.array([7, 9, 5], np.int32), np.array([42], np.int32)]
+    reached, heap, regs, pc, st = oracle_lib.state_at(p.bytecode, 2, ins, 1)
+    check_interval(oracle_lib, p, 2, [3, 1], heap, regs, pc, st, full=True)
+    p = K.program(K.BENIGN["K_inc"])
+    reached, heap, regs, pc, st = oracle_lib.state_at(p.bytecode, 4, [np.array([40], np.int32), np.zeros(4, np.int32)], 0)
+    check_interval(oracle_lib, p, 4, [1, 4], heap, regs, pc, st, full=False)

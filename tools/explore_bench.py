@@ -5,7 +5,8 @@ workload).
 Workloads (seeded): K_inc (App. A.3 lost update, 2 accesses per work-item)
 at n = 5 / 6 and guarded Fig. 1 interval 1 at n = 4, shared-access
 scheduling (RC_EXPLORE_REDUCED).  GPU time = CUDA events around one complete
-rc_explore call (after one warm-up call); the first case schedules every
+rc_explore call, best of 5 (after one warm-up call; the call includes its
+device allocations and the start-state upload); the first case schedules every
 instruction, as the un-memoised oracle walk does, the others only the
 shared accesses.  The oracle legs: the memoised
 enumerator over the whole interval, and the un-memoised walk (every schedule
@@ -46,7 +47,8 @@ def case(name, p, n, ins, k, reduced=True):
     d = dict(heap=torch.from_numpy(heap.astype(np.int32)).cuda(), regs=torch.from_numpy(regs).cuda(),
              pc=torch.from_numpy(pc.astype(np.int32)).cuda(), st=torch.from_numpy(st).cuda())
     explore_all(prog, n, sizes, d["heap"], d["regs"], d["pc"], d["st"], reduced)  # warm-up
-    r, end, ms = explore_all(prog, n, sizes, d["heap"], d["regs"], d["pc"], d["st"], reduced)
+    runs = [explore_all(prog, n, sizes, d["heap"], d["regs"], d["pc"], d["st"], reduced) for _ in range(5)]
+    r, end, ms = min(runs, key=lambda x: x[2])  # best of 5 complete calls
     t0 = time.perf_counter()
     e = orc.enumerate_interval(p.bytecode, n, sizes, heap, regs, pc, st)
     t_memo = time.perf_counter() - t0
