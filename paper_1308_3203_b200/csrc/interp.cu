@@ -888,6 +888,9 @@ __global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_B
     if (b_staged) atomicAdd(&p.ctr->staged_recs, b_staged);
   }
   // ---- block flush: sentinels in the last chunk's tail, statistics, flags
+  // (the barrier: other warps may still be padding the last tile's abandoned
+  // chunk from wbase[W] / wcnt[W])
+  __syncthreads();
   if (t == 0) {
     wbase[W] = c_base + c_used;
     wcnt[W] = c_cap - c_used;

@@ -1,5 +1,6 @@
 """Workload for tools/sanitize.sh: stencil (2 instances, n = 70000) and the
-classified tree reduction (300 instances, n = 1024) through the C ABI."""
+classified tree reduction (300 instances, n = 1024) through the C ABI, and
+the interleaving explorer on K_inc (n = 4, both scheduling modes)."""
 import sys, os; sys.path.insert(0, os.getcwd())
 import numpy as np, torch
 from paper_1308_3203_b200 import rc_load_program, rc_run
@@ -12,3 +13,12 @@ p = K.program(K.TREE_OFF_BY_ONE); prog = rc_load_program(p.bytecode)
 ins = I.cfg3_inputs(0, 300, 1024)
 r = rc_run(prog, 1024, [torch.from_numpy(x).cuda() for x in ins], classify_rw=True)
 print("tree ok", len(r.reports))
+from oracle import oracle as orc  # noqa: E402  (test infrastructure: the explorer's start state)
+from paper_1308_3203_b200 import rc_explore  # noqa: E402
+p = K.program(K.BENIGN["K_inc"]); prog = rc_load_program(p.bytecode)
+_, heap, regs, pc, st = orc.state_at(p.bytecode, 4, [np.array([40], np.int32), np.zeros(4, np.int32)], 0)
+args = dict(regs=torch.from_numpy(regs).cuda(), pc=torch.from_numpy(pc.astype(np.int32)).cuda(),
+            status=torch.from_numpy(st).cuda(), sizes=[1, 4], index_end=1 << 12, cap=64, max_len=16)
+for red in (True, False):
+    r = rc_explore(prog, 4, torch.from_numpy(heap.astype(np.int32)).cuda(), reduced=red, **args)
+    print("explore ok", r.n_schedules, r.n_differ)
