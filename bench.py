@@ -124,6 +124,40 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def explorer_line(dev):
+    """SURVEY.md §8(f) row 2, measured beside the main path (rank 0): every
+    interleaving of interval 0 of App. A.3's K_inc (lost update) at n = 6 with
+    shared-access scheduling — 7 484 400 schedules — through rc_explore.  The
+    start state needs no oracle: A[0] = 40, zero registers, pc 0, all running.
+    Best of 3 complete calls, CUDA events on the calling stream."""
+    import torch
+
+    from paper_1308_3203_b200 import rc_explore, rc_load_program
+    from workloads import kernels as K
+    n = 6
+    prog = rc_load_program(K.program(K.BENIGN["K_inc"]).bytecode)
+    heap = torch.zeros(1 + n, dtype=torch.int32, device=dev)
+    heap[0] = 40
+    regs = torch.zeros((n, prog.n_regs), dtype=torch.int32, device=dev)
+    pc = torch.zeros(n, dtype=torch.int32, device=dev)
+    st = torch.zeros(n, dtype=torch.uint8, device=dev)
+    end = 33592320  # the largest radix product of this interval: one call is complete (asserted)
+    times, r = [], None
+    for it in range(4):  # the first call allocates the cached buffers (untimed)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = rc_explore(prog, n, heap, regs=regs, pc=pc, status=st, sizes=[1, n], index_end=end, reduced=True)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        if it:
+            times.append(e0.elapsed_time(e1))
+    best = min(times)
+    assert r.complete and r.n_schedules == 7484400  # 12! / 2^6 interleavings of 6 x (LD, ST)
+    return {"workload": "K_inc (App. A.3) n=6, interval 0, shared-access scheduling", "schedules": r.n_schedules,
+            "indices": end, "schedules_differing_from_schedule_0": r.n_differ, "ms": best,
+            "schedules_per_s": r.n_schedules / (best / 1e3), "bound": "alu (issue; profiles/r01_explore_ncu_prof.txt)"}
+
+
 def cpu_cores():
     return len(os.sched_getaffinity(0))
 
@@ -180,6 +214,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--no-explorer", action="store_true", help="skip the rc_explore line (SURVEY §8(f) row 2)")
     ap.add_argument("--instances", type=int, default=0, help="override instances per GPU (debug)")
     ap.add_argument("--classify-rw", action="store_true",
                     help="RW value classification (RC_OPT_CLASSIFY_RW, SURVEY §8(f) row 1)")
@@ -378,6 +413,7 @@ def main():
                "sample": f"first {sample} instances of the workload ({n} work-items each), "
                          f"{cores} threads over instances, {dt:.1f} s"}
 
+    explorer = None if args.no_explorer else explorer_line(dev)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
@@ -391,7 +427,7 @@ def main():
             "interpreter": {"bytecode_instr_per_s": instrs / args.steps / (ms_step / 1000),
                             "bytecode_instr_per_step": instrs / args.steps,
                             "bound": "issue (ALU/LSU pipes; ncu sm__inst_executed.avg.per_cycle_active in profiles/)"},
-            "clocks": clocks, "kernels": kernels}
+            "clocks": clocks, "kernels": kernels, "explorer": explorer}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
