@@ -292,7 +292,7 @@ void interp_phase_io(unsigned long long* out, bool reset) {
 // parallelism of the warp.
 // ALT: the RW-classification re-run (reads of alt_mask cells see alt_heap).
 template <bool CODE_SMEM, bool FUEL, int H, bool ALT>
-__global__ void __launch_bounds__(256, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_BLOCKS_H)
+__global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_BLOCKS_H)
     interp_kernel(const __grid_constant__ InterpParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (p.ctr->abort) return;  // speculative interval (DevCounters::abort)
