@@ -26,6 +26,11 @@ def _newer(target: str, deps: list[str]) -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    # a change of flags (e.g. RC_EXTRA_NVCC_FLAGS of an A/B run) rebuilds everything
+    stamp = os.path.join(BUILD, "flags.txt")
+    want = " ".join([NVCC, *ARCH, *FLAGS])
+    if not os.path.exists(stamp) or open(stamp).read() != want:
+        force = True
     headers = [os.path.join(CSRC, "rc_internal.h"), os.path.join(ROOT, "include", "rc.h")]
     objs, jobs = [], []
     for src in SOURCES:
@@ -50,6 +55,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 print(err)
     if force or jobs or _newer(LIB, objs):
         run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt", "-lpthread", "-ldl"])
+    with open(stamp, "w") as f:
+        f.write(want)
     return LIB
 
 
