@@ -31,6 +31,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -329,7 +330,21 @@ extern "C" int rc_explore(const rc_program* prog, uint32_t n, const uint32_t* si
   if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
     return fail(RC_ECUDA, "rc_explore: no CUDA device");
   const uint64_t todo = index_end - index_begin;
-  uint64_t blocks = (uint64_t)nsm * 8;  // 8 x 128 threads per SM: latency of the dependent heap/lane loads
+  const size_t row_b = row_words * 4;
+  // state rows in shared memory when a block's rows fit (small problems: all
+  // the explorer is for), else in the L1/L2-cached global scratch
+  const size_t smem = row_b * 128;
+  const bool use_smem = smem <= 96 * 1024 && !getenv("RC_DEBUG_EXPLORE_GLOBAL") &&  // (test hook)
+                        cudaFuncSetAttribute(explore_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem) == cudaSuccess;
+  // resident blocks per SM (latency of the dependent state loads): as many as
+  // fit, up to 16 x 128 threads
+  int per_sm = 8;
+  if (use_smem && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, explore_kernel<true>, 128, smem) != cudaSuccess)
+    per_sm = 8;
+  if (getenv("RC_EXPLORE_BPS")) per_sm = atoi(getenv("RC_EXPLORE_BPS"));  // (A/B knob)
+  per_sm = std::max(1, std::min(per_sm, 16));
+  uint64_t blocks = (uint64_t)nsm * per_sm;
   while (blocks > 1 && blocks * 128 / 2 >= todo) blocks /= 2;
   const uint64_t G = blocks * 128;
 
@@ -356,13 +371,6 @@ extern "C" int rc_explore(const rc_program* prog, uint32_t n, const uint32_t* si
     }
     return P->xc.p[i];
   };
-  const size_t row_b = row_words * 4;
-  // state rows in shared memory when a block's rows fit (small problems: all
-  // the explorer is for), else in the L1/L2-cached global scratch
-  const size_t smem = row_b * 128;
-  const bool use_smem = smem <= 96 * 1024 && !getenv("RC_DEBUG_EXPLORE_GLOBAL") &&  // (test hook)
-                        cudaFuncSetAttribute(explore_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem) == cudaSuccess;
   const uint64_t scr_stride = use_smem ? 1 : G;
   void* b0 = buf(0, row_b + cells * 4 + (prog->n_arrays + 2) * 4 + prog->n_instr * sizeof(Ins));
   void* b1 = buf(1, row_words * scr_stride * 4);
