@@ -436,6 +436,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   // dev instrumentation (RC_GAPS=1): GPU time inside interval enqueues vs the whole run
   const bool gaps = getenv("RC_GAPS") != nullptr;
   std::vector<std::array<cudaEvent_t, 2>> gap_ev;
+  std::vector<uint32_t> gap_b;  // batch of each recorded interval
   cudaEvent_t g0 = nullptr, g1 = nullptr;
   if (gaps) { cudaEventCreate(&g0); cudaEventCreate(&g1); cudaEventRecord(g0, s); }
   // A2, double-buffered: batch i's inputs are copied (2-D copies into the
@@ -585,7 +586,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     auto enqueue_interval = [&](uint32_t kk, int cc, Marks* mk) -> cudaError_t {
       cudaError_t e;
 #define EQ(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
-      if (gaps) { gap_ev.push_back({}); cudaEventCreate(&gap_ev.back()[0]); cudaEventCreate(&gap_ev.back()[1]); cudaEventRecord(gap_ev.back()[0], s); }
+      if (gaps) { gap_ev.push_back({}); gap_b.push_back(bi); cudaEventCreate(&gap_ev.back()[0]); cudaEventCreate(&gap_ev.back()[1]); cudaEventRecord(gap_ev.back()[0], s); }
       if (opt.profile) W.prof.on = (prof_intervals++ % prof_every) == 0;  // sampled interval profile
       // write-set map: a fresh tag per interval attempt; zeroed only when the tags wrap
       if (++W.wtag == 0 || W.wtag == 1) {
@@ -846,17 +847,22 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   if (gaps) {
     cudaEventRecord(g1, s);
     cudaEventSynchronize(g1);
-    float tot = 0, iv = 0, gapsum = 0;
+    float tot = 0, iv = 0, gap_in = 0, gap_x = 0;
     cudaEventElapsedTime(&tot, g0, g1);
     for (size_t i = 0; i < gap_ev.size(); i++) {
       float x = 0;
       cudaEventElapsedTime(&x, gap_ev[i][0], gap_ev[i][1]);
       iv += x;
-      if (i + 1 < gap_ev.size()) { float y = 0; cudaEventElapsedTime(&y, gap_ev[i][1], gap_ev[i + 1][0]); gapsum += y; }
+      if (i + 1 < gap_ev.size()) {
+        float y = 0;
+        cudaEventElapsedTime(&y, gap_ev[i][1], gap_ev[i + 1][0]);
+        (gap_b[i + 1] == gap_b[i] ? gap_in : gap_x) += y;
+      }
       cudaEventDestroy(gap_ev[i][0]);
       cudaEventDestroy(gap_ev[i][1]);
     }
-    fprintf(stderr, "RC_GAPS run %.2f ms, %zu interval enqueues %.2f ms, between them %.2f ms\n", tot, gap_ev.size(), iv, gapsum);
+    fprintf(stderr, "RC_GAPS run %.2f ms, %zu interval enqueues %.2f ms, between them %.2f ms in batches + %.2f ms across batches\n",
+            tot, gap_ev.size(), iv, gap_in, gap_x);
   }
 #ifdef INTERP_PHASE_TIMING
   if (getenv("RC_PHASES")) {
