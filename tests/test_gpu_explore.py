@@ -184,3 +184,36 @@ def test_explore_global_scratch_path(oracle_lib, monkeypatch):
     p = K.program(K.BENIGN["K_inc"])
     reached, heap, regs, pc, st = oracle_lib.state_at(p.bytecode, 4, [np.array([40], np.int32), np.zeros(4, np.int32)], 0)
     check_interval(oracle_lib, p, 4, [1, 4], heap, regs, pc, st, full=False)
+
+
+def test_explore_edge_cases(oracle_lib):
+    """n = 1 (one schedule), no runnable work-item (the empty schedule), and
+    index sub-ranges: disjoint ranges add up to the whole exploration."""
+    import torch
+
+    from paper_1308_3203_b200 import rc_explore, rc_load_program
+    p = K.program(K.BENIGN["K_inc"])
+    prog = rc_load_program(p.bytecode)
+
+    def state(n):
+        _, heap, regs, pc, st = oracle_lib.state_at(p.bytecode, n, [np.array([40], np.int32), np.zeros(n, np.int32)], 0)
+        return (torch.from_numpy(heap.astype(np.int32)).cuda(), torch.from_numpy(regs).cuda(),
+                torch.from_numpy(pc.astype(np.int32)).cuda(), torch.from_numpy(st).cuda())
+
+    heap, regs, pc, st = state(1)
+    for red in (True, False):
+        r = rc_explore(prog, 1, heap, regs=regs, pc=pc, status=st, sizes=[1, 1], index_end=8, reduced=red, cap=8)
+        assert r.complete and r.n_schedules == 1 and r.n_differ == 0 and r.witness is None
+        assert int(r.terminals[0, 0]) == 41  # A[0] + 1
+    heap, regs, pc, st = state(3)
+    waiting = torch.ones_like(st)  # every work-item suspended at a barrier: nothing steps
+    r = rc_explore(prog, 3, heap, regs=regs, pc=pc, status=waiting, sizes=[1, 3], index_end=4, cap=4)
+    assert r.complete and r.n_schedules == 1 and r.max_product == 1
+    assert r.terminals[0].cpu().tolist()[:4] == heap.cpu().tolist()  # the heap is untouched
+    whole = rc_explore(prog, 3, heap, regs=regs, pc=pc, status=st, sizes=[1, 3], index_end=1 << 12)
+    assert whole.complete and whole.n_schedules == 90  # 6! / 2^3 interleavings of 3 x (LD, ST)
+    parts = [rc_explore(prog, 3, heap, regs=regs, pc=pc, status=st, sizes=[1, 3], index_begin=a, index_end=b)
+             for a, b in ((0, 100), (100, 1000), (1000, 1 << 12))]
+    assert sum(x.n_schedules for x in parts) == 90 and sum(x.n_differ for x in parts) == whole.n_differ
+    assert min(x.witness for x in parts if x.witness is not None) == whole.witness
+    assert not parts[1].complete  # only a range that starts at 0 can be complete
