@@ -413,7 +413,12 @@ def main():
                "sample": f"first {sample} instances of the workload ({n} work-items each), "
                          f"{cores} threads over instances, {dt:.1f} s"}
 
-    explorer = None if args.no_explorer else explorer_line(dev)
+    explorer = None
+    if not args.no_explorer:
+        try:  # a side measurement: never costs the main line
+            explorer = explorer_line(dev)
+        except Exception as ex:  # noqa: BLE001
+            explorer = {"error": f"{type(ex).__name__}: {ex}"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
