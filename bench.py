@@ -5,13 +5,15 @@ One step = one rc_run over the whole workload (all §8(a) rows: heap init,
 every barrier interval's interpretation, onesweep sort, detect + commit,
 boundary bookkeeping, report finalize, report copy-out) plus, at N>1, the NCCL
 report gather.  Default workload = BASELINE config 5 (3-point stencil,
-2^20 work-items x 512 instances per GPU, 8 barrier intervals; weak scaling:
-every rank checks its own 512 instances).  Inputs (4.3 GB per GPU) are far
-larger than the 126 MB L2, so no explicit flush is needed.
+2^20 work-items x 512 instances, 8 barrier intervals), STRONG scaling as
+SURVEY.md §8(e) defines it: the 512 instances are split over the N ranks
+(512/N each, contiguous shards).  Inputs (4.3 GB in all) are far larger than
+the 126 MB L2, so no explicit flush is needed for the main line; the
+secondary config-3 line flushes L2 before every timed step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Prints ONE JSON line on rank 0 (contract in the task statement / DESIGN.md §7).
+Prints ONE JSON line on rank 0 (contract in the task statement / DESIGN.md §6).
 """
 from __future__ import annotations
 
@@ -31,18 +33,20 @@ import numpy as np  # noqa: E402
 from workloads import inputs as I  # noqa: E402
 from workloads import kernels as K  # noqa: E402
 
+# total = instances of the BASELINE configuration; strong scaling splits them
+# over the ranks, weak scaling gives every rank `total` instances
 WORKLOADS = {
-    "cfg5": dict(name="config5: 3-point stencil, 2^20 work-items x 512 instances per GPU, 8 barriers",
-                 n=1 << 20, per_gpu=512, src=lambda: K.program(K.STENCIL),
+    "cfg5": dict(name="config5: 3-point stencil, 2^20 work-items x 512 instances, 8 barriers",
+                 n=1 << 20, total=512, src=lambda: K.program(K.STENCIL),
                  gen=lambda lo, hi, n: I.cfg5_inputs(lo, hi, n)),
-    "cfg4": dict(name="config4: random straight-line stencil kernel (seed 0), 65536 work-items x 512 instances per GPU",
-                 n=65536, per_gpu=512, src=lambda: K.random_stencil_kernel(0),
+    "cfg4": dict(name="config4: random straight-line stencil kernel (seed 0), 65536 work-items x 4096 instances",
+                 n=65536, total=4096, src=lambda: K.random_stencil_kernel(0),
                  gen=lambda lo, hi, n: I.cfg4_inputs(lo, hi, n)),
-    "cfg3": dict(name="config3: race-free tree reduction, 1024 work-items x 16384 instances per GPU, 11 intervals",
-                 n=1024, per_gpu=16384, src=lambda: K.program(K.TREE),
+    "cfg3": dict(name="config3: race-free tree reduction, 1024 work-items x 16384 instances, 11 intervals",
+                 n=1024, total=16384, src=lambda: K.program(K.TREE),
                  gen=lambda lo, hi, n: I.cfg3_inputs(lo, hi, n)),
     "cfg3off": dict(name="config3: off-by-one tree reduction (1 OOB + 9 RW per instance), 1024 work-items x 16384 "
-                         "instances per GPU", n=1024, per_gpu=16384, src=lambda: K.program(K.TREE_OFF_BY_ONE),
+                         "instances", n=1024, total=16384, src=lambda: K.program(K.TREE_OFF_BY_ONE),
                     gen=lambda lo, hi, n: I.cfg3_inputs(lo, hi, n)),
 }
 METRIC = "checked memory accesses/s"
@@ -173,13 +177,19 @@ def oracle_sample(wl, n_inst, threads):
     return r.stats["checked_accesses"], dt
 
 
+def instances_of(wl, scaling, world):
+    """(total instances of the job, instances per rank) for a workload."""
+    total = wl["total"] * world if scaling == "weak" else wl["total"]
+    return total, total // world
+
+
 def run_reference(args, wl):
     """--impl reference: the CPU oracle timed on the host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     cores = cpu_cores()
-    sample = min(wl["per_gpu"], cores)
+    sample = min(wl["total"], cores)
     for _ in range(args.warmup):
         oracle_sample(wl, sample, cores)
     acc = 0
@@ -189,17 +199,123 @@ def run_reference(args, wl):
         acc += a
         tot += dt
     v = acc / tot / 1e9
+    total, _ = instances_of(wl, args.scaling, args.gpus)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int32",
             "data": "synthetic",
-            "config": {"workload": wl["name"], "work_items": wl["n"], "sample_instances_per_step": sample},
+            "config": {"workload": wl["name"], "work_items": wl["n"], "instances_total": total,
+                       "sample_instances_per_step": sample},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"first {sample} instances of the workload per step (oracle/oracle.c, "
                                        f"{cores} threads over instances)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _sum_profiles(acc, prof):
+    if prof is None:
+        return acc
+    if acc is None:
+        return prof
+    for k, v in prof.items():
+        if isinstance(v, dict):
+            for kk in v:
+                acc[k][kk] += v[kk]
+        elif k != "sample_every":
+            acc[k] += v
+    return acc
+
+
+class Job:
+    """One workload's shard on this rank: program, inputs resident in HBM, the
+    per-step call (rc_run + the N>1 gather)."""
+
+    def __init__(self, wl, lo, hi, dev, local, stream, world, cdev, args):
+        from paper_1308_3203_b200 import rc_load_program
+        self.wl, self.lo, self.hi, self.n = wl, lo, hi, wl["n"]
+        self.dev, self.local, self.stream, self.world, self.cdev, self.args = dev, local, stream, world, cdev, args
+        self.prog = rc_load_program(wl["src"]().bytecode)
+        self.host = wl["gen"](lo, hi, self.n)
+        import torch
+        self.arrays = [torch.from_numpy(x).to(dev) for x in self.host]
+
+    def step(self, profile=False, arrs=None):
+        from paper_1308_3203_b200 import rc_run
+        from paper_1308_3203_b200.gather import gather_reports
+        a = self.args
+        r = rc_run(self.prog, self.n, arrs if arrs is not None else self.arrays, instance_offset=self.lo,
+                   want_final=False, profile=profile, device=self.local, stream=self.stream,
+                   keep_all_reads=a.keep_all_reads, classify_rw=a.classify_rw)
+        if self.world > 1:
+            reps, st = gather_reports(r.reports, r.stats, device=self.cdev)
+        else:
+            reps, st = r.reports, r.stats
+        return r, reps, st
+
+    def timed(self, steps, warmup, profile=False, flush=None):
+        """W untimed steps, then K timed steps (CUDA events on the launch
+        stream; with `flush` an untimed L2 flush before every timed step).
+        Returns (ms per step, max over ranks; accesses per step, whole job;
+        instructions per step; reports per step; summed profile)."""
+        import torch
+        import torch.distributed as dist
+        for _ in range(warmup):
+            self.step()
+        if self.world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(self.dev)
+        prof = None
+        acc = ins = nrep = 0
+        ms = 0.0
+        evs = []
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        if flush is None:
+            e0.record(self.stream)
+        for _ in range(steps):
+            if flush is not None:
+                flush()
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(self.stream)
+            r, reps, st = self.step(profile=profile)
+            if flush is not None:
+                a1.record(self.stream)
+                evs.append((a0, a1))
+            acc += st["checked_accesses"]
+            ins += st["instructions"]
+            nrep = len(reps)
+            prof = _sum_profiles(prof, r.profile)
+        if flush is None:
+            e1.record(self.stream)
+        torch.cuda.synchronize(self.dev)
+        ms = sum(a.elapsed_time(b) for a, b in evs) if flush is not None else e0.elapsed_time(e1)
+        if self.world > 1:
+            t = torch.tensor([ms], device=self.cdev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms / steps, acc // steps, ins // steps, nrep, prof
+
+
+def secondary_line(key, args, world, rank, dev, local, stream, cdev, scaling, steps, warmup, flush=None):
+    """A second configuration measured beside the main line (north_star covers
+    stencils AND reductions): value, ms per step, accesses per step."""
+    from paper_1308_3203_b200.gather import shard
+    wl = WORKLOADS[key]
+    total = wl["total"] * world if scaling == "weak" else wl["total"]
+    if scaling == "per_gpu_share":  # BASELINE's 8-GPU configuration: every GPU its 1/8
+        total = wl["total"] // 8 * world
+    lo, hi = shard(total, rank, world)
+    job = Job(wl, lo, hi, dev, local, stream, world, cdev, args)
+    ms, acc, ins, nrep, _ = job.timed(steps, warmup, flush=flush)
+    out = {"workload": wl["name"], "instances_total": total, "instances_per_gpu": hi - lo, "scaling": scaling,
+           "value": acc / (ms / 1000) / 1e9, "unit": UNIT, "ms_per_step": ms, "steps": steps, "warmup": warmup,
+           "checked_accesses_per_step": acc, "reports_per_step": nrep,
+           "l2": "flushed (256 MB write) before every timed step" if flush else "inputs >> 126 MB L2"}
+    del job
+    return out
 
 
 def main():
@@ -209,13 +325,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg5", choices=list(WORKLOADS))
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (default): the BASELINE configuration's instances split over the ranks; "
+                         "weak: every rank runs the whole configuration")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--no-explorer", action="store_true", help="skip the rc_explore line (SURVEY §8(f) row 2)")
-    ap.add_argument("--instances", type=int, default=0, help="override instances per GPU (debug)")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the config-3 / config-4 lines")
+    ap.add_argument("--instances", type=int, default=0, help="override the configuration's instances (debug)")
     ap.add_argument("--classify-rw", action="store_true",
                     help="RW value classification (RC_OPT_CLASSIFY_RW, SURVEY §8(f) row 1)")
     ap.add_argument("--keep-all-reads", action="store_true",
@@ -223,15 +342,14 @@ def main():
     args = ap.parse_args()
     wl = dict(WORKLOADS[args.workload])
     if args.instances:
-        wl["per_gpu"] = args.instances
+        wl["total"] = args.instances
     if args.impl == "reference":
         return run_reference(args, wl)
 
     import torch
     import torch.distributed as dist
 
-    from paper_1308_3203_b200 import rc_load_program, rc_run
-    from paper_1308_3203_b200.gather import gather_reports, shard
+    from paper_1308_3203_b200.gather import shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -244,75 +362,37 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cdev = dev if backend == "nccl" else torch.device("cpu")  # where collectives' tensors live
+    group_info = {"backend": None, "world_size": 1}
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    total_inst = wl["per_gpu"] * world if args.scaling == "weak" else wl["per_gpu"]
+        # the communicator's own rank count (the driver checks every rank joined)
+        group_info = {"backend": dist.get_backend(), "world_size": dist.get_world_size()}
+        probe = torch.ones(1, device=cdev)
+        dist.all_reduce(probe)
+        group_info["all_reduce_ranks"] = int(probe.item())
+        if rank == 0:
+            print(f"bench: process group {group_info}", file=sys.stderr, flush=True)
+    total_inst, _ = instances_of(wl, args.scaling, world)
     lo, hi = shard(total_inst, rank, world)
     n = wl["n"]
-    p = wl["src"]()
-    prog = rc_load_program(p.bytecode)
-    host = wl["gen"](lo, hi, n)
-    arrays = [torch.from_numpy(x).to(dev) for x in host]
     stream = torch.cuda.current_stream(dev)
+    job = Job(wl, lo, hi, dev, local, stream, world, cdev, args)
 
-    def step(profile=False, arrs=arrays):
-        r = rc_run(prog, n, arrs, instance_offset=lo, want_final=False, profile=profile, device=local,
-                   stream=stream, keep_all_reads=args.keep_all_reads, classify_rw=args.classify_rw)
-        if world > 1:
-            reps, st = gather_reports(r.reports, r.stats, device=cdev)
-        else:
-            reps, st = r.reports, r.stats
-        return r, reps, st
-
-    for _ in range(args.warmup):
-        step()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    prof_sum = None
-    accesses = 0
-    instrs = 0
-    n_reports = 0
     with Clocks(local) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            r, reps, st = step(profile=not args.no_profile)
-            accesses += st["checked_accesses"]
-            instrs += st["instructions"]
-            n_reports = len(reps)
-            if r.profile:
-                if prof_sum is None:
-                    prof_sum = r.profile
-                else:
-                    for k, v in r.profile.items():
-                        if isinstance(v, dict):
-                            for kk in v:
-                                prof_sum[k][kk] += v[kk]
-                        elif k != "sample_every":
-                            prof_sum[k] += v
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device=cdev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        dist.barrier()
-    ms_step = ms / args.steps
-    # `accesses` already sums all ranks (gathered stats) at N>1
-    value = accesses / args.steps / (ms_step / 1000) / 1e9
+        ms_step, acc_step, ins_step, n_reports, prof_sum = job.timed(args.steps, args.warmup,
+                                                                     profile=not args.no_profile)
+    # accesses already sum all ranks (gathered stats) at N>1
+    value = acc_step / (ms_step / 1000) / 1e9
 
     # ---- end to end through the C ABI with HOST buffers (RC_OPT_HOST_IO)
     e2e = None
     if not args.no_e2e:
-        pinned = [torch.from_numpy(x).pin_memory() for x in host]
+        pinned = [torch.from_numpy(x).pin_memory() for x in job.host]
         h2d = sum(x.numel() * 4 for x in pinned)
-        step(arrs=pinned)
+        job.step(arrs=pinned)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
@@ -322,7 +402,7 @@ def main():
         d2h = 0
         a0.record(stream)
         for _ in range(args.e2e_steps):
-            r, reps, st = step(arrs=pinned)
+            r, reps, st = job.step(arrs=pinned)
             acc2 += st["checked_accesses"]
             d2h = len(r.reports) * 32 + 13 * 8
         a1.record(stream)
@@ -334,7 +414,28 @@ def main():
             ems = float(t.item())
         e2e = {"value": acc2 / args.e2e_steps / (ems / args.e2e_steps / 1000) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-               "ms_per_step": ems / args.e2e_steps}
+               "ms_per_step": ems / args.e2e_steps,
+               "what": "rc_run with pinned host arrays (RC_OPT_HOST_IO): the H2D copy of every input inside the "
+                       "step, the reports and counters back; final heaps not requested (optional in the ABI)"}
+        del pinned
+    del job
+    torch.cuda.empty_cache()
+
+    # ---- secondary configurations (every rank takes part in their gathers)
+    secondary = None
+    if not args.no_secondary and args.workload == "cfg5" and not args.instances:
+        secondary = {}
+        flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+        def flush():
+            flush_buf.fill_(1)
+        for key, scaling, steps, flush_fn in (("cfg4", "per_gpu_share", 3, None), ("cfg3", "strong", 5, flush)):
+            try:
+                secondary[key] = secondary_line(key, args, world, rank, dev, local, stream, cdev, scaling,
+                                                steps, 3, flush=flush_fn)
+            except Exception as ex:  # noqa: BLE001 — a side measurement never costs the main line
+                secondary[key] = {"error": f"{type(ex).__name__}: {ex}"}
+        del flush_buf
 
     if rank != 0:
         if world > 1:
@@ -405,13 +506,13 @@ def main():
         gpu_launches = prof_sum["kernel_launches"]
 
     cpu = None
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline:  # rank 0 (the others wait at the final barrier)
         cores = cpu_cores()
-        sample = min(wl["per_gpu"], 2 * cores)
+        sample = min(total_inst, 2 * cores)
         acc, dt = oracle_sample(wl, sample, cores)
         cpu = {"value": acc / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"first {sample} instances of the workload ({n} work-items each), "
-                         f"{cores} threads over instances, {dt:.1f} s"}
+                         f"{cores} threads over instances, {dt:.1f} s (rank 0)"}
 
     explorer = None
     if not args.no_explorer:
@@ -422,17 +523,19 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": wl["name"], "work_items": n, "instances_per_gpu": hi - lo,
-                       "write_set_filter": not args.keep_all_reads, "classify_rw": args.classify_rw,
-                       "instances_total": total_inst, "parallelism": f"dp{world} (instance shards)",
-                       "l2": "inputs 4.3 GB/GPU >> 126 MB L2 (no flush needed)",
-                       "checked_accesses_per_step": accesses // args.steps, "reports_per_step": n_reports},
+            "config": {"workload": wl["name"], "work_items": n, "instances_total": total_inst,
+                       "instances_per_gpu": hi - lo, "write_set_filter": not args.keep_all_reads,
+                       "classify_rw": args.classify_rw, "final_heaps": False,
+                       "parallelism": f"dp{world} (contiguous instance shards, NCCL gather of reports)",
+                       "process_group": group_info,
+                       "l2": "inputs 4.3 GB in all >> 126 MB L2 (no flush needed)",
+                       "checked_accesses_per_step": acc_step, "reports_per_step": n_reports},
             "roofline": roofline, "roofline_interp": roofline_interp, "roofline_detect": roofline_detect,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
-            "interpreter": {"bytecode_instr_per_s": instrs / args.steps / (ms_step / 1000),
-                            "bytecode_instr_per_step": instrs / args.steps,
+            "interpreter": {"bytecode_instr_per_s": ins_step / (ms_step / 1000),
+                            "bytecode_instr_per_step": ins_step,
                             "bound": "issue (ALU/LSU pipes; ncu sm__inst_executed.avg.per_cycle_active in profiles/)"},
-            "clocks": clocks, "kernels": kernels, "explorer": explorer}
+            "clocks": clocks, "kernels": kernels, "secondary": secondary, "explorer": explorer}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -163,6 +163,7 @@ typedef struct { uint32_t arr; int32_t idx; int32_t val; } ownw; /* own-write ov
 
 typedef struct {
   uint64_t checked, loads, stores, instructions, intervals_max, lanes_final[8];
+  uint64_t op_count[32]; /* executed instructions per opcode (test coverage only; no semantics) */
 } ostats;
 
 typedef struct {
@@ -199,6 +200,7 @@ static void exec_thread(const oprog* P, uint32_t t, const uint32_t* sizes, int32
     steps++;
     st->instructions++;
     const oins* I = &P->code[pc[t]];
+    st->op_count[I->op & 31]++;
     int fault;
     if (step_private(P, I, r, t, sizes, &pc[t], &fault)) {
       if (fault == S_DIV0) {
@@ -488,8 +490,9 @@ static void* worker(void* p) {
 
 /* Public: run the canonical algorithm on n_instances instances.
  * inputs[a] = n_instances * sizes[a] int32 (instance-major).  Reports are
- * returned malloc'd in canonical order (free with oracle_free).  stats[13] =
- * checked, loads, stores, instructions, intervals_max, lanes_final[8].
+ * returned malloc'd in canonical order (free with oracle_free).  stats[45] =
+ * checked, loads, stores, instructions, intervals_max, lanes_final[8],
+ * op_count[32] (executed instructions per opcode; a coverage counter).
  * classify != 0: RW value classification flags on the RW reports. */
 int oracle_run(const uint8_t* bc, size_t nbytes, uint32_t n, const uint32_t* sizes,
                const int32_t* const* inputs, uint32_t n_instances, uint32_t instance_offset,
@@ -518,6 +521,7 @@ int oracle_run(const uint8_t* bc, size_t nbytes, uint32_t n, const uint32_t* siz
     S.instructions += W[i].out.st.instructions;
     if (W[i].out.st.intervals_max > S.intervals_max) S.intervals_max = W[i].out.st.intervals_max;
     for (int q = 0; q < 8; q++) S.lanes_final[q] += W[i].out.st.lanes_final[q];
+    for (int q = 0; q < 32; q++) S.op_count[q] += W[i].out.st.op_count[q];
   }
   if (all.n) qsort(all.v, all.n, sizeof(orep), rep_cmp);
   *reports = all.v; *n_reports = all.n;
@@ -525,6 +529,7 @@ int oracle_run(const uint8_t* bc, size_t nbytes, uint32_t n, const uint32_t* siz
     stats[0] = S.checked; stats[1] = S.loads; stats[2] = S.stores; stats[3] = S.instructions;
     stats[4] = S.intervals_max;
     for (int q = 0; q < 8; q++) stats[5 + q] = S.lanes_final[q];
+    for (int q = 0; q < 32; q++) stats[13 + q] = S.op_count[q];
   }
   free(W); free(th); free(P.code);
   pthread_mutex_destroy(&c.mu);
@@ -577,7 +582,7 @@ typedef struct {
   int32_t* keys; uint64_t* counts; uint8_t* used; size_t tcap, tn;
   /* terminal set */
   int32_t* terms; uint8_t* tused; size_t ttcap, ttn;
-  uint64_t n_schedules; int memo; uint64_t budget; int over_budget;
+  uint64_t n_schedules; int memo; int reduced; uint64_t budget; int over_budget;
 } enumctx;
 
 /* state layout (int32 words): heap[cells] | per thread: pc, status, steps_lo, steps_hi, regs[R] */
@@ -676,8 +681,21 @@ static uint64_t enum_dfs(enumctx* E, int32_t* s) {
   }
   uint64_t total = 0;
   int32_t* nxt = (int32_t*)malloc(W * sizeof(int32_t));
+  /* reduced: a step that touches no shared cell (everything but LD / ST:
+   * it reads and writes only the thread's own τ — pc, status, registers,
+   * fuel — PAPER.md:168-201) commutes with every step of every other
+   * thread, so running the lowest such thread first reaches the same set of
+   * terminal states; only LD / ST remain scheduling points. */
+  int32_t eager = -1;
+  for (uint32_t t = 0; E->reduced && t < E->n && eager < 0; t++) {
+    const int32_t* L = s + E->cells + (size_t)t * LW;
+    if (L[1] != S_RUNNING) continue;
+    const uint8_t op = E->P->code[(uint32_t)L[0]].op;
+    if (op != O_LD && op != O_ST) eager = (int32_t)t;
+  }
   for (uint32_t t = 0; t < E->n; t++) {
     if (s[E->cells + (size_t)t * LW + 1] != S_RUNNING) continue;
+    if (eager >= 0 && t != (uint32_t)eager) continue;
     memcpy(nxt, s, W * sizeof(int32_t));
     enum_step(E, nxt, t);
     total += enum_dfs(E, nxt);
@@ -698,7 +716,10 @@ static uint64_t enum_dfs(enumctx* E, int32_t* s) {
  * Outputs: *n_schedules (saturating), terminal states malloc'd into *terms as
  * *n_terms rows of (cells + n*(4+n_regs)) int32 words (heap, then per thread
  * pc, status, 0, 0, regs).  Returns 0, or 1 if `budget` states/schedules were
- * exceeded (results incomplete), -1 on decode error. */
+ * exceeded (results incomplete), -1 on decode error.
+ * memo: bit 0 = merge equal states (counts summed); bit 1 = reduced
+ * scheduling (only LD / ST are interleaving points; the same terminal set,
+ * fewer schedules — see enum_dfs). */
 int oracle_enumerate(const uint8_t* bc, size_t nbytes, uint32_t n, const uint32_t* sizes,
                      const int32_t* heap0, const int32_t* regs0, const uint32_t* pc0,
                      const uint8_t* status0, uint64_t fuel, int memo, uint64_t budget,
@@ -707,7 +728,8 @@ int oracle_enumerate(const uint8_t* bc, size_t nbytes, uint32_t n, const uint32_
   if (decode(bc, nbytes, &P)) return -1;
   enumctx E;
   memset(&E, 0, sizeof E);
-  E.P = &P; E.n = n; E.sizes = sizes; E.fuel = fuel; E.memo = memo; E.budget = budget;
+  E.P = &P; E.n = n; E.sizes = sizes; E.fuel = fuel; E.memo = memo & 1; E.reduced = (memo >> 1) & 1;
+  E.budget = budget;
   for (uint32_t a = 0; a < P.n_arrays; a++) E.cells += sizes[a];
   size_t LW = lane_words(&P);
   E.state_words = E.cells + (size_t)n * LW;

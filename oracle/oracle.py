@@ -98,7 +98,7 @@ def run(bytecode: bytes, n: int, inputs: list[np.ndarray], *, instance_offset: i
     fin_ptrs = (C.POINTER(C.c_int32) * max(n_arrays, 1))(*[_ptr(x, C.c_int32) for x in finals]) if want_final else None
     rep_p = C.c_void_p()
     n_rep = C.c_uint64()
-    stats = np.zeros(13, dtype=np.uint64)
+    stats = np.zeros(13 + 32, dtype=np.uint64)
     if threads is None:
         threads = max(1, min(len(os.sched_getaffinity(0)), n_inst))
     rc = lib.oracle_run(bytecode, len(bytecode), n, _ptr(sizes, C.c_uint32), in_ptrs, n_inst, instance_offset,
@@ -115,6 +115,7 @@ def run(bytecode: bytes, n: int, inputs: list[np.ndarray], *, instance_offset: i
     lib.oracle_free(rep_p)
     st = dict(zip(STAT_NAMES, (int(x) for x in stats)))
     st["lanes_final"] = [int(x) for x in stats[5:13]]
+    st["op_counts"] = [int(x) for x in stats[13:45]]  # executed instructions per opcode (coverage)
     return Result(reps, finals, st)
 
 
@@ -149,9 +150,11 @@ class Enumeration:
 
 def enumerate_interval(bytecode: bytes, n: int, sizes: list[int], heap: np.ndarray, regs: np.ndarray,
                        pc: np.ndarray, status: np.ndarray, *, fuel: int = DEFAULT_FUEL, memo: bool = True,
-                       budget: int = 5_000_000) -> Enumeration:
+                       budget: int = 5_000_000, reduced: bool = False) -> Enumeration:
     """All interleavings of one barrier interval from the given state under the
-    paper's immediate-visibility global semantics."""
+    paper's immediate-visibility global semantics.
+    reduced: only LD / ST are scheduling points (private steps commute with
+    every other thread's steps): the same terminal states, fewer schedules."""
     lib = _load()
     n_regs, _ = _header(bytecode)
     sz = np.array(sizes or [0], dtype=np.uint32)
@@ -162,7 +165,7 @@ def enumerate_interval(bytecode: bytes, n: int, sizes: list[int], heap: np.ndarr
     nsch = C.c_uint64(); terms = C.c_void_p(); nterm = C.c_uint64(); roww = C.c_uint64()
     rc = lib.oracle_enumerate(bytecode, len(bytecode), n, _ptr(sz, C.c_uint32), _ptr(heap, C.c_int32),
                               _ptr(regs, C.c_int32), _ptr(pc, C.c_uint32), _ptr(status, C.c_uint8), fuel,
-                              1 if memo else 0, budget, C.byref(nsch), C.byref(terms), C.byref(nterm),
+                              (1 if memo else 0) | (2 if reduced else 0), budget, C.byref(nsch), C.byref(terms), C.byref(nterm),
                               C.byref(roww))
     if rc < 0:
         raise ValueError("oracle: bytecode decode failed")

@@ -244,11 +244,15 @@ cudaError_t finalize_reports(rc_report* reports, uint64_t n, rc_report* scratch,
   if (n <= 1) return cudaSuccess;
   uint64_t n2 = 2 * BLK;
   while (n2 < n) n2 <<= 1;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(bitonic_local, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * BLK * (int)sizeof(rc_report));
-    attr = true;
-  }
+  static DeviceSetup setup;
+  int dev = 0;
+  cudaError_t se = setup.run(
+      [](int) -> cudaError_t {
+        return cudaFuncSetAttribute(bitonic_local, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    2 * BLK * (int)sizeof(rc_report));
+      },
+      &dev);
+  if (se != cudaSuccess) return se;
   cudaMemcpyAsync(scratch, reports, n * sizeof(rc_report), cudaMemcpyDeviceToDevice, s);
   if (n2 > n) { pad_kernel<<<(unsigned)((n2 - n + 255) / 256), 256, 0, s>>>(scratch, n, n2); launched(); }
   const unsigned blocks_local = (unsigned)(n2 / (2 * BLK));

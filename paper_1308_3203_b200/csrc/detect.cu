@@ -422,14 +422,20 @@ cudaError_t launch_rw_flag(rc_report* reports, uint64_t r0, uint64_t r1, uint32_
 
 cudaError_t launch_detect(const DetectParams& p, cudaStream_t s) {
   if (p.n_records == 0 && !p.with_boundary) return cudaSuccess;
-  static int nsm = 0, per_sm = 1;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, detect_kernel, 256, 0);
-    per_sm = std::max(per_sm, 1);
-  }
+  static DeviceSetup setup;
+  static int nsm_of[RC_MAX_DEVICES], per_sm_of[RC_MAX_DEVICES];
+  int dev = 0;
+  cudaError_t se = setup.run(
+      [](int d) -> cudaError_t {
+        int per_sm = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, detect_kernel, 256, 0);
+        if (e != cudaSuccess) return e;
+        per_sm_of[d] = std::max(per_sm, 1);
+        return cudaDeviceGetAttribute(&nsm_of[d], cudaDevAttrMultiProcessorCount, d);
+      },
+      &dev);
+  if (se != cudaSuccess) return se;
+  const int nsm = nsm_of[dev], per_sm = per_sm_of[dev];
   // one resident wave (persistent warps stride over the chunks)
   const uint64_t warps = (p.n_records + DET_CHUNK - 1) / DET_CHUNK;  // upper bound
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((warps + 7) / 8, (uint64_t)nsm * per_sm));

@@ -346,6 +346,9 @@ extern "C" int rc_explore(const rc_program* prog, uint32_t n, const uint32_t* si
   per_sm = std::max(1, std::min(per_sm, 16));
   uint64_t blocks = (uint64_t)nsm * per_sm;
   while (blocks > 1 && blocks * 128 / 2 >= todo) blocks /= 2;
+  // global-scratch rows: one per thread; keep the scratch within 256 MB
+  // (the grid-stride loop covers every index with any grid)
+  while (!use_smem && blocks > 1 && row_b * blocks * 128 > (256ull << 20)) blocks /= 2;
   const uint64_t G = blocks * 128;
 
   // device buffers cached on the program (grow-only; rc_release_workspace /
@@ -427,6 +430,8 @@ extern "C" int rc_explore(const rc_program* prog, uint32_t n, const uint32_t* si
   out->max_product = h[3];
   out->n_terminal = h[4] < cap ? h[4] : cap;
   out->witness_len = (uint32_t)(h[5] & 0xFFFFFFFFu);
-  out->complete = index_begin == 0 && h[3] <= index_end;
+  // complete: every schedule has an index in [0, index_end) — only known when
+  // something was examined (schedule 0 always exists)
+  out->complete = index_begin == 0 && todo > 0 && h[3] <= index_end;
   return RC_OK;
 }

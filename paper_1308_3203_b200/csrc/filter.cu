@@ -141,12 +141,14 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
 
 cudaError_t launch_filter(const FilterParams& p, cudaStream_t s) {
   if (p.n_slots == 0) return cudaSuccess;
-  static int nsm = 0;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  static DeviceSetup setup;
+  static int nsm_of[RC_MAX_DEVICES];
+  int dev = 0;
+  cudaError_t se = setup.run(
+      [](int d) -> cudaError_t { return cudaDeviceGetAttribute(&nsm_of[d], cudaDevAttrMultiProcessorCount, d); },
+      &dev);
+  if (se != cudaSuccess) return se;
+  const int nsm = nsm_of[dev];
   const uint64_t per_block = (uint64_t)F_THREADS * F_ITEMS;
   const uint32_t grid = (uint32_t)std::min<uint64_t>((p.n_slots + per_block - 1) / per_block, (uint64_t)nsm * 8);
   filter_kernel<<<grid, F_THREADS, 0, s>>>(p);

@@ -953,38 +953,32 @@ cudaError_t launch_interp_h(const InterpParams& p, cudaStream_t s, int nsm) {
 
 cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
   if (p.n_lanes == 0) return cudaSuccess;
-  static bool attr_set = false;
-  static int nsm = 0;
-  if (!attr_set) {
-    for (auto f : {interp_kernel<true, true, 1, false>, interp_kernel<false, true, 1, false>,
-                   interp_kernel<true, false, 1, false>, interp_kernel<false, false, 1, false>,
-                   interp_kernel<true, true, 2, false>, interp_kernel<false, true, 2, false>,
-                   interp_kernel<true, false, 2, false>, interp_kernel<false, false, 2, false>,
-                   interp_kernel<true, true, 1, true>, interp_kernel<false, true, 1, true>,
-                   interp_kernel<true, false, 1, true>, interp_kernel<false, false, 1, true>
-#if INTERP_H == 4
-                   , interp_kernel<true, true, 4, false>, interp_kernel<false, true, 4, false>,
-                   interp_kernel<true, false, 4, false>, interp_kernel<false, false, 4, false>
-#endif
-                   }) {
-      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      if (e != cudaSuccess) return e;
-      cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    }
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    attr_set = true;
-  }
+  static DeviceSetup setup;
+  static int nsm_of[RC_MAX_DEVICES];
+  int dev = 0;
+  cudaError_t se = setup.run(
+      [](int d) -> cudaError_t {
+        for (auto f : {interp_kernel<true, true, 1, false>, interp_kernel<false, true, 1, false>,
+                       interp_kernel<true, false, 1, false>, interp_kernel<false, false, 1, false>,
+                       interp_kernel<true, true, 2, false>, interp_kernel<false, true, 2, false>,
+                       interp_kernel<true, false, 2, false>, interp_kernel<false, false, 2, false>,
+                       interp_kernel<true, true, 1, true>, interp_kernel<false, true, 1, true>,
+                       interp_kernel<true, false, 1, true>, interp_kernel<false, false, 1, true>}) {
+          cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+          if (e != cudaSuccess) return e;
+          cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        }
+        return cudaDeviceGetAttribute(&nsm_of[d], cudaDevAttrMultiProcessorCount, d);
+      },
+      &dev);
+  if (se != cudaSuccess) return se;
+  const int nsm = nsm_of[dev];
   // two work-items per thread when the batch has enough lanes to fill the GPU
   // (test hook RC_DEBUG_INTERP_H=1|2 forces one variant; results never differ)
   const char* force = getenv("RC_DEBUG_INTERP_H");
   const int h = force ? (force[0] == '2' ? 2 : 1)
                       : (INTERP_H >= 2 && p.n_lanes >= (uint32_t)INTERP_H * 256u * (uint32_t)nsm ? INTERP_H : 1);
   if (p.alt_mask) return launch_interp_h<1, true>(p, s, nsm);  // classification re-run (rare)
-#if INTERP_H == 4
-  if (h == 4) return launch_interp_h<4, false>(p, s, nsm);
-#endif
   return h == 2 ? launch_interp_h<2, false>(p, s, nsm) : launch_interp_h<1, false>(p, s, nsm);
 }
 

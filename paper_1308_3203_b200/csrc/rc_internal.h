@@ -14,6 +14,28 @@
 
 namespace rc {
 
+// Per-device one-time setup of a launcher (kernel attribute opt-ins such as
+// the large dynamic shared memory, the SM count, occupancy): attributes
+// apply to one device context and rc_options.device selects any GPU, so the
+// setup runs once per device, under std::call_once (values are published to
+// other threads only after every one of them is computed).
+constexpr int RC_MAX_DEVICES = 64;
+struct DeviceSetup {
+  std::once_flag once[RC_MAX_DEVICES];
+  cudaError_t err[RC_MAX_DEVICES] = {};
+  // f(dev) -> cudaError_t, run once for the current device; returns its device via *dev_out
+  template <class F>
+  cudaError_t run(F&& f, int* dev_out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= RC_MAX_DEVICES) return cudaErrorInvalidDevice;
+    std::call_once(once[dev], [&] { err[dev] = f(dev); });
+    *dev_out = dev;
+    return err[dev];
+  }
+};
+
 // count of librc kernel launches (reported in rc_profile.kernel_launches)
 extern std::atomic<uint64_t> g_launches;
 inline void launched(uint64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }

@@ -579,25 +579,31 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, const unsigned long long* 
   *in_alt = false;  // n: upper bound of the record count (exact when n_a == NULL)
   if (n == 0 || bits <= 0) return cudaSuccess;
   const int passes = (bits + 7) / 8;
-  static int nsm = 0, per_sm = 0;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const void* ks[4] = {(const void*)onesweep_kernel<true, unsigned long long>,
-                         (const void*)onesweep_kernel<true, unsigned>,
-                         (const void*)onesweep_kernel<false, unsigned long long>,
-                         (const void*)onesweep_kernel<false, unsigned>};
-    for (int i = 0; i < 4; i++) {
-      cudaError_t e = cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           i < 2 ? (int)sizeof(SortSmem<2>) : (int)sizeof(SortSmem<1>));
-      if (e != cudaSuccess) return e;
-      cudaFuncSetAttribute(ks[i], cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    }
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, onesweep_kernel<true, unsigned long long>, SORT_THREADS,
-                                                  sizeof(SortSmem<2>));
-    if (per_sm < 1) per_sm = 1;
-  }
+  static DeviceSetup setup;
+  static int nsm_of[RC_MAX_DEVICES], per_sm_of[RC_MAX_DEVICES];
+  int dev = 0;
+  cudaError_t se = setup.run(
+      [](int d) -> cudaError_t {
+        const void* ks[4] = {(const void*)onesweep_kernel<true, unsigned long long>,
+                             (const void*)onesweep_kernel<true, unsigned>,
+                             (const void*)onesweep_kernel<false, unsigned long long>,
+                             (const void*)onesweep_kernel<false, unsigned>};
+        for (int i = 0; i < 4; i++) {
+          cudaError_t e = cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               i < 2 ? (int)sizeof(SortSmem<2>) : (int)sizeof(SortSmem<1>));
+          if (e != cudaSuccess) return e;
+          cudaFuncSetAttribute(ks[i], cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        }
+        int per_sm = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, onesweep_kernel<true, unsigned long long>, SORT_THREADS, sizeof(SortSmem<2>));
+        if (e != cudaSuccess) return e;
+        per_sm_of[d] = per_sm < 1 ? 1 : per_sm;
+        return cudaDeviceGetAttribute(&nsm_of[d], cudaDevAttrMultiProcessorCount, d);
+      },
+      &dev);
+  if (se != cudaSuccess) return se;
+  const int nsm = nsm_of[dev], per_sm = per_sm_of[dev];
   if (ws.reset_tile_ctr) cudaMemsetAsync(ws.tile_ctr, 0, 4 * sizeof(uint32_t), s);
   if (!hist_ready) {  // (each pass scans its digit counts itself)
     if (prof) prof->begin(s);

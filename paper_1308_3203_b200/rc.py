@@ -188,7 +188,10 @@ def rc_run(prog: Program, work_group_size: int, arrays: list, *, n_instances: in
         n_instances = int(arrays[0].shape[0]) if arrays else 1
     for i, a in enumerate(arrays):
         if host_io:
-            a = np.ascontiguousarray(a.numpy() if isinstance(a, torch.Tensor) else a, dtype=np.int32)
+            a = a.numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+            if a.dtype != np.int32:  # as on the device path: no silent wrap or truncation
+                raise TypeError(f"array {i}: arrays must be int32, got {a.dtype}")
+            a = np.ascontiguousarray(a)
             if a.ndim == 1:
                 a = a[None, :]
             keep.append(a)
@@ -287,9 +290,10 @@ def rc_explore(prog: Program, work_group_size: int, heap, *, regs=None, pc=None,
     if stream is None:
         stream = torch.cuda.current_stream(dev)
     out = rc_explore_result()
-    code = lib().rc_explore(prog._h, n, sz, heap.data_ptr(), regs.data_ptr(), pc.data_ptr(), status.data_ptr(), fuel,
-                            index_begin, index_end, RC_EXPLORE_REDUCED if reduced else 0, terms.data_ptr(), cap,
-                            wsched.data_ptr(), max_len, C.c_void_p(stream.cuda_stream), C.byref(out))
+    with torch.cuda.device(dev):  # the C side launches on the current device (the tensors' GPU)
+        code = lib().rc_explore(prog._h, n, sz, heap.data_ptr(), regs.data_ptr(), pc.data_ptr(), status.data_ptr(),
+                                fuel, index_begin, index_end, RC_EXPLORE_REDUCED if reduced else 0, terms.data_ptr(),
+                                cap, wsched.data_ptr(), max_len, C.c_void_p(stream.cuda_stream), C.byref(out))
     if code != RC_OK:
         raise RCError(code, rc_last_error())
     wl = min(out.witness_len, max_len)

@@ -4,8 +4,11 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TESTS = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
+if TESTS not in sys.path:  # test helper modules (parity_corpus)
+    sys.path.insert(0, TESTS)
 
 
 def pytest_configure(config):

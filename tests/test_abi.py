@@ -142,3 +142,14 @@ def test_explore_argument_errors_without_gpu(rc):
     big = (ctypes.c_uint32 * 2)(4000, 100)
     assert call(sz=big) == ELIMIT and "state row" in rc.rc_last_error()
     assert out.n_schedules == 0 and out.complete == 0  # `out` is cleared on every call
+
+
+def test_host_arrays_must_be_int32(rc):
+    """The host-buffer path rejects non-int32 arrays exactly like the device
+    path (no silent wrap of int64 or truncation of floats); the check runs
+    before any CUDA call."""
+    import numpy as np
+    prog = rc.rc_load_program(assemble(K.BENIGN["K_c"]).bytecode)
+    for bad in (np.zeros((2, 1), np.int64), np.zeros((2, 1), np.float32)):
+        with pytest.raises(TypeError):
+            rc.rc_run(prog, 4, [bad, np.zeros((2, 4), np.int32)])

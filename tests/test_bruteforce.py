@@ -29,9 +29,11 @@ from workloads.asm import assemble
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
 
-def check_intervals(orc, prog, n, inputs, fuel=64, budget=3_000_000):
+def check_intervals(orc, prog, n, inputs, fuel=64, budget=3_000_000, reduced=False):
     """Run the canonical oracle on one instance and check I1-I4 for every
-    interval against exhaustive enumeration.  Returns per-interval |F|."""
+    interval against exhaustive enumeration.  Returns per-interval |F|.
+    reduced: enumerate with only LD / ST as scheduling points (the same
+    terminal set, checked against the full enumeration below)."""
     sizes = [int(x.shape[-1]) for x in inputs]
     ins2 = [x.reshape(1, -1) for x in inputs]
     res = orc.run(prog.bytecode, n, ins2, fuel=fuel, threads=1)
@@ -41,7 +43,8 @@ def check_intervals(orc, prog, n, inputs, fuel=64, budget=3_000_000):
     for k in range(n_int):
         reached, heap, regs, pc, st = orc.state_at(prog.bytecode, n, [x.reshape(-1) for x in inputs], k, fuel=fuel)
         assert reached
-        e = orc.enumerate_interval(prog.bytecode, n, sizes, heap, regs, pc, st, fuel=fuel, budget=budget)
+        e = orc.enumerate_interval(prog.bytecode, n, sizes, heap, regs, pc, st, fuel=fuel, budget=budget,
+                                   reduced=reduced)
         assert e.complete, "enumeration budget exceeded"
         kinds = {t[4] for t in reps if t[1] == k}
         F = set(e.heaps)
@@ -165,15 +168,84 @@ def test_schedule_count(oracle_lib, a, b):
     assert len(e0.lanes) == 1  # private-only: one end state
 
 
+def _tiny_case(i):
+    """Random tiny kernel #i and its inputs: n in {2, 3, 4} work-items, two
+    arrays of 3, 3-6 commands (full ALU, barriers, forward branches)."""
+    rng = np.random.default_rng(np.random.SeedSequence([1308_3203, i]))
+    n = int(rng.integers(2, 5))
+    p = K.random_tiny_kernel(rng, n_arrays=2, n_regs=4, n_commands=int(rng.integers(3, 7)), size=3)
+    ins = I.tiny_inputs(rng, 2, 3)
+    return n, p, [x[0] for x in ins]
+
+
+def _tiny_chunk(lo, hi):
+    import oracle
+    intervals = racy = 0
+    by_n = [0, 0, 0, 0, 0]
+    for i in range(lo, hi):
+        n, p, ins = _tiny_case(i)
+        try:
+            F = check_intervals(oracle, p, n, ins, reduced=True)
+        except AssertionError as ex:
+            raise AssertionError(f"kernel #{i} (n={n}): {ex}\n{p.source}") from None
+        intervals += len(F)
+        racy += sum(f > 1 for f in F)
+        by_n[n] += 1
+    return intervals, racy, by_n
+
+
+N_RANDOM_KERNELS = 12_000
+
+
 def test_random_tiny_kernels(oracle_lib):
-    """I1-I4 on random tiny kernels (n <= 3 threads, arrays of 3), SURVEY §8(c)."""
-    rng = np.random.default_rng(1308_3203)
-    n_checked = racy = 0
-    for it in range(3000):
+    """I1-I4 on 12 000 random tiny kernels at n <= 4 (>= 10^4),
+    enumerated with only the shared accesses as scheduling points (pinned
+    against the full enumeration by test_reduced_enumeration_same_terminals).
+    Chunks run in forked worker processes (the oracle is a C library)."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+    workers = max(1, min(len(os.sched_getaffinity(0)), 16))
+    step = 250
+    chunks = [(lo, min(lo + step, N_RANDOM_KERNELS)) for lo in range(0, N_RANDOM_KERNELS, step)]
+    tot = racy = 0
+    by_n = [0] * 5
+    with cf.ProcessPoolExecutor(workers, mp_context=mp.get_context("fork")) as ex:
+        for a, b, c in ex.map(_tiny_chunk, *zip(*chunks)):
+            tot += a
+            racy += b
+            by_n = [x + y for x, y in zip(by_n, c)]
+    assert sum(by_n) == N_RANDOM_KERNELS and min(by_n[2:]) > 3000  # every n in {2, 3, 4} well covered
+    assert tot > N_RANDOM_KERNELS and racy > 500  # the generator does produce non-determinism
+
+
+def test_reduced_enumeration_same_terminals(oracle_lib):
+    """The reduced enumeration (only LD / ST interleave; every other step
+    touches only its own thread's state, and commutes with
+    the others) reaches exactly the terminal states (heap and every lane) of
+    the full enumeration of PAPER.md:204-227, on the App. A kernels and 600
+    random tiny kernels at n <= 3, every interval."""
+    cases = [(K.program(K.FIG1_GUARDED), 4, [np.array([1, 2, 3, 4], np.int32), np.array([10, 20, 30, 40], np.int32),
+                                               np.array([100, 101, 102, 103], np.int32)]),
+             (K.program(K.FIG2), 2, [np.array([7, 9, 5], np.int32), np.array([42], np.int32)]),
+             (K.program(K.BENIGN["K_inc"]), 3, [np.array([40], np.int32), np.zeros(3, np.int32)])]
+    for i in range(600):
+        rng = np.random.default_rng(np.random.SeedSequence([0xE4E4, i]))
         n = int(rng.integers(2, 4))
         p = K.random_tiny_kernel(rng, n_arrays=2, n_regs=4, n_commands=int(rng.integers(3, 7)), size=3)
-        ins = I.tiny_inputs(rng, 2, 3)
-        F = check_intervals(oracle_lib, p, n, [x[0] for x in ins])
-        n_checked += len(F)
-        racy += sum(f > 1 for f in F)
-    assert n_checked > 3000 and racy > 100  # the generator does produce non-determinism
+        cases.append((p, n, [x[0] for x in I.tiny_inputs(rng, 2, 3)]))
+    fewer = 0
+    for p, n, ins in cases:
+        sizes = [int(x.shape[-1]) for x in ins]
+        k = 0
+        while True:
+            reached, heap, regs, pc, st = oracle_lib.state_at(p.bytecode, n, ins, k, fuel=64)
+            if not reached:
+                break
+            full = oracle_lib.enumerate_interval(p.bytecode, n, sizes, heap, regs, pc, st, fuel=64)
+            red = oracle_lib.enumerate_interval(p.bytecode, n, sizes, heap, regs, pc, st, fuel=64, reduced=True)
+            assert full.complete and red.complete
+            assert red.lanes == full.lanes, (k, p.source)
+            assert red.n_schedules <= full.n_schedules
+            fewer += red.n_schedules < full.n_schedules
+            k += 1
+    assert fewer > 100

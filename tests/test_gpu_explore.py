@@ -217,3 +217,5 @@ def test_explore_edge_cases(oracle_lib):
     assert sum(x.n_schedules for x in parts) == 90 and sum(x.n_differ for x in parts) == whole.n_differ
     assert min(x.witness for x in parts if x.witness is not None) == whole.witness
     assert not parts[1].complete  # only a range that starts at 0 can be complete
+    empty = rc_explore(prog, 3, heap, regs=regs, pc=pc, status=st, sizes=[1, 3], index_begin=0, index_end=0)
+    assert not empty.complete and empty.n_schedules == 0  # nothing examined: schedule 0 exists but was not seen

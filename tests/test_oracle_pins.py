@@ -267,23 +267,59 @@ def test_int32_arithmetic(oracle_lib):
         if op == "eq": return int(a == b)
         if op == "land": return int(a != 0 and b != 0)
 
+    # unary forms: v := v' (mov) and ¬b (lnot) of the first operand
+    unary = {"mov": lambda a: a, "lnot": lambda a: int(a == 0)}
+    cols = ops + list(unary)
     src = [".arrays X Y O", " tid r0", " ld r1, X, r0", " ld r2, Y, r0"]
-    for j, op in enumerate(ops):
-        src += [f" {op} r3, r1, r2", f" const r4, {len(ops)}", " mul r5, r0, r4", f" addi r5, r5, {j}",
+    for j, op in enumerate(cols):
+        operands = "r1" if op in unary else "r1, r2"
+        src += [f" {op} r3, {operands}", f" const r4, {len(cols)}", " mul r5, r0, r4", f" addi r5, r5, {j}",
                 " st O, r5, r3"]
-    src += [" lnot r3, r1", f" const r4, {len(ops)}", " const r6, 0", " st O, r6, r6", " exit"]
+    src += [" exit"]
     p = assemble("\n".join(src))
     n = len(pairs)
     X = np.array([[a for a, _ in pairs]], np.int32)
     Y = np.array([[b for _, b in pairs]], np.int32)
-    O = np.zeros((1, n * len(ops)), np.int32)
+    O = np.zeros((1, n * len(cols)), np.int32)
     r = oracle_lib.run(p.bytecode, n, [X, Y, O])
-    out = r.final[2][0].reshape(n, len(ops))
+    assert len(r.reports) == 0  # every work-item writes its own row of O
+    out = r.final[2][0].reshape(n, len(cols))
     for t, (a, b) in enumerate(pairs):
-        for j, op in enumerate(ops):
-            if t == 0 and j == 0:
-                continue  # O[0] is also written with 0 by every tid (benign WW)
-            assert int(out[t, j]) == ref(op, a, b), (op, a, b)
+        for j, op in enumerate(cols):
+            want = unary[op](a) if op in unary else ref(op, a, b)
+            assert int(out[t, j]) == want, (op, a, b)
+
+
+def test_mov_operand_order(oracle_lib):
+    """MOV rd, rs (`v := v'`, rc.h RC_OP_MOV: r[a] := r[b]),
+    hand-derived.  Per work-item t: r1 := t; r2 := 100; mov r2, r1 (r2 = t);
+    addi r1, r1, 5 (r1 = t + 5, r2 must keep t: a copy, not an alias);
+    mov r3, r3 (self-copy keeps the zero-initialised r3, reading L18);
+    A[t] := r2 + 1000 r3 = t; B[t] := r1 = t + 5.  A transposed MOV
+    (r[b] := r[a]) would give r1 = 100, so A[t] = 100 and B[t] = 105; a
+    MOV that aliases the registers would give A[t] = t + 5."""
+    src = """
+.arrays A B
+    tid   r1
+    const r2, 100
+    mov   r2, r1
+    addi  r1, r1, 5
+    mov   r3, r3
+    const r4, 1000
+    mul   r4, r4, r3
+    add   r5, r2, r4
+    tid   r6
+    st    A, r6, r5
+    st    B, r6, r1
+    exit
+"""
+    n = 6
+    p = assemble(src)
+    r = oracle_lib.run(p.bytecode, n, [np.zeros((1, n), np.int32), np.zeros((1, n), np.int32)])
+    assert len(r.reports) == 0
+    assert r.final[0][0].tolist() == [0, 1, 2, 3, 4, 5]
+    assert r.final[1][0].tolist() == [5, 6, 7, 8, 9, 10]
+    assert r.stats["op_counts"][2] == 2 * n  # both MOVs executed by every work-item
 
 
 # --------------------------------------------------------------- ⊥ / ⊤ policy

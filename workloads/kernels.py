@@ -205,7 +205,7 @@ def program(src: str) -> Program:
 HALO = 4
 
 
-def random_stencil_kernel(seed: int, n_commands: int = 64) -> Program:
+def random_stencil_kernel(seed: int, n_commands: int = 64, isa: str = "cfg4") -> Program:
     """Config 4 generator: 64 commands over 4 arrays X0..X3.
 
     Mix per command: 30% stencil load pair (ri := tid+K+k, k in [-4,4]; load
@@ -213,11 +213,21 @@ def random_stencil_kernel(seed: int, n_commands: int = 64) -> Program:
     20% home store Xw[tid+K], 4% indirect store Xw[X3[tid+K]], 4% indirect
     load Xw[X3[tid+K]], 8% barrier (w := (w+1) mod 3).  Then EXIT.
     Registers: r0 = tid, r1 = tid+K, r2..r9 data, r10 index temp.
+
+    isa="full" (parity corpus, not config 4): the ALU draws from every
+    register-to-register opcode of the §3 grammar: add sub
+    mul div mod min max and or xor lt eq land, and the unary mov / lnot; a
+    div / mod divisor is sometimes a 0/1 comparison result, so DIV0 (⊥)
+    occurs.  Same memory-command mix.
     """
     rng = np.random.default_rng(np.random.SeedSequence([0x13083203, 4, seed]))
     lines = [".arrays X0 X1 X2 X3", ".regs 11", "    tid r0", f"    addi r1, r0, {HALO}"]
     w = 0
     alu = ["add", "sub", "mul", "xor", "min", "max"]
+    if isa == "full":
+        alu = alu + ["div", "mod", "and", "or", "lt", "eq", "land", "mov", "lnot"]
+    elif isa != "cfg4":
+        raise ValueError(isa)
     for _ in range(n_commands):
         u = rng.random()
         d = int(rng.integers(2, 10))
@@ -228,7 +238,13 @@ def random_stencil_kernel(seed: int, n_commands: int = 64) -> Program:
         elif u < 0.60:
             op = alu[int(rng.integers(0, len(alu)))]
             a, b = int(rng.integers(2, 10)), int(rng.integers(2, 10))
-            lines.append(f"    {op} r{d}, r{a}, r{b}")
+            if op in ("mov", "lnot"):
+                lines.append(f"    {op} r{d}, r{a}")
+            elif op in ("div", "mod") and rng.random() < 0.5:
+                # divisor from a comparison (0 or 1): DIV0 on some work-items
+                lines += [f"    lt r10, r{a}, r{b}", f"    {op} r{d}, r{a}, r10"]
+            else:
+                lines.append(f"    {op} r{d}, r{a}, r{b}")
         elif u < 0.80:
             lines.append(f"    st X{w}, r1, r{d}")
         elif u < 0.84:
@@ -249,6 +265,9 @@ def random_tiny_kernel(rng: np.random.Generator, n_arrays: int = 2, n_regs: int 
 
     Indices are drawn as (tid*m + c) mod size so most accesses are in bounds
     and threads collide often; values come from tid, constants and loads.
+    The ALU draws from every register-to-register opcode of the grammar
+    (PAPER.md:87-88), mov and lnot included; div / mod by a zero register
+    halts the work-item with DIV0.
     """
     lines = [".arrays " + " ".join(f"A{i}" for i in range(n_arrays)), f".regs {n_regs + 3}",
              "    tid r0", f"    const r1, {size}"]
@@ -268,8 +287,14 @@ def random_tiny_kernel(rng: np.random.Generator, n_arrays: int = 2, n_regs: int 
                      f"    mod r{t}, r{t}, r1", f"    ld r{d}, A{int(rng.integers(0, n_arrays))}, r{t}"]
         elif u < 0.80:  # alu
             d = int(rng.integers(2, n_regs)) if n_regs > 2 else 2
-            op = ["add", "sub", "mul", "xor", "min", "max", "eq", "lt"][int(rng.integers(0, 8))]
-            body.append(f"    {op} r{d}, r{int(rng.integers(0, n_regs))}, r{int(rng.integers(0, n_regs))}")
+            ops = ["add", "sub", "mul", "xor", "min", "max", "eq", "lt", "and", "or", "land", "div", "mod",
+                   "mov", "lnot"]
+            op = ops[int(rng.integers(0, len(ops)))]
+            x, y = int(rng.integers(0, n_regs)), int(rng.integers(0, n_regs))
+            if op in ("mov", "lnot"):  # unary (v := v', ¬b)
+                body.append(f"    {op} r{d}, r{x}")
+            else:  # div / mod by a zero register halts the work-item (DIV0, reading L7)
+                body.append(f"    {op} r{d}, r{x}, r{y}")
         elif u < 0.88 and allow_bar:
             body.append("    bar")
         elif u < 0.96 and allow_branch:
