@@ -43,9 +43,11 @@ typedef enum {
   RC_ECUDA = 3,  /* a CUDA runtime call failed (no device, launch error ...)  */
   RC_ETRUNC = 4, /* more reports than `capacity`; the first `capacity` were
                     written, *n_reports_total holds the full count (snprintf) */
-  RC_ELIMIT = 5  /* an implementation limit was hit: a work-item wrote more
-                    distinct cells in one interval than the own-write overlay
-                    holds (RC_OVERLAY_CAP), or cells per batch exceed 2^32     */
+  RC_ELIMIT = 5  /* an address-space limit was hit: cells per instance exceed
+                    2^32, more than 2^32 access records in one interval, or
+                    more distinct cells written by one work-item in one
+                    interval than 2^24 (the own-write overlay itself spills
+                    to device memory: its capacity is not semantic)          */
 } rc_status;
 
 /* ---- bytecode (RCB1) ----------------------------------------------------
@@ -242,7 +244,6 @@ RC_API int rc_abi_version(void);
 /* Release all cached device workspace of `prog` (also done by rc_free_program). */
 RC_API int rc_release_workspace(rc_program* prog);
 
-#define RC_OVERLAY_CAP 16 /* distinct cells one work-item may write per interval */
 
 /* ---- interleaving explorer -------------------------
  * Every interleaving of ONE barrier interval under the paper's global

@@ -31,9 +31,18 @@ __device__ __forceinline__ uint32_t rec_cell(uint64_t r) { return (uint32_t)(r >
 // lanes and emit() turns them into tids
 __device__ __forceinline__ uint32_t rec_tid(uint64_t r) { return ((uint32_t)r >> 5) & (MAX_WG - 1); }
 __device__ __forceinline__ bool rec_w(uint64_t r) { return (r & 1) != 0; }
+// a spilled write (slot SLOT_SPILL): the value is in the lane's spill list (rare)
+__device__ __noinline__ int32_t spilled_val(const DetectParams& p, uint64_t r) {
+  const uint32_t lane = rec_tid(r), cell = rec_cell(r), ns = p.spill_n[lane];
+  for (uint32_t j = 0; j < ns; j++)
+    if (p.spill_cell[(size_t)j * p.n_lanes + lane] == cell) return p.spill_val[(size_t)j * p.n_lanes + lane];
+  return 0;  // unreachable: K1 wrote the record from this list
+}
 __device__ __forceinline__ int32_t rec_val(const DetectParams& p, uint64_t r) {
-  // slot * n_lanes + lane < 16 * 2^27: 32-bit index arithmetic
-  return __ldg(p.wval + ((((uint32_t)r >> 1) & 0xF) * p.n_lanes + rec_tid(r)));
+  // slot * n_lanes + lane < 15 * 2^27: 32-bit index arithmetic
+  const uint32_t slot = ((uint32_t)r >> 1) & 0xF;
+  if (slot == SLOT_SPILL) return spilled_val(p, r);
+  return __ldg(p.wval + (slot * p.n_lanes + rec_tid(r)));
 }
 
 __device__ __forceinline__ void emit(const DetectParams& p, uint32_t cell, uint32_t t1, uint32_t t2, uint16_t kind,
@@ -333,7 +342,7 @@ __device__ __forceinline__ void boundary_tail(const DetectParams& p) {
   // leaves the divergence flags of the previous interval in place: the re-run
   // of K1 reads them (static write-set elision, InterpParams::inst_div)
   const volatile DevCounters* cv = c;
-  const bool rerun = cv->log_overflow || cv->k1_reports > p.report_cap;
+  const bool rerun = cv->log_overflow || cv->ovl_overflow || cv->k1_reports > p.report_cap;
   bool any_div = false;
   for (uint32_t inst = lane; inst < p.n_inst; inst += 32) {
     const int32_t lo = p.node_min[inst], hi = p.node_max[inst];
@@ -359,11 +368,11 @@ __device__ __forceinline__ void boundary_tail(const DetectParams& p) {
 
 // Persistent: warps stride over the chunks; the record count is read from
 // device memory (no host sync).  Skips the detection (no commit) when this
-// interval's log overflowed or K1's reports overflowed: the host then re-runs
-// the interval from the saved lane state on an untouched heap.
+// interval's log, a spill list or K1's reports overflowed: the host then
+// re-runs the interval from the saved lane state on an untouched heap.
 __global__ void __launch_bounds__(256, DET_MINB) detect_kernel(const DetectParams p) {
   if (p.ctr->abort) return;  // speculative interval after one that needs the host (grid-uniform)
-  if (!(p.ctr->log_overflow || p.ctr->k1_reports > p.report_cap)) {
+  if (!(p.ctr->log_overflow || p.ctr->ovl_overflow || p.ctr->k1_reports > p.report_cap)) {
     const uint32_t n_records = (uint32_t)p.ctr->kept_count;
     const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wg * DET_CHUNK < n_records;

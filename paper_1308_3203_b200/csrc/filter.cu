@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   for (int i = t; i < p.passes * 256; i += F_THREADS) bh[i] = 0;
   if (blockIdx.x == 0 && t == 0) p.ctr->k1_reports = p.ctr->report_count;  // K1 is complete here
-  if (p.ctr->log_overflow) return;  // the interval will be re-run
+  if (p.ctr->log_overflow || p.ctr->ovl_overflow) return;  // the interval will be re-run
   // slots reserved past the buffer end only ever held sentinel padding (a real
   // record there sets log_overflow): clamp to the capacity
   // (slot indices < n_slots < 2^32: 32-bit index arithmetic)

@@ -560,8 +560,16 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
               cell = cell_base[h] + et.x + (uint32_t)idx;
               int32_t v = 0;
               bool found = false;
-              for (int j = 0; j < n_own[h]; j++)
+              const int n_sm = min(n_own[h], (int)OV);
+              for (int j = 0; j < n_sm; j++)
                 if ((uint32_t)lds32(OC(h) + j * orow) == cell) { v = lds32(OVL(h) + j * orow); found = true; }
+              if (n_own[h] > (int)OV && !found) {  // the lane's spill list (rare)
+                for (int j = 0; j < n_own[h] - (int)OV; j++)
+                  if (p.spill_cell[(size_t)j * p.n_lanes + g[h]] == cell) {
+                    v = p.spill_val[(size_t)j * p.n_lanes + g[h]];
+                    found = true;
+                  }
+              }
               if (found) {
                 sts32(RA(h), v);
               } else {
@@ -591,13 +599,30 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
             status[h] = L_OOB;
           } else {
             const uint32_t cell = cell_base[h] + et.x + (uint32_t)idx;
+            const int n_sm = min(n_own[h], (int)OV);
             int j = 0;
-            while (j < n_own[h] && (uint32_t)lds32(OC(h) + j * orow) != cell) j++;
-            if (j == n_own[h]) {
-              if (n_own[h] < (int)OV) { sts32(OC(h) + j * orow, (int32_t)cell); n_own[h]++; }
-              else { ovl_over[h] = true; j = -1; }
+            while (j < n_sm && (uint32_t)lds32(OC(h) + j * orow) != cell) j++;
+            if (j < n_sm) {
+              sts32(OVL(h) + j * orow, lds32(RC(h)));
+            } else if (n_own[h] < (int)OV) {
+              sts32(OC(h) + j * orow, (int32_t)cell);
+              n_own[h]++;
+              sts32(OVL(h) + j * orow, lds32(RC(h)));
+            } else {  // beyond the smem overlay: the lane's spill list in HBM (rare)
+              const int ns = n_own[h] - (int)OV;
+              int k = 0;
+              while (k < ns && p.spill_cell[(size_t)k * p.n_lanes + g[h]] != cell) k++;
+              if (k == ns) {
+                if ((uint32_t)ns < p.spill_cap) {
+                  p.spill_cell[(size_t)k * p.n_lanes + g[h]] = cell;
+                  n_own[h]++;
+                } else {
+                  ovl_over[h] = true;  // full: the interval is re-run with a larger list
+                  k = -1;
+                }
+              }
+              if (k >= 0) p.spill_val[(size_t)k * p.n_lanes + g[h]] = lds32(RC(h));
             }
-            if (j >= 0) sts32(OVL(h) + j * orow, lds32(RC(h)));
             pc[h]++;
             nstores[h]++;
           }
@@ -700,13 +725,21 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
         const unsigned m = __ballot_sync(FULL, has);
         if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane);
         if (has) {
-          const uint32_t cell = ocell[j * TL + l];
-          S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, g[h], (uint32_t)j, 1);
-          p.wval[(size_t)j * p.n_lanes + g[h]] = oval[j * TL + l];
+          uint32_t cell, slot;
+          if (j < (int)OV) {
+            cell = ocell[j * TL + l];
+            slot = (uint32_t)j;
+            p.wval[(size_t)j * p.n_lanes + g[h]] = oval[j * TL + l];
+          } else {  // spilled: detect looks the value up in the lane's list
+            cell = p.spill_cell[(size_t)(j - (int)OV) * p.n_lanes + g[h]];
+            slot = SLOT_SPILL;
+          }
+          S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, g[h], slot, 1);
           p.wmap[cell] = p.wtag;  // write-set map (filter.cu)
         }
         S.fill += __popc(m);
       }
+      if (n_own[h] > (int)OV) p.spill_n[g[h]] = (uint32_t)(n_own[h] - (int)OV);
     }
 
     IPHASE(3);

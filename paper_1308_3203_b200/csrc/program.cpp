@@ -289,6 +289,7 @@ void analyze(rc_program* P) {
   const int64_t st = max_path_weight(P, wst);
   const int64_t rec = max_path_weight(P, wrec);
   P->ovl_cap = (st < 0 || st > OVL_CAP) ? OVL_CAP : (int)std::max<int64_t>(st, 1);
+  P->may_spill = st < 0 || st > OVL_CAP;  // more distinct written cells than the smem overlay holds
   P->rec_bound = (rec < 0 || rec > 1024) ? -1 : (int)rec;
   const int64_t ins = max_path_weight(P, std::vector<int>(N, 1));
   P->instr_bound = (ins < 0 || ins >= (1ll << 31)) ? -1 : ins;

@@ -66,7 +66,13 @@ enum LaneStatus : uint8_t {
 constexpr int32_t NODE_NONE = -2;
 constexpr int32_t NODE_EXIT = -1;
 constexpr uint32_t NOTID = 0xFFFFFFFFu;
-constexpr int OVL_CAP = 16;        // own-write overlay entries per work-item (smem)
+constexpr int OVL_CAP = 15;        // own-write overlay entries per work-item in shared memory
+// A work-item's distinct written cells beyond the shared-memory overlay go to
+// its HBM spill list (spill_cell / spill_val [spill_cap][n_lanes]); their
+// write records carry this slot and detect finds the value in the list.  The
+// capacity is not semantic: when a list is full the interval is re-run with a
+// larger one (runtime.cu).
+constexpr uint32_t SLOT_SPILL = 15;
 
 // One access-log record is a single u64:
 //   bits 63..32  cell id (batch-local; the sort key — only these bits are sorted)
@@ -92,7 +98,7 @@ __host__ __device__ inline uint64_t make_rec(uint32_t cell, uint32_t lane, uint3
   return ((uint64_t)cell << 32) | (lane << 5) | (slot << 1) | w;
 }
 
-static_assert(RC_OVERLAY_CAP == OVL_CAP, "overlay capacity in rc.h and the interpreter agree");
+static_assert(OVL_CAP < (int)SLOT_SPILL + 1 && SLOT_SPILL == 15, "the record's 4-bit slot: overlay slots, then the spill marker");
 
 // Device counters of one run; zeroed per attempt where noted.
 struct DevCounters {
@@ -103,7 +109,7 @@ struct DevCounters {
   unsigned long long iv_stores;
   unsigned long long iv_instr;
   unsigned int log_overflow;        // per attempt
-  unsigned int ovl_overflow;        // per attempt
+  unsigned int ovl_overflow;        // per attempt: a work-item's spill list was full (re-run with a larger one)
   unsigned int any_waiting;         // per interval
   unsigned int diverged;            // per interval
   unsigned long long k1_reports;    // report_count after K1 (snapshot taken by the filter)
@@ -146,7 +152,11 @@ struct InterpParams {
   uint8_t* status_out;
   const uint8_t* live;        // registers saved / restored across barriers
   uint32_t n_live;
-  uint32_t ovl_cap;           // own-write overlay entries per work-item (static bound)
+  uint32_t ovl_cap;           // own-write overlay entries per work-item in smem (static bound, <= OVL_CAP)
+  uint32_t* spill_cell;       // [spill_cap][n_lanes] cells written beyond the smem overlay (null: none possible)
+  int32_t* spill_val;         // [spill_cap][n_lanes] their values
+  uint32_t* spill_n;          // [n_lanes] spill entries of a lane (written when > 0)
+  uint32_t spill_cap;
   uint32_t stage_warp;        // records staged per warp in shared memory
   int32_t* node_min;          // [I_b] min / max arrival node (fused A4)
   int32_t* node_max;
@@ -167,7 +177,7 @@ struct InterpParams {
   const uint8_t* alt_mask;
   uint8_t* wmap;              // [I_b * cpi] == wtag: cell written in this interval
   uint8_t wtag;               // this interval's tag (1..255; the map is zeroed when tags wrap)
-  int32_t* wval;              // [ovl_cap][n_lanes] final value of each written overlay slot
+  int32_t* wval;              // [ovl_cap][n_lanes] final value of each written smem overlay slot
   rc_report* reports;
   unsigned long long report_cap;
   DevCounters* ctr;
@@ -176,6 +186,9 @@ struct InterpParams {
 struct DetectParams {
   const uint64_t* recs;       // sorted by cell; count = ctr->kept_count
   const int32_t* wval;        // [ovl_cap][n_lanes]
+  const uint32_t* spill_cell; // slot SLOT_SPILL: the lane's spill list (K1)
+  const int32_t* spill_val;
+  const uint32_t* spill_n;
   uint32_t n_lanes, n;        // lane = inst_local * n + tid
   uint32_t n_records;         // host upper bound (grid size)
   int32_t* heap;
@@ -329,7 +342,8 @@ struct rc_program {
   std::vector<uint8_t> live_regs;  // registers live across a barrier (+ live at pc 0)
   std::vector<uint8_t> live_at_entry;  // live_in(pc 0): the rows zeroed at a batch start (reading L18)
   std::vector<uint32_t> entry_ro;  // [n_instr] at interval entries: arrays (< 32) the region never stores to
-  int ovl_cap = rc::OVL_CAP;       // max distinct cells written per work-item per interval
+  int ovl_cap = rc::OVL_CAP;       // smem overlay entries (max distinct cells written per work-item per interval, capped)
+  bool may_spill = true;           // a work-item may write more than OVL_CAP distinct cells in one interval
   int rec_bound = -1;              // max log records per work-item per interval (-1 unbounded)
   int64_t instr_bound = -1;        // max instructions per work-item per interval (-1 unbounded)
   std::mutex mu;

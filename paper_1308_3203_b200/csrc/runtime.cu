@@ -121,6 +121,8 @@ struct rc_workspace {
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_start = nullptr;
   DevBuf regs[2], pc[2], status[2], live, entry_ro;
   DevBuf log, log_alt, wval, wmap, sort_status, ctr_block;
+  DevBuf spill_cell, spill_val, spill_n;  // own-write overlay spill lists (grown on demand)
+  uint32_t spill_cap = 0;                 // entries per lane the spill buffers hold
   uint8_t wtag = 0;  // write-set map tag of the last interval attempt
   bool plan_valid = false;      // cached batch plan (rc_run)
   uint64_t plan_key[4] = {0, 0, 0, 0};
@@ -142,7 +144,7 @@ struct rc_workspace {
     for (DevBuf* b : {&code, &arr_off, &arr_size, &heap, &heap2, &regs[0], &regs[1], &pc[0], &pc[1], &status[0],
                       &status[1], &live, &entry_ro, &log, &log_alt, &wval, &wmap, &sort_status,
                       &ctr_block, &reports, &reports_scratch, &inst_tmp, &heap_snap[0], &heap_snap[1], &heapB, &amap,
-                      &regs_b, &pc_b, &status_b, &cmp_inst})  // (ctr is a view into ctr_block)
+                      &regs_b, &pc_b, &status_b, &cmp_inst, &spill_cell, &spill_val, &spill_n})  // (ctr: a view)
       b->release();
     if (h_ctr) cudaFreeHost(h_ctr);
     for (cudaEvent_t e : iv_done)
@@ -371,6 +373,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       CK(W.cmp_inst.ensure((uint64_t)I_b * 4));
     }
     CK(W.wval.ensure(std::max<uint64_t>(1, L_max * (uint64_t)P->ovl_cap) * 4));
+    if (P->may_spill) CK(W.spill_n.ensure(L_pad * 4));
     const void* wmap_before = W.wmap.p;
     CK(W.wmap.ensure(std::max<uint64_t>(1, (uint64_t)I_b * cpi)));
     if (W.wmap.p != wmap_before) W.wtag = 0;  // new memory: zero it before the next tag is used
@@ -405,6 +408,24 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     return cudaSuccess;
   };
   CK(ensure_sort_status(log_cap));
+  // own-write overlay spill lists [spill_cap][L_max] (PAPER.md:176-179 puts no
+  // bound on the cells a work-item writes in an interval): grown when K1
+  // reports a full list, and the interval re-run
+  auto ensure_spill = [&](uint32_t cap) -> cudaError_t {
+    if (!P->may_spill || cap == 0) return cudaSuccess;
+    cudaError_t e = W.spill_cell.ensure((uint64_t)cap * std::max<uint64_t>(L_max, 1) * 4);
+    if (e == cudaSuccess) e = W.spill_val.ensure((uint64_t)cap * std::max<uint64_t>(L_max, 1) * 4);
+    if (e == cudaSuccess) W.spill_cap = cap;
+    return e;
+  };
+  CK(ensure_spill(W.spill_cap));  // (L_max may have grown since the capacity was set)
+  auto grow_spill = [&]() -> int {
+    const uint64_t want = W.spill_cap ? 4ull * W.spill_cap : 16ull;
+    if (want > (1ull << 24) - OVL_CAP)
+      return fail(RC_ELIMIT, "a work-item wrote more than 2^24 distinct cells in one barrier interval");
+    CK(ensure_spill((uint32_t)want));
+    return RC_OK;
+  };
   uint64_t rep_cap = W.reports.bytes / sizeof(rc_report);
   if (rep_cap < (1u << 16) && !small_buffers) {
     CK(W.reports.ensure((1u << 16) * sizeof(rc_report)));
@@ -515,6 +536,9 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       DetectParams dp;
       dp.recs = sr;
       dp.wval = W.wval.as<int32_t>();
+      dp.spill_cell = W.spill_cell.as<uint32_t>();
+      dp.spill_val = W.spill_val.as<int32_t>();
+      dp.spill_n = W.spill_n.as<uint32_t>();
       dp.n_lanes = L;
       dp.n = n;
       dp.n_records = (uint32_t)log_cap;  // upper bound; the kernel reads the exact count
@@ -565,6 +589,10 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       ip.live = W.live.as<uint8_t>();
       ip.n_live = (uint32_t)P->live_regs.size();
       ip.ovl_cap = (uint32_t)P->ovl_cap;
+      ip.spill_cell = P->may_spill ? W.spill_cell.as<uint32_t>() : nullptr;
+      ip.spill_val = P->may_spill ? W.spill_val.as<int32_t>() : nullptr;
+      ip.spill_n = P->may_spill ? W.spill_n.as<uint32_t>() : nullptr;
+      ip.spill_cap = P->may_spill ? W.spill_cap : 0;
       ip.stage_warp = stage_warp;
       ip.node_min = node_min;
       ip.node_max = node_max;
@@ -696,7 +724,11 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         dp.report_cap = ~0ull;  // (quiet: nothing is written; K1's uncounted reports never skip the commit)
         EQ(launch_detect(dp, s));
         EQ(read_ctr());
-        if (!W.h_ctr[2].log_overflow || attempt >= 8) break;
+        if ((!W.h_ctr[2].log_overflow && !W.h_ctr[2].ovl_overflow) || attempt >= 16) break;
+        if (W.h_ctr[2].ovl_overflow) {  // a spill list was full: grow it and re-run
+          if (grow_spill() != RC_OK) return cudaErrorMemoryAllocation;
+          continue;
+        }
         const uint64_t n_all = W.h_ctr[2].stage_count;  // grow the log and re-run (as for an interval)
         const uint64_t want = std::min<uint64_t>(n_all + n_all / 4 + 1024, 0xFFFFFFFFull);
         EQ(W.log.ensure(want * 8));
@@ -704,7 +736,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
         EQ(ensure_sort_status(log_cap));
       }
-      if (W.h_ctr[2].log_overflow) return cudaErrorMemoryAllocation;
+      if (W.h_ctr[2].log_overflow || W.h_ctr[2].ovl_overflow) return cudaErrorMemoryAllocation;
       EQ(cudaMemsetAsync(W.cmp_inst.p, 0, (size_t)nb * 4, s));
       EQ(launch_heap_compare(W.heapB.as<int32_t>(), heap_cur, cells, (uint32_t)cpi,
                              W.cmp_inst.as<uint32_t>(), s));
@@ -732,15 +764,15 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       const DevCounters h = W.h_ctr[k & 1];  // interval k's counters
       const bool next_aborted = h.abort != 0;
       if (spec && next_aborted) W.prof.marks.resize(mk_next.m0);  // k+1 did nothing
-      if (h.ovl_overflow)
-        return fail(RC_ELIMIT,
-                    "a work-item wrote more than %d distinct cells in one barrier interval (instance batch at "
-                    "%u, interval %u)",
-                    P->ovl_cap, inst_base, k);
       const uint64_t n_all = h.stage_count;  // staging slots reserved (records + padding)
       const bool log_over = h.log_overflow != 0;  // a real record did not fit
       const bool k1_rep_over = h.k1_reports > rep_cap;
-      if (log_over || k1_rep_over) {  // filter/detect skipped: grow and re-run the interval
+      const bool spill_over = h.ovl_overflow != 0;  // a work-item's spill list was full
+      if (log_over || k1_rep_over || spill_over) {  // filter/detect skipped: grow and re-run the interval
+        if (spill_over) {
+          const int e = grow_spill();
+          if (e != RC_OK) return e;
+        }
         if (log_over) {
           const uint64_t want = std::min<uint64_t>(n_all + n_all / 4 + 1024, 0xFFFFFFFFull);
           if (n_all > 0xFFFFFFFFull) return fail(RC_ELIMIT, "more than 2^32 access records in one interval");

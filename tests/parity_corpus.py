@@ -101,7 +101,9 @@ def corpus():
          ("error_kinds", assemble(ERROR_KINDS), 40, [np.zeros((3, 40), np.int32)]),
          ("tree_off_by_one", K.program(K.TREE_OFF_BY_ONE), 256, I.cfg3_inputs(0, 4, 256)),
          ("stencil", K.program(K.STENCIL), 500, I.cfg5_inputs(0, 2, 500)),
-         ("alu", _alu_kernel(), 47 * 47, _alu_inputs())]
+         ("alu", _alu_kernel(), 47 * 47, _alu_inputs()),
+         ("many_writes", K.many_writes_kernel(), 40, [np.arange(2 * (64 * 40 + 6), dtype=np.int32).reshape(2, -1),
+                                                      np.zeros((2, 40), np.int32)])]
     c += [_cfg4_full(s) for s in range(4)]
     c += _tiny(2024, 40)
     return c

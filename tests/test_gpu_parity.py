@@ -351,16 +351,26 @@ def test_truncation(rc):
     assert ei.value.code == 4
 
 
-def test_overlay_limit_is_a_call_error(rc):
-    src = [".arrays A", " tid r0", " const r1, 20", " mul r2, r0, r1"]
-    for j in range(20):
-        src += [f" addi r3, r2, {j}", " st A, r3, r0"]
-    src += [" exit"]
-    p = assemble("\n".join(src))
-    prog = rc.rc_load_program(p.bytecode)
-    with pytest.raises(rc.RCError) as ei:
-        rc.rc_run(prog, 4, [torch.zeros((1, 80), dtype=torch.int32, device="cuda")])
-    assert ei.value.code == 5
+@pytest.mark.parametrize("classify", [False, True])
+def test_many_writes_spill(rc, monkeypatch, classify):
+    """The own-write overlay holds 15 cells per work-item in shared memory and
+    spills the rest to HBM (its capacity is not semantic):
+    70 distinct cells per work-item in one interval (reads hitting both the
+    shared-memory part and the spill list, WW / RW on spilled cells), and a
+    loop with no static bound writing up to 100; ragged n, several batches,
+    the spill lists grown by re-running the interval (and with
+    RC_DEBUG_SMALL_BUFFERS every other buffer too)."""
+    for small in (False, True):
+        if small:
+            monkeypatch.setenv("RC_DEBUG_SMALL_BUFFERS", "1")
+        for n, n_inst, mb in ((5, 1, 0), (97, 3, 0), (300, 4, 2)):
+            p = K.many_writes_kernel()
+            ins = [np.arange(n_inst * (64 * n + 6), dtype=np.int32).reshape(n_inst, -1), np.zeros((n_inst, n), np.int32)]
+            _, g, o = run_both(rc, p, n, ins, classify_rw=classify, max_batch_instances=mb)
+            assert_parity(g, o, ins)
+            ins = [np.full((n_inst, 64 * n + 64), -7, np.int32)]
+            _, g, o = run_both(rc, K.program(K.MANY_WRITES_LOOP), n, ins, classify_rw=classify, max_batch_instances=mb)
+            assert_parity(g, o, ins)
 
 
 def test_random_tiny_kernels(rc):

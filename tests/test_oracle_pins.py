@@ -466,3 +466,66 @@ def test_own_write_visible(oracle_lib):
     assert r.final[1][0].tolist() == [10, 11, 12, 13, 101, 102, 103, 100]
     kinds = [t[4] for t in r.report_tuples()]
     assert kinds == [1, 1, 1, 1]  # each A[c] written by c, read by c-1
+
+
+def test_many_writes_per_interval(oracle_lib):
+    """the store rule bounds nothing, so a work-item may
+    write any number of distinct cells in one interval (workloads
+    many_writes_kernel, hand-derived).  Work-item t writes A[64t + j] :=
+    1000t + j, j = 0..69; cells 64(t+1) + j, j < 6, are also written by t+1
+    with 1000(t+1) + j: WW_NONBENIGN (t, t+1); t also reads 64(t+1) + 2, so
+    that cell has RW (t, t+1) with flags 0xB (t read + wrote, t+1 wrote) and
+    its WW flags are 0xB too; t+1 reads its own 64(t+1) + 3, which t wrote:
+    RW (t, t+1) with flags 0xE (t wrote, t+1 read + wrote), WW flags 0xE.
+    B[t] = A[64t+3] + A[64t+40] + A[64t+66] read from t's own writes:
+    (1000t + 3) + (1000t + 40) + (1000t + 66).  Final A: the max-tid writer."""
+    n = 5
+    p = K.many_writes_kernel()
+    A = np.zeros((1, 64 * n + 6), np.int32)
+    B = np.zeros((1, n), np.int32)
+    r = oracle_lib.run(p.bytecode, n, [A, B])
+    want = []
+    for t in range(n - 1):
+        for j in range(6):
+            c = 64 * (t + 1) + j
+            fl = {2: 0xB, 3: 0xE}.get(j, 0xA)
+            if j in (2, 3):
+                want.append((0, 0, 0, c, 1, t, t + 1, fl))
+            want.append((0, 0, 0, c, 3, t, t + 1, fl))
+    assert r.report_tuples() == want
+    assert r.final[1][0].tolist() == [3000 * t + 109 for t in range(n)]
+    fin = r.final[0][0]
+    for t in range(n):  # a cell written by t and t+1 keeps t+1's value
+        for j in range(70):
+            c = 64 * t + j
+            if j >= 64 and t + 1 < n:
+                assert fin[c] == 1000 * (t + 1) + (j - 64)
+            else:
+                assert fin[c] == 1000 * t + j, (t, j)
+
+
+def test_many_writes_loop(oracle_lib):
+    """The loop variant (no static bound on the stores of an interval):
+    work-item t writes A[64t + j] := j - t for j < 40 + 30 (t mod 3); when
+    the count exceeds 64 (t mod 3 = 1, 2) its last cells are t+1's first:
+    WW_NONBENIGN (t, t+1) there; after the barrier each reads A[64t + 39]
+    (no writer in that interval: clean)."""
+    n = 7
+    p = K.program(K.MANY_WRITES_LOOP)
+    A = np.full((1, 64 * n + 64), -7, np.int32)
+    r = oracle_lib.run(p.bytecode, n, [A])
+    want = []
+    for t in range(n - 1):
+        cnt = 40 + 30 * (t % 3)
+        for j in range(64, cnt):
+            want.append((0, 0, 0, 64 * t + j, 3, t, t + 1, 0xA))
+    assert r.report_tuples() == want
+    fin = r.final[0][0]
+    for t in range(n):
+        cnt = 40 + 30 * (t % 3)
+        for j in range(cnt):
+            c = 64 * t + j
+            if j >= 64 and t + 1 < n:
+                assert fin[c] == (j - 64) - (t + 1)
+            else:
+                assert fin[c] == j - t

@@ -308,3 +308,48 @@ def random_tiny_kernel(rng: np.random.Generator, n_arrays: int = 2, n_regs: int 
             body.append(f"    addi r{int(rng.integers(2, n_regs)) if n_regs > 2 else 2}, r0, {int(rng.integers(-2, 3))}")
     lines += body + ["    exit"]
     return assemble("\n".join(lines))
+
+
+# --- Many distinct writes per work-item per interval (PAPER.md:176-179 puts no
+#     bound on them; the own-write overlay's capacity must not be semantic):
+#     work-item t writes A[64t + j] := 1000 t + j for j = 0..69 (its last 6
+#     cells are the first 6 of t+1), then reads back A[64t+3], A[64t+40] and
+#     A[64t+66] (its own writes) and stores B[t] := their sum.
+def many_writes_kernel(per_item: int = 64, extra: int = 6) -> Program:
+    lines = [".arrays A B", "    tid r0", f"    const r1, {per_item}", "    mul r2, r0, r1",
+             "    const r3, 1000", "    mul r3, r0, r3"]
+    for j in range(per_item + extra):
+        lines += [f"    addi r4, r2, {j}", f"    addi r5, r3, {j}", "    st A, r4, r5"]
+    lines += ["    addi r4, r2, 3", "    ld r6, A, r4", "    addi r4, r2, 40", "    ld r7, A, r4",
+              f"    addi r4, r2, {per_item + 2}", "    ld r8, A, r4", "    add r6, r6, r7", "    add r6, r6, r8",
+              "    st B, r0, r6", "    exit"]
+    return assemble("\n".join(lines))
+
+
+# the same with a loop (no static bound on the stores of an interval):
+# work-item t writes A[t*stride + j] := j - t for j = 0 .. count-1, count =
+# 40 + 30 (t mod 3); then a barrier and a read of A[t*stride + 39]
+MANY_WRITES_LOOP = """
+.arrays A
+    tid   r0
+    const r1, 3
+    mod   r2, r0, r1
+    const r1, 30
+    mul   r2, r2, r1
+    addi  r2, r2, 40       ; count
+    const r1, 64
+    mul   r3, r0, r1       ; base
+    const r4, 0            ; j
+loop:
+    add   r5, r3, r4
+    sub   r6, r4, r0
+    st    A, r5, r6        ; A[base + j] := j - t
+    addi  r4, r4, 1
+    lt    r7, r4, r2
+    br    r7, loop, done
+done:
+    bar
+    addi  r5, r3, 39
+    ld    r6, A, r5
+    exit
+"""
