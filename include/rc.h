@@ -91,7 +91,13 @@ enum rc_opcode {
                        successor pair of the CFG)          */
   RC_OP_JMP = 25,   /* pc = imm                                              */
   RC_OP_EXIT = 26,  /* the `exit` node; implicit final barrier */
-  RC_OP_ADDI = 27   /* r[a] := r[b] + imm   (op(v, c) with a constant)      */
+  RC_OP_ADDI = 27,  /* r[a] := r[b] + imm   (op(v, c) with a constant)      */
+  /* work-groups ("both threads and work-groups have a unique
+     identifier ... threads can also query the size of the work-group";
+     DESIGN.md reading L20).  RC_OP_TID is the global id gid * LSIZE + lid. */
+  RC_OP_GID = 28,   /* r[a] := work-group id, 0 .. n_groups-1                  */
+  RC_OP_LID = 29,   /* r[a] := id inside the work-group, 0 .. LSIZE-1          */
+  RC_OP_LSIZE = 30  /* r[a] := work-group size (rc_run's work_group_size)      */
 };
 
 /* ---- report kinds -------------------------------------------------------- */
@@ -105,11 +111,20 @@ enum rc_kind {
   RC_FUEL = 7,         /* per-interval fuel exhausted (tid1=tid, index=pc), or
                           max_intervals reached (tid1=tid2=0xFFFFFFFF,
                           index=-1, interval=max_intervals)                 */
-  RC_BARRIER_DIVERGENCE = 8 /* arrived work-items at different barrier nodes
+  RC_BARRIER_DIVERGENCE = 8, /* arrived work-items at different barrier nodes
                           ("the same instruction barrier"); array=-1,
                           index = pc of tid1's BAR or -1 for exit; tid1 = min
                           arrived tid, tid2 = min arrived tid at another node */
+  /* inter-group races (options->n_groups > 1, reading L20): no
+     barrier orders two work-groups, so accesses of two work-items of
+     different groups to one cell, anywhere in the kernel, at least one a
+     write, race.  interval = RC_IG_INTERVAL, flags = 0, tid1 < tid2 global
+     ids of different groups, the lexicographically smallest such pair.    */
+  RC_IG_RW = 9,        /* one reads, the other writes                        */
+  RC_IG_WW_BENIGN = 10,/* both write; every group's last value of the cell equal */
+  RC_IG_WW_NONBENIGN = 11 /* both write; two groups' last values differ       */
 };
+#define RC_IG_INTERVAL 0xFFFFFFFFu
 
 /* 32-byte report.  Canonical order = ascending (instance, interval, array
  * (signed), index (signed), kind, tid1, tid2); the array returned by rc_run is
@@ -205,7 +220,10 @@ typedef struct {
   uint32_t flags;              /* RC_OPT_*                                     */
   void* cuda_stream;           /* cudaStream_t; NULL = legacy default stream  */
   uint32_t max_batch_instances;/* 0 = library chooses the instance batch      */
-  uint32_t reserved0;
+  uint32_t n_groups;           /* work-groups per instance (0 = 1), each of
+                                  work_group_size work-items; they run one
+                                  after another in ascending order on the
+                                  instance's heap (reading L20)              */
   rc_profile* profile;         /* nullable                                     */
 } rc_options;
 
@@ -224,7 +242,8 @@ RC_API int rc_program_info(const rc_program* prog, uint32_t* n_regs, uint32_t* n
                     uint32_t* n_instr);
 
 /* Run `prog` with `work_group_size` work-items (tids 0..n-1) on each of
- * `n_instances` instances.  `arrays` has exactly the program's n_arrays
+ * `n_instances` instances (with options->n_groups = G > 1: G work-groups of
+ * `work_group_size` work-items each, global tids 0..G*n-1, see RC_OP_GID).  `arrays` has exactly the program's n_arrays
  * entries.  Reports go to the HOST buffer `out` (caller-owned, `capacity`
  * entries, may be NULL when capacity == 0) in canonical order;
  * *n_reports_total is always set (nullable).  `stats` (host, nullable).

@@ -38,7 +38,8 @@
 enum {
   O_CONST = 1, O_MOV, O_TID, O_SIZE, O_ADD, O_SUB, O_MUL, O_DIV, O_MOD, O_MIN,
   O_MAX, O_AND, O_OR, O_XOR, O_LT, O_EQ, O_LAND, O_LNOT, O_LD, O_ST, O_BAR,
-  O_ASSUME, O_ASSERT, O_BR, O_JMP, O_EXIT, O_ADDI
+  O_ASSUME, O_ASSERT, O_BR, O_JMP, O_EXIT, O_ADDI,
+  O_GID, O_LID, O_LSIZE  /* work-group id, local id, work-group size (reading L20) */
 };
 
 typedef struct { uint8_t op, a, b, c; int32_t imm; } oins;
@@ -71,7 +72,12 @@ typedef struct {
   uint32_t reserved;
 } orep;
 
-enum { K_RW = 1, K_WWB = 2, K_WWN = 3, K_OOB = 4, K_ASSERT = 5, K_DIV0 = 6, K_FUEL = 7, K_DIV = 8 };
+enum { K_RW = 1, K_WWB = 2, K_WWN = 3, K_OOB = 4, K_ASSERT = 5, K_DIV0 = 6, K_FUEL = 7, K_DIV = 8,
+       K_IG_RW = 9, K_IG_WWB = 10, K_IG_WWN = 11 /* inter-group races (reading L20) */ };
+#define IG_INTERVAL 0xFFFFFFFFu /* inter-group reports concern the whole kernel */
+
+/* the work-group a work-item belongs to (reading L20): tids base .. base+lsize-1 */
+typedef struct { uint32_t base, gid, lsize; } ogroup;
 #define NOTID 0xFFFFFFFFu
 
 typedef struct { orep* v; size_t n, cap; } replist;
@@ -110,13 +116,16 @@ static int32_t w_mod(int32_t x, int32_t y) { if (y == -1) return 0; return x % y
 /* Outcome of one ALU/control instruction that does not touch shared memory.
  * Returns 1 if handled (regs/pc updated), 0 if the instruction is a memory,
  * barrier or termination instruction the caller must handle. */
-static int step_private(const oprog* P, const oins* I, int32_t* r, uint32_t tid,
+static int step_private(const oprog* P, const oins* I, int32_t* r, uint32_t t, const ogroup* G,
                         const uint32_t* sizes, uint32_t* pc, int* fault) {
   *fault = 0;
   switch (I->op) {
     case O_CONST: r[I->a] = I->imm; break;
     case O_MOV: r[I->a] = r[I->b]; break;
-    case O_TID: r[I->a] = (int32_t)tid; break;
+    case O_TID: r[I->a] = (int32_t)(G->base + t); break; /* global id = gid * lsize + lid */
+    case O_GID: r[I->a] = (int32_t)G->gid; break;
+    case O_LID: r[I->a] = (int32_t)t; break;
+    case O_LSIZE: r[I->a] = (int32_t)G->lsize; break;
     case O_SIZE: r[I->a] = (int32_t)sizes[I->b]; break;
     case O_ADD: r[I->a] = w_add(r[I->b], r[I->c]); break;
     case O_SUB: r[I->a] = w_sub(r[I->b], r[I->c]); break;
@@ -172,6 +181,7 @@ typedef struct {
   uint64_t fuel; uint32_t max_intervals;
   int32_t* const* final_heaps;
   int classify;
+  uint32_t n_groups; /* work-groups per instance, each of n work-items (reading L20) */
   /* per-thread results */
   int next_instance; pthread_mutex_t mu;
 } runctx;
@@ -185,16 +195,17 @@ typedef struct { replist reps; ostats st; } thread_out;
  * c sees the work-item's own earlier write, else snap[c] — or alt[c] when
  * altmask[c] is set (the second visibility of the RW value classification,
  * DESIGN.md §3; NULL in the canonical run). */
-static void exec_thread(const oprog* P, uint32_t t, const uint32_t* sizes, int32_t* r, uint32_t* pc,
+static void exec_thread(const oprog* P, uint32_t t, const ogroup* G, const uint32_t* sizes, int32_t* r, uint32_t* pc,
                         uint8_t* status, int32_t* node, uint8_t* arrived, int32_t* const* snap,
                         int32_t* const* alt, uint8_t* const* altmask, uint64_t fuel, uint32_t inst_global,
                         uint32_t k, replist* reps, ostats* st, acclist* log, ownw** ownp, size_t* own_cap) {
   ownw* own = *ownp;
   size_t n_own = 0;
   uint64_t steps = 0;
+  const uint32_t tg = G->base + t; /* the work-item's (global) tid in reports and the log */
   for (;;) {
     if (steps == fuel) { /* fuel exhausted (reading L17) */
-      rep_push(reps, mkrep(inst_global, k, -1, (int32_t)pc[t], t, NOTID, K_FUEL, 0));
+      rep_push(reps, mkrep(inst_global, k, -1, (int32_t)pc[t], tg, NOTID, K_FUEL, 0));
       status[t] = S_FUEL; break;
     }
     steps++;
@@ -202,9 +213,9 @@ static void exec_thread(const oprog* P, uint32_t t, const uint32_t* sizes, int32
     const oins* I = &P->code[pc[t]];
     st->op_count[I->op & 31]++;
     int fault;
-    if (step_private(P, I, r, t, sizes, &pc[t], &fault)) {
+    if (step_private(P, I, r, t, G, sizes, &pc[t], &fault)) {
       if (fault == S_DIV0) {
-        rep_push(reps, mkrep(inst_global, k, -1, (int32_t)pc[t], t, NOTID, K_DIV0, 0));
+        rep_push(reps, mkrep(inst_global, k, -1, (int32_t)pc[t], tg, NOTID, K_DIV0, 0));
         status[t] = S_DIV0; break;
       }
       continue;
@@ -212,13 +223,13 @@ static void exec_thread(const oprog* P, uint32_t t, const uint32_t* sizes, int32
     if (I->op == O_LD) { /* v := a[w]   (reading L11) */
       int32_t idx = r[I->c];
       if (idx < 0 || (uint32_t)idx >= sizes[I->b]) { /* ⊥: not performed, not logged (L5) */
-        rep_push(reps, mkrep(inst_global, k, I->b, idx, t, NOTID, K_OOB, 0));
+        rep_push(reps, mkrep(inst_global, k, I->b, idx, tg, NOTID, K_OOB, 0));
         status[t] = S_OOB; break;
       }
       int32_t v = (altmask && altmask[I->b][idx]) ? alt[I->b][idx] : snap[I->b][idx];
       for (size_t j = 0; j < n_own; j++)
         if (own[j].arr == I->b && own[j].idx == idx) v = own[j].val; /* own earlier write */
-      acc a = {I->b, idx, t, 0, 0};
+      acc a = {I->b, idx, tg, 0, 0};
       acc_push(log, a);
       st->checked++; st->loads++;
       r[I->a] = v;
@@ -226,7 +237,7 @@ static void exec_thread(const oprog* P, uint32_t t, const uint32_t* sizes, int32
     } else if (I->op == O_ST) { /* a[v] := e */
       int32_t idx = r[I->b];
       if (idx < 0 || (uint32_t)idx >= sizes[I->a]) {
-        rep_push(reps, mkrep(inst_global, k, I->a, idx, t, NOTID, K_OOB, 0));
+        rep_push(reps, mkrep(inst_global, k, I->a, idx, tg, NOTID, K_OOB, 0));
         status[t] = S_OOB; break;
       }
       size_t j;
@@ -248,7 +259,7 @@ static void exec_thread(const oprog* P, uint32_t t, const uint32_t* sizes, int32
       pc[t]++;
     } else if (I->op == O_ASSERT) { /* false -> ⊥ */
       if (r[I->a] == 0) {
-        rep_push(reps, mkrep(inst_global, k, -1, (int32_t)pc[t], t, NOTID, K_ASSERT, 0));
+        rep_push(reps, mkrep(inst_global, k, -1, (int32_t)pc[t], tg, NOTID, K_ASSERT, 0));
         status[t] = S_ASSERT; break;
       }
       pc[t]++;
@@ -258,7 +269,7 @@ static void exec_thread(const oprog* P, uint32_t t, const uint32_t* sizes, int32
   }
   /* the work-item's writes of this interval, one per cell, final value (L3) */
   for (size_t j = 0; j < n_own; j++) {
-    acc a = {own[j].arr, own[j].idx, t, 1, own[j].val};
+    acc a = {own[j].arr, own[j].idx, tg, 1, own[j].val};
     acc_push(log, a);
   }
 }
@@ -268,11 +279,11 @@ static void exec_thread(const oprog* P, uint32_t t, const uint32_t* sizes, int32
  * copied out (used to seed the enumerator); returns 1 if that interval is
  * reached, 0 otherwise.  classify: RW value classification of every interval
  * with an RW report. */
-static int run_instance(const oprog* P, uint32_t n, const uint32_t* sizes, int32_t** heap,
+static int run_instance(const oprog* P, uint32_t n, const ogroup* G, const uint32_t* sizes, int32_t** heap,
                         uint32_t inst_global, uint64_t fuel, uint32_t max_intervals,
                         replist* reps, ostats* st, int stop_at,
                         int32_t* out_regs, uint32_t* out_pc, uint8_t* out_status, uint64_t* out_intervals,
-                        int classify) {
+                        int classify, acclist* glog) {
   uint32_t A = P->n_arrays, R = P->n_regs;
   int32_t* regs = (int32_t*)calloc((size_t)n * R + 1, sizeof(int32_t)); /* registers start at 0 (L18) */
   uint32_t* pc = (uint32_t*)calloc(n + 1, sizeof(uint32_t));              /* start = pc 0 */
@@ -309,11 +320,13 @@ static int run_instance(const oprog* P, uint32_t n, const uint32_t* sizes, int32
     memset(arrived, 0, n);
     for (uint32_t t = 0; t < n; t++) {
       if (status[t] != S_RUNNING) continue;
-      exec_thread(P, t, sizes, regs + (size_t)t * R, pc, status, node, arrived, snap, NULL, NULL, fuel,
+      exec_thread(P, t, G, sizes, regs + (size_t)t * R, pc, status, node, arrived, snap, NULL, NULL, fuel,
                   inst_global, k, reps, st, &log, &own, &own_cap);
     }
 
     const size_t rep_mark = reps->n;  /* reports of this interval start here */
+    if (glog) /* every access of the group, all intervals (inter-group races, reading L20) */
+      for (size_t i = 0; i < log.n; i++) acc_push(glog, log.v[i]);
     /* race rule per cell (PAPER.md:224-229 as reading L1), in (array,index) order */
     qsort(log.v, log.n, sizeof(acc), acc_cmp);
     size_t g = 0;
@@ -395,7 +408,7 @@ static int run_instance(const oprog* P, uint32_t n, const uint32_t* sizes, int32
         acclist logB = {0};
         for (uint32_t t = 0; t < n; t++) {
           if (sB[t] != S_RUNNING) continue;
-          exec_thread(P, t, sizes, rB + (size_t)t * R, pB, sB, nodeB, arrB, snap, heap, mask, fuel,
+          exec_thread(P, t, G, sizes, rB + (size_t)t * R, pB, sB, nodeB, arrB, snap, heap, mask, fuel,
                       inst_global, k, &junk, &junk_st, &logB, &own, &own_cap);
         }
         for (uint32_t a = 0; a < A; a++) memcpy(heapB[a], snap[a], (size_t)sizes[a] * sizeof(int32_t));
@@ -419,7 +432,7 @@ static int run_instance(const oprog* P, uint32_t n, const uint32_t* sizes, int32
       if (t1 >= 0) {
         for (uint32_t t = (uint32_t)t1 + 1; t < n; t++)
           if (arrived[t] && node[t] != node[t1]) {
-            rep_push(reps, mkrep(inst_global, k, -1, node[t1], (uint32_t)t1, t, K_DIV, 0));
+            rep_push(reps, mkrep(inst_global, k, -1, node[t1], G->base + (uint32_t)t1, G->base + t, K_DIV, 0));
             break;
           }
       }
@@ -463,6 +476,56 @@ static int run_instance(const oprog* P, uint32_t n, const uint32_t* sizes, int32
 
 typedef struct { runctx* ctx; thread_out out; } worker_arg;
 
+/* one group's last written value of a cell (reading L20) */
+typedef struct { uint32_t arr; int32_t idx; uint32_t g; int32_t val; } lastv;
+static int lastv_cmp(const void* x, const void* y) {
+  const lastv* a = (const lastv*)x; const lastv* b = (const lastv*)y;
+  if (a->arr != b->arr) return a->arr < b->arr ? -1 : 1;
+  if (a->idx != b->idx) return a->idx < b->idx ? -1 : 1;
+  if (a->g != b->g) return a->g < b->g ? -1 : 1;
+  return 0;
+}
+
+/* Inter-group races of one instance (reading L20): no barrier orders two
+ * work-groups, so two work-items of different groups that touch the same cell
+ * anywhere in the kernel, at least one writing, race.  Per cell, plainly:
+ *   IG_RW: lexicographically smallest (t1 < t2), different groups, one reads
+ *          and the other writes;
+ *   IG_WW: smallest (t1 < t2), different groups, both write; non-benign iff
+ *          two groups' last written values differ (the final value of a
+ *          write-only cell is the last value of whichever group writes last);
+ * interval = IG_INTERVAL, flags 0.  log: every access of every group (tids
+ * global); lv: per group and written cell its last value. */
+static void inter_group_reports(acclist* log, lastv* lv, size_t nlv, uint32_t lsize, uint32_t inst_global,
+                                replist* reps) {
+  qsort(log->v, log->n, sizeof(acc), acc_cmp);
+  qsort(lv, nlv, sizeof(lastv), lastv_cmp);
+  size_t g = 0, q = 0;
+  while (g < log->n) {
+    size_t e = g;
+    while (e < log->n && log->v[e].cell_arr == log->v[g].cell_arr && log->v[e].idx == log->v[g].idx) e++;
+    const uint32_t arr = log->v[g].cell_arr; const int32_t idx = log->v[g].idx;
+    /* every access pair (x, y) of the cell, plain O(m^2) */
+    uint32_t rw1 = NOTID, rw2 = NOTID, ww1 = NOTID, ww2 = NOTID;
+    for (size_t x = g; x < e; x++)
+      for (size_t y = g; y < e; y++) {
+        const acc* A = &log->v[x]; const acc* B = &log->v[y];
+        if (!(A->tid < B->tid) || A->tid / lsize == B->tid / lsize) continue;
+        if (A->w != B->w && (A->tid < rw1 || (A->tid == rw1 && B->tid < rw2))) { rw1 = A->tid; rw2 = B->tid; }
+        if (A->w && B->w && (A->tid < ww1 || (A->tid == ww1 && B->tid < ww2))) { ww1 = A->tid; ww2 = B->tid; }
+      }
+    if (rw1 != NOTID) rep_push(reps, mkrep(inst_global, IG_INTERVAL, (int32_t)arr, idx, rw1, rw2, K_IG_RW, 0));
+    if (ww1 != NOTID) {
+      while (q < nlv && (lv[q].arr < arr || (lv[q].arr == arr && lv[q].idx < idx))) q++;
+      int differ = 0;
+      for (size_t j = q; j < nlv && lv[j].arr == arr && lv[j].idx == idx; j++)
+        if (lv[j].val != lv[q].val) differ = 1;
+      rep_push(reps, mkrep(inst_global, IG_INTERVAL, (int32_t)arr, idx, ww1, ww2, differ ? K_IG_WWN : K_IG_WWB, 0));
+    }
+    g = e;
+  }
+}
+
 static void* worker(void* p) {
   worker_arg* W = (worker_arg*)p;
   runctx* c = W->ctx;
@@ -476,8 +539,28 @@ static void* worker(void* p) {
     if (i >= (int)c->n_instances) break;
     for (uint32_t a = 0; a < P->n_arrays; a++)  /* heap <- copy(inputs[inst]) */
       memcpy(heap[a], c->inputs[a] + (size_t)i * c->sizes[a], (size_t)c->sizes[a] * sizeof(int32_t));
-    run_instance(P, c->n, c->sizes, heap, c->instance_offset + (uint32_t)i, c->fuel, c->max_intervals,
-                 &W->out.reps, &W->out.st, -1, NULL, NULL, NULL, NULL, c->classify);
+    /* the work-groups one after another in ascending order (reading L20):
+     * each runs the paper's semantics on the heap the previous ones left */
+    acclist glog = {0}, gone = {0};
+    lastv* lv = NULL; size_t nlv = 0, lvcap = 0;
+    for (uint32_t gi = 0; gi < c->n_groups; gi++) {
+      const ogroup G = {gi * c->n, gi, c->n};
+      gone.n = 0;
+      run_instance(P, c->n, &G, c->sizes, heap, c->instance_offset + (uint32_t)i, c->fuel, c->max_intervals,
+                   &W->out.reps, &W->out.st, -1, NULL, NULL, NULL, NULL, c->classify,
+                   c->n_groups > 1 ? &gone : NULL);
+      for (size_t j = 0; j < gone.n; j++) {
+        acc_push(&glog, gone.v[j]);
+        if (!gone.v[j].w) continue;
+        /* a cell this group wrote: its value now is the group's last (committed) one */
+        if (nlv == lvcap) { lvcap = lvcap ? 2 * lvcap : 256; lv = (lastv*)realloc(lv, lvcap * sizeof(lastv)); }
+        lv[nlv].arr = gone.v[j].cell_arr; lv[nlv].idx = gone.v[j].idx; lv[nlv].g = gi;
+        lv[nlv].val = heap[gone.v[j].cell_arr][gone.v[j].idx];
+        nlv++;
+      }
+    }
+    if (c->n_groups > 1) inter_group_reports(&glog, lv, nlv, c->n, c->instance_offset + (uint32_t)i, &W->out.reps);
+    free(glog.v); free(gone.v); free(lv);
     if (c->final_heaps)
       for (uint32_t a = 0; a < P->n_arrays; a++)
         if (c->final_heaps[a])
@@ -497,7 +580,8 @@ static void* worker(void* p) {
 int oracle_run(const uint8_t* bc, size_t nbytes, uint32_t n, const uint32_t* sizes,
                const int32_t* const* inputs, uint32_t n_instances, uint32_t instance_offset,
                uint64_t fuel, uint32_t max_intervals, int n_threads,
-               orep** reports, uint64_t* n_reports, int32_t* const* final_heaps, uint64_t* stats, int classify) {
+               orep** reports, uint64_t* n_reports, int32_t* const* final_heaps, uint64_t* stats, int classify,
+               uint32_t n_groups) {
   oprog P;
   if (decode(bc, nbytes, &P)) return -1;
   runctx c;
@@ -506,6 +590,7 @@ int oracle_run(const uint8_t* bc, size_t nbytes, uint32_t n, const uint32_t* siz
   c.instance_offset = instance_offset; c.fuel = fuel; c.max_intervals = max_intervals;
   c.final_heaps = final_heaps;
   c.classify = classify;
+  c.n_groups = n_groups ? n_groups : 1;
   pthread_mutex_init(&c.mu, NULL);
   if (n_threads < 1) n_threads = 1;
   worker_arg* W = (worker_arg*)calloc((size_t)n_threads, sizeof(worker_arg));
@@ -553,8 +638,9 @@ int oracle_state_at(const uint8_t* bc, size_t nbytes, uint32_t n, const uint32_t
     memcpy(heap[a], inputs[a], (size_t)sizes[a] * sizeof(int32_t));
   }
   replist reps = {0}; ostats st; memset(&st, 0, sizeof st);
-  int reached = run_instance(&P, n, sizes, heap, 0, fuel, 0xFFFFFFFFu, &reps, &st, (int)k,
-                             regs_out, pc_out, status_out, NULL, 0);
+  const ogroup G = {0, 0, n}; /* (work-group 0) */
+  int reached = run_instance(&P, n, &G, sizes, heap, 0, fuel, 0xFFFFFFFFu, &reps, &st, (int)k,
+                             regs_out, pc_out, status_out, NULL, 0, NULL);
   size_t off = 0;
   for (uint32_t a = 0; a < P.n_arrays; a++) {
     memcpy(heap_out + off, heap[a], (size_t)sizes[a] * sizeof(int32_t));
@@ -634,7 +720,8 @@ static void enum_step(enumctx* E, int32_t* s, uint32_t t) {
   L[2] = (int32_t)(uint32_t)steps; L[3] = (int32_t)(uint32_t)(steps >> 32);
   const oins* I = &P->code[*pc];
   int fault;
-  if (step_private(P, I, r, t, E->sizes, pc, &fault)) { if (fault) *st = fault; return; }
+  const ogroup G = {0, 0, E->n}; /* the enumerator explores one work-group (group 0) */
+  if (step_private(P, I, r, t, &G, E->sizes, pc, &fault)) { if (fault) *st = fault; return; }
   size_t base = 0;
   switch (I->op) {
     case O_LD: {

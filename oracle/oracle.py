@@ -21,6 +21,7 @@ _lib = None
 REPORT_DTYPE = np.dtype([("instance", "<u4"), ("interval", "<u4"), ("array", "<i4"), ("index", "<i4"),
                          ("tid1", "<u4"), ("tid2", "<u4"), ("kind", "<u2"), ("flags", "<u2"),
                          ("reserved", "<u4")])
+IG_INTERVAL = 0xFFFFFFFF  # interval field of the inter-group reports (kinds 9-11, reading L20)
 STATUS = {"RUNNING": 0, "WAITING": 1, "EXITED": 2, "PRUNED": 3, "OOB": 4, "ASSERT": 5, "DIV0": 6, "FUEL": 7}
 STAT_NAMES = ["checked_accesses", "loads", "stores", "instructions", "intervals_max"] + \
     [f"lanes_final{i}" for i in range(8)]
@@ -41,7 +42,8 @@ def _load():
         P = C.POINTER
         lib.oracle_run.argtypes = [C.c_char_p, C.c_size_t, C.c_uint32, P(C.c_uint32), P(P(C.c_int32)),
                                    C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_int,
-                                   P(C.c_void_p), P(C.c_uint64), P(P(C.c_int32)), P(C.c_uint64), C.c_int]
+                                   P(C.c_void_p), P(C.c_uint64), P(P(C.c_int32)), P(C.c_uint64), C.c_int,
+                                   C.c_uint32]
         lib.oracle_run.restype = C.c_int
         lib.oracle_free.argtypes = [C.c_void_p]
         lib.oracle_state_at.argtypes = [C.c_char_p, C.c_size_t, C.c_uint32, P(C.c_uint32), P(P(C.c_int32)),
@@ -84,9 +86,10 @@ DEFAULT_MAX_INTERVALS = 65536
 
 def run(bytecode: bytes, n: int, inputs: list[np.ndarray], *, instance_offset: int = 0,
         fuel: int = DEFAULT_FUEL, max_intervals: int = DEFAULT_MAX_INTERVALS, threads: int | None = None,
-        want_final: bool = True, classify_rw: bool = False) -> Result:
+        want_final: bool = True, classify_rw: bool = False, n_groups: int = 1) -> Result:
     """Run the canonical algorithm.  inputs[a] has shape [n_instances, size(a)].
-    classify_rw: RW value classification flags (bit 4 / bit 5) on the RW reports."""
+    classify_rw: RW value classification flags (bit 4 / bit 5) on the RW reports.
+    n_groups: work-groups per instance, each of n work-items (reading L20)."""
     lib = _load()
     _, n_arrays = _header(bytecode)
     assert len(inputs) == n_arrays, (len(inputs), n_arrays)
@@ -103,7 +106,7 @@ def run(bytecode: bytes, n: int, inputs: list[np.ndarray], *, instance_offset: i
         threads = max(1, min(len(os.sched_getaffinity(0)), n_inst))
     rc = lib.oracle_run(bytecode, len(bytecode), n, _ptr(sizes, C.c_uint32), in_ptrs, n_inst, instance_offset,
                         fuel, max_intervals, threads, C.byref(rep_p), C.byref(n_rep), fin_ptrs,
-                        _ptr(stats, C.c_uint64), 1 if classify_rw else 0)
+                        _ptr(stats, C.c_uint64), 1 if classify_rw else 0, n_groups)
     if rc != 0:
         raise ValueError("oracle: bytecode decode failed")
     nr = n_rep.value

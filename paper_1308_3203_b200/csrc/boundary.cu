@@ -91,8 +91,8 @@ __global__ void div_report_kernel(const BoundaryParams p) {
   r.interval = p.interval;
   r.array = -1;
   r.index = n1;
-  r.tid1 = t1;
-  r.tid2 = p.second_tid[inst];
+  r.tid1 = p.gbase + t1;  // global ids (reading L20)
+  r.tid2 = p.gbase + p.second_tid[inst];
   r.kind = RC_BARRIER_DIVERGENCE;
   r.flags = 0;
   r.reserved = 0;

@@ -38,10 +38,11 @@ __device__ __noinline__ int32_t spilled_val(const DetectParams& p, uint64_t r) {
     if (p.spill_cell[(size_t)j * p.n_lanes + lane] == cell) return p.spill_val[(size_t)j * p.n_lanes + lane];
   return 0;  // unreachable: K1 wrote the record from this list
 }
+template <bool SPILL>
 __device__ __forceinline__ int32_t rec_val(const DetectParams& p, uint64_t r) {
   // slot * n_lanes + lane < 15 * 2^27: 32-bit index arithmetic
   const uint32_t slot = ((uint32_t)r >> 1) & 0xF;
-  if (slot == SLOT_SPILL) return spilled_val(p, r);
+  if (SPILL && slot == SLOT_SPILL) return spilled_val(p, r);
   return __ldg(p.wval + (slot * p.n_lanes + rec_tid(r)));
 }
 
@@ -51,8 +52,8 @@ __device__ __forceinline__ void emit(const DetectParams& p, uint32_t cell, uint3
   if (kind == RC_RW) atomicAdd(&p.ctr->rw_reports, 1ull);
   const uint32_t inst = fast_div(cell, p.cpi_magic);
   const uint32_t rem = cell - inst * p.cpi;
-  t1 -= inst * p.n;  // batch lanes -> tids
-  if (t2 != INF) t2 -= inst * p.n;
+  t1 = t1 - inst * p.n + p.gbase;  // batch lanes -> (global) tids
+  if (t2 != INF) t2 = t2 - inst * p.n + p.gbase;
   uint32_t a = 0;
   while (a + 1 < p.n_arrays && __ldg(p.arr_off + a + 1) <= rem) a++;
   unsigned long long pos = atomicAdd(&p.ctr->report_count, 1ull);
@@ -113,7 +114,7 @@ __device__ __noinline__ void serial_segment(const DetectParams& p, uint32_t i, u
     const uint64_t v = __ldg(p.recs + end);
     const uint32_t tid = rec_tid(v);
     if (rec_w(v)) {
-      const int32_t val = rec_val(p, v);
+      const int32_t val = rec_val<true>(p, v);
       if (tid < w1) { w2 = w1; w1 = tid; vw1 = val; }
       else if (tid < w2) w2 = tid;
       if (nw == 0 || tid > wmax) { wmax = tid; vwmax = val; }
@@ -137,7 +138,7 @@ __device__ __noinline__ void serial_segment(const DetectParams& p, uint32_t i, u
     const uint64_t v = __ldg(p.recs + j);
     const uint32_t tid = rec_tid(v);
     if (rec_w(v)) {
-      if (rec_val(p, v) != vw1 && tid < nb) nb = tid;
+      if (rec_val<true>(p, v) != vw1 && tid < nb) nb = tid;
       t2w |= tid == t2;
     } else {
       t1r |= tid == t1;
@@ -218,24 +219,38 @@ __device__ __forceinline__ Seg seg_shfl(const Seg& a, int src) {
 // round; one that crosses the chunk end, and every COMPLEX cell, is handled by
 // serial_segment from the segment's head.  Segments that start before the
 // chunk belong to the previous warp.
-__device__ __forceinline__ void detect_chunk(const DetectParams& p, uint64_t wg, uint32_t n_records) {
-  const unsigned FULL = 0xFFFFFFFFu;
+// The records of chunk wg (and its two boundary keys), issued as independent
+// loads: the caller fetches the next chunk while it processes this one.
+struct Chunk {
+  uint64_t vr[DET_ROUNDS];
+  uint32_t key_before, key_after;
+};
+__device__ __forceinline__ void load_chunk(const DetectParams& p, uint64_t wg, uint32_t n_records, Chunk& ch) {
   const int lane = threadIdx.x & 31;
   // record indices are < 2^32 (n_records is): 32-bit index arithmetic
   const uint32_t c0 = (uint32_t)wg * DET_CHUNK;
   const uint32_t c1 = min(n_records, c0 + DET_CHUNK);
-  // ---- prefetch the chunk
-  uint64_t vr[DET_ROUNDS];
-  int32_t wv[DET_ROUNDS];
 #pragma unroll
   for (int rd = 0; rd < (int)DET_ROUNDS; rd++) {
     const uint32_t r = c0 + rd * 32 + lane;
-    vr[rd] = r < c1 ? __ldg(p.recs + r) : ~0ull;
+    ch.vr[rd] = r < c1 ? __ldg(p.recs + r) : ~0ull;
   }
-  const uint32_t key_before = c0 > 0 ? rec_cell(__ldg(p.recs + c0 - 1)) : 0xFFFFFFFFu;
-  const uint32_t key_after = c1 < n_records ? rec_cell(__ldg(p.recs + c1)) : 0xFFFFFFFFu;
+  ch.key_before = c0 > 0 ? rec_cell(__ldg(p.recs + c0 - 1)) : 0xFFFFFFFFu;
+  ch.key_after = c1 < n_records ? rec_cell(__ldg(p.recs + c1)) : 0xFFFFFFFFu;
+}
+
+template <bool SPILL>
+__device__ __forceinline__ void detect_chunk(const DetectParams& p, uint64_t wg, uint32_t n_records, const Chunk& ch) {
+  const unsigned FULL = 0xFFFFFFFFu;
+  const int lane = threadIdx.x & 31;
+  const uint32_t c0 = (uint32_t)wg * DET_CHUNK;
+  const uint32_t c1 = min(n_records, c0 + DET_CHUNK);
+  const uint64_t(&vr)[DET_ROUNDS] = ch.vr;
+  const uint32_t key_before = ch.key_before, key_after = ch.key_after;
+  // final values of the chunk's write records (all gathers in flight at once)
+  int32_t wv[DET_ROUNDS];
 #pragma unroll
-  for (int rd = 0; rd < (int)DET_ROUNDS; rd++) wv[rd] = (vr[rd] != ~0ull && rec_w(vr[rd])) ? rec_val(p, vr[rd]) : 0;
+  for (int rd = 0; rd < (int)DET_ROUNDS; rd++) wv[rd] = (vr[rd] != ~0ull && rec_w(vr[rd])) ? rec_val<SPILL>(p, vr[rd]) : 0;
 
   const Seg ident{INF, 0u, 0u, 0, 0u};
   bool carry = false;       // an open segment started in an earlier round of this chunk
@@ -370,14 +385,21 @@ __device__ __forceinline__ void boundary_tail(const DetectParams& p) {
 // device memory (no host sync).  Skips the detection (no commit) when this
 // interval's log, a spill list or K1's reports overflowed: the host then
 // re-runs the interval from the saved lane state on an untouched heap.
+template <bool SPILL>
 __global__ void __launch_bounds__(256, DET_MINB) detect_kernel(const DetectParams p) {
   if (p.ctr->abort) return;  // speculative interval after one that needs the host (grid-uniform)
   if (!(p.ctr->log_overflow || p.ctr->ovl_overflow || p.ctr->k1_reports > p.report_cap)) {
     const uint32_t n_records = (uint32_t)p.ctr->kept_count;
     const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wg * DET_CHUNK < n_records;
-         wg += warps)
-      detect_chunk(p, wg, n_records);
+    uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    Chunk cur, nxt;
+    if (wg * DET_CHUNK < n_records) load_chunk(p, wg, n_records, cur);
+    for (; wg * DET_CHUNK < n_records; wg += warps) {
+      // software pipeline: the next chunk's records load while this one is processed
+      if ((wg + warps) * DET_CHUNK < n_records) load_chunk(p, wg + warps, n_records, nxt);
+      detect_chunk<SPILL>(p, wg, n_records, cur);
+      cur = nxt;
+    }
   }
   __syncwarp();
   if (p.with_boundary) boundary_tail(p);
@@ -437,7 +459,7 @@ cudaError_t launch_detect(const DetectParams& p, cudaStream_t s) {
   cudaError_t se = setup.run(
       [](int d) -> cudaError_t {
         int per_sm = 0;
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, detect_kernel, 256, 0);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, detect_kernel<false>, 256, 0);
         if (e != cudaSuccess) return e;
         per_sm_of[d] = std::max(per_sm, 1);
         return cudaDeviceGetAttribute(&nsm_of[d], cudaDevAttrMultiProcessorCount, d);
@@ -448,7 +470,8 @@ cudaError_t launch_detect(const DetectParams& p, cudaStream_t s) {
   // one resident wave (persistent warps stride over the chunks)
   const uint64_t warps = (p.n_records + DET_CHUNK - 1) / DET_CHUNK;  // upper bound
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((warps + 7) / 8, (uint64_t)nsm * per_sm));
-  detect_kernel<<<grid, 256, 0, s>>>(p);
+  if (p.spill_n) detect_kernel<true><<<grid, 256, 0, s>>>(p);  // (spill_n: set iff the program may spill)
+  else detect_kernel<false><<<grid, 256, 0, s>>>(p);
   launched();
   return cudaGetLastError();
 }

@@ -92,6 +92,10 @@ __device__ void step(const ExploreParams& p, int32_t* H, const Lane& L, uint32_t
     case RC_OP_CONST: L.r(I.a) = I.imm; break;
     case RC_OP_MOV: L.r(I.a) = L.r(I.b); break;
     case RC_OP_TID: L.r(I.a) = (int32_t)t; break;
+    // one work-group is explored (group 0 of p.n work-items, reading L20)
+    case RC_OP_GID: L.r(I.a) = 0; break;
+    case RC_OP_LID: L.r(I.a) = (int32_t)t; break;
+    case RC_OP_LSIZE: L.r(I.a) = (int32_t)p.n; break;
     case RC_OP_SIZE: L.r(I.a) = (int32_t)(p.arr_off[I.b + 1] - p.arr_off[I.b]); break;
     case RC_OP_ADDI: L.r(I.a) = wrap_add(L.r(I.b), I.imm); break;
     case RC_OP_ADD: case RC_OP_SUB: case RC_OP_MUL: case RC_OP_DIV: case RC_OP_MOD: case RC_OP_MIN:

@@ -87,7 +87,7 @@ __device__ __noinline__ void emit_report_(const InterpParams* pp, uint32_t inst,
     r.interval = pp->interval;
     r.array = arr;
     r.index = idx;
-    r.tid1 = t1;
+    r.tid1 = pp->gbase + t1;  // global id (work-group base + local id, reading L20)
     r.tid2 = NOTID;
     r.kind = (uint16_t)kind;
     r.flags = 0;
@@ -148,16 +148,6 @@ __device__ __noinline__ uint32_t flush_warp_(const LogOut p, const uint64_t* rec
   return 0;
 }
 
-#ifndef INTERP_CONV  // 1: converged-warp steps skip the minimum pc (parity-green, measured 15% slower)
-#define INTERP_CONV 0
-#endif
-#ifndef INTERP_INDEP  // 1: no block barrier in the tile loop (per-warp chunks and stores); measured 30% slower
-#define INTERP_INDEP 0
-#endif
-#ifndef STAGE_CHUNK_W_OPT
-#define STAGE_CHUNK_W_OPT 1024
-#endif
-[[maybe_unused]] constexpr uint32_t STAGE_CHUNK_W = STAGE_CHUNK_W_OPT;  // staging slots a warp reserves at a time (INTERP_INDEP)
 #ifndef STAGE_CHUNK_OPT
 #define STAGE_CHUNK_OPT 8192
 #endif
@@ -243,16 +233,25 @@ struct Dec {
   uint4 h;
   uint2 t;
 };
-__device__ __forceinline__ Dec predecode(uint2 raw, int T, const uint32_t* s_off, const uint32_t* s_size) {
-  const uint32_t op = raw.x & 0x7F, a = (raw.x >> 8) & 0xFF, b = (raw.x >> 16) & 0xFF, c = raw.x >> 24;
+// Work-group ids (reading L20) are launch constants: TID becomes "local id +
+// imm" with imm = the group's first global tid, LID the same with imm = 0,
+// GID and LSIZE become CONST.
+__device__ __forceinline__ Dec predecode(uint2 raw, int T, const uint32_t* s_off, const uint32_t* s_size,
+                                         const InterpParams& p) {
+  uint32_t op = raw.x & 0x7F;
+  const uint32_t a = (raw.x >> 8) & 0xFF, b = (raw.x >> 16) & 0xFF, c = raw.x >> 24;
   uint32_t aux = 0, z = raw.y, w = 0;
+  if (op == RC_OP_TID) { z = p.gbase; }
+  else if (op == RC_OP_LID) { op = RC_OP_TID; z = 0; }
+  else if (op == RC_OP_GID) { op = RC_OP_CONST; z = p.gid; }
+  else if (op == RC_OP_LSIZE) { op = RC_OP_CONST; z = p.n; }
   if (op == RC_OP_LD) { aux = b; z = s_off[b]; w = s_size[b]; }
   else if (op == RC_OP_ST) { aux = a; z = s_off[a]; w = s_size[a]; }
   else if (op == RC_OP_SIZE) { z = s_size[b]; }
   else if (op == RC_OP_BR) { w = b + 256u * c; }
   const uint32_t rb = 4u * (uint32_t)T;  // bytes per register row
   Dec d;
-  d.h = make_uint4((raw.x & 0xFF) | (aux << 8), a * rb, b * rb, c * rb);  // op keeps its OP_WAIT bit
+  d.h = make_uint4(op | (raw.x & OP_WAIT) | (aux << 8), a * rb, b * rb, c * rb);  // op keeps its OP_WAIT bit
   d.t = make_uint2(z, w);
   return d;
 }
@@ -291,7 +290,9 @@ void interp_phase_io(unsigned long long* out, bool reset) {
 // vote serve H lanes, and each lane's heap loads add to the memory-level
 // parallelism of the warp.
 // ALT: the RW-classification re-run (reads of alt_mask cells see alt_heap).
-template <bool CODE_SMEM, bool FUEL, int H, bool ALT>
+// SPILL: a work-item may write more distinct cells in one interval than the
+// shared-memory overlay holds (program.cpp may_spill): the spill-list paths.
+template <bool CODE_SMEM, bool FUEL, int H, bool ALT, bool SPILL>
 __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_BLOCKS_H)
     interp_kernel(const __grid_constant__ InterpParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -318,8 +319,7 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
 #define SREGS(b) (sregs0 + (size_t)(b) * R * TL)
 #define SPC(b) (spc0 + (size_t)(b) * TL)
 #define SSTAT(b) (sstat0 + (size_t)(b) * TL)
-  // mbar[0, LS_NB): lane state of a buffer landed (TMA); mbar[LS_NB + b]
-  // (INTERP_INDEP): every warp's bulk stores have read buffer b
+  // mbar[b]: the lane state of buffer b landed (TMA)
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(q); q += (16 * LS_NB + 15) & ~15;
   uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)W * SW * 8;
   uint4* s_code = reinterpret_cast<uint4*>(q); q += CODE_SMEM ? (size_t)(p.n_instr + 1) * 16 : 0;  // heads + pad entry
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
   __syncthreads();  // s_off / s_size before the pre-decode
   if (CODE_SMEM) {
     for (uint32_t i = t; i < p.n_instr; i += T) {
-      const Dec d = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + i), TL, s_off, s_size);
+      const Dec d = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + i), TL, s_off, s_size, p);
       s_code[i] = d.h;
       s_tail[i] = d.t;
       s_ro[i] = __ldg(p.entry_ro + i);
@@ -358,8 +358,6 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
   const uint32_t n_tiles = (p.n_lanes + TL - 1) / TL;
   if (t == 0) {
     for (int b = 0; b < LS_NB; b++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[b])));
-    for (int b = 0; b < LS_NB; b++)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar[LS_NB + b])), "r"(W));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -378,46 +376,18 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
   unsigned long long b_staged = 0;  // thread 0: records staged by the block
   uint32_t parity = 0;  // bit b: expected phase of mbar[b]
   int cur = 0;
-#if INTERP_INDEP
-  // every warp is independent inside the tile loop: its own staging chunk and
-  // its own lane-state bulk stores; buffer b is refilled only after all warps
-  // arrived on mbar[LS_NB + b] (their stores read it)
-  unsigned long long w_base = 0;  // this warp's staging chunk (warp-uniform)
-  uint32_t w_used = 0, w_cap = 0;
-  uint32_t eparity = 0;           // thread 0: expected phase of each empty barrier
-  uint32_t eused = 0;             // thread 0: buffers that held a tile before
-  int prev = -1;                  // buffer of this warp's previous tile
-#endif
 #ifdef INTERP_PHASE_TIMING
   long long tprev_ = clock64();
 #endif
   for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, cur = cur + 1 == LS_NB ? 0 : cur + 1) {
     // prefetch the next tile's lane state into the next buffer once the bulk
     // stores of its previous use (LS_NB - 1 tiles back) have read it
-#if INTERP_INDEP
-    // this warp's stores of its previous tile have read their buffer: say so
-    if (lane == 0 && prev >= 0) {
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&mbar[LS_NB + prev])) : "memory");
-    }
-    if (t == 0 && tile + gridDim.x < n_tiles) {
-      const int nx = cur + 1 == LS_NB ? 0 : cur + 1;
-      if ((eused >> nx) & 1u) {  // its previous tile's stores must be done
-        mbar_wait_parity(&mbar[LS_NB + nx], (eparity >> nx) & 1u);
-        eparity ^= 1u << nx;
-      }
-      eused |= 1u << nx;
-      prefetch_lanes(p, tile + gridDim.x, TL, SSTAT(nx), SPC(nx), SREGS(nx), s_live, &mbar[nx]);
-    }
-    if (t == 0) eused |= 1u << cur;
-#else
     if (t == 0 && tile + gridDim.x < n_tiles) {
       const int nx = cur + 1 == LS_NB ? 0 : cur + 1;
       if (LS_NB == 2) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       prefetch_lanes(p, tile + gridDim.x, TL, SSTAT(nx), SPC(nx), SREGS(nx), s_live, &mbar[nx]);
     }
-#endif
     IPHASE(0);
     // per-lane state, lane h*T + t of the tile
     uint32_t g[H], pc[H], inst[H], tid[H], cell_base[H];
@@ -478,36 +448,16 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
     __syncwarp();
     Stage S{st_recs + (size_t)warp * SW, 0, SW};
 
-    // Converged mode (warp-uniform `conv`): every running lane of the warp is
-    // at pc `upc`, so the step needs no minimum and no pc comparison.  It is
-    // entered after a step whose running lanes all sat at the minimum (one
-    // vote), kept across every instruction that only advances or stops lanes,
-    // and left at BR / JMP (the next step takes the minimum again — that is
-    // also where a warp whose lanes all stopped notices it).
-    bool conv = false;
-    uint32_t upc = 0;
     for (;;) {
-      uint32_t minpc;
       bool ex[H];
-      if (INTERP_CONV && conv) {
-        minpc = upc;
+      uint32_t mine = 0xFFFFFFFFu;
 #pragma unroll
-        for (int h = 0; h < H; h++) ex[h] = running[h];
-      } else {
-        uint32_t mine = 0xFFFFFFFFu;
+      for (int h = 0; h < H; h++)
+        if (running[h]) mine = min(mine, pc[h]);
+      const uint32_t minpc = __reduce_min_sync(FULL, mine);
+      if (minpc == 0xFFFFFFFFu) break;  // no lane of the warp is running (pcs are < 65536)
 #pragma unroll
-        for (int h = 0; h < H; h++)
-          if (running[h]) mine = min(mine, pc[h]);
-        minpc = __reduce_min_sync(FULL, mine);
-        if (minpc == 0xFFFFFFFFu) break;  // no lane of the warp is running (pcs are < 65536)
-        bool all = true;
-#pragma unroll
-        for (int h = 0; h < H; h++) {
-          ex[h] = running[h] && pc[h] == minpc;
-          all = all && (ex[h] || !running[h]);
-        }
-        if (INTERP_CONV) conv = __all_sync(FULL, all);
-      }
+      for (int h = 0; h < H; h++) ex[h] = running[h] && pc[h] == minpc;
       uint4 eh;
       uint2 et;
       if (CODE_SMEM) {
@@ -517,7 +467,7 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
                      : "memory");
         asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(et.x), "=r"(et.y) : "r"(code_t + 8u * minpc) : "memory");
       } else {
-        const Dec d = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + minpc), TL, s_off, s_size);
+        const Dec d = predecode(__ldg(reinterpret_cast<const uint2*>(p.code) + minpc), TL, s_off, s_size, p);
         eh = d.h;
         et = d.t;
       }
@@ -560,10 +510,10 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
               cell = cell_base[h] + et.x + (uint32_t)idx;
               int32_t v = 0;
               bool found = false;
-              const int n_sm = min(n_own[h], (int)OV);
+              const int n_sm = SPILL ? min(n_own[h], (int)OV) : n_own[h];
               for (int j = 0; j < n_sm; j++)
                 if ((uint32_t)lds32(OC(h) + j * orow) == cell) { v = lds32(OVL(h) + j * orow); found = true; }
-              if (n_own[h] > (int)OV && !found) {  // the lane's spill list (rare)
+              if (SPILL && n_own[h] > (int)OV && !found) {  // the lane's spill list (rare)
                 for (int j = 0; j < n_own[h] - (int)OV; j++)
                   if (p.spill_cell[(size_t)j * p.n_lanes + g[h]] == cell) {
                     v = p.spill_val[(size_t)j * p.n_lanes + g[h]];
@@ -599,12 +549,12 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
             status[h] = L_OOB;
           } else {
             const uint32_t cell = cell_base[h] + et.x + (uint32_t)idx;
-            const int n_sm = min(n_own[h], (int)OV);
+            const int n_sm = SPILL ? min(n_own[h], (int)OV) : n_own[h];
             int j = 0;
             while (j < n_sm && (uint32_t)lds32(OC(h) + j * orow) != cell) j++;
             if (j < n_sm) {
               sts32(OVL(h) + j * orow, lds32(RC(h)));
-            } else if (n_own[h] < (int)OV) {
+            } else if (!SPILL || n_own[h] < (int)OV) {  // (!SPILL: the static bound fits the overlay)
               sts32(OC(h) + j * orow, (int32_t)cell);
               n_own[h]++;
               sts32(OVL(h) + j * orow, lds32(RC(h)));
@@ -629,10 +579,10 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
         })
       } else switch (op & 31) {
         case RC_OP_LD: case RC_OP_ST: break;  // handled above
-        case 0: case 28: case 29: case 30: case 31: break;  // unused (the validator rejects them)
+        case 0: case 28: case 29: case 30: case 31: break;  // (GID / LID / LSIZE are pre-decoded away)
         case RC_OP_CONST: EACH({ sts32(RA(h), imm); pc[h]++; }) break;
         case RC_OP_MOV: EACH({ sts32(RA(h), lds32(RB(h))); pc[h]++; }) break;
-        case RC_OP_TID: EACH({ sts32(RA(h), (int32_t)tid[h]); pc[h]++; }) break;
+        case RC_OP_TID: EACH({ sts32(RA(h), wadd(imm, (int32_t)tid[h])); pc[h]++; }) break;  // imm: pre-decode
         case RC_OP_SIZE: EACH({ sts32(RA(h), imm); pc[h]++; }) break;
         case RC_OP_ADDI: EACH({ sts32(RA(h), wadd(lds32(RB(h)), imm)); pc[h]++; }) break;
         // binary ALU ops, one case each (a flat jump table; int32 wrap, reading L7)
@@ -695,13 +645,6 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
         case RC_OP_BR: EACH({ pc[h] = lds32(RA(h)) != 0 ? (uint32_t)imm : et.y; }) break;
         case RC_OP_JMP: EACH({ pc[h] = (uint32_t)imm; }) break;
       }
-      if (INTERP_CONV) {
-        // every executing lane advanced to minpc + 1 or stopped (BAR / EXIT
-        // stop all of them in converged mode: nothing is left to run)
-        if (op == RC_OP_BR || op == RC_OP_JMP) conv = false;
-        else if (conv && (op == RC_OP_BAR || op == RC_OP_EXIT)) break;
-        upc = minpc + 1;
-      }
 #undef EACH
 #undef RA
 #undef RB
@@ -726,7 +669,7 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
         if (S.fill + __popc(m) > S.cap) S.fill = flush_warp_(lo, S.recs, S.fill, lane);
         if (has) {
           uint32_t cell, slot;
-          if (j < (int)OV) {
+          if (!SPILL || j < (int)OV) {
             cell = ocell[j * TL + l];
             slot = (uint32_t)j;
             p.wval[(size_t)j * p.n_lanes + g[h]] = oval[j * TL + l];
@@ -739,7 +682,7 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
         }
         S.fill += __popc(m);
       }
-      if (n_own[h] > (int)OV) p.spill_n[g[h]] = (uint32_t)(n_own[h] - (int)OV);
+      if (SPILL && n_own[h] > (int)OV) p.spill_n[g[h]] = (uint32_t)(n_own[h] - (int)OV);
     }
 
     IPHASE(3);
@@ -783,57 +726,6 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
       if (lane == 0) S.recs[S.fill] = REC_SENTINEL;
       S.fill++;
     }
-#if INTERP_INDEP
-    {
-      // this warp's staging room: its own chunk (a new one — one atomic — when
-      // full; the abandoned tail is padded with sentinels)
-      unsigned long long pad_from = 0;
-      uint32_t pad_n = 0;
-      if (S.fill && w_used + S.fill > w_cap) {
-        pad_from = w_base + w_used;
-        pad_n = w_cap - w_used;
-        const uint32_t sz = max(STAGE_CHUNK_W, S.fill);
-        unsigned long long nb = 0;
-        if (lane == 0) nb = atomicAdd(&p.ctr->stage_count, (unsigned long long)sz);
-        w_base = __shfl_sync(FULL, nb, 0);
-        w_used = 0;
-        w_cap = sz;
-      }
-      const unsigned long long base = w_base + w_used;
-      w_used += S.fill;
-      if (lane == 0) b_staged += S.fill;
-      for (uint32_t i = lane; i < pad_n; i += 32)
-        if (pad_from + i < p.stage_cap) p.stage[pad_from + i] = REC_SENTINEL;
-      // lane state out: this warp's slices of the status / pc / live register
-      // rows, and its records: bulk stores issued by lane 0
-#pragma unroll
-      for (int h = 0; h < H; h++) {
-        sstat[h * T + t] = valid[h] ? status[h] : (uint8_t)L_EXITED;
-        spc[h * T + t] = pc[h];
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) {
-#pragma unroll
-        for (int h = 0; h < H; h++) {
-          const uint32_t l0 = h * T + warp * 32;
-          const size_t g0 = (size_t)tile * TL + l0;
-          bulk_s2g(p.status_out + g0, sstat + l0, 32u);
-          bulk_s2g(p.pc_out + g0, spc + l0, 128u);
-          for (uint32_t i = 0; i < p.n_live; i++) {
-            const uint32_t r = s_live[i];
-            bulk_s2g(p.regs_out + (size_t)r * p.reg_stride + g0, SREGS(cur) + (size_t)r * TL + l0, 128u);
-          }
-        }
-        if (S.fill) {
-          if (base + S.fill <= p.stage_cap) bulk_s2g(p.stage + base, S.recs, S.fill * 8u);
-          else b_over = true;
-        }
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-      prev = cur;
-    }
-#else
     if (lane == 0) wcnt[warp] = S.fill;
     __syncthreads();
     IPHASE(4);
@@ -902,7 +794,6 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
     }
     for (uint32_t i = t; i < wcnt[W]; i += T)  // sentinels in the abandoned chunk tail
       if (wbase[W] + i < p.stage_cap) p.stage[wbase[W] + i] = REC_SENTINEL;
-#endif
     IPHASE(6);
     // no block barrier here: the next tile's first __syncthreads orders every
     // shared word a warp could overwrite early (wcnt / wbase are rewritten only
@@ -912,11 +803,6 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
   }
 
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // record / lane-state stores complete
-#if INTERP_INDEP
-  if (lane == 0 && b_staged) atomicAdd(&p.ctr->staged_recs, b_staged);
-  for (uint32_t i = lane; i < w_cap - w_used; i += 32)  // sentinels in this warp's last chunk tail
-    if (w_base + w_used + i < p.stage_cap) p.stage[w_base + w_used + i] = REC_SENTINEL;
-#else
   if (t == 0) {
     if (b_staged) atomicAdd(&p.ctr->staged_recs, b_staged);
   }
@@ -931,7 +817,6 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
   __syncthreads();
   for (uint32_t i = t; i < wcnt[W]; i += T)
     if (wbase[W] + i < p.stage_cap) p.stage[wbase[W] + i] = REC_SENTINEL;
-#endif
   if (__any_sync(FULL, b_over) && lane == 0) p.ctr->log_overflow = 1;
   {  // per-warp totals
     b_instr = warp_sum64(b_instr);
@@ -966,14 +851,14 @@ size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem, int H)
 }
 
 namespace {
-template <int H, bool ALT>
+template <int H, bool ALT, bool SPILL>
 cudaError_t launch_interp_h(const InterpParams& p, cudaStream_t s, int nsm) {
   const bool code_smem = p.n_instr <= 2048;
   int T = INTERP_T;
   while (T > 32 && interp_smem_bytes(p, T, code_smem, H) > 96 * 1024) T >>= 1;
   const size_t sm = interp_smem_bytes(p, T, code_smem, H);
-  auto kern = code_smem ? (p.fuel_check ? interp_kernel<true, true, H, ALT> : interp_kernel<true, false, H, ALT>)
-                        : (p.fuel_check ? interp_kernel<false, true, H, ALT> : interp_kernel<false, false, H, ALT>);
+  auto kern = code_smem ? (p.fuel_check ? interp_kernel<true, true, H, ALT, SPILL> : interp_kernel<true, false, H, ALT, SPILL>)
+                        : (p.fuel_check ? interp_kernel<false, true, H, ALT, SPILL> : interp_kernel<false, false, H, ALT, SPILL>);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, sm);
   const uint32_t tiles = (p.n_lanes + H * T - 1) / (H * T);
@@ -991,12 +876,15 @@ cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
   int dev = 0;
   cudaError_t se = setup.run(
       [](int d) -> cudaError_t {
-        for (auto f : {interp_kernel<true, true, 1, false>, interp_kernel<false, true, 1, false>,
-                       interp_kernel<true, false, 1, false>, interp_kernel<false, false, 1, false>,
-                       interp_kernel<true, true, 2, false>, interp_kernel<false, true, 2, false>,
-                       interp_kernel<true, false, 2, false>, interp_kernel<false, false, 2, false>,
-                       interp_kernel<true, true, 1, true>, interp_kernel<false, true, 1, true>,
-                       interp_kernel<true, false, 1, true>, interp_kernel<false, false, 1, true>}) {
+#define RC_K1_VARIANTS(SP)                                                                                   \
+  interp_kernel<true, true, 1, false, SP>, interp_kernel<false, true, 1, false, SP>,                         \
+      interp_kernel<true, false, 1, false, SP>, interp_kernel<false, false, 1, false, SP>,                   \
+      interp_kernel<true, true, 2, false, SP>, interp_kernel<false, true, 2, false, SP>,                     \
+      interp_kernel<true, false, 2, false, SP>, interp_kernel<false, false, 2, false, SP>
+        for (auto f : {RC_K1_VARIANTS(false), RC_K1_VARIANTS(true), interp_kernel<true, true, 1, true, true>,
+                       interp_kernel<false, true, 1, true, true>, interp_kernel<true, false, 1, true, true>,
+                       interp_kernel<false, false, 1, true, true>}) {
+#undef RC_K1_VARIANTS
           cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
           if (e != cudaSuccess) return e;
           cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1011,8 +899,10 @@ cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
   const char* force = getenv("RC_DEBUG_INTERP_H");
   const int h = force ? (force[0] == '2' ? 2 : 1)
                       : (INTERP_H >= 2 && p.n_lanes >= (uint32_t)INTERP_H * 256u * (uint32_t)nsm ? INTERP_H : 1);
-  if (p.alt_mask) return launch_interp_h<1, true>(p, s, nsm);  // classification re-run (rare)
-  return h == 2 ? launch_interp_h<2, false>(p, s, nsm) : launch_interp_h<1, false>(p, s, nsm);
+  if (p.alt_mask) return launch_interp_h<1, true, true>(p, s, nsm);  // classification re-run (rare)
+  if (p.may_spill)
+    return h == 2 ? launch_interp_h<2, false, true>(p, s, nsm) : launch_interp_h<1, false, true>(p, s, nsm);
+  return h == 2 ? launch_interp_h<2, false, false>(p, s, nsm) : launch_interp_h<1, false, false>(p, s, nsm);
 }
 
 }  // namespace rc

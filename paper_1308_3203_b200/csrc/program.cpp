@@ -33,14 +33,14 @@ static uint16_t rd16(const uint8_t* p) { uint16_t v; memcpy(&v, p, 2); return v;
 static const char* op_name(int op) {
   static const char* names[] = {"?", "CONST", "MOV", "TID", "SIZE", "ADD", "SUB", "MUL", "DIV", "MOD", "MIN",
                                 "MAX", "AND", "OR", "XOR", "LT", "EQ", "LAND", "LNOT", "LD", "ST", "BAR",
-                                "ASSUME", "ASSERT", "BR", "JMP", "EXIT", "ADDI"};
-  return (op >= 1 && op <= RC_OP_ADDI) ? names[op] : "?";
+                                "ASSUME", "ASSERT", "BR", "JMP", "EXIT", "ADDI", "GID", "LID", "LSIZE"};
+  return (op >= 1 && op <= RC_OP_LSIZE) ? names[op] : "?";
 }
 
 // register / array operands of each opcode: 'r' register, 'a' array, '-' unused
 static const char* operand_kinds(int op) {
   switch (op) {
-    case RC_OP_CONST: case RC_OP_TID: return "r--";
+    case RC_OP_CONST: case RC_OP_TID: case RC_OP_GID: case RC_OP_LID: case RC_OP_LSIZE: return "r--";
     case RC_OP_MOV: case RC_OP_LNOT: case RC_OP_ADDI: return "rr-";
     case RC_OP_SIZE: return "ra-";
     case RC_OP_ADD: case RC_OP_SUB: case RC_OP_MUL: case RC_OP_DIV: case RC_OP_MOD: case RC_OP_MIN:

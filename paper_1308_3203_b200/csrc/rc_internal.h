@@ -132,6 +132,7 @@ struct InterpParams {
   const Ins* code;
   uint32_t n_instr, n_regs, n_arrays;
   uint32_t n;                 // work-group size
+  uint32_t gid, gbase;        // work-group of this pass and its first global tid (gid * n; reading L20)
   uint64_t n_magic;           // div_magic(n)
   uint32_t n_lanes;           // I_b * n
   uint32_t cpi;               // cells per instance
@@ -157,6 +158,7 @@ struct InterpParams {
   int32_t* spill_val;         // [spill_cap][n_lanes] their values
   uint32_t* spill_n;          // [n_lanes] spill entries of a lane (written when > 0)
   uint32_t spill_cap;
+  bool may_spill;             // the program may write more cells than the smem overlay holds (SPILL kernels)
   uint32_t stage_warp;        // records staged per warp in shared memory
   int32_t* node_min;          // [I_b] min / max arrival node (fused A4)
   int32_t* node_max;
@@ -190,6 +192,7 @@ struct DetectParams {
   const int32_t* spill_val;
   const uint32_t* spill_n;
   uint32_t n_lanes, n;        // lane = inst_local * n + tid
+  uint32_t gbase;             // global tid of local id 0 (work-group pass, reading L20)
   uint32_t n_records;         // host upper bound (grid size)
   int32_t* heap;
   uint32_t cpi, n_arrays;
@@ -300,6 +303,7 @@ cudaError_t launch_rw_flag(rc_report* reports, uint64_t r0, uint64_t r1, uint32_
 
 struct BoundaryParams {
   uint32_t n, n_lanes, n_inst, interval, inst_base;
+  uint32_t gbase;          // global tid of local id 0 (reading L20)
   const uint8_t* status;   // status_out of the interval just run
   const uint32_t* pc;      // pc_out of the interval just run
   int32_t* node_min;       // [n_inst] from K1
@@ -320,6 +324,17 @@ cudaError_t launch_lane_hist(const uint8_t* status, uint32_t n_lanes, DevCounter
 cudaError_t launch_init_lanes(uint8_t* status, uint32_t* pc, int32_t* regs, uint32_t n_regs,
                               uint32_t n_lanes, cudaStream_t s);
 cudaError_t finalize_reports(rc_report* reports, uint64_t n, rc_report* scratch, cudaStream_t s);
+
+// inter-group races (groups.cu, reading L20): per-cell state of IG_FIELDS u32
+// planes over the batch's cells
+constexpr int IG_FIELDS = 10;
+cudaError_t ig_reset(uint32_t* st, uint64_t cells, cudaStream_t s);
+cudaError_t launch_ig_accumulate(const uint64_t* stage, const DevCounters* ctr, uint64_t cap, uint32_t* st,
+                                 uint64_t cells, uint32_t n, uint32_t cpi, uint32_t gbase, cudaStream_t s);
+cudaError_t launch_ig_combine(uint32_t* st, const int32_t* heap, uint64_t cells, cudaStream_t s);
+cudaError_t launch_ig_emit(const uint32_t* st, uint64_t cells, uint32_t cpi, const uint32_t* arr_off, uint32_t n_arrays,
+                           uint32_t inst_base, rc_report* reports, unsigned long long cap, DevCounters* ctr,
+                           cudaStream_t s);
 
 }  // namespace rc
 

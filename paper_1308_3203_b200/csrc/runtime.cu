@@ -122,6 +122,7 @@ struct rc_workspace {
   DevBuf regs[2], pc[2], status[2], live, entry_ro;
   DevBuf log, log_alt, wval, wmap, sort_status, ctr_block;
   DevBuf spill_cell, spill_val, spill_n;  // own-write overlay spill lists (grown on demand)
+  DevBuf ig;                              // inter-group race state (groups.cu), IG_FIELDS planes
   uint32_t spill_cap = 0;                 // entries per lane the spill buffers hold
   uint8_t wtag = 0;  // write-set map tag of the last interval attempt
   bool plan_valid = false;      // cached batch plan (rc_run)
@@ -144,7 +145,7 @@ struct rc_workspace {
     for (DevBuf* b : {&code, &arr_off, &arr_size, &heap, &heap2, &regs[0], &regs[1], &pc[0], &pc[1], &status[0],
                       &status[1], &live, &entry_ro, &log, &log_alt, &wval, &wmap, &sort_status,
                       &ctr_block, &reports, &reports_scratch, &inst_tmp, &heap_snap[0], &heap_snap[1], &heapB, &amap,
-                      &regs_b, &pc_b, &status_b, &cmp_inst, &spill_cell, &spill_val, &spill_n})  // (ctr: a view)
+                      &regs_b, &pc_b, &status_b, &cmp_inst, &spill_cell, &spill_val, &spill_n, &ig})  // (ctr: a view)
       b->release();
     if (h_ctr) cudaFreeHost(h_ctr);
     for (cudaEvent_t e : iv_done)
@@ -187,13 +188,13 @@ struct DeviceGuard {
 // prefer the fewest 8-bit sort passes that still give >= ~4M lanes per batch,
 // then the largest batch with that pass count, within a memory budget.
 uint32_t plan_batch(uint32_t n_inst, uint32_t n, uint64_t cpi, uint32_t n_regs, uint32_t max_batch,
-                    size_t free_bytes) {
+                    size_t free_bytes, bool groups) {
   if (n_inst == 0) return 0;
   const uint64_t cells_cap = cpi ? (uint64_t)0xFFFFFFFFull / cpi : (uint64_t)n_inst;
   const uint64_t lane_cap = n ? ((uint64_t)1 << 27) / n : (uint64_t)n_inst;  // batch lanes fit the record's 27 bits
   // bytes per lane: 2x lane state + node + ~6 log records (keys+vals, double buffered)
   const uint64_t per_lane = 2 * (4ull * n_regs + 5) + 4 + 6 * 24;
-  const uint64_t per_inst = (uint64_t)n * per_lane + cpi * 4 + 16;
+  const uint64_t per_inst = (uint64_t)n * per_lane + cpi * 4 * (groups ? 1 + IG_FIELDS : 1) + 16;
   const uint64_t mem_cap = std::max<uint64_t>(1, (uint64_t)(free_bytes * 0.5) / std::max<uint64_t>(per_inst, 1));
   uint64_t hi = std::min<uint64_t>({(uint64_t)n_inst, cells_cap, lane_cap, mem_cap});
   if (max_batch) hi = std::min<uint64_t>(hi, max_batch);
@@ -264,6 +265,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   if (!opt.max_intervals) opt.max_intervals = 65536;
   if (!opt.fuel_per_interval) opt.fuel_per_interval = 1ull << 20;
   const bool host_io = (opt.flags & RC_OPT_HOST_IO) != 0;
+  const uint32_t G = opt.n_groups ? opt.n_groups : 1;  // work-groups per instance (reading L20)
+  if ((uint64_t)G * n > 0xFFFFFFFEull) return fail(RC_EINVAL, "n_groups * work_group_size exceeds 2^32 - 2");
   const bool classify = (opt.flags & RC_OPT_CLASSIFY_RW) != 0;  // RW value classification (reading L19)
   uint64_t cpi = 0;
   std::vector<uint32_t> off(n_arrays + 1, 0), size(n_arrays + 1, 0);
@@ -338,11 +341,11 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
 
   // batch plan, cached per shape: cudaMemGetInfo can take milliseconds (it
   // was the largest host stall between back-to-back runs)
-  const uint64_t plan_key[4] = {n_inst, n, cpi, opt.max_batch_instances};
+  const uint64_t plan_key[4] = {n_inst, n, cpi, (uint64_t)opt.max_batch_instances | (uint64_t)(G > 1) << 32};
   if (!W.plan_valid || memcmp(plan_key, W.plan_key, sizeof plan_key) != 0) {
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
-    W.plan_ib = plan_batch(n_inst, n, cpi, P->n_regs, opt.max_batch_instances, free_b);
+    W.plan_ib = plan_batch(n_inst, n, cpi, P->n_regs, opt.max_batch_instances, free_b, G > 1);
     memcpy(W.plan_key, plan_key, sizeof plan_key);
     W.plan_valid = true;
   }
@@ -374,6 +377,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     }
     CK(W.wval.ensure(std::max<uint64_t>(1, L_max * (uint64_t)P->ovl_cap) * 4));
     if (P->may_spill) CK(W.spill_n.ensure(L_pad * 4));
+    if (G > 1) CK(W.ig.ensure(std::max<uint64_t>(1, (uint64_t)I_b * cpi) * 4 * IG_FIELDS));
     const void* wmap_before = W.wmap.p;
     CK(W.wmap.ensure(std::max<uint64_t>(1, (uint64_t)I_b * cpi)));
     if (W.wmap.p != wmap_before) W.wtag = 0;  // new memory: zero it before the next tag is used
@@ -496,11 +500,13 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     uint32_t* first_tid = reinterpret_cast<uint32_t*>(node_max + I_b);
     uint32_t* second_tid = first_tid + I_b;
     uint32_t* inst_flag = second_tid + I_b;
-    CK(cudaMemsetAsync(node_min, 0x7F, (size_t)nb * 4, s));  // large positive: "no arrival"
-    CK(cudaMemsetAsync(node_max, 0x80, (size_t)nb * 4, s));  // large negative
+    uint32_t gi = 0;  // work-group pass (reading L20; one pass when n_groups == 1)
+    const uint64_t bcells = (uint64_t)nb * cpi;
+    if (G > 1) CK(ig_reset(W.ig.as<uint32_t>(), bcells, s));
     auto bparams = [&](uint32_t interval) {
       BoundaryParams bp;
       bp.n = n;
+      bp.gbase = gi * n;
       bp.n_lanes = L;
       bp.n_inst = nb;
       bp.interval = interval;
@@ -517,15 +523,6 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     };
     int cur = 0;
     const uint32_t reg_stride = (uint32_t)((L + LANE_PAD - 1) / LANE_PAD * LANE_PAD);
-    if (L) {
-      CK(cudaMemsetAsync(W.status[cur].p, 0, reg_stride, s));
-      CK(cudaMemsetAsync(W.pc[cur].p, 0, (size_t)reg_stride * 4, s));
-      // registers start at 0 (reading L18): only a register read before it is
-      // written in interval 0 (live_in(pc 0)) can observe it; the other rows K1
-      // loads are overwritten before any read
-      for (uint8_t r : P->live_at_entry)
-        CK(cudaMemsetAsync(W.regs[cur].as<int32_t>() + (size_t)r * reg_stride, 0, (size_t)reg_stride * 4, s));
-    }
     // ---- one interval = K1 → filter → sort → detect → A4 (+ verdict), then
     //      the counters to a pinned slot and an event.  No kernel needs a host
     //      count (each reads its record count from device memory).
@@ -536,11 +533,12 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       DetectParams dp;
       dp.recs = sr;
       dp.wval = W.wval.as<int32_t>();
-      dp.spill_cell = W.spill_cell.as<uint32_t>();
-      dp.spill_val = W.spill_val.as<int32_t>();
-      dp.spill_n = W.spill_n.as<uint32_t>();
+      dp.spill_cell = P->may_spill ? W.spill_cell.as<uint32_t>() : nullptr;  // (null: no spilled record)
+      dp.spill_val = P->may_spill ? W.spill_val.as<int32_t>() : nullptr;
+      dp.spill_n = P->may_spill ? W.spill_n.as<uint32_t>() : nullptr;
       dp.n_lanes = L;
       dp.n = n;
+      dp.gbase = gi * n;
       dp.n_records = (uint32_t)log_cap;  // upper bound; the kernel reads the exact count
       dp.heap = heap_cur;
       dp.cpi = (uint32_t)std::max<uint64_t>(cpi, 1);
@@ -569,6 +567,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       ip.n_regs = P->n_regs;
       ip.n_arrays = n_arrays;
       ip.n = n;
+      ip.gid = gi;
+      ip.gbase = gi * n;
       ip.n_magic = div_magic(n);
       ip.n_lanes = L;
       ip.cpi = (uint32_t)cpi;
@@ -593,6 +593,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       ip.spill_val = P->may_spill ? W.spill_val.as<int32_t>() : nullptr;
       ip.spill_n = P->may_spill ? W.spill_n.as<uint32_t>() : nullptr;
       ip.spill_cap = P->may_spill ? W.spill_cap : 0;
+      ip.may_spill = P->may_spill;
       ip.stage_warp = stage_warp;
       ip.node_min = node_min;
       ip.node_max = node_max;
@@ -608,7 +609,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       ip.alt_mask = nullptr;
       ip.entry_ro = W.entry_ro.as<uint32_t>();
       ip.inst_div = inst_flag;
-      ip.ro_skip = (opt.flags & RC_OPT_KEEP_ALL_READS) == 0;
+      // (inter-group races need every read logged: no static elision with groups)
+      ip.ro_skip = (opt.flags & RC_OPT_KEEP_ALL_READS) == 0 && G == 1;
       return ip;
     };
     auto enqueue_interval = [&](uint32_t kk, int cc, Marks* mk) -> cudaError_t {
@@ -634,6 +636,11 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       W.prof.begin(s);
       EQ(launch_interp(ip, s));
       W.prof.end(RC_PROF_INTERP, s, 0, L);
+      // inter-group races: this group's smallest reader / writer per cell
+      // (from the staging buffer, before the sort reuses it)
+      if (G > 1)
+        EQ(launch_ig_accumulate(W.log_alt.as<uint64_t>(), dctr, log_cap, W.ig.as<uint32_t>(), bcells, n,
+                                (uint32_t)cpi, gi * n, s));
       // ---- write-set filter: writes + reads of written cells, dense, with histograms
       FilterParams fp;
       fp.stage = W.log_alt.as<uint64_t>();
@@ -753,6 +760,19 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     // k needs the host (overflow, divergence, or no lane left waiting), its
     // verdict makes every kernel of k+1 return at entry; the host then acts
     // and queues k+1 again.
+    for (gi = 0; gi < G; gi++) {  // work-groups one after another (reading L20)
+    cur = 0;
+    if (L) {
+      CK(cudaMemsetAsync(W.status[cur].p, 0, reg_stride, s));
+      CK(cudaMemsetAsync(W.pc[cur].p, 0, (size_t)reg_stride * 4, s));
+      // registers start at 0 (reading L18): only a register read before it is
+      // written in interval 0 (live_in(pc 0)) can observe it; the other rows K1
+      // loads are overwritten before any read
+      for (uint8_t r : P->live_at_entry)
+        CK(cudaMemsetAsync(W.regs[cur].as<int32_t>() + (size_t)r * reg_stride, 0, (size_t)reg_stride * 4, s));
+    }
+    CK(cudaMemsetAsync(node_min, 0x7F, (size_t)nb * 4, s));  // large positive: "no arrival"
+    CK(cudaMemsetAsync(node_max, 0x80, (size_t)nb * 4, s));  // large negative
     uint32_t k = 0;
     Marks mk_cur, mk_next;
     CK(enqueue_interval(k, cur, &mk_cur));
@@ -860,6 +880,19 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     }
     intervals_max = std::max<uint64_t>(intervals_max, (uint64_t)k + 1);
     CK(launch_lane_hist(W.status[cur].as<uint8_t>(), L, dctr, s));
+    if (G > 1) CK(launch_ig_combine(W.ig.as<uint32_t>(), heap_cur, bcells, s));
+    }  // work-group passes
+    if (G > 1) {  // inter-group reports of the batch's instances
+      for (;;) {
+        CK(launch_ig_emit(W.ig.as<uint32_t>(), bcells, (uint32_t)cpi, W.arr_off.as<uint32_t>(), n_arrays, inst_base,
+                          W.reports.as<rc_report>(), rep_cap, dctr, s));
+        CK(read_ctr());
+        if (W.h_ctr[2].report_count <= rep_cap) break;
+        CK(grow_reports(W.h_ctr[2].report_count));
+        CK(set_report_count(rep_count));
+      }
+      rep_count = W.h_ctr[2].report_count;
+    }
     // final heaps out
     if (final_heaps) {
       W.prof.cut();

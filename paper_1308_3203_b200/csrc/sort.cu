@@ -30,24 +30,6 @@
 #ifndef SORT_LB
 #define SORT_LB 4
 #endif
-#ifndef SORT_EXP
-#define SORT_EXP 0
-#endif
-#ifndef SORT_MATCH  // in-tile digit matching: 0 fast paths + ballots, 1 ballots only (branch-free)
-#define SORT_MATCH 3
-#endif
-#ifndef SORT_RANK  // ranking: 0 per-round LDS/STS with __syncwarp, 1 leader atomicAdd + shuffle
-#define SORT_RANK 0
-#endif
-#ifndef SORT_BACKOFF  // ns to sleep before re-polling a look-back predecessor (0 = spin)
-#define SORT_BACKOFF 0
-#endif
-#ifndef SORT_EARLY_LB  // predecessors read right after publishing AGGREGATE (0 = none)
-#define SORT_EARLY_LB 0
-#endif
-#ifndef SORT_CLAIM_LATE  // 1: claim the next tile after the look-back, 0: one tile ahead
-#define SORT_CLAIM_LATE 1
-#endif
 #ifndef SORT_W32  // 1: 32-bit look-back status words for sorts of < 2^26 records
 #define SORT_W32 1
 #endif
@@ -209,13 +191,10 @@ __global__ void __launch_bounds__(256) hist_kernel(const uint64_t* __restrict__ 
 // counter (claiming one tile ahead to hide the atomic); each block keeps two
 // tile buffers and prefetches (TMA) the next claimed tile while it processes
 // the current one.
-template <int NBUF>
 struct SortSmem {
-  uint64_t buf[NBUF][SORT_TILE];
+  uint64_t buf[2][SORT_TILE];
   uint32_t whist[WARPS][RADIX];  // per-warp digit counters (ranking; <= 512 per warp)
-#if SORT_MATCH == 3
   uint32_t wmask[3][WARPS][RADIX];  // per-warp digit lane masks (zero between uses)
-#endif
   uint32_t thist[2][RADIX];      // early tile counts (two copies: fewer atomic conflicts)
   uint32_t glob_base[RADIX];
   uint32_t bin_base[RADIX];      // global exclusive start of each digit (this pass)
@@ -249,24 +228,10 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* mbar, uint32_t pha
   }
 }
 
-// lanes of the warp holding the same 8-bit digit: one ballot per digit bit
-// (MATCH.ANY has far lower throughput on this part)
-__device__ __forceinline__ unsigned match_digit(uint32_t d, unsigned valid_mask) {
-  unsigned peers = valid_mask;
-#pragma unroll
-  for (int b = 0; b < 8; b++) {
-    const unsigned bb = __ballot_sync(FULL, (d >> b) & 1u);
-    peers &= ((d >> b) & 1u) ? bb : ~bb;
-  }
-  return peers;
-}
-
-// PERSISTENT: resident grid, two buffers, next tile prefetched (TMA) while
-// the current one is processed.  Otherwise: one tile per block (grid = tiles;
-// the hardware block scheduler staggers tiles, which keeps look-back walks
-// short) with a single buffer.
-template <bool PERSISTENT, typename SWORD>
-__global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256 / SORT_THREADS) onesweep_kernel(const uint64_t* __restrict__ in,
+// Persistent: a resident grid, two tile buffers per block, the next tile
+// prefetched (TMA) while the current one is processed.
+template <typename SWORD>
+__global__ void __launch_bounds__(SORT_THREADS, SORT_MINB) onesweep_kernel(const uint64_t* __restrict__ in,
                                                                    uint64_t* __restrict__ out, uint32_t n_host,
                                                                    const unsigned long long* n_a,
                                                                    const unsigned long long* n_b, int shift,
@@ -274,18 +239,14 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
                                                                    SWORD* __restrict__ status,
                                                                    uint32_t* __restrict__ tile_ctr, uint32_t epoch) {
   using L = LB<SWORD>;
-  constexpr int NB = PERSISTENT ? 2 : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  SortSmem<NB>& S = *reinterpret_cast<SortSmem<NB>*>(smem_raw);
+  SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const uint32_t n = dev_count(n_host, n_a, n_b);
   const uint32_t n_tiles = (uint32_t)((n + SORT_TILE - 1) / SORT_TILE);
   const int dsh = REC_CELL_SHIFT + shift;
-  uint32_t claimed = 0xFFFFFFFFu;  // thread 0: tile claimed ahead
 
-#if SORT_MATCH == 3
   for (int i = t; i < 3 * WARPS * RADIX; i += SORT_THREADS) (&S.wmask[0][0][0])[i] = 0u;
-#endif
   if (t == 0) {
     for (int b = 0; b < 2; b++)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar[b])));
@@ -295,9 +256,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
     if (t0 < n_tiles) {
       tile_fetch(S.buf[0], &S.mbar[0], in + (uint64_t)t0 * SORT_TILE,
                  (uint32_t)umin64(SORT_TILE, n - (uint64_t)t0 * SORT_TILE));
-      if (PERSISTENT && !SORT_CLAIM_LATE) claimed = atomicAdd(tile_ctr, 1u);
     }
-    if (!PERSISTENT) S.tile[1] = 0xFFFFFFFFu;
   }
   {  // global start of every digit of this pass: exclusive scan of its counts
     const uint32_t e = block_excl_scan(t < RADIX ? hist[t] : 0u, S.wt);  // (synchronises the block)
@@ -312,18 +271,6 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
   for (;;) {
     const uint32_t tile = S.tile[cur];
     if (tile >= n_tiles) break;  // block-uniform
-    // fetch the tile claimed last iteration into the other buffer (freed by
-    // the __syncthreads that ended the previous iteration); claim the next
-    if (PERSISTENT && !SORT_CLAIM_LATE && t == 0) {
-      const uint32_t tn = claimed;
-      S.tile[cur ^ 1] = tn;
-      claimed = 0xFFFFFFFFu;
-      if (tn < n_tiles) {
-        tile_fetch(S.buf[(cur ^ 1) % NB], &S.mbar[cur ^ 1], in + (uint64_t)tn * SORT_TILE,
-                   (uint32_t)umin64(SORT_TILE, n - (uint64_t)tn * SORT_TILE));
-        claimed = atomicAdd(tile_ctr, 1u);
-      }
-    }
     for (int i = t; i < WARPS * RADIX; i += SORT_THREADS) (&S.whist[0][0])[i] = 0;
     if (t < RADIX) {
       S.thist[0][t] = 0;
@@ -331,7 +278,7 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
     }
     const uint64_t base = (uint64_t)tile * SORT_TILE;
     const uint32_t cnt = (uint32_t)umin64(SORT_TILE, n - base);
-    uint64_t* B = S.buf[cur % NB];
+    uint64_t* B = S.buf[cur];
     PHASE_T(0);
     mbar_wait(&S.mbar[cur], (phase >> cur) & 1u);
     phase ^= 1u << cur;
@@ -355,17 +302,6 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
 #pragma unroll
       for (int j = 0; j < SORT_ITEMS; j++) {
         const uint32_t dd = DIGIT(j);
-#if SORT_EXP == 2  // timing experiment only: no matching (wrong ranks)
-        pm[j] = 1u << lane;
-        (void)vm;
-#elif SORT_MATCH == 1
-        const unsigned valid = vm ? vm : __ballot_sync(FULL, dd < RADIX);
-        pm[j] = dd < RADIX ? match_digit(dd, valid) : 0u;
-#elif SORT_MATCH == 2
-        (void)vm;
-        pm[j] = __match_any_sync(FULL, dd);
-        if (dd >= RADIX) pm[j] = 0u;
-#elif SORT_MATCH == 3
         // peers through shared-memory lane masks: three mask sets rotate so
         // one __syncwarp per round suffices (set j%3 is cleared in round j+1,
         // after that round's __syncwarp, and reused in round j+3)
@@ -378,37 +314,19 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
           if (dp < RADIX && lane == __ffs(pm[j - 1]) - 1) S.wmask[(j - 1) % 3][w][dp] = 0u;
         }
         pm[j] = m;
-#else
-        // exact fast paths for the structured runs of access logs: a round
-        // whose 32 digits are all equal, or strictly increasing by lane
-        const unsigned valid = vm ? vm : __ballot_sync(FULL, dd < RADIX);
-        const uint32_t d0 = __shfl_sync(FULL, dd, 0);
-        const uint32_t dprev = __shfl_up_sync(FULL, dd, 1);
-        if (__all_sync(FULL, dd == d0)) {
-          pm[j] = dd < RADIX ? valid : 0u;
-        } else if (__all_sync(FULL, lane == 0 || dd > dprev)) {
-          pm[j] = 1u << lane;  // all distinct (invalid lanes carry 0x100, the largest)
-        } else {
-          pm[j] = match_digit(dd, valid);
-        }
-#endif
       }
     }
-#if SORT_MATCH == 3
     __syncwarp();
     {
       const uint32_t dp = DIGIT(SORT_ITEMS - 1);
       if (dp < RADIX && lane == __ffs(pm[SORT_ITEMS - 1]) - 1) S.wmask[(SORT_ITEMS - 1) % 3][w][dp] = 0u;
     }
-#endif
     PHASE_T(3);
     // early tile counts: one shared atomic per digit group, then publish AGGREGATE
 #pragma unroll
     for (int j = 0; j < SORT_ITEMS; j++) {
       const uint32_t dd = DIGIT(j);
-#if SORT_EXP != 1  // timing experiment 1: no early counts
       if (dd < RADIX && lane == __ffs(pm[j]) - 1) atomicAdd(&S.thist[w & 1][dd], (uint32_t)__popc(pm[j]));
-#endif
     }
     __syncthreads();
     // per-digit steps: thread d < RADIX owns digit d
@@ -418,30 +336,9 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
     SWORD* my_status = status + (size_t)tile * RADIX + d;
     if (dig) st_relaxed(my_status, L::make(tile == 0 ? FLAG_INC : FLAG_AGG, epoch, tile_cnt));
     const uint32_t excl_tile = block_excl_scan(tile_cnt, S.wt);  // tile-local start of digit d
-#if SORT_EARLY_LB
-    // first look-back round issued now; its latency hides behind rank + scatter
-    SWORD esw[SORT_EARLY_LB];
-#pragma unroll
-    for (int j = 0; j < SORT_EARLY_LB; j++)
-      esw[j] = dig && (int64_t)tile - 1 - j >= 0 ? ld_relaxed(status + (size_t)(tile - 1 - j) * RADIX + d) : (SWORD)0;
-#endif
     PHASE_T(4);
 
     // ---- stable in-tile ranking (warp w owns items [w*512, w*512+512), striped)
-#if SORT_RANK == 1
-    // the round's leader adds the group size to the warp's digit counter and
-    // hands the previous count to its peers (the warp's shared-memory atomics
-    // execute in issue order, so rounds rank in order)
-#pragma unroll
-    for (int j = 0; j < SORT_ITEMS; j++) {
-      const uint32_t dd = DIGIT(j);
-      const int leader = __ffs(pm[j]) - 1;
-      uint32_t prev = 0;
-      if (dd < RADIX && lane == leader) prev = atomicAdd(&S.whist[w][dd], (uint32_t)__popc(pm[j]));
-      prev = __shfl_sync(FULL, prev, leader < 0 ? lane : leader);
-      pm[j] = prev + __popc(pm[j] & lanemask_lt());
-    }
-#else
 #pragma unroll
     for (int j = 0; j < SORT_ITEMS; j++) {
       const uint32_t dd = DIGIT(j);
@@ -453,7 +350,6 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
       __syncwarp();
       pm[j] = prev + __popc(pm[j] & lanemask_lt());
     }
-#endif
     __syncthreads();
     if (dig) {  // per digit: tile-local start of each warp's items of digit d
       uint32_t run = excl_tile;
@@ -483,16 +379,6 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
       constexpr int LBN = SORT_LB;  // predecessors per L2 round trip
       int64_t tp = (int64_t)tile - 1;
       bool done = false;
-#if SORT_EARLY_LB
-#pragma unroll
-      for (int j = 0; j < SORT_EARLY_LB; j++) {
-        if (done) break;
-        if (!L::ready(esw[j], epoch)) break;
-        excl += L::value(esw[j]);
-        tp--;
-        if (L::inclusive(esw[j])) done = true;
-      }
-#endif
 #ifdef SORT_PHASE_TIMING
       uint32_t st_rounds = 0, st_notready = 0, st_walk = 0;
 #endif
@@ -510,9 +396,6 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
           if (!ready) {  // re-poll from this predecessor
 #ifdef SORT_PHASE_TIMING
             st_notready++;
-#endif
-#if SORT_BACKOFF
-            __nanosleep(SORT_BACKOFF);
 #endif
             break;
           }
@@ -534,18 +417,16 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
 #endif
     }
     if (dig) S.glob_base[d] = (uint32_t)(S.bin_base[d] + excl) - excl_tile;
-#if SORT_CLAIM_LATE
     // claim the next tile only now (its AGGREGATE follows within a few
     // thousand cycles, so successors' look-backs never wait on a tile claimed
     // long before it is processed); its TMA load overlaps the write-out
-    if (PERSISTENT && t == 0) {
+    if (t == 0) {
       const uint32_t tn = atomicAdd(tile_ctr, 1u);
       S.tile[cur ^ 1] = tn;
       if (tn < n_tiles)
-        tile_fetch(S.buf[(cur ^ 1) % NB], &S.mbar[cur ^ 1], in + (uint64_t)tn * SORT_TILE,
+        tile_fetch(S.buf[cur ^ 1], &S.mbar[cur ^ 1], in + (uint64_t)tn * SORT_TILE,
                    (uint32_t)umin64(SORT_TILE, n - (uint64_t)tn * SORT_TILE));
     }
-#endif
     __syncthreads();
     PHASE_T(7);
 
@@ -564,12 +445,9 @@ __global__ void __launch_bounds__(SORT_THREADS, PERSISTENT ? SORT_MINB : 3 * 256
     }
     __syncthreads();  // buffer `cur`, whist, glob_base free for reuse
     PHASE_T(8);
-    if (!PERSISTENT) break;
     cur ^= 1;
   }
 }
-
-int g_sort_variant = 1;  // 1 = persistent double-buffered, 0 = one tile per block (sortbench knob)
 
 size_t sort_tiles(size_t n) { return (n + SORT_TILE - 1) / SORT_TILE; }
 
@@ -584,19 +462,15 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, const unsigned long long* 
   int dev = 0;
   cudaError_t se = setup.run(
       [](int d) -> cudaError_t {
-        const void* ks[4] = {(const void*)onesweep_kernel<true, unsigned long long>,
-                             (const void*)onesweep_kernel<true, unsigned>,
-                             (const void*)onesweep_kernel<false, unsigned long long>,
-                             (const void*)onesweep_kernel<false, unsigned>};
-        for (int i = 0; i < 4; i++) {
-          cudaError_t e = cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               i < 2 ? (int)sizeof(SortSmem<2>) : (int)sizeof(SortSmem<1>));
+        const void* ks[2] = {(const void*)onesweep_kernel<unsigned long long>, (const void*)onesweep_kernel<unsigned>};
+        for (int i = 0; i < 2; i++) {
+          cudaError_t e = cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SortSmem));
           if (e != cudaSuccess) return e;
           cudaFuncSetAttribute(ks[i], cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         }
         int per_sm = 0;
         cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, onesweep_kernel<true, unsigned long long>, SORT_THREADS, sizeof(SortSmem<2>));
+            &per_sm, onesweep_kernel<unsigned long long>, SORT_THREADS, sizeof(SortSmem));
         if (e != cudaSuccess) return e;
         per_sm_of[d] = per_sm < 1 ? 1 : per_sm;
         return cudaDeviceGetAttribute(&nsm_of[d], cudaDevAttrMultiProcessorCount, d);
@@ -615,8 +489,7 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, const unsigned long long* 
   }
   const uint32_t tiles = (uint32_t)sort_tiles(n);
   // persistent: never more blocks than can be resident (look-back progress)
-  const bool pers = g_sort_variant == 1;
-  const uint32_t grid = pers ? (uint32_t)umin64(tiles, (uint64_t)per_sm * nsm) : tiles;
+  const uint32_t grid = (uint32_t)umin64(tiles, (uint64_t)per_sm * nsm);
   uint64_t* kin = recs;
   uint64_t* kout = ws.alt;
   // 32-bit look-back words when every prefix fits 26 bits
@@ -634,14 +507,10 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, const unsigned long long* 
     const uint32_t* h = ws.hist + p * RADIX;
     uint32_t* tc = ws.tile_ctr + p;
     unsigned* st32 = reinterpret_cast<unsigned*>(ws.status);
-    if (pers && fmt)
-      onesweep_kernel<true, unsigned><<<g, b, sizeof(SortSmem<2>), s>>>(kin, kout, n, n_a, n_b, 8 * p, h, st32, tc, ws.epoch);
-    else if (pers)
-      onesweep_kernel<true, unsigned long long><<<g, b, sizeof(SortSmem<2>), s>>>(kin, kout, n, n_a, n_b, 8 * p, h, ws.status, tc, ws.epoch);
-    else if (fmt)
-      onesweep_kernel<false, unsigned><<<g, b, sizeof(SortSmem<1>), s>>>(kin, kout, n, n_a, n_b, 8 * p, h, st32, tc, ws.epoch);
+    if (fmt)
+      onesweep_kernel<unsigned><<<g, b, sizeof(SortSmem), s>>>(kin, kout, n, n_a, n_b, 8 * p, h, st32, tc, ws.epoch);
     else
-      onesweep_kernel<false, unsigned long long><<<g, b, sizeof(SortSmem<1>), s>>>(kin, kout, n, n_a, n_b, 8 * p, h, ws.status, tc, ws.epoch);
+      onesweep_kernel<unsigned long long><<<g, b, sizeof(SortSmem), s>>>(kin, kout, n, n_a, n_b, 8 * p, h, ws.status, tc, ws.epoch);
     launched();
     if (prof) prof->end(RC_PROF_SORT, s, (uint64_t)n * 16, n);
     cudaError_t e = cudaGetLastError();

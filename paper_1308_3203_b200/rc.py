@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "librc.so")
 RC_OK, RC_EINVAL, RC_ENOMEM, RC_ECUDA, RC_ETRUNC, RC_ELIMIT = range(6)
 STATUS_NAMES = {0: "RC_OK", 1: "RC_EINVAL", 2: "RC_ENOMEM", 3: "RC_ECUDA", 4: "RC_ETRUNC", 5: "RC_ELIMIT"}
 KINDS = {1: "RW", 2: "WW_BENIGN", 3: "WW_NONBENIGN", 4: "OOB", 5: "ASSERT", 6: "DIV0", 7: "FUEL",
-         8: "BARRIER_DIVERGENCE"}
+         8: "BARRIER_DIVERGENCE", 9: "IG_RW", 10: "IG_WW_BENIGN", 11: "IG_WW_NONBENIGN"}
 RC_OPT_HOST_IO = 1
 RC_OPT_KEEP_ALL_READS = 2
 RC_OPT_CLASSIFY_RW = 4
@@ -54,7 +54,7 @@ class rc_array(C.Structure):
 class rc_options(C.Structure):
     _fields_ = [("instance_offset", C.c_uint32), ("max_intervals", C.c_uint32), ("fuel_per_interval", C.c_uint64),
                 ("device", C.c_int32), ("flags", C.c_uint32), ("cuda_stream", C.c_void_p),
-                ("max_batch_instances", C.c_uint32), ("reserved0", C.c_uint32),
+                ("max_batch_instances", C.c_uint32), ("n_groups", C.c_uint32),
                 ("profile", C.POINTER(rc_profile))]
 
 
@@ -167,8 +167,9 @@ def rc_run(prog: Program, work_group_size: int, arrays: list, *, n_instances: in
            instance_offset: int = 0, fuel_per_interval: int = 0, max_intervals: int = 0, device: int | None = None,
            stream=None, capacity: int = 1 << 20, want_final: bool = True, final_out: list | None = None,
            profile: bool = False, max_batch_instances: int = 0, allow_truncate: bool = False,
-           keep_all_reads: bool = False, classify_rw: bool = False) -> RunResult:
-    """Run `prog` on the arrays.
+           keep_all_reads: bool = False, classify_rw: bool = False, n_groups: int = 1) -> RunResult:
+    """Run `prog` on the arrays (n_groups work-groups of work_group_size
+    work-items per instance, include/rc.h rc_options.n_groups).
 
     arrays: per shared array either a CUDA int32 torch tensor [n_instances, size]
     (device path), or a host numpy / CPU torch int32 array (RC_OPT_HOST_IO: the
@@ -221,6 +222,7 @@ def rc_run(prog: Program, work_group_size: int, arrays: list, *, n_instances: in
         (RC_OPT_CLASSIFY_RW if classify_rw else 0)
     opt.cuda_stream = C.c_void_p(stream.cuda_stream if stream is not None else 0)
     opt.max_batch_instances = max_batch_instances
+    opt.n_groups = n_groups
     prof = rc_profile()
     if profile:
         opt.profile = C.pointer(prof)

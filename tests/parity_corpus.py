@@ -1,6 +1,6 @@
 """Opcode-coverage corpus of the GPU parity tests (test infrastructure).
 
-Every entry is (name, Program, n, inputs).  Together they execute every
+Every entry is (name, Program, n, inputs, rc_run keyword arguments).  Together they execute every
 RCB1 opcode of include/rc.h (the §3 grammar lowered):
 `tests/test_opcode_coverage.py` checks that on the oracle (CPU), and
 `tests/test_gpu_parity.py::test_opcode_corpus` runs each entry through the
@@ -84,14 +84,28 @@ def _tiny(seed, count):
         p = K.random_tiny_kernel(rng, n_arrays=2, n_regs=5, n_commands=int(rng.integers(3, 12)), size=5)
         ins = [rng.integers(-3, 4, size=(int(rng.integers(1, 4)), 5)).astype(np.int32)]
         ins.append(rng.integers(-3, 4, size=(ins[0].shape[0], 5)).astype(np.int32))
-        out.append((f"tiny{seed}_{i}", p, n, ins))
+        out.append((f"tiny{seed}_{i}", p, n, ins, {}))
     return out
 
 
 def _cfg4_full(seed, n=300):
     ins = I.cfg4_inputs(0, 4, n)
     ins[3][:, 40:80] += 1  # dense index perturbation: input-dependent WW / RW
-    return (f"cfg4_full_isa_{seed}", K.random_stencil_kernel(seed, isa="full"), n, ins)
+    return (f"cfg4_full_isa_{seed}", K.random_stencil_kernel(seed, isa="full"), n, ins, {})
+
+
+GROUPS = """
+.arrays A B
+    lid   r0
+    gid   r1
+    lsize r2
+    mul   r3, r1, r2
+    add   r3, r3, r0       ; = tid
+    st    A, r3, r1        ; A[tid] := gid (disjoint)
+    const r4, 0
+    st    B, r4, r2        ; B[0] := n in every group (IG_WW_BENIGN)
+    exit
+"""
 
 
 def corpus():
@@ -104,6 +118,9 @@ def corpus():
          ("alu", _alu_kernel(), 47 * 47, _alu_inputs()),
          ("many_writes", K.many_writes_kernel(), 40, [np.arange(2 * (64 * 40 + 6), dtype=np.int32).reshape(2, -1),
                                                       np.zeros((2, 40), np.int32)])]
+    c = [x + ({},) for x in c]
+    c.append(("groups", assemble(GROUPS), 33, [np.zeros((2, 99), np.int32), np.zeros((2, 1), np.int32)],
+              {"n_groups": 3}))
     c += [_cfg4_full(s) for s in range(4)]
     c += _tiny(2024, 40)
     return c

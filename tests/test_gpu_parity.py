@@ -37,7 +37,8 @@ def run_both(rc, src_or_prog, n, ins, *, fuel=0, max_intervals=0, host=False, **
     g = rc.rc_run(prog, n, arrays, fuel_per_interval=fuel, max_intervals=max_intervals, **kw)
     o = oracle.run(p.bytecode, n, ins, fuel=fuel or oracle.oracle.DEFAULT_FUEL,
                    max_intervals=max_intervals or oracle.oracle.DEFAULT_MAX_INTERVALS,
-                   instance_offset=kw.get("instance_offset", 0), classify_rw=kw.get("classify_rw", False))
+                   instance_offset=kw.get("instance_offset", 0), classify_rw=kw.get("classify_rw", False),
+                   n_groups=kw.get("n_groups", 1))
     return p, g, o
 
 
@@ -176,8 +177,8 @@ def test_opcode_corpus(rc):
     executed (so every K1 dispatch case ran under a parity check)."""
     from parity_corpus import FUEL, all_opcodes, corpus
     counts = [0] * 32
-    for name, p, n, ins in corpus():
-        _, g, o = run_both(rc, p, n, ins, fuel=FUEL)
+    for name, p, n, ins, kw in corpus():
+        _, g, o = run_both(rc, p, n, ins, fuel=FUEL, **kw)
         try:
             assert_parity(g, o, ins)
         except AssertionError as ex:
@@ -539,3 +540,80 @@ def test_grow_and_retry_paths(rc, monkeypatch):
     ins[3][:, 20:60] += 1
     p, g, o = run_both(rc, K.random_stencil_kernel(2), 300, ins)
     assert_parity(g, o, ins)
+
+
+# ------------------------------------------------------------------ work-groups (§8(f) row 3, reading L20)
+def _groups_cases():
+    lead = """
+.arrays A P S
+    lid   r0
+    gid   r1
+    lsize r2
+    tid   r3
+    const r4, 2
+    div   r5, r2, r4
+loop:
+    const r6, 0
+    lt    r7, r6, r5
+    br    r7, body, done
+body:
+    lt    r7, r0, r5
+    br    r7, work, sync
+work:
+    ld    r8, A, r3
+    add   r9, r3, r5
+    ld    r10, A, r9
+    add   r8, r8, r10
+    st    A, r3, r8
+sync:
+    bar
+    div   r5, r5, r4
+    jmp   loop
+done:
+    const r6, 0
+    eq    r7, r0, r6
+    br    r7, lead, end
+lead:
+    ld    r8, A, r3
+    st    P, r1, r8
+    ld    r9, S, r6
+    add   r9, r9, r8
+    st    S, r6, r9
+    addi  r11, r1, 1
+    const r12, 3
+    mod   r11, r11, r12
+    ld    r13, P, r11
+end:
+    exit
+"""
+    return [(".arrays A\n lid r0\n gid r1\n st A, r0, r1\n exit\n", 4, 3,
+             [np.zeros((2, 4), np.int32)]),
+            (lead, 8, 3, [np.arange(1, 3 * 24 + 1, dtype=np.int32).reshape(3, 24), np.zeros((3, 3), np.int32),
+                          np.zeros((3, 1), np.int32)]),
+            (lead, 256, 3, [I.cfg3_inputs(0, 4, 768)[0], np.zeros((4, 3), np.int32), np.zeros((4, 1), np.int32)]),
+            (K.TREE_OFF_BY_ONE, 64, 4, I.cfg3_inputs(0, 5, 64)),
+            (K.FIG1, 8, 2, I.cfg1_inputs()),
+            (K.many_writes_kernel(), 12, 3, [np.zeros((2, 64 * 12 + 6), np.int32), np.zeros((2, 12), np.int32)])]
+
+
+@pytest.mark.parametrize("classify", [False, True])
+def test_work_groups(rc, classify):
+    """n_groups > 1 (groups one after another, inter-group races over the
+    whole kernel) through the C ABI against the oracle: the hand-pinned
+    kernels of test_oracle_pins, shared-array kernels with every report kind,
+    random tiny kernels indexing by tid / lid / gid."""
+    for src, n, G, ins in _groups_cases():
+        _, g, o = run_both(rc, src, n, ins, n_groups=G, classify_rw=classify)
+        assert_parity(g, o, ins)
+        if "lsize" in (src if isinstance(src, str) else ""):  # the shared-partial kernel races across groups
+            assert any(t[1] == 0xFFFFFFFF for t in o.report_tuples())
+    rng = np.random.default_rng(404)
+    for it in range(120):
+        n = int(rng.integers(1, 40))
+        G = int(rng.integers(2, 6))
+        pr = K.random_tiny_kernel(rng, n_arrays=2, n_regs=5, n_commands=int(rng.integers(3, 12)), size=7,
+                                  groups=True)
+        ins = [rng.integers(-3, 4, size=(int(rng.integers(1, 4)), 7)).astype(np.int32)]
+        ins.append(rng.integers(-3, 4, size=(ins[0].shape[0], 7)).astype(np.int32))
+        _, g, o = run_both(rc, pr, n, ins, fuel=500, n_groups=G, classify_rw=classify)
+        assert_parity(g, o, ins)

@@ -8,8 +8,8 @@ from parity_corpus import FUEL, all_opcodes, corpus
 
 def test_corpus_executes_every_opcode(oracle_lib):
     counts = [0] * 32
-    for name, p, n, ins in corpus():
-        r = oracle.run(p.bytecode, n, ins, fuel=FUEL)
+    for name, p, n, ins, kw in corpus():
+        r = oracle.run(p.bytecode, n, ins, fuel=FUEL, **kw)
         counts = [a + b for a, b in zip(counts, r.stats["op_counts"])]
     missing = [op for op in all_opcodes() if counts[op] == 0]
     assert not missing, f"opcodes never executed by the parity corpus: {missing}"

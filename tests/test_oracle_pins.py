@@ -529,3 +529,136 @@ def test_many_writes_loop(oracle_lib):
                 assert fin[c] == (j - 64) - (t + 1)
             else:
                 assert fin[c] == j - t
+
+
+# --------------------------------------------------------------- work-groups (reading L20)
+IG = 0xFFFFFFFF  # interval field of the inter-group reports
+
+
+def test_groups_write_write(oracle_lib):
+    """PAPER.md:55-56 (work-groups with ids and a size), reading L20: G
+    work-groups of n work-items run one after another; no barrier orders
+    two groups.  A[lid] := gid: every cell c < n is written by work-item c of
+    every group and by nobody else in that group: no intra-group report; per
+    cell one IG_WW_NONBENIGN with the smallest cross-group writer pair
+    (c, n + c) (the groups' last values 0, 1, 2 differ); the last group's
+    value stays.  A[lid] := 7 instead: IG_WW_BENIGN."""
+    n, G = 4, 3
+    for val, kind, final in (("gid r1", 11, 2), ("const r1, 7", 10, 7)):
+        src = f".arrays A\n lid r0\n {val}\n st A, r0, r1\n exit\n"
+        p = assemble(src)
+        r = oracle_lib.run(p.bytecode, n, [np.zeros((1, n), np.int32)], n_groups=G)
+        assert r.report_tuples() == [(0, IG, 0, c, kind, c, n + c, 0) for c in range(n)]
+        assert r.final[0][0].tolist() == [final] * n
+        assert r.stats["lanes_final"][0] == n * G and r.stats["intervals_max"] == 1
+        assert r.stats["checked_accesses"] == n * G
+
+
+def test_groups_ids_and_partial_sums(oracle_lib):
+    """Per-group tree reduction over the group's own slice of A (tid = gid*n +
+    lid, LSIZE = n, barriers inside each group), then work-item 0 of every
+    group adds its partial sum into S[0] and reads the next group's partial
+    P[(gid+1) mod G].  Hand-derived: the slices are disjoint, so the
+    reduction is race-free; S[0] is read and written by lid 0 of every group:
+    IG_RW (0, n) and IG_WW_NONBENIGN (0, n) at S[0] (last values differ:
+    running sums); P[g] is written by group g (lid 0) and read by group g-1's
+    lid 0: IG_RW at P[g] with pair (lid 0 of group g-1, lid 0 of group g) for
+    g >= 1 and (0, (G-1) n) at P[0].  Final S[0] = sum of all A; P[g] = the
+    sum of group g's slice."""
+    n, G = 8, 3
+    src = """
+.arrays A P S
+    lid   r0
+    gid   r1
+    lsize r2
+    tid   r3               ; = gid * n + lid
+    const r4, 2
+    div   r5, r2, r4       ; s := n/2
+loop:
+    const r6, 0
+    lt    r7, r6, r5
+    br    r7, body, done
+body:
+    lt    r7, r0, r5
+    br    r7, work, sync
+work:
+    ld    r8, A, r3
+    add   r9, r3, r5
+    ld    r10, A, r9
+    add   r8, r8, r10
+    st    A, r3, r8
+sync:
+    bar
+    div   r5, r5, r4
+    jmp   loop
+done:
+    const r6, 0
+    eq    r7, r0, r6
+    br    r7, lead, end
+lead:
+    ld    r8, A, r3        ; the group's sum
+    st    P, r1, r8
+    ld    r9, S, r6
+    add   r9, r9, r8
+    st    S, r6, r9        ; S[0] += partial
+    addi  r11, r1, 1
+    const r12, 3
+    mod   r11, r11, r12
+    ld    r13, P, r11      ; the next group's partial
+end:
+    exit
+"""
+    p = assemble(src)
+    A = np.arange(1, n * G + 1, dtype=np.int32)[None, :]
+    r = oracle_lib.run(p.bytecode, n, [A, np.zeros((1, G), np.int32), np.zeros((1, 1), np.int32)], n_groups=G)
+    want = [(0, IG, 1, 0, 9, 0, (G - 1) * n, 0)]  # P[0]: written by group 0, read by group G-1
+    want += [(0, IG, 1, g, 9, (g - 1) * n, g * n, 0) for g in range(1, G)]
+    want += [(0, IG, 2, 0, 9, 0, n, 0), (0, IG, 2, 0, 11, 0, n, 0)]
+    assert r.report_tuples() == want
+    sums = [int(A[0, g * n:(g + 1) * n].sum()) for g in range(G)]
+    assert r.final[1][0].tolist() == sums and r.final[2][0].tolist() == [sum(sums)]
+    assert r.stats["intervals_max"] == 4  # log2(8) = 3 barriers per group
+
+
+def test_one_group_is_the_plain_run(oracle_lib):
+    """n_groups = 1 is exactly the single-work-group semantics; and G groups
+    on disjoint slices (index = tid) report each group's intra-group races
+    with global tids, the same as G separate instances would (tids offset)."""
+    p = K.program(K.TREE_OFF_BY_ONE)
+    ins = I.cfg3_inputs(0, 3, 16)
+    a = oracle_lib.run(p.bytecode, 16, ins)
+    b = oracle_lib.run(p.bytecode, 16, ins, n_groups=1)
+    assert a.report_tuples() == b.report_tuples() and a.stats == b.stats
+    # every group works on its own slice R[gid*n .. gid*n + n-1] (Fig. 1's
+    # second interval with the neighbour taken mod n): the groups' reports are
+    # the single-group run's on each slice, cells and tids shifted by gid*n;
+    # no inter-group report (the slices are disjoint); heaps concatenate
+    src = """
+.arrays R
+    lid   r0
+    lsize r1
+    gid   r2
+    mul   r3, r2, r1       ; gid * n
+    add   r4, r3, r0       ; my cell
+    st    R, r4, r0        ; R[me] := lid
+    bar
+    addi  r5, r0, 1
+    mod   r5, r5, r1
+    add   r5, r5, r3
+    ld    r6, R, r5        ; R[gid*n + (lid+1) mod n]
+    add   r6, r6, r6
+    st    R, r4, r6
+    exit
+"""
+    pg = assemble(src)
+    n, G = 6, 4
+    X = np.arange(n * G, dtype=np.int32)[None, :] * 5
+    g = oracle_lib.run(pg.bytecode, n, [X], n_groups=G)
+    want, fin = [], []
+    for j in range(G):
+        sr = oracle_lib.run(pg.bytecode, n, [X[:, j * n:(j + 1) * n]])
+        want += [(i, iv, a, idx + j * n, k, t1 + j * n, t2 + j * n, fl)
+                 for i, iv, a, idx, k, t1, t2, fl in sr.report_tuples()]
+        fin += sr.final[0][0].tolist()
+    assert len(want) == G * n and g.report_tuples() == sorted(want)
+    assert g.final[0][0].tolist() == fin

@@ -23,7 +23,6 @@ Profiler::~Profiler() {}
 #ifdef SORT_PHASE_TIMING
 void sort_phase_io(unsigned long long* out, bool reset);
 #endif
-extern int g_sort_variant;
 }  // namespace rc
 
 #define CK(x)                                                                      \
@@ -40,8 +39,6 @@ int main(int argc, char** argv) {
   const int bits = argc > 2 ? atoi(argv[2]) : 24;
   const std::string pat = argc > 3 ? argv[3] : "stencil";
   const int reps = argc > 4 ? atoi(argv[4]) : 10;
-  rc::g_sort_variant = argc > 5 ? atoi(argv[5]) : 1;
-  printf("variant %d\n", rc::g_sort_variant);
   std::vector<uint64_t> hk(n);
   // stencil-like log (config 5 even interval): per 32-lane warp: reads of
   // A[c-1], A[c], A[c+1] then the write of B[c]; instance-major

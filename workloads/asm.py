@@ -33,6 +33,7 @@ OPCODES = {
     "and": 12, "or": 13, "xor": 14, "lt": 15, "eq": 16, "land": 17, "lnot": 18,
     "ld": 19, "st": 20, "bar": 21, "assume": 22, "assert": 23, "br": 24,
     "jmp": 25, "exit": 26, "addi": 27,
+    "gid": 28, "lid": 29, "lsize": 30,  # work-group id / local id / work-group size (reading L20)
 }
 _ALU3 = {"add", "sub", "mul", "div", "mod", "min", "max", "and", "or", "xor",
          "lt", "eq", "land"}
@@ -153,7 +154,7 @@ def assemble(text: str) -> Program:
                 a, imm = _reg(args[0]), _imm(args[1]); regs = [a]
             elif mn == "mov" or mn == "lnot":
                 a, b = _reg(args[0]), _reg(args[1]); regs = [a, b]
-            elif mn == "tid":
+            elif mn in ("tid", "gid", "lid", "lsize"):
                 a = _reg(args[0]); regs = [a]
             elif mn == "size":
                 a, b = _reg(args[0]), arr(args[1]); regs = [a]

@@ -260,7 +260,7 @@ def random_stencil_kernel(seed: int, n_commands: int = 64, isa: str = "cfg4") ->
 
 def random_tiny_kernel(rng: np.random.Generator, n_arrays: int = 2, n_regs: int = 4,
                        n_commands: int = 6, size: int = 3, allow_bar: bool = True,
-                       allow_branch: bool = True) -> Program:
+                       allow_branch: bool = True, groups: bool = False) -> Program:
     """Tiny random kernels for the brute-force interleaving checks (n <= 4).
 
     Indices are drawn as (tid*m + c) mod size so most accesses are in bounds
@@ -269,21 +269,27 @@ def random_tiny_kernel(rng: np.random.Generator, n_arrays: int = 2, n_regs: int 
     (PAPER.md:87-88), mov and lnot included; div / mod by a zero register
     halts the work-item with DIV0.
     """
-    lines = [".arrays " + " ".join(f"A{i}" for i in range(n_arrays)), f".regs {n_regs + 3}",
+    lines = [".arrays " + " ".join(f"A{i}" for i in range(n_arrays)), f".regs {n_regs + (5 if groups else 3)}",
              "    tid r0", f"    const r1, {size}"]
     t = n_regs  # temp registers: r{n_regs}, r{n_regs+1}, r{n_regs+2}
+    ids = ["r0"]
+    if groups:  # work-group ids as index bases too (reading L20): r{n_regs+3} = lid, r{n_regs+4} = gid
+        lines += [f"    lid r{n_regs + 3}", f"    gid r{n_regs + 4}"]
+        ids = ["r0", f"r{n_regs + 3}", f"r{n_regs + 4}"]
     body = []
     for ci in range(n_commands):
         u = rng.random()
         if u < 0.30:  # store
             m, c = int(rng.integers(0, 3)), int(rng.integers(0, size))
             v = int(rng.integers(0, n_regs))
-            body += [f"    const r{t}, {m}", f"    mul r{t}, r0, r{t}", f"    addi r{t}, r{t}, {c}",
+            base = ids[int(rng.integers(0, len(ids)))] if groups else "r0"
+            body += [f"    const r{t}, {m}", f"    mul r{t}, {base}, r{t}", f"    addi r{t}, r{t}, {c}",
                      f"    mod r{t}, r{t}, r1", f"    st A{int(rng.integers(0, n_arrays))}, r{t}, r{v}"]
         elif u < 0.60:  # load
             m, c = int(rng.integers(0, 3)), int(rng.integers(0, size))
             d = int(rng.integers(2, n_regs)) if n_regs > 2 else 2
-            body += [f"    const r{t}, {m}", f"    mul r{t}, r0, r{t}", f"    addi r{t}, r{t}, {c}",
+            base = ids[int(rng.integers(0, len(ids)))] if groups else "r0"
+            body += [f"    const r{t}, {m}", f"    mul r{t}, {base}, r{t}", f"    addi r{t}, r{t}, {c}",
                      f"    mod r{t}, r{t}, r1", f"    ld r{d}, A{int(rng.integers(0, n_arrays))}, r{t}"]
         elif u < 0.80:  # alu
             d = int(rng.integers(2, n_regs)) if n_regs > 2 else 2
