@@ -380,14 +380,6 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
   long long tprev_ = clock64();
 #endif
   for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, cur = cur + 1 == LS_NB ? 0 : cur + 1) {
-    // prefetch the next tile's lane state into the next buffer once the bulk
-    // stores of its previous use (LS_NB - 1 tiles back) have read it
-    if (t == 0 && tile + gridDim.x < n_tiles) {
-      const int nx = cur + 1 == LS_NB ? 0 : cur + 1;
-      if (LS_NB == 2) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-      prefetch_lanes(p, tile + gridDim.x, TL, SSTAT(nx), SPC(nx), SREGS(nx), s_live, &mbar[nx]);
-    }
     IPHASE(0);
     // per-lane state, lane h*T + t of the tile
     uint32_t g[H], pc[H], inst[H], tid[H], cell_base[H];
@@ -655,6 +647,17 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
     }
 
     IPHASE(2);
+    // prefetch the next tile's lane state into the next buffer once the bulk
+    // stores of its previous use (LS_NB - 1 tiles back) have read it: issued
+    // after this warp's interpretation, when those stores (from the end of
+    // the previous tile) are long done, so thread 0 does not wait on them;
+    // the copy still lands during this tile's write-out
+    if (t == 0 && tile + gridDim.x < n_tiles) {
+      const int nx = cur + 1 == LS_NB ? 0 : cur + 1;
+      if (LS_NB == 2) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      prefetch_lanes(p, tile + gridDim.x, TL, SSTAT(nx), SPC(nx), SREGS(nx), s_live, &mbar[nx]);
+    }
     ld_async_wait();  // registers of suspended lanes are saved below
 
     // write records: one per distinct written cell; its final value (reading
