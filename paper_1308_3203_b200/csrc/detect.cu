@@ -72,6 +72,22 @@ __device__ __forceinline__ void emit(const DetectParams& p, uint32_t cell, uint3
   }
 }
 
+// Where a detection reads its sorted records from: the global sorted log
+// (read-only for the kernel: non-coherent loads), a bucket sorted into
+// global scratch by the same kernel (L2 loads), or a bucket in shared memory.
+struct SrcLdg {
+  const uint64_t* p;
+  __device__ __forceinline__ uint64_t operator[](uint32_t i) const { return __ldg(p + i); }
+};
+struct SrcCg {
+  const uint64_t* p;
+  __device__ __forceinline__ uint64_t operator[](uint32_t i) const { return __ldcg(p + i); }
+};
+struct SrcSmem {
+  const uint64_t* p;
+  __device__ __forceinline__ uint64_t operator[](uint32_t i) const { return p[i]; }
+};
+
 // Emit the RW / WW reports of one cell.
 __device__ __forceinline__ void finish_cell(const DetectParams& p, uint32_t key, uint32_t w1, uint32_t w2,
                                             uint32_t nw, uint32_t t1, uint32_t t2, uint32_t nb, bool t1r,
@@ -104,14 +120,15 @@ __device__ __forceinline__ void rw_pair(bool hasr, uint32_t r1, uint32_t r2, uin
 // thread walks it (pass 1: statistics; pass 2: first differing writer and
 // membership flags; pass 3 only for a non-benign pair with readers).
 // (out of line: the rare path stays out of the streaming loop's instruction footprint)
-__device__ __noinline__ void serial_segment(const DetectParams& p, uint32_t i, uint32_t n_records) {
-  const uint32_t key = rec_cell(__ldg(p.recs + i));
+template <class Src>
+__device__ __noinline__ void serial_segment(const DetectParams& p, const Src recs, uint32_t i, uint32_t n_records) {
+  const uint32_t key = rec_cell(recs[i]);
   uint32_t r1 = INF, r2 = INF, rmax = 0, w1 = INF, w2 = INF, wmax = 0, nw = 0;
   bool hasr = false;
   int32_t vw1 = 0, vwmax = 0;
   uint32_t end = i;
   do {
-    const uint64_t v = __ldg(p.recs + end);
+    const uint64_t v = recs[end];
     const uint32_t tid = rec_tid(v);
     if (rec_w(v)) {
       const int32_t val = rec_val<true>(p, v);
@@ -126,7 +143,7 @@ __device__ __noinline__ void serial_segment(const DetectParams& p, uint32_t i, u
       hasr = true;
     }
     end++;
-  } while (end < n_records && rec_cell(__ldg(p.recs + end)) == key);
+  } while (end < n_records && rec_cell(recs[end]) == key);
   if (nw == 0) return;  // only reads: no conflict, nothing to commit
   p.heap[key] = vwmax;  // barrier release: max-tid writer wins
   uint32_t t1, t2;
@@ -135,7 +152,7 @@ __device__ __noinline__ void serial_segment(const DetectParams& p, uint32_t i, u
   uint32_t nb = INF;
   bool t1r = false, t2r = false, t2w = false, w1r = false, w2r = false;
   for (uint32_t j = i; j < end; j++) {
-    const uint64_t v = __ldg(p.recs + j);
+    const uint64_t v = recs[j];
     const uint32_t tid = rec_tid(v);
     if (rec_w(v)) {
       if (rec_val<true>(p, v) != vw1 && tid < nb) nb = tid;
@@ -150,7 +167,7 @@ __device__ __noinline__ void serial_segment(const DetectParams& p, uint32_t i, u
   bool nbr = false;
   if (nb != INF && hasr)
     for (uint32_t j = i; j < end; j++) {
-      const uint64_t v = __ldg(p.recs + j);
+      const uint64_t v = recs[j];
       if (!rec_w(v) && rec_tid(v) == nb) nbr = true;
     }
   finish_cell(p, key, w1, w2, nw, t1, t2, nb, t1r, t2r, t2w, w1r, w2r, nbr);
@@ -221,36 +238,39 @@ __device__ __forceinline__ Seg seg_shfl(const Seg& a, int src) {
 // chunk belong to the previous warp.
 // The records of chunk wg (and its two boundary keys), issued as independent
 // loads: the caller fetches the next chunk while it processes this one.
+template <int ROUNDS = DET_ROUNDS>
 struct Chunk {
-  uint64_t vr[DET_ROUNDS];
+  uint64_t vr[ROUNDS];
   uint32_t key_before, key_after;
 };
-__device__ __forceinline__ void load_chunk(const DetectParams& p, uint64_t wg, uint32_t n_records, Chunk& ch) {
+template <class Src, int ROUNDS>
+__device__ __forceinline__ void load_chunk(const Src recs, uint64_t wg, uint32_t n_records, Chunk<ROUNDS>& ch) {
   const int lane = threadIdx.x & 31;
   // record indices are < 2^32 (n_records is): 32-bit index arithmetic
-  const uint32_t c0 = (uint32_t)wg * DET_CHUNK;
-  const uint32_t c1 = min(n_records, c0 + DET_CHUNK);
+  const uint32_t c0 = (uint32_t)wg * (32 * ROUNDS);
+  const uint32_t c1 = min(n_records, c0 + 32 * ROUNDS);
 #pragma unroll
-  for (int rd = 0; rd < (int)DET_ROUNDS; rd++) {
+  for (int rd = 0; rd < ROUNDS; rd++) {
     const uint32_t r = c0 + rd * 32 + lane;
-    ch.vr[rd] = r < c1 ? __ldg(p.recs + r) : ~0ull;
+    ch.vr[rd] = r < c1 ? recs[r] : ~0ull;
   }
-  ch.key_before = c0 > 0 ? rec_cell(__ldg(p.recs + c0 - 1)) : 0xFFFFFFFFu;
-  ch.key_after = c1 < n_records ? rec_cell(__ldg(p.recs + c1)) : 0xFFFFFFFFu;
+  ch.key_before = c0 > 0 ? rec_cell(recs[c0 - 1]) : 0xFFFFFFFFu;
+  ch.key_after = c1 < n_records ? rec_cell(recs[c1]) : 0xFFFFFFFFu;
 }
 
-template <bool SPILL>
-__device__ __forceinline__ void detect_chunk(const DetectParams& p, uint64_t wg, uint32_t n_records, const Chunk& ch) {
+template <bool SPILL, class Src, int ROUNDS>
+__device__ __forceinline__ void detect_chunk(const DetectParams& p, const Src recs, uint64_t wg, uint32_t n_records,
+                                             const Chunk<ROUNDS>& ch) {
   const unsigned FULL = 0xFFFFFFFFu;
   const int lane = threadIdx.x & 31;
-  const uint32_t c0 = (uint32_t)wg * DET_CHUNK;
-  const uint32_t c1 = min(n_records, c0 + DET_CHUNK);
-  const uint64_t(&vr)[DET_ROUNDS] = ch.vr;
+  const uint32_t c0 = (uint32_t)wg * (32 * ROUNDS);
+  const uint32_t c1 = min(n_records, c0 + 32 * ROUNDS);
+  const uint64_t(&vr)[ROUNDS] = ch.vr;
   const uint32_t key_before = ch.key_before, key_after = ch.key_after;
   // final values of the chunk's write records (all gathers in flight at once)
-  int32_t wv[DET_ROUNDS];
+  int32_t wv[ROUNDS];
 #pragma unroll
-  for (int rd = 0; rd < (int)DET_ROUNDS; rd++) wv[rd] = (vr[rd] != ~0ull && rec_w(vr[rd])) ? rec_val<SPILL>(p, vr[rd]) : 0;
+  for (int rd = 0; rd < ROUNDS; rd++) wv[rd] = (vr[rd] != ~0ull && rec_w(vr[rd])) ? rec_val<SPILL>(p, vr[rd]) : 0;
 
   const Seg ident{INF, 0u, 0u, 0, 0u};
   bool carry = false;       // an open segment started in an earlier round of this chunk
@@ -258,7 +278,7 @@ __device__ __forceinline__ void detect_chunk(const DetectParams& p, uint64_t wg,
   Seg cs = ident;
   uint32_t last_key = key_before;  // key of the record before this round
 #pragma unroll
-  for (int rd = 0; rd < (int)DET_ROUNDS; rd++) {
+  for (int rd = 0; rd < ROUNDS; rd++) {
     const uint32_t b = c0 + rd * 32;
     if (b >= c1) break;  // warp-uniform
     const uint32_t r = b + lane;
@@ -268,7 +288,7 @@ __device__ __forceinline__ void detect_chunk(const DetectParams& p, uint64_t wg,
     uint32_t prev = __shfl_up_sync(FULL, key, 1);
     if (lane == 0) prev = b > 0 ? last_key : ~key;
     uint32_t next = __shfl_down_sync(FULL, key, 1);
-    const uint32_t next_round_first = rd + 1 < (int)DET_ROUNDS ? rec_cell(__shfl_sync(FULL, vr[rd + 1 < (int)DET_ROUNDS ? rd + 1 : rd], 0)) : 0u;
+    const uint32_t next_round_first = rd + 1 < ROUNDS ? rec_cell(__shfl_sync(FULL, vr[rd + 1 < ROUNDS ? rd + 1 : rd], 0)) : 0u;
     if (lane == 31) next = r + 1 < c1 ? next_round_first : (r + 1 < n_records ? key_after : ~key);
     last_key = __shfl_sync(FULL, key, 31);
     const bool head = inb && prev != key;
@@ -309,7 +329,7 @@ __device__ __forceinline__ void detect_chunk(const DetectParams& p, uint64_t wg,
       const Seg M = seg_merge(cs, S0);
       if (l0_closes) {
         if (lane == 0) {
-          if (seg_complex(M)) serial_segment(p, (uint32_t)carry_start, n_records);
+          if (seg_complex(M)) serial_segment(p, recs, (uint32_t)carry_start, n_records);
           else if (M.nw == 1) p.heap[key] = M.vw;
         }
         carry = false;
@@ -319,7 +339,7 @@ __device__ __forceinline__ void detect_chunk(const DetectParams& p, uint64_t wg,
     }
     // segments starting in this round
     if (head && closes) {
-      if (seg_complex(S)) serial_segment(p, (uint32_t)r, n_records);
+      if (seg_complex(S)) serial_segment(p, recs, (uint32_t)r, n_records);
       else if (S.nw == 1) p.heap[key] = S.vw;
     }
     // the last segment of the round stays open: carry it
@@ -332,7 +352,7 @@ __device__ __forceinline__ void detect_chunk(const DetectParams& p, uint64_t wg,
       carry = true;
     }
   }
-  if (carry && lane == 0) serial_segment(p, (uint32_t)carry_start, n_records);  // continues into the next chunk
+  if (carry && lane == 0) serial_segment(p, recs, (uint32_t)carry_start, n_records);  // continues into the next chunk
 }
 
 // A4 fused as the tail of K4 (readings L9, L17): the
@@ -392,13 +412,187 @@ __global__ void __launch_bounds__(256, DET_MINB) detect_kernel(const DetectParam
     const uint32_t n_records = (uint32_t)p.ctr->kept_count;
     const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     uint64_t wg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    Chunk cur, nxt;
-    if (wg * DET_CHUNK < n_records) load_chunk(p, wg, n_records, cur);
+    const SrcLdg recs{p.recs};
+    Chunk<> cur, nxt;
+    if (wg * DET_CHUNK < n_records) load_chunk(recs, wg, n_records, cur);
     for (; wg * DET_CHUNK < n_records; wg += warps) {
       // software pipeline: the next chunk's records load while this one is processed
-      if ((wg + warps) * DET_CHUNK < n_records) load_chunk(p, wg + warps, n_records, nxt);
-      detect_chunk<SPILL>(p, wg, n_records, cur);
+      if ((wg + warps) * DET_CHUNK < n_records) load_chunk(recs, wg + warps, n_records, nxt);
+      detect_chunk<SPILL>(p, recs, wg, n_records, cur);
       cur = nxt;
+    }
+  }
+  __syncwarp();
+  if (p.with_boundary) boundary_tail(p);
+}
+
+// ---- K4+K5 on the bucket path -------------------------------
+// A bucket = the records of BUCKET_CELLS consecutive cells (bucket_scatter,
+// sort.cu, grouped them in arbitrary order).  A block claims buckets from a
+// counter.  A bucket of <= BD_CAP records is loaded into registers and
+// counted per cell in shared memory; a cell with one record only commits (a
+// lone writer can race with nobody, a lone read does nothing); the records of
+// the other cells are placed by cell into shared memory (a counting sort on
+// the low BUCKET_BITS bits) and run through the segmented detection above.
+// A larger bucket is counting-sorted into global scratch (`tmp`) and detected
+// there.  Any order inside a cell is fine: every statistic is
+// order-independent.
+constexpr int BD_THREADS = 512;
+constexpr int BD_ITEMS = 16;
+constexpr uint32_t BD_CAP = BD_THREADS * BD_ITEMS;  // records of a bucket held in registers
+constexpr int BD_WARPS = BD_THREADS / 32;
+constexpr int BD_ROUNDS = 2;  // 32-record rounds per detection chunk (the records are in shared memory / L2)
+struct BucketSmem {
+  uint64_t sorted[BD_CAP];      // records of the bucket's multi-record cells, by cell (global path: u32 offsets)
+  uint32_t cnt[BUCKET_CELLS];   // per cell: record count (bits 0-15), then | start << 16 during the placement
+  uint32_t wsum[BD_WARPS];
+  uint32_t bucket[2];           // claimed buckets (current, next)
+};
+__device__ __forceinline__ uint32_t bucket_low(uint64_t r) {
+  return (uint32_t)(r >> REC_CELL_SHIFT) & (BUCKET_CELLS - 1);
+}
+
+// exclusive scan over the 4096 per-cell values v[] (8 consecutive per thread);
+// returns this thread's start, *total = the sum (synchronises the block)
+__device__ __forceinline__ uint32_t bd_scan8(const uint32_t (&v)[BUCKET_CELLS / BD_THREADS], uint32_t* wsum,
+                                             uint32_t* total) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  uint32_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < (int)(BUCKET_CELLS / BD_THREADS); k++) sum += v[k];
+  uint32_t x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  uint32_t run = x - sum, tot = 0;
+#pragma unroll
+  for (int i = 0; i < BD_WARPS; i++) {
+    const uint32_t c = wsum[i];
+    run += i < w ? c : 0u;
+    tot += c;
+  }
+  *total = tot;
+  return run;
+}
+
+template <bool SPILL>
+__device__ __forceinline__ void bucket_smem(const DetectParams& p, BucketSmem& S, uint32_t s0, uint32_t m) {
+  const int t = threadIdx.x;
+  uint64_t r[BD_ITEMS];
+#pragma unroll
+  for (int j = 0; j < BD_ITEMS; j++) {
+    const uint32_t i = t + j * BD_THREADS;
+    r[j] = i < m ? __ldcs(p.recs + s0 + i) : REC_SENTINEL;  // (read once)
+  }
+#pragma unroll
+  for (int j = 0; j < BD_ITEMS; j++)
+    if (r[j] != REC_SENTINEL) atomicAdd(&S.cnt[bucket_low(r[j])], 1u);
+  __syncthreads();
+  // single-record cells: the commit of a lone writer (barrier release)
+  bool multi = false;
+#pragma unroll
+  for (int j = 0; j < BD_ITEMS; j++) {
+    if (r[j] == REC_SENTINEL) continue;
+    if ((S.cnt[bucket_low(r[j])] & 0xFFFFu) == 1u) {
+      if (rec_w(r[j])) p.heap[rec_cell(r[j])] = rec_val<SPILL>(p, r[j]);
+    } else {
+      multi = true;
+    }
+  }
+  const bool any_multi = __syncthreads_or(multi);
+  if (any_multi) {
+    // counting sort of the multi-record cells' records by cell
+    constexpr int PER = BUCKET_CELLS / BD_THREADS;
+    uint32_t v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; k++) {
+      const uint32_t c = S.cnt[t * PER + k] & 0xFFFFu;
+      v[k] = c > 1 ? c : 0u;
+    }
+    uint32_t M = 0;
+    uint32_t run = bd_scan8(v, S.wsum, &M);
+#pragma unroll
+    for (int k = 0; k < PER; k++)
+      if (v[k]) {
+        S.cnt[t * PER + k] = (run << 16) | v[k];
+        run += v[k];
+      }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < BD_ITEMS; j++) {
+      if (r[j] == REC_SENTINEL) continue;
+      uint32_t* c = &S.cnt[bucket_low(r[j])];
+      if ((*c & 0xFFFFu) > 1u) S.sorted[atomicAdd(c, 1u << 16) >> 16] = r[j];
+    }
+    __syncthreads();
+    // segmented detection over sorted[0, M): warps take 256-record chunks
+    const SrcSmem src{S.sorted};
+    for (uint32_t wg = (uint32_t)t >> 5; wg * (32 * BD_ROUNDS) < M; wg += BD_WARPS) {
+      Chunk<BD_ROUNDS> ch;
+      load_chunk(src, wg, M, ch);
+      detect_chunk<SPILL>(p, src, wg, M, ch);
+    }
+  }
+  // (the records are dead here: the counters are cleared whole, 8 per thread)
+#pragma unroll
+  for (int k = 0; k < (int)(BUCKET_CELLS / BD_THREADS); k++) S.cnt[t + k * BD_THREADS] = 0u;  // (the caller synchronises)
+}
+
+// a bucket larger than BD_CAP: counting sort by cell into tmp[s0, s0 + m), then detect there
+template <bool SPILL>
+__device__ __noinline__ void bucket_global(const DetectParams& p, BucketSmem& S, uint32_t s0, uint32_t m) {
+  const int t = threadIdx.x;
+  for (uint32_t i = t; i < m; i += BD_THREADS) atomicAdd(&S.cnt[bucket_low(__ldcg(p.recs + s0 + i))], 1u);
+  __syncthreads();
+  constexpr int PER = BUCKET_CELLS / BD_THREADS;
+  uint32_t* offs = reinterpret_cast<uint32_t*>(S.sorted);
+  uint32_t v[PER];
+#pragma unroll
+  for (int k = 0; k < PER; k++) v[k] = S.cnt[t * PER + k];
+  uint32_t tot = 0;
+  uint32_t run = bd_scan8(v, S.wsum, &tot);
+#pragma unroll
+  for (int k = 0; k < PER; k++) {
+    offs[t * PER + k] = run;
+    run += v[k];
+  }
+  __syncthreads();
+  for (uint32_t i = t; i < m; i += BD_THREADS) {
+    const uint64_t r = __ldcg(p.recs + s0 + i);
+    const uint32_t l = bucket_low(r);
+    p.tmp[s0 + offs[l] + atomicSub(&S.cnt[l], 1u) - 1u] = r;  // (counts return to 0)
+  }
+  __syncthreads();  // the block's global stores are visible to the block
+  const SrcCg src{p.tmp + s0};
+  for (uint32_t wg = (uint32_t)t >> 5; wg * (32 * BD_ROUNDS) < m; wg += BD_WARPS) {
+    Chunk<BD_ROUNDS> ch;
+    load_chunk(src, wg, m, ch);
+    detect_chunk<SPILL>(p, src, wg, m, ch);
+  }
+}
+
+template <bool SPILL>
+__global__ void __launch_bounds__(BD_THREADS, 2) bucket_detect_kernel(const DetectParams p) {
+  extern __shared__ __align__(16) unsigned char bd_smem_raw[];
+  BucketSmem& S = *reinterpret_cast<BucketSmem*>(bd_smem_raw);
+  if (p.ctr->abort) return;  // speculative interval after one that needs the host (grid-uniform)
+  const int t = threadIdx.x;
+  if (!(p.ctr->log_overflow || p.ctr->ovl_overflow || p.ctr->k1_reports > p.report_cap)) {
+    for (uint32_t i = t; i < BUCKET_CELLS; i += BD_THREADS) S.cnt[i] = 0u;
+    if (t == 0) S.bucket[0] = atomicAdd(&p.ctr->bucket_next, 1u);
+    __syncthreads();
+    for (int cur = 0;; cur ^= 1) {
+      const uint32_t b = S.bucket[cur];
+      if (b >= p.nb) break;  // block-uniform
+      if (t == 0) S.bucket[cur ^ 1] = atomicAdd(&p.ctr->bucket_next, 1u);  // claimed while this one runs
+      const uint32_t s0 = __ldg(p.bstart + b), m = __ldg(p.bend + b) - s0;
+      if (m > BD_CAP) bucket_global<SPILL>(p, S, s0, m);
+      else if (m) bucket_smem<SPILL>(p, S, s0, m);
+      __syncthreads();
     }
   }
   __syncwarp();
@@ -451,7 +645,35 @@ cudaError_t launch_rw_flag(rc_report* reports, uint64_t r0, uint64_t r1, uint32_
   return cudaGetLastError();
 }
 
+cudaError_t launch_bucket_detect(const DetectParams& p, cudaStream_t s) {
+  static DeviceSetup setup;
+  static int nsm_of[RC_MAX_DEVICES], per_sm_of[RC_MAX_DEVICES];
+  int dev = 0;
+  cudaError_t se = setup.run(
+      [](int d) -> cudaError_t {
+        const void* ks[2] = {(const void*)bucket_detect_kernel<false>, (const void*)bucket_detect_kernel<true>};
+        for (const void* k : ks) {
+          cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BucketSmem));
+          if (e != cudaSuccess) return e;
+        }
+        int per_sm = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bucket_detect_kernel<false>, BD_THREADS,
+                                                                      sizeof(BucketSmem));
+        if (e != cudaSuccess) return e;
+        per_sm_of[d] = std::max(per_sm, 1);
+        return cudaDeviceGetAttribute(&nsm_of[d], cudaDevAttrMultiProcessorCount, d);
+      },
+      &dev);
+  if (se != cudaSuccess) return se;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(p.nb, (uint64_t)nsm_of[dev] * per_sm_of[dev]));
+  if (p.spill_n) bucket_detect_kernel<true><<<grid, BD_THREADS, sizeof(BucketSmem), s>>>(p);
+  else bucket_detect_kernel<false><<<grid, BD_THREADS, sizeof(BucketSmem), s>>>(p);
+  launched();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_detect(const DetectParams& p, cudaStream_t s) {
+  if (p.nb) return launch_bucket_detect(p, s);
   if (p.n_records == 0 && !p.with_boundary) return cudaSuccess;
   static DeviceSetup setup;
   static int nsm_of[RC_MAX_DEVICES], per_sm_of[RC_MAX_DEVICES];

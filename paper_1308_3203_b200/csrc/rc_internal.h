@@ -115,6 +115,8 @@ struct DevCounters {
   unsigned long long k1_reports;    // report_count after K1 (snapshot taken by the filter)
   unsigned long long rw_reports;    // RW reports emitted by detect (RC_OPT_CLASSIFY_RW)
   unsigned long long kept_writes;   // write records among the kept ones (profile bytes of detect)
+  unsigned int f_done;              // filter blocks finished (last-block pattern: bucket offsets)
+  unsigned int bucket_next;         // next bucket to claim (bucket detect)
   // ---- fields above: zeroed per interval attempt (one memset, runtime.cu)
   unsigned long long report_count;  // reports appended (whole run, rolled back on retry)
   unsigned long long lanes_final[8];
@@ -210,6 +212,16 @@ struct DetectParams {
   int32_t* node_min;          // [n_inst] from K1, reset by the tail
   int32_t* node_max;
   uint32_t* inst_flag;        // [n_inst] diverged
+  // bucket path (nb > 0): recs = the bucketed records; bucket b holds
+  // recs[bstart[b], bend[b]) (bend = the scatter's cursors when it is done;
+  // unlike the counts, which the speculative next interval's scratch reset
+  // clears, they survive until the next scatter, so a detect-only re-run
+  // still finds its buckets); tmp = scratch of the same size (a bucket too
+  // large for shared memory is sorted there)
+  uint32_t nb;
+  const uint32_t* bstart;
+  const uint32_t* bend;
+  uint64_t* tmp;
 };
 
 // ---- launchers (defined in the .cu files) --------------------------------
@@ -225,14 +237,26 @@ struct FilterParams {
   const uint8_t* wmap;
   uint8_t wtag;           // wmap[c] == wtag: c written in this interval
   uint64_t* out;          // sort buffer, [0, kept_count)
-  uint32_t* hist;         // [4][256]
-  int passes;
+  uint32_t* hist;         // LSD: [4][256] digit counts; bucket path: [nb] bucket counts
+  int passes;             // LSD passes (0 on the bucket path)
+  uint32_t nb;            // bucket path: buckets (cell >> BUCKET_BITS) of the batch, <= NB_MAX; 0: LSD
+  uint32_t* bstart;       // bucket path: [nb] exclusive starts (written by the filter's last block)
+  uint32_t* bcur;         // bucket path: [nb] scatter cursors (= bstart, advanced by the scatter)
   DevCounters* ctr;
   uint32_t n_slots;       // staging buffer capacity (slots); the kernel reads stage_count
   bool keep_all;          // RC_OPT_KEEP_ALL_READS: only drop the sentinels
 };
 constexpr uint64_t REC_SENTINEL = ~0ull;  // cell 0xFFFFFFFF is never a real cell
 cudaError_t launch_filter(const FilterParams& p, cudaStream_t s);
+
+// ---- bucket path: the kept records are grouped by cell with
+// one MSD scatter on the high cell bits (bucket = cell >> BUCKET_BITS, 4096
+// cells) into the alt buffer, then bucket_detect sorts each bucket by its low
+// bits in shared memory and runs the segmented detection on it.
+constexpr int BUCKET_BITS = 12;
+constexpr uint32_t BUCKET_CELLS = 1u << BUCKET_BITS;
+constexpr uint32_t NB_MAX = 8192;                     // buckets per batch: cells per batch <= 2^25
+constexpr uint64_t BUCKET_PATH_CELLS = (uint64_t)NB_MAX * BUCKET_CELLS;
 
 struct SortWorkspace {
   uint64_t* alt = nullptr;         // ping-pong buffer
@@ -290,6 +314,9 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n_ub, const unsigned long lon
                           const unsigned long long* n_b, int bits, SortWorkspace& ws, cudaStream_t s, bool* in_alt,
                           Profiler* prof, bool hist_ready);
 
+// bucket scatter: records [0, *n_dev) of `in` to out[bcur[bucket]++] (any order inside a bucket)
+cudaError_t launch_bucket_scatter(const uint64_t* in, uint64_t* out, const unsigned long long* n_dev, uint32_t n_ub,
+                                  uint32_t* bcur, const DevCounters* ctr, cudaStream_t s, Profiler* prof);
 cudaError_t launch_detect(const DetectParams& p, cudaStream_t s);
 // RW classification helpers (detect.cu): mark the cells of the RW reports in
 // reports[r0, r1) (instance ids relative to inst_base), compare two heaps per

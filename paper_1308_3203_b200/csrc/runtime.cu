@@ -110,9 +110,9 @@ struct DevBuf {
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
-// interval scratch layout (one memset per interval attempt): digit histograms
-// [4][256] u32, sort tile counters, then DevCounters
-constexpr size_t CTR_OFF = 4096 + 64;
+// interval scratch layout (one memset per interval attempt): digit / bucket
+// histograms [NB_MAX] u32 (LSD: [4][256]), sort tile counters, then DevCounters
+constexpr size_t CTR_OFF = NB_MAX * 4 + 64;
 
 struct rc_workspace {
   int device = -1;
@@ -121,6 +121,7 @@ struct rc_workspace {
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_start = nullptr;
   DevBuf regs[2], pc[2], status[2], live, entry_ro;
   DevBuf log, log_alt, wval, wmap, sort_status, ctr_block;
+  DevBuf buckets;  // bucket path: [NB_MAX] starts | [NB_MAX] scatter cursors
   DevBuf spill_cell, spill_val, spill_n;  // own-write overlay spill lists (grown on demand)
   DevBuf ig;                              // inter-group race state (groups.cu), IG_FIELDS planes
   uint32_t spill_cap = 0;                 // entries per lane the spill buffers hold
@@ -143,7 +144,7 @@ struct rc_workspace {
       if (e) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     for (DevBuf* b : {&code, &arr_off, &arr_size, &heap, &heap2, &regs[0], &regs[1], &pc[0], &pc[1], &status[0],
-                      &status[1], &live, &entry_ro, &log, &log_alt, &wval, &wmap, &sort_status,
+                      &status[1], &live, &entry_ro, &log, &log_alt, &wval, &wmap, &sort_status, &buckets,
                       &ctr_block, &reports, &reports_scratch, &inst_tmp, &heap_snap[0], &heap_snap[1], &heapB, &amap,
                       &regs_b, &pc_b, &status_b, &cmp_inst, &spill_cell, &spill_val, &spill_n, &ig})  // (ctr: a view)
       b->release();
@@ -184,11 +185,12 @@ struct DeviceGuard {
   }
 };
 
-// Instance batch size: a batch's cells must fit the u32 key;
-// prefer the fewest 8-bit sort passes that still give >= ~4M lanes per batch,
-// then the largest batch with that pass count, within a memory budget.
+// Instance batch size: a batch's cells must fit the u32 key
+// (bucket path: the NB_MAX buckets); LSD path: prefer the fewest 8-bit sort
+// passes that still give >= ~4M lanes per batch, then the largest batch with
+// that pass count, within a memory budget.
 uint32_t plan_batch(uint32_t n_inst, uint32_t n, uint64_t cpi, uint32_t n_regs, uint32_t max_batch,
-                    size_t free_bytes, bool groups) {
+                    size_t free_bytes, bool groups, bool bucket) {
   if (n_inst == 0) return 0;
   const uint64_t cells_cap = cpi ? (uint64_t)0xFFFFFFFFull / cpi : (uint64_t)n_inst;
   const uint64_t lane_cap = n ? ((uint64_t)1 << 27) / n : (uint64_t)n_inst;  // batch lanes fit the record's 27 bits
@@ -199,6 +201,9 @@ uint32_t plan_batch(uint32_t n_inst, uint32_t n, uint64_t cpi, uint32_t n_regs, 
   uint64_t hi = std::min<uint64_t>({(uint64_t)n_inst, cells_cap, lane_cap, mem_cap});
   if (max_batch) hi = std::min<uint64_t>(hi, max_batch);
   hi = std::max<uint64_t>(hi, 1);
+  // bucket path: the largest batch whose cells fit the NB_MAX buckets (fewer
+  // batches: fewer interval launches for the same work)
+  if (bucket) return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(hi, BUCKET_PATH_CELLS / std::max<uint64_t>(cpi, 1)));
   const uint64_t target_lanes = 1ull << 22;
   uint64_t need = n ? (target_lanes + n - 1) / n : hi;
   need = std::min(std::max<uint64_t>(need, 1), hi);
@@ -305,8 +310,9 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     if (!P->live_regs.empty())
       CK(cudaMemcpy(W.live.p, P->live_regs.data(), P->live_regs.size(), cudaMemcpyHostToDevice));
     // interval scratch in one allocation, zeroed by one memset per interval:
-    // [digit histograms 4 KB][sort tile counters, 64 B][DevCounters]
+    // [digit / bucket histograms 32 KB][sort tile counters, 64 B][DevCounters]
     CK(W.ctr_block.ensure(CTR_OFF + sizeof(DevCounters)));
+    CK(W.buckets.ensure(2 * NB_MAX * sizeof(uint32_t)));
     W.ctr.p = static_cast<char*>(W.ctr_block.p) + CTR_OFF;
     W.ctr.bytes = sizeof(DevCounters);
     CK(cudaMallocHost(&W.h_ctr, 4 * sizeof(DevCounters)));
@@ -316,7 +322,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     W.sort.hist = W.ctr_block.as<uint32_t>();
     W.sort.bin_off = nullptr;  // each pass scans its counts itself
-    W.sort.tile_ctr = W.sort.hist + 1024;
+    W.sort.tile_ctr = W.sort.hist + NB_MAX;
     W.sort.reset_tile_ctr = false;
   }
   rc_workspace& W = *P->ws;
@@ -341,11 +347,16 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
 
   // batch plan, cached per shape: cudaMemGetInfo can take milliseconds (it
   // was the largest host stall between back-to-back runs)
-  const uint64_t plan_key[4] = {n_inst, n, cpi, (uint64_t)opt.max_batch_instances | (uint64_t)(G > 1) << 32};
+  // the bucket path groups the log by cell whenever one
+  // instance's cells fit its buckets; else (and under the A/B hook
+  // RC_SORT_LSD=1) the onesweep LSD sort
+  const bool bucket = cpi <= BUCKET_PATH_CELLS && getenv("RC_SORT_LSD") == nullptr;
+  const uint64_t plan_key[4] = {n_inst, n, cpi,
+                                (uint64_t)opt.max_batch_instances | (uint64_t)(G > 1) << 32 | (uint64_t)bucket << 33};
   if (!W.plan_valid || memcmp(plan_key, W.plan_key, sizeof plan_key) != 0) {
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
-    W.plan_ib = plan_batch(n_inst, n, cpi, P->n_regs, opt.max_batch_instances, free_b, G > 1);
+    W.plan_ib = plan_batch(n_inst, n, cpi, P->n_regs, opt.max_batch_instances, free_b, G > 1, bucket);
     memcpy(W.plan_key, plan_key, sizeof plan_key);
     W.plan_valid = true;
   }
@@ -502,6 +513,38 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     uint32_t* inst_flag = second_tid + I_b;
     uint32_t gi = 0;  // work-group pass (reading L20; one pass when n_groups == 1)
     const uint64_t bcells = (uint64_t)nb * cpi;
+    const uint64_t* sr = nullptr;  // sorted log of the last enqueued interval
+    const uint32_t nbk = bucket ? (uint32_t)std::max<uint64_t>(1, (bcells + BUCKET_CELLS - 1) / BUCKET_CELLS) : 0u;
+    // the sort of one interval's kept records (K3): bucket scatter, or the onesweep passes
+    auto enqueue_sort = [&](Profiler* prof) -> cudaError_t {
+      if (bucket) {
+        sr = W.log_alt.as<uint64_t>();
+        return launch_bucket_scatter(W.log.as<uint64_t>(), W.log_alt.as<uint64_t>(), &dctr->kept_count,
+                                     (uint32_t)log_cap, W.buckets.as<uint32_t>() + NB_MAX, dctr, s, prof);
+      }
+      bool in_alt = false;
+      W.sort.alt = W.log_alt.as<uint64_t>();
+      cudaError_t e = onesweep_sort(W.log.as<uint64_t>(), (uint32_t)log_cap, &dctr->kept_count, nullptr, key_bits,
+                                    W.sort, s, &in_alt, prof, /*hist_ready=*/true);
+      sr = in_alt ? W.log_alt.as<uint64_t>() : W.log.as<uint64_t>();
+      return e;
+    };
+    auto filter_params = [&]() {
+      FilterParams fp;
+      fp.stage = W.log_alt.as<uint64_t>();
+      fp.wmap = W.wmap.as<uint8_t>();
+      fp.wtag = W.wtag;
+      fp.out = W.log.as<uint64_t>();
+      fp.hist = W.sort.hist;
+      fp.passes = bucket ? 0 : passes;
+      fp.nb = nbk;
+      fp.bstart = W.buckets.as<uint32_t>();
+      fp.bcur = W.buckets.as<uint32_t>() + NB_MAX;
+      fp.ctr = dctr;
+      fp.n_slots = (uint32_t)log_cap;  // upper bound; the kernel reads stage_count
+      fp.keep_all = false;
+      return fp;
+    };
     if (G > 1) CK(ig_reset(W.ig.as<uint32_t>(), bcells, s));
     auto bparams = [&](uint32_t interval) {
       BoundaryParams bp;
@@ -528,7 +571,6 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     //      count (each reads its record count from device memory).
     const uint32_t stage_warp =
         P->rec_bound > 0 ? (uint32_t)std::min(256, ((32 * P->rec_bound + 31) / 32) * 32) : 256u;
-    const uint64_t* sr = nullptr;  // sorted log of the last enqueued interval
     auto detect_params = [&](uint32_t kk) {
       DetectParams dp;
       dp.recs = sr;
@@ -557,6 +599,10 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       dp.node_min = node_min;
       dp.node_max = node_max;
       dp.inst_flag = inst_flag;
+      dp.nb = nbk;
+      dp.bstart = W.buckets.as<uint32_t>();
+      dp.bend = W.buckets.as<uint32_t>() + NB_MAX;
+      dp.tmp = W.log.as<uint64_t>();
       return dp;
     };
     struct Marks { size_t m0 = 0, m1 = 0; };
@@ -642,25 +688,13 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         EQ(launch_ig_accumulate(W.log_alt.as<uint64_t>(), dctr, log_cap, W.ig.as<uint32_t>(), bcells, n,
                                 (uint32_t)cpi, gi * n, s));
       // ---- write-set filter: writes + reads of written cells, dense, with histograms
-      FilterParams fp;
-      fp.stage = W.log_alt.as<uint64_t>();
-      fp.wmap = W.wmap.as<uint8_t>();
-      fp.wtag = W.wtag;
-      fp.out = W.log.as<uint64_t>();
-      fp.hist = W.sort.hist;
-      fp.passes = passes;
-      fp.ctr = dctr;
-      fp.n_slots = (uint32_t)log_cap;  // upper bound; the kernel reads stage_count
+      FilterParams fp = filter_params();
       fp.keep_all = (opt.flags & RC_OPT_KEEP_ALL_READS) != 0;
       W.prof.begin(s);
       EQ(launch_filter(fp, s));
       W.prof.end(RC_PROF_FILTER, s, 0, 0);
-      // ---- K3: onesweep sort of the kept records by cell
-      bool in_alt = false;
-      W.sort.alt = W.log_alt.as<uint64_t>();
-      EQ(onesweep_sort(W.log.as<uint64_t>(), (uint32_t)log_cap, &dctr->kept_count, nullptr, key_bits, W.sort, s,
-                       &in_alt, W.prof.on ? &W.prof : nullptr, /*hist_ready=*/true));
-      sr = in_alt ? W.log_alt.as<uint64_t>() : W.log.as<uint64_t>();
+      // ---- K3: group the kept records by cell
+      EQ(enqueue_sort(W.prof.on ? &W.prof : nullptr));
       // ---- K4+K5 detect + commit, A4 check + verdict
       DetectParams dp = detect_params(kk);
       dp.with_boundary = true;  // A4 as detect's tail: consumes (and resets) K1's per-instance node ranges
@@ -709,23 +743,10 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         ip.status_out = W.status_b.as<uint8_t>();
         ip.report_cap = 0;  // error reports of the re-run are not written (the count is restored below)
         EQ(launch_interp(ip, s));
-        FilterParams fp;
-        fp.stage = W.log_alt.as<uint64_t>();
-        fp.wmap = W.wmap.as<uint8_t>();
-        fp.wtag = W.wtag;
-        fp.out = W.log.as<uint64_t>();
-        fp.hist = W.sort.hist;
-        fp.passes = passes;
-        fp.ctr = dctr;
-        fp.n_slots = (uint32_t)log_cap;
-        fp.keep_all = false;
+        FilterParams fp = filter_params();
         EQ(launch_filter(fp, s));
-        bool in_alt = false;
-        W.sort.alt = W.log_alt.as<uint64_t>();
-        EQ(onesweep_sort(W.log.as<uint64_t>(), (uint32_t)log_cap, &dctr->kept_count, nullptr, key_bits, W.sort, s,
-                         &in_alt, nullptr, /*hist_ready=*/true));
+        EQ(enqueue_sort(nullptr));  // (the classified interval's own sorted log is not needed again)
         DetectParams dp = detect_params(kk);
-        dp.recs = in_alt ? W.log_alt.as<uint64_t>() : W.log.as<uint64_t>();
         dp.heap = W.heapB.as<int32_t>();
         dp.quiet = true;
         dp.report_cap = ~0ull;  // (quiet: nothing is written; K1's uncounted reports never skip the commit)
@@ -822,6 +843,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         do {
           CK(grow_reports(rc));
           CK(set_report_count(h.k1_reports));
+          CK(cudaMemsetAsync(&dctr->bucket_next, 0, sizeof(unsigned int), s));  // (bucket path: claim again)
           DetectParams dp = detect_params(k);
           CK(launch_detect(dp, s));
           CK(read_ctr());

@@ -521,4 +521,82 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, const unsigned long long* 
   return cudaGetLastError();
 }
 
+// ---- K3 on the bucket path: one MSD scatter on the high cell bits ----------
+// Record i goes to out[bcur[bucket]++], bucket = cell >> BUCKET_BITS; the
+// filter's last block set bcur to the buckets' exclusive starts.  The order
+// inside a bucket is arbitrary (bucket_detect sorts each bucket by its low
+// bits, and the detection only uses order-independent reductions inside a
+// cell).  A warp takes BS_ROUNDS rounds of 32 consecutive records (all loads
+// in flight), groups each round's lanes by bucket (one vote when the round is
+// one bucket — the common case, records come in staging order — else
+// __match_any_sync), and the group leader reserves the group's slots with one
+// atomic; the atomics of all rounds are issued before any of them is waited on.
+constexpr int BS_ROUNDS = 8;
+constexpr int BS_THREADS = 256;
+__global__ void __launch_bounds__(BS_THREADS) bucket_scatter_kernel(const uint64_t* __restrict__ in,
+                                                                     uint64_t* __restrict__ out,
+                                                                     const unsigned long long* n_dev, uint32_t n_ub,
+                                                                     uint32_t* __restrict__ bcur,
+                                                                     const DevCounters* ctr) {
+  if (ctr->abort || ctr->log_overflow || ctr->ovl_overflow) return;  // (as the filter: nothing to group)
+  const uint32_t n = dev_count(n_ub, n_dev, nullptr);
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (BS_THREADS / 32);
+  const unsigned lt = lanemask_lt();
+  for (uint32_t c = blockIdx.x * (BS_THREADS / 32) + (threadIdx.x >> 5); (uint64_t)c * (32 * BS_ROUNDS) < n;
+       c += warps) {
+    const uint32_t c0 = c * (32 * BS_ROUNDS);
+    uint64_t r[BS_ROUNDS];
+#pragma unroll
+    for (int j = 0; j < BS_ROUNDS; j++) {
+      const uint32_t i = c0 + j * 32 + lane;
+      r[j] = i < n ? __ldcs(in + i) : REC_SENTINEL;  // (streamed: read once)
+    }
+    uint32_t base[BS_ROUNDS], rank[BS_ROUNDS], lead[BS_ROUNDS];
+#pragma unroll
+    for (int j = 0; j < BS_ROUNDS; j++) {
+      const uint32_t b = (uint32_t)(r[j] >> (REC_CELL_SHIFT + BUCKET_BITS));  // sentinel: 0xFFFFF (no bucket)
+      const uint32_t b0 = __shfl_sync(FULL, b, 0);
+      unsigned peers;
+      if (__all_sync(FULL, b == b0)) peers = FULL;
+      else peers = __match_any_sync(FULL, b);
+      lead[j] = __ffs(peers) - 1;
+      rank[j] = __popc(peers & lt);
+      base[j] = 0;
+      if (r[j] != REC_SENTINEL && rank[j] == 0) base[j] = atomicAdd(bcur + b, (uint32_t)__popc(peers));
+    }
+#pragma unroll
+    for (int j = 0; j < BS_ROUNDS; j++) {
+      const uint32_t bb = __shfl_sync(FULL, base[j], lead[j]);
+      if (r[j] != REC_SENTINEL) __stcs(out + bb + rank[j], r[j]);
+    }
+  }
+}
+
+cudaError_t launch_bucket_scatter(const uint64_t* in, uint64_t* out, const unsigned long long* n_dev, uint32_t n_ub,
+                                  uint32_t* bcur, const DevCounters* ctr, cudaStream_t s, Profiler* prof) {
+  if (n_ub == 0) return cudaSuccess;
+  static DeviceSetup setup;
+  static int nsm_of[RC_MAX_DEVICES], per_sm_of[RC_MAX_DEVICES];
+  int dev = 0;
+  cudaError_t se = setup.run(
+      [](int d) -> cudaError_t {
+        int per_sm = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bucket_scatter_kernel, BS_THREADS, 0);
+        if (e != cudaSuccess) return e;
+        per_sm_of[d] = std::max(per_sm, 1);
+        return cudaDeviceGetAttribute(&nsm_of[d], cudaDevAttrMultiProcessorCount, d);
+      },
+      &dev);
+  if (se != cudaSuccess) return se;
+  const uint64_t chunks = ((uint64_t)n_ub + 32 * BS_ROUNDS - 1) / (32 * BS_ROUNDS);
+  const uint32_t grid = (uint32_t)std::max<uint64_t>(
+      1, std::min<uint64_t>((chunks + BS_THREADS / 32 - 1) / (BS_THREADS / 32), (uint64_t)nsm_of[dev] * per_sm_of[dev]));
+  if (prof) prof->begin(s);
+  bucket_scatter_kernel<<<grid, BS_THREADS, 0, s>>>(in, out, n_dev, n_ub, bcur, ctr);
+  launched();
+  if (prof) prof->end(RC_PROF_SORT, s, (uint64_t)n_ub * 16, n_ub);
+  return cudaGetLastError();
+}
+
 }  // namespace rc

@@ -617,3 +617,80 @@ def test_work_groups(rc, classify):
         ins.append(rng.integers(-3, 4, size=(ins[0].shape[0], 7)).astype(np.int32))
         _, g, o = run_both(rc, pr, n, ins, fuel=500, n_groups=G, classify_rw=classify)
         assert_parity(g, o, ins)
+
+
+# ------------------------------------------------- grouping paths
+def _grouping_cases(rng):
+    """Cases that hit every branch of the log grouping: single-record cells
+    only (stencil), multi-record cells (tree, benign suite, random kernels),
+    report buffers that overflow (detect-only re-run), ragged bucket
+    boundaries (cells per instance not a multiple of 4096)."""
+    yield K.TREE_OFF_BY_ONE, 1024, I.cfg3_inputs(0, 24, 1024)
+    yield K.BENIGN["K_inc"], 256, I.cfg2_inputs(0, 40, 256)
+    yield K.BENIGN["K_Btid"], 256, I.cfg2_inputs(1, 33, 256)
+    yield K.STENCIL, 5000, I.cfg5_inputs(0, 5, 5000)
+    ins = I.cfg4_inputs(0, 6, 3000)
+    ins[3][:, 100:180] += 1
+    yield K.random_stencil_kernel(2), 3000, ins
+    for it in range(40):
+        n = int(rng.integers(1, 300))
+        pr = K.random_tiny_kernel(rng, n_arrays=2, n_regs=5, n_commands=int(rng.integers(3, 12)), size=5)
+        ins = [rng.integers(-3, 4, size=(int(rng.integers(1, 60)), 5)).astype(np.int32)]
+        ins.append(rng.integers(-3, 4, size=(ins[0].shape[0], 5)).astype(np.int32))
+        yield pr, n, ins
+
+
+@pytest.mark.parametrize("path", ["bucket", "lsd"])
+def test_grouping_paths(rc, monkeypatch, path):
+    """The bucket path (MSD scatter + per-bucket counting sort and detection,
+    the default) and the onesweep LSD path (RC_SORT_LSD=1; also taken when one
+    instance has more cells than the buckets cover) give the oracle's results,
+    also when every buffer starts tiny (grow-and-retry, detect-only re-runs)."""
+    if path == "lsd":
+        monkeypatch.setenv("RC_SORT_LSD", "1")
+    for small in (False, True):
+        if small:
+            monkeypatch.setenv("RC_DEBUG_SMALL_BUFFERS", "1")
+        rng = np.random.default_rng(11)
+        for src, n, ins in _grouping_cases(rng):
+            p, g, o = run_both(rc, src, n, ins, fuel=500 if not isinstance(src, str) else 0)
+            assert_parity(g, o, ins)
+
+
+@pytest.mark.parametrize("n", [8193, 20000])
+def test_oversized_bucket(rc, n):
+    """A bucket with more records than the shared-memory capacity (8192) is
+    counting-sorted in global scratch: every work-item reads and writes A[0]
+    (K_inc: 2n records in one cell) and writes its own B cell."""
+    src = """
+.arrays A B
+    tid   r0
+    const r1, 0
+    ld    r2, A, r1
+    add   r3, r2, r0
+    st    A, r1, r3
+    st    B, r0, r3
+    bar
+    ld    r4, B, r0
+    add   r5, r0, r1
+    st    B, r5, r4
+    exit
+"""
+    ins = [np.array([[5], [7]], np.int32), np.zeros((2, n), np.int32)]
+    p, g, o = run_both(rc, src, n, ins)
+    assert_parity(g, o, ins)
+    for src2, ins2 in [(K.BENIGN["K_inc"], I.cfg2_inputs(0, 3, n)), (K.BENIGN["K_tid"], I.cfg2_inputs(0, 2, n))]:
+        p, g, o = run_both(rc, src2, n, ins2)
+        assert_parity(g, o, ins2)
+
+
+def test_lsd_for_huge_instances(rc):
+    """One instance with more cells than the buckets cover (> 2^25) takes the
+    LSD path automatically; results as the oracle's."""
+    n = 3000
+    ins = I.cfg5_inputs(0, 1, n)
+    big = [np.zeros((1, (1 << 24) + 7), np.int32) for _ in ins]
+    for a, b in zip(ins, big):
+        b[:, :a.shape[1]] = a
+    p, g, o = run_both(rc, K.STENCIL, n, big)
+    assert_parity(g, o, big)
