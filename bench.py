@@ -2,7 +2,8 @@
 """Benchmark of the race-checking hot path.
 
 One step = one rc_run over the whole workload (all §8(a) rows: heap init,
-every barrier interval's interpretation, onesweep sort, detect + commit,
+every barrier interval's interpretation, write-set filter, grouping of the
+log by cell (bucket scatter), per-bucket sort + detect + commit,
 boundary bookkeeping, report finalize, report copy-out) plus, at N>1, the NCCL
 report gather.  Default workload = BASELINE config 5 (3-point stencil,
 2^20 work-items x 512 instances, 8 barrier intervals), STRONG scaling as
@@ -448,53 +449,61 @@ def main():
     clk_mhz = clocks.get("sm_mhz")  # median SM clock during the timed steps
     n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
     peak, peak_src = peaks()
-    roofline = roofline_interp = roofline_detect = None
+    roofline = roofline_sort = roofline_detect = None
     kernels = None
     gpu_launches = None
     if prof_sum:
         every = max(1, int(prof_sum.get("sample_every", 1)))
         s = prof_sum["sort"]
         achieved = s["alg_bytes"] / (s["ms"] / 1e3) / 1e9 if s["ms"] > 0 else None
-        traffic = None
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         tr = {}
         if os.path.exists(tpath):
             with open(tpath) as f:
                 tr = json.load(f)
-            traffic = tr.get("onesweep_kernel", {}).get("dram_bytes_per_launch")
-        roofline = {"kernel": "onesweep_kernel (K3, one LSD digit pass)", "bound": "hbm",
-                    "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak if achieved else None,
-                    "traffic": traffic, "alg_bytes_per_launch": s["alg_bytes"] / max(1, s["launches"]),
-                    "alg_bytes_per_record": 16, "launches_sampled": s["launches"],
-                    "sampling": f"CUDA events around every {every}th interval's kernels of the timed steps",
-                    "peak_source": peak_src, "library_baseline": cub_baseline()}
-        # the detect kernel (K4+K5): every sorted record read, one value
+        lsd = bool(os.environ.get("RC_SORT_LSD"))
+        sort_k = "onesweep_kernel" if lsd else "bucket_scatter_kernel"
+        det_k = "detect_kernel" if lsd else "bucket_detect_kernel"
+        roofline_sort = {"kernel": ("onesweep_kernel (K3, one LSD digit pass)" if lsd else
+                                    "bucket_scatter_kernel (K3, MSD scatter of the kept records into 4096-cell buckets)"),
+                         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if achieved else None,
+                         "traffic": tr.get(sort_k, {}).get("dram_bytes_per_launch"),
+                         "alg_bytes_per_launch": s["alg_bytes"] / max(1, s["launches"]),
+                         "alg_bytes_per_record": 16, "launches_sampled": s["launches"],
+                         "sampling": f"CUDA events around every {every}th interval's kernels of the timed steps",
+                         "peak_source": peak_src,
+                         "library_sort_same_keys": cub_baseline()}
+        # the detect kernel (K4+K5): every grouped record read, one value
         # gathered and one cell committed per write record
         dd = prof_sum["detect"]
         dach = dd["alg_bytes"] / (dd["ms"] / 1e3) / 1e9 if dd["ms"] > 0 else None
-        roofline_detect = {"kernel": "detect_kernel (K4+K5, segmented detect + commit, A4 tail)", "bound": "hbm",
-                           "achieved": dach, "peak": peak, "unit": "GB/s",
+        roofline_detect = {"kernel": (det_k + " (K4+K5, " +
+                                      ("segmented detect + commit, A4 tail)" if lsd else
+                                       "per-bucket counting sort in shared memory + segmented detect + commit, A4 tail)")),
+                           "bound": "hbm", "achieved": dach, "peak": peak, "unit": "GB/s",
                            "frac": dach / peak if dach else None,
-                           "traffic": tr.get("detect_kernel", {}).get("dram_bytes_per_launch"),
+                           "traffic": tr.get(det_k, {}).get("dram_bytes_per_launch"),
                            "alg_bytes_per_launch": dd["alg_bytes"] / max(1, dd["launches"]),
-                           "alg_bytes": "8 per sorted record + 8 per write record"}
-        # the interpreter (K1), the largest share of the step: issue-bound
-        # (ALU/LSU pipes, no contraction).  Achieved = ncu's warp instructions
-        # of one launch / (live average launch duration x SM clock x SMs);
-        # peak = 4 warp instructions per cycle per SM (4 SMSPs, 1 issue each).
+                           "alg_bytes": "8 per grouped record + 8 per write record"}
+        # the interpreter (K1), the dominant kernel (largest share of the
+        # step): issue-bound (ALU/LSU pipes, no contraction).  Achieved = ncu's
+        # warp instructions of one launch / (live average launch duration x SM
+        # clock x SMs); peak = 4 warp instructions per cycle per SM (4 SMSPs,
+        # 1 issue each).
         di = prof_sum["interp"]
         ti = tr.get("interp_kernel", {})
         ipc = None
         if di["ms"] > 0 and di["launches"] and ti.get("warp_instructions_per_launch") and clk_mhz:
             avg_s = di["ms"] / di["launches"] / 1e3
             ipc = ti["warp_instructions_per_launch"] / (avg_s * clk_mhz * 1e6 * n_sms)
-        roofline_interp = {"kernel": "interp_kernel (K1, bytecode interpreter)", "bound": "alu",
-                           "achieved": ipc, "peak": 4.0, "unit": "warp-instr/cycle/SM",
-                           "frac": ipc / 4.0 if ipc else None,
-                           "ncu_ipc_per_sm": ti.get("ipc_per_sm"),
-                           "peak_source": "B200: 4 SMSPs per SM, one warp instruction issued per SMSP per cycle",
-                           "traffic": ti.get("dram_bytes_per_launch")}
+        roofline = {"kernel": "interp_kernel (K1, bytecode interpreter; the dominant kernel)", "bound": "alu",
+                    "achieved": ipc, "peak": 4.0, "unit": "warp-instr/cycle/SM",
+                    "frac": ipc / 4.0 if ipc else None,
+                    "ncu_ipc_per_sm": ti.get("ipc_per_sm"),
+                    "peak_source": "B200: 4 SMSPs per SM, one warp instruction issued per SMSP per cycle",
+                    "traffic": ti.get("dram_bytes_per_launch"),
+                    "traffic_note": "DRAM bytes of one captured launch (heap loads, lane state, staged records)"}
         kernels = {"sample_every": every}
         for c in ("interp", "filter", "hist", "sort", "detect", "boundary", "finalize", "copy"):
             d = prof_sum[c]
@@ -530,7 +539,7 @@ def main():
                        "process_group": group_info,
                        "l2": "inputs 4.3 GB in all >> 126 MB L2 (no flush needed)",
                        "checked_accesses_per_step": acc_step, "reports_per_step": n_reports},
-            "roofline": roofline, "roofline_interp": roofline_interp, "roofline_detect": roofline_detect,
+            "roofline": roofline, "roofline_sort": roofline_sort, "roofline_detect": roofline_detect,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
             "interpreter": {"bytecode_instr_per_s": ins_step / (ms_step / 1000),
                             "bytecode_instr_per_step": ins_step,

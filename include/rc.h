@@ -165,8 +165,8 @@ typedef struct {
  * ALGORITHMIC bytes those launches must move.               */
 enum rc_prof_class {
   RC_PROF_INTERP = 0,   /* K1  interval interpretation + log append          */
-  RC_PROF_HIST = 1,     /* K2  onesweep upfront digit histograms             */
-  RC_PROF_SORT = 2,     /* K3  onesweep scatter passes                       */
+  RC_PROF_HIST = 1,     /* K2  digit histograms / bucket counts + starts     */
+  RC_PROF_SORT = 2,     /* K3  onesweep passes / bucket scatter              */
   RC_PROF_DETECT = 3,   /* K4+K5 segmented detect + commit                   */
   RC_PROF_BOUNDARY = 4, /* A4  barrier bookkeeping, divergence               */
   RC_PROF_FINALIZE = 5, /* K6  canonical report sort                         */

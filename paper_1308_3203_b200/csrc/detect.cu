@@ -492,17 +492,25 @@ __device__ __forceinline__ void bucket_smem(const DetectParams& p, BucketSmem& S
   for (int j = 0; j < BD_ITEMS; j++)
     if (r[j] != REC_SENTINEL) atomicAdd(&S.cnt[bucket_low(r[j])], 1u);
   __syncthreads();
-  // single-record cells: the commit of a lone writer (barrier release)
+  // single-record cells: the commit of a lone writer (barrier release);
+  // every value gather is issued before the first commit store
   bool multi = false;
+  int32_t val[BD_ITEMS];
 #pragma unroll
   for (int j = 0; j < BD_ITEMS; j++) {
+    val[j] = 0;
     if (r[j] == REC_SENTINEL) continue;
     if ((S.cnt[bucket_low(r[j])] & 0xFFFFu) == 1u) {
-      if (rec_w(r[j])) p.heap[rec_cell(r[j])] = rec_val<SPILL>(p, r[j]);
+      if (rec_w(r[j])) val[j] = rec_val<SPILL>(p, r[j]);
+      else r[j] = REC_SENTINEL;  // a lone read: nothing to do
     } else {
       multi = true;
+      r[j] = r[j] | (1ull << 63);  // (marked: multi-record cell; cells < 2^25 on the bucket path)
     }
   }
+#pragma unroll
+  for (int j = 0; j < BD_ITEMS; j++)
+    if (r[j] != REC_SENTINEL && !(r[j] >> 63)) p.heap[rec_cell(r[j])] = val[j];
   const bool any_multi = __syncthreads_or(multi);
   if (any_multi) {
     // counting sort of the multi-record cells' records by cell
@@ -524,9 +532,9 @@ __device__ __forceinline__ void bucket_smem(const DetectParams& p, BucketSmem& S
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < BD_ITEMS; j++) {
-      if (r[j] == REC_SENTINEL) continue;
-      uint32_t* c = &S.cnt[bucket_low(r[j])];
-      if ((*c & 0xFFFFu) > 1u) S.sorted[atomicAdd(c, 1u << 16) >> 16] = r[j];
+      if (r[j] == REC_SENTINEL || !(r[j] >> 63)) continue;
+      const uint64_t rec = r[j] & ~(1ull << 63);
+      S.sorted[atomicAdd(&S.cnt[bucket_low(rec)], 1u << 16) >> 16] = rec;
     }
     __syncthreads();
     // segmented detection over sorted[0, M): warps take 256-record chunks

@@ -10,9 +10,7 @@
 // dropping it is exact: R(c) and W(c) of every cell with W(c) != {} are
 // unchanged, and cells with W(c) = {} produce no output.
 //
-// Also computes the sort's digit histograms of the kept records (fused K2) —
-// on the bucket path the bucket counts, turned into bucket starts by the
-// last block to finish.
+// Also computes the sort's digit histograms of the kept records (fused K2).
 #include "rc_internal.h"
 
 #ifndef F_ITEMS_OPT
@@ -27,60 +25,14 @@ static_assert(F_ITEMS % 2 == 0, "two records per 16-byte load");
 
 }  // namespace
 
-// Bucket path: the last block to finish turns the bucket counts into
-// exclusive starts (and the scatter's cursors).  nb <= NB_MAX = 8192.
-__device__ __forceinline__ void bucket_offsets(const FilterParams& p) {
-  __shared__ uint32_t wsum[F_THREADS / 32];
-  __shared__ bool last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&p.ctr->f_done, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  constexpr uint32_t PER = NB_MAX / F_THREADS;  // consecutive buckets per thread
-  const uint32_t b0 = (uint32_t)t * PER;
-  uint32_t c[PER], sum = 0;
-#pragma unroll
-  for (uint32_t j = 0; j < PER; j++) {
-    c[j] = b0 + j < p.nb ? __ldcg(p.hist + b0 + j) : 0u;
-    sum += c[j];
-  }
-  uint32_t x = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(FULL, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) wsum[w] = x;
-  __syncthreads();
-  uint32_t run = x - sum;
-  for (int i = 0; i < w; i++) run += wsum[i];
-#pragma unroll
-  for (uint32_t j = 0; j < PER; j++) {
-    if (b0 + j < p.nb) {
-      p.bstart[b0 + j] = run;
-      p.bcur[b0 + j] = run;
-    }
-    run += c[j];
-  }
-}
-
-template <bool BUCKET>
 __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p) {
-  // digit / bucket counts of the block's kept records (bucket path: p.nb
-  // entries of dynamic shared memory)
-  extern __shared__ uint32_t bh_dyn[];
-  __shared__ uint32_t bh_lsd[BUCKET ? 1 : 4 * 256];
-  uint32_t* bh = BUCKET ? bh_dyn : bh_lsd;
-  const uint32_t nbins = BUCKET ? p.nb : (uint32_t)p.passes * 256u;
+  __shared__ uint32_t bh[4 * 256];
   __shared__ uint32_t wcnt[F_THREADS / 32];
   __shared__ unsigned long long sbase;
   __shared__ uint64_t sbuf[F_THREADS * F_ITEMS + 8 * F_ITEMS];
   if (p.ctr->abort) return;  // speculative interval (DevCounters::abort)
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  for (uint32_t i = t; i < nbins; i += F_THREADS) bh[i] = 0;
+  for (int i = t; i < p.passes * 256; i += F_THREADS) bh[i] = 0;
   if (blockIdx.x == 0 && t == 0) p.ctr->k1_reports = p.ctr->report_count;  // K1 is complete here
   if (p.ctr->log_overflow || p.ctr->ovl_overflow) return;  // the interval will be re-run
   // slots reserved past the buffer end only ever held sentinel padding (a real
@@ -119,24 +71,8 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
       mine += keep[j];
       kept_w += keep[j] && (rec[j] & 1);
     }
-    // digit / bucket histograms of the kept records: one shared add per run of equal digits
-    if (mine && BUCKET) {
-      uint32_t cur = 0xFFFFFFFFu, run = 0;
-#pragma unroll
-      for (int j = 0; j < F_ITEMS; j++) {
-        if (!keep[j]) continue;
-        const uint32_t d = (uint32_t)(rec[j] >> (REC_CELL_SHIFT + BUCKET_BITS));
-        if (d == cur) {
-          run++;
-        } else {
-          if (run) atomicAdd(&bh[cur], run);
-          cur = d;
-          run = 1;
-        }
-      }
-      atomicAdd(&bh[cur], run);
-    }
-    if (mine && !BUCKET) {
+    // digit histograms of the kept records: one shared add per run of equal digits
+    if (mine) {
       for (int ps = 0; ps < p.passes; ps++) {
         const int sh = REC_CELL_SHIFT + 8 * ps;
         uint32_t cur = 0xFFFFFFFFu, run = 0;
@@ -180,32 +116,27 @@ __global__ void __launch_bounds__(F_THREADS) filter_kernel(const FilterParams p)
     // correct (a stable sort by cell; detect reduces each cell's segment
     // order-independently).  Group r lives at r*(Q+8) in sbuf: the 8-word skew
     // keeps a warp's interleaved reads at two wavefronts.
-    // (bucket path: plain staging order — consecutive cells stay together
-    // for the bucket scatter's warp aggregation)
-    const uint32_t Q = BUCKET ? 0u : tot / F_ITEMS, QF = Q * F_ITEMS;
+    const uint32_t Q = tot / F_ITEMS, QF = Q * F_ITEMS;
     uint32_t pos = woff + x - mine;
 #pragma unroll
     for (int j = 0; j < F_ITEMS; j++)
       if (keep[j]) {
         uint32_t r = 0;
-        if (!BUCKET) {
 #pragma unroll
-          for (int g = 1; g <= F_ITEMS; g++) r += pos >= (uint32_t)g * Q;
-        }
-        sbuf[BUCKET ? pos : pos + 8 * r] = rec[j];
+        for (int g = 1; g <= F_ITEMS; g++) r += pos >= (uint32_t)g * Q;
+        sbuf[pos + 8 * r] = rec[j];
         pos++;
       }
     __syncthreads();
     const unsigned long long base = sbase;
     for (uint32_t i = t; i < tot; i += F_THREADS)
-      p.out[base + i] = BUCKET ? sbuf[i] : sbuf[i < QF ? (i % F_ITEMS) * (Q + 8) + i / F_ITEMS : i + 8 * F_ITEMS];
+      p.out[base + i] = sbuf[i < QF ? (i % F_ITEMS) * (Q + 8) + i / F_ITEMS : i + 8 * F_ITEMS];
     __syncthreads();  // wcnt / sbase / sbuf reuse
   }
-  for (uint32_t i = t; i < nbins; i += F_THREADS)
+  for (int i = t; i < p.passes * 256; i += F_THREADS)
     if (bh[i]) atomicAdd(&p.hist[i], bh[i]);
   for (int o = 16; o > 0; o >>= 1) kept_w += __shfl_xor_sync(FULL, kept_w, o);
   if (lane == 0 && kept_w) atomicAdd(&p.ctr->kept_writes, (unsigned long long)kept_w);
-  if (BUCKET) bucket_offsets(p);
 }
 
 cudaError_t launch_filter(const FilterParams& p, cudaStream_t s) {
@@ -220,12 +151,7 @@ cudaError_t launch_filter(const FilterParams& p, cudaStream_t s) {
   const int nsm = nsm_of[dev];
   const uint64_t per_block = (uint64_t)F_THREADS * F_ITEMS;
   const uint32_t grid = (uint32_t)std::min<uint64_t>((p.n_slots + per_block - 1) / per_block, (uint64_t)nsm * 8);
-  if (p.nb) {
-    if (p.nb > NB_MAX) return cudaErrorInvalidValue;
-    filter_kernel<true><<<grid, F_THREADS, p.nb * sizeof(uint32_t), s>>>(p);
-  } else {
-    filter_kernel<false><<<grid, F_THREADS, 0, s>>>(p);
-  }
+  filter_kernel<<<grid, F_THREADS, 0, s>>>(p);
   launched();
   return cudaGetLastError();
 }

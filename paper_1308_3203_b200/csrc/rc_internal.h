@@ -115,8 +115,8 @@ struct DevCounters {
   unsigned long long k1_reports;    // report_count after K1 (snapshot taken by the filter)
   unsigned long long rw_reports;    // RW reports emitted by detect (RC_OPT_CLASSIFY_RW)
   unsigned long long kept_writes;   // write records among the kept ones (profile bytes of detect)
-  unsigned int f_done;              // filter blocks finished (last-block pattern: bucket offsets)
   unsigned int bucket_next;         // next bucket to claim (bucket detect)
+  unsigned int count_done;          // bucket_count blocks finished (last-block pattern: the bucket starts)
   // ---- fields above: zeroed per interval attempt (one memset, runtime.cu)
   unsigned long long report_count;  // reports appended (whole run, rolled back on retry)
   unsigned long long lanes_final[8];
@@ -237,11 +237,9 @@ struct FilterParams {
   const uint8_t* wmap;
   uint8_t wtag;           // wmap[c] == wtag: c written in this interval
   uint64_t* out;          // sort buffer, [0, kept_count)
-  uint32_t* hist;         // LSD: [4][256] digit counts; bucket path: [nb] bucket counts
-  int passes;             // LSD passes (0 on the bucket path)
-  uint32_t nb;            // bucket path: buckets (cell >> BUCKET_BITS) of the batch, <= NB_MAX; 0: LSD
-  uint32_t* bstart;       // bucket path: [nb] exclusive starts (written by the filter's last block)
-  uint32_t* bcur;         // bucket path: [nb] scatter cursors (= bstart, advanced by the scatter)
+  uint32_t* hist;         // [4][256] digit counts
+  int passes;
+
   DevCounters* ctr;
   uint32_t n_slots;       // staging buffer capacity (slots); the kernel reads stage_count
   bool keep_all;          // RC_OPT_KEEP_ALL_READS: only drop the sentinels
@@ -314,9 +312,26 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n_ub, const unsigned long lon
                           const unsigned long long* n_b, int bits, SortWorkspace& ws, cudaStream_t s, bool* in_alt,
                           Profiler* prof, bool hist_ready);
 
-// bucket scatter: records [0, *n_dev) of `in` to out[bcur[bucket]++] (any order inside a bucket)
-cudaError_t launch_bucket_scatter(const uint64_t* in, uint64_t* out, const unsigned long long* n_dev, uint32_t n_ub,
-                                  uint32_t* bcur, const DevCounters* ctr, cudaStream_t s, Profiler* prof);
+// bucket scatter (K3 on the bucket path, fused with the write-set filter):
+// from the staging buffer keep every write record and the reads of cells
+// written in this interval (as the filter), drop sentinels, and place each
+// kept record at out[bcur[bucket]++] (any order inside a bucket)
+struct ScatterParams {
+  const uint64_t* stage;
+  uint32_t n_slots;       // staging capacity; the kernel reads stage_count
+  const uint8_t* wmap;
+  uint8_t wtag;
+  bool keep_all;          // RC_OPT_KEEP_ALL_READS
+  uint64_t* out;
+  uint32_t* bcur;
+  DevCounters* ctr;
+};
+cudaError_t launch_bucket_scatter(const ScatterParams& p, cudaStream_t s, Profiler* prof);
+// bucket_count: the kept records of the staging buffer per bucket into
+// hist[0, nb) (zeroed by the caller); the last block to finish writes the
+// exclusive starts to bstart and bcur (= ScatterParams::bcur).
+cudaError_t launch_bucket_count(const ScatterParams& p, uint32_t* hist, uint32_t nb, uint32_t* bstart,
+                                cudaStream_t s, Profiler* prof);
 cudaError_t launch_detect(const DetectParams& p, cudaStream_t s);
 // RW classification helpers (detect.cu): mark the cells of the RW reports in
 // reports[r0, r1) (instance ids relative to inst_base), compare two heaps per

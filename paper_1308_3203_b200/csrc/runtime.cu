@@ -515,35 +515,44 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     const uint64_t bcells = (uint64_t)nb * cpi;
     const uint64_t* sr = nullptr;  // sorted log of the last enqueued interval
     const uint32_t nbk = bucket ? (uint32_t)std::max<uint64_t>(1, (bcells + BUCKET_CELLS - 1) / BUCKET_CELLS) : 0u;
-    // the sort of one interval's kept records (K3): bucket scatter, or the onesweep passes
-    auto enqueue_sort = [&](Profiler* prof) -> cudaError_t {
+    // write-set filter + grouping of one interval's records by cell (K3): the
+    // bucket scatter (filter fused), or the filter and the onesweep passes
+    auto enqueue_sort = [&](Profiler* prof, bool keep_all) -> cudaError_t {
       if (bucket) {
-        sr = W.log_alt.as<uint64_t>();
-        return launch_bucket_scatter(W.log.as<uint64_t>(), W.log_alt.as<uint64_t>(), &dctr->kept_count,
-                                     (uint32_t)log_cap, W.buckets.as<uint32_t>() + NB_MAX, dctr, s, prof);
+        sr = W.log.as<uint64_t>();
+        ScatterParams sp;
+        sp.stage = W.log_alt.as<uint64_t>();
+        sp.n_slots = (uint32_t)log_cap;  // upper bound; the kernel reads stage_count
+        sp.wmap = W.wmap.as<uint8_t>();
+        sp.wtag = W.wtag;
+        sp.keep_all = keep_all;
+        sp.out = W.log.as<uint64_t>();
+        sp.bcur = W.buckets.as<uint32_t>() + NB_MAX;
+        sp.ctr = dctr;
+        cudaError_t e = launch_bucket_count(sp, W.sort.hist, nbk, W.buckets.as<uint32_t>(), s, prof);
+        if (e != cudaSuccess) return e;
+        return launch_bucket_scatter(sp, s, prof);
       }
-      bool in_alt = false;
-      W.sort.alt = W.log_alt.as<uint64_t>();
-      cudaError_t e = onesweep_sort(W.log.as<uint64_t>(), (uint32_t)log_cap, &dctr->kept_count, nullptr, key_bits,
-                                    W.sort, s, &in_alt, prof, /*hist_ready=*/true);
-      sr = in_alt ? W.log_alt.as<uint64_t>() : W.log.as<uint64_t>();
-      return e;
-    };
-    auto filter_params = [&]() {
       FilterParams fp;
       fp.stage = W.log_alt.as<uint64_t>();
       fp.wmap = W.wmap.as<uint8_t>();
       fp.wtag = W.wtag;
       fp.out = W.log.as<uint64_t>();
       fp.hist = W.sort.hist;
-      fp.passes = bucket ? 0 : passes;
-      fp.nb = nbk;
-      fp.bstart = W.buckets.as<uint32_t>();
-      fp.bcur = W.buckets.as<uint32_t>() + NB_MAX;
+      fp.passes = passes;
       fp.ctr = dctr;
       fp.n_slots = (uint32_t)log_cap;  // upper bound; the kernel reads stage_count
-      fp.keep_all = false;
-      return fp;
+      fp.keep_all = keep_all;
+      if (prof) prof->begin(s);
+      cudaError_t e = launch_filter(fp, s);
+      if (prof) prof->end(RC_PROF_FILTER, s, 0, 0);
+      if (e != cudaSuccess) return e;
+      bool in_alt = false;
+      W.sort.alt = W.log_alt.as<uint64_t>();
+      e = onesweep_sort(W.log.as<uint64_t>(), (uint32_t)log_cap, &dctr->kept_count, nullptr, key_bits, W.sort, s,
+                        &in_alt, prof, /*hist_ready=*/true);
+      sr = in_alt ? W.log_alt.as<uint64_t>() : W.log.as<uint64_t>();
+      return e;
     };
     if (G > 1) CK(ig_reset(W.ig.as<uint32_t>(), bcells, s));
     auto bparams = [&](uint32_t interval) {
@@ -602,7 +611,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       dp.nb = nbk;
       dp.bstart = W.buckets.as<uint32_t>();
       dp.bend = W.buckets.as<uint32_t>() + NB_MAX;
-      dp.tmp = W.log.as<uint64_t>();
+      dp.tmp = W.log_alt.as<uint64_t>();  // (the staging buffer: free once the scatter has read it)
       return dp;
     };
     struct Marks { size_t m0 = 0, m1 = 0; };
@@ -688,13 +697,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         EQ(launch_ig_accumulate(W.log_alt.as<uint64_t>(), dctr, log_cap, W.ig.as<uint32_t>(), bcells, n,
                                 (uint32_t)cpi, gi * n, s));
       // ---- write-set filter: writes + reads of written cells, dense, with histograms
-      FilterParams fp = filter_params();
-      fp.keep_all = (opt.flags & RC_OPT_KEEP_ALL_READS) != 0;
-      W.prof.begin(s);
-      EQ(launch_filter(fp, s));
-      W.prof.end(RC_PROF_FILTER, s, 0, 0);
-      // ---- K3: group the kept records by cell
-      EQ(enqueue_sort(W.prof.on ? &W.prof : nullptr));
+      // ---- write-set filter + K3: group the kept records by cell
+      EQ(enqueue_sort(W.prof.on ? &W.prof : nullptr, (opt.flags & RC_OPT_KEEP_ALL_READS) != 0));
       // ---- K4+K5 detect + commit, A4 check + verdict
       DetectParams dp = detect_params(kk);
       dp.with_boundary = true;  // A4 as detect's tail: consumes (and resets) K1's per-instance node ranges
@@ -743,9 +747,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         ip.status_out = W.status_b.as<uint8_t>();
         ip.report_cap = 0;  // error reports of the re-run are not written (the count is restored below)
         EQ(launch_interp(ip, s));
-        FilterParams fp = filter_params();
-        EQ(launch_filter(fp, s));
-        EQ(enqueue_sort(nullptr));  // (the classified interval's own sorted log is not needed again)
+        EQ(enqueue_sort(nullptr, false));  // (the classified interval's own sorted log is not needed again)
         DetectParams dp = detect_params(kk);
         dp.heap = W.heapB.as<int32_t>();
         dp.quiet = true;
@@ -869,9 +871,12 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       if (W.prof.on) {  // exact record counts are known now: fix this interval's profile bytes
         for (size_t i = mk_cur.m0; i < mk_cur.m1; i++) {
           Profiler::Mark& m = W.prof.marks[i];
-          if (m.cls == RC_PROF_SORT) { m.bytes = Ns * 16; m.items = Ns; }
+          // the sort: LSD 16 B per record and pass; the bucket scatter reads
+          // every staging slot and writes every kept record
+          if (m.cls == RC_PROF_SORT) { m.bytes = bucket ? Nslots * 8 + Ns * 8 : Ns * 16; m.items = Ns; }
           // detect: every record read, a value gathered and a cell committed per write record
           if (m.cls == RC_PROF_DETECT) { m.bytes = Ns * 8 + h.kept_writes * 8; m.items = Ns; }
+          if (m.cls == RC_PROF_HIST && bucket) { m.bytes = Nslots * 8; m.items = Nslots; }  // bucket counts
           if (m.cls == RC_PROF_FILTER) { m.bytes = Nslots * 8 + h.staged_recs + Ns * 8; m.items = Nslots; }
         }
       }

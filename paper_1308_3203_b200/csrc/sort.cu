@@ -521,28 +521,148 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, const unsigned long long* 
   return cudaGetLastError();
 }
 
+// ---- K2 on the bucket path: bucket counts of the kept records + starts ------
+// The staging buffer is read as by the scatter (same slots, same write-set
+// filter rule); a warp's rounds of one bucket are summed in registers and
+// flushed when the bucket changes (records come in lane order: long runs),
+// other rounds add per group of equal buckets (__match_any_sync).  The last
+// block to finish turns the counts into the buckets' exclusive starts
+// (bstart) and the scatter's cursors (bcur).
+constexpr int BC_THREADS = 512;
+constexpr int BC_ROUNDS = 8;
+__device__ __forceinline__ bool scatter_keep(const ScatterParams& p, uint64_t r) {
+  return r != REC_SENTINEL &&
+         ((r & 1) || p.keep_all || __ldg(p.wmap + (uint32_t)(r >> REC_CELL_SHIFT)) == p.wtag);
+}
+__global__ void __launch_bounds__(BC_THREADS) bucket_count_kernel(const ScatterParams p, uint32_t* __restrict__ hist,
+                                                                   uint32_t nb, uint32_t* __restrict__ bstart) {
+  DevCounters* ctr = p.ctr;
+  if (ctr->abort || ctr->log_overflow || ctr->ovl_overflow) return;  // grid-uniform
+  const uint32_t n = (uint32_t)umin64(ctr->stage_count, p.n_slots);
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const uint32_t warps = gridDim.x * (BC_THREADS / 32);
+  uint32_t run_b = 0xFFFFFFFFu, run_n = 0;  // (warp-uniform) the open run of one-bucket rounds
+  for (uint32_t c = blockIdx.x * (BC_THREADS / 32) + w; (uint64_t)c * (32 * BC_ROUNDS) < n; c += warps) {
+    const uint32_t c0 = c * (32 * BC_ROUNDS);
+    uint64_t r[BC_ROUNDS];
+#pragma unroll
+    for (int j = 0; j < BC_ROUNDS; j++) {
+      const uint32_t i = c0 + j * 32 + lane;
+      r[j] = i < n ? __ldg(p.stage + i) : REC_SENTINEL;
+    }
+#pragma unroll
+    for (int j = 0; j < BC_ROUNDS; j++) {
+      const bool keep = scatter_keep(p, r[j]);
+      const uint32_t b = keep ? (uint32_t)(r[j] >> (REC_CELL_SHIFT + BUCKET_BITS)) : 0xFFFFFFFFu;
+      const unsigned km = __ballot_sync(FULL, keep);
+      if (!km) continue;
+      const uint32_t b0 = __shfl_sync(FULL, b, __ffs(km) - 1);
+      if (__all_sync(FULL, !keep || b == b0)) {
+        if (b0 != run_b) {
+          if (lane == 0 && run_n) atomicAdd(hist + run_b, run_n);
+          run_b = b0;
+          run_n = 0;
+        }
+        run_n += __popc(km);
+      } else {
+        const unsigned peers = __match_any_sync(FULL, b);
+        if (keep && (peers & lanemask_lt()) == 0) atomicAdd(hist + b, (uint32_t)__popc(peers));
+      }
+    }
+  }
+  if (lane == 0 && run_n) atomicAdd(hist + run_b, run_n);
+  // the last block: exclusive scan of the counts (nb <= NB_MAX)
+  __shared__ uint32_t wsum[BC_THREADS / 32];
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (t == 0) last = atomicAdd(&ctr->count_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  constexpr int PER = NB_MAX / BC_THREADS;
+  uint32_t v[PER], sum = 0;
+#pragma unroll
+  for (int k = 0; k < PER; k++) {
+    const uint32_t b = (uint32_t)t * PER + k;
+    v[k] = b < nb ? __ldcg(hist + b) : 0u;
+    sum += v[k];
+  }
+  uint32_t x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  uint32_t run = x - sum;
+  for (int i = 0; i < w; i++) run += wsum[i];
+#pragma unroll
+  for (int k = 0; k < PER; k++) {
+    const uint32_t b = (uint32_t)t * PER + k;
+    if (b < nb) {
+      bstart[b] = run;
+      p.bcur[b] = run;
+    }
+    run += v[k];
+  }
+}
+
+cudaError_t launch_bucket_count(const ScatterParams& p, uint32_t* hist, uint32_t nb, uint32_t* bstart,
+                                cudaStream_t s, Profiler* prof) {
+  if (nb == 0 || nb > NB_MAX) return nb ? cudaErrorInvalidValue : cudaSuccess;
+  static DeviceSetup setup;
+  static int nsm_of[RC_MAX_DEVICES], per_sm_of[RC_MAX_DEVICES];
+  int dev = 0;
+  cudaError_t se = setup.run(
+      [](int d) -> cudaError_t {
+        int per_sm = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bucket_count_kernel, BC_THREADS, 0);
+        if (e != cudaSuccess) return e;
+        per_sm_of[d] = std::max(per_sm, 1);
+        return cudaDeviceGetAttribute(&nsm_of[d], cudaDevAttrMultiProcessorCount, d);
+      },
+      &dev);
+  if (se != cudaSuccess) return se;
+  const uint64_t chunks = ((uint64_t)std::max<uint32_t>(p.n_slots, 1) + 32 * BC_ROUNDS - 1) / (32 * BC_ROUNDS);
+  const uint32_t grid = (uint32_t)std::max<uint64_t>(
+      1, std::min<uint64_t>((chunks + BC_THREADS / 32 - 1) / (BC_THREADS / 32), (uint64_t)nsm_of[dev] * per_sm_of[dev]));
+  if (prof) prof->begin(s);
+  bucket_count_kernel<<<grid, BC_THREADS, 0, s>>>(p, hist, nb, bstart);
+  launched();
+  if (prof) prof->end(RC_PROF_HIST, s, (uint64_t)p.n_slots * 8, p.n_slots);
+  return cudaGetLastError();
+}
+
 // ---- K3 on the bucket path: one MSD scatter on the high cell bits ----------
-// Record i goes to out[bcur[bucket]++], bucket = cell >> BUCKET_BITS; the
-// filter's last block set bcur to the buckets' exclusive starts.  The order
-// inside a bucket is arbitrary (bucket_detect sorts each bucket by its low
-// bits, and the detection only uses order-independent reductions inside a
-// cell).  A warp takes BS_ROUNDS rounds of 32 consecutive records (all loads
-// in flight), groups each round's lanes by bucket (one vote when the round is
-// one bucket — the common case, records come in staging order — else
+// Fused with the write-set filter (filter.cu, the same rule): from the
+// staging buffer every write record and every read of a cell written in this
+// interval goes to out[bcur[bucket]++], bucket = cell >> BUCKET_BITS (bucket_count
+// counted the kept records per bucket and set bcur to the buckets' starts).
+// Sentinels and the other reads are dropped: a read of a cell no work-item
+// wrote can take part in no report and no commit.  The
+// order inside a bucket is arbitrary (bucket_detect sorts each bucket by its
+// low bits; the detection only uses order-independent reductions inside a
+// cell).  A warp takes BS_ROUNDS rounds of 32 consecutive slots (all loads in
+// flight), groups each round's kept lanes by bucket (one vote when the round
+// is one bucket — the common case, K1 stages in lane order — else
 // __match_any_sync), and the group leader reserves the group's slots with one
-// atomic; the atomics of all rounds are issued before any of them is waited on.
+// atomic; the atomics of all rounds are issued before any result is used.
 constexpr int BS_ROUNDS = 8;
 constexpr int BS_THREADS = 256;
-__global__ void __launch_bounds__(BS_THREADS) bucket_scatter_kernel(const uint64_t* __restrict__ in,
-                                                                     uint64_t* __restrict__ out,
-                                                                     const unsigned long long* n_dev, uint32_t n_ub,
-                                                                     uint32_t* __restrict__ bcur,
-                                                                     const DevCounters* ctr) {
-  if (ctr->abort || ctr->log_overflow || ctr->ovl_overflow) return;  // (as the filter: nothing to group)
-  const uint32_t n = dev_count(n_ub, n_dev, nullptr);
+__global__ void __launch_bounds__(BS_THREADS) bucket_scatter_kernel(const ScatterParams p) {
+  const DevCounters* ctr = p.ctr;
+  if (ctr->abort) return;  // speculative interval (DevCounters::abort)
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.ctr->k1_reports = p.ctr->report_count;  // K1 is complete here
+  if (ctr->log_overflow || ctr->ovl_overflow) return;  // the interval will be re-run
+  // slots reserved past the buffer end only ever held sentinel padding (a
+  // real record there sets log_overflow): clamp to the capacity
+  const uint32_t n = (uint32_t)umin64(ctr->stage_count, p.n_slots);
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (BS_THREADS / 32);
   const unsigned lt = lanemask_lt();
+  uint32_t kept = 0, kept_w = 0;  // lane 0: the warp's kept records / write records
   for (uint32_t c = blockIdx.x * (BS_THREADS / 32) + (threadIdx.x >> 5); (uint64_t)c * (32 * BS_ROUNDS) < n;
        c += warps) {
     const uint32_t c0 = c * (32 * BS_ROUNDS);
@@ -550,8 +670,11 @@ __global__ void __launch_bounds__(BS_THREADS) bucket_scatter_kernel(const uint64
 #pragma unroll
     for (int j = 0; j < BS_ROUNDS; j++) {
       const uint32_t i = c0 + j * 32 + lane;
-      r[j] = i < n ? __ldcs(in + i) : REC_SENTINEL;  // (streamed: read once)
+      r[j] = i < n ? __ldcs(p.stage + i) : REC_SENTINEL;  // (streamed: read once)
     }
+#pragma unroll
+    for (int j = 0; j < BS_ROUNDS; j++)  // the write-set filter
+      if (!scatter_keep(p, r[j])) r[j] = REC_SENTINEL;
     uint32_t base[BS_ROUNDS], rank[BS_ROUNDS], lead[BS_ROUNDS];
 #pragma unroll
     for (int j = 0; j < BS_ROUNDS; j++) {
@@ -563,19 +686,24 @@ __global__ void __launch_bounds__(BS_THREADS) bucket_scatter_kernel(const uint64
       lead[j] = __ffs(peers) - 1;
       rank[j] = __popc(peers & lt);
       base[j] = 0;
-      if (r[j] != REC_SENTINEL && rank[j] == 0) base[j] = atomicAdd(bcur + b, (uint32_t)__popc(peers));
+      if (r[j] != REC_SENTINEL && rank[j] == 0) base[j] = atomicAdd(p.bcur + b, (uint32_t)__popc(peers));
+      kept += __popc(__ballot_sync(FULL, r[j] != REC_SENTINEL));
+      kept_w += __popc(__ballot_sync(FULL, r[j] != REC_SENTINEL && (r[j] & 1)));
     }
 #pragma unroll
     for (int j = 0; j < BS_ROUNDS; j++) {
       const uint32_t bb = __shfl_sync(FULL, base[j], lead[j]);
-      if (r[j] != REC_SENTINEL) __stcs(out + bb + rank[j], r[j]);
+      if (r[j] != REC_SENTINEL) __stcs(p.out + bb + rank[j], r[j]);
     }
+  }
+  if (lane == 0 && kept) {
+    atomicAdd(&p.ctr->kept_count, (unsigned long long)kept);
+    if (kept_w) atomicAdd(&p.ctr->kept_writes, (unsigned long long)kept_w);
   }
 }
 
-cudaError_t launch_bucket_scatter(const uint64_t* in, uint64_t* out, const unsigned long long* n_dev, uint32_t n_ub,
-                                  uint32_t* bcur, const DevCounters* ctr, cudaStream_t s, Profiler* prof) {
-  if (n_ub == 0) return cudaSuccess;
+cudaError_t launch_bucket_scatter(const ScatterParams& p, cudaStream_t s, Profiler* prof) {
+  if (p.n_slots == 0) return cudaSuccess;
   static DeviceSetup setup;
   static int nsm_of[RC_MAX_DEVICES], per_sm_of[RC_MAX_DEVICES];
   int dev = 0;
@@ -589,13 +717,13 @@ cudaError_t launch_bucket_scatter(const uint64_t* in, uint64_t* out, const unsig
       },
       &dev);
   if (se != cudaSuccess) return se;
-  const uint64_t chunks = ((uint64_t)n_ub + 32 * BS_ROUNDS - 1) / (32 * BS_ROUNDS);
+  const uint64_t chunks = ((uint64_t)p.n_slots + 32 * BS_ROUNDS - 1) / (32 * BS_ROUNDS);
   const uint32_t grid = (uint32_t)std::max<uint64_t>(
       1, std::min<uint64_t>((chunks + BS_THREADS / 32 - 1) / (BS_THREADS / 32), (uint64_t)nsm_of[dev] * per_sm_of[dev]));
   if (prof) prof->begin(s);
-  bucket_scatter_kernel<<<grid, BS_THREADS, 0, s>>>(in, out, n_dev, n_ub, bcur, ctr);
+  bucket_scatter_kernel<<<grid, BS_THREADS, 0, s>>>(p);
   launched();
-  if (prof) prof->end(RC_PROF_SORT, s, (uint64_t)n_ub * 16, n_ub);
+  if (prof) prof->end(RC_PROF_SORT, s, (uint64_t)p.n_slots * 16, p.n_slots);
   return cudaGetLastError();
 }
 

@@ -2,7 +2,8 @@
 # Quick GPU-box pass: smoke, the fast gpu tests, and short bench A/B lines
 # (default path vs the env variants given as arguments, e.g. RC_SORT_LSD=1).
 mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke=$?"; tail -3 gpurun_out/smoke.log
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { echo "build failed"; tail -20 gpurun_out/build.log; exit 1; }
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke=$?"; tail -3 gpurun_out/smoke.log
 if [ "${TESTS:-1}" != "0" ]; then
   timeout 1200 python -m pytest tests -m gpu -x -q -k "not slow" ${PYTEST_ARGS} > gpurun_out/gpu_tests.log 2>&1; echo "tests=$?"; tail -15 gpurun_out/gpu_tests.log
 fi

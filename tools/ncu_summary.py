@@ -6,7 +6,7 @@
 * launches.csv (the `--metrics gpu__time_duration.sum` launch list of a bench
   command) -> per-kernel count / total / share / average.
 * *.ncu-rep (`--set full` captures) -> key metrics, stall reasons, hottest
-  SASS lines; the onesweep capture also refreshes profiles/ncu_traffic.json
+  SASS lines; every capture also refreshes profiles/ncu_traffic.json
   (DRAM bytes of that launch, read by bench.py for roofline.traffic).
 """
 from __future__ import annotations
@@ -108,14 +108,16 @@ def main():
         s, d = summarize_rep(rep)
         open(os.path.join(PROF, f"{a.round}{tag}_ncu_{base}.txt"), "w").write(s + "\n")
         print(s)
-        if base in ("prof_onesweep", "prof_detect", "prof_interp"):
+        names = {"prof_onesweep": "onesweep_kernel", "prof_detect": "detect_kernel", "prof_interp": "interp_kernel",
+                 "prof_bucket_scatter": "bucket_scatter_kernel", "prof_bucket_detect": "bucket_detect_kernel",
+                 "prof_filter": "filter_kernel"}
+        if base in names:
             mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             byts = sum(float(d[k].replace(",", "")) * mult[d["_units"][k]]
                        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
             path = os.path.join(PROF, "ncu_traffic.json")
             tr = json.load(open(path)) if os.path.exists(path) else {}
-            name = {"prof_onesweep": "onesweep_kernel", "prof_detect": "detect_kernel",
-                    "prof_interp": "interp_kernel"}[base]
+            name = names[base]
             tr[name] = {"dram_bytes_per_launch": byts,
                         "warp_instructions_per_launch": float(d["smsp__inst_executed.sum"].replace(",", "")),
                         "ipc_per_sm": float(d["sm__inst_executed.avg.per_cycle_active"].replace(",", "")),
