@@ -428,8 +428,8 @@ __global__ void __launch_bounds__(256, DET_MINB) detect_kernel(const DetectParam
 
 // ---- K4+K5 on the bucket path -------------------------------
 // A bucket = the records of BUCKET_CELLS consecutive cells (bucket_scatter,
-// sort.cu, grouped them in arbitrary order).  A block claims buckets from a
-// counter.  A bucket of <= BD_CAP records is loaded into registers and
+// sort.cu, grouped them in arbitrary order).  Block j takes buckets j,
+// j + G, j + 2G, ... (G blocks).  A bucket of <= BD_CAP records is loaded into registers and
 // counted per cell in shared memory; a cell with one record only commits (a
 // lone writer can race with nobody, a lone read does nothing); the records of
 // the other cells are placed by cell into shared memory (a counting sort on
@@ -437,17 +437,24 @@ __global__ void __launch_bounds__(256, DET_MINB) detect_kernel(const DetectParam
 // A larger bucket is counting-sorted into global scratch (`tmp`) and detected
 // there.  Any order inside a cell is fine: every statistic is
 // order-independent.
-constexpr int BD_THREADS = 512;
+#ifndef BD_THREADS_OPT
+#define BD_THREADS_OPT 512
+#endif
+constexpr int BD_THREADS = BD_THREADS_OPT;
 constexpr int BD_ITEMS = 16;
+constexpr int BD_MINB = 1024 / BD_THREADS;  // resident blocks per SM (64 registers per thread)
 constexpr uint32_t BD_CAP = BD_THREADS * BD_ITEMS;  // records of a bucket held in registers
 constexpr int BD_WARPS = BD_THREADS / 32;
 constexpr int BD_ROUNDS = 2;  // 32-record rounds per detection chunk (the records are in shared memory / L2)
 struct BucketSmem {
   uint64_t sorted[BD_CAP];      // records of the bucket's multi-record cells, by cell (global path: u32 offsets)
-  uint32_t cnt[BUCKET_CELLS];   // per cell: record count (bits 0-15), then | start << 16 during the placement
+  uint32_t cnt[BUCKET_CELLS + 4];  // per cell: record count (bits 0-15), then | start << 16 during the
+                                   // placement; [BUCKET_CELLS]: the spare counter of absent items
   uint32_t wsum[BD_WARPS];
-  uint32_t bucket[2];           // claimed buckets (current, next)
+  uint32_t ls0[32], lm[32];     // the block's non-empty buckets: start, record count
+  uint32_t nlist;
 };
+constexpr int BD_LIST = 32;  // buckets per block (blockIdx.x + i * gridDim.x, i < BD_LIST)
 __device__ __forceinline__ uint32_t bucket_low(uint64_t r) {
   return (uint32_t)(r >> REC_CELL_SHIFT) & (BUCKET_CELLS - 1);
 }
@@ -479,75 +486,78 @@ __device__ __forceinline__ uint32_t bd_scan8(const uint32_t (&v)[BUCKET_CELLS / 
   return run;
 }
 
+// The bucket's cells with more than one record (S.cnt holds every cell's
+// count): their records, re-read from L2, are placed by cell into shared
+// memory (a counting sort on the low BUCKET_BITS bits) and run through the
+// segmented detection.  Out of line: the single-record path stays lean.
 template <bool SPILL>
+__device__ __noinline__ void bucket_multi(const DetectParams& p, BucketSmem& S, uint32_t s0, uint32_t m) {
+  const int t = threadIdx.x;
+  constexpr int PER = BUCKET_CELLS / BD_THREADS;
+  uint32_t v[PER];
+#pragma unroll
+  for (int k = 0; k < PER; k++) {
+    const uint32_t c = S.cnt[t * PER + k] & 0xFFFFu;
+    v[k] = c > 1 ? c : 0u;
+  }
+  uint32_t M = 0;
+  uint32_t run = bd_scan8(v, S.wsum, &M);
+#pragma unroll
+  for (int k = 0; k < PER; k++)
+    if (v[k]) {
+      S.cnt[t * PER + k] = (run << 16) | v[k];
+      run += v[k];
+    }
+  __syncthreads();
+  for (uint32_t i = t; i < m; i += BD_THREADS) {
+    const uint64_t r = __ldcg(p.recs + s0 + i);
+    uint32_t* c = &S.cnt[bucket_low(r)];
+    if ((*c & 0xFFFFu) > 1u) S.sorted[atomicAdd(c, 1u << 16) >> 16] = r;
+  }
+  __syncthreads();
+  // segmented detection over sorted[0, M): warps take 64-record chunks
+  const SrcSmem src{S.sorted};
+  for (uint32_t wg = (uint32_t)t >> 5; wg * (32 * BD_ROUNDS) < M; wg += BD_WARPS) {
+    Chunk<BD_ROUNDS> ch;
+    load_chunk(src, wg, M, ch);
+    detect_chunk<SPILL>(p, src, wg, M, ch);
+  }
+  __syncthreads();
+}
+
+template <bool SPILL, int ITEMS>
 __device__ __forceinline__ void bucket_smem(const DetectParams& p, BucketSmem& S, uint32_t s0, uint32_t m) {
   const int t = threadIdx.x;
-  uint64_t r[BD_ITEMS];
+  uint64_t r[ITEMS];
 #pragma unroll
-  for (int j = 0; j < BD_ITEMS; j++) {
+  for (int j = 0; j < ITEMS; j++) {
     const uint32_t i = t + j * BD_THREADS;
-    r[j] = i < m ? __ldcs(p.recs + s0 + i) : REC_SENTINEL;  // (read once)
+    r[j] = i < m ? __ldg(p.recs + s0 + i) : REC_SENTINEL;
   }
+  // the final values of the write records, gathered while the cells are
+  // counted (used for the lone writers' commits; detect_chunk re-reads the
+  // others')
+  int32_t val[ITEMS];
 #pragma unroll
-  for (int j = 0; j < BD_ITEMS; j++)
-    if (r[j] != REC_SENTINEL) atomicAdd(&S.cnt[bucket_low(r[j])], 1u);
+  for (int j = 0; j < ITEMS; j++) val[j] = (r[j] != REC_SENTINEL && rec_w(r[j])) ? rec_val<SPILL>(p, r[j]) : 0;
+  // (an absent item counts into the spare counter: no branch per item)
+#pragma unroll
+  for (int j = 0; j < ITEMS; j++) atomicAdd(&S.cnt[r[j] != REC_SENTINEL ? bucket_low(r[j]) : BUCKET_CELLS], 1u);
   __syncthreads();
-  // single-record cells: the commit of a lone writer (barrier release);
-  // every value gather is issued before the first commit store
+  // single-record cells: the commit of a lone writer (barrier release)
   bool multi = false;
-  int32_t val[BD_ITEMS];
 #pragma unroll
-  for (int j = 0; j < BD_ITEMS; j++) {
-    val[j] = 0;
-    if (r[j] == REC_SENTINEL) continue;
-    if ((S.cnt[bucket_low(r[j])] & 0xFFFFu) == 1u) {
-      if (rec_w(r[j])) val[j] = rec_val<SPILL>(p, r[j]);
-      else r[j] = REC_SENTINEL;  // a lone read: nothing to do
-    } else {
-      multi = true;
-      r[j] = r[j] | (1ull << 63);  // (marked: multi-record cell; cells < 2^25 on the bucket path)
-    }
+  for (int j = 0; j < ITEMS; j++) {
+    const bool ok = r[j] != REC_SENTINEL;
+    const bool lone = (S.cnt[ok ? bucket_low(r[j]) : BUCKET_CELLS] & 0xFFFFu) == 1u;
+    if (ok && lone && rec_w(r[j])) p.heap[rec_cell(r[j])] = val[j];
+    multi |= ok && !lone;
   }
-#pragma unroll
-  for (int j = 0; j < BD_ITEMS; j++)
-    if (r[j] != REC_SENTINEL && !(r[j] >> 63)) p.heap[rec_cell(r[j])] = val[j];
-  const bool any_multi = __syncthreads_or(multi);
-  if (any_multi) {
-    // counting sort of the multi-record cells' records by cell
-    constexpr int PER = BUCKET_CELLS / BD_THREADS;
-    uint32_t v[PER];
-#pragma unroll
-    for (int k = 0; k < PER; k++) {
-      const uint32_t c = S.cnt[t * PER + k] & 0xFFFFu;
-      v[k] = c > 1 ? c : 0u;
-    }
-    uint32_t M = 0;
-    uint32_t run = bd_scan8(v, S.wsum, &M);
-#pragma unroll
-    for (int k = 0; k < PER; k++)
-      if (v[k]) {
-        S.cnt[t * PER + k] = (run << 16) | v[k];
-        run += v[k];
-      }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < BD_ITEMS; j++) {
-      if (r[j] == REC_SENTINEL || !(r[j] >> 63)) continue;
-      const uint64_t rec = r[j] & ~(1ull << 63);
-      S.sorted[atomicAdd(&S.cnt[bucket_low(rec)], 1u << 16) >> 16] = rec;
-    }
-    __syncthreads();
-    // segmented detection over sorted[0, M): warps take 256-record chunks
-    const SrcSmem src{S.sorted};
-    for (uint32_t wg = (uint32_t)t >> 5; wg * (32 * BD_ROUNDS) < M; wg += BD_WARPS) {
-      Chunk<BD_ROUNDS> ch;
-      load_chunk(src, wg, M, ch);
-      detect_chunk<SPILL>(p, src, wg, M, ch);
-    }
-  }
+  if (__syncthreads_or(multi)) bucket_multi<SPILL>(p, S, s0, m);
   // (the records are dead here: the counters are cleared whole, 8 per thread)
 #pragma unroll
   for (int k = 0; k < (int)(BUCKET_CELLS / BD_THREADS); k++) S.cnt[t + k * BD_THREADS] = 0u;  // (the caller synchronises)
+  if (t == 0) S.cnt[BUCKET_CELLS] = 0u;
 }
 
 // a bucket larger than BD_CAP: counting sort by cell into tmp[s0, s0 + m), then detect there
@@ -584,22 +594,37 @@ __device__ __noinline__ void bucket_global(const DetectParams& p, BucketSmem& S,
 }
 
 template <bool SPILL>
-__global__ void __launch_bounds__(BD_THREADS, 2) bucket_detect_kernel(const DetectParams p) {
+__global__ void __launch_bounds__(BD_THREADS, BD_MINB) bucket_detect_kernel(const DetectParams p) {
   extern __shared__ __align__(16) unsigned char bd_smem_raw[];
   BucketSmem& S = *reinterpret_cast<BucketSmem*>(bd_smem_raw);
   if (p.ctr->abort) return;  // speculative interval after one that needs the host (grid-uniform)
   const int t = threadIdx.x;
   if (!(p.ctr->log_overflow || p.ctr->ovl_overflow || p.ctr->k1_reports > p.report_cap)) {
-    for (uint32_t i = t; i < BUCKET_CELLS; i += BD_THREADS) S.cnt[i] = 0u;
-    if (t == 0) S.bucket[0] = atomicAdd(&p.ctr->bucket_next, 1u);
+    for (uint32_t i = t; i < BUCKET_CELLS + 4; i += BD_THREADS) S.cnt[i] = 0u;
+    // the block's buckets (static round robin: no claim round trips; empty
+    // buckets — e.g. those of an array the interval does not write — drop out)
+    if (t < 32) {
+      const uint32_t b = blockIdx.x + (uint32_t)t * gridDim.x;
+      uint32_t s0 = 0, m = 0;
+      if (b < p.nb) {
+        s0 = __ldg(p.bstart + b);
+        m = __ldg(p.bend + b) - s0;
+      }
+      const unsigned nz = __ballot_sync(0xFFFFFFFFu, m != 0);
+      if (m) {
+        const int k = __popc(nz & ((1u << t) - 1u));
+        S.ls0[k] = s0;
+        S.lm[k] = m;
+      }
+      if (t == 0) S.nlist = __popc(nz);
+    }
     __syncthreads();
-    for (int cur = 0;; cur ^= 1) {
-      const uint32_t b = S.bucket[cur];
-      if (b >= p.nb) break;  // block-uniform
-      if (t == 0) S.bucket[cur ^ 1] = atomicAdd(&p.ctr->bucket_next, 1u);  // claimed while this one runs
-      const uint32_t s0 = __ldg(p.bstart + b), m = __ldg(p.bend + b) - s0;
+    const uint32_t nl = S.nlist;
+    for (uint32_t i = 0; i < nl; i++) {
+      const uint32_t s0 = S.ls0[i], m = S.lm[i];
       if (m > BD_CAP) bucket_global<SPILL>(p, S, s0, m);
-      else if (m) bucket_smem<SPILL>(p, S, s0, m);
+      else if (m <= BD_CAP / 2) bucket_smem<SPILL, BD_ITEMS / 2>(p, S, s0, m);
+      else bucket_smem<SPILL, BD_ITEMS>(p, S, s0, m);
       __syncthreads();
     }
   }
@@ -673,7 +698,9 @@ cudaError_t launch_bucket_detect(const DetectParams& p, cudaStream_t s) {
       },
       &dev);
   if (se != cudaSuccess) return se;
-  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(p.nb, (uint64_t)nsm_of[dev] * per_sm_of[dev]));
+  // one resident wave, but never more than BD_LIST buckets per block
+  const unsigned grid = (unsigned)std::max<uint64_t>({uint64_t{1}, std::min<uint64_t>(p.nb, (uint64_t)nsm_of[dev] * per_sm_of[dev]),
+                                                      (p.nb + BD_LIST - 1) / BD_LIST});
   if (p.spill_n) bucket_detect_kernel<true><<<grid, BD_THREADS, sizeof(BucketSmem), s>>>(p);
   else bucket_detect_kernel<false><<<grid, BD_THREADS, sizeof(BucketSmem), s>>>(p);
   launched();

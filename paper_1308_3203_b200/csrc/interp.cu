@@ -52,7 +52,7 @@
 #ifndef INTERP_T  // threads per block (<= 256)
 #define INTERP_T 256
 #endif
-#ifndef INTERP_H  // work-items per thread for large batches (1 or 2)
+#ifndef INTERP_H  // work-items per thread for large batches (>= 2)
 #define INTERP_H 2
 #endif
 #ifndef INTERP_MIN_BLOCKS_H  // resident blocks per SM of the 2-work-items-per-thread kernel
@@ -63,6 +63,9 @@
 #endif
 #ifndef INTERP_MIN_BLOCKS
 #define INTERP_MIN_BLOCKS 3
+#endif
+#ifndef INTERP_SMEM_CAP  // dynamic shared memory per block (the block size halves until it fits)
+#define INTERP_SMEM_CAP (96 * 1024)
 #endif
 
 namespace rc {
@@ -858,7 +861,7 @@ template <int H, bool ALT, bool SPILL>
 cudaError_t launch_interp_h(const InterpParams& p, cudaStream_t s, int nsm) {
   const bool code_smem = p.n_instr <= 2048;
   int T = INTERP_T;
-  while (T > 32 && interp_smem_bytes(p, T, code_smem, H) > 96 * 1024) T >>= 1;
+  while (T > 32 && interp_smem_bytes(p, T, code_smem, H) > INTERP_SMEM_CAP) T >>= 1;
   const size_t sm = interp_smem_bytes(p, T, code_smem, H);
   auto kern = code_smem ? (p.fuel_check ? interp_kernel<true, true, H, ALT, SPILL> : interp_kernel<true, false, H, ALT, SPILL>)
                         : (p.fuel_check ? interp_kernel<false, true, H, ALT, SPILL> : interp_kernel<false, false, H, ALT, SPILL>);
@@ -882,8 +885,8 @@ cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
 #define RC_K1_VARIANTS(SP)                                                                                   \
   interp_kernel<true, true, 1, false, SP>, interp_kernel<false, true, 1, false, SP>,                         \
       interp_kernel<true, false, 1, false, SP>, interp_kernel<false, false, 1, false, SP>,                   \
-      interp_kernel<true, true, 2, false, SP>, interp_kernel<false, true, 2, false, SP>,                     \
-      interp_kernel<true, false, 2, false, SP>, interp_kernel<false, false, 2, false, SP>
+      interp_kernel<true, true, INTERP_H, false, SP>, interp_kernel<false, true, INTERP_H, false, SP>,       \
+      interp_kernel<true, false, INTERP_H, false, SP>, interp_kernel<false, false, INTERP_H, false, SP>
         for (auto f : {RC_K1_VARIANTS(false), RC_K1_VARIANTS(true), interp_kernel<true, true, 1, true, true>,
                        interp_kernel<false, true, 1, true, true>, interp_kernel<true, false, 1, true, true>,
                        interp_kernel<false, false, 1, true, true>}) {
@@ -900,12 +903,12 @@ cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
   // two work-items per thread when the batch has enough lanes to fill the GPU
   // (test hook RC_DEBUG_INTERP_H=1|2 forces one variant; results never differ)
   const char* force = getenv("RC_DEBUG_INTERP_H");
-  const int h = force ? (force[0] == '2' ? 2 : 1)
+  const int h = force ? (force[0] != '1' ? INTERP_H : 1)
                       : (INTERP_H >= 2 && p.n_lanes >= (uint32_t)INTERP_H * 256u * (uint32_t)nsm ? INTERP_H : 1);
   if (p.alt_mask) return launch_interp_h<1, true, true>(p, s, nsm);  // classification re-run (rare)
   if (p.may_spill)
-    return h == 2 ? launch_interp_h<2, false, true>(p, s, nsm) : launch_interp_h<1, false, true>(p, s, nsm);
-  return h == 2 ? launch_interp_h<2, false, false>(p, s, nsm) : launch_interp_h<1, false, false>(p, s, nsm);
+    return h > 1 ? launch_interp_h<INTERP_H, false, true>(p, s, nsm) : launch_interp_h<1, false, true>(p, s, nsm);
+  return h > 1 ? launch_interp_h<INTERP_H, false, false>(p, s, nsm) : launch_interp_h<1, false, false>(p, s, nsm);
 }
 
 }  // namespace rc

@@ -1,6 +1,7 @@
 // rc_internal.h — shared definitions of the CUDA path (librc.so).  Not part of
 // the ABI (include/rc.h is).  Nothing here is shared with oracle/.
 #pragma once
+#include <algorithm>
 #include <cstddef>
 #include <atomic>
 #include <cstdint>
@@ -115,7 +116,6 @@ struct DevCounters {
   unsigned long long k1_reports;    // report_count after K1 (snapshot taken by the filter)
   unsigned long long rw_reports;    // RW reports emitted by detect (RC_OPT_CLASSIFY_RW)
   unsigned long long kept_writes;   // write records among the kept ones (profile bytes of detect)
-  unsigned int bucket_next;         // next bucket to claim (bucket detect)
   unsigned int count_done;          // bucket_count blocks finished (last-block pattern: the bucket starts)
   // ---- fields above: zeroed per interval attempt (one memset, runtime.cu)
   unsigned long long report_count;  // reports appended (whole run, rolled back on retry)

@@ -845,7 +845,6 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         do {
           CK(grow_reports(rc));
           CK(set_report_count(h.k1_reports));
-          CK(cudaMemsetAsync(&dctr->bucket_next, 0, sizeof(unsigned int), s));  // (bucket path: claim again)
           DetectParams dp = detect_params(k);
           CK(launch_detect(dp, s));
           CK(read_ctr());

@@ -550,9 +550,35 @@ __global__ void __launch_bounds__(BC_THREADS) bucket_count_kernel(const ScatterP
       const uint32_t i = c0 + j * 32 + lane;
       r[j] = i < n ? __ldg(p.stage + i) : REC_SENTINEL;
     }
+    // the common case first: every kept record of the chunk in one bucket
+    uint32_t bmin = 0xFFFFFFFFu, bmax = 0, nk = 0;
 #pragma unroll
     for (int j = 0; j < BC_ROUNDS; j++) {
-      const bool keep = scatter_keep(p, r[j]);
+      if (!scatter_keep(p, r[j])) {
+        r[j] = REC_SENTINEL;
+        continue;
+      }
+      const uint32_t b = (uint32_t)(r[j] >> (REC_CELL_SHIFT + BUCKET_BITS));
+      bmin = min(bmin, b);
+      bmax = max(bmax, b);
+      nk++;
+    }
+    bmin = __reduce_min_sync(FULL, bmin);
+    bmax = __reduce_max_sync(FULL, bmax);
+    if (bmin == bmax) {
+      const uint32_t k = __reduce_add_sync(FULL, nk);
+      if (bmin != run_b) {
+        if (lane == 0 && run_n) atomicAdd(hist + run_b, run_n);
+        run_b = bmin;
+        run_n = 0;
+      }
+      run_n += k;
+      continue;
+    }
+    if (bmin > bmax) continue;  // nothing kept
+#pragma unroll
+    for (int j = 0; j < BC_ROUNDS; j++) {
+      const bool keep = r[j] != REC_SENTINEL;
       const uint32_t b = keep ? (uint32_t)(r[j] >> (REC_CELL_SHIFT + BUCKET_BITS)) : 0xFFFFFFFFu;
       const unsigned km = __ballot_sync(FULL, keep);
       if (!km) continue;
@@ -672,9 +698,36 @@ __global__ void __launch_bounds__(BS_THREADS) bucket_scatter_kernel(const Scatte
       const uint32_t i = c0 + j * 32 + lane;
       r[j] = i < n ? __ldcs(p.stage + i) : REC_SENTINEL;  // (streamed: read once)
     }
+    uint32_t bmin = 0xFFFFFFFFu, bmax = 0, nk = 0;
 #pragma unroll
-    for (int j = 0; j < BS_ROUNDS; j++)  // the write-set filter
-      if (!scatter_keep(p, r[j])) r[j] = REC_SENTINEL;
+    for (int j = 0; j < BS_ROUNDS; j++) {  // the write-set filter
+      if (!scatter_keep(p, r[j])) {
+        r[j] = REC_SENTINEL;
+        continue;
+      }
+      const uint32_t b = (uint32_t)(r[j] >> (REC_CELL_SHIFT + BUCKET_BITS));
+      bmin = min(bmin, b);
+      bmax = max(bmax, b);
+      nk++;
+    }
+    bmin = __reduce_min_sync(FULL, bmin);
+    bmax = __reduce_max_sync(FULL, bmax);
+    if (bmin > bmax) continue;  // nothing kept
+    if (bmin == bmax) {  // the common case: one bucket, one reservation for the chunk
+      uint32_t base = 0;
+      const uint32_t k = __reduce_add_sync(FULL, nk);
+      if (lane == 0) base = atomicAdd(p.bcur + bmin, k);
+      base = __shfl_sync(FULL, base, 0);
+#pragma unroll
+      for (int j = 0; j < BS_ROUNDS; j++) {
+        const unsigned m = __ballot_sync(FULL, r[j] != REC_SENTINEL);
+        if (r[j] != REC_SENTINEL) __stcs(p.out + base + __popc(m & lt), r[j]);
+        base += __popc(m);
+        kept_w += __popc(__ballot_sync(FULL, r[j] != REC_SENTINEL && (r[j] & 1)));
+      }
+      kept += k;
+      continue;
+    }
     uint32_t base[BS_ROUNDS], rank[BS_ROUNDS], lead[BS_ROUNDS];
 #pragma unroll
     for (int j = 0; j < BS_ROUNDS; j++) {
