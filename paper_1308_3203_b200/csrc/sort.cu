@@ -529,10 +529,44 @@ cudaError_t onesweep_sort(uint64_t* recs, uint32_t n, const unsigned long long* 
 // block to finish turns the counts into the buckets' exclusive starts
 // (bstart) and the scatter's cursors (bcur).
 constexpr int BC_THREADS = 512;
-constexpr int BC_ROUNDS = 8;
-__device__ __forceinline__ bool scatter_keep(const ScatterParams& p, uint64_t r) {
-  return r != REC_SENTINEL &&
-         ((r & 1) || p.keep_all || __ldg(p.wmap + (uint32_t)(r >> REC_CELL_SHIFT)) == p.wtag);
+#ifndef BC_ROUNDS_OPT
+#define BC_ROUNDS_OPT 4
+#endif
+constexpr int BC_ROUNDS = BC_ROUNDS_OPT;  // 16-byte loads per lane and chunk
+constexpr int BC_ITEMS = 2 * BC_ROUNDS;
+// A warp's chunk of 64 * ROUNDS staging slots: 16-byte loads, lane L of round
+// j takes slots c0 + 64 j + 2 L, + 1 into items 2 j, 2 j + 1 (slots >= n:
+// REC_SENTINEL).  Any order of a chunk's records inside a bucket is fine.
+template <int ROUNDS>
+__device__ __forceinline__ void load_chunk2(const uint64_t* __restrict__ stage, uint32_t c0, uint32_t n, int lane,
+                                            uint64_t (&r)[2 * ROUNDS]) {
+#pragma unroll
+  for (int j = 0; j < ROUNDS; j++) {
+    const uint32_t i = c0 + 64 * j + 2 * lane;
+    if (i + 1 < n) {
+      const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2*>(stage + i));
+      r[2 * j] = v.x;
+      r[2 * j + 1] = v.y;
+    } else {
+      r[2 * j] = i < n ? __ldcs(stage + i) : REC_SENTINEL;
+      r[2 * j + 1] = REC_SENTINEL;
+    }
+  }
+}
+
+// the write-set filter over a warp's chunk (records -> REC_SENTINEL when
+// dropped): the map is looked up only when the chunk holds read records
+// (none at all when K1 elided every read statically)
+template <int ROUNDS>
+__device__ __forceinline__ void filter_chunk(const ScatterParams& p, uint64_t (&r)[ROUNDS]) {
+  bool rd = false;
+#pragma unroll
+  for (int j = 0; j < ROUNDS; j++) rd |= r[j] != REC_SENTINEL && !(r[j] & 1);
+  if (p.keep_all || !__any_sync(FULL, rd)) return;
+#pragma unroll
+  for (int j = 0; j < ROUNDS; j++)
+    if (r[j] != REC_SENTINEL && !(r[j] & 1) && __ldg(p.wmap + (uint32_t)(r[j] >> REC_CELL_SHIFT)) != p.wtag)
+      r[j] = REC_SENTINEL;
 }
 __global__ void __launch_bounds__(BC_THREADS) bucket_count_kernel(const ScatterParams p, uint32_t* __restrict__ hist,
                                                                    uint32_t nb, uint32_t* __restrict__ bstart) {
@@ -542,26 +576,19 @@ __global__ void __launch_bounds__(BC_THREADS) bucket_count_kernel(const ScatterP
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const uint32_t warps = gridDim.x * (BC_THREADS / 32);
   uint32_t run_b = 0xFFFFFFFFu, run_n = 0;  // (warp-uniform) the open run of one-bucket rounds
-  for (uint32_t c = blockIdx.x * (BC_THREADS / 32) + w; (uint64_t)c * (32 * BC_ROUNDS) < n; c += warps) {
-    const uint32_t c0 = c * (32 * BC_ROUNDS);
-    uint64_t r[BC_ROUNDS];
-#pragma unroll
-    for (int j = 0; j < BC_ROUNDS; j++) {
-      const uint32_t i = c0 + j * 32 + lane;
-      r[j] = i < n ? __ldg(p.stage + i) : REC_SENTINEL;
-    }
+  for (uint32_t c = blockIdx.x * (BC_THREADS / 32) + w; (uint64_t)c * (64 * BC_ROUNDS) < n; c += warps) {
+    uint64_t r[BC_ITEMS];
+    load_chunk2<BC_ROUNDS>(p.stage, c * (64 * BC_ROUNDS), n, lane, r);
+    filter_chunk<BC_ITEMS>(p, r);
     // the common case first: every kept record of the chunk in one bucket
     uint32_t bmin = 0xFFFFFFFFu, bmax = 0, nk = 0;
 #pragma unroll
-    for (int j = 0; j < BC_ROUNDS; j++) {
-      if (!scatter_keep(p, r[j])) {
-        r[j] = REC_SENTINEL;
-        continue;
-      }
+    for (int j = 0; j < BC_ITEMS; j++) {
+      const bool ok = r[j] != REC_SENTINEL;
       const uint32_t b = (uint32_t)(r[j] >> (REC_CELL_SHIFT + BUCKET_BITS));
-      bmin = min(bmin, b);
-      bmax = max(bmax, b);
-      nk++;
+      bmin = min(bmin, ok ? b : 0xFFFFFFFFu);
+      bmax = max(bmax, ok ? b : 0u);
+      nk += ok;
     }
     bmin = __reduce_min_sync(FULL, bmin);
     bmax = __reduce_max_sync(FULL, bmax);
@@ -577,7 +604,7 @@ __global__ void __launch_bounds__(BC_THREADS) bucket_count_kernel(const ScatterP
     }
     if (bmin > bmax) continue;  // nothing kept
 #pragma unroll
-    for (int j = 0; j < BC_ROUNDS; j++) {
+    for (int j = 0; j < BC_ITEMS; j++) {
       const bool keep = r[j] != REC_SENTINEL;
       const uint32_t b = keep ? (uint32_t)(r[j] >> (REC_CELL_SHIFT + BUCKET_BITS)) : 0xFFFFFFFFu;
       const unsigned km = __ballot_sync(FULL, keep);
@@ -651,7 +678,7 @@ cudaError_t launch_bucket_count(const ScatterParams& p, uint32_t* hist, uint32_t
       },
       &dev);
   if (se != cudaSuccess) return se;
-  const uint64_t chunks = ((uint64_t)std::max<uint32_t>(p.n_slots, 1) + 32 * BC_ROUNDS - 1) / (32 * BC_ROUNDS);
+  const uint64_t chunks = ((uint64_t)std::max<uint32_t>(p.n_slots, 1) + 64 * BC_ROUNDS - 1) / (64 * BC_ROUNDS);
   const uint32_t grid = (uint32_t)std::max<uint64_t>(
       1, std::min<uint64_t>((chunks + BC_THREADS / 32 - 1) / (BC_THREADS / 32), (uint64_t)nsm_of[dev] * per_sm_of[dev]));
   if (prof) prof->begin(s);
@@ -670,12 +697,16 @@ cudaError_t launch_bucket_count(const ScatterParams& p, uint32_t* hist, uint32_t
 // wrote can take part in no report and no commit.  The
 // order inside a bucket is arbitrary (bucket_detect sorts each bucket by its
 // low bits; the detection only uses order-independent reductions inside a
-// cell).  A warp takes BS_ROUNDS rounds of 32 consecutive slots (all loads in
+// cell).  A warp takes 64 * BS_ROUNDS consecutive slots (16-byte loads, all in
 // flight), groups each round's kept lanes by bucket (one vote when the round
 // is one bucket — the common case, K1 stages in lane order — else
 // __match_any_sync), and the group leader reserves the group's slots with one
 // atomic; the atomics of all rounds are issued before any result is used.
-constexpr int BS_ROUNDS = 8;
+#ifndef BS_ROUNDS_OPT
+#define BS_ROUNDS_OPT 4
+#endif
+constexpr int BS_ROUNDS = BS_ROUNDS_OPT;  // 16-byte loads per lane and chunk
+constexpr int BS_ITEMS = 2 * BS_ROUNDS;
 constexpr int BS_THREADS = 256;
 __global__ void __launch_bounds__(BS_THREADS) bucket_scatter_kernel(const ScatterParams p) {
   const DevCounters* ctr = p.ctr;
@@ -689,26 +720,19 @@ __global__ void __launch_bounds__(BS_THREADS) bucket_scatter_kernel(const Scatte
   const uint32_t warps = gridDim.x * (BS_THREADS / 32);
   const unsigned lt = lanemask_lt();
   uint32_t kept = 0, kept_w = 0;  // lane 0: the warp's kept records / write records
-  for (uint32_t c = blockIdx.x * (BS_THREADS / 32) + (threadIdx.x >> 5); (uint64_t)c * (32 * BS_ROUNDS) < n;
+  for (uint32_t c = blockIdx.x * (BS_THREADS / 32) + (threadIdx.x >> 5); (uint64_t)c * (64 * BS_ROUNDS) < n;
        c += warps) {
-    const uint32_t c0 = c * (32 * BS_ROUNDS);
-    uint64_t r[BS_ROUNDS];
-#pragma unroll
-    for (int j = 0; j < BS_ROUNDS; j++) {
-      const uint32_t i = c0 + j * 32 + lane;
-      r[j] = i < n ? __ldcs(p.stage + i) : REC_SENTINEL;  // (streamed: read once)
-    }
+    uint64_t r[BS_ITEMS];
+    load_chunk2<BS_ROUNDS>(p.stage, c * (64 * BS_ROUNDS), n, lane, r);
+    filter_chunk<BS_ITEMS>(p, r);  // the write-set filter
     uint32_t bmin = 0xFFFFFFFFu, bmax = 0, nk = 0;
 #pragma unroll
-    for (int j = 0; j < BS_ROUNDS; j++) {  // the write-set filter
-      if (!scatter_keep(p, r[j])) {
-        r[j] = REC_SENTINEL;
-        continue;
-      }
+    for (int j = 0; j < BS_ITEMS; j++) {
+      const bool ok = r[j] != REC_SENTINEL;
       const uint32_t b = (uint32_t)(r[j] >> (REC_CELL_SHIFT + BUCKET_BITS));
-      bmin = min(bmin, b);
-      bmax = max(bmax, b);
-      nk++;
+      bmin = min(bmin, ok ? b : 0xFFFFFFFFu);
+      bmax = max(bmax, ok ? b : 0u);
+      nk += ok;
     }
     bmin = __reduce_min_sync(FULL, bmin);
     bmax = __reduce_max_sync(FULL, bmax);
@@ -719,7 +743,7 @@ __global__ void __launch_bounds__(BS_THREADS) bucket_scatter_kernel(const Scatte
       if (lane == 0) base = atomicAdd(p.bcur + bmin, k);
       base = __shfl_sync(FULL, base, 0);
 #pragma unroll
-      for (int j = 0; j < BS_ROUNDS; j++) {
+      for (int j = 0; j < BS_ITEMS; j++) {
         const unsigned m = __ballot_sync(FULL, r[j] != REC_SENTINEL);
         if (r[j] != REC_SENTINEL) __stcs(p.out + base + __popc(m & lt), r[j]);
         base += __popc(m);
@@ -728,9 +752,9 @@ __global__ void __launch_bounds__(BS_THREADS) bucket_scatter_kernel(const Scatte
       kept += k;
       continue;
     }
-    uint32_t base[BS_ROUNDS], rank[BS_ROUNDS], lead[BS_ROUNDS];
+    uint32_t base[BS_ITEMS], rank[BS_ITEMS], lead[BS_ITEMS];
 #pragma unroll
-    for (int j = 0; j < BS_ROUNDS; j++) {
+    for (int j = 0; j < BS_ITEMS; j++) {
       const uint32_t b = (uint32_t)(r[j] >> (REC_CELL_SHIFT + BUCKET_BITS));  // sentinel: 0xFFFFF (no bucket)
       const uint32_t b0 = __shfl_sync(FULL, b, 0);
       unsigned peers;
@@ -744,7 +768,7 @@ __global__ void __launch_bounds__(BS_THREADS) bucket_scatter_kernel(const Scatte
       kept_w += __popc(__ballot_sync(FULL, r[j] != REC_SENTINEL && (r[j] & 1)));
     }
 #pragma unroll
-    for (int j = 0; j < BS_ROUNDS; j++) {
+    for (int j = 0; j < BS_ITEMS; j++) {
       const uint32_t bb = __shfl_sync(FULL, base[j], lead[j]);
       if (r[j] != REC_SENTINEL) __stcs(p.out + bb + rank[j], r[j]);
     }
@@ -770,7 +794,7 @@ cudaError_t launch_bucket_scatter(const ScatterParams& p, cudaStream_t s, Profil
       },
       &dev);
   if (se != cudaSuccess) return se;
-  const uint64_t chunks = ((uint64_t)p.n_slots + 32 * BS_ROUNDS - 1) / (32 * BS_ROUNDS);
+  const uint64_t chunks = ((uint64_t)p.n_slots + 64 * BS_ROUNDS - 1) / (64 * BS_ROUNDS);
   const uint32_t grid = (uint32_t)std::max<uint64_t>(
       1, std::min<uint64_t>((chunks + BS_THREADS / 32 - 1) / (BS_THREADS / 32), (uint64_t)nsm_of[dev] * per_sm_of[dev]));
   if (prof) prof->begin(s);
