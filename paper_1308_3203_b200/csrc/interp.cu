@@ -300,44 +300,41 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
     interp_kernel(const __grid_constant__ InterpParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (p.ctr->abort) return;  // speculative interval (DevCounters::abort)
-  const int T = blockDim.x;
-  const int TL = H * T;  // lanes per tile
-  const int W = T >> 5;
+  const int T = (int)p.lay.T;    // == blockDim.x
+  const int TL = (int)p.lay.TL;  // lanes per tile (H * T)
+  const int W = (int)p.lay.W;
   const int t = threadIdx.x;
   const int warp = t >> 5, lane = t & 31;
   const uint32_t R = p.n_regs, OV = p.ovl_cap;
   const uint32_t SW = H * p.stage_warp;  // staged records per warp
   const LogOut lo{p.stage, p.wmap, p.ctr, p.stage_cap};
+  (void)R;
 
-  // ---- shared memory carve-up (sizes mirrored in interp_smem_bytes)
-  unsigned char* q = smem;
-  // register files [reg][lane], status and pc rows, LS_NB-buffered (TMA: the
-  // next tile's state lands while this one runs; a buffer is refilled only
-  // after the bulk stores of its previous tile have read it); buffer b is
-  // addressed arithmetically from these bases (a runtime-indexed array of
-  // pointers would lose the shared address space)
-  int32_t* const sregs0 = reinterpret_cast<int32_t*>(q); q += (size_t)LS_NB * R * TL * 4;
-  uint32_t* const spc0 = reinterpret_cast<uint32_t*>(q); q += (size_t)LS_NB * TL * 4;
-  uint8_t* const sstat0 = reinterpret_cast<uint8_t*>(q); q += (size_t)LS_NB * TL;
-#define SREGS(b) (sregs0 + (size_t)(b) * R * TL)
+  // ---- shared memory carve-up (k1_layout): register files [reg][lane],
+  // status and pc rows, LS_NB-buffered (TMA: the next tile's state lands
+  // while this one runs; a buffer is refilled only after the bulk stores of
+  // its previous tile have read it); buffer b is addressed arithmetically
+  // from these bases (a runtime-indexed array of pointers would lose the
+  // shared address space)
+  int32_t* const sregs0 = reinterpret_cast<int32_t*>(smem + p.lay.regs);
+  uint32_t* const spc0 = reinterpret_cast<uint32_t*>(smem + p.lay.spc);
+  uint8_t* const sstat0 = smem + p.lay.sstat;
+#define SREGS(b) (reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(sregs0) + (size_t)(b) * p.lay.regs_buf))
 #define SPC(b) (spc0 + (size_t)(b) * TL)
 #define SSTAT(b) (sstat0 + (size_t)(b) * TL)
   // mbar[b]: the lane state of buffer b landed (TMA)
-  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(q); q += (16 * LS_NB + 15) & ~15;
-  uint64_t* st_recs = reinterpret_cast<uint64_t*>(q); q += (size_t)W * SW * 8;
-  uint4* s_code = reinterpret_cast<uint4*>(q); q += CODE_SMEM ? (size_t)(p.n_instr + 1) * 16 : 0;  // heads + pad entry
-  uint2* s_tail = reinterpret_cast<uint2*>(q); q += CODE_SMEM ? (size_t)(p.n_instr + 1) * 8 : 0;   // tails + pad
-  uint32_t* s_ro = reinterpret_cast<uint32_t*>(q); q += CODE_SMEM ? (size_t)(p.n_instr + 1) * 4 : 0; // entry_ro
-  uint32_t* ocell = reinterpret_cast<uint32_t*>(q); q += (size_t)OV * TL * 4;
-  int32_t* oval = reinterpret_cast<int32_t*>(q); q += (size_t)OV * TL * 4;
-  uint32_t* s_off = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
-  uint32_t* s_size = reinterpret_cast<uint32_t*>(q); q += (size_t)p.n_arrays * 4;
-  uint8_t* s_live = reinterpret_cast<uint8_t*>(q); q += (p.n_live + 3) & ~3u;
-  uint32_t* wcnt = reinterpret_cast<uint32_t*>(q); q += (size_t)W * 4 + 8;  // per-warp staged records, pad count
-  q = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(q) + 7) & ~uintptr_t(7));
-  unsigned long long* wbase = reinterpret_cast<unsigned long long*>(q); q += (size_t)(W + 1) * 8;  // [W], pad start
-  (void)wcnt;
-  (void)wbase;
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem + p.lay.mbar);
+  uint64_t* st_recs = reinterpret_cast<uint64_t*>(smem + p.lay.recs);
+  uint4* s_code = reinterpret_cast<uint4*>(smem + p.lay.code);   // heads + pad entry
+  uint2* s_tail = reinterpret_cast<uint2*>(smem + p.lay.tail);   // tails + pad
+  uint32_t* s_ro = reinterpret_cast<uint32_t*>(smem + p.lay.ro);  // entry_ro
+  uint32_t* ocell = reinterpret_cast<uint32_t*>(smem + p.lay.ocell);
+  int32_t* oval = reinterpret_cast<int32_t*>(smem + p.lay.oval);
+  uint32_t* s_off = reinterpret_cast<uint32_t*>(smem + p.lay.soff);
+  uint32_t* s_size = reinterpret_cast<uint32_t*>(smem + p.lay.ssize);
+  uint8_t* s_live = smem + p.lay.live;
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem + p.lay.wcnt);  // per-warp staged records, pad count
+  unsigned long long* wbase = reinterpret_cast<unsigned long long*>(smem + p.lay.wbase);  // [W], pad start
 
   for (uint32_t a = t; a < p.n_arrays; a += T) {
     s_off[a] = p.arr_off[a];
@@ -842,18 +839,39 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
 #undef SSTAT
 }
 
+// The carve-up of K1's dynamic shared memory for T threads and H lanes per
+// thread (offsets in bytes; every buffer a TMA copy touches is 16-B aligned).
+K1Layout k1_layout(const InterpParams& p, int T, bool code_in_smem, int H) {
+  K1Layout L;
+  const uint32_t W = (uint32_t)T / 32, TL = (uint32_t)(H * T);
+  L.T = (uint32_t)T;
+  L.TL = TL;
+  L.W = W;
+  uint32_t q = 0;
+  L.regs = q; L.regs_buf = p.n_regs * TL * 4; q += LS_NB * L.regs_buf;  // register files (LS_NB buffers)
+  L.spc = q; q += LS_NB * TL * 4;                                        // pc rows
+  L.sstat = q; q += LS_NB * TL;                                          // status rows
+  q = (q + 15) & ~15u;
+  L.mbar = q; q += (16 * LS_NB + 15) & ~15;                              // mbarriers
+  L.recs = q; q += W * (uint32_t)H * p.stage_warp * 8;                   // staging
+  L.code = q; q += code_in_smem ? (p.n_instr + 1) * 16 : 0;              // pre-decoded heads + pad entry
+  L.tail = q; q += code_in_smem ? (p.n_instr + 1) * 8 : 0;               // tails + pad
+  L.ro = q; q += code_in_smem ? (p.n_instr + 1) * 4 : 0;                 // entry_ro
+  q = (q + 15) & ~15u;
+  L.ocell = q; q += p.ovl_cap * TL * 4;                                  // overlay cells
+  L.oval = q; q += p.ovl_cap * TL * 4;                                   // overlay values
+  L.soff = q; q += p.n_arrays * 4;                                       // array offsets
+  L.ssize = q; q += p.n_arrays * 4;                                      // array sizes
+  L.live = q; q += (p.n_live + 3) & ~3u;                                 // live register list
+  L.wcnt = q; q += W * 4 + 8;                                            // warp counts, pad count
+  q = (q + 7) & ~7u;
+  L.wbase = q; q += (W + 1) * 8;                                         // warp bases, pad start
+  L.total = q;
+  return L;
+}
+
 size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem, int H) {
-  const int W = T / 32, TL = H * T;
-  size_t b = (size_t)LS_NB * p.n_regs * TL * 4;                // register files (LS_NB buffers)
-  b += (size_t)LS_NB * TL * 5 + ((16 * LS_NB + 15) & ~15);     // status / pc rows, mbarriers
-  b += (size_t)W * H * p.stage_warp * 8;                        // staging
-  b += code_in_smem ? (size_t)(p.n_instr + 1) * 28 : 0;        // pre-decoded program + pad entry, entry_ro
-  b += (size_t)p.ovl_cap * TL * 8;                             // overlay
-  b += (size_t)p.n_arrays * 8;                                 // array offsets / sizes
-  b += ((size_t)p.n_live + 3) & ~size_t(3);                    // live register list
-  b += (size_t)W * 4 + 8 + 8;                                  // warp counts, pad count (+align)
-  b += (size_t)(W + 1) * 8;                                    // warp bases, pad start
-  return b;
+  return k1_layout(p, T, code_in_smem, H).total;
 }
 
 namespace {
@@ -862,14 +880,16 @@ cudaError_t launch_interp_h(const InterpParams& p, cudaStream_t s, int nsm) {
   const bool code_smem = p.n_instr <= 2048;
   int T = INTERP_T;
   while (T > 32 && interp_smem_bytes(p, T, code_smem, H) > INTERP_SMEM_CAP) T >>= 1;
-  const size_t sm = interp_smem_bytes(p, T, code_smem, H);
+  InterpParams q = p;
+  q.lay = k1_layout(p, T, code_smem, H);
+  const size_t sm = q.lay.total;
   auto kern = code_smem ? (p.fuel_check ? interp_kernel<true, true, H, ALT, SPILL> : interp_kernel<true, false, H, ALT, SPILL>)
                         : (p.fuel_check ? interp_kernel<false, true, H, ALT, SPILL> : interp_kernel<false, false, H, ALT, SPILL>);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, sm);
   const uint32_t tiles = (p.n_lanes + H * T - 1) / (H * T);
   const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)std::max(1, per_sm) * nsm);
-  kern<<<grid, T, sm, s>>>(p);
+  kern<<<grid, T, sm, s>>>(q);
   launched();
   return cudaGetLastError();
 }

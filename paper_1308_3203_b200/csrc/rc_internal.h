@@ -129,8 +129,23 @@ struct DevCounters {
   unsigned int bdone;               // A4 blocks (K4 tail: warps) finished (last-one pattern; self-resetting)
 };
 
+// K1's shared-memory carve-up, computed on the host for the launch's block
+// size (byte offsets from the dynamic shared-memory base; interp.cu
+// k1_layout): kernel parameters live in the constant bank, so the tile loop
+// addresses its buffers through constant operands instead of re-deriving them
+// from blockDim and the program sizes in registers.
+struct K1Layout {
+  uint32_t T, TL, W;   // threads per block, lanes per tile, warps per block
+  uint32_t regs;       // register files, LS_NB buffers of regs_buf bytes
+  uint32_t regs_buf;   // n_regs * TL * 4
+  uint32_t spc, sstat; // pc / status rows, LS_NB buffers of TL * 4 / TL bytes
+  uint32_t mbar, recs, code, tail, ro, ocell, oval, soff, ssize, live, wcnt, wbase;
+  uint32_t total;
+};
+
 // Parameters of the interval interpreter (K1), passed by value.
 struct InterpParams {
+  K1Layout lay;               // (filled by launch_interp)
   const Ins* code;
   uint32_t n_instr, n_regs, n_arrays;
   uint32_t n;                 // work-group size
