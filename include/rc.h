@@ -318,6 +318,50 @@ RC_API int rc_explore(const rc_program* prog, uint32_t n, const uint32_t* sizes,
                uint64_t cap, uint32_t* witness_sched, uint32_t max_len, void* cuda_stream,
                rc_explore_result* out);
 
+/* ---- symbolic NoRace pre-pass ----
+ * The paper's symbolic execution (Table 1): one generic work-item
+ * whose tid is universally quantified, sets of symbolic heaps, and at every
+ * barrier the NoRace check for two renamed instances i != j, with
+ * a prover the paper leaves open — here a decision procedure
+ * over the concrete shape: work_group_size work-items (one work-group), the
+ * given array sizes, any input values.  Host only; no device work.
+ * verdict: RC_PROVE_NO_CONFLICT — in every interval no two work-items touch
+ *   one cell with a write, and no ⊥ (OOB / ASSERT / DIV0 / FUEL) and no
+ *   barrier divergence is possible: rc_run reports nothing, for any input;
+ * RC_PROVE_NORACE — as above except that write-write conflicts are possible,
+ *   each provably benign (equal values): rc_run can report only WW_BENIGN
+ *   (the paper's NoRace: the shared state at every barrier is deterministic);
+ * RC_PROVE_UNKNOWN — not proved (the checker must run); `reason` / `pc` say
+ *   where the proof stopped.  Sound, not complete.
+ * sizes: HOST, n_arrays element counts.  fuel_per_interval: as rc_options (0
+ * = 2^20).  budget: prover work units (~ tid evaluations; 0 = 2^32).  out
+ * (HOST) is always written.  RC_EINVAL for bad arguments.                  */
+#define RC_PROVE_UNKNOWN 0u
+#define RC_PROVE_NO_CONFLICT 1u
+#define RC_PROVE_NORACE 2u
+/* reasons (RC_PROVE_UNKNOWN) */
+#define RC_PROVE_R_RW 1u           /* a read and another work-item's write may meet */
+#define RC_PROVE_R_WW 2u           /* two writes may meet with values not provably equal */
+#define RC_PROVE_R_OOB 3u          /* an index may leave its array */
+#define RC_PROVE_R_DATA_INDEX 4u   /* an index depends on loaded values */
+#define RC_PROVE_R_ASSERT 5u       /* an assert may fail */
+#define RC_PROVE_R_DIV0 6u         /* a divisor may be 0 */
+#define RC_PROVE_R_DIVERGENCE 7u   /* work-items may reach different barriers */
+#define RC_PROVE_R_OWN_ALIAS 8u    /* a work-item's own writes may alias */
+#define RC_PROVE_R_FUEL 9u         /* fuel or the interval limit may run out */
+#define RC_PROVE_R_BUDGET 10u      /* the prover's budget (paths, work) ran out */
+#define RC_PROVE_R_UNSUPPORTED 11u
+typedef struct {
+  uint32_t verdict;   /* RC_PROVE_*                                     */
+  uint32_t reason;    /* RC_PROVE_R_* when UNKNOWN                        */
+  uint32_t pc;        /* instruction where the proof stopped (0: at a barrier check) */
+  uint32_t intervals; /* barrier intervals checked                       */
+  uint64_t terms;     /* symbolic terms built                             */
+  uint64_t work;      /* prover work units spent                          */
+} rc_prove_result;
+RC_API int rc_prove(const rc_program* prog, uint32_t work_group_size, const uint32_t* sizes, uint32_t n_arrays,
+             uint64_t fuel_per_interval, uint64_t budget, rc_prove_result* out);
+
 #ifdef __cplusplus
 }
 #endif

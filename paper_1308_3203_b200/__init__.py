@@ -7,5 +7,5 @@ The compute path is librc.so (hand-written sm_100a CUDA behind the C ABI in
 include/rc.h); this package is its thin ctypes binding plus the multi-GPU
 report gather (gather.py).
 """
-from .rc import (KINDS, REPORT_DTYPE, ExploreResult, Program, RCError, RunResult, lib, rc_explore,  # noqa: F401
-                 rc_last_error, rc_load_program, rc_run)
+from .rc import (KINDS, REPORT_DTYPE, ExploreResult, Program, ProveResult, RCError, RunResult, lib,  # noqa: F401
+                 rc_explore, rc_last_error, rc_load_program, rc_prove, rc_run)

@@ -67,6 +67,16 @@ class rc_explore_result(C.Structure):
 
 
 RC_EXPLORE_REDUCED = 1
+
+
+class rc_prove_result(C.Structure):
+    _fields_ = [("verdict", C.c_uint32), ("reason", C.c_uint32), ("pc", C.c_uint32), ("intervals", C.c_uint32),
+                ("terms", C.c_uint64), ("work", C.c_uint64)]
+
+
+PROVE_VERDICTS = {0: "UNKNOWN", 1: "NO_CONFLICT", 2: "NORACE"}
+PROVE_REASONS = {0: None, 1: "RW", 2: "WW", 3: "OOB", 4: "DATA_INDEX", 5: "ASSERT", 6: "DIV0", 7: "DIVERGENCE",
+                 8: "OWN_ALIAS", 9: "FUEL", 10: "BUDGET", 11: "UNSUPPORTED"}
 _lib = None
 
 
@@ -102,6 +112,9 @@ def lib():
                                  C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_void_p,
                                  C.c_uint64, C.c_void_p, C.c_uint32, C.c_void_p, P(rc_explore_result)]
         L.rc_explore.restype = C.c_int
+        L.rc_prove.argtypes = [C.c_void_p, C.c_uint32, P(C.c_uint32), C.c_uint32, C.c_uint64, C.c_uint64,
+                               P(rc_prove_result)]
+        L.rc_prove.restype = C.c_int
         _lib = L
     return _lib
 
@@ -303,3 +316,25 @@ def rc_explore(prog: Program, work_group_size: int, heap, *, regs=None, pc=None,
                          None if out.witness == (1 << 64) - 1 else int(out.witness),
                          wsched[:wl].cpu().tolist() if out.witness != (1 << 64) - 1 else [],
                          int(out.max_product), bool(out.complete), terms[:out.n_terminal] if cap else None)
+
+
+@dataclass
+class ProveResult:
+    verdict: str          # "NO_CONFLICT" | "NORACE" | "UNKNOWN"
+    reason: str | None    # why UNKNOWN (RC_PROVE_R_*)
+    pc: int
+    intervals: int
+    terms: int
+    work: int
+
+
+def rc_prove(prog: Program, work_group_size: int, sizes: list, *, fuel_per_interval: int = 0,
+             budget: int = 0) -> ProveResult:
+    """The symbolic NoRace pre-pass (include/rc.h rc_prove): host only."""
+    sz = (C.c_uint32 * max(1, len(sizes)))(*[int(x) for x in sizes])
+    out = rc_prove_result()
+    code = lib().rc_prove(prog._h, work_group_size, sz, len(sizes), fuel_per_interval, budget, C.byref(out))
+    if code != RC_OK:
+        raise RCError(code, rc_last_error())
+    return ProveResult(PROVE_VERDICTS[out.verdict], PROVE_REASONS.get(out.reason, str(out.reason)), int(out.pc),
+                       int(out.intervals), int(out.terms), int(out.work))
