@@ -248,7 +248,7 @@ class Job:
         a = self.args
         r = rc_run(self.prog, self.n, arrs if arrs is not None else self.arrays, instance_offset=self.lo,
                    want_final=False, profile=profile, device=self.local, stream=self.stream,
-                   keep_all_reads=a.keep_all_reads, classify_rw=a.classify_rw)
+                   keep_all_reads=a.keep_all_reads, classify_rw=a.classify_rw, prepass=getattr(a, "prepass", False))
         if self.world > 1:
             reps, st = gather_reports(r.reports, r.stats, device=self.cdev)
         else:
@@ -317,6 +317,36 @@ def secondary_line(key, args, world, rank, dev, local, stream, cdev, scaling, st
            "l2": "flushed (256 MB write) before every timed step" if flush else "inputs >> 126 MB L2"}
     del job
     return out
+
+
+def prepass_line(args, world, rank, dev, local, stream, cdev):
+    """SURVEY.md §8(f) row 4 measured beside the main line: the symbolic
+    pre-pass (rc_prove, host) on config 5's shape, and the same workload run
+    with RC_OPT_PREPASS — proved conflict-free, its intervals run in
+    direct-commit mode without the grouping / detect kernels.  Not the
+    headline: the main line measures the concrete checker."""
+    import copy
+
+    from paper_1308_3203_b200 import rc_load_program, rc_prove
+    from paper_1308_3203_b200.gather import shard
+    wl = WORKLOADS["cfg5"]
+    prog = rc_load_program(wl["src"]().bytecode)
+    sizes = [x.shape[1] for x in wl["gen"](0, 1, wl["n"])]
+    t0 = time.perf_counter()
+    pr = rc_prove(prog, wl["n"], sizes)
+    prove_ms = (time.perf_counter() - t0) * 1e3
+    a2 = copy.copy(args)
+    a2.prepass = True
+    total = wl["total"]
+    lo, hi = shard(total, rank, world)
+    job = Job(wl, lo, hi, dev, local, stream, world, cdev, a2)
+    ms, acc, ins, nrep, _ = job.timed(3, 3)
+    del job
+    return {"workload": wl["name"], "verdict": pr.verdict, "intervals_proved": pr.intervals,
+            "prove_ms": prove_ms, "prover_work": pr.work, "value": acc / (ms / 1000) / 1e9, "unit": UNIT,
+            "ms_per_step": ms, "steps": 3, "warmup": 3, "reports_per_step": nrep,
+            "what": "rc_run with RC_OPT_PREPASS: the symbolic NoRace pre-pass (host, cached per shape) proved the "
+                    "run conflict-free, so intervals commit directly and skip the grouping / detect kernels"}
 
 
 def main():
@@ -437,6 +467,10 @@ def main():
             except Exception as ex:  # noqa: BLE001 — a side measurement never costs the main line
                 secondary[key] = {"error": f"{type(ex).__name__}: {ex}"}
         del flush_buf
+        try:  # §8(f) row 4 (every rank takes part, as in the main line)
+            secondary["prepass"] = prepass_line(args, world, rank, dev, local, stream, cdev)
+        except Exception as ex:  # noqa: BLE001
+            secondary["prepass"] = {"error": f"{type(ex).__name__}: {ex}"}
 
     if rank != 0:
         if world > 1:

@@ -212,6 +212,16 @@ typedef struct {
                              or 5 (see rc_report); costs a heap snapshot per
                              interval and one extra pass per racy interval     */
 
+#define RC_OPT_PREPASS 8u /* run rc_prove on the run's shape first (cached per
+                             shape); when it proves RC_PROVE_NO_CONFLICT no
+                             report is possible, so the intervals run without
+                             logging: each work-item's writes are committed at
+                             the end of its interval (exact: no other work-item
+                             touches those cells in it) and the grouping /
+                             detect kernels are skipped.  Same reports (none),
+                             final heaps and stats.  Ignored with n_groups > 1
+                             or RC_OPT_CLASSIFY_RW.                         */
+
 typedef struct {
   uint32_t instance_offset;    /* added to report.instance (multi-GPU shards) */
   uint32_t max_intervals;      /* default 65536 (reading L17)                  */

@@ -292,12 +292,17 @@ void interp_phase_io(unsigned long long* out, bool reset) {
 // H*T lanes side by side: one instruction fetch, decode, dispatch and warp
 // vote serve H lanes, and each lane's heap loads add to the memory-level
 // parallelism of the warp.
-// ALT: the RW-classification re-run (reads of alt_mask cells see alt_heap).
+// MODE 1 (ALT): the RW-classification re-run (reads of alt_mask cells see
+// alt_heap); MODE 2 (DIRECT): rc_prove proved the run conflict-free
+// (RC_OPT_PREPASS): writes are committed at the end of each work-item's
+// interval and nothing is logged.
 // SPILL: a work-item may write more distinct cells in one interval than the
 // shared-memory overlay holds (program.cpp may_spill): the spill-list paths.
-template <bool CODE_SMEM, bool FUEL, int H, bool ALT, bool SPILL>
+template <bool CODE_SMEM, bool FUEL, int H, int MODE, bool SPILL>
 __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_MIN_BLOCKS_H)
     interp_kernel(const __grid_constant__ InterpParams p) {
+  constexpr bool ALT = MODE == 1;     // RW-classification re-run
+  constexpr bool DIRECT = MODE == 2;  // RC_OPT_PREPASS: commit at the interval end, log nothing
   extern __shared__ __align__(16) unsigned char smem[];
   if (p.ctr->abort) return;  // speculative interval (DevCounters::abort)
   const int T = (int)p.lay.T;    // == blockDim.x
@@ -522,7 +527,7 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
               pc[h]++;
               nloads[h]++;
               const uint32_t arr = (eh.x >> 8) & 0xFF;
-              ok = arr >= 32 || !((ro[h] >> arr) & 1u);  // a read of a written-in-no-way array is not logged
+              ok = !DIRECT && (arr >= 32 || !((ro[h] >> arr) & 1u));  // a read of a written-in-no-way array is not logged
             }
           }
           const unsigned m = __ballot_sync(FULL, ok);
@@ -661,9 +666,26 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
     ld_async_wait();  // registers of suspended lanes are saved below
 
     // write records: one per distinct written cell; its final value (reading
-    // L3) goes to the side table wval[slot][lane] read by detect
+    // L3) goes to the side table wval[slot][lane] read by detect.  Direct
+    // mode (rc_prove proved the run conflict-free, RC_OPT_PREPASS): no other
+    // work-item touches the cell in this interval, so the final value is
+    // committed right away and nothing is logged.
+    if (DIRECT) {
 #pragma unroll
-    for (int h = 0; h < H; h++) {
+      for (int h = 0; h < H; h++) {
+        const int l = h * T + t;
+        for (int j = 0; j < n_own[h]; j++) {
+          if (!SPILL || j < (int)OV) {
+            p.heap_w[ocell[j * TL + l]] = oval[j * TL + l];
+          } else {
+            const size_t k = (size_t)(j - (int)OV) * p.n_lanes + g[h];
+            p.heap_w[p.spill_cell[k]] = p.spill_val[k];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < H && !DIRECT; h++) {
       const int l = h * T + t;
       const int max_own = __reduce_max_sync(FULL, (unsigned)n_own[h]);
       for (int j = 0; j < max_own; j++) {
@@ -875,7 +897,7 @@ size_t interp_smem_bytes(const InterpParams& p, int T, bool code_in_smem, int H)
 }
 
 namespace {
-template <int H, bool ALT, bool SPILL>
+template <int H, int MODE, bool SPILL>
 cudaError_t launch_interp_h(const InterpParams& p, cudaStream_t s, int nsm) {
   const bool code_smem = p.n_instr <= 2048;
   int T = INTERP_T;
@@ -883,8 +905,8 @@ cudaError_t launch_interp_h(const InterpParams& p, cudaStream_t s, int nsm) {
   InterpParams q = p;
   q.lay = k1_layout(p, T, code_smem, H);
   const size_t sm = q.lay.total;
-  auto kern = code_smem ? (p.fuel_check ? interp_kernel<true, true, H, ALT, SPILL> : interp_kernel<true, false, H, ALT, SPILL>)
-                        : (p.fuel_check ? interp_kernel<false, true, H, ALT, SPILL> : interp_kernel<false, false, H, ALT, SPILL>);
+  auto kern = code_smem ? (p.fuel_check ? interp_kernel<true, true, H, MODE, SPILL> : interp_kernel<true, false, H, MODE, SPILL>)
+                        : (p.fuel_check ? interp_kernel<false, true, H, MODE, SPILL> : interp_kernel<false, false, H, MODE, SPILL>);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, sm);
   const uint32_t tiles = (p.n_lanes + H * T - 1) / (H * T);
@@ -902,14 +924,15 @@ cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
   int dev = 0;
   cudaError_t se = setup.run(
       [](int d) -> cudaError_t {
-#define RC_K1_VARIANTS(SP)                                                                                   \
-  interp_kernel<true, true, 1, false, SP>, interp_kernel<false, true, 1, false, SP>,                         \
-      interp_kernel<true, false, 1, false, SP>, interp_kernel<false, false, 1, false, SP>,                   \
-      interp_kernel<true, true, INTERP_H, false, SP>, interp_kernel<false, true, INTERP_H, false, SP>,       \
-      interp_kernel<true, false, INTERP_H, false, SP>, interp_kernel<false, false, INTERP_H, false, SP>
-        for (auto f : {RC_K1_VARIANTS(false), RC_K1_VARIANTS(true), interp_kernel<true, true, 1, true, true>,
-                       interp_kernel<false, true, 1, true, true>, interp_kernel<true, false, 1, true, true>,
-                       interp_kernel<false, false, 1, true, true>}) {
+#define RC_K1_VARIANTS(M, SP)                                                                                \
+  interp_kernel<true, true, 1, M, SP>, interp_kernel<false, true, 1, M, SP>,                                 \
+      interp_kernel<true, false, 1, M, SP>, interp_kernel<false, false, 1, M, SP>,                           \
+      interp_kernel<true, true, INTERP_H, M, SP>, interp_kernel<false, true, INTERP_H, M, SP>,               \
+      interp_kernel<true, false, INTERP_H, M, SP>, interp_kernel<false, false, INTERP_H, M, SP>
+        for (auto f : {RC_K1_VARIANTS(0, false), RC_K1_VARIANTS(0, true), RC_K1_VARIANTS(2, false),
+                       RC_K1_VARIANTS(2, true), interp_kernel<true, true, 1, 1, true>,
+                       interp_kernel<false, true, 1, 1, true>, interp_kernel<true, false, 1, 1, true>,
+                       interp_kernel<false, false, 1, 1, true>}) {
 #undef RC_K1_VARIANTS
           cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
           if (e != cudaSuccess) return e;
@@ -925,10 +948,15 @@ cudaError_t launch_interp(const InterpParams& p, cudaStream_t s) {
   const char* force = getenv("RC_DEBUG_INTERP_H");
   const int h = force ? (force[0] != '1' ? INTERP_H : 1)
                       : (INTERP_H >= 2 && p.n_lanes >= (uint32_t)INTERP_H * 256u * (uint32_t)nsm ? INTERP_H : 1);
-  if (p.alt_mask) return launch_interp_h<1, true, true>(p, s, nsm);  // classification re-run (rare)
+  if (p.alt_mask) return launch_interp_h<1, 1, true>(p, s, nsm);  // classification re-run (rare)
+  if (p.direct) {
+    if (p.may_spill)
+      return h > 1 ? launch_interp_h<INTERP_H, 2, true>(p, s, nsm) : launch_interp_h<1, 2, true>(p, s, nsm);
+    return h > 1 ? launch_interp_h<INTERP_H, 2, false>(p, s, nsm) : launch_interp_h<1, 2, false>(p, s, nsm);
+  }
   if (p.may_spill)
-    return h > 1 ? launch_interp_h<INTERP_H, false, true>(p, s, nsm) : launch_interp_h<1, false, true>(p, s, nsm);
-  return h > 1 ? launch_interp_h<INTERP_H, false, false>(p, s, nsm) : launch_interp_h<1, false, false>(p, s, nsm);
+    return h > 1 ? launch_interp_h<INTERP_H, 0, true>(p, s, nsm) : launch_interp_h<1, 0, true>(p, s, nsm);
+  return h > 1 ? launch_interp_h<INTERP_H, 0, false>(p, s, nsm) : launch_interp_h<1, 0, false>(p, s, nsm);
 }
 
 }  // namespace rc

@@ -160,6 +160,9 @@ struct InterpParams {
   const uint32_t* arr_off;    // [n_arrays] cell offset of each array inside an instance
   const uint32_t* arr_size;   // [n_arrays]
   const int32_t* heap;        // interval-start shared heap [I_b][cpi]
+  int32_t* heap_w;            // the same heap, written only in direct mode
+  bool direct;                // RC_OPT_PREPASS proved the run conflict-free: commit writes at the end of each
+                              // work-item's interval, log nothing (no grouping / detect kernels run)
   // lane state in / out (SoA)
   uint32_t reg_stride;        // row stride of the register arrays (>= n_lanes, multiple of 256)
   const int32_t* regs_in;     // [n_regs][reg_stride]; status / pc rows are padded to reg_stride too

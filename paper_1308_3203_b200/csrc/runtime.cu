@@ -126,6 +126,9 @@ struct rc_workspace {
   DevBuf ig;                              // inter-group race state (groups.cu), IG_FIELDS planes
   uint32_t spill_cap = 0;                 // entries per lane the spill buffers hold
   uint8_t wtag = 0;  // write-set map tag of the last interval attempt
+  bool prove_valid = false;     // cached rc_prove verdict (RC_OPT_PREPASS) for prove_key
+  std::vector<uint64_t> prove_key;
+  uint32_t prove_verdict = 0;
   bool plan_valid = false;      // cached batch plan (rc_run)
   uint64_t plan_key[4] = {0, 0, 0, 0};
   uint32_t plan_ib = 0;
@@ -361,6 +364,23 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     W.plan_valid = true;
   }
   const uint32_t I_b = W.plan_ib;
+  // RC_OPT_PREPASS: a run proved conflict-free by the
+  // symbolic pre-pass interprets its intervals in direct-commit mode
+  bool direct = false;
+  if ((opt.flags & RC_OPT_PREPASS) && G == 1 && !classify && n_inst) {
+    std::vector<uint64_t> key{n, opt.fuel_per_interval, opt.max_intervals};
+    key.insert(key.end(), size.begin(), size.begin() + n_arrays);
+    if (!W.prove_valid || W.prove_key != key) {
+      rc_prove_result pr;
+      const int pe = rc_prove(P, n, size.data(), n_arrays, opt.fuel_per_interval, 0, &pr);
+      if (pe != RC_OK) return pe;
+      // (an interval count beyond max_intervals is the host's instance-level FUEL report, unchanged)
+      W.prove_verdict = pr.verdict;
+      W.prove_key = key;
+      W.prove_valid = true;
+    }
+    direct = W.prove_verdict == RC_PROVE_NO_CONFLICT;
+  }
   const uint64_t L_max = (uint64_t)I_b * n;
   const uint64_t L_pad = (L_max + LANE_PAD - 1) / LANE_PAD * LANE_PAD + LANE_PAD;  // TMA rows, + a spare tile
   const int key_bits = bits_for((uint64_t)I_b * std::max<uint64_t>(cpi, 1));
@@ -634,6 +654,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       ip.arr_off = W.arr_off.as<uint32_t>();
       ip.arr_size = W.arr_size.as<uint32_t>();
       ip.heap = heap_cur;
+      ip.heap_w = heap_cur;
+      ip.direct = direct;
       ip.reg_stride = reg_stride;
       ip.regs_in = W.regs[cc].as<int32_t>();
       ip.pc_in = W.pc[cc].as<uint32_t>();
@@ -698,10 +720,14 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
                                 (uint32_t)cpi, gi * n, s));
       // ---- write-set filter: writes + reads of written cells, dense, with histograms
       // ---- write-set filter + K3: group the kept records by cell
-      EQ(enqueue_sort(W.prof.on ? &W.prof : nullptr, (opt.flags & RC_OPT_KEEP_ALL_READS) != 0));
+      if (!direct) EQ(enqueue_sort(W.prof.on ? &W.prof : nullptr, (opt.flags & RC_OPT_KEEP_ALL_READS) != 0));
       // ---- K4+K5 detect + commit, A4 check + verdict
       DetectParams dp = detect_params(kk);
       dp.with_boundary = true;  // A4 as detect's tail: consumes (and resets) K1's per-instance node ranges
+      if (direct) {  // nothing was logged: the kernel runs only its A4 tail (one block)
+        dp.nb = 0;
+        dp.n_records = 0;
+      }
       W.prof.begin(s);
       EQ(launch_detect(dp, s));
       W.prof.end(RC_PROF_DETECT, s, 0, 0);

@@ -23,6 +23,7 @@ KINDS = {1: "RW", 2: "WW_BENIGN", 3: "WW_NONBENIGN", 4: "OOB", 5: "ASSERT", 6: "
 RC_OPT_HOST_IO = 1
 RC_OPT_KEEP_ALL_READS = 2
 RC_OPT_CLASSIFY_RW = 4
+RC_OPT_PREPASS = 8
 PROF_CLASSES = ["interp", "hist", "sort", "detect", "boundary", "finalize", "copy", "filter"]
 
 REPORT_DTYPE = np.dtype([("instance", "<u4"), ("interval", "<u4"), ("array", "<i4"), ("index", "<i4"),
@@ -180,7 +181,8 @@ def rc_run(prog: Program, work_group_size: int, arrays: list, *, n_instances: in
            instance_offset: int = 0, fuel_per_interval: int = 0, max_intervals: int = 0, device: int | None = None,
            stream=None, capacity: int = 1 << 20, want_final: bool = True, final_out: list | None = None,
            profile: bool = False, max_batch_instances: int = 0, allow_truncate: bool = False,
-           keep_all_reads: bool = False, classify_rw: bool = False, n_groups: int = 1) -> RunResult:
+           keep_all_reads: bool = False, classify_rw: bool = False, n_groups: int = 1,
+           prepass: bool = False) -> RunResult:
     """Run `prog` on the arrays (n_groups work-groups of work_group_size
     work-items per instance, include/rc.h rc_options.n_groups).
 
@@ -232,7 +234,7 @@ def rc_run(prog: Program, work_group_size: int, arrays: list, *, n_instances: in
     opt.fuel_per_interval = fuel_per_interval
     opt.device = device
     opt.flags = (RC_OPT_HOST_IO if host_io else 0) | (RC_OPT_KEEP_ALL_READS if keep_all_reads else 0) | \
-        (RC_OPT_CLASSIFY_RW if classify_rw else 0)
+        (RC_OPT_CLASSIFY_RW if classify_rw else 0) | (RC_OPT_PREPASS if prepass else 0)
     opt.cuda_stream = C.c_void_p(stream.cuda_stream if stream is not None else 0)
     opt.max_batch_instances = max_batch_instances
     opt.n_groups = n_groups

@@ -694,3 +694,30 @@ def test_lsd_for_huge_instances(rc):
         b[:, :a.shape[1]] = a
     p, g, o = run_both(rc, K.STENCIL, n, big)
     assert_parity(g, o, big)
+
+
+def test_prepass_direct_commit(rc):
+    """RC_OPT_PREPASS: runs the symbolic pre-pass proves
+    conflict-free are interpreted in direct-commit mode with no grouping or
+    detect kernels — same (no) reports, final heaps and stats as the oracle;
+    runs it cannot prove take the normal path with the same results."""
+    proved = [(K.STENCIL, 3000, I.cfg5_inputs(0, 6, 3000)), (K.TREE, 1024, I.cfg3_inputs(0, 20, 1024)),
+              (K.PRIVATE_ONLY, 100, [np.arange(12, dtype=np.int32).reshape(3, 4)])]
+    for src, n, ins in proved:
+        p, g, o = run_both(rc, src, n, ins, prepass=True, profile=True)
+        assert_parity(g, o, ins)
+        assert g.profile["sort"]["launches"] == 0 and g.profile["hist"]["launches"] == 0, "direct mode not taken"
+        assert g.profile["interp"]["launches"] > 0
+    unproved = [(K.TREE_OFF_BY_ONE, 1024, I.cfg3_inputs(0, 10, 1024)), (K.BENIGN["K_c"], 256, I.cfg2_inputs(0, 8, 256)),
+                (K.BENIGN["K_inc"], 64, I.cfg2_inputs(0, 8, 64)), (K.FIG1, 8, I.cfg1_inputs())]
+    for src, n, ins in unproved:
+        p, g, o = run_both(rc, src, n, ins, prepass=True)
+        assert_parity(g, o, ins)
+    rng = np.random.default_rng(5)
+    for it in range(150):
+        n = int(rng.integers(1, 300))
+        pr = K.random_tiny_kernel(rng, n_arrays=2, n_regs=4, n_commands=int(rng.integers(2, 9)), size=5)
+        ins = [rng.integers(-3, 4, size=(int(rng.integers(1, 5)), 5)).astype(np.int32)]
+        ins.append(rng.integers(-3, 4, size=(ins[0].shape[0], 5)).astype(np.int32))
+        p, g, o = run_both(rc, pr, n, ins, fuel=500, prepass=True)
+        assert_parity(g, o, ins)
