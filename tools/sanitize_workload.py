@@ -1,4 +1,5 @@
 """Workload for tools/sanitize.sh: stencil (2 instances, n = 70000) and the
+round-2 paths at the end (oversized bucket, prepass, LSD sort, work-groups),
 classified tree reduction (300 instances, n = 1024) through the C ABI, and
 the interleaving explorer on K_inc (n = 4, both scheduling modes)."""
 import sys, os; sys.path.insert(0, os.getcwd())
@@ -22,3 +23,21 @@ args = dict(regs=torch.from_numpy(regs).cuda(), pc=torch.from_numpy(pc.astype(np
 for red in (True, False):
     r = rc_explore(prog, 4, torch.from_numpy(heap.astype(np.int32)).cuda(), reduced=red, **args)
     print("explore ok", r.n_schedules, r.n_differ)
+# round 2 paths: an oversized bucket (global counting sort), the prepass
+# direct-commit mode, the onesweep LSD path, work-groups
+p = K.program(K.BENIGN["K_inc"]); prog = rc_load_program(p.bytecode)
+ins = I.cfg2_inputs(0, 2, 20000)
+r = rc_run(prog, 20000, [torch.from_numpy(x).cuda() for x in ins])
+print("oversized bucket ok", len(r.reports))
+p = K.program(K.STENCIL); prog = rc_load_program(p.bytecode)
+ins = I.cfg5_inputs(0, 2, 70000)
+r = rc_run(prog, 70000, [torch.from_numpy(x).cuda() for x in ins], prepass=True)
+print("prepass ok", r.stats["checked_accesses"])
+os.environ["RC_SORT_LSD"] = "1"
+p = K.program(K.TREE_OFF_BY_ONE); prog = rc_load_program(p.bytecode)
+ins = I.cfg3_inputs(0, 40, 1024)
+r = rc_run(prog, 1024, [torch.from_numpy(x).cuda() for x in ins])
+print("lsd ok", len(r.reports))
+del os.environ["RC_SORT_LSD"]
+r = rc_run(prog, 512, [torch.from_numpy(x).cuda() for x in ins], n_groups=2)
+print("groups ok", len(r.reports))
