@@ -389,10 +389,14 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
     // per-lane state, lane h*T + t of the tile
     uint32_t g[H], pc[H], inst[H], tid[H], cell_base[H];
     uint32_t div[H];  // the instance's previous interval diverged (loaded before the lane state lands)
+    // a tile of TL <= n lanes spans at most two instances: one division per tile
+    const uint32_t inst_t = fast_div(tile * (uint32_t)TL, p.n_magic);
+    const uint32_t next_t = (inst_t + 1) * p.n;  // first lane of the next instance
 #pragma unroll
     for (int h = 0; h < H; h++) {
       g[h] = tile * (uint32_t)TL + h * T + t;
-      inst[h] = g[h] < p.n_lanes ? fast_div(g[h], p.n_magic) : 0;
+      inst[h] = g[h] >= p.n_lanes ? 0u
+                : (p.n >= (uint32_t)TL ? inst_t + (g[h] >= next_t ? 1u : 0u) : fast_div(g[h], p.n_magic));
       div[h] = (!ALT && p.ro_skip && p.interval > 0 && g[h] < p.n_lanes) ? __ldg(p.inst_div + inst[h]) : 0u;
     }
     mbar_wait_parity(&mbar[cur], (parity >> cur) & 1u);
@@ -527,7 +531,7 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
               pc[h]++;
               nloads[h]++;
               const uint32_t arr = (eh.x >> 8) & 0xFF;
-              ok = !DIRECT && (arr >= 32 || !((ro[h] >> arr) & 1u));  // a read of a written-in-no-way array is not logged
+              ok = !DIRECT && (arr >= 31 || !((ro[h] >> arr) & 1u));  // a read of a written-in-no-way array is not logged
             }
           }
           const unsigned m = __ballot_sync(FULL, ok);
@@ -703,7 +707,9 @@ __global__ void __launch_bounds__(INTERP_T, H == 1 ? INTERP_MIN_BLOCKS : INTERP_
             slot = SLOT_SPILL;
           }
           S.recs[S.fill + __popc(m & lanemask_lt())] = make_rec(cell, g[h], slot, 1);
-          p.wmap[cell] = p.wtag;  // write-set map (filter.cu)
+          // write-set map (the filter's dynamic half): not needed when no
+          // read of this instance's region is logged (entry_ro bit 31)
+          if (!(ro[h] >> 31)) p.wmap[cell] = p.wtag;
         }
         S.fill += __popc(m);
       }

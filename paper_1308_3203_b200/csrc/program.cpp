@@ -338,7 +338,7 @@ void analyze(rc_program* P) {
     if (wait[pc]) P->dev_code[pc].op |= OP_WAIT;
   // (5) arrays no instruction of an interval region stores to: for every
   //     interval entry e (pc 0, BAR + 1), the instructions reachable from e
-  //     without crossing a BAR; entry_ro[e] bit a (a < 32) = no ST to array a
+  //     without crossing a BAR; entry_ro[e] bit a (a < 31) = no ST to array a
   //     there.  When every running work-item of an instance starts interval k
   //     at the same entry e (interval 0, or interval k - 1 had no barrier
   //     divergence), no work-item writes array a in interval k, so a read of a
@@ -349,17 +349,18 @@ void analyze(rc_program* P) {
     std::vector<uint32_t> mark(N, 0xFFFFFFFFu), stack;
     for (uint32_t e = 0; e < N; e++) {
       if (!(e == 0 || P->code[e - 1].op == RC_OP_BAR)) continue;
-      uint32_t stored = 0;
-      bool big = false;  // a store to an array >= 32 (not in the mask) is fine; track nothing for it
+      uint32_t stored = 0, loaded = 0;
+      bool big_load = false;  // a load of an array >= 31 (outside the mask): always logged
       stack.assign(1, e);
       mark[e] = e;
       while (!stack.empty()) {
         const uint32_t pc = stack.back();
         stack.pop_back();
         const Ins& I = P->code[pc];
-        if (I.op == RC_OP_ST) {
-          if (I.a < 32) stored |= 1u << I.a;
-          else big = true;
+        if (I.op == RC_OP_ST && I.a < 31) stored |= 1u << I.a;
+        if (I.op == RC_OP_LD) {
+          if (I.b < 31) loaded |= 1u << I.b;
+          else big_load = true;
         }
         if (I.op == RC_OP_BAR) continue;  // the region ends at the barrier
         uint32_t sc[2];
@@ -368,8 +369,11 @@ void analyze(rc_program* P) {
         for (int j = 0; j < ns; j++)
           if (mark[sc[j]] != e) { mark[sc[j]] = e; stack.push_back(sc[j]); }
       }
-      (void)big;
-      P->entry_ro[e] = ~stored & (P->n_arrays >= 32 ? 0xFFFFFFFFu : ((1u << P->n_arrays) - 1));
+      const uint32_t ro = ~stored & (P->n_arrays >= 31 ? 0x7FFFFFFFu : ((1u << P->n_arrays) - 1));
+      // bit 31: no read of the region is logged (every load reads an array of
+      // the mask) — then no filter consults the write-set map for this
+      // instance's cells, and K1 need not mark it
+      P->entry_ro[e] = ro | ((!big_load && (loaded & ~ro) == 0) ? 0x80000000u : 0u);
     }
   }
 }
