@@ -455,6 +455,9 @@ struct BucketSmem {
   uint32_t nlist;
 };
 constexpr int BD_LIST = 32;  // buckets per block (blockIdx.x + i * gridDim.x, i < BD_LIST)
+// block barrier that does not assume a converged warp (barrier.sync without
+// .aligned): it follows detect_chunk, whose serial path runs on some lanes only
+__device__ __forceinline__ void block_sync() { asm volatile("barrier.sync 0;" ::: "memory"); }
 __device__ __forceinline__ uint32_t bucket_low(uint64_t r) {
   return (uint32_t)(r >> REC_CELL_SHIFT) & (BUCKET_CELLS - 1);
 }
@@ -522,7 +525,7 @@ __device__ __noinline__ void bucket_multi(const DetectParams& p, BucketSmem& S, 
     load_chunk(src, wg, M, ch);
     detect_chunk<SPILL>(p, src, wg, M, ch);
   }
-  __syncthreads();
+  block_sync();
 }
 
 template <bool SPILL, int ITEMS>
@@ -553,6 +556,7 @@ __device__ __forceinline__ void bucket_smem(const DetectParams& p, BucketSmem& S
     if (ok && lone && rec_w(r[j])) p.heap[rec_cell(r[j])] = val[j];
     multi |= ok && !lone;
   }
+  __syncwarp();
   if (__syncthreads_or(multi)) bucket_multi<SPILL>(p, S, s0, m);
   // (the records are dead here: the counters are cleared whole, 8 per thread)
 #pragma unroll
@@ -625,7 +629,7 @@ __global__ void __launch_bounds__(BD_THREADS, BD_MINB) bucket_detect_kernel(cons
       if (m > BD_CAP) bucket_global<SPILL>(p, S, s0, m);
       else if (m <= BD_CAP / 2) bucket_smem<SPILL, BD_ITEMS / 2>(p, S, s0, m);
       else bucket_smem<SPILL, BD_ITEMS>(p, S, s0, m);
-      __syncthreads();
+      block_sync();  // (after detect_chunk the lanes of a warp need not have reconverged)
     }
   }
   __syncwarp();
