@@ -442,12 +442,19 @@ __global__ void __launch_bounds__(256, DET_MINB) detect_kernel(const DetectParam
 #endif
 constexpr int BD_THREADS = BD_THREADS_OPT;
 constexpr int BD_ITEMS = 16;
-constexpr int BD_MINB = 1024 / BD_THREADS;  // resident blocks per SM (64 registers per thread)
+#ifndef BD_MINB_OPT
+#define BD_MINB_OPT (1024 / BD_THREADS_OPT)
+#endif
+constexpr int BD_MINB = BD_MINB_OPT;  // resident blocks per SM (1024 threads: 64 registers per thread)
+#ifndef BD_SORTED_OPT
+#define BD_SORTED_OPT (BD_THREADS_OPT * 16)
+#endif
+constexpr uint32_t BD_SORTED = BD_SORTED_OPT;  // multi-record cells' records placed in shared memory
 constexpr uint32_t BD_CAP = BD_THREADS * BD_ITEMS;  // records of a bucket held in registers
 constexpr int BD_WARPS = BD_THREADS / 32;
 constexpr int BD_ROUNDS = 2;  // 32-record rounds per detection chunk (the records are in shared memory / L2)
 struct BucketSmem {
-  uint64_t sorted[BD_CAP];      // records of the bucket's multi-record cells, by cell (global path: u32 offsets)
+  uint64_t sorted[BD_SORTED];   // records of the bucket's multi-record cells, by cell (global path: u32 offsets)
   uint32_t cnt[BUCKET_CELLS + 4];  // per cell: record count (bits 0-15), then | start << 16 during the
                                    // placement; [BUCKET_CELLS]: the spare counter of absent items
   uint32_t wsum[BD_WARPS];
@@ -512,18 +519,29 @@ __device__ __noinline__ void bucket_multi(const DetectParams& p, BucketSmem& S, 
       run += v[k];
     }
   __syncthreads();
+  // (more than BD_SORTED such records: placed in the global scratch instead)
+  uint64_t* dst = M <= BD_SORTED ? S.sorted : p.tmp + s0;
   for (uint32_t i = t; i < m; i += BD_THREADS) {
     const uint64_t r = __ldcg(p.recs + s0 + i);
     uint32_t* c = &S.cnt[bucket_low(r)];
-    if ((*c & 0xFFFFu) > 1u) S.sorted[atomicAdd(c, 1u << 16) >> 16] = r;
+    if ((*c & 0xFFFFu) > 1u) dst[atomicAdd(c, 1u << 16) >> 16] = r;
   }
   __syncthreads();
-  // segmented detection over sorted[0, M): warps take 64-record chunks
-  const SrcSmem src{S.sorted};
-  for (uint32_t wg = (uint32_t)t >> 5; wg * (32 * BD_ROUNDS) < M; wg += BD_WARPS) {
-    Chunk<BD_ROUNDS> ch;
-    load_chunk(src, wg, M, ch);
-    detect_chunk<SPILL>(p, src, wg, M, ch);
+  // segmented detection over dst[0, M): warps take 64-record chunks
+  if (M <= BD_SORTED) {
+    const SrcSmem src{S.sorted};
+    for (uint32_t wg = (uint32_t)t >> 5; wg * (32 * BD_ROUNDS) < M; wg += BD_WARPS) {
+      Chunk<BD_ROUNDS> ch;
+      load_chunk(src, wg, M, ch);
+      detect_chunk<SPILL>(p, src, wg, M, ch);
+    }
+  } else {
+    const SrcCg src{p.tmp + s0};
+    for (uint32_t wg = (uint32_t)t >> 5; wg * (32 * BD_ROUNDS) < M; wg += BD_WARPS) {
+      Chunk<BD_ROUNDS> ch;
+      load_chunk(src, wg, M, ch);
+      detect_chunk<SPILL>(p, src, wg, M, ch);
+    }
   }
   block_sync();
 }
