@@ -546,8 +546,10 @@ __device__ __noinline__ void bucket_multi(const DetectParams& p, BucketSmem& S, 
   block_sync();
 }
 
+// returns true (block-uniform) when the segmented detection ran (its lanes
+// may not have reconverged: the caller then uses the non-aligned barrier)
 template <bool SPILL, int ITEMS>
-__device__ __forceinline__ void bucket_smem(const DetectParams& p, BucketSmem& S, uint32_t s0, uint32_t m) {
+__device__ __forceinline__ bool bucket_smem(const DetectParams& p, BucketSmem& S, uint32_t s0, uint32_t m) {
   const int t = threadIdx.x;
   uint64_t r[ITEMS];
 #pragma unroll
@@ -575,11 +577,13 @@ __device__ __forceinline__ void bucket_smem(const DetectParams& p, BucketSmem& S
     multi |= ok && !lone;
   }
   __syncwarp();
-  if (__syncthreads_or(multi)) bucket_multi<SPILL>(p, S, s0, m);
+  const bool any_multi = __syncthreads_or(multi);
+  if (any_multi) bucket_multi<SPILL>(p, S, s0, m);
   // (the records are dead here: the counters are cleared whole, 8 per thread)
 #pragma unroll
   for (int k = 0; k < (int)(BUCKET_CELLS / BD_THREADS); k++) S.cnt[t + k * BD_THREADS] = 0u;  // (the caller synchronises)
   if (t == 0) S.cnt[BUCKET_CELLS] = 0u;
+  return any_multi;
 }
 
 // a bucket larger than BD_CAP: counting sort by cell into tmp[s0, s0 + m), then detect there
@@ -644,10 +648,12 @@ __global__ void __launch_bounds__(BD_THREADS, BD_MINB) bucket_detect_kernel(cons
     const uint32_t nl = S.nlist;
     for (uint32_t i = 0; i < nl; i++) {
       const uint32_t s0 = S.ls0[i], m = S.lm[i];
+      bool ran = true;
       if (m > BD_CAP) bucket_global<SPILL>(p, S, s0, m);
-      else if (m <= BD_CAP / 2) bucket_smem<SPILL, BD_ITEMS / 2>(p, S, s0, m);
-      else bucket_smem<SPILL, BD_ITEMS>(p, S, s0, m);
-      block_sync();  // (after detect_chunk the lanes of a warp need not have reconverged)
+      else if (m <= BD_CAP / 2) ran = bucket_smem<SPILL, BD_ITEMS / 2>(p, S, s0, m);
+      else ran = bucket_smem<SPILL, BD_ITEMS>(p, S, s0, m);
+      if (ran) block_sync();  // (after detect_chunk the lanes of a warp need not have reconverged)
+      else __syncthreads();
     }
   }
   __syncwarp();
