@@ -394,7 +394,7 @@ __device__ __forceinline__ void boundary_tail(const DetectParams& p) {
     __threadfence();
     c->bdone = 0;
     const volatile DevCounters* v = c;
-    const bool need_host = v->log_overflow || v->ovl_overflow || v->k1_reports > p.report_cap ||
+    const bool need_host = v->log_overflow || v->ovl_overflow || v->k1_reports > p.report_cap || v->bucket_overflow ||
                            v->report_count > p.report_cap || v->diverged || !v->any_waiting ||
                            (p.classify && v->rw_reports > 0);
     if (need_host) c->abort = 1;
@@ -625,7 +625,8 @@ __global__ void __launch_bounds__(BD_THREADS, BD_MINB) bucket_detect_kernel(cons
   BucketSmem& S = *reinterpret_cast<BucketSmem*>(bd_smem_raw);
   if (p.ctr->abort) return;  // speculative interval after one that needs the host (grid-uniform)
   const int t = threadIdx.x;
-  if (!(p.ctr->log_overflow || p.ctr->ovl_overflow || p.ctr->k1_reports > p.report_cap)) {
+  if (!(p.ctr->log_overflow || p.ctr->ovl_overflow || p.ctr->k1_reports > p.report_cap ||
+        (p.ctr->bucket_overflow && !p.region_rerun))) {
     for (uint32_t i = t; i < BUCKET_CELLS + 4; i += BD_THREADS) S.cnt[i] = 0u;
     // the block's buckets (static round robin: no claim round trips; empty
     // buckets — e.g. those of an array the interval does not write — drop out)
@@ -633,8 +634,18 @@ __global__ void __launch_bounds__(BD_THREADS, BD_MINB) bucket_detect_kernel(cons
       const uint32_t b = blockIdx.x + (uint32_t)t * gridDim.x;
       uint32_t s0 = 0, m = 0;
       if (b < p.nb) {
-        s0 = __ldg(p.bstart + b);
-        m = __ldg(p.bend + b) - s0;
+        if (p.region) {  // region mode: bucket b = recs[b * region, + min(rcur[b], region))
+          s0 = b * p.region;
+          if (p.region_rerun) {
+            m = p.rend[b] - s0;
+          } else {
+            m = min(__ldcg(p.rcur + b), p.region);
+            p.rend[b] = s0 + m;  // (for a detect-only re-run: the next interval resets rcur)
+          }
+        } else {
+          s0 = __ldg(p.bstart + b);
+          m = __ldg(p.bend + b) - s0;
+        }
       }
       const unsigned nz = __ballot_sync(0xFFFFFFFFu, m != 0);
       if (m) {

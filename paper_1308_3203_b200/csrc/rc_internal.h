@@ -117,6 +117,7 @@ struct DevCounters {
   unsigned long long rw_reports;    // RW reports emitted by detect (RC_OPT_CLASSIFY_RW)
   unsigned long long kept_writes;   // write records among the kept ones (profile bytes of detect)
   unsigned int count_done;          // bucket_count blocks finished (last-block pattern: the bucket starts)
+  unsigned int bucket_overflow;     // region mode: a bucket got more records than its region holds
   // ---- fields above: zeroed per interval attempt (one memset, runtime.cu)
   unsigned long long report_count;  // reports appended (whole run, rolled back on retry)
   unsigned long long lanes_final[8];
@@ -240,6 +241,12 @@ struct DetectParams {
   const uint32_t* bstart;
   const uint32_t* bend;
   uint64_t* tmp;
+  // region mode (ScatterParams::region): bucket b = recs[b * region, + min(rcur[b], region));
+  // the kernel records that end in rend[b]; a detect-only re-run (region_rerun) reads rend
+  uint32_t region;
+  const uint32_t* rcur;
+  uint32_t* rend;
+  bool region_rerun;
 };
 
 // ---- launchers (defined in the .cu files) --------------------------------
@@ -273,6 +280,7 @@ constexpr int BUCKET_BITS = 12;
 constexpr uint32_t BUCKET_CELLS = 1u << BUCKET_BITS;
 constexpr uint32_t NB_MAX = 8192;                     // buckets per batch: cells per batch <= 2^25
 constexpr uint64_t BUCKET_PATH_CELLS = (uint64_t)NB_MAX * BUCKET_CELLS;
+constexpr uint32_t BUCKET_REGION = 2 * BUCKET_CELLS;  // region mode: record slots a bucket owns
 
 struct SortWorkspace {
   uint64_t* alt = nullptr;         // ping-pong buffer
@@ -343,6 +351,11 @@ struct ScatterParams {
   uint64_t* out;
   uint32_t* bcur;
   DevCounters* ctr;
+  // region mode (region > 0): bucket b owns out[b * region, (b + 1) * region)
+  // and bcur[b] starts at 0 (no count pass); records beyond a region set
+  // ctr->bucket_overflow and are dropped (the host then regroups the interval
+  // with the counts).  0: count mode (bcur = the starts from bucket_count).
+  uint32_t region;
 };
 cudaError_t launch_bucket_scatter(const ScatterParams& p, cudaStream_t s, Profiler* prof);
 // bucket_count: the kept records of the staging buffer per bucket into

@@ -129,6 +129,7 @@ struct rc_workspace {
   bool prove_valid = false;     // cached rc_prove verdict (RC_OPT_PREPASS) for prove_key
   std::vector<uint64_t> prove_key;
   uint32_t prove_verdict = 0;
+  bool region_ok = true;        // bucket region mode for the cached plan (cleared after a bucket overflow)
   bool plan_valid = false;      // cached batch plan (rc_run)
   uint64_t plan_key[4] = {0, 0, 0, 0};
   uint32_t plan_ib = 0;
@@ -360,6 +361,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
     W.plan_ib = plan_batch(n_inst, n, cpi, P->n_regs, opt.max_batch_instances, free_b, G > 1, bucket);
+    W.region_ok = true;
     memcpy(W.plan_key, plan_key, sizeof plan_key);
     W.plan_valid = true;
   }
@@ -443,6 +445,13 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     return cudaSuccess;
   };
   CK(ensure_sort_status(log_cap));
+  // bucket region mode: bucket b owns W.log[b * BUCKET_REGION, + BUCKET_REGION)
+  // — no count pass; an overflowing bucket makes the host regroup the interval with the counts
+  bool region = bucket && W.region_ok && getenv("RC_BUCKET_COUNT") == nullptr;
+  if (region) {
+    const uint64_t nb_max = std::max<uint64_t>(1, ((uint64_t)I_b * cpi + BUCKET_CELLS - 1) / BUCKET_CELLS);
+    CK(W.log.ensure(std::max<uint64_t>(W.log.bytes, nb_max * BUCKET_REGION * 8 + 64)));
+  }
   // own-write overlay spill lists [spill_cap][L_max] (PAPER.md:176-179 puts no
   // bound on the cells a work-item writes in an interval): grown when K1
   // reports a full list, and the interval re-run
@@ -537,10 +546,11 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     const uint32_t nbk = bucket ? (uint32_t)std::max<uint64_t>(1, (bcells + BUCKET_CELLS - 1) / BUCKET_CELLS) : 0u;
     // write-set filter + grouping of one interval's records by cell (K3): the
     // bucket scatter (filter fused), or the filter and the onesweep passes
-    auto enqueue_sort = [&](Profiler* prof, bool keep_all) -> cudaError_t {
+    auto enqueue_sort = [&](Profiler* prof, bool keep_all, bool use_region) -> cudaError_t {
       if (bucket) {
         sr = W.log.as<uint64_t>();
         ScatterParams sp;
+        sp.region = 0;
         sp.stage = W.log_alt.as<uint64_t>();
         sp.n_slots = (uint32_t)log_cap;  // upper bound; the kernel reads stage_count
         sp.wmap = W.wmap.as<uint8_t>();
@@ -549,6 +559,11 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         sp.out = W.log.as<uint64_t>();
         sp.bcur = W.buckets.as<uint32_t>() + NB_MAX;
         sp.ctr = dctr;
+        if (use_region) {  // no count pass: the cursors (zeroed with the interval scratch) start at 0
+          sp.region = BUCKET_REGION;
+          sp.bcur = W.sort.hist;
+          return launch_bucket_scatter(sp, s, prof);
+        }
         cudaError_t e = launch_bucket_count(sp, W.sort.hist, nbk, W.buckets.as<uint32_t>(), s, prof);
         if (e != cudaSuccess) return e;
         return launch_bucket_scatter(sp, s, prof);
@@ -632,6 +647,10 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       dp.bstart = W.buckets.as<uint32_t>();
       dp.bend = W.buckets.as<uint32_t>() + NB_MAX;
       dp.tmp = W.log_alt.as<uint64_t>();  // (the staging buffer: free once the scatter has read it)
+      dp.region = region ? BUCKET_REGION : 0u;
+      dp.rcur = W.sort.hist;
+      dp.rend = W.buckets.as<uint32_t>() + NB_MAX;  // (free in region mode)
+      dp.region_rerun = false;
       return dp;
     };
     struct Marks { size_t m0 = 0, m1 = 0; };
@@ -720,7 +739,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
                                 (uint32_t)cpi, gi * n, s));
       // ---- write-set filter: writes + reads of written cells, dense, with histograms
       // ---- write-set filter + K3: group the kept records by cell
-      if (!direct) EQ(enqueue_sort(W.prof.on ? &W.prof : nullptr, (opt.flags & RC_OPT_KEEP_ALL_READS) != 0));
+      if (!direct) EQ(enqueue_sort(W.prof.on ? &W.prof : nullptr, (opt.flags & RC_OPT_KEEP_ALL_READS) != 0, region));
       // ---- K4+K5 detect + commit, A4 check + verdict
       DetectParams dp = detect_params(kk);
       dp.with_boundary = true;  // A4 as detect's tail: consumes (and resets) K1's per-instance node ranges
@@ -773,8 +792,9 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         ip.status_out = W.status_b.as<uint8_t>();
         ip.report_cap = 0;  // error reports of the re-run are not written (the count is restored below)
         EQ(launch_interp(ip, s));
-        EQ(enqueue_sort(nullptr, false));  // (the classified interval's own sorted log is not needed again)
+        EQ(enqueue_sort(nullptr, false, false));  // (the classified interval's own sorted log is not needed again)
         DetectParams dp = detect_params(kk);
+        dp.region = 0;  // (count mode: a re-run never overflows a region)
         dp.heap = W.heapB.as<int32_t>();
         dp.quiet = true;
         dp.report_cap = ~0ull;  // (quiet: nothing is written; K1's uncounted reports never skip the commit)
@@ -858,11 +878,33 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         continue;
       }
       if (next_aborted) CK(clear_abort());  // k+1 (if queued) has drained as a no-op before this
+      uint64_t rc_fix = UINT64_MAX;  // report count after a regrouping
+      if (h.bucket_overflow) {
+        // region mode: a bucket outgrew its region (detect skipped, K1's work
+        // stands): regroup this interval from the staging buffer with the
+        // bucket counts, and keep the count mode for this shape
+        // (the speculative next interval's scratch reset has run: restore this
+        // interval's staged-slot count; its write-set tag may be gone — the
+        // map is re-tagged or wiped per attempt — so every read record is
+        // kept, which changes no report and no commit)
+        W.region_ok = false;
+        region = false;
+        W.h_ctr[3].stage_count = h.stage_count;
+        CK(cudaMemcpyAsync(&dctr->stage_count, &W.h_ctr[3].stage_count, 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(W.sort.hist, 0, NB_MAX * sizeof(uint32_t), s));
+        CK(cudaMemsetAsync(&dctr->count_done, 0, sizeof(unsigned int), s));
+        CK(cudaMemsetAsync(&dctr->bucket_overflow, 0, sizeof(unsigned int), s));
+        CK(enqueue_sort(nullptr, /*keep_all=*/true, false));
+        DetectParams dp = detect_params(k);
+        CK(launch_detect(dp, s));
+        CK(read_ctr());
+        rc_fix = W.h_ctr[2].report_count;
+      }
       tot_loads += h.iv_loads;
       tot_stores += h.iv_stores;
       tot_instr += h.iv_instr;
       const uint64_t Ns = h.kept_count, Nslots = h.stage_count;
-      uint64_t rc = h.report_count;
+      uint64_t rc = rc_fix != UINT64_MAX ? rc_fix : h.report_count;
       // detect reports overflowed: grow, re-run detect (idempotent commits).  A
       // speculative interval's counter reset may have run: restore the count.
       if (rc > rep_cap) {
@@ -872,6 +914,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
           CK(grow_reports(rc));
           CK(set_report_count(h.k1_reports));
           DetectParams dp = detect_params(k);
+          dp.region_rerun = dp.region != 0;  // (the region cursors were reset by the next interval's scratch)
           CK(launch_detect(dp, s));
           CK(read_ctr());
           rc = W.h_ctr[2].report_count;

@@ -534,6 +534,9 @@ constexpr int BC_THREADS = 512;
 #endif
 constexpr int BC_ROUNDS = BC_ROUNDS_OPT;  // 16-byte loads per lane and chunk
 constexpr int BC_ITEMS = 2 * BC_ROUNDS;
+#ifndef BC_MINB
+#define BC_MINB 1
+#endif
 // A warp's chunk of 64 * ROUNDS staging slots: 16-byte loads, lane L of round
 // j takes slots c0 + 64 j + 2 L, + 1 into items 2 j, 2 j + 1 (slots >= n:
 // REC_SENTINEL).  Any order of a chunk's records inside a bucket is fine.
@@ -568,7 +571,7 @@ __device__ __forceinline__ void filter_chunk(const ScatterParams& p, uint64_t (&
     if (r[j] != REC_SENTINEL && !(r[j] & 1) && __ldg(p.wmap + (uint32_t)(r[j] >> REC_CELL_SHIFT)) != p.wtag)
       r[j] = REC_SENTINEL;
 }
-__global__ void __launch_bounds__(BC_THREADS) bucket_count_kernel(const ScatterParams p, uint32_t* __restrict__ hist,
+__global__ void __launch_bounds__(BC_THREADS, BC_MINB) bucket_count_kernel(const ScatterParams p, uint32_t* __restrict__ hist,
                                                                    uint32_t nb, uint32_t* __restrict__ bstart) {
   DevCounters* ctr = p.ctr;
   if (ctr->abort || ctr->log_overflow || ctr->ovl_overflow) return;  // grid-uniform
@@ -707,8 +710,21 @@ cudaError_t launch_bucket_count(const ScatterParams& p, uint32_t* hist, uint32_t
 #endif
 constexpr int BS_ROUNDS = BS_ROUNDS_OPT;  // 16-byte loads per lane and chunk
 constexpr int BS_ITEMS = 2 * BS_ROUNDS;
+#ifndef BS_MINB
+#define BS_MINB 1
+#endif
 constexpr int BS_THREADS = 256;
-__global__ void __launch_bounds__(BS_THREADS) bucket_scatter_kernel(const ScatterParams p) {
+// store record r at position pos of bucket b (count mode: pos is absolute)
+__device__ __forceinline__ void place(const ScatterParams& p, uint32_t b, uint32_t pos, uint64_t r) {
+  if (!p.region) {
+    __stcs(p.out + pos, r);
+  } else if (pos < p.region) {
+    __stcs(p.out + (size_t)b * p.region + pos, r);
+  } else {
+    p.ctr->bucket_overflow = 1;  // (idempotent; the host regroups the interval with the counts)
+  }
+}
+__global__ void __launch_bounds__(BS_THREADS, BS_MINB) bucket_scatter_kernel(const ScatterParams p) {
   const DevCounters* ctr = p.ctr;
   if (ctr->abort) return;  // speculative interval (DevCounters::abort)
   if (blockIdx.x == 0 && threadIdx.x == 0) p.ctr->k1_reports = p.ctr->report_count;  // K1 is complete here
@@ -745,7 +761,7 @@ __global__ void __launch_bounds__(BS_THREADS) bucket_scatter_kernel(const Scatte
 #pragma unroll
       for (int j = 0; j < BS_ITEMS; j++) {
         const unsigned m = __ballot_sync(FULL, r[j] != REC_SENTINEL);
-        if (r[j] != REC_SENTINEL) __stcs(p.out + base + __popc(m & lt), r[j]);
+        if (r[j] != REC_SENTINEL) place(p, bmin, base + __popc(m & lt), r[j]);
         base += __popc(m);
         kept_w += __popc(__ballot_sync(FULL, r[j] != REC_SENTINEL && (r[j] & 1)));
       }
@@ -770,7 +786,7 @@ __global__ void __launch_bounds__(BS_THREADS) bucket_scatter_kernel(const Scatte
 #pragma unroll
     for (int j = 0; j < BS_ITEMS; j++) {
       const uint32_t bb = __shfl_sync(FULL, base[j], lead[j]);
-      if (r[j] != REC_SENTINEL) __stcs(p.out + bb + rank[j], r[j]);
+      if (r[j] != REC_SENTINEL) place(p, (uint32_t)(r[j] >> (REC_CELL_SHIFT + BUCKET_BITS)), bb + rank[j], r[j]);
     }
   }
   if (lane == 0 && kept) {

@@ -640,14 +640,18 @@ def _grouping_cases(rng):
         yield pr, n, ins
 
 
-@pytest.mark.parametrize("path", ["bucket", "lsd"])
+@pytest.mark.parametrize("path", ["bucket", "count", "lsd"])
 def test_grouping_paths(rc, monkeypatch, path):
     """The bucket path (MSD scatter + per-bucket counting sort and detection,
-    the default) and the onesweep LSD path (RC_SORT_LSD=1; also taken when one
-    instance has more cells than the buckets cover) give the oracle's results,
-    also when every buffer starts tiny (grow-and-retry, detect-only re-runs)."""
+    the default: fixed bucket regions, no count pass), its count mode
+    (RC_BUCKET_COUNT=1; also taken after a bucket outgrew its region) and the
+    onesweep LSD path (RC_SORT_LSD=1; also taken when one instance has more
+    cells than the buckets cover) give the oracle's results, also when every
+    buffer starts tiny (grow-and-retry, detect-only re-runs)."""
     if path == "lsd":
         monkeypatch.setenv("RC_SORT_LSD", "1")
+    if path == "count":
+        monkeypatch.setenv("RC_BUCKET_COUNT", "1")
     for small in (False, True):
         if small:
             monkeypatch.setenv("RC_DEBUG_SMALL_BUFFERS", "1")
@@ -659,9 +663,11 @@ def test_grouping_paths(rc, monkeypatch, path):
 
 @pytest.mark.parametrize("n", [8193, 20000])
 def test_oversized_bucket(rc, n):
-    """A bucket with more records than the shared-memory capacity (8192) is
-    counting-sorted in global scratch: every work-item reads and writes A[0]
-    (K_inc: 2n records in one cell) and writes its own B cell."""
+    """A bucket with more records than its region (8192 slots) makes the host
+    regroup the interval with the bucket counts, and one with more than the
+    shared-memory capacity (8192) is counting-sorted in global scratch: every
+    work-item reads and writes A[0] (K_inc: 2n records in one cell) and writes
+    its own B cell."""
     src = """
 .arrays A B
     tid   r0
