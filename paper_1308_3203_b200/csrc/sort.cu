@@ -711,19 +711,22 @@ cudaError_t launch_bucket_count(const ScatterParams& p, uint32_t* hist, uint32_t
 constexpr int BS_ROUNDS = BS_ROUNDS_OPT;  // 16-byte loads per lane and chunk
 constexpr int BS_ITEMS = 2 * BS_ROUNDS;
 #ifndef BS_MINB
-#define BS_MINB 1
+#define BS_MINB 4
 #endif
 constexpr int BS_THREADS = 256;
-// store record r at position pos of bucket b (count mode: pos is absolute)
+// store record r at position pos of bucket b (count mode: pos is absolute;
+// region mode: pos is relative to the bucket's region, b * BUCKET_REGION)
+template <bool REGION>
 __device__ __forceinline__ void place(const ScatterParams& p, uint32_t b, uint32_t pos, uint64_t r) {
-  if (!p.region) {
+  if (!REGION) {
     __stcs(p.out + pos, r);
-  } else if (pos < p.region) {
-    __stcs(p.out + (size_t)b * p.region + pos, r);
+  } else if (pos < BUCKET_REGION) {
+    __stcs(p.out + (b * BUCKET_REGION + pos), r);  // (< 2^26: 32-bit arithmetic)
   } else {
     p.ctr->bucket_overflow = 1;  // (idempotent; the host regroups the interval with the counts)
   }
 }
+template <bool REGION>
 __global__ void __launch_bounds__(BS_THREADS, BS_MINB) bucket_scatter_kernel(const ScatterParams p) {
   const DevCounters* ctr = p.ctr;
   if (ctr->abort) return;  // speculative interval (DevCounters::abort)
@@ -761,7 +764,7 @@ __global__ void __launch_bounds__(BS_THREADS, BS_MINB) bucket_scatter_kernel(con
 #pragma unroll
       for (int j = 0; j < BS_ITEMS; j++) {
         const unsigned m = __ballot_sync(FULL, r[j] != REC_SENTINEL);
-        if (r[j] != REC_SENTINEL) place(p, bmin, base + __popc(m & lt), r[j]);
+        if (r[j] != REC_SENTINEL) place<REGION>(p, bmin, base + __popc(m & lt), r[j]);
         base += __popc(m);
         kept_w += __popc(__ballot_sync(FULL, r[j] != REC_SENTINEL && (r[j] & 1)));
       }
@@ -786,7 +789,7 @@ __global__ void __launch_bounds__(BS_THREADS, BS_MINB) bucket_scatter_kernel(con
 #pragma unroll
     for (int j = 0; j < BS_ITEMS; j++) {
       const uint32_t bb = __shfl_sync(FULL, base[j], lead[j]);
-      if (r[j] != REC_SENTINEL) place(p, (uint32_t)(r[j] >> (REC_CELL_SHIFT + BUCKET_BITS)), bb + rank[j], r[j]);
+      if (r[j] != REC_SENTINEL) place<REGION>(p, (uint32_t)(r[j] >> (REC_CELL_SHIFT + BUCKET_BITS)), bb + rank[j], r[j]);
     }
   }
   if (lane == 0 && kept) {
@@ -803,7 +806,7 @@ cudaError_t launch_bucket_scatter(const ScatterParams& p, cudaStream_t s, Profil
   cudaError_t se = setup.run(
       [](int d) -> cudaError_t {
         int per_sm = 0;
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bucket_scatter_kernel, BS_THREADS, 0);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bucket_scatter_kernel<true>, BS_THREADS, 0);
         if (e != cudaSuccess) return e;
         per_sm_of[d] = std::max(per_sm, 1);
         return cudaDeviceGetAttribute(&nsm_of[d], cudaDevAttrMultiProcessorCount, d);
@@ -814,7 +817,12 @@ cudaError_t launch_bucket_scatter(const ScatterParams& p, cudaStream_t s, Profil
   const uint32_t grid = (uint32_t)std::max<uint64_t>(
       1, std::min<uint64_t>((chunks + BS_THREADS / 32 - 1) / (BS_THREADS / 32), (uint64_t)nsm_of[dev] * per_sm_of[dev]));
   if (prof) prof->begin(s);
-  bucket_scatter_kernel<<<grid, BS_THREADS, 0, s>>>(p);
+  if (p.region) {
+    if (p.region != BUCKET_REGION) return cudaErrorInvalidValue;
+    bucket_scatter_kernel<true><<<grid, BS_THREADS, 0, s>>>(p);
+  } else {
+    bucket_scatter_kernel<false><<<grid, BS_THREADS, 0, s>>>(p);
+  }
   launched();
   if (prof) prof->end(RC_PROF_SORT, s, (uint64_t)p.n_slots * 16, p.n_slots);
   return cudaGetLastError();
