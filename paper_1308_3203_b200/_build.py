@@ -14,7 +14,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"] + os.environ.get("RC_EXTRA_NVCC_FLAGS", "").split()
-SOURCES = ["program.cpp", "prove.cpp", "interp.cu", "filter.cu", "sort.cu", "detect.cu", "boundary.cu", "runtime.cu", "explore.cu", "groups.cu"]
+SOURCES = ["program.cpp", "prove.cpp", "interp.cu", "filter.cu", "sort.cu", "detect.cu", "boundary.cu", "runtime.cu", "explore.cu", "groups.cu", "jit.cpp"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:

@@ -172,7 +172,8 @@ static void uses_defs(const Ins& I, int* use, int* nu, int* def) {
 // -1 = unbounded.  Tarjan SCCs of the barrier-free CFG (edges out of BAR and
 // EXIT removed): a cyclic SCC with positive weight is unbounded, otherwise DP
 // over the condensation (Tarjan emits SCCs in reverse topological order).
-static int64_t max_path_weight(const rc_program* P, const std::vector<int>& w) {
+// from >= 0: the longest path from that entry only.
+static int64_t max_path_weight(const rc_program* P, const std::vector<int>& w, int64_t from = -1) {
   const uint32_t N = P->n_instr;
   auto succ = [&](uint32_t pc, uint32_t* s, int* ns) {
     successors(P->code[pc], pc, N, s, ns);
@@ -239,6 +240,7 @@ static int64_t max_path_weight(const rc_program* P, const std::vector<int>& w) {
     }
   }
   if (unbounded) return -1;
+  if (from >= 0) return comp_best[comp[from]];
   int64_t m = comp_best[comp[0]];
   for (uint32_t pc = 0; pc + 1 < N; pc++)
     if (P->code[pc].op == RC_OP_BAR) m = std::max(m, comp_best[comp[pc + 1]]);
@@ -375,6 +377,27 @@ void analyze(rc_program* P) {
       // instance's cells, and K1 need not mark it
       P->entry_ro[e] = ro | ((!big_load && (loaded & ~ro) == 0) ? 0x80000000u : 0u);
     }
+  }
+  // (6) records per work-item per interval with (5) applied: per entry e, the
+  //     longest barrier-free path from e counting every ST and every LD of an
+  //     array e's region stores to.  Sizes K1c's record planes (jit.cpp); a
+  //     lane of a divergent instance (which logs every read) that exceeds it
+  //     makes K1c hand the interval back to the interpreter.
+  P->rec_bound_ro = P->rec_bound;
+  if (P->rec_bound >= 0) {
+    int64_t b = 0;
+    std::vector<int> w(N, 0);
+    for (uint32_t e = 0; e < N && b >= 0; e++) {
+      if (!(e == 0 || P->code[e - 1].op == RC_OP_BAR)) continue;
+      const uint32_t ro = P->entry_ro[e] & 0x7FFFFFFFu;
+      for (uint32_t pc = 0; pc < N; pc++) {
+        const Ins& I = P->code[pc];
+        w[pc] = I.op == RC_OP_ST || (I.op == RC_OP_LD && (I.b >= 31 || !((ro >> I.b) & 1u)));
+      }
+      const int64_t x = max_path_weight(P, w, e);
+      b = x < 0 ? -1 : std::max(b, x);
+    }
+    P->rec_bound_ro = (b < 0 || b > 1024) ? -1 : (int)b;
   }
 }
 

@@ -118,6 +118,7 @@ struct DevCounters {
   unsigned long long kept_writes;   // write records among the kept ones (profile bytes of detect)
   unsigned int count_done;          // bucket_count blocks finished (last-block pattern: the bucket starts)
   unsigned int bucket_overflow;     // region mode: a bucket got more records than its region holds
+  unsigned int jit_bail;            // K1c: a work-item had more records than its planes (re-run interpreted)
   // ---- fields above: zeroed per interval attempt (one memset, runtime.cu)
   unsigned long long report_count;  // reports appended (whole run, rolled back on retry)
   unsigned long long lanes_final[8];
@@ -205,6 +206,48 @@ struct InterpParams {
   unsigned long long report_cap;
   DevCounters* ctr;
 };
+
+// K1c (jit.cpp): the interval interpreter specialised to one program and run
+// shape — the bytecode compiled to a CUDA kernel with NVRTC at first use.
+// The parameter block is declared once here and handed to NVRTC as text, so
+// the host and the generated kernel share one layout.
+#define RC_K1C_PARAMS_DECL                                                                                \
+  struct K1cParams {                                                                                      \
+    const unsigned char* status_in; const unsigned int* pc_in; const int* regs_in;                        \
+    unsigned char* status_out; unsigned int* pc_out; int* regs_out;                                       \
+    const int* heap; int* heap_w; unsigned long long* stage; int* wval; unsigned char* wmap;             \
+    int* node_min; int* node_max; const unsigned int* inst_div; void* reports;                            \
+    unsigned long long* report_count; unsigned long long* stage_count; unsigned long long* staged_recs;   \
+    unsigned long long* iv_loads; unsigned long long* iv_stores; unsigned long long* iv_instr;            \
+    unsigned int* log_overflow; unsigned int* any_waiting; unsigned int* jit_bail; const unsigned int* abort; \
+    unsigned long long report_cap; unsigned long long fuel; unsigned long long stage_cap;                 \
+    unsigned int n_lanes, lane_pad, reg_stride, interval, inst_base, planes, wtag, check_div;              \
+  };
+RC_K1C_PARAMS_DECL
+#define RC_STR2_(...) #__VA_ARGS__
+#define RC_STR_(x) RC_STR2_(x)
+
+// What a K1c kernel is specialised to (besides the program): the cache key.
+struct JitShape {
+  uint32_t n = 0, gid = 0, cpi = 0;
+  std::vector<uint32_t> off, size;  // per array
+  bool direct = false;   // RC_OPT_PREPASS direct-commit mode (no log)
+  bool fuel = false;     // per-instruction fuel check
+  bool ro_skip = false;  // static write-set elision (off with RC_OPT_KEEP_ALL_READS / work-groups)
+};
+struct JitKernel {
+  void* fn = nullptr;   // CUfunction
+  int grid = 0;         // persistent grid (resident blocks per SM x SMs)
+};
+// The program's K1c kernel for this shape on the current device: compiled and
+// loaded on first use, cached on the program.  false (with a reason in *why)
+// when the program is not eligible or NVRTC / the driver is unavailable; the
+// caller then runs the interpreter.
+bool jit_get(rc_program* P, const JitShape& S, JitKernel* out, std::string* why);
+cudaError_t jit_launch(const JitKernel& k, const K1cParams& p, cudaStream_t s);
+void jit_release(rc_program* P);  // unload the cached modules (on their devices)
+// the K1c source for a program and shape (tests / RC_JIT_DUMP)
+std::string jit_source(const rc_program* P, const JitShape& S);
 
 struct DetectParams {
   const uint64_t* recs;       // sorted by cell; count = ctr->kept_count
@@ -433,8 +476,10 @@ struct rc_program {
   int ovl_cap = rc::OVL_CAP;       // smem overlay entries (max distinct cells written per work-item per interval, capped)
   bool may_spill = true;           // a work-item may write more than OVL_CAP distinct cells in one interval
   int rec_bound = -1;              // max log records per work-item per interval (-1 unbounded)
+  int rec_bound_ro = -1;           // the same with the static write-set elision (5) applied (K1c record planes)
   int64_t instr_bound = -1;        // max instructions per work-item per interval (-1 unbounded)
   std::mutex mu;
   rc_workspace* ws = nullptr;
   rc::ExploreCache xc;
+  void* jit = nullptr;             // K1c kernels compiled for this program (jit.cpp)
 };

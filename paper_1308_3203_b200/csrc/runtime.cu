@@ -239,6 +239,7 @@ void rc_free_program(rc_program* P) {
     }
     if (prev >= 0) cudaSetDevice(prev);
   }
+  rc::jit_release(P);
   delete P;
 }
 
@@ -254,6 +255,7 @@ int rc_release_workspace(rc_program* P) {
     DeviceGuard g(P->xc.device);
     P->xc.release();
   }
+  jit_release(P);
   return RC_OK;
 }
 
@@ -478,6 +480,46 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     CK(W.reports.ensure(4 * sizeof(rc_report)));
     rep_cap = W.reports.bytes / sizeof(rc_report);
   }
+
+  // K1c (jit.cpp): the intervals run in a kernel compiled for this program
+  // and shape when the batches are large enough to repay the compile (once per
+  // program and shape; RC_JIT=1 forces it for any size, RC_JIT=0 keeps K1).
+  // Not with work-groups, RW classification re-runs (always K1) or programs
+  // jit_get declines; a K1c interval that bails (jit_bail) is re-run by K1 and
+  // K1 keeps the rest of the run.
+  JitKernel jk;
+  bool jit_on = false;
+  int jit_planes = 0;
+  {
+    const char* je = getenv("RC_JIT");
+    const bool force = je && je[0] == '1';
+    const uint64_t min_lanes = getenv("RC_JIT_MIN_LANES") ? strtoull(getenv("RC_JIT_MIN_LANES"), nullptr, 10) : (1ull << 20);
+    if (!(je && je[0] == '0') && G == 1 && I_b && (force || L_max >= min_lanes)) {
+      JitShape S;
+      S.n = n;
+      S.gid = 0;
+      S.cpi = (uint32_t)cpi;
+      S.off.assign(off.begin(), off.begin() + n_arrays);
+      S.size.assign(size.begin(), size.begin() + n_arrays);
+      S.direct = direct;
+      S.fuel = P->instr_bound < 0 || (uint64_t)P->instr_bound > opt.fuel_per_interval;
+      S.ro_skip = (opt.flags & RC_OPT_KEEP_ALL_READS) == 0;
+      std::string why;
+      jit_on = jit_get(P, S, &jk, &why);
+      if (!jit_on && getenv("RC_JIT_VERBOSE")) fprintf(stderr, "rc: K1c not used: %s\n", why.c_str());
+      jit_planes = direct ? 0 : (S.ro_skip ? P->rec_bound_ro : P->rec_bound);
+      if (jit_on && jit_planes > 0) {  // fixed record slots: planes x (lanes rounded up to LANE_PAD)
+        const uint64_t want = (uint64_t)jit_planes * ((L_max + LANE_PAD - 1) / LANE_PAD * LANE_PAD);
+        if (log_cap < want) {
+          CK(W.log.ensure(std::max<uint64_t>(W.log.bytes, want * 8)));
+          CK(W.log_alt.ensure(want * 8));
+          log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
+          CK(ensure_sort_status(log_cap));
+        }
+      }
+    }
+  }
+  bool jit_off = false;  // a K1c interval bailed: K1 for the rest of the run
 
   uint64_t tot_loads = 0, tot_stores = 0, tot_instr = 0, intervals_max = 0;
   uint64_t rep_count = 0;  // host mirror of ctr.report_count
@@ -730,7 +772,48 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       mk->m0 = W.prof.marks.size();
       W.prof.cut();
       W.prof.begin(s);
-      EQ(launch_interp(ip, s));
+      if (jit_on && !jit_off) {
+        K1cParams kp;
+        kp.status_in = ip.status_in;
+        kp.pc_in = ip.pc_in;
+        kp.regs_in = ip.regs_in;
+        kp.status_out = ip.status_out;
+        kp.pc_out = ip.pc_out;
+        kp.regs_out = ip.regs_out;
+        kp.heap = ip.heap;
+        kp.heap_w = ip.heap_w;
+        kp.stage = reinterpret_cast<unsigned long long*>(ip.stage);
+        kp.wval = ip.wval;
+        kp.wmap = ip.wmap;
+        kp.node_min = ip.node_min;
+        kp.node_max = ip.node_max;
+        kp.inst_div = ip.inst_div;
+        kp.reports = ip.reports;
+        kp.report_count = &dctr->report_count;
+        kp.stage_count = &dctr->stage_count;
+        kp.staged_recs = &dctr->staged_recs;
+        kp.iv_loads = &dctr->iv_loads;
+        kp.iv_stores = &dctr->iv_stores;
+        kp.iv_instr = &dctr->iv_instr;
+        kp.log_overflow = &dctr->log_overflow;
+        kp.any_waiting = &dctr->any_waiting;
+        kp.jit_bail = &dctr->jit_bail;
+        kp.abort = &dctr->abort;
+        kp.report_cap = ip.report_cap;
+        kp.fuel = ip.fuel;
+        kp.stage_cap = ip.stage_cap;
+        kp.n_lanes = L;
+        kp.lane_pad = reg_stride;
+        kp.reg_stride = reg_stride;
+        kp.interval = kk;
+        kp.inst_base = inst_base;
+        kp.planes = (uint32_t)jit_planes;
+        kp.wtag = W.wtag;
+        kp.check_div = ip.ro_skip && kk > 0;
+        EQ(jit_launch(jk, kp, s));
+      } else {
+        EQ(launch_interp(ip, s));
+      }
       W.prof.end(RC_PROF_INTERP, s, 0, L);
       // inter-group races: this group's smallest reader / writer per cell
       // (from the staging buffer, before the sort reuses it)
@@ -858,11 +941,12 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       const bool k1_rep_over = h.k1_reports > rep_cap;
       const bool spill_over = h.ovl_overflow != 0;  // a work-item's spill list was full
       if (log_over || k1_rep_over || spill_over) {  // filter/detect skipped: grow and re-run the interval
+        if (h.jit_bail) jit_off = true;  // a K1c work-item had more records than its planes: K1 re-runs it
         if (spill_over) {
           const int e = grow_spill();
           if (e != RC_OK) return e;
         }
-        if (log_over) {
+        if (log_over && !h.jit_bail) {
           const uint64_t want = std::min<uint64_t>(n_all + n_all / 4 + 1024, 0xFFFFFFFFull);
           if (n_all > 0xFFFFFFFFull) return fail(RC_ELIMIT, "more than 2^32 access records in one interval");
           CK(W.log.ensure(want * 8));

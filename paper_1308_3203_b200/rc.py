@@ -116,6 +116,12 @@ def lib():
         L.rc_prove.argtypes = [C.c_void_p, C.c_uint32, P(C.c_uint32), C.c_uint32, C.c_uint64, C.c_uint64,
                                P(rc_prove_result)]
         L.rc_prove.restype = C.c_int
+        # test hooks (jit.cpp; not part of include/rc.h)
+        L.rc_debug_jit_kernels.argtypes = [C.c_void_p]
+        L.rc_debug_jit_kernels.restype = C.c_int
+        L.rc_debug_jit_source.argtypes = [C.c_void_p, C.c_uint32, P(C.c_uint32), C.c_uint32, C.c_uint32,
+                                          C.c_char_p, C.c_size_t]
+        L.rc_debug_jit_source.restype = C.c_size_t
         _lib = L
     return _lib
 
@@ -136,6 +142,20 @@ class Program:
 
     def release_workspace(self):
         lib().rc_release_workspace(self._h)
+
+    def jit_kernels(self) -> int:
+        """Test hook: K1c kernels compiled for this program so far (jit.cpp)."""
+        return int(lib().rc_debug_jit_kernels(self._h))
+
+    def jit_source(self, work_group_size: int, sizes: list, *, direct=False, fuel=False, ro_skip=True) -> str:
+        """Test hook: the K1c CUDA source for this program and shape (no GPU needed)."""
+        arr = (C.c_uint32 * max(1, len(sizes)))(*sizes)
+        flags = (1 if direct else 0) | (2 if fuel else 0) | (4 if ro_skip else 0)
+        f = lib().rc_debug_jit_source
+        nb = f(self._h, work_group_size, arr, len(sizes), flags, None, 0)
+        buf = C.create_string_buffer(nb + 1)
+        f(self._h, work_group_size, arr, len(sizes), flags, buf, nb + 1)
+        return buf.value.decode()
 
     def __del__(self):
         if getattr(self, "_h", None) and self._h.value and _lib is not None:

@@ -21,13 +21,23 @@ from workloads.asm import assemble  # noqa: E402
 STAT_KEYS = ("checked_accesses", "loads", "stores", "instructions", "intervals_max", "lanes_final")
 
 
-@pytest.fixture(scope="module")
-def rc():
+@pytest.fixture(scope="module", params=["k1", "k1c"])
+def rc(request):
+    """The library, once per interval kernel: K1 (the bytecode interpreter,
+    RC_JIT=0) and K1c (the kernel compiled per program with NVRTC, RC_JIT=1
+    forces it at every size; programs it declines run K1)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
+    import os
     import paper_1308_3203_b200 as pkg
     pkg.lib()
-    return pkg
+    old = os.environ.get("RC_JIT")
+    os.environ["RC_JIT"] = "1" if request.param == "k1c" else "0"
+    yield pkg
+    if old is None:
+        os.environ.pop("RC_JIT", None)
+    else:
+        os.environ["RC_JIT"] = old
 
 
 def run_both(rc, src_or_prog, n, ins, *, fuel=0, max_intervals=0, host=False, **kw):
