@@ -53,6 +53,11 @@ namespace {
 constexpr int JIT_MAX_PLANES = 32;
 constexpr uint32_t JIT_MAX_INSTR = 4096;
 constexpr int JIT_THREADS = 256;
+// resident blocks per SM the register allocation must allow (RC_JIT_MINB, A/B knob)
+int jit_min_blocks() {
+  const char* e = getenv("RC_JIT_MINB");
+  return e ? std::max(1, atoi(e)) : 2;
+}
 
 // ---- NVRTC (dlopen: librc.so loads without it) and the driver API (entry
 //      points through the runtime: no -lcuda) -------------------------------
@@ -135,7 +140,7 @@ namespace {
 
 std::string shape_key(const JitShape& S) {
   std::ostringstream o;
-  o << S.n << ':' << S.gid << ':' << S.cpi << ':' << S.direct << S.fuel << S.ro_skip;
+  o << S.n << ':' << S.gid << ':' << S.cpi << ':' << S.direct << S.fuel << S.ro_skip << S.wbucket;
   for (size_t a = 0; a < S.off.size(); a++) o << ':' << S.off[a] << '/' << S.size[a];
   return o.str();
 }
@@ -189,11 +194,123 @@ Facts facts(const rc_program* P) {
   return F;
 }
 
+// Registers live on entry to each pc (backward dataflow; BAR -> pc + 1 is an
+// edge: registers persist across barriers).
+std::vector<std::vector<uint8_t>> live_in(const rc_program* P) {
+  const uint32_t N = P->n_instr, R = P->n_regs;
+  std::vector<std::vector<uint8_t>> L(N, std::vector<uint8_t>(R, 0));
+  for (bool changed = true; changed;) {
+    changed = false;
+    for (int64_t pc = (int64_t)N - 1; pc >= 0; pc--) {
+      const Ins& I = P->code[pc];
+      std::vector<uint8_t> v(R, 0);
+      uint32_t s[2];
+      int ns = 0;
+      if (I.op == RC_OP_BR) { s[ns++] = (uint32_t)I.imm; s[ns++] = (uint32_t)I.b + 256u * I.c; }
+      else if (I.op == RC_OP_JMP) s[ns++] = (uint32_t)I.imm;
+      else if (I.op != RC_OP_EXIT && pc + 1 < N) s[ns++] = (uint32_t)pc + 1;
+      for (int j = 0; j < ns; j++)
+        for (uint32_t r = 0; r < R; r++) v[r] |= L[s[j]][r];
+      int def = -1, use[2] = {-1, -1};
+      switch (I.op) {
+        case RC_OP_ST: use[0] = I.b; use[1] = I.c; break;
+        case RC_OP_LD: use[0] = I.c; def = I.a; break;
+        case RC_OP_ASSUME: case RC_OP_ASSERT: case RC_OP_BR: use[0] = I.a; break;
+        case RC_OP_BAR: case RC_OP_JMP: case RC_OP_EXIT: break;
+        case RC_OP_CONST: case RC_OP_TID: case RC_OP_GID: case RC_OP_LID: case RC_OP_LSIZE: case RC_OP_SIZE:
+          def = I.a; break;
+        case RC_OP_MOV: case RC_OP_LNOT: case RC_OP_ADDI: def = I.a; use[0] = I.b; break;
+        default: def = I.a; use[0] = I.b; use[1] = I.c; break;
+      }
+      if (def >= 0) v[def] = 0;
+      for (int u : use)
+        if (u >= 0) v[u] = 1;
+      if (v != L[pc]) { L[pc] = v; changed = true; }
+    }
+  }
+  return L;
+}
+
+// Register values that are the same affine function a*lid + b (mod 2^32) of
+// the work-item's local id on every path into pc — over the whole program,
+// barriers included (registers start at 0, reading L18).  K1c rematerialises
+// such a register at an interval entry instead of carrying it through HBM.
+struct Aff {
+  uint8_t k = 0;  // 0 unreached, 1 known, 2 unknown
+  uint32_t a = 0, b = 0;
+  bool operator==(const Aff& o) const { return k == o.k && (k != 1 || (a == o.a && b == o.b)); }
+};
+std::vector<std::vector<Aff>> affine_in(const rc_program* P, const JitShape& S) {
+  const uint32_t N = P->n_instr, R = P->n_regs;
+  std::vector<std::vector<Aff>> A(N, std::vector<Aff>(R));
+  for (uint32_t r = 0; r < R; r++) A[0][r] = Aff{1, 0, 0};
+  auto known = [](uint32_t a, uint32_t b) { return Aff{1, a, b}; };
+  const Aff top{2, 0, 0};
+  auto join = [](Aff& d, const Aff& x) {
+    if (x.k == 0 || d.k == 2) return false;
+    if (d.k == 0) { d = x; return true; }
+    if (x.k == 2 || !(x == d)) { d = Aff{2, 0, 0}; return true; }
+    return false;
+  };
+  std::vector<uint8_t> work(N, 0);
+  work[0] = 1;
+  for (bool any = true; any;) {
+    any = false;
+    for (uint32_t pc = 0; pc < N; pc++) {
+      if (!work[pc]) continue;
+      work[pc] = 0;
+      const Ins& I = P->code[pc];
+      std::vector<Aff> v = A[pc];
+      const Aff x = v[I.b < R ? I.b : 0], y = v[I.c < R ? I.c : 0];
+      switch (I.op) {
+        case RC_OP_CONST: v[I.a] = known(0, (uint32_t)I.imm); break;
+        case RC_OP_TID: v[I.a] = known(1, S.gid * S.n); break;
+        case RC_OP_LID: v[I.a] = known(1, 0); break;
+        case RC_OP_GID: v[I.a] = known(0, S.gid); break;
+        case RC_OP_LSIZE: v[I.a] = known(0, S.n); break;
+        case RC_OP_SIZE: v[I.a] = known(0, S.size[I.b]); break;
+        case RC_OP_MOV: v[I.a] = x; break;
+        case RC_OP_ADDI: v[I.a] = x.k == 1 ? known(x.a, x.b + (uint32_t)I.imm) : x; break;
+        case RC_OP_ADD: v[I.a] = (x.k == 1 && y.k == 1) ? known(x.a + y.a, x.b + y.b) : top; break;
+        case RC_OP_SUB: v[I.a] = (x.k == 1 && y.k == 1) ? known(x.a - y.a, x.b - y.b) : top; break;
+        case RC_OP_MUL:
+          v[I.a] = (x.k == 1 && y.k == 1 && x.a == 0) ? known(x.b * y.a, x.b * y.b)
+                   : (x.k == 1 && y.k == 1 && y.a == 0) ? known(x.a * y.b, x.b * y.b) : top;
+          break;
+        case RC_OP_ST: case RC_OP_BAR: case RC_OP_JMP: case RC_OP_EXIT: case RC_OP_ASSUME: case RC_OP_ASSERT:
+        case RC_OP_BR: break;
+        default: v[I.a] = top; break;  // LD and the other ALU ops
+      }
+      uint32_t s[2];
+      int ns = 0;
+      if (I.op == RC_OP_BR) { s[ns++] = (uint32_t)I.imm; s[ns++] = (uint32_t)I.b + 256u * I.c; }
+      else if (I.op == RC_OP_JMP) s[ns++] = (uint32_t)I.imm;
+      else if (I.op != RC_OP_EXIT && pc + 1 < N) s[ns++] = pc + 1;
+      for (int j = 0; j < ns; j++) {
+        bool ch = false;
+        for (uint32_t r = 0; r < R; r++) ch |= join(A[s[j]][r], v[r]);
+        if (ch) { work[s[j]] = 1; any = true; }
+      }
+    }
+  }
+  return A;
+}
+
 }  // namespace
 
 std::string jit_source(const rc_program* P, const JitShape& S) {
   const uint32_t N = P->n_instr;
   const Facts F = facts(P);
+  const auto LIVE = live_in(P);
+  const auto AFF = affine_in(P, S);
+  // registers carried through HBM: live at some interval entry where their
+  // value is not a known affine function of the local id (the others are
+  // rematerialised at the entry and never stored)
+  std::vector<uint8_t> carried(P->n_regs, 0);
+  for (uint32_t e = 0; e < N; e++)
+    if (F.entry[e])
+      for (uint32_t r = 0; r < P->n_regs; r++)
+        if (LIVE[e][r] && AFF[e][r].k != 1) carried[r] = 1;
   const int K = std::max(1, P->ovl_cap);
   const bool D = S.direct;
   std::ostringstream o;
@@ -215,11 +332,12 @@ std::string jit_source(const rc_program* P, const JitShape& S) {
     << "  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);\n"
     << "  return v;\n"
     << "}\n"
-    << "extern \"C\" __global__ void __launch_bounds__(" << JIT_THREADS << ") rc_k1c(const __grid_constant__ K1cParams p) {\n"
+    << "extern \"C\" __global__ void __launch_bounds__(" << JIT_THREADS << ", " << jit_min_blocks()
+    << ") rc_k1c(const __grid_constant__ K1cParams p) {\n"
     << "  if (*p.abort) return;  // speculative interval (DevCounters::abort)\n"
     << "  const u32 lane = threadIdx.x & 31u;\n"
     << "  u64 s_instr = 0, s_loads = 0, s_stores = 0, s_recs = 0;\n"
-    << "  bool s_wait = false, s_bail = false;\n"
+    << "  bool s_wait = false, s_bail = false, s_bover = false;\n"
     << "  u32 a4_inst = 0xFFFFFFFFu; i32 a4_lo = 0, a4_hi = 0;\n";
   if (!D)
     o << "  if (blockIdx.x == 0 && threadIdx.x == 0) {\n"
@@ -227,13 +345,56 @@ std::string jit_source(const rc_program* P, const JitShape& S) {
       << "    if ((u64)p.planes * p.lane_pad > p.stage_cap) *p.log_overflow = 1;  // the host grows the buffer, re-runs\n"
       << "  }\n"
       << "  if ((u64)p.planes * p.lane_pad > p.stage_cap) return;\n";
+  // the next lane's state is loaded while this lane runs (software pipeline:
+  // its latency overlaps the heap loads and the writes of the current one)
+  auto prefetch = [&](const char* gexpr, const char* cond) {
+    o << "    { const u32 g2 = " << gexpr << "; n_st = " << (int)L_EXITED << "; n_pc = 0u;\n"
+      << "      if (" << cond << " && g2 < p.n_lanes) {\n"
+      << "        n_st = p.status_in[g2]; n_pc = p.pc_in[g2];\n";
+    for (uint32_t r = 0; r < P->n_regs; r++)
+      if (carried[r]) o << "        n_r" << r << " = p.regs_in[(u64)" << r << " * p.reg_stride + g2];\n";
+    o << "      } }\n";
+  };
   o << "  const u32 stride = gridDim.x * blockDim.x;\n"
-    << "  for (u32 base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < p.lane_pad; base += stride) {\n"
+    << "  u32 base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);\n"
+    << "  u8 n_st; u32 n_pc;";
+  for (uint32_t r = 0; r < P->n_regs; r++)
+    if (carried[r]) o << " i32 n_r" << r << " = 0;";
+  o << "\n";
+  // (RC_JIT_NOPF=1, A/B knob: load each lane's state when it starts.  With
+  // every register carried the prefetch cost occupancy — 87.6 vs 82.4 ms/step;
+  // with the rematerialised registers only status, pc and the carried ones
+  // are in flight: 57.1 vs 70.7 ms/step)
+  const bool pf = getenv("RC_JIT_NOPF") == nullptr;
+  if (pf) prefetch("base + lane", "base < p.lane_pad");
+  // bucket writes with a deferred slot: the cursor atomic of a lane's write
+  // record is issued at the end of its iteration and its result consumed at
+  // the top of the warp's next one, so the L2 round trip overlaps the next
+  // lane's loads (up to two overlay slots; RC_JIT_NODEFER=1: A/B knob)
+  const int DEF = (S.wbucket && !D && getenv("RC_JIT_NODEFER") == nullptr) ? std::min(K, 2) : 0;
+  for (int j = 0; j < DEF; j++)
+    o << "  u64 d_rec" << j << " = 0; u32 d_raw" << j << " = 0, d_m" << j << " = 0, d_b" << j << " = 0;\n";
+  auto flush = [&](int j) {
+    o << "    if (d_m" << j << ") {  // the previous lane's write record, slot " << j << "\n"
+      << "      const u32 pos = __shfl_sync(d_m" << j << ", d_raw" << j << ", __ffs(d_m" << j << ") - 1) + __popc(d_m" << j
+      << " & ((1u << lane) - 1u));\n"
+      << "      if (pos < p.region) p.bucket_out[(u64)d_b" << j << " * p.region + pos] = d_rec" << j
+      << "; else s_bover = true;\n"
+      << "      d_m" << j << " = 0;\n"
+      << "    }\n";
+  };
+  o << "  for (; base < p.lane_pad; base += stride) {\n"
     << "    const u32 g = base + lane;\n"
-    << "    const bool valid = g < p.n_lanes;\n"
-    << "    u8 st = valid ? p.status_in[g] : (u8)" << (int)L_EXITED << ";\n"
-    << "    u32 pc = valid ? p.pc_in[g] : 0u;\n"
-    << "    if (st == " << (int)L_EXITED_NOW << ") st = " << (int)L_EXITED << ";\n"
+    << "    const bool valid = g < p.n_lanes;\n";
+  if (!pf) prefetch("g", "true");
+  o << "    u8 st = n_st;\n"
+    << "    u32 pc = n_pc;\n";
+  for (uint32_t r = 0; r < P->n_regs; r++) {
+    o << "    i32 r" << r << " = " << (carried[r] ? "n_r" + std::to_string(r) : std::string("0")) << ";\n";
+  }
+  if (pf) prefetch("g + stride", "base + stride < p.lane_pad");
+  for (int j = 0; j < DEF; j++) flush(j);
+  o << "    if (st == " << (int)L_EXITED_NOW << ") st = " << (int)L_EXITED << ";\n"
     << "    const bool running = valid && (st == " << (int)L_RUNNING << " || st == " << (int)L_WAITING << ");\n"
     << "    const u32 inst = valid ? g / " << S.n << "u : 0u;\n"
     << "    const u32 tid = g - inst * " << S.n << "u;\n"
@@ -241,11 +402,7 @@ std::string jit_source(const rc_program* P, const JitShape& S) {
     << "    " << (S.fuel ? "u64" : "u32") << " steps = 0;\n"
     << "    u32 nl = 0, ns = 0, nrec = 0, ro = 0, n_own = 0;\n";
   for (int j = 0; j < K; j++) o << "    u32 oc" << j << " = 0; i32 ov" << j << " = 0;\n";
-  for (uint32_t r = 0; r < P->n_regs; r++) o << "    i32 r" << r << " = 0;\n";
-  o << "    if (valid) {\n";
-  for (uint8_t r : P->live_regs) o << "      r" << (int)r << " = p.regs_in[(u64)" << (int)r << " * p.reg_stride + g];\n";
-  o << "    }\n"
-    << "    if (running) {\n"
+  o    << "    if (running) {\n"
     << "      st = " << (int)L_RUNNING << ";\n";
   if (S.ro_skip && !D)
     o << "      const bool rodiv = !(p.check_div && p.inst_div[inst]);  // the instance did not diverge\n";
@@ -255,6 +412,9 @@ std::string jit_source(const rc_program* P, const JitShape& S) {
     const uint32_t ro = P->entry_ro.empty() ? 0u : P->entry_ro[e];
     o << "        case " << e << "u: ";
     if (S.ro_skip && !D) o << "ro = rodiv ? " << ro << "u : 0u; ";
+    for (uint32_t r = 0; r < P->n_regs; r++)  // rematerialised registers
+      if (LIVE[e][r] && AFF[e][r].k == 1)
+        o << "r" << r << " = (i32)(" << AFF[e][r].a << "u * tid + " << AFF[e][r].b << "u); ";
     o << "goto L" << e << ";\n";
   }
   o << "        default: s_bail = true; goto Lend;  // not an interval entry (never: K1 would not get here either)\n"
@@ -346,6 +506,11 @@ std::string jit_source(const rc_program* P, const JitShape& S) {
         break;
       }
       case RC_OP_BAR:
+        // the registers the work-item resumes with at pc + 1 (the carried ones)
+        if (pc + 1 < N)
+          for (uint32_t r = 0; r < P->n_regs; r++)
+            if (LIVE[pc + 1][r] && AFF[pc + 1][r].k != 1)
+              o << "        p.regs_out[(u64)" << r << " * p.reg_stride + g] = r" << r << ";\n";
         o << "        pc = " << pc + 1 << "u; st = " << (int)L_WAITING << "; goto Lend;\n";
         break;
       case RC_OP_EXIT:
@@ -373,11 +538,35 @@ std::string jit_source(const rc_program* P, const JitShape& S) {
   o << "    if (valid) {\n"
     << "      p.status_out[g] = st;\n"
     << "      p.pc_out[g] = pc;\n";
-  for (uint8_t r : P->live_regs) o << "      p.regs_out[(u64)" << (int)r << " * p.reg_stride + g] = r" << (int)r << ";\n";
   o << "    }\n";
   // the interval's writes: write records (final value, reading L3, to wval;
   // the write-set map) — or, in direct mode, the commit itself
+  if (S.wbucket) o << "    __syncwarp();\n";
   for (int j = 0; j < K; j++) {
+    if (S.wbucket && !D) {
+      // straight into the bucket regions: lanes of one bucket
+      // take their slots with one atomic on the bucket's cursor
+      o << "    { const bool has = n_own > " << j << "u; const u32 act = __ballot_sync(FULL, has);\n"
+        << "      if (has) {\n"
+        << "        const u32 b = oc" << j << " >> 12;\n"
+        << "        const u32 m = __match_any_sync(act, b);\n"
+        << "        const u32 leader = __ffs(m) - 1;\n"
+        << "        u32 pos = 0;\n"
+        << "        if (lane == leader) pos = atomicAdd(p.bcur + b, (u32)__popc(m));\n";
+      if (j < DEF) {
+        o << "        d_rec" << j << " = ((u64)oc" << j << " << 32) | (g << 5) | " << (j << 1 | 1) << "u; d_raw" << j
+          << " = pos; d_m" << j << " = m; d_b" << j << " = b;\n";
+      } else {
+        o << "        pos = __shfl_sync(m, pos, leader) + __popc(m & ((1u << lane) - 1u));\n"
+          << "        if (pos < p.region) p.bucket_out[(u64)b * p.region + pos] = ((u64)oc" << j << " << 32) | (g << 5) | "
+          << (j << 1 | 1) << "u; else s_bover = true;\n";
+      }
+      o
+        << "        p.wval[(u64)" << j << " * p.n_lanes + g] = ov" << j << ";\n"
+        << "        if (!(ro >> 31)) p.wmap[oc" << j << "] = (u8)p.wtag;\n"
+        << "      } }\n";
+      continue;
+    }
     o << "    if (n_own > " << j << "u) {\n";
     if (D) {
       o << "      p.heap_w[oc" << j << "] = ov" << j << ";\n";
@@ -415,9 +604,10 @@ std::string jit_source(const rc_program* P, const JitShape& S) {
     << "    }\n"
     << "    s_instr += steps; s_loads += nl; s_stores += ns;\n"
     << "    s_wait |= st == " << (int)L_WAITING << ";\n"
-    << "  }\n"
-    << "  s_instr = wsum(s_instr); s_loads = wsum(s_loads); s_stores = wsum(s_stores); s_recs = wsum(s_recs);\n"
-    << "  const bool any_bail = __any_sync(FULL, s_bail), any_wait = __any_sync(FULL, s_wait);\n"
+    << "  }\n";
+  for (int j = 0; j < DEF; j++) flush(j);
+  o << "  s_instr = wsum(s_instr); s_loads = wsum(s_loads); s_stores = wsum(s_stores); s_recs = wsum(s_recs);\n"
+    << "  const bool any_bail = __any_sync(FULL, s_bail), any_wait = __any_sync(FULL, s_wait), any_bover = __any_sync(FULL, s_bover);\n"
     << "  if (lane == 0) {\n"
     << "    if (s_instr) atomicAdd(p.iv_instr, s_instr);\n"
     << "    if (s_loads) atomicAdd(p.iv_loads, s_loads);\n"
@@ -425,6 +615,29 @@ std::string jit_source(const rc_program* P, const JitShape& S) {
     << "    if (s_recs) atomicAdd(p.staged_recs, s_recs);\n"
     << "    if (any_bail) { *p.jit_bail = 1; *p.log_overflow = 1; }\n"
     << "    if (any_wait) *p.any_waiting = 1;\n"
+    << "    if (any_bover) *p.bucket_overflow = 1;  // the host re-runs the interval with K1\n"
+    << "  }\n"
+    << "}\n";
+  // rc_k1c_fix: before K1 (the interpreter, which reads every live register
+  // row) runs on lane state K1c produced, write the rematerialised registers
+  // of every work-item waiting at an interval entry into the rows
+  o << "extern \"C\" __global__ void __launch_bounds__(256) rc_k1c_fix(const __grid_constant__ K1cParams p) {\n"
+    << "  for (u32 g = blockIdx.x * blockDim.x + threadIdx.x; g < p.n_lanes; g += gridDim.x * blockDim.x) {\n"
+    << "    const u8 st = p.status_in[g];\n"
+    << "    if (st != " << (int)L_RUNNING << " && st != " << (int)L_WAITING << ") continue;\n"
+    << "    const u32 inst = g / " << S.n << "u, tid = g - inst * " << S.n << "u;\n"
+    << "    switch (p.pc_in[g]) {\n";
+  for (uint32_t e = 0; e < N; e++) {
+    if (!F.entry[e]) continue;
+    o << "      case " << e << "u:";
+    for (uint32_t r = 0; r < P->n_regs; r++)
+      if (LIVE[e][r] && AFF[e][r].k == 1)
+        o << " p.regs_out[(u64)" << r << " * p.reg_stride + g] = (i32)(" << AFF[e][r].a << "u * tid + " << AFF[e][r].b
+          << "u);";
+    o << " break;\n";
+  }
+  o << "      default: break;\n"
+    << "    }\n"
     << "  }\n"
     << "}\n";
   return o.str();
@@ -438,7 +651,8 @@ bool jit_get(rc_program* P, const JitShape& S, JitKernel* out, std::string* why)
   if (P->may_spill) return no("the own-write overlay may spill");
   if (P->n_instr > JIT_MAX_INSTR) return no("program too large");
   if (!S.direct) {
-    const int planes = S.ro_skip ? P->rec_bound_ro : P->rec_bound;
+    const int planes = S.wbucket ? (S.ro_skip ? P->read_bound_ro : P->read_bound)
+                                 : (S.ro_skip ? P->rec_bound_ro : P->rec_bound);
     if (planes < 0 || planes > JIT_MAX_PLANES) return no("no small static bound on records per interval");
   }
   int dev = 0;
@@ -489,8 +703,9 @@ bool jit_get(rc_program* P, const JitShape& S, JitKernel* out, std::string* why)
   std::vector<char> cubin(nb);
   A.get_cubin(prog, cubin.data());
   A.destroy(&prog);
-  CUfunction fn = nullptr;
-  if (A.load(&E.mod, cubin.data()) != CUDA_SUCCESS || A.get_fn(&fn, E.mod, "rc_k1c") != CUDA_SUCCESS) {
+  CUfunction fn = nullptr, fix = nullptr;
+  if (A.load(&E.mod, cubin.data()) != CUDA_SUCCESS || A.get_fn(&fn, E.mod, "rc_k1c") != CUDA_SUCCESS ||
+      A.get_fn(&fix, E.mod, "rc_k1c_fix") != CUDA_SUCCESS) {
     E.why = "cuModuleLoadData / cuModuleGetFunction failed";
     return no(E.why);
   }
@@ -498,6 +713,7 @@ bool jit_get(rc_program* P, const JitShape& S, JitKernel* out, std::string* why)
   A.occupancy(&per_sm, fn, JIT_THREADS, 0);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   E.k.fn = fn;
+  E.k.fix = fix;
   E.k.grid = std::max(1, per_sm) * nsm;
   E.ok = true;
   *out = E.k;
@@ -510,6 +726,16 @@ cudaError_t jit_launch(const JitKernel& k, const K1cParams& p, cudaStream_t s) {
   K1cParams q = p;
   void* args[] = {&q};
   const CUresult r = api().launch(static_cast<CUfunction>(k.fn), grid, 1, 1, JIT_THREADS, 1, 1, 0,
+                                  reinterpret_cast<CUstream>(s), args, nullptr);
+  launched();
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
+}
+
+cudaError_t jit_fix(const JitKernel& k, const K1cParams& p, cudaStream_t s) {
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((p.n_lanes + 255) / 256, (uint32_t)k.grid));
+  K1cParams q = p;
+  void* args[] = {&q};
+  const CUresult r = api().launch(static_cast<CUfunction>(k.fix), grid, 1, 1, 256, 1, 1, 0,
                                   reinterpret_cast<CUstream>(s), args, nullptr);
   launched();
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
@@ -550,6 +776,7 @@ RC_API size_t rc_debug_jit_source(const rc_program* P, uint32_t n, const uint32_
   S.direct = (flags & 1u) != 0;
   S.fuel = (flags & 2u) != 0;
   S.ro_skip = (flags & 4u) != 0;
+  S.wbucket = (flags & 8u) != 0;
   const std::string src = rc::jit_source(P, S);
   if (buf && cap) {
     const size_t k = std::min(cap - 1, src.size());

@@ -383,22 +383,27 @@ void analyze(rc_program* P) {
   //     array e's region stores to.  Sizes K1c's record planes (jit.cpp); a
   //     lane of a divergent instance (which logs every read) that exceeds it
   //     makes K1c hand the interval back to the interpreter.
-  P->rec_bound_ro = P->rec_bound;
-  if (P->rec_bound >= 0) {
+  //     The same for the read records alone (K1c writes its write records
+  //     straight into the bucket regions): read_bound_ro, and read_bound
+  //     when every read is logged.
+  auto bound = [&](bool with_st, bool elide) -> int {
     int64_t b = 0;
     std::vector<int> w(N, 0);
     for (uint32_t e = 0; e < N && b >= 0; e++) {
       if (!(e == 0 || P->code[e - 1].op == RC_OP_BAR)) continue;
-      const uint32_t ro = P->entry_ro[e] & 0x7FFFFFFFu;
+      const uint32_t ro = elide ? P->entry_ro[e] & 0x7FFFFFFFu : 0u;
       for (uint32_t pc = 0; pc < N; pc++) {
         const Ins& I = P->code[pc];
-        w[pc] = I.op == RC_OP_ST || (I.op == RC_OP_LD && (I.b >= 31 || !((ro >> I.b) & 1u)));
+        w[pc] = (with_st && I.op == RC_OP_ST) || (I.op == RC_OP_LD && (I.b >= 31 || !((ro >> I.b) & 1u)));
       }
       const int64_t x = max_path_weight(P, w, e);
       b = x < 0 ? -1 : std::max(b, x);
     }
-    P->rec_bound_ro = (b < 0 || b > 1024) ? -1 : (int)b;
-  }
+    return (b < 0 || b > 1024) ? -1 : (int)b;
+  };
+  P->rec_bound_ro = P->rec_bound >= 0 ? bound(true, true) : -1;
+  P->read_bound = P->rec_bound >= 0 ? bound(false, false) : -1;
+  P->read_bound_ro = P->rec_bound >= 0 ? bound(false, true) : -1;
 }
 
 }  // namespace rc

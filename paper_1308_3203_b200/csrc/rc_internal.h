@@ -221,6 +221,7 @@ struct InterpParams {
     unsigned long long* iv_loads; unsigned long long* iv_stores; unsigned long long* iv_instr;            \
     unsigned int* log_overflow; unsigned int* any_waiting; unsigned int* jit_bail; const unsigned int* abort; \
     unsigned long long report_cap; unsigned long long fuel; unsigned long long stage_cap;                 \
+    unsigned long long* bucket_out; unsigned int* bcur; unsigned int* bucket_overflow; unsigned int region; \
     unsigned int n_lanes, lane_pad, reg_stride, interval, inst_base, planes, wtag, check_div;              \
   };
 RC_K1C_PARAMS_DECL
@@ -234,9 +235,11 @@ struct JitShape {
   bool direct = false;   // RC_OPT_PREPASS direct-commit mode (no log)
   bool fuel = false;     // per-instruction fuel check
   bool ro_skip = false;  // static write-set elision (off with RC_OPT_KEEP_ALL_READS / work-groups)
+  bool wbucket = false;  // bucket region mode: write records go straight into their bucket regions
 };
 struct JitKernel {
   void* fn = nullptr;   // CUfunction
+  void* fix = nullptr;  // CUfunction rc_k1c_fix (registers K1c rematerialises, written out for K1)
   int grid = 0;         // persistent grid (resident blocks per SM x SMs)
 };
 // The program's K1c kernel for this shape on the current device: compiled and
@@ -245,6 +248,11 @@ struct JitKernel {
 // caller then runs the interpreter.
 bool jit_get(rc_program* P, const JitShape& S, JitKernel* out, std::string* why);
 cudaError_t jit_launch(const JitKernel& k, const K1cParams& p, cudaStream_t s);
+// K1c carries only the registers that are not an affine function of the
+// local id at the entry; before K1 runs on K1c-produced lane state (a K1c
+// interval handed back, the RW-classification re-run) this writes the others
+// into the rows p.regs_out of the lanes p.status_in / p.pc_in describe
+cudaError_t jit_fix(const JitKernel& k, const K1cParams& p, cudaStream_t s);
 void jit_release(rc_program* P);  // unload the cached modules (on their devices)
 // the K1c source for a program and shape (tests / RC_JIT_DUMP)
 std::string jit_source(const rc_program* P, const JitShape& S);
@@ -477,6 +485,7 @@ struct rc_program {
   bool may_spill = true;           // a work-item may write more than OVL_CAP distinct cells in one interval
   int rec_bound = -1;              // max log records per work-item per interval (-1 unbounded)
   int rec_bound_ro = -1;           // the same with the static write-set elision (5) applied (K1c record planes)
+  int read_bound = -1, read_bound_ro = -1;  // read records alone (K1c with its writes straight into the buckets)
   int64_t instr_bound = -1;        // max instructions per work-item per interval (-1 unbounded)
   std::mutex mu;
   rc_workspace* ws = nullptr;

@@ -488,7 +488,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   // jit_get declines; a K1c interval that bails (jit_bail) is re-run by K1 and
   // K1 keeps the rest of the run.
   JitKernel jk;
-  bool jit_on = false;
+  bool jit_on = false, jit_wbucket = false;
   int jit_planes = 0;
   {
     const char* je = getenv("RC_JIT");
@@ -504,10 +504,16 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       S.direct = direct;
       S.fuel = P->instr_bound < 0 || (uint64_t)P->instr_bound > opt.fuel_per_interval;
       S.ro_skip = (opt.flags & RC_OPT_KEEP_ALL_READS) == 0;
+      // bucket region mode: K1c places its write records in the bucket
+      // regions itself; the planes (and the scatter) carry only reads
+      S.wbucket = region && !direct && getenv("RC_JIT_NO_WBUCKET") == nullptr;
       std::string why;
       jit_on = jit_get(P, S, &jk, &why);
       if (!jit_on && getenv("RC_JIT_VERBOSE")) fprintf(stderr, "rc: K1c not used: %s\n", why.c_str());
-      jit_planes = direct ? 0 : (S.ro_skip ? P->rec_bound_ro : P->rec_bound);
+      jit_wbucket = S.wbucket;
+      jit_planes = direct ? 0
+                   : S.wbucket ? (S.ro_skip ? P->read_bound_ro : P->read_bound)
+                               : (S.ro_skip ? P->rec_bound_ro : P->rec_bound);
       if (jit_on && jit_planes > 0) {  // fixed record slots: planes x (lanes rounded up to LANE_PAD)
         const uint64_t want = (uint64_t)jit_planes * ((L_max + LANE_PAD - 1) / LANE_PAD * LANE_PAD);
         if (log_cap < want) {
@@ -520,6 +526,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     }
   }
   bool jit_off = false;  // a K1c interval bailed: K1 for the rest of the run
+  bool jit_fix_pending = false;  // lane state K1c produced has rematerialised registers missing from the rows
+  bool jit_used_wb[2] = {false, false};  // interval k & 1 ran K1c with its writes in the buckets
 
   uint64_t tot_loads = 0, tot_stores = 0, tot_instr = 0, intervals_max = 0;
   uint64_t rep_count = 0;  // host mirror of ctr.report_count
@@ -751,6 +759,51 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       ip.ro_skip = (opt.flags & RC_OPT_KEEP_ALL_READS) == 0 && G == 1;
       return ip;
     };
+    // K1c's parameter block for the interval interpreter's parameters
+    auto make_kp = [&](const InterpParams& ip, uint32_t kk) {
+      K1cParams kp;
+      kp.status_in = ip.status_in;
+      kp.pc_in = ip.pc_in;
+      kp.regs_in = ip.regs_in;
+      kp.status_out = ip.status_out;
+      kp.pc_out = ip.pc_out;
+      kp.regs_out = ip.regs_out;
+      kp.heap = ip.heap;
+      kp.heap_w = ip.heap_w;
+      kp.stage = reinterpret_cast<unsigned long long*>(ip.stage);
+      kp.wval = ip.wval;
+      kp.wmap = ip.wmap;
+      kp.node_min = ip.node_min;
+      kp.node_max = ip.node_max;
+      kp.inst_div = ip.inst_div;
+      kp.reports = ip.reports;
+      kp.report_count = &dctr->report_count;
+      kp.stage_count = &dctr->stage_count;
+      kp.staged_recs = &dctr->staged_recs;
+      kp.iv_loads = &dctr->iv_loads;
+      kp.iv_stores = &dctr->iv_stores;
+      kp.iv_instr = &dctr->iv_instr;
+      kp.log_overflow = &dctr->log_overflow;
+      kp.any_waiting = &dctr->any_waiting;
+      kp.jit_bail = &dctr->jit_bail;
+      kp.abort = &dctr->abort;
+      kp.report_cap = ip.report_cap;
+      kp.fuel = ip.fuel;
+      kp.stage_cap = ip.stage_cap;
+      kp.n_lanes = L;
+      kp.lane_pad = reg_stride;
+      kp.reg_stride = reg_stride;
+      kp.interval = kk;
+      kp.inst_base = inst_base;
+      kp.planes = (uint32_t)jit_planes;
+      kp.wtag = W.wtag;
+      kp.check_div = ip.ro_skip && kk > 0;
+      kp.bucket_out = reinterpret_cast<unsigned long long*>(W.log.as<uint64_t>());
+      kp.bcur = W.sort.hist;
+      kp.bucket_overflow = &dctr->bucket_overflow;
+      kp.region = BUCKET_REGION;
+      return kp;
+    };
     auto enqueue_interval = [&](uint32_t kk, int cc, Marks* mk) -> cudaError_t {
       cudaError_t e;
 #define EQ(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
@@ -773,47 +826,20 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       W.prof.cut();
       W.prof.begin(s);
       if (jit_on && !jit_off) {
-        K1cParams kp;
-        kp.status_in = ip.status_in;
-        kp.pc_in = ip.pc_in;
-        kp.regs_in = ip.regs_in;
-        kp.status_out = ip.status_out;
-        kp.pc_out = ip.pc_out;
-        kp.regs_out = ip.regs_out;
-        kp.heap = ip.heap;
-        kp.heap_w = ip.heap_w;
-        kp.stage = reinterpret_cast<unsigned long long*>(ip.stage);
-        kp.wval = ip.wval;
-        kp.wmap = ip.wmap;
-        kp.node_min = ip.node_min;
-        kp.node_max = ip.node_max;
-        kp.inst_div = ip.inst_div;
-        kp.reports = ip.reports;
-        kp.report_count = &dctr->report_count;
-        kp.stage_count = &dctr->stage_count;
-        kp.staged_recs = &dctr->staged_recs;
-        kp.iv_loads = &dctr->iv_loads;
-        kp.iv_stores = &dctr->iv_stores;
-        kp.iv_instr = &dctr->iv_instr;
-        kp.log_overflow = &dctr->log_overflow;
-        kp.any_waiting = &dctr->any_waiting;
-        kp.jit_bail = &dctr->jit_bail;
-        kp.abort = &dctr->abort;
-        kp.report_cap = ip.report_cap;
-        kp.fuel = ip.fuel;
-        kp.stage_cap = ip.stage_cap;
-        kp.n_lanes = L;
-        kp.lane_pad = reg_stride;
-        kp.reg_stride = reg_stride;
-        kp.interval = kk;
-        kp.inst_base = inst_base;
-        kp.planes = (uint32_t)jit_planes;
-        kp.wtag = W.wtag;
-        kp.check_div = ip.ro_skip && kk > 0;
+        const K1cParams kp = make_kp(ip, kk);
+        jit_fix_pending = true;
         EQ(jit_launch(jk, kp, s));
       } else {
+        if (jit_fix_pending) {  // K1 reads every live register row: write K1c's rematerialised ones
+          K1cParams kp = make_kp(ip, kk);
+          kp.regs_out = const_cast<int32_t*>(ip.regs_in);
+          EQ(jit_fix(jk, kp, s));
+          jit_fix_pending = false;
+        }
         EQ(launch_interp(ip, s));
       }
+      const bool wb = jit_on && !jit_off && jit_wbucket;
+      jit_used_wb[kk & 1] = wb;
       W.prof.end(RC_PROF_INTERP, s, 0, L);
       // inter-group races: this group's smallest reader / writer per cell
       // (from the staging buffer, before the sort reuses it)
@@ -822,7 +848,15 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
                                 (uint32_t)cpi, gi * n, s));
       // ---- write-set filter: writes + reads of written cells, dense, with histograms
       // ---- write-set filter + K3: group the kept records by cell
-      if (!direct) EQ(enqueue_sort(W.prof.on ? &W.prof : nullptr, (opt.flags & RC_OPT_KEEP_ALL_READS) != 0, region));
+      // (K1c with its writes in the buckets and no read record possible: nothing to scatter)
+      if (!direct && !(wb && jit_planes == 0))
+        EQ(enqueue_sort(W.prof.on ? &W.prof : nullptr, (opt.flags & RC_OPT_KEEP_ALL_READS) != 0, region));
+      else if (wb) {
+        sr = W.log.as<uint64_t>();  // the bucket regions K1c filled
+        // the scatter's snapshot of the report count after K1 (a detect-only
+        // re-run rolls back to it)
+        EQ(cudaMemcpyAsync(&dctr->k1_reports, &dctr->report_count, 8, cudaMemcpyDeviceToDevice, s));
+      }
       // ---- K4+K5 detect + commit, A4 check + verdict
       DetectParams dp = detect_params(kk);
       dp.with_boundary = true;  // A4 as detect's tail: consumes (and resets) K1's per-instance node ranges
@@ -867,6 +901,11 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         }
         EQ(cudaMemsetAsync(W.ctr_block.p, 0, CTR_OFF + offsetof(DevCounters, report_count), s));
         InterpParams ip = make_ip(kk, cur);
+        if (jit_on) {  // the interval's input lane state may be K1c's (rematerialised registers)
+          K1cParams kp = make_kp(ip, kk);
+          kp.regs_out = const_cast<int32_t*>(ip.regs_in);
+          EQ(jit_fix(jk, kp, s));
+        }
         ip.heap = W.heap_snap[kk & 1].as<int32_t>();  // interval-start heap
         ip.alt_heap = heap_cur;                       // committed heap (writers first)
         ip.alt_mask = W.amap.as<uint8_t>();
@@ -940,8 +979,16 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       const bool log_over = h.log_overflow != 0;  // a real record did not fit
       const bool k1_rep_over = h.k1_reports > rep_cap;
       const bool spill_over = h.ovl_overflow != 0;  // a work-item's spill list was full
-      if (log_over || k1_rep_over || spill_over) {  // filter/detect skipped: grow and re-run the interval
-        if (h.jit_bail) jit_off = true;  // a K1c work-item had more records than its planes: K1 re-runs it
+      // a bucket outgrew its region while K1c wrote records straight into the
+      // regions: the staging buffer does not hold them, so the interval is
+      // re-run with K1 in count mode (K1 for the rest of the run)
+      const bool jit_bucket_over = h.bucket_overflow && jit_used_wb[k & 1];
+      if (log_over || k1_rep_over || spill_over || jit_bucket_over) {  // filter/detect skipped: grow and re-run
+        if (h.jit_bail || jit_bucket_over) jit_off = true;  // a K1c work-item had more records than its planes
+        if (jit_bucket_over) {
+          W.region_ok = false;
+          region = false;
+        }
         if (spill_over) {
           const int e = grow_spill();
           if (e != RC_OK) return e;

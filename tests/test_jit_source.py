@@ -1,6 +1,7 @@
 """K1c source (jit.cpp) without a GPU: the CUDA C++ the library generates
 for a program and run shape compiles with NVRTC for sm_100a in every mode
-(normal, fuel-checked, direct commit, every read logged), for the workload
+(write records into the bucket regions or into the record planes,
+fuel-checked, direct commit, every read logged), for the workload
 kernels, the opcode corpus and random kernels.  Semantics are checked on the
 GPU (tests/test_gpu_parity.py runs every parity test under K1 and K1c)."""
 import ctypes
@@ -63,8 +64,8 @@ def programs():
 def test_k1c_source_compiles(rc, name, p, n, sizes):
     prog = rc.rc_load_program(p.bytecode)
     sizes = sizes or [n + 16] * prog.n_arrays
-    modes = [dict(), dict(fuel=True), dict(direct=True), dict(ro_skip=False)]
-    for m in modes[: 4 if name in ("stencil", "tree", "tiny0") else 1]:
+    modes = [dict(wbucket=True), dict(), dict(fuel=True), dict(direct=True), dict(ro_skip=False, wbucket=True)]
+    for m in modes[: 5 if name in ("stencil", "tree", "tiny0") else 2]:
         src = prog.jit_source(n, sizes, **m)
         assert 'extern "C" __global__' in src and "rc_k1c" in src
         r, log, nb = nvrtc_compile(src)
