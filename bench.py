@@ -538,6 +538,28 @@ def main():
                     "peak_source": "B200: 4 SMSPs per SM, one warp instruction issued per SMSP per cycle",
                     "traffic": ti.get("dram_bytes_per_launch"),
                     "traffic_note": "DRAM bytes of one captured launch (heap loads, lane state, staged records)"}
+        if prof_sum.get("k1c"):
+            # K1c, the interval kernel compiled for the program (the dominant
+            # kernel): no fetch / decode left, bound by the bytes it moves —
+            # status + pc in and out, the carried registers, 4 B per heap load,
+            # the log; achieved = those algorithmic bytes of the
+            # sampled launches / their CUDA-event time
+            tk = tr.get("rc_k1c", {})
+            kach = di["alg_bytes"] / (di["ms"] / 1e3) / 1e9 if di["ms"] > 0 and di["alg_bytes"] else None
+            kipc = None
+            if di["ms"] > 0 and di["launches"] and tk.get("warp_instructions_per_launch") and clk_mhz:
+                kipc = tk["warp_instructions_per_launch"] / (di["ms"] / di["launches"] / 1e3 * clk_mhz * 1e6 * n_sms)
+            roofline = {"kernel": "rc_k1c (K1c: the interval kernel compiled for the program with NVRTC; the "
+                                  "dominant kernel)",
+                        "bound": "hbm", "achieved": kach, "peak": peak, "unit": "GB/s",
+                        "frac": kach / peak if kach else None, "peak_source": peak_src,
+                        "traffic": tk.get("dram_bytes_per_launch"),
+                        "alg_bytes_per_launch": di["alg_bytes"] / max(1, di["launches"]),
+                        "alg_bytes": "10 per lane (status, pc in/out) + 8 per carried register and lane + 4 per heap "
+                                     "load + 8 per logged read + 12 per write record (record, final value)",
+                        "launches_sampled": di["launches"],
+                        "issue": {"achieved": kipc, "peak": 4.0, "unit": "warp-instr/cycle/SM",
+                                  "frac": kipc / 4.0 if kipc else None, "ncu_ipc_per_sm": tk.get("ipc_per_sm")}}
         kernels = {"sample_every": every}
         for c in ("interp", "filter", "hist", "sort", "detect", "boundary", "finalize", "copy"):
             d = prof_sum[c]

@@ -188,7 +188,10 @@ typedef struct {
    * averages are unbiased; totals scale by k).  Event bookkeeping for every
    * interval would cost the host more than the GPU work of small intervals. */
   uint32_t sample_every;
-  uint32_t reserved;
+  uint32_t flags;            /* out: bit 0 = intervals ran K1c, the interval
+                                kernel compiled for the program;
+                                its alg_bytes[RC_PROF_INTERP] are then the lane
+                                state, heap loads and log it must move       */
 } rc_profile;
 
 /* One shared array of the kernel (an element of Args).

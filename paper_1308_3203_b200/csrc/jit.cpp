@@ -33,6 +33,7 @@
 // (may_spill), record bounds above 32 planes, the RW-classification re-run.
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -298,7 +299,7 @@ std::vector<std::vector<Aff>> affine_in(const rc_program* P, const JitShape& S) 
 
 }  // namespace
 
-std::string jit_source(const rc_program* P, const JitShape& S) {
+std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
   const uint32_t N = P->n_instr;
   const Facts F = facts(P);
   const auto LIVE = live_in(P);
@@ -311,6 +312,7 @@ std::string jit_source(const rc_program* P, const JitShape& S) {
     if (F.entry[e])
       for (uint32_t r = 0; r < P->n_regs; r++)
         if (LIVE[e][r] && AFF[e][r].k != 1) carried[r] = 1;
+  if (n_carried) *n_carried = (int)std::count(carried.begin(), carried.end(), (uint8_t)1);
   const int K = std::max(1, P->ovl_cap);
   const bool D = S.direct;
   std::ostringstream o;
@@ -336,7 +338,7 @@ std::string jit_source(const rc_program* P, const JitShape& S) {
     << ") rc_k1c(const __grid_constant__ K1cParams p) {\n"
     << "  if (*p.abort) return;  // speculative interval (DevCounters::abort)\n"
     << "  const u32 lane = threadIdx.x & 31u;\n"
-    << "  u64 s_instr = 0, s_loads = 0, s_stores = 0, s_recs = 0;\n"
+    << "  u64 s_instr = 0, s_loads = 0, s_stores = 0, s_recs = 0, s_wrec = 0;\n"
     << "  bool s_wait = false, s_bail = false, s_bover = false;\n"
     << "  u32 a4_inst = 0xFFFFFFFFu; i32 a4_lo = 0, a4_hi = 0;\n";
   if (!D)
@@ -367,22 +369,7 @@ std::string jit_source(const rc_program* P, const JitShape& S) {
   // are in flight: 57.1 vs 70.7 ms/step)
   const bool pf = getenv("RC_JIT_NOPF") == nullptr;
   if (pf) prefetch("base + lane", "base < p.lane_pad");
-  // bucket writes with a deferred slot: the cursor atomic of a lane's write
-  // record is issued at the end of its iteration and its result consumed at
-  // the top of the warp's next one, so the L2 round trip overlaps the next
-  // lane's loads (up to two overlay slots; RC_JIT_NODEFER=1: A/B knob)
-  const int DEF = (S.wbucket && !D && getenv("RC_JIT_NODEFER") == nullptr) ? std::min(K, 2) : 0;
-  for (int j = 0; j < DEF; j++)
-    o << "  u64 d_rec" << j << " = 0; u32 d_raw" << j << " = 0, d_m" << j << " = 0, d_b" << j << " = 0;\n";
-  auto flush = [&](int j) {
-    o << "    if (d_m" << j << ") {  // the previous lane's write record, slot " << j << "\n"
-      << "      const u32 pos = __shfl_sync(d_m" << j << ", d_raw" << j << ", __ffs(d_m" << j << ") - 1) + __popc(d_m" << j
-      << " & ((1u << lane) - 1u));\n"
-      << "      if (pos < p.region) p.bucket_out[(u64)d_b" << j << " * p.region + pos] = d_rec" << j
-      << "; else s_bover = true;\n"
-      << "      d_m" << j << " = 0;\n"
-      << "    }\n";
-  };
+
   o << "  for (; base < p.lane_pad; base += stride) {\n"
     << "    const u32 g = base + lane;\n"
     << "    const bool valid = g < p.n_lanes;\n";
@@ -393,7 +380,6 @@ std::string jit_source(const rc_program* P, const JitShape& S) {
     o << "    i32 r" << r << " = " << (carried[r] ? "n_r" + std::to_string(r) : std::string("0")) << ";\n";
   }
   if (pf) prefetch("g + stride", "base + stride < p.lane_pad");
-  for (int j = 0; j < DEF; j++) flush(j);
   o << "    if (st == " << (int)L_EXITED_NOW << ") st = " << (int)L_EXITED << ";\n"
     << "    const bool running = valid && (st == " << (int)L_RUNNING << " || st == " << (int)L_WAITING << ");\n"
     << "    const u32 inst = valid ? g / " << S.n << "u : 0u;\n"
@@ -552,18 +538,13 @@ std::string jit_source(const rc_program* P, const JitShape& S) {
         << "        const u32 m = __match_any_sync(act, b);\n"
         << "        const u32 leader = __ffs(m) - 1;\n"
         << "        u32 pos = 0;\n"
-        << "        if (lane == leader) pos = atomicAdd(p.bcur + b, (u32)__popc(m));\n";
-      if (j < DEF) {
-        o << "        d_rec" << j << " = ((u64)oc" << j << " << 32) | (g << 5) | " << (j << 1 | 1) << "u; d_raw" << j
-          << " = pos; d_m" << j << " = m; d_b" << j << " = b;\n";
-      } else {
-        o << "        pos = __shfl_sync(m, pos, leader) + __popc(m & ((1u << lane) - 1u));\n"
-          << "        if (pos < p.region) p.bucket_out[(u64)b * p.region + pos] = ((u64)oc" << j << " << 32) | (g << 5) | "
-          << (j << 1 | 1) << "u; else s_bover = true;\n";
-      }
-      o
+        << "        if (lane == leader) pos = atomicAdd(p.bcur + b, (u32)__popc(m));\n"
+        << "        pos = __shfl_sync(m, pos, leader) + __popc(m & ((1u << lane) - 1u));\n"
+        << "        if (pos < p.region) p.bucket_out[(u64)b * p.region + pos] = ((u64)oc" << j << " << 32) | (g << 5) | "
+        << (j << 1 | 1) << "u; else s_bover = true;\n"
         << "        p.wval[(u64)" << j << " * p.n_lanes + g] = ov" << j << ";\n"
         << "        if (!(ro >> 31)) p.wmap[oc" << j << "] = (u8)p.wtag;\n"
+        << "        s_wrec++;\n"
         << "      } }\n";
       continue;
     }
@@ -605,14 +586,15 @@ std::string jit_source(const rc_program* P, const JitShape& S) {
     << "    s_instr += steps; s_loads += nl; s_stores += ns;\n"
     << "    s_wait |= st == " << (int)L_WAITING << ";\n"
     << "  }\n";
-  for (int j = 0; j < DEF; j++) flush(j);
   o << "  s_instr = wsum(s_instr); s_loads = wsum(s_loads); s_stores = wsum(s_stores); s_recs = wsum(s_recs);\n"
+    << "  s_wrec = wsum(s_wrec);\n"
     << "  const bool any_bail = __any_sync(FULL, s_bail), any_wait = __any_sync(FULL, s_wait), any_bover = __any_sync(FULL, s_bover);\n"
     << "  if (lane == 0) {\n"
     << "    if (s_instr) atomicAdd(p.iv_instr, s_instr);\n"
     << "    if (s_loads) atomicAdd(p.iv_loads, s_loads);\n"
     << "    if (s_stores) atomicAdd(p.iv_stores, s_stores);\n"
     << "    if (s_recs) atomicAdd(p.staged_recs, s_recs);\n"
+    << "    if (s_wrec) { atomicAdd(p.kept_count, s_wrec); atomicAdd(p.kept_writes, s_wrec); }  // (bucket writes)\n"
     << "    if (any_bail) { *p.jit_bail = 1; *p.log_overflow = 1; }\n"
     << "    if (any_wait) *p.any_waiting = 1;\n"
     << "    if (any_bover) *p.bucket_overflow = 1;  // the host re-runs the interval with K1\n"
@@ -675,7 +657,7 @@ bool jit_get(rc_program* P, const JitShape& S, JitKernel* out, std::string* why)
     E.why = A.why;
     return no(E.why);
   }
-  const std::string src = jit_source(P, S);
+  const std::string src = jit_source(P, S, &E.k.carried);
   if (const char* dump = getenv("RC_JIT_DUMP")) {
     if (FILE* f = fopen(dump, "w")) {
       fputs(src.c_str(), f);

@@ -222,6 +222,7 @@ struct InterpParams {
     unsigned int* log_overflow; unsigned int* any_waiting; unsigned int* jit_bail; const unsigned int* abort; \
     unsigned long long report_cap; unsigned long long fuel; unsigned long long stage_cap;                 \
     unsigned long long* bucket_out; unsigned int* bcur; unsigned int* bucket_overflow; unsigned int region; \
+    unsigned long long* kept_count; unsigned long long* kept_writes;                                      \
     unsigned int n_lanes, lane_pad, reg_stride, interval, inst_base, planes, wtag, check_div;              \
   };
 RC_K1C_PARAMS_DECL
@@ -241,6 +242,7 @@ struct JitKernel {
   void* fn = nullptr;   // CUfunction
   void* fix = nullptr;  // CUfunction rc_k1c_fix (registers K1c rematerialises, written out for K1)
   int grid = 0;         // persistent grid (resident blocks per SM x SMs)
+  int carried = 0;      // registers carried through HBM across barriers (the rest rematerialised)
 };
 // The program's K1c kernel for this shape on the current device: compiled and
 // loaded on first use, cached on the program.  false (with a reason in *why)
@@ -255,7 +257,7 @@ cudaError_t jit_launch(const JitKernel& k, const K1cParams& p, cudaStream_t s);
 cudaError_t jit_fix(const JitKernel& k, const K1cParams& p, cudaStream_t s);
 void jit_release(rc_program* P);  // unload the cached modules (on their devices)
 // the K1c source for a program and shape (tests / RC_JIT_DUMP)
-std::string jit_source(const rc_program* P, const JitShape& S);
+std::string jit_source(const rc_program* P, const JitShape& S, int* carried = nullptr);
 
 struct DetectParams {
   const uint64_t* recs;       // sorted by cell; count = ctr->kept_count

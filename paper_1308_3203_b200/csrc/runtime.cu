@@ -528,6 +528,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   bool jit_off = false;  // a K1c interval bailed: K1 for the rest of the run
   bool jit_fix_pending = false;  // lane state K1c produced has rematerialised registers missing from the rows
   bool jit_used_wb[2] = {false, false};  // interval k & 1 ran K1c with its writes in the buckets
+  bool jit_used_iv[2] = {false, false};  // interval k & 1 ran K1c
+  bool jit_ran = false;
 
   uint64_t tot_loads = 0, tot_stores = 0, tot_instr = 0, intervals_max = 0;
   uint64_t rep_count = 0;  // host mirror of ctr.report_count
@@ -802,6 +804,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       kp.bcur = W.sort.hist;
       kp.bucket_overflow = &dctr->bucket_overflow;
       kp.region = BUCKET_REGION;
+      kp.kept_count = &dctr->kept_count;
+      kp.kept_writes = &dctr->kept_writes;
       return kp;
     };
     auto enqueue_interval = [&](uint32_t kk, int cc, Marks* mk) -> cudaError_t {
@@ -840,6 +844,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       }
       const bool wb = jit_on && !jit_off && jit_wbucket;
       jit_used_wb[kk & 1] = wb;
+      jit_used_iv[kk & 1] = jit_on && !jit_off;
+      if (jit_on && !jit_off) jit_ran = true;
       W.prof.end(RC_PROF_INTERP, s, 0, L);
       // inter-group races: this group's smallest reader / writer per cell
       // (from the staging buffer, before the sort reuses it)
@@ -1077,6 +1083,13 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
           if (m.cls == RC_PROF_DETECT) { m.bytes = Ns * 8 + h.kept_writes * 8; m.items = Ns; }
           if (m.cls == RC_PROF_HIST && bucket) { m.bytes = Nslots * 8; m.items = Nslots; }  // bucket counts
           if (m.cls == RC_PROF_FILTER) { m.bytes = Nslots * 8 + h.staged_recs + Ns * 8; m.items = Nslots; }
+          // K1c: status + pc in and out, the carried
+          // registers in and out, 4 B per performed load, 8 B per logged
+          // read, 8 B record + 4 B final value per write record
+          if (m.cls == RC_PROF_INTERP && jit_used_iv[k & 1]) {
+            const uint64_t wrec = jit_wbucket ? h.kept_writes : h.iv_stores;
+            m.bytes = (uint64_t)L * (10 + 8 * (uint64_t)jk.carried) + 4 * h.iv_loads + 8 * h.staged_recs + 12 * wrec;
+          }
         }
       }
       cur ^= 1;  // the interval's lane state becomes current
@@ -1188,6 +1201,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     opt.profile->total_ms = ms;
     opt.profile->kernel_launches = g_launches.load() - launches0;
     opt.profile->sample_every = prof_every;
+    opt.profile->flags = jit_ran ? 1u : 0u;
     cudaEventDestroy(t_begin);
     cudaEventDestroy(t_end);
   }

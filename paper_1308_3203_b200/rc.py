@@ -45,7 +45,7 @@ class rc_stats(C.Structure):
 class rc_profile(C.Structure):
     _fields_ = [("launches", C.c_uint64 * 8), ("ms", C.c_double * 8), ("alg_bytes", C.c_uint64 * 8),
                 ("items", C.c_uint64 * 8), ("total_ms", C.c_double), ("kernel_launches", C.c_uint64),
-                ("sample_every", C.c_uint32), ("reserved", C.c_uint32)]
+                ("sample_every", C.c_uint32), ("flags", C.c_uint32)]
 
 
 class rc_array(C.Structure):
@@ -194,6 +194,7 @@ def _stats_dict(s: rc_stats) -> dict:
 
 def _profile_dict(p: rc_profile) -> dict:
     return {"total_ms": p.total_ms, "kernel_launches": int(p.kernel_launches), "sample_every": int(p.sample_every),
+            "k1c": bool(p.flags & 1),
             **{c: {"launches": int(p.launches[i]), "ms": float(p.ms[i]), "alg_bytes": int(p.alg_bytes[i]),
                    "items": int(p.items[i])} for i, c in enumerate(PROF_CLASSES)}}
 

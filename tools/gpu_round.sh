@@ -14,7 +14,8 @@ fi
 if [ "${NCU:-1}" != "0" ]; then
   Q="--steps 1 --warmup 0 --no-e2e --no-cpu-baseline ${BENCH_ARGS}"
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --csv --log-file gpurun_out/launches.csv python bench.py $Q > gpurun_out/ncu_launch_run.log 2>&1; echo "ncu_launches=$?"
-  for k in ${NCU_KERNELS:-bucket_scatter bucket_detect bucket_count interp}; do
-    timeout 600 ncu --set full --clock-control none --import-source on -k regex:${k}_kernel -s 7 -c 1 -o gpurun_out/prof_${k} -f python bench.py $Q > gpurun_out/ncu_${k}.log 2>&1; echo "ncu_${k}=$?"
+  for k in ${NCU_KERNELS:-k1c bucket_detect}; do
+    re="${k}_kernel"; [ "$k" == "k1c" ] && re="rc_k1c"
+    timeout 600 ncu --set full --clock-control none --import-source on -k regex:${re} -s 7 -c 1 -o gpurun_out/prof_${k} -f python bench.py $Q > gpurun_out/ncu_${k}.log 2>&1; echo "ncu_${k}=$?"
   done
 fi

@@ -110,7 +110,7 @@ def main():
         print(s)
         names = {"prof_onesweep": "onesweep_kernel", "prof_detect": "detect_kernel", "prof_interp": "interp_kernel",
                  "prof_bucket_scatter": "bucket_scatter_kernel", "prof_bucket_detect": "bucket_detect_kernel",
-                 "prof_filter": "filter_kernel"}
+                 "prof_filter": "filter_kernel", "prof_k1c": "rc_k1c"}
         if base in names:
             mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             byts = sum(float(d[k].replace(",", "")) * mult[d["_units"][k]]
