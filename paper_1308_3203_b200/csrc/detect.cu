@@ -561,8 +561,16 @@ __device__ __forceinline__ bool bucket_smem(const DetectParams& p, BucketSmem& S
   // counted (used for the lone writers' commits; detect_chunk re-reads the
   // others')
   int32_t val[ITEMS];
+  if (p.bval) {  // K1c wrote each value beside its record: no dependent gather
 #pragma unroll
-  for (int j = 0; j < ITEMS; j++) val[j] = (r[j] != REC_SENTINEL && rec_w(r[j])) ? rec_val<SPILL>(p, r[j]) : 0;
+    for (int j = 0; j < ITEMS; j++) {
+      const uint32_t i = t + j * BD_THREADS;
+      val[j] = i < m ? __ldg(p.bval + s0 + i) : 0;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < ITEMS; j++) val[j] = (r[j] != REC_SENTINEL && rec_w(r[j])) ? rec_val<SPILL>(p, r[j]) : 0;
+  }
   // (an absent item counts into the spare counter: no branch per item)
 #pragma unroll
   for (int j = 0; j < ITEMS; j++) atomicAdd(&S.cnt[r[j] != REC_SENTINEL ? bucket_low(r[j]) : BUCKET_CELLS], 1u);

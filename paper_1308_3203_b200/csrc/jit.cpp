@@ -57,7 +57,7 @@ constexpr int JIT_THREADS = 256;
 // resident blocks per SM the register allocation must allow (RC_JIT_MINB, A/B knob)
 int jit_min_blocks() {
   const char* e = getenv("RC_JIT_MINB");
-  return e ? std::max(1, atoi(e)) : 2;
+  return e ? std::max(1, atoi(e)) : 4;
 }
 
 // ---- NVRTC (dlopen: librc.so loads without it) and the driver API (entry
@@ -141,7 +141,7 @@ namespace {
 
 std::string shape_key(const JitShape& S) {
   std::ostringstream o;
-  o << S.n << ':' << S.gid << ':' << S.cpi << ':' << S.direct << S.fuel << S.ro_skip << S.wbucket;
+  o << S.n << ':' << S.gid << ':' << S.cpi << ':' << S.direct << S.fuel << S.ro_skip << S.wbucket << S.narrow;
   for (size_t a = 0; a < S.off.size(); a++) o << ':' << S.off[a] << '/' << S.size[a];
   return o.str();
 }
@@ -338,7 +338,8 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
     << ") rc_k1c(const __grid_constant__ K1cParams p) {\n"
     << "  if (*p.abort) return;  // speculative interval (DevCounters::abort)\n"
     << "  const u32 lane = threadIdx.x & 31u;\n"
-    << "  u64 s_instr = 0, s_loads = 0, s_stores = 0, s_recs = 0, s_wrec = 0;\n"
+    << "  " << (S.narrow ? "u32" : "u64") << " s_instr = 0, s_loads = 0, s_stores = 0, s_recs = 0, s_wrec = 0;"
+    << (S.narrow ? "  // (per-thread sums < 2^32: the host's step bound)" : "") << "\n"
     << "  bool s_wait = false, s_bail = false, s_bover = false;\n"
     << "  u32 a4_inst = 0xFFFFFFFFu; i32 a4_lo = 0, a4_hi = 0;\n";
   if (!D)
@@ -542,6 +543,7 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
         << "        pos = __shfl_sync(m, pos, leader) + __popc(m & ((1u << lane) - 1u));\n"
         << "        if (pos < p.region) p.bucket_out[(u64)b * p.region + pos] = ((u64)oc" << j << " << 32) | (g << 5) | "
         << (j << 1 | 1) << "u; else s_bover = true;\n"
+        << "        if (pos < p.region) p.bucket_val[(u64)b * p.region + pos] = ov" << j << ";  // (beside the record)\n"
         << "        p.wval[(u64)" << j << " * p.n_lanes + g] = ov" << j << ";\n"
         << "        if (!(ro >> 31)) p.wmap[oc" << j << "] = (u8)p.wtag;\n"
         << "        s_wrec++;\n"
@@ -586,15 +588,15 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
     << "    s_instr += steps; s_loads += nl; s_stores += ns;\n"
     << "    s_wait |= st == " << (int)L_WAITING << ";\n"
     << "  }\n";
-  o << "  s_instr = wsum(s_instr); s_loads = wsum(s_loads); s_stores = wsum(s_stores); s_recs = wsum(s_recs);\n"
-    << "  s_wrec = wsum(s_wrec);\n"
+  o << "  const u64 w_instr = wsum(s_instr), w_loads = wsum(s_loads), w_stores = wsum(s_stores), w_recs = wsum(s_recs);\n"
+    << "  const u64 w_wrec = wsum(s_wrec);\n"
     << "  const bool any_bail = __any_sync(FULL, s_bail), any_wait = __any_sync(FULL, s_wait), any_bover = __any_sync(FULL, s_bover);\n"
     << "  if (lane == 0) {\n"
-    << "    if (s_instr) atomicAdd(p.iv_instr, s_instr);\n"
-    << "    if (s_loads) atomicAdd(p.iv_loads, s_loads);\n"
-    << "    if (s_stores) atomicAdd(p.iv_stores, s_stores);\n"
-    << "    if (s_recs) atomicAdd(p.staged_recs, s_recs);\n"
-    << "    if (s_wrec) { atomicAdd(p.kept_count, s_wrec); atomicAdd(p.kept_writes, s_wrec); }  // (bucket writes)\n"
+    << "    if (w_instr) atomicAdd(p.iv_instr, w_instr);\n"
+    << "    if (w_loads) atomicAdd(p.iv_loads, w_loads);\n"
+    << "    if (w_stores) atomicAdd(p.iv_stores, w_stores);\n"
+    << "    if (w_recs) atomicAdd(p.staged_recs, w_recs);\n"
+    << "    if (w_wrec) { atomicAdd(p.kept_count, w_wrec); atomicAdd(p.kept_writes, w_wrec); }  // (bucket writes)\n"
     << "    if (any_bail) { *p.jit_bail = 1; *p.log_overflow = 1; }\n"
     << "    if (any_wait) *p.any_waiting = 1;\n"
     << "    if (any_bover) *p.bucket_overflow = 1;  // the host re-runs the interval with K1\n"
@@ -759,6 +761,7 @@ RC_API size_t rc_debug_jit_source(const rc_program* P, uint32_t n, const uint32_
   S.fuel = (flags & 2u) != 0;
   S.ro_skip = (flags & 4u) != 0;
   S.wbucket = (flags & 8u) != 0;
+  S.narrow = (flags & 16u) != 0;
   const std::string src = rc::jit_source(P, S);
   if (buf && cap) {
     const size_t k = std::min(cap - 1, src.size());

@@ -222,7 +222,7 @@ struct InterpParams {
     unsigned int* log_overflow; unsigned int* any_waiting; unsigned int* jit_bail; const unsigned int* abort; \
     unsigned long long report_cap; unsigned long long fuel; unsigned long long stage_cap;                 \
     unsigned long long* bucket_out; unsigned int* bcur; unsigned int* bucket_overflow; unsigned int region; \
-    unsigned long long* kept_count; unsigned long long* kept_writes;                                      \
+    unsigned long long* kept_count; unsigned long long* kept_writes; int* bucket_val;                     \
     unsigned int n_lanes, lane_pad, reg_stride, interval, inst_base, planes, wtag, check_div;              \
   };
 RC_K1C_PARAMS_DECL
@@ -237,6 +237,7 @@ struct JitShape {
   bool fuel = false;     // per-instruction fuel check
   bool ro_skip = false;  // static write-set elision (off with RC_OPT_KEEP_ALL_READS / work-groups)
   bool wbucket = false;  // bucket region mode: write records go straight into their bucket regions
+  bool narrow = false;   // per-thread statistics fit 32 bits (steps per work-item-interval < 2^20)
 };
 struct JitKernel {
   void* fn = nullptr;   // CUfunction
@@ -300,6 +301,10 @@ struct DetectParams {
   const uint32_t* rcur;
   uint32_t* rend;
   bool region_rerun;
+  // K1c in region mode wrote every write record's final value beside it
+  // (bval[slot] for recs[slot]): the lone writers' commits read it in the
+  // same pass as the records (null: gather from wval by lane)
+  const int32_t* bval;
 };
 
 // ---- launchers (defined in the .cu files) --------------------------------

@@ -122,6 +122,7 @@ struct rc_workspace {
   DevBuf regs[2], pc[2], status[2], live, entry_ro;
   DevBuf log, log_alt, wval, wmap, sort_status, ctr_block;
   DevBuf buckets;  // bucket path: [NB_MAX] starts | [NB_MAX] scatter cursors
+  DevBuf bval;     // K1c region mode: the write records' final values beside them (W.log slot -> value)
   DevBuf spill_cell, spill_val, spill_n;  // own-write overlay spill lists (grown on demand)
   DevBuf ig;                              // inter-group race state (groups.cu), IG_FIELDS planes
   uint32_t spill_cap = 0;                 // entries per lane the spill buffers hold
@@ -490,41 +491,54 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   JitKernel jk;
   bool jit_on = false, jit_wbucket = false;
   int jit_planes = 0;
-  {
-    const char* je = getenv("RC_JIT");
-    const bool force = je && je[0] == '1';
-    const uint64_t min_lanes = getenv("RC_JIT_MIN_LANES") ? strtoull(getenv("RC_JIT_MIN_LANES"), nullptr, 10) : (1ull << 20);
-    if (!(je && je[0] == '0') && G == 1 && I_b && (force || L_max >= min_lanes)) {
-      JitShape S;
-      S.n = n;
-      S.gid = 0;
-      S.cpi = (uint32_t)cpi;
-      S.off.assign(off.begin(), off.begin() + n_arrays);
-      S.size.assign(size.begin(), size.begin() + n_arrays);
-      S.direct = direct;
-      S.fuel = P->instr_bound < 0 || (uint64_t)P->instr_bound > opt.fuel_per_interval;
-      S.ro_skip = (opt.flags & RC_OPT_KEEP_ALL_READS) == 0;
-      // bucket region mode: K1c places its write records in the bucket
-      // regions itself; the planes (and the scatter) carry only reads
-      S.wbucket = region && !direct && getenv("RC_JIT_NO_WBUCKET") == nullptr;
-      std::string why;
-      jit_on = jit_get(P, S, &jk, &why);
-      if (!jit_on && getenv("RC_JIT_VERBOSE")) fprintf(stderr, "rc: K1c not used: %s\n", why.c_str());
-      jit_wbucket = S.wbucket;
-      jit_planes = direct ? 0
-                   : S.wbucket ? (S.ro_skip ? P->read_bound_ro : P->read_bound)
-                               : (S.ro_skip ? P->rec_bound_ro : P->rec_bound);
-      if (jit_on && jit_planes > 0) {  // fixed record slots: planes x (lanes rounded up to LANE_PAD)
-        const uint64_t want = (uint64_t)jit_planes * ((L_max + LANE_PAD - 1) / LANE_PAD * LANE_PAD);
-        if (log_cap < want) {
-          CK(W.log.ensure(std::max<uint64_t>(W.log.bytes, want * 8)));
-          CK(W.log_alt.ensure(want * 8));
-          log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
-          CK(ensure_sort_status(log_cap));
-        }
+  const char* jit_env = getenv("RC_JIT");
+  const uint64_t jit_min_lanes =
+      getenv("RC_JIT_MIN_LANES") ? strtoull(getenv("RC_JIT_MIN_LANES"), nullptr, 10) : (1ull << 20);
+  const bool jit_wanted = !(jit_env && jit_env[0] == '0') && G == 1 && I_b &&
+                          ((jit_env && jit_env[0] == '1') || L_max >= jit_min_lanes);
+  // the K1c variant for this run: wb = its write records go straight into the
+  // bucket regions (region mode; the planes and the scatter carry only reads)
+  auto select_jit = [&](bool wb) -> cudaError_t {
+    JitShape S;
+    S.n = n;
+    S.gid = 0;
+    S.cpi = (uint32_t)cpi;
+    S.off.assign(off.begin(), off.begin() + n_arrays);
+    S.size.assign(size.begin(), size.begin() + n_arrays);
+    S.direct = direct;
+    S.fuel = P->instr_bound < 0 || (uint64_t)P->instr_bound > opt.fuel_per_interval;
+    S.ro_skip = (opt.flags & RC_OPT_KEEP_ALL_READS) == 0;
+    // a thread runs <= 2^27 / (148 * 256) < 3600 lanes: 32-bit statistics
+    // when no work-item can execute 2^20 instructions in one interval
+    const uint64_t sb = P->instr_bound >= 0 ? std::min<uint64_t>((uint64_t)P->instr_bound, opt.fuel_per_interval)
+                                            : opt.fuel_per_interval;
+    S.narrow = sb < (1ull << 20);
+    S.wbucket = wb && !direct;
+    std::string why;
+    jit_on = jit_get(P, S, &jk, &why);
+    if (!jit_on && getenv("RC_JIT_VERBOSE")) fprintf(stderr, "rc: K1c not used: %s\n", why.c_str());
+    jit_wbucket = S.wbucket;
+    if (jit_on && jit_wbucket) {  // values beside the records: one int32 per region slot
+      const uint64_t nb_max = std::max<uint64_t>(1, ((uint64_t)I_b * cpi + BUCKET_CELLS - 1) / BUCKET_CELLS);
+      const cudaError_t e = W.bval.ensure(nb_max * BUCKET_REGION * 4 + 64);
+      if (e != cudaSuccess) return e;
+    }
+    jit_planes = direct ? 0
+                 : S.wbucket ? (S.ro_skip ? P->read_bound_ro : P->read_bound)
+                             : (S.ro_skip ? P->rec_bound_ro : P->rec_bound);
+    if (jit_on && jit_planes > 0) {  // fixed record slots: planes x (lanes rounded up to LANE_PAD)
+      const uint64_t want = (uint64_t)jit_planes * ((L_max + LANE_PAD - 1) / LANE_PAD * LANE_PAD);
+      if (log_cap < want) {
+        cudaError_t e = W.log.ensure(std::max<uint64_t>(W.log.bytes, want * 8));
+        if (e == cudaSuccess) e = W.log_alt.ensure(want * 8);
+        if (e != cudaSuccess) return e;
+        log_cap = std::min(W.log.bytes, W.log_alt.bytes) / 8;
+        return ensure_sort_status(log_cap);
       }
     }
-  }
+    return cudaSuccess;
+  };
+  if (jit_wanted) CK(select_jit(region && getenv("RC_JIT_NO_WBUCKET") == nullptr));
   bool jit_off = false;  // a K1c interval bailed: K1 for the rest of the run
   bool jit_fix_pending = false;  // lane state K1c produced has rematerialised registers missing from the rows
   bool jit_used_wb[2] = {false, false};  // interval k & 1 ran K1c with its writes in the buckets
@@ -703,6 +717,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       dp.rcur = W.sort.hist;
       dp.rend = W.buckets.as<uint32_t>() + NB_MAX;  // (free in region mode)
       dp.region_rerun = false;
+      dp.bval = nullptr;
       return dp;
     };
     struct Marks { size_t m0 = 0, m1 = 0; };
@@ -804,6 +819,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       kp.bcur = W.sort.hist;
       kp.bucket_overflow = &dctr->bucket_overflow;
       kp.region = BUCKET_REGION;
+      kp.bucket_val = W.bval.as<int32_t>();
       kp.kept_count = &dctr->kept_count;
       kp.kept_writes = &dctr->kept_writes;
       return kp;
@@ -866,6 +882,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       // ---- K4+K5 detect + commit, A4 check + verdict
       DetectParams dp = detect_params(kk);
       dp.with_boundary = true;  // A4 as detect's tail: consumes (and resets) K1's per-instance node ranges
+      if (wb) dp.bval = W.bval.as<int32_t>();  // every write record's value is beside it
       if (direct) {  // nothing was logged: the kernel runs only its A4 tail (one block)
         dp.nb = 0;
         dp.n_records = 0;
@@ -990,10 +1007,11 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       // re-run with K1 in count mode (K1 for the rest of the run)
       const bool jit_bucket_over = h.bucket_overflow && jit_used_wb[k & 1];
       if (log_over || k1_rep_over || spill_over || jit_bucket_over) {  // filter/detect skipped: grow and re-run
-        if (h.jit_bail || jit_bucket_over) jit_off = true;  // a K1c work-item had more records than its planes
-        if (jit_bucket_over) {
+        if (h.jit_bail) jit_off = true;  // a K1c work-item had more records than its planes: K1 from here
+        if (jit_bucket_over) {  // count mode from here; K1c places its write records in the planes again
           W.region_ok = false;
           region = false;
+          if (!jit_off) CK(select_jit(false));
         }
         if (spill_over) {
           const int e = grow_spill();
@@ -1052,6 +1070,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
           CK(set_report_count(h.k1_reports));
           DetectParams dp = detect_params(k);
           dp.region_rerun = dp.region != 0;  // (the region cursors were reset by the next interval's scratch)
+          if (jit_used_wb[k & 1]) dp.bval = W.bval.as<int32_t>();
           CK(launch_detect(dp, s));
           CK(read_ctr());
           rc = W.h_ctr[2].report_count;

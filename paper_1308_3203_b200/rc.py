@@ -148,10 +148,10 @@ class Program:
         return int(lib().rc_debug_jit_kernels(self._h))
 
     def jit_source(self, work_group_size: int, sizes: list, *, direct=False, fuel=False, ro_skip=True,
-                   wbucket=False) -> str:
+                   wbucket=False, narrow=False) -> str:
         """Test hook: the K1c CUDA source for this program and shape (no GPU needed)."""
         arr = (C.c_uint32 * max(1, len(sizes)))(*sizes)
-        flags = (1 if direct else 0) | (2 if fuel else 0) | (4 if ro_skip else 0) | (8 if wbucket else 0)
+        flags = (1 if direct else 0) | (2 if fuel else 0) | (4 if ro_skip else 0) | (8 if wbucket else 0) | (16 if narrow else 0)
         f = lib().rc_debug_jit_source
         nb = f(self._h, work_group_size, arr, len(sizes), flags, None, 0)
         buf = C.create_string_buffer(nb + 1)

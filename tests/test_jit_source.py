@@ -64,7 +64,8 @@ def programs():
 def test_k1c_source_compiles(rc, name, p, n, sizes):
     prog = rc.rc_load_program(p.bytecode)
     sizes = sizes or [n + 16] * prog.n_arrays
-    modes = [dict(wbucket=True), dict(), dict(fuel=True), dict(direct=True), dict(ro_skip=False, wbucket=True)]
+    modes = [dict(wbucket=True, narrow=True), dict(), dict(fuel=True), dict(direct=True, narrow=True),
+             dict(ro_skip=False, wbucket=True)]
     for m in modes[: 5 if name in ("stencil", "tree", "tiny0") else 2]:
         src = prog.jit_source(n, sizes, **m)
         assert 'extern "C" __global__' in src and "rc_k1c" in src
