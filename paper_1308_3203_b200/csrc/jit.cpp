@@ -313,14 +313,6 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
       for (uint32_t r = 0; r < P->n_regs; r++)
         if (LIVE[e][r] && AFF[e][r].k != 1) carried[r] = 1;
   if (n_carried) *n_carried = (int)std::count(carried.begin(), carried.end(), (uint8_t)1);
-  // group-uniform lane state: carried register r has slot
-  // cslot[r] in the per-group mask (the first 32 carried registers)
-  std::vector<int> cslot(P->n_regs, -1);
-  {
-    int k = 0;
-    for (uint32_t r = 0; r < P->n_regs; r++)
-      if (carried[r] && k < 32) cslot[r] = k++;
-  }
   const int K = std::max(1, P->ovl_cap);
   const bool D = S.direct;
   std::ostringstream o;
@@ -361,20 +353,9 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
   auto prefetch = [&](const char* gexpr, const char* cond) {
     o << "    { const u32 g2 = " << gexpr << "; n_st = " << (int)L_EXITED << "; n_pc = 0u;\n"
       << "      if (" << cond << " && g2 < p.n_lanes) {\n"
-      << "        n_st = p.status_in[g2];\n"
-      << "        const u32 gp = p.gpc_in[g2 >> 5];  // the group's pc when all its lanes agree\n"
-      << "        n_pc = (gp >> 31) ? (gp & 0xFFFFu) : p.pc_in[g2];\n";
-    bool any_c = false;
-    for (uint32_t r = 0; r < P->n_regs; r++) any_c = any_c || cslot[r] >= 0;
-    if (any_c) o << "        const u32 um = p.umask_in[g2 >> 5];  // the group's uniform registers\n";
-    for (uint32_t r = 0; r < P->n_regs; r++) {
-      if (!carried[r]) continue;
-      if (cslot[r] >= 0)
-        o << "        n_r" << r << " = ((um >> " << cslot[r] << ") & 1u) ? p.uval_in[(u64)" << r
-          << " * p.ngroups + (g2 >> 5)] : p.regs_in[(u64)" << r << " * p.reg_stride + g2];\n";
-      else
-        o << "        n_r" << r << " = p.regs_in[(u64)" << r << " * p.reg_stride + g2];\n";
-    }
+      << "        n_st = p.status_in[g2]; n_pc = p.pc_in[g2];\n";
+    for (uint32_t r = 0; r < P->n_regs; r++)
+      if (carried[r]) o << "        n_r" << r << " = p.regs_in[(u64)" << r << " * p.reg_stride + g2];\n";
     o << "      } }\n";
   };
   o << "  const u32 stride = gridDim.x * blockDim.x;\n"
@@ -406,7 +387,7 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
     << "    const u32 tid = g - inst * " << S.n << "u;\n"
     << "    const u32 cb = inst * " << S.cpi << "u;\n"
     << "    " << (S.fuel ? "u64" : "u32") << " steps = 0;\n"
-    << "    u32 nl = 0, ns = 0, nrec = 0, ro = 0, n_own = 0, smask = 0;\n";
+    << "    u32 nl = 0, ns = 0, nrec = 0, ro = 0, n_own = 0;\n";
   for (int j = 0; j < K; j++) o << "    u32 oc" << j << " = 0; i32 ov" << j << " = 0;\n";
   o    << "    if (running) {\n"
     << "      st = " << (int)L_RUNNING << ";\n";
@@ -511,19 +492,14 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
         o << "        ns++;\n";
         break;
       }
-      case RC_OP_BAR: {
-        // the registers the work-item resumes with at pc + 1 (the carried
-        // ones): stored at the interval end, per lane or once per group
-        uint64_t need = 0;
+      case RC_OP_BAR:
+        // the registers the work-item resumes with at pc + 1 (the carried ones)
         if (pc + 1 < N)
           for (uint32_t r = 0; r < P->n_regs; r++)
-            if (LIVE[pc + 1][r] && AFF[pc + 1][r].k != 1) {
-              if (cslot[r] >= 0) need |= 1ull << cslot[r];
-              else o << "        p.regs_out[(u64)" << r << " * p.reg_stride + g] = r" << r << ";\n";
-            }
-        o << "        smask = " << need << "u; pc = " << pc + 1 << "u; st = " << (int)L_WAITING << "; goto Lend;\n";
+            if (LIVE[pc + 1][r] && AFF[pc + 1][r].k != 1)
+              o << "        p.regs_out[(u64)" << r << " * p.reg_stride + g] = r" << r << ";\n";
+        o << "        pc = " << pc + 1 << "u; st = " << (int)L_WAITING << "; goto Lend;\n";
         break;
-      }
       case RC_OP_EXIT:
         o << "        pc = " << pc << "u; st = " << (int)L_EXITED_NOW << "; goto Lend;\n";
         break;
@@ -545,36 +521,11 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
   }
   o << "    Lend:;\n"
     << "    }\n";
-  // lane state out: status per lane; pc and the carried registers once per
-  // 32-lane group when every lane of the group agrees (else per lane)
-  o << "    __syncwarp();\n"
-    << "    if (valid) p.status_out[g] = st;\n"
-    << "    { const u32 p0 = __shfl_sync(FULL, pc, 0);\n"
-    << "      const bool upc = __all_sync(FULL, !valid || pc == p0);\n"
-    << "      if (lane == 0) p.gpc_out[g >> 5] = upc ? (0x80000000u | p0) : 0u;\n"
-    << "      if (valid && !upc) p.pc_out[g] = pc;\n"
-    << "    }\n";
-  {
-    bool any_c = false;
-    for (uint32_t r = 0; r < P->n_regs; r++) any_c = any_c || cslot[r] >= 0;
-    if (any_c) {
-      o << "    { u32 um = 0;\n";
-      for (uint32_t r = 0; r < P->n_regs; r++) {
-        if (cslot[r] < 0) continue;
-        const int i = cslot[r];
-        o << "      { const bool need = (smask >> " << i << ") & 1u;\n"
-          << "        bool uni = false;\n"
-          << "        if (__all_sync(FULL, need)) { const i32 v0 = __shfl_sync(FULL, r" << r << ", 0); uni = __all_sync(FULL, r" << r
-          << " == v0); }\n"
-          << "        if (uni) { if (lane == 0) p.uval_out[(u64)" << r << " * p.ngroups + (g >> 5)] = r" << r << "; um |= "
-          << (1u << i) << "u; }\n"
-          << "        else if (need) p.regs_out[(u64)" << r << " * p.reg_stride + g] = r" << r << ";\n"
-          << "      }\n";
-      }
-      o << "      if (lane == 0) p.umask_out[g >> 5] = um;\n"
-        << "    }\n";
-    }
-  }
+  // lane state out
+  o << "    if (valid) {\n"
+    << "      p.status_out[g] = st;\n"
+    << "      p.pc_out[g] = pc;\n";
+  o << "    }\n";
   // the interval's writes: write records (final value, reading L3, to wval;
   // the write-set map) — or, in direct mode, the commit itself
   if (S.wbucket) o << "    __syncwarp();\n";
@@ -651,24 +602,15 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
     << "    if (any_bover) *p.bucket_overflow = 1;  // the host re-runs the interval with K1\n"
     << "  }\n"
     << "}\n";
-  // rc_k1c_fix: before anything but K1c reads lane state K1c produced (K1,
-  // the divergence / interval-limit scans), expand it into plain rows: the
-  // group-uniform pcs and registers, and the rematerialised registers of
-  // every work-item waiting at an interval entry
+  // rc_k1c_fix: before K1 (the interpreter, which reads every live register
+  // row) runs on lane state K1c produced, write the rematerialised registers
+  // of every work-item waiting at an interval entry into the rows
   o << "extern \"C\" __global__ void __launch_bounds__(256) rc_k1c_fix(const __grid_constant__ K1cParams p) {\n"
     << "  for (u32 g = blockIdx.x * blockDim.x + threadIdx.x; g < p.n_lanes; g += gridDim.x * blockDim.x) {\n"
-    << "    const u32 gp = p.gpc_in[g >> 5];\n"
-    << "    u32 pc = p.pc_in[g];\n"
-    << "    if (gp >> 31) { pc = gp & 0xFFFFu; p.pc_out[g] = pc; }  // the group's pc into the row\n"
     << "    const u8 st = p.status_in[g];\n"
     << "    if (st != " << (int)L_RUNNING << " && st != " << (int)L_WAITING << ") continue;\n"
     << "    const u32 inst = g / " << S.n << "u, tid = g - inst * " << S.n << "u;\n"
-    << "    const u32 um = p.umask_in[g >> 5];\n";
-  for (uint32_t r = 0; r < P->n_regs; r++)
-    if (cslot[r] >= 0)
-      o << "    if ((um >> " << cslot[r] << ") & 1u) p.regs_out[(u64)" << r << " * p.reg_stride + g] = p.uval_in[(u64)" << r
-        << " * p.ngroups + (g >> 5)];\n";
-  o << "    switch (pc) {\n";
+    << "    switch (p.pc_in[g]) {\n";
   for (uint32_t e = 0; e < N; e++) {
     if (!F.entry[e]) continue;
     o << "      case " << e << "u:";

@@ -223,8 +223,6 @@ struct InterpParams {
     unsigned long long report_cap; unsigned long long fuel; unsigned long long stage_cap;                 \
     unsigned long long* bucket_out; unsigned int* bcur; unsigned int* bucket_overflow; unsigned int region; \
     unsigned long long* kept_count; unsigned long long* kept_writes; int* bucket_val;                     \
-    const unsigned int* gpc_in; unsigned int* gpc_out; const unsigned int* umask_in; unsigned int* umask_out; \
-    const int* uval_in; int* uval_out; unsigned int ngroups;                                              \
     unsigned int n_lanes, lane_pad, reg_stride, interval, inst_base, planes, wtag, check_div;              \
   };
 RC_K1C_PARAMS_DECL

@@ -122,7 +122,6 @@ struct rc_workspace {
   DevBuf regs[2], pc[2], status[2], live, entry_ro;
   DevBuf log, log_alt, wval, wmap, sort_status, ctr_block;
   DevBuf buckets;  // bucket path: [NB_MAX] starts | [NB_MAX] scatter cursors
-  DevBuf gpc[2], umask[2], uval[2];  // K1c: per 32-lane group uniform pc / register mask / register values
   DevBuf bval;     // K1c region mode: the write records' final values beside them (W.log slot -> value)
   DevBuf spill_cell, spill_val, spill_n;  // own-write overlay spill lists (grown on demand)
   DevBuf ig;                              // inter-group race state (groups.cu), IG_FIELDS planes
@@ -399,9 +398,6 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       CK(W.regs[b].ensure(L_pad * P->n_regs * 4));
       CK(W.pc[b].ensure(L_pad * 4));
       CK(W.status[b].ensure(L_pad));
-      CK(W.gpc[b].ensure(L_pad / 32 * 4 + 64));
-      CK(W.umask[b].ensure(L_pad / 32 * 4 + 64));
-      CK(W.uval[b].ensure((uint64_t)P->n_regs * (L_pad / 32) * 4 + 64));
     }
     CK(W.inst_tmp.ensure((uint64_t)I_b * 20));
     if (classify) {
@@ -781,15 +777,8 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       return ip;
     };
     // K1c's parameter block for the interval interpreter's parameters
-    auto make_kp = [&](const InterpParams& ip, uint32_t kk, int cc) {
+    auto make_kp = [&](const InterpParams& ip, uint32_t kk) {
       K1cParams kp;
-      kp.gpc_in = W.gpc[cc].as<uint32_t>();
-      kp.gpc_out = W.gpc[cc ^ 1].as<uint32_t>();
-      kp.umask_in = W.umask[cc].as<uint32_t>();
-      kp.umask_out = W.umask[cc ^ 1].as<uint32_t>();
-      kp.uval_in = W.uval[cc].as<int32_t>();
-      kp.uval_out = W.uval[cc ^ 1].as<int32_t>();
-      kp.ngroups = reg_stride / 32;
       kp.status_in = ip.status_in;
       kp.pc_in = ip.pc_in;
       kp.regs_in = ip.regs_in;
@@ -835,14 +824,6 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       kp.kept_writes = &dctr->kept_writes;
       return kp;
     };
-    // lane state buffer cc as plain rows (pc and the carried / rematerialised
-    // registers of K1c's compact form written out) for K1 and the scans
-    auto expand_state = [&](uint32_t kk, int cc) -> cudaError_t {
-      K1cParams kp = make_kp(make_ip(kk, cc), kk, cc);
-      kp.pc_out = W.pc[cc].as<uint32_t>();
-      kp.regs_out = W.regs[cc].as<int32_t>();
-      return jit_fix(jk, kp, s);
-    };
     auto enqueue_interval = [&](uint32_t kk, int cc, Marks* mk) -> cudaError_t {
       cudaError_t e;
 #define EQ(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
@@ -865,17 +846,15 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       W.prof.cut();
       W.prof.begin(s);
       if (jit_on && !jit_off) {
-        const K1cParams kp = make_kp(ip, kk, cc);
+        const K1cParams kp = make_kp(ip, kk);
         jit_fix_pending = true;
         EQ(jit_launch(jk, kp, s));
       } else {
-        if (jit_fix_pending) {  // K1 reads plain rows: expand the lane state K1c produced
-          EQ(expand_state(kk, cc));
+        if (jit_fix_pending) {  // K1 reads every live register row: write K1c's rematerialised ones
+          K1cParams kp = make_kp(ip, kk);
+          kp.regs_out = const_cast<int32_t*>(ip.regs_in);
+          EQ(jit_fix(jk, kp, s));
           jit_fix_pending = false;
-        }
-        if (jit_on) {  // K1 writes plain rows: no group-uniform word of the output buffer is current
-          EQ(cudaMemsetAsync(W.gpc[cc ^ 1].p, 0, (size_t)reg_stride / 32 * 4, s));
-          EQ(cudaMemsetAsync(W.umask[cc ^ 1].p, 0, (size_t)reg_stride / 32 * 4, s));
         }
         EQ(launch_interp(ip, s));
       }
@@ -945,7 +924,11 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         }
         EQ(cudaMemsetAsync(W.ctr_block.p, 0, CTR_OFF + offsetof(DevCounters, report_count), s));
         InterpParams ip = make_ip(kk, cur);
-        if (jit_ran) EQ(expand_state(kk, cur));  // the interval's input lane state may be K1c's
+        if (jit_on) {  // the interval's input lane state may be K1c's (rematerialised registers)
+          K1cParams kp = make_kp(ip, kk);
+          kp.regs_out = const_cast<int32_t*>(ip.regs_in);
+          EQ(jit_fix(jk, kp, s));
+        }
         ip.heap = W.heap_snap[kk & 1].as<int32_t>();  // interval-start heap
         ip.alt_heap = heap_cur;                       // committed heap (writers first)
         ip.alt_mask = W.amap.as<uint8_t>();
@@ -996,10 +979,6 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     if (L) {
       CK(cudaMemsetAsync(W.status[cur].p, 0, reg_stride, s));
       CK(cudaMemsetAsync(W.pc[cur].p, 0, (size_t)reg_stride * 4, s));
-      if (jit_on) {  // K1c's group-uniform words: none yet
-        CK(cudaMemsetAsync(W.gpc[cur].p, 0, (size_t)reg_stride / 32 * 4, s));
-        CK(cudaMemsetAsync(W.umask[cur].p, 0, (size_t)reg_stride / 32 * 4, s));
-      }
       // registers start at 0 (reading L18): only a register read before it is
       // written in interval 0 (live_in(pc 0)) can observe it; the other rows K1
       // loads are overwritten before any read
@@ -1100,7 +1079,6 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       if (h.diverged) {  // rare path: lane scans for the divergence report (idempotent)
         const uint64_t before = rc;
         for (;;) {
-          if (jit_ran) CK(expand_state(k + 1, cur ^ 1));  // the scan reads plain pc rows
           BoundaryParams bp = bparams(k);
           bp.status = W.status[cur ^ 1].as<uint8_t>();
           bp.pc = W.pc[cur ^ 1].as<uint32_t>();
@@ -1138,7 +1116,6 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       k++;
       if (k >= opt.max_intervals) {  // instance-level FUEL (reading L17); nothing was speculated
         for (;;) {
-          if (jit_ran) CK(expand_state(k, cur));  // the scan reads plain pc rows
           BoundaryParams bp = bparams(k);
           bp.status = W.status[cur].as<uint8_t>();
           bp.pc = W.pc[cur].as<uint32_t>();
