@@ -57,7 +57,7 @@ constexpr int JIT_THREADS = 256;
 // resident blocks per SM the register allocation must allow (RC_JIT_MINB, A/B knob)
 int jit_min_blocks() {
   const char* e = getenv("RC_JIT_MINB");
-  return e ? std::max(1, atoi(e)) : 4;
+  return e ? std::max(1, atoi(e)) : 5;
 }
 
 // ---- NVRTC (dlopen: librc.so loads without it) and the driver API (entry
@@ -358,8 +358,22 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
       if (carried[r]) o << "        n_r" << r << " = p.regs_in[(u64)" << r << " * p.reg_stride + g2];\n";
     o << "      } }\n";
   };
-  o << "  const u32 stride = gridDim.x * blockDim.x;\n"
-    << "  u32 base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);\n"
+  // lanes -> warps: blocked (a warp walks a contiguous run of 32-lane
+  // groups), so the warps in flight at any moment are spread over the whole
+  // batch and seldom meet on one bucket cursor (cyclic: every warp of the
+  // grid in the same few buckets; RC_JIT_CYCLIC=1 is the A/B knob)
+  const bool cyc = getenv("RC_JIT_CYCLIC") != nullptr;
+  if (cyc)
+    o << "  const u32 stride = gridDim.x * blockDim.x;\n"
+      << "  u32 base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);\n"
+      << "  const u32 base_end = p.lane_pad;\n";
+  else
+    o << "  const u32 stride = 32u;\n"
+      << "  const u32 n_w = gridDim.x * (blockDim.x >> 5), w_id = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);\n"
+      << "  const u32 n_grp = p.lane_pad >> 5, per_w = (n_grp + n_w - 1) / n_w;\n"
+      << "  u32 base = min(w_id * per_w, n_grp) * 32u;\n"
+      << "  const u32 base_end = min((w_id + 1) * per_w, n_grp) * 32u;\n";
+  o
     << "  u8 n_st; u32 n_pc;";
   for (uint32_t r = 0; r < P->n_regs; r++)
     if (carried[r]) o << " i32 n_r" << r << " = 0;";
@@ -369,9 +383,9 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
   // with the rematerialised registers only status, pc and the carried ones
   // are in flight: 57.1 vs 70.7 ms/step)
   const bool pf = getenv("RC_JIT_NOPF") == nullptr;
-  if (pf) prefetch("base + lane", "base < p.lane_pad");
+  if (pf) prefetch("base + lane", "base < base_end");
 
-  o << "  for (; base < p.lane_pad; base += stride) {\n"
+  o << "  for (; base < base_end; base += stride) {\n"
     << "    const u32 g = base + lane;\n"
     << "    const bool valid = g < p.n_lanes;\n";
   if (!pf) prefetch("g", "true");
@@ -380,7 +394,7 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
   for (uint32_t r = 0; r < P->n_regs; r++) {
     o << "    i32 r" << r << " = " << (carried[r] ? "n_r" + std::to_string(r) : std::string("0")) << ";\n";
   }
-  if (pf) prefetch("g + stride", "base + stride < p.lane_pad");
+  if (pf) prefetch("g + stride", "base + stride < base_end");
   o << "    if (st == " << (int)L_EXITED_NOW << ") st = " << (int)L_EXITED << ";\n"
     << "    const bool running = valid && (st == " << (int)L_RUNNING << " || st == " << (int)L_WAITING << ");\n"
     << "    const u32 inst = valid ? g / " << S.n << "u : 0u;\n"
