@@ -337,6 +337,8 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
     << "extern \"C\" __global__ void __launch_bounds__(" << JIT_THREADS << ", " << jit_min_blocks()
     << ") rc_k1c(const __grid_constant__ K1cParams p) {\n"
     << "  if (*p.abort) return;  // speculative interval (DevCounters::abort)\n"
+    << "  __shared__ u32 s_done;  // warps of the block finished (the report-count snapshot)\n"
+    << "  if (p.snapshot) { if (threadIdx.x == 0) s_done = 0; __syncthreads(); }  // (converged: the kernel start)\n"
     << "  const u32 lane = threadIdx.x & 31u;\n"
     << "  " << (S.narrow ? "u32" : "u64") << " s_instr = 0, s_loads = 0, s_stores = 0, s_recs = 0, s_wrec = 0;"
     << (S.narrow ? "  // (per-thread sums < 2^32: the host's step bound)" : "") << "\n"
@@ -352,7 +354,12 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
   // its latency overlaps the heap loads and the writes of the current one)
   auto prefetch = [&](const char* gexpr, const char* cond) {
     o << "    { const u32 g2 = " << gexpr << "; n_st = " << (int)L_EXITED << "; n_pc = 0u;\n"
-      << "      if (" << cond << " && g2 < p.n_lanes) {\n"
+      << "      if (p.fresh) {  // a batch's first interval: RUNNING at pc 0, registers 0 (reading L18)\n"
+      << "        if (" << cond << " && g2 < p.n_lanes) n_st = " << (int)L_RUNNING << ";\n";
+    for (uint32_t r = 0; r < P->n_regs; r++)
+      if (carried[r]) o << "        n_r" << r << " = 0;\n";
+    o << "      }\n"
+      << "      else if (" << cond << " && g2 < p.n_lanes) {\n"
       << "        n_st = p.status_in[g2]; n_pc = p.pc_in[g2];\n";
     for (uint32_t r = 0; r < P->n_regs; r++)
       if (carried[r]) o << "        n_r" << r << " = p.regs_in[(u64)" << r << " * p.reg_stride + g2];\n";
@@ -614,6 +621,17 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
     << "    if (any_bail) { *p.jit_bail = 1; *p.log_overflow = 1; }\n"
     << "    if (any_wait) *p.any_waiting = 1;\n"
     << "    if (any_bover) *p.bucket_overflow = 1;  // the host re-runs the interval with K1\n"
+    << "  }\n"
+    // no scatter runs after this launch: its last block takes the scatter's
+    // snapshot of the report count after K1 (a detect-only re-run rolls back to it)
+    // (per warp, no block barrier: after the goto-structured code a warp's
+    // lanes need not have reconverged for an aligned __syncthreads; the warp
+    // is converged here — the reductions above are full-warp — and every
+    // report a lane emitted took its slot with a returning atomic)
+    << "  if (p.snapshot && lane == 0) {\n"
+    << "    __threadfence();\n"
+    << "    if (atomicAdd(&s_done, 1u) == (blockDim.x >> 5) - 1 && atomicAdd(p.k1c_done, 1u) == gridDim.x - 1)\n"
+    << "      *p.k1_reports = atomicAdd(p.report_count, 0ull);  // the block's last warp, the grid's last block\n"
     << "  }\n"
     << "}\n";
   // rc_k1c_fix: before K1 (the interpreter, which reads every live register

@@ -119,6 +119,7 @@ struct DevCounters {
   unsigned int count_done;          // bucket_count blocks finished (last-block pattern: the bucket starts)
   unsigned int bucket_overflow;     // region mode: a bucket got more records than its region holds
   unsigned int jit_bail;            // K1c: a work-item had more records than its planes (re-run interpreted)
+  unsigned int k1c_done;            // K1c blocks finished (the last one snapshots k1_reports)
   // ---- fields above: zeroed per interval attempt (one memset, runtime.cu)
   unsigned long long report_count;  // reports appended (whole run, rolled back on retry)
   unsigned long long lanes_final[8];
@@ -223,6 +224,7 @@ struct InterpParams {
     unsigned long long report_cap; unsigned long long fuel; unsigned long long stage_cap;                 \
     unsigned long long* bucket_out; unsigned int* bcur; unsigned int* bucket_overflow; unsigned int region; \
     unsigned long long* kept_count; unsigned long long* kept_writes; int* bucket_val;                     \
+    unsigned int* k1c_done; unsigned long long* k1_reports; unsigned int snapshot, fresh;                 \
     unsigned int n_lanes, lane_pad, reg_stride, interval, inst_base, planes, wtag, check_div;              \
   };
 RC_K1C_PARAMS_DECL

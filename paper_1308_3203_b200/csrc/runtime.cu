@@ -544,6 +544,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
   bool jit_used_wb[2] = {false, false};  // interval k & 1 ran K1c with its writes in the buckets
   bool jit_used_iv[2] = {false, false};  // interval k & 1 ran K1c
   bool jit_ran = false;
+  bool fresh_pending = false;  // this batch's initial lane state is not in the rows yet (K1c reads none)
 
   uint64_t tot_loads = 0, tot_stores = 0, tot_instr = 0, intervals_max = 0;
   uint64_t rep_count = 0;  // host mirror of ctr.report_count
@@ -656,6 +657,18 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       return e;
     };
     if (G > 1) CK(ig_reset(W.ig.as<uint32_t>(), bcells, s));
+    // the initial lane state as rows (status RUNNING, pc 0, the registers live
+    // at pc 0 zero — reading L18: a register read before it is written in
+    // interval 0 can observe it; the other rows are written before any read)
+    auto materialize_fresh = [&](int cc) -> cudaError_t {
+      const uint32_t rs = (uint32_t)((L + LANE_PAD - 1) / LANE_PAD * LANE_PAD);
+      cudaError_t e = cudaMemsetAsync(W.status[cc].p, 0, rs, s);
+      if (e == cudaSuccess) e = cudaMemsetAsync(W.pc[cc].p, 0, (size_t)rs * 4, s);
+      for (uint8_t r : P->live_at_entry)
+        if (e == cudaSuccess) e = cudaMemsetAsync(W.regs[cc].as<int32_t>() + (size_t)r * rs, 0, (size_t)rs * 4, s);
+      fresh_pending = false;
+      return e;
+    };
     auto bparams = [&](uint32_t interval) {
       BoundaryParams bp;
       bp.n = n;
@@ -821,6 +834,10 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       kp.region = BUCKET_REGION;
       kp.bucket_val = W.bval.as<int32_t>();
       kp.kept_count = &dctr->kept_count;
+      kp.k1c_done = &dctr->k1c_done;
+      kp.k1_reports = &dctr->k1_reports;
+      kp.snapshot = 0;
+      kp.fresh = 0;
       kp.kept_writes = &dctr->kept_writes;
       return kp;
     };
@@ -846,10 +863,15 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       W.prof.cut();
       W.prof.begin(s);
       if (jit_on && !jit_off) {
-        const K1cParams kp = make_kp(ip, kk);
+        K1cParams kp = make_kp(ip, kk);
+        // no scatter will run (writes in the buckets, no read record possible):
+        // K1c's last block snapshots the report count after K1 itself
+        kp.snapshot = jit_wbucket && jit_planes == 0 && !direct && !getenv("RC_JIT_NOSNAP");
+        kp.fresh = fresh_pending && kk == 0;
         jit_fix_pending = true;
         EQ(jit_launch(jk, kp, s));
       } else {
+        if (fresh_pending && kk == 0) EQ(materialize_fresh(cc));  // K1 reads the initial state
         if (jit_fix_pending) {  // K1 reads every live register row: write K1c's rematerialised ones
           K1cParams kp = make_kp(ip, kk);
           kp.regs_out = const_cast<int32_t*>(ip.regs_in);
@@ -874,10 +896,9 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       if (!direct && !(wb && jit_planes == 0))
         EQ(enqueue_sort(W.prof.on ? &W.prof : nullptr, (opt.flags & RC_OPT_KEEP_ALL_READS) != 0, region));
       else if (wb) {
-        sr = W.log.as<uint64_t>();  // the bucket regions K1c filled
-        // the scatter's snapshot of the report count after K1 (a detect-only
-        // re-run rolls back to it)
-        EQ(cudaMemcpyAsync(&dctr->k1_reports, &dctr->report_count, 8, cudaMemcpyDeviceToDevice, s));
+        sr = W.log.as<uint64_t>();  // the bucket regions K1c filled (its last block took the report snapshot)
+        if (getenv("RC_JIT_NOSNAP"))
+          EQ(cudaMemcpyAsync(&dctr->k1_reports, &dctr->report_count, 8, cudaMemcpyDeviceToDevice, s));
       }
       // ---- K4+K5 detect + commit, A4 check + verdict
       DetectParams dp = detect_params(kk);
@@ -924,6 +945,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
         }
         EQ(cudaMemsetAsync(W.ctr_block.p, 0, CTR_OFF + offsetof(DevCounters, report_count), s));
         InterpParams ip = make_ip(kk, cur);
+        if (fresh_pending && kk == 0) EQ(materialize_fresh(cur));
         if (jit_on) {  // the interval's input lane state may be K1c's (rematerialised registers)
           K1cParams kp = make_kp(ip, kk);
           kp.regs_out = const_cast<int32_t*>(ip.regs_in);
@@ -976,15 +998,12 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     // and queues k+1 again.
     for (gi = 0; gi < G; gi++) {  // work-groups one after another (reading L20)
     cur = 0;
-    if (L) {
-      CK(cudaMemsetAsync(W.status[cur].p, 0, reg_stride, s));
-      CK(cudaMemsetAsync(W.pc[cur].p, 0, (size_t)reg_stride * 4, s));
-      // registers start at 0 (reading L18): only a register read before it is
-      // written in interval 0 (live_in(pc 0)) can observe it; the other rows K1
-      // loads are overwritten before any read
-      for (uint8_t r : P->live_at_entry)
-        CK(cudaMemsetAsync(W.regs[cur].as<int32_t>() + (size_t)r * reg_stride, 0, (size_t)reg_stride * 4, s));
-    }
+    // K1c starts a batch from the initial state without reading it (every
+    // lane RUNNING at pc 0, registers 0): the rows are written only if
+    // something else reads them first (K1 after a hand-back, the
+    // classification re-run) — materialize_fresh()
+    fresh_pending = L && jit_on && !jit_off && !getenv("RC_JIT_NOFRESH");
+    if (L && !fresh_pending) CK(materialize_fresh(cur));
     CK(cudaMemsetAsync(node_min, 0x7F, (size_t)nb * 4, s));  // large positive: "no arrival"
     CK(cudaMemsetAsync(node_max, 0x80, (size_t)nb * 4, s));  // large negative
     uint32_t k = 0;
