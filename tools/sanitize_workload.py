@@ -41,3 +41,42 @@ print("lsd ok", len(r.reports))
 del os.environ["RC_SORT_LSD"]
 r = rc_run(prog, 512, [torch.from_numpy(x).cuda() for x in ins], n_groups=2)
 print("groups ok", len(r.reports))
+# K1c (the interval kernel compiled per program): bucket writes + fresh start
+# + report snapshot (stencil), reports / fuel (tree), the plane variant after
+# a bucket overflow, direct mode, and the hand-back to K1 (rc_k1c_fix)
+os.environ["RC_JIT"] = "1"
+p = K.program(K.STENCIL); prog = rc_load_program(p.bytecode)
+ins = I.cfg5_inputs(0, 2, 70000)
+r = rc_run(prog, 70000, [torch.from_numpy(x).cuda() for x in ins])
+r = rc_run(prog, 70000, [torch.from_numpy(x).cuda() for x in ins], prepass=True)
+print("k1c stencil ok", r.stats["checked_accesses"], prog.jit_kernels())
+p = K.program(K.TREE_OFF_BY_ONE); prog = rc_load_program(p.bytecode)
+ins = I.cfg3_inputs(0, 40, 1024)
+r = rc_run(prog, 1024, [torch.from_numpy(x).cuda() for x in ins])
+print("k1c tree ok", len(r.reports), prog.jit_kernels())
+p = K.program(K.BENIGN["K_inc"]); prog = rc_load_program(p.bytecode)
+ins = I.cfg2_inputs(0, 2, 20000)
+r = rc_run(prog, 20000, [torch.from_numpy(x).cuda() for x in ins])
+print("k1c oversized bucket ok", len(r.reports), prog.jit_kernels())
+from workloads.asm import assemble  # noqa: E402
+p = assemble(""".arrays X Y
+    tid r0
+    const r1, 2
+    lt r2, r0, r1
+    br r2, left, right
+left:
+    bar
+    const r5, 0
+    ld r3, X, r5
+    ld r4, X, r0
+    ld r6, Y, r0
+    exit
+right:
+    bar
+    const r5, 0
+    st X, r5, r0
+    exit
+"""); prog = rc_load_program(p.bytecode)
+ins = [np.arange(600, dtype=np.int32).reshape(2, 300), np.zeros((2, 300), np.int32)]
+r = rc_run(prog, 300, [torch.from_numpy(x).cuda() for x in ins])
+print("k1c hand-back ok", len(r.reports), prog.jit_kernels())
