@@ -338,7 +338,7 @@ cudaError_t launch_filter(const FilterParams& p, cudaStream_t s);
 // bits in shared memory and runs the segmented detection on it.
 constexpr int BUCKET_BITS = 12;
 constexpr uint32_t BUCKET_CELLS = 1u << BUCKET_BITS;
-constexpr uint32_t NB_MAX = 8192;                     // buckets per batch: cells per batch <= 2^25
+constexpr uint32_t NB_MAX = 32768;                    // buckets per batch: cells per batch <= 2^27
 constexpr uint64_t BUCKET_PATH_CELLS = (uint64_t)NB_MAX * BUCKET_CELLS;
 constexpr uint32_t BUCKET_REGION = 2 * BUCKET_CELLS;  // region mode: record slots a bucket owns
 

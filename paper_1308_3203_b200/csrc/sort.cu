@@ -637,12 +637,11 @@ __global__ void __launch_bounds__(BC_THREADS, BC_MINB) bucket_count_kernel(const
   if (!last) return;
   __threadfence();
   constexpr int PER = NB_MAX / BC_THREADS;
-  uint32_t v[PER], sum = 0;
-#pragma unroll
+  uint32_t sum = 0;  // (the counts are re-read below, not held in registers: PER is large)
+#pragma unroll 8
   for (int k = 0; k < PER; k++) {
     const uint32_t b = (uint32_t)t * PER + k;
-    v[k] = b < nb ? __ldcg(hist + b) : 0u;
-    sum += v[k];
+    sum += b < nb ? __ldcg(hist + b) : 0u;
   }
   uint32_t x = sum;
 #pragma unroll
@@ -654,14 +653,14 @@ __global__ void __launch_bounds__(BC_THREADS, BC_MINB) bucket_count_kernel(const
   __syncthreads();
   uint32_t run = x - sum;
   for (int i = 0; i < w; i++) run += wsum[i];
-#pragma unroll
+#pragma unroll 8
   for (int k = 0; k < PER; k++) {
     const uint32_t b = (uint32_t)t * PER + k;
     if (b < nb) {
       bstart[b] = run;
       p.bcur[b] = run;
+      run += __ldcg(hist + b);
     }
-    run += v[k];
   }
 }
 
