@@ -25,6 +25,8 @@
 
 #include <array>
 
+#include <nvtx3/nvToolsExt.h>  // header-only; the ranges cost a pointer test unless a tool is attached
+
 #include "rc_internal.h"
 
 namespace rc {
@@ -77,6 +79,15 @@ Profiler::~Profiler() {
 }  // namespace rc
 
 using namespace rc;
+
+// NVTX range for the host span of rc_run, a batch, an interval enqueue
+// (SURVEY §5 tracing; visible under nsys / ncu --nvtx)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // grow-only device buffer
 struct DevBuf {
@@ -296,6 +307,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
 
   std::lock_guard<std::mutex> lk(P->mu);
   DeviceGuard dg(opt.device);
+  NvtxRange nvtx_run("rc_run");
   cudaStream_t s = static_cast<cudaStream_t>(opt.cuda_stream);
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
@@ -596,6 +608,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     CK(enqueue_inputs(0, 0));
   }
   for (uint32_t b0 = 0, bi = 0; b0 < n_inst; b0 += I_b, bi++) {
+    NvtxRange nvtx_batch("rc batch");
     const uint32_t nb = std::min(I_b, n_inst - b0);
     const uint32_t L = nb * n;
     const uint32_t inst_base = opt.instance_offset + b0;
@@ -842,6 +855,7 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
       return kp;
     };
     auto enqueue_interval = [&](uint32_t kk, int cc, Marks* mk) -> cudaError_t {
+      NvtxRange nvtx_iv(jit_on && !jit_off ? "rc interval (K1c)" : "rc interval (K1)");
       cudaError_t e;
 #define EQ(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
       if (gaps) { gap_ev.push_back({}); gap_b.push_back(bi); cudaEventCreate(&gap_ev.back()[0]); cudaEventCreate(&gap_ev.back()[1]); cudaEventRecord(gap_ev.back()[0], s); }
