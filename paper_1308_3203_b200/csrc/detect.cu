@@ -43,7 +43,14 @@ __device__ __forceinline__ int32_t rec_val(const DetectParams& p, uint64_t r) {
   // slot * n_lanes + lane < 15 * 2^27: 32-bit index arithmetic
   const uint32_t slot = ((uint32_t)r >> 1) & 0xF;
   if (SPILL && slot == SLOT_SPILL) return spilled_val(p, r);
-  return __ldg(p.wval + (slot * p.n_lanes + rec_tid(r)));
+  // (L2, not the read-only path: with bval the bucket kernels fill wval for
+  // the multi-record cells in this very launch)
+  return __ldcg(p.wval + (slot * p.n_lanes + rec_tid(r)));
+}
+// K1c in region mode writes each value beside its record (bval) and no wval:
+// the multi-record cells' write values are put where rec_val looks for them
+__device__ __forceinline__ void put_val(const DetectParams& p, uint64_t r, int32_t v) {
+  p.wval[(((uint32_t)r >> 1) & 0xF) * p.n_lanes + rec_tid(r)] = v;
 }
 
 __device__ __forceinline__ void emit(const DetectParams& p, uint32_t cell, uint32_t t1, uint32_t t2, uint16_t kind,
@@ -582,6 +589,7 @@ __device__ __forceinline__ bool bucket_smem(const DetectParams& p, BucketSmem& S
     const bool ok = r[j] != REC_SENTINEL;
     const bool lone = (S.cnt[ok ? bucket_low(r[j]) : BUCKET_CELLS] & 0xFFFFu) == 1u;
     if (ok && lone && rec_w(r[j])) p.heap[rec_cell(r[j])] = val[j];
+    if (p.bval && ok && !lone && rec_w(r[j])) put_val(p, r[j], val[j]);  // (visible to the block after the barrier)
     multi |= ok && !lone;
   }
   __syncwarp();
@@ -598,7 +606,11 @@ __device__ __forceinline__ bool bucket_smem(const DetectParams& p, BucketSmem& S
 template <bool SPILL>
 __device__ __noinline__ void bucket_global(const DetectParams& p, BucketSmem& S, uint32_t s0, uint32_t m) {
   const int t = threadIdx.x;
-  for (uint32_t i = t; i < m; i += BD_THREADS) atomicAdd(&S.cnt[bucket_low(__ldcg(p.recs + s0 + i))], 1u);
+  for (uint32_t i = t; i < m; i += BD_THREADS) {
+    const uint64_t r = __ldcg(p.recs + s0 + i);
+    atomicAdd(&S.cnt[bucket_low(r)], 1u);
+    if (p.bval && rec_w(r)) put_val(p, r, __ldcg(p.bval + s0 + i));
+  }
   __syncthreads();
   constexpr int PER = BUCKET_CELLS / BD_THREADS;
   uint32_t* offs = reinterpret_cast<uint32_t*>(S.sorted);

@@ -564,8 +564,8 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* n_carried) {
         << "        pos = __shfl_sync(m, pos, leader) + __popc(m & ((1u << lane) - 1u));\n"
         << "        if (pos < p.region) p.bucket_out[(u64)b * p.region + pos] = ((u64)oc" << j << " << 32) | (g << 5) | "
         << (j << 1 | 1) << "u; else s_bover = true;\n"
-        << "        if (pos < p.region) p.bucket_val[(u64)b * p.region + pos] = ov" << j << ";  // (beside the record)\n"
-        << "        p.wval[(u64)" << j << " * p.n_lanes + g] = ov" << j << ";\n"
+        << "        if (pos < p.region) p.bucket_val[(u64)b * p.region + pos] = ov" << j
+        << ";  // (beside the record; detect fills wval for multi-record cells)\n"
         << "        if (!(ro >> 31)) p.wmap[oc" << j << "] = (u8)p.wtag;\n"
         << "        s_wrec++;\n"
         << "      } }\n";

@@ -264,7 +264,7 @@ std::string jit_source(const rc_program* P, const JitShape& S, int* carried = nu
 
 struct DetectParams {
   const uint64_t* recs;       // sorted by cell; count = ctr->kept_count
-  const int32_t* wval;        // [ovl_cap][n_lanes]
+  int32_t* wval;              // [ovl_cap][n_lanes] (written by the bucket kernels for multi-record cells when bval)
   const uint32_t* spill_cell; // slot SLOT_SPILL: the lane's spill list (K1)
   const int32_t* spill_val;
   const uint32_t* spill_n;
@@ -338,7 +338,7 @@ cudaError_t launch_filter(const FilterParams& p, cudaStream_t s);
 // bits in shared memory and runs the segmented detection on it.
 constexpr int BUCKET_BITS = 12;
 constexpr uint32_t BUCKET_CELLS = 1u << BUCKET_BITS;
-constexpr uint32_t NB_MAX = 32768;                    // buckets per batch: cells per batch <= 2^27
+constexpr uint32_t NB_MAX = 65536;                    // buckets per batch: cells per batch <= 2^28
 constexpr uint64_t BUCKET_PATH_CELLS = (uint64_t)NB_MAX * BUCKET_CELLS;
 constexpr uint32_t BUCKET_REGION = 2 * BUCKET_CELLS;  // region mode: record slots a bucket owns
 
