@@ -83,3 +83,33 @@ def test_k1c_source_shape_constants(rc):
     # the first loads of an interval search no overlay (nothing stored yet)
     first_ld = src.index("pc 4\n")
     assert "oc0 == cell" not in src[first_ld:src.index("pc 5\n")]
+
+
+def test_k1c_rematerialised_registers(rc):
+    """The affine-register analysis on the stencil (hand-derived: c = tid+1,
+    the index registers r0 = tid, r1 = tid + 1, r3 = tid + 2 at both barrier
+    entries; r7, the loop counter, is not a function of tid): r0 / r1 / r3 are
+    recomputed at the entries and never loaded or stored, r7 is carried."""
+    prog = rc.rc_load_program(K.program(K.STENCIL).bytecode)
+    src = prog.jit_source(1 << 10, [(1 << 10) + 2] * 2, wbucket=True)
+    for e in (11, 14):
+        case = next(l for l in src.splitlines() if l.strip().startswith(f"case {e}u:"))
+        assert "r0 = (i32)(1u * tid + 0u)" in case and "r1 = (i32)(1u * tid + 1u)" in case
+        assert "r3 = (i32)(1u * tid + 2u)" in case and "r7 =" not in case
+    loads = [l for l in src.splitlines() if "p.regs_in[" in l]
+    stores = [l for l in src.splitlines() if "p.regs_out[" in l and "rc_k1c_fix" not in l]
+    assert loads and all("(u64)7 *" in l for l in loads)
+    assert any("(u64)7 *" in l for l in stores)
+    # the fix kernel writes exactly the rematerialised ones for K1
+    fix = src[src.index("rc_k1c_fix"):]
+    assert "(u64)0 * p.reg_stride" in fix and "(u64)3 * p.reg_stride" in fix and "(u64)7 * p.reg_stride" not in fix
+
+
+def test_k1c_no_aligned_barrier_after_body(rc):
+    """After the goto-structured body a warp's lanes need not have
+    reconverged: the generated kernel has no block barrier past its start."""
+    for src_text in (K.STENCIL, K.TREE):
+        prog = rc.rc_load_program(K.program(src_text).bytecode)
+        src = prog.jit_source(1024, [1100] * prog.n_arrays, wbucket=True)
+        body = src[src.index("switch (pc)"):src.index("rc_k1c_fix")]
+        assert "__syncthreads" not in body
