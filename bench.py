@@ -508,6 +508,10 @@ def main():
                          "sampling": f"CUDA events around every {every}th interval's kernels of the timed steps",
                          "peak_source": peak_src,
                          "library_sort_same_keys": cub_baseline()}
+        if not s["launches"]:  # (K1c placed every write record; the workload logs no read record)
+            roofline_sort = {"kernel": roofline_sort["kernel"], "launched": False,
+                             "note": "not launched: K1c writes the write records straight into their bucket regions "
+                                     "and no read record of this workload survives the static write-set elision"}
         # the detect kernel (K4+K5): every grouped record read, one value
         # gathered and one cell committed per write record
         dd = prof_sum["detect"]
@@ -599,7 +603,8 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
             "interpreter": {"bytecode_instr_per_s": ins_step / (ms_step / 1000),
                             "bytecode_instr_per_step": ins_step,
-                            "bound": "issue (ALU/LSU pipes; ncu sm__inst_executed.avg.per_cycle_active in profiles/)"},
+                            "executed_by": "K1c (the interval kernel compiled for the program)" if
+                            (prof_sum or {}).get("k1c") else "K1 (the bytecode interpreter)"},
             "clocks": clocks, "kernels": kernels, "secondary": secondary, "explorer": explorer}
     print(json.dumps(line), flush=True)
     if world > 1:
