@@ -380,7 +380,13 @@ int rc_run(const rc_program* prog, uint32_t n, const rc_array* arrays, uint32_t 
     memcpy(W.plan_key, plan_key, sizeof plan_key);
     W.plan_valid = true;
   }
-  const uint32_t I_b = W.plan_ib;
+  // with host inputs (RC_OPT_HOST_IO) the run is bound by the host->device
+  // copies, overlapped batch by batch (A2): the last batch's work is the part
+  // no copy hides, so the batch is capped at 1/16 of the run (config 5: 32
+  // instances; 4 batches of 128 left 25% of the step exposed)
+  const uint32_t I_b = (host_io && !opt.max_batch_instances && n_inst >= 32)
+                           ? std::min<uint32_t>(W.plan_ib, (n_inst + 15) / 16)
+                           : W.plan_ib;
   // RC_OPT_PREPASS: a run proved conflict-free by the
   // symbolic pre-pass interprets its intervals in direct-commit mode
   bool direct = false;
